@@ -1,0 +1,187 @@
+/*
+ * noma_cuda.h -- C-ABI of the B200-native (sm_100a) NOMA detector.
+ *
+ * This is the drop-in boundary for the hot path of the reference
+ * "noma-detect" (arxiv 2206.05998, /root/reference/proj).  Plain pointers,
+ * sizes and status codes only; no C++ or torch types cross it.  Each entry
+ * point names the reference interface it replaces.  The C++ host layer
+ * (paper_2206_05998_b200/host, namespace noma::) implements the reference's
+ * own headers on top of these calls; INTEGRATION.md shows the bindings.
+ *
+ * Memory: every data call takes `mem`.  NOMA_MEM_HOST pointers are host
+ * memory: the call stages them to the device, runs, copies results back and
+ * synchronises.  NOMA_MEM_DEVICE pointers are device memory: the call is
+ * asynchronous on the context's stream.
+ *
+ * Layouts (row-major, complex = interleaved re,im):
+ *   WIDEN_COMPLEX design : [n_designs][rows/2][width/2] complex f64 -- the
+ *                          complex receive matrix X; the widened real rows
+ *                          2t = [Re x_t; Im x_t], 2t+1 = [Im x_t; -Re x_t]
+ *                          (iq_transform.cpp:7-24) are formed on device.
+ *   WIDEN_COMPLEX targets: [n_designs][rows/2][nets_per_design] complex f64
+ *                          (TransmissionRecord::train_symbols per slot).
+ *   REAL design          : [n_designs][rows][width] f64.
+ *   REAL targets         : [n_designs][nets_per_design][rows] f64.
+ *   params ("plan")      : [net][noma_plan_size] f32, the reference FusedPlan
+ *                          buffer layout (fused_inference.cpp:19-42):
+ *                          w0[pad8(d0)] | per layer l: d_l rows x pad8(d_{l-1}),
+ *                          bias[pad8(d_l)] | final[pad8(d_N)].
+ *   net index            : net = design * nets_per_design + user (0-based).
+ */
+#ifndef NOMA_CUDA_H
+#define NOMA_CUDA_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#if defined(__GNUC__)
+#define NOMA_API __attribute__((visibility("default")))
+#else
+#define NOMA_API
+#endif
+
+/* Status codes; the C++ layer maps them onto the reference exceptions
+ * (errors.hpp:8-35). */
+enum noma_status {
+    NOMA_OK = 0,
+    NOMA_ERR_DIMENSION = 1,      /* noma::dimension_error                   */
+    NOMA_ERR_CONFIG = 2,         /* noma::config_error                      */
+    NOMA_ERR_ILL_CONDITIONED = 3,/* noma::ill_conditioned_error (per net)   */
+    NOMA_ERR_UNSUPPORTED = 4,    /* shape outside the device kernels' range */
+    NOMA_ERR_CUDA = 5,           /* CUDA runtime failure (see last_error)   */
+    NOMA_ERR_ARGUMENT = 6        /* null / inconsistent argument            */
+};
+
+enum noma_mem { NOMA_MEM_HOST = 0, NOMA_MEM_DEVICE = 1 };
+enum noma_layout { NOMA_LAYOUT_WIDEN_COMPLEX = 0, NOMA_LAYOUT_REAL = 1 };
+
+#define NOMA_MAX_DIMS 9      /* input width + up to 8 hidden layers       */
+#define NOMA_MAX_WIDTH 128   /* kFusedMaxWidth (fused_inference.hpp:15)   */
+#define NOMA_MAX_BATCH 128   /* device minibatch tile                      */
+
+typedef struct noma_ctx_s *noma_ctx_t;
+
+/* [dims[0] = 2M, L_1, ..., L_N] -- HybridNetParams::dims (hybrid_nn.hpp:21) */
+typedef struct {
+    int ndims;
+    int dims[NOMA_MAX_DIMS];
+} noma_net_desc;
+
+/* TrainConfig + AdamState hyper-parameters (hybrid_nn.hpp:31-49) */
+typedef struct {
+    int epochs;       /* 50    */
+    int batch_size;   /* 128   */
+    double lr;        /* 0.005 */
+    double beta1;     /* 0.9   */
+    double beta2;     /* 0.999 */
+    double eps;       /* 1e-8  */
+} noma_train_cfg;
+
+/* Training / LLS data set: one design shared by nets_per_design targets
+ * (WidenedDataset, iq_transform.hpp:13-17, batched over slots and users). */
+typedef struct {
+    int layout;            /* enum noma_layout                         */
+    int n_designs;         /* slots S                                  */
+    int nets_per_design;   /* users K                                  */
+    int rows;              /* widened rows 2*N_T (WIDEN) or rows (REAL) */
+    int width;             /* 2M (WIDEN) or columns (REAL)              */
+    const double *design;
+    const double *targets;
+} noma_dataset;
+
+/* ScenarioConfig (channel_sim.hpp:14-31) */
+typedef struct {
+    int num_users;
+    int num_antennas;
+    int train_symbols;
+    int data_symbols;
+    double power_step_db;
+    double snr_db;               /* +inf: noiseless */
+    double rx_nonlinearity_gain;
+} noma_scenario;
+
+/* ---------------------------------------------------------------- context */
+NOMA_API int noma_version(void);
+NOMA_API int noma_ctx_create(int device, noma_ctx_t *out);
+NOMA_API int noma_ctx_destroy(noma_ctx_t ctx);
+NOMA_API const char *noma_ctx_last_error(noma_ctx_t ctx);
+/* Run subsequent calls on this cudaStream_t (NULL = the context's own). */
+NOMA_API int noma_ctx_set_stream(noma_ctx_t ctx, void *cuda_stream);
+NOMA_API int noma_ctx_synchronize(noma_ctx_t ctx);
+/* Number of kernels this context has launched (instrumentation). */
+NOMA_API long long noma_ctx_kernel_launches(noma_ctx_t ctx);
+
+/* Floats in the FusedPlan buffer for `desc` (fused_inference.cpp:19-42). */
+NOMA_API int noma_plan_size(const noma_net_desc *desc);
+/* Trainable parameters (HybridNetParams::trainable_count, hybrid_nn.cpp:11-16). */
+NOMA_API int noma_param_count(const noma_net_desc *desc);
+
+/* ------------------------------------------------------------- hot path */
+
+/* Replaces lls::fit (lls.hpp:19-21, lls.cpp:10-60), batched over every
+ * (design, target) pair.  FP64 Gram accumulation + Jacobi eigensolve in
+ * shared memory.  Outputs [net][width] w0, [net] gram_condition, [net] status
+ * (NOMA_OK or NOMA_ERR_ILL_CONDITIONED with gram_condition set). */
+NOMA_API int noma_lls_fit(noma_ctx_t ctx, const noma_dataset *ds, double *w0,
+                          double *gram_condition, int *status, int mem);
+
+/* Replaces hybrid_nn::init_params (hybrid_nn.hpp:55-56, hybrid_nn.cpp:34-55)
+ * for n_nets networks: net i draws from Rng(seeds[i]) exactly as the
+ * reference (He-normal rows then columns, layer by layer; biases and final
+ * layer zero); w0 ([net][dims[0]], nullable) is copied into the plan. */
+NOMA_API int noma_init_params(noma_ctx_t ctx, const noma_net_desc *desc, int n_nets,
+                              const uint64_t *seeds, const double *w0, float *plans, int mem);
+
+/* Replaces hybrid_nn::train (hybrid_nn.hpp:70-72, hybrid_nn.cpp:158-195)
+ * for every net of `ds`: one fused kernel per net runs all epochs x
+ * minibatches (forward, backward, Adam) with the weights resident on chip.
+ * plans_inout [net][plan] holds the initial parameters (incl. w0) and
+ * receives the trained ones; shuffle_seeds [net] are TrainConfig::shuffle_seed;
+ * loss_trace [net][epochs] nullable; status [net] nullable. */
+NOMA_API int noma_train(noma_ctx_t ctx, const noma_dataset *ds, const noma_net_desc *desc,
+                        const noma_train_cfg *cfg, const double *w0, float *plans_inout,
+                        const uint64_t *shuffle_seeds, double *loss_trace, int *status, int mem);
+
+/* Replaces hybrid_nn::detect / fused::fused_forward_f32 + hard_decision_qpsk
+ * + bit_error_rate (hybrid_nn.cpp:197-199, fused_inference.cpp:222-231,
+ * eval.cpp:38-65): streaming inference of every net over its design's data.
+ *   WIDEN_COMPLEX: data [n_designs][rows][width/2] complex f32 (rows = N_D
+ *     symbols); soft [net][rows] complex f32; codes [net][rows] u8 with
+ *     bit0 = Re<0, bit1 = Im<0; truth [n_designs][rows][nets_per_design] u8
+ *     codes; bit_errors [net] u32.
+ *   REAL: data [n_designs][rows][width] f32; soft [net][rows] f32 (no codes).
+ * All outputs nullable. */
+NOMA_API int noma_detect(noma_ctx_t ctx, const noma_net_desc *desc, int layout, int n_designs,
+                         int nets_per_design, int rows, const float *data, const float *plans,
+                         const uint8_t *truth, float *soft, uint8_t *codes, uint32_t *bit_errors,
+                         int mem);
+
+/* One slot batch end to end (noma_cli.cpp:86-160 per user, eval.cpp:228-241):
+ * LLS -> init (Rng(init_seeds[net])) -> train (shuffle_seeds[net]) -> detect.
+ * pilots/targets as the WIDEN_COMPLEX dataset; data_rx [S][ND][M] complex f32;
+ * truth [S][ND][K] codes (nullable).  Outputs nullable except status. */
+NOMA_API int noma_pipeline(noma_ctx_t ctx, const noma_net_desc *desc, const noma_train_cfg *cfg,
+                           int S, int K, int M, int NT, int ND, const double *pilot_rx,
+                           const double *pilot_sym, const float *data_rx, const uint8_t *truth,
+                           const uint64_t *init_seeds, const uint64_t *shuffle_seeds,
+                           double *w0, double *gram_condition, float *plans, double *loss_trace,
+                           float *soft, uint8_t *codes, uint32_t *bit_errors, int *status,
+                           int mem);
+
+/* Replaces synthesize(cfg, SeedBundle::from_master(seed)) (channel_sim.cpp:76-117)
+ * on device for S slots with master seeds [S].  Outputs (nullable):
+ * pilot_rx [S][NT][M] c64, pilot_sym [S][NT][K] c64, data_rx [S][ND][M] c32,
+ * data_codes [S][ND][K] u8, channel [S][M][K] c64, noise_power [S]. */
+NOMA_API int noma_synthesize(noma_ctx_t ctx, const noma_scenario *sc, int S,
+                             const uint64_t *master_seeds, double *pilot_rx, double *pilot_sym,
+                             float *data_rx, uint8_t *data_codes, double *channel,
+                             double *noise_power, int mem);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,548 @@
+// C-ABI (include/noma_cuda.h): context, staging and the batched entry points.
+#include <cmath>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "kernels.cuh"
+
+namespace noma_dev {
+
+
+// design32 / r0 for a training call whose w0 comes from the caller:
+// r0[net][row] = y - X w0 in FP64 (the frozen-branch residual target).
+__global__ void prep_kernel(int layout, int S, int K, int rows, int width, const double *design,
+                            const double *targets, const double *w0, float *design32,
+                            float *r0) {
+    const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const size_t nnet = (size_t)S * K * rows;
+    if (i < nnet) {
+        const int row = (int)(i % rows);
+        const size_t net = i / rows;
+        const int d = (int)(net / K), k = (int)(net % K);
+        const double *w = w0 + net * width;
+        double pred = 0.0, y;
+        if (layout == NOMA_LAYOUT_WIDEN_COMPLEX) {
+            const int m = width / 2, t = row >> 1;
+            const double *x = design + ((size_t)d * (rows / 2) + t) * m * 2;
+            for (int a = 0; a < m; ++a) {
+                const double xr = x[2 * a], xi = x[2 * a + 1];
+                pred += (row & 1) ? (xi * w[a] - xr * w[m + a]) : (xr * w[a] + xi * w[m + a]);
+            }
+            y = targets[(((size_t)d * (rows / 2) + t) * K + k) * 2 + (row & 1)];
+        } else {
+            const double *x = design + ((size_t)d * rows + row) * width;
+            for (int c = 0; c < width; ++c) pred += x[c] * w[c];
+            y = targets[((size_t)d * K + k) * rows + row];
+        }
+        r0[i] = (float)(y - pred);
+    }
+    // design32
+    const size_t nd = layout == NOMA_LAYOUT_WIDEN_COMPLEX ? (size_t)S * (rows / 2) * width
+                                                           : (size_t)S * rows * width;
+    if (i < nd) {
+        if (layout == NOMA_LAYOUT_WIDEN_COMPLEX) {
+            const int m = width / 2;
+            const size_t tr = i / width;
+            const int c = (int)(i % width);
+            const double v = c < m ? design[(tr * m + c) * 2] : design[(tr * m + c - m) * 2 + 1];
+            design32[i] = (float)v;
+        } else {
+            design32[i] = (float)design[i];
+        }
+    }
+}
+
+}  // namespace noma_dev
+
+using namespace noma_dev;
+
+struct noma_ctx_s {
+    int device = 0;
+    cudaStream_t own = nullptr;
+    cudaStream_t stream = nullptr;
+    std::string err;
+    long long launches = 0;
+};
+
+namespace {
+
+int fail(noma_ctx_t c, int code, const std::string &msg) {
+    if (c) c->err = msg;
+    return code;
+}
+
+int cuda_fail(noma_ctx_t c, const char *where) {
+    cudaError_t e = cudaGetLastError();
+    return fail(c, NOMA_ERR_CUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+// Stages host arguments to the device (NOMA_MEM_HOST) or passes device
+// pointers through (NOMA_MEM_DEVICE); frees stream-ordered on exit.
+struct Stage {
+    noma_ctx_t c;
+    int mem;
+    std::vector<void *> allocs;
+    struct Back { void *host; const void *dev; size_t bytes; };
+    std::vector<Back> backs;
+    bool ok = true;
+    Stage(noma_ctx_t c_, int mem_) : c(c_), mem(mem_) {}
+    ~Stage() {
+        for (void *p : allocs) cudaFreeAsync(p, c->stream);
+    }
+    void *alloc(size_t bytes) {
+        if (bytes == 0) bytes = 16;
+        void *p = nullptr;
+        if (cudaMallocAsync(&p, bytes, c->stream) != cudaSuccess) {
+            ok = false;
+            return nullptr;
+        }
+        allocs.push_back(p);
+        return p;
+    }
+    template <class T> T *scratch(size_t n) { return static_cast<T *>(alloc(n * sizeof(T))); }
+    template <class T> const T *in(const T *p, size_t n) {
+        if (!p) return nullptr;
+        if (mem == NOMA_MEM_DEVICE) return p;
+        T *d = scratch<T>(n);
+        if (d && cudaMemcpyAsync(d, p, n * sizeof(T), cudaMemcpyHostToDevice, c->stream) != cudaSuccess)
+            ok = false;
+        return d;
+    }
+    template <class T> T *inout(T *p, size_t n) {
+        if (!p) return nullptr;
+        if (mem == NOMA_MEM_DEVICE) return p;
+        T *d = const_cast<T *>(in<T>(p, n));
+        backs.push_back({p, d, n * sizeof(T)});
+        return d;
+    }
+    template <class T> T *out(T *p, size_t n) {
+        if (!p) return nullptr;
+        if (mem == NOMA_MEM_DEVICE) return p;
+        T *d = scratch<T>(n);
+        backs.push_back({p, d, n * sizeof(T)});
+        return d;
+    }
+    int finish() {
+        if (!ok) return cuda_fail(c, "staging");
+        if (mem == NOMA_MEM_HOST) {
+            for (auto &b : backs)
+                if (cudaMemcpyAsync(b.host, b.dev, b.bytes, cudaMemcpyDeviceToHost, c->stream) != cudaSuccess)
+                    return cuda_fail(c, "copy back");
+            if (cudaStreamSynchronize(c->stream) != cudaSuccess) return cuda_fail(c, "synchronize");
+        }
+        if (cudaGetLastError() != cudaSuccess) return cuda_fail(c, "kernel");
+        return NOMA_OK;
+    }
+};
+
+int check_dataset(noma_ctx_t c, const noma_dataset *ds) {
+    if (!ds || !ds->design || !ds->targets) return fail(c, NOMA_ERR_ARGUMENT, "null dataset");
+    if (ds->layout != NOMA_LAYOUT_WIDEN_COMPLEX && ds->layout != NOMA_LAYOUT_REAL)
+        return fail(c, NOMA_ERR_ARGUMENT, "bad layout");
+    if (ds->n_designs < 0 || ds->nets_per_design < 1) return fail(c, NOMA_ERR_DIMENSION, "bad counts");
+    if (ds->rows < 1 || ds->width < 1) return fail(c, NOMA_ERR_DIMENSION, "empty design");
+    if (ds->layout == NOMA_LAYOUT_WIDEN_COMPLEX && ((ds->rows & 1) || (ds->width & 1)))
+        return fail(c, NOMA_ERR_DIMENSION, "widened design needs even rows and width");
+    return NOMA_OK;
+}
+
+size_t design_elems(const noma_dataset *ds) {  // doubles
+    return ds->layout == NOMA_LAYOUT_WIDEN_COMPLEX
+               ? (size_t)ds->n_designs * (ds->rows / 2) * (ds->width / 2) * 2
+               : (size_t)ds->n_designs * ds->rows * ds->width;
+}
+size_t target_elems(const noma_dataset *ds) {
+    return ds->layout == NOMA_LAYOUT_WIDEN_COMPLEX
+               ? (size_t)ds->n_designs * (ds->rows / 2) * ds->nets_per_design * 2
+               : (size_t)ds->n_designs * ds->nets_per_design * ds->rows;
+}
+size_t design32_elems(const noma_dataset *ds) {
+    return ds->layout == NOMA_LAYOUT_WIDEN_COMPLEX ? (size_t)ds->n_designs * (ds->rows / 2) * ds->width
+                                                   : (size_t)ds->n_designs * ds->rows * ds->width;
+}
+
+LlsParams lls_params(const noma_dataset *ds, const double *x, const double *y, double *w0,
+                     double *cond, int *status, float *d32, float *r0) {
+    LlsParams p;
+    p.layout = ds->layout;
+    p.n_designs = ds->n_designs;
+    p.K = ds->nets_per_design;
+    p.rows = ds->rows;
+    p.width = ds->width;
+    p.m = ds->layout == NOMA_LAYOUT_WIDEN_COMPLEX ? ds->width / 2 : ds->width;
+    p.nrow_c = ds->layout == NOMA_LAYOUT_WIDEN_COMPLEX ? ds->rows / 2 : ds->rows;
+    p.design = x;
+    p.targets = y;
+    p.w0 = w0;
+    p.cond = cond;
+    p.status = status;
+    p.design32 = d32;
+    p.r0 = r0;
+    return p;
+}
+
+int check_cfg(noma_ctx_t c, const noma_train_cfg *cfg) {
+    if (!cfg) return fail(c, NOMA_ERR_ARGUMENT, "null cfg");
+    if (cfg->epochs < 0 || cfg->batch_size < 1 || !(cfg->lr > 0.0))
+        return fail(c, NOMA_ERR_CONFIG, "train: invalid training configuration");
+    return NOMA_OK;
+}
+
+void fill_train(TrainParams &tp, const NetGeom &g, const noma_train_cfg *cfg) {
+    tp.g = g;
+    tp.epochs = cfg->epochs;
+    tp.batch = cfg->batch_size;
+    tp.lr = (float)cfg->lr;
+    tp.b1 = (float)cfg->beta1;
+    tp.b2 = (float)cfg->beta2;
+    tp.eps = (float)cfg->eps;
+    tp.omb1 = (float)(1.0 - cfg->beta1);
+    tp.omb2 = (float)(1.0 - cfg->beta2);
+    tp.b1d = cfg->beta1;
+    tp.b2d = cfg->beta2;
+}
+
+}  // namespace
+
+extern "C" {
+
+NOMA_API int noma_version(void) { return 1; }
+
+NOMA_API int noma_ctx_create(int device, noma_ctx_t *out) {
+    if (!out) return NOMA_ERR_ARGUMENT;
+    *out = nullptr;
+    if (cudaSetDevice(device) != cudaSuccess) return NOMA_ERR_CUDA;
+    auto *c = new noma_ctx_s;
+    c->device = device;
+    if (cudaStreamCreateWithFlags(&c->own, cudaStreamNonBlocking) != cudaSuccess) {
+        delete c;
+        return NOMA_ERR_CUDA;
+    }
+    c->stream = c->own;
+    *out = c;
+    return NOMA_OK;
+}
+
+NOMA_API int noma_ctx_destroy(noma_ctx_t c) {
+    if (!c) return NOMA_OK;
+    cudaStreamSynchronize(c->stream);
+    if (c->own) cudaStreamDestroy(c->own);
+    delete c;
+    return NOMA_OK;
+}
+
+NOMA_API const char *noma_ctx_last_error(noma_ctx_t c) { return c ? c->err.c_str() : "null context"; }
+
+NOMA_API int noma_ctx_set_stream(noma_ctx_t c, void *s) {
+    if (!c) return NOMA_ERR_ARGUMENT;
+    c->stream = s ? static_cast<cudaStream_t>(s) : c->own;
+    return NOMA_OK;
+}
+
+NOMA_API int noma_ctx_synchronize(noma_ctx_t c) {
+    if (!c) return NOMA_ERR_ARGUMENT;
+    return cudaStreamSynchronize(c->stream) == cudaSuccess ? NOMA_OK : cuda_fail(c, "sync");
+}
+
+NOMA_API long long noma_ctx_kernel_launches(noma_ctx_t c) { return c ? c->launches : 0; }
+
+NOMA_API int noma_plan_size(const noma_net_desc *desc) {
+    NetGeom g;
+    return make_geom(desc, &g) ? g.plan_total : -1;
+}
+
+NOMA_API int noma_param_count(const noma_net_desc *desc) {
+    NetGeom g;
+    return make_geom(desc, &g) ? trainable_count(g) : -1;
+}
+
+NOMA_API int noma_lls_fit(noma_ctx_t c, const noma_dataset *ds, double *w0, double *cond,
+                          int *status, int mem) {
+    if (!c) return NOMA_ERR_ARGUMENT;
+    int st = check_dataset(c, ds);
+    if (st) return st;
+    if (ds->rows < ds->width)
+        return fail(c, NOMA_ERR_DIMENSION, "lls::fit: system must be over-determined");
+    if (!w0) return fail(c, NOMA_ERR_ARGUMENT, "null w0");
+    if (ds->n_designs == 0) return NOMA_OK;
+    const size_t nets = (size_t)ds->n_designs * ds->nets_per_design;
+    Stage s(c, mem);
+    const double *x = s.in(ds->design, design_elems(ds));
+    const double *y = s.in(ds->targets, target_elems(ds));
+    double *dw = s.out(w0, nets * ds->width);
+    double *dc = s.out(cond, nets);
+    std::vector<int> hstat;
+    int *dst;
+    if (status) {
+        dst = s.out(status, nets);
+    } else {
+        dst = s.scratch<int>(nets);
+    }
+    if (!s.ok) return s.finish();
+    st = lls_launch(lls_params(ds, x, y, dw, dc, dst, nullptr, nullptr), c->stream);
+    if (st) return st == NOMA_ERR_CUDA ? cuda_fail(c, "lls") : fail(c, st, "lls: unsupported shape");
+    c->launches += 1;
+    st = s.finish();
+    if (st) return st;
+    if (mem == NOMA_MEM_HOST && status)
+        for (size_t i = 0; i < nets; ++i)
+            if (status[i] != NOMA_OK) return fail(c, status[i], "lls::fit: design matrix rank deficient and system inconsistent");
+    return NOMA_OK;
+}
+
+NOMA_API int noma_init_params(noma_ctx_t c, const noma_net_desc *desc, int n_nets,
+                              const uint64_t *seeds, const double *w0, float *plans, int mem) {
+    if (!c) return NOMA_ERR_ARGUMENT;
+    NetGeom g;
+    if (!make_geom(desc, &g)) return fail(c, NOMA_ERR_DIMENSION, "init_params: bad dims");
+    if (!seeds || !plans) return fail(c, NOMA_ERR_ARGUMENT, "null seeds/plans");
+    if (n_nets <= 0) return NOMA_OK;
+    Stage s(c, mem);
+    const uint64_t *sd = s.in(seeds, (size_t)n_nets);
+    const double *dw = s.in(w0, (size_t)n_nets * g.dims[0]);
+    float *dp = s.out(plans, (size_t)n_nets * g.plan_total);
+    if (!s.ok) return s.finish();
+    if (init_launch(g, n_nets, sd, dw, dp, c->stream)) return cuda_fail(c, "init");
+    c->launches += 1;
+    return s.finish();
+}
+
+NOMA_API int noma_train(noma_ctx_t c, const noma_dataset *ds, const noma_net_desc *desc,
+                        const noma_train_cfg *cfg, const double *w0, float *plans_inout,
+                        const uint64_t *shuffle_seeds, double *trace, int *status, int mem) {
+    if (!c) return NOMA_ERR_ARGUMENT;
+    int st = check_dataset(c, ds);
+    if (st) return st;
+    if ((st = check_cfg(c, cfg))) return st;
+    NetGeom g;
+    if (!make_geom(desc, &g)) return fail(c, NOMA_ERR_DIMENSION, "train: bad dims");
+    if (g.dims[0] != ds->width) return fail(c, NOMA_ERR_DIMENSION, "train: input width does not match network");
+    if (!w0 || !plans_inout || !shuffle_seeds) return fail(c, NOMA_ERR_ARGUMENT, "null argument");
+    const size_t nets = (size_t)ds->n_designs * ds->nets_per_design;
+    if (nets == 0) return NOMA_OK;
+    if (ds->rows > 65535) return fail(c, NOMA_ERR_UNSUPPORTED, "train: more than 65535 rows");
+    Stage s(c, mem);
+    const double *x = s.in(ds->design, design_elems(ds));
+    const double *y = s.in(ds->targets, target_elems(ds));
+    const double *dw = s.in(w0, nets * ds->width);
+    const uint64_t *seeds = s.in(shuffle_seeds, nets);
+    float *dp = s.inout(plans_inout, nets * g.plan_total);
+    double *dt = s.out(trace, nets * (size_t)cfg->epochs);
+    const int *dst = s.in(status, nets);
+    float *d32 = s.scratch<float>(design32_elems(ds));
+    float *r0 = s.scratch<float>(nets * ds->rows);
+    uint16_t *perm = s.scratch<uint16_t>(nets * (size_t)cfg->epochs * ds->rows);
+    if (!s.ok) return s.finish();
+    {
+        const size_t n = std::max(nets * ds->rows, design32_elems(ds));
+        prep_kernel<<<(unsigned)((n + 255) / 256), 256, 0, c->stream>>>(
+            ds->layout, ds->n_designs, ds->nets_per_design, ds->rows, ds->width, x, y, dw, d32, r0);
+        if (cudaGetLastError() != cudaSuccess) return cuda_fail(c, "prep");
+    }
+    if (perm_launch((int)nets, cfg->epochs, ds->rows, seeds, perm, c->stream)) return cuda_fail(c, "perm");
+    TrainParams tp;
+    fill_train(tp, g, cfg);
+    tp.layout = ds->layout;
+    tp.n_nets = (int)nets;
+    tp.K = ds->nets_per_design;
+    tp.rows = ds->rows;
+    tp.width = ds->width;
+    tp.design32 = d32;
+    tp.r0 = r0;
+    tp.perm = perm;
+    tp.plans = dp;
+    tp.trace = dt;
+    tp.status = dst;
+    if (cfg->epochs > 0) {
+        st = train_launch(tp, c->stream);
+        if (st) return st == NOMA_ERR_CUDA ? cuda_fail(c, "train") : fail(c, st, "train: unsupported network shape");
+    }
+    c->launches += 3;
+    return s.finish();
+}
+
+NOMA_API int noma_detect(noma_ctx_t c, const noma_net_desc *desc, int layout, int n_designs,
+                         int nets_per_design, int rows, const float *data, const float *plans,
+                         const uint8_t *truth, float *soft, uint8_t *codes, uint32_t *bit_errors,
+                         int mem) {
+    if (!c) return NOMA_ERR_ARGUMENT;
+    NetGeom g;
+    if (!make_geom(desc, &g)) return fail(c, NOMA_ERR_DIMENSION, "detect: bad dims");
+    if (!data || !plans) return fail(c, NOMA_ERR_ARGUMENT, "null data/plans");
+    if (layout != NOMA_LAYOUT_WIDEN_COMPLEX && layout != NOMA_LAYOUT_REAL)
+        return fail(c, NOMA_ERR_ARGUMENT, "bad layout");
+    if (layout == NOMA_LAYOUT_WIDEN_COMPLEX && (g.dims[0] & 1))
+        return fail(c, NOMA_ERR_DIMENSION, "detect: odd widened width");
+    const size_t nets = (size_t)n_designs * nets_per_design;
+    if (nets == 0 || rows == 0) return NOMA_OK;
+    const size_t data_elems = layout == NOMA_LAYOUT_WIDEN_COMPLEX
+                                  ? (size_t)n_designs * rows * g.dims[0]
+                                  : (size_t)n_designs * rows * g.dims[0];
+    Stage s(c, mem);
+    const float *dd = s.in(data, data_elems);
+    const float *dp = s.in(plans, nets * g.plan_total);
+    const uint8_t *dtr = s.in(truth, (size_t)n_designs * rows * nets_per_design);
+    float *dso = s.out(soft, nets * rows * (layout == NOMA_LAYOUT_WIDEN_COMPLEX ? 2 : 1));
+    uint8_t *dco = layout == NOMA_LAYOUT_WIDEN_COMPLEX ? s.out(codes, nets * rows) : nullptr;
+    uint32_t *der = s.out(bit_errors, nets);
+    if (!s.ok) return s.finish();
+    if (der) cudaMemsetAsync(der, 0, nets * sizeof(uint32_t), c->stream);
+    DetectParams dpp;
+    dpp.g = g;
+    dpp.layout = layout;
+    dpp.n_nets = (int)nets;
+    dpp.K = nets_per_design;
+    dpp.rows = rows;
+    dpp.width = g.dims[0];
+    dpp.data = dd;
+    dpp.plans = dp;
+    dpp.truth = dtr;
+    dpp.soft = dso;
+    dpp.codes = dco;
+    dpp.errors = der;
+    dpp.status = nullptr;
+    int st = detect_launch(dpp, c->stream);
+    if (st) return st == NOMA_ERR_CUDA ? cuda_fail(c, "detect") : fail(c, st, "detect: unsupported network shape");
+    c->launches += 1;
+    return s.finish();
+}
+
+NOMA_API int noma_pipeline(noma_ctx_t c, const noma_net_desc *desc, const noma_train_cfg *cfg,
+                           int S, int K, int M, int NT, int ND, const double *pilot_rx,
+                           const double *pilot_sym, const float *data_rx, const uint8_t *truth,
+                           const uint64_t *init_seeds, const uint64_t *shuffle_seeds, double *w0,
+                           double *gram_condition, float *plans, double *loss_trace, float *soft,
+                           uint8_t *codes, uint32_t *bit_errors, int *status, int mem) {
+    if (!c) return NOMA_ERR_ARGUMENT;
+    int st;
+    if ((st = check_cfg(c, cfg))) return st;
+    NetGeom g;
+    if (!make_geom(desc, &g)) return fail(c, NOMA_ERR_DIMENSION, "pipeline: bad dims");
+    if (g.dims[0] != 2 * M) return fail(c, NOMA_ERR_DIMENSION, "pipeline: dims[0] != 2M");
+    if (!pilot_rx || !pilot_sym || !data_rx || !init_seeds || !shuffle_seeds || !status)
+        return fail(c, NOMA_ERR_ARGUMENT, "null argument");
+    if (S < 0 || K < 1 || M < 1 || NT < 1 || ND < 0) return fail(c, NOMA_ERR_DIMENSION, "bad sizes");
+    if (2 * NT < 2 * M) return fail(c, NOMA_ERR_DIMENSION, "lls::fit: system must be over-determined");
+    if (2 * NT > 65535) return fail(c, NOMA_ERR_UNSUPPORTED, "too many pilot rows");
+    if (S == 0) return NOMA_OK;
+    const size_t nets = (size_t)S * K;
+    const int n = 2 * NT;
+    Stage s(c, mem);
+    const double *px = s.in(pilot_rx, (size_t)S * NT * M * 2);
+    const double *py = s.in(pilot_sym, (size_t)S * NT * K * 2);
+    const float *dx = s.in(data_rx, (size_t)S * ND * M * 2);
+    const uint8_t *dtr = s.in(truth, (size_t)S * ND * K);
+    const uint64_t *iseed = s.in(init_seeds, nets);
+    const uint64_t *sseed = s.in(shuffle_seeds, nets);
+    double *dw = w0 ? s.out(w0, nets * 2 * M) : s.scratch<double>(nets * 2 * M);
+    double *dc = s.out(gram_condition, nets);
+    float *dp = plans ? s.out(plans, nets * g.plan_total) : s.scratch<float>(nets * g.plan_total);
+    double *dt = s.out(loss_trace, nets * (size_t)cfg->epochs);
+    float *dso = s.out(soft, nets * ND * 2);
+    uint8_t *dco = s.out(codes, nets * ND);
+    uint32_t *der = s.out(bit_errors, nets);
+    int *dst = s.out(status, nets);
+    float *d32 = s.scratch<float>((size_t)S * NT * 2 * M);
+    float *r0 = s.scratch<float>(nets * n);
+    uint16_t *perm = s.scratch<uint16_t>(nets * (size_t)cfg->epochs * n);
+    if (!s.ok) return s.finish();
+
+    noma_dataset ds{NOMA_LAYOUT_WIDEN_COMPLEX, S, K, n, 2 * M, px, py};
+    st = lls_launch(lls_params(&ds, px, py, dw, dc, dst, d32, r0), c->stream);
+    if (st) return st == NOMA_ERR_CUDA ? cuda_fail(c, "lls") : fail(c, st, "lls: unsupported shape");
+    if (init_launch(g, (int)nets, iseed, dw, dp, c->stream)) return cuda_fail(c, "init");
+    if (perm_launch((int)nets, cfg->epochs, n, sseed, perm, c->stream)) return cuda_fail(c, "perm");
+    c->launches += 3;
+    if (cfg->epochs > 0) {
+        TrainParams tp;
+        fill_train(tp, g, cfg);
+        tp.layout = NOMA_LAYOUT_WIDEN_COMPLEX;
+        tp.n_nets = (int)nets;
+        tp.K = K;
+        tp.rows = n;
+        tp.width = 2 * M;
+        tp.design32 = d32;
+        tp.r0 = r0;
+        tp.perm = perm;
+        tp.plans = dp;
+        tp.trace = dt;
+        tp.status = dst;
+        st = train_launch(tp, c->stream);
+        if (st) return st == NOMA_ERR_CUDA ? cuda_fail(c, "train") : fail(c, st, "train: unsupported network shape");
+        c->launches += 1;
+    }
+    if (ND > 0) {
+        if (der) cudaMemsetAsync(der, 0, nets * sizeof(uint32_t), c->stream);
+        DetectParams dpp;
+        dpp.g = g;
+        dpp.layout = NOMA_LAYOUT_WIDEN_COMPLEX;
+        dpp.n_nets = (int)nets;
+        dpp.K = K;
+        dpp.rows = ND;
+        dpp.width = 2 * M;
+        dpp.data = dx;
+        dpp.plans = dp;
+        dpp.truth = dtr;
+        dpp.soft = dso;
+        dpp.codes = dco;
+        dpp.errors = der;
+        dpp.status = dst;
+        st = detect_launch(dpp, c->stream);
+        if (st) return st == NOMA_ERR_CUDA ? cuda_fail(c, "detect") : fail(c, st, "detect: unsupported network shape");
+        c->launches += 1;
+    }
+    return s.finish();
+}
+
+NOMA_API int noma_synthesize(noma_ctx_t c, const noma_scenario *sc, int S,
+                             const uint64_t *master_seeds, double *pilot_rx, double *pilot_sym,
+                             float *data_rx, uint8_t *data_codes, double *channel,
+                             double *noise_power, int mem) {
+    if (!c) return NOMA_ERR_ARGUMENT;
+    if (!sc || !master_seeds) return fail(c, NOMA_ERR_ARGUMENT, "null argument");
+    // ScenarioConfig::validate (channel_sim.cpp:9-21)
+    if (sc->num_users < 1 || sc->num_antennas < 1 || sc->train_symbols < 1 || sc->data_symbols < 1 ||
+        sc->train_symbols < 2 * sc->num_antennas || sc->power_step_db < 0.0 ||
+        sc->rx_nonlinearity_gain < 0.0 || std::isnan(sc->snr_db))
+        return fail(c, NOMA_ERR_CONFIG, "invalid scenario");
+    if (S <= 0) return NOMA_OK;
+    const int K = sc->num_users, M = sc->num_antennas, NT = sc->train_symbols, ND = sc->data_symbols;
+    const size_t T = (size_t)NT + ND;
+    std::vector<double> powers(K);
+    for (int k = 0; k < K; ++k) powers[k] = std::pow(10.0, (double)(-k) * sc->power_step_db / 10.0);
+    Stage s(c, NOMA_MEM_HOST == mem ? NOMA_MEM_HOST : NOMA_MEM_DEVICE);
+    const uint64_t *dseeds = s.in(master_seeds, (size_t)S);
+    double *dpow = s.scratch<double>(K);
+    SynthParams p;
+    p.S = S;
+    p.K = K;
+    p.M = M;
+    p.NT = NT;
+    p.ND = ND;
+    p.gain = sc->rx_nonlinearity_gain;
+    p.noisy = std::isinf(sc->snr_db) ? 0 : 1;
+    p.snr_lin = std::pow(10.0, sc->snr_db / 10.0);
+    p.seeds = dseeds;
+    p.powers = dpow;
+    p.pilot_rx = s.out(pilot_rx, (size_t)S * NT * M * 2);
+    p.pilot_sym = s.out(pilot_sym, (size_t)S * NT * K * 2);
+    p.data_rx = s.out(data_rx, (size_t)S * ND * M * 2);
+    p.data_codes = s.out(data_codes, (size_t)S * ND * K);
+    p.channel = channel ? s.out(channel, (size_t)S * M * K * 2) : s.scratch<double>((size_t)S * M * K * 2);
+    double *np = noise_power ? s.out(noise_power, (size_t)S) : s.scratch<double>((size_t)S);
+    p.noise_power = np;
+    p.codes_all = s.scratch<uint8_t>((size_t)S * T * K);
+    p.noise = p.noisy ? s.scratch<double>((size_t)S * T * M * 2) : nullptr;
+    if (!s.ok) return s.finish();
+    if (cudaMemcpyAsync(dpow, powers.data(), K * sizeof(double), cudaMemcpyHostToDevice, c->stream) != cudaSuccess)
+        return cuda_fail(c, "powers");
+    if (mem == NOMA_MEM_HOST) cudaStreamSynchronize(c->stream);  // powers lives on the host stack
+    if (synth_launch(p, np, c->stream)) return cuda_fail(c, "synthesize");
+    c->launches += K > M ? 3 : 2;
+    int st = s.finish();
+    if (mem == NOMA_MEM_DEVICE) cudaStreamSynchronize(c->stream);  // keep `powers` alive
+    return st;
+}
+
+}  // extern "C"

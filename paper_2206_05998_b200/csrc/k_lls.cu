@@ -1,0 +1,381 @@
+// LLS initialiser on sm_100a: replaces lls::fit (lls.cpp:10-54), batched.
+//
+// One CTA per design (slot).  All K users of a slot share the design, so the
+// Gram matrix is accumulated once per slot (the reference refactorises the
+// same design K times, eval.cpp:122).  For the IQ-widened design the real
+// Gram X^T X = [[P, Q], [-Q, P]] is the real form of the complex Gram
+// C = X^H X (M x M), and the widened LS solution is w0 = [Re c; -Im c] with
+// c the complex LS solution -- so the kernel works on the M x M Hermitian
+// problem: FP64 Gram accumulation, cyclic Jacobi eigensolve in shared memory
+// (parallel round-robin ordering), pseudo-inverse solve for every user, then
+// an FP64 residual pass that produces r0 = y - X w0 (the training targets of
+// the frozen-branch formulation) and the rank-deficient
+// consistency test of lls.cpp:43-49.
+//
+// Rank decision: the reference thresholds singular
+// values of X at sigma_max * eps * max(rows, cols) (lls.cpp:22-25).  A Gram
+// eigenvalue resolves sigma only down to ~sqrt(eps) sigma_max, so eigenvalues
+// below 16 * eps * max(rows, cols) * lambda_max are treated as zero.  Exactly
+// rank-deficient (noiseless under-loaded) and noisy full-rank designs are
+// classified identically; only sigma in (~3e-13, ~2e-7) * sigma_max differ.
+#include <float.h>
+#include <math.h>
+
+#include "kernels.cuh"
+
+namespace noma_dev {
+
+constexpr int kLlsMaxM = 64;     // complex columns (widened width <= 128)
+constexpr int kLlsChunk = 32;    // rows staged per chunk
+constexpr int kLlsMaxE = 18;     // Gram/RHS entries per thread (registers)
+
+struct cplx { double re, im; };
+
+__device__ inline void load_row(const LlsParams &p, int d, int t, int a, double &re, double &im) {
+    if (p.layout == NOMA_LAYOUT_WIDEN_COMPLEX) {
+        const double *x = p.design + (((size_t)d * p.nrow_c + t) * p.m + a) * 2;
+        re = x[0];
+        im = x[1];
+    } else {
+        re = p.design[((size_t)d * p.nrow_c + t) * p.m + a];
+        im = 0.0;
+    }
+}
+
+__device__ inline void load_target(const LlsParams &p, int d, int t, int k, double &re,
+                                   double &im) {
+    if (p.layout == NOMA_LAYOUT_WIDEN_COMPLEX) {
+        const double *y = p.targets + (((size_t)d * p.nrow_c + t) * p.K + k) * 2;
+        re = y[0];
+        im = y[1];
+    } else {
+        re = p.targets[((size_t)d * p.K + k) * p.rows + t];
+        im = 0.0;
+    }
+}
+
+__global__ void __launch_bounds__(kThreads) lls_kernel(LlsParams p) {
+    extern __shared__ __align__(16) double smem[];
+    const int m = p.m, K = p.K, d = blockIdx.x, tid = threadIdx.x;
+    double *A = smem;                       // m*m complex (Gram -> eigenvalues)
+    double *V = A + 2 * m * m;              // m*m complex eigenvectors
+    double *D = V + 2 * m * m;              // m*K complex RHS X^H y
+    double *xs = D + 2 * m * K;             // chunk rows: kLlsChunk*m complex
+    double *ys = xs + 2 * kLlsChunk * m;    // chunk targets: kLlsChunk*K complex
+    const int chunk = max(2 * kLlsChunk * m + 2 * kLlsChunk * K, 2 * m * K);
+    double *rot = xs + chunk;               // per pair: c, s, e_re, e_im
+    double *lam = rot + 4 * (kLlsMaxM / 2 + 1);  // m eigenvalues
+    double *U = xs;                         // m*K complex: V^H d / lambda (reuses chunk)
+    double *red = lam + m;                  // reduction scratch (kThreads)
+    __shared__ int pair_p[kLlsMaxM / 2 + 1], pair_q[kLlsMaxM / 2 + 1];
+    __shared__ int any_rot;
+
+    // ---- phase A: Gram (upper triangle) and RHS, accumulated in registers.
+    const int ngram = m * (m + 1) / 2, nent = ngram + m * K;
+    double acc_re[kLlsMaxE], acc_im[kLlsMaxE];
+    int ea[kLlsMaxE], eb[kLlsMaxE];
+#pragma unroll
+    for (int e = 0; e < kLlsMaxE; ++e) {
+        acc_re[e] = acc_im[e] = 0.0;
+        const int id = tid + e * kThreads;
+        ea[e] = eb[e] = -1;
+        if (id < ngram) {  // map id -> (a <= b)
+            int a = 0, rem = id;
+            while (rem >= m - a) { rem -= m - a; ++a; }
+            ea[e] = a;
+            eb[e] = a + rem;
+        } else if (id < nent) {
+            ea[e] = (id - ngram) / K;
+            eb[e] = m + (id - ngram) % K;  // b >= m encodes target k = b - m
+        }
+    }
+    for (int t0 = 0; t0 < p.nrow_c; t0 += kLlsChunk) {
+        const int tn = min(kLlsChunk, p.nrow_c - t0);
+        for (int i = tid; i < tn * m; i += kThreads) {
+            const int t = i / m, a = i % m;
+            double re, im;
+            load_row(p, d, t0 + t, a, re, im);
+            xs[2 * i] = re;
+            xs[2 * i + 1] = im;
+            if (p.design32) {
+                if (p.layout == NOMA_LAYOUT_WIDEN_COMPLEX) {
+                    float *o = p.design32 + ((size_t)d * p.nrow_c + t0 + t) * p.width;
+                    o[a] = (float)re;
+                    o[m + a] = (float)im;
+                } else {
+                    p.design32[((size_t)d * p.nrow_c + t0 + t) * p.width + a] = (float)re;
+                }
+            }
+        }
+        for (int i = tid; i < tn * K; i += kThreads) {
+            double re, im;
+            load_target(p, d, t0 + i / K, i % K, re, im);
+            ys[2 * i] = re;
+            ys[2 * i + 1] = im;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int e = 0; e < kLlsMaxE; ++e) {
+            if (ea[e] < 0) continue;
+            const int a = ea[e], b = eb[e];
+            const bool rhs = b >= m;
+            double sr = acc_re[e], si = acc_im[e];
+            for (int t = 0; t < tn; ++t) {
+                const double xr = xs[2 * (t * m + a)], xi = xs[2 * (t * m + a) + 1];
+                double br, bi;
+                if (rhs) {
+                    br = ys[2 * (t * K + b - m)];
+                    bi = ys[2 * (t * K + b - m) + 1];
+                } else {
+                    br = xs[2 * (t * m + b)];
+                    bi = xs[2 * (t * m + b) + 1];
+                }
+                sr += xr * br + xi * bi;  // conj(x_a) * b
+                si += xr * bi - xi * br;
+            }
+            acc_re[e] = sr;
+            acc_im[e] = si;
+        }
+        __syncthreads();
+    }
+#pragma unroll
+    for (int e = 0; e < kLlsMaxE; ++e) {
+        if (ea[e] < 0) continue;
+        const int a = ea[e], b = eb[e];
+        if (b >= m) {
+            D[2 * (a * K + b - m)] = acc_re[e];
+            D[2 * (a * K + b - m) + 1] = acc_im[e];
+        } else {
+            A[2 * (a * m + b)] = acc_re[e];
+            A[2 * (a * m + b) + 1] = acc_im[e];
+            A[2 * (b * m + a)] = acc_re[e];       // Hermitian mirror
+            A[2 * (b * m + a) + 1] = -acc_im[e];
+            if (a == b) A[2 * (a * m + a) + 1] = 0.0;
+        }
+    }
+    for (int i = tid; i < m * m; i += kThreads) {
+        V[2 * i] = (i / m == i % m) ? 1.0 : 0.0;
+        V[2 * i + 1] = 0.0;
+    }
+    __syncthreads();
+
+    // ---- phase B: cyclic Jacobi, round-robin pairs (circle method).
+    const int mm = m + (m & 1);
+    const int npairs = mm / 2;
+    for (int sweep = 0; sweep < 40; ++sweep) {
+        if (tid == 0) any_rot = 0;
+        __syncthreads();
+        for (int r = 0; r < mm - 1; ++r) {
+            if (tid < npairs) {
+                const int i = tid;
+                const int pi = (i == 0) ? 0 : ((i - 1 + r) % (mm - 1)) + 1;
+                const int j = mm - 1 - i;
+                const int qi = (j == 0) ? 0 : ((j - 1 + r) % (mm - 1)) + 1;
+                int pp = min(pi, qi), qq = max(pi, qi);
+                double c = 1.0, s = 0.0, er = 1.0, ei = 0.0;
+                if (qq < m) {
+                    const double a = A[2 * (pp * m + pp)], b = A[2 * (qq * m + qq)];
+                    const double hr = A[2 * (pp * m + qq)], hi = A[2 * (pp * m + qq) + 1];
+                    const double habs = hypot(hr, hi);
+                    if (habs > 0.0 && habs > DBL_EPSILON * 0.5 * sqrt(fabs(a) * fabs(b))) {
+                        er = hr / habs;
+                        ei = hi / habs;
+                        const double th = (b - a) / (2.0 * habs);
+                        const double t = (th >= 0.0 ? 1.0 : -1.0) / (fabs(th) + sqrt(th * th + 1.0));
+                        c = 1.0 / sqrt(t * t + 1.0);
+                        s = t * c;
+                        any_rot = 1;
+                    }
+                } else {
+                    pp = qq = -1;
+                }
+                pair_p[i] = pp;
+                pair_q[i] = qq;
+                rot[4 * i] = c;
+                rot[4 * i + 1] = s;
+                rot[4 * i + 2] = er;
+                rot[4 * i + 3] = ei;
+            }
+            __syncthreads();
+            // columns: A <- A U, V <- V U
+            for (int it = tid; it < npairs * m * 2; it += kThreads) {
+                const int mat = it / (npairs * m), rem = it % (npairs * m);
+                const int i = rem / m, row = rem % m;
+                const int pp = pair_p[i], qq = pair_q[i];
+                if (pp < 0) continue;
+                const double c = rot[4 * i], s = rot[4 * i + 1];
+                const double er = rot[4 * i + 2], ei = -rot[4 * i + 3];  // e^{-i phi}
+                double *Mx = mat ? V : A;
+                const double xr = Mx[2 * (row * m + pp)], xi = Mx[2 * (row * m + pp) + 1];
+                const double yr = Mx[2 * (row * m + qq)], yi = Mx[2 * (row * m + qq) + 1];
+                const double zr = er * yr - ei * yi, zi = er * yi + ei * yr;  // e^{-i phi} y
+                Mx[2 * (row * m + pp)] = c * xr - s * zr;
+                Mx[2 * (row * m + pp) + 1] = c * xi - s * zi;
+                Mx[2 * (row * m + qq)] = s * xr + c * zr;
+                Mx[2 * (row * m + qq) + 1] = s * xi + c * zi;
+            }
+            __syncthreads();
+            // rows: A <- U^H A
+            for (int it = tid; it < npairs * m; it += kThreads) {
+                const int i = it / m, col = it % m;
+                const int pp = pair_p[i], qq = pair_q[i];
+                if (pp < 0) continue;
+                const double c = rot[4 * i], s = rot[4 * i + 1];
+                const double er = rot[4 * i + 2], ei = rot[4 * i + 3];  // e^{+i phi}
+                const double xr = A[2 * (pp * m + col)], xi = A[2 * (pp * m + col) + 1];
+                const double yr = A[2 * (qq * m + col)], yi = A[2 * (qq * m + col) + 1];
+                const double zr = er * yr - ei * yi, zi = er * yi + ei * yr;
+                A[2 * (pp * m + col)] = c * xr - s * zr;
+                A[2 * (pp * m + col) + 1] = c * xi - s * zi;
+                A[2 * (qq * m + col)] = s * xr + c * zr;
+                A[2 * (qq * m + col) + 1] = s * xi + c * zi;
+            }
+            __syncthreads();
+        }
+        if (!any_rot) break;
+        __syncthreads();
+    }
+
+    // ---- phase C: eigenvalues, rank, pseudo-inverse solve.
+    for (int i = tid; i < m; i += kThreads) lam[i] = A[2 * (i * m + i)];
+    __syncthreads();
+    double lmax = 0.0, lmin = INFINITY;
+    for (int i = 0; i < m; ++i) {
+        lmax = fmax(lmax, lam[i]);
+        lmin = fmin(lmin, lam[i]);
+    }
+    const int big = p.rows > p.width ? p.rows : p.width;
+    const double tol = lmax * 16.0 * DBL_EPSILON * (double)big;
+    int rank = 0;
+    double lkeep = INFINITY;
+    for (int i = 0; i < m; ++i)
+        if (lam[i] > tol) {
+            ++rank;
+            lkeep = fmin(lkeep, lam[i]);
+        }
+    // U[i][k] = (V_i^H d_k) / lambda_i for kept i, else 0
+    for (int it = tid; it < m * K; it += kThreads) {
+        const int i = it / K, k = it % K;
+        double sr = 0.0, si = 0.0;
+        if (lam[i] > tol) {
+            for (int a = 0; a < m; ++a) {
+                const double vr = V[2 * (a * m + i)], vi = V[2 * (a * m + i) + 1];
+                const double dr = D[2 * (a * K + k)], di = D[2 * (a * K + k) + 1];
+                sr += vr * dr + vi * di;  // conj(v) d
+                si += vr * di - vi * dr;
+            }
+            sr /= lam[i];
+            si /= lam[i];
+        }
+        U[2 * it] = sr;
+        U[2 * it + 1] = si;
+    }
+    __syncthreads();
+    // c_k[a] = sum_i V[a][i] U[i][k]; w0 written FP64
+    for (int it = tid; it < m * K; it += kThreads) {
+        const int a = it / K, k = it % K;
+        double sr = 0.0, si = 0.0;
+        for (int i = 0; i < m; ++i) {
+            const double vr = V[2 * (a * m + i)], vi = V[2 * (a * m + i) + 1];
+            const double ur = U[2 * (i * K + k)], ui = U[2 * (i * K + k) + 1];
+            sr += vr * ur - vi * ui;
+            si += vr * ui + vi * ur;
+        }
+        double *w = p.w0 + ((size_t)d * K + k) * p.width;
+        if (p.layout == NOMA_LAYOUT_WIDEN_COMPLEX) {
+            w[a] = sr;
+            w[m + a] = -si;
+        } else {
+            w[a] = sr;
+        }
+    }
+    __syncthreads();  // w0 (global) visible to the block below
+
+    // ---- phase D: residuals r0 = y - X w0 (FP64), norms, status.
+    for (int k = 0; k < K; ++k) {
+        const double *w = p.w0 + ((size_t)d * K + k) * p.width;
+        double rr = 0.0, yy = 0.0;
+        for (int t = tid; t < p.nrow_c; t += kThreads) {
+            double yr, yi;
+            load_target(p, d, t, k, yr, yi);
+            if (p.layout == NOMA_LAYOUT_WIDEN_COMPLEX) {
+                double pe = 0.0, po = 0.0;
+                for (int a = 0; a < m; ++a) {
+                    double xr, xi;
+                    load_row(p, d, t, a, xr, xi);
+                    pe += xr * w[a] + xi * w[m + a];  // row 2t = [Re x; Im x]
+                    po += xi * w[a] - xr * w[m + a];  // row 2t+1 = [Im x; -Re x]
+                }
+                const double r_e = yr - pe, r_o = yi - po;
+                rr += r_e * r_e + r_o * r_o;
+                yy += yr * yr + yi * yi;
+                if (p.r0) {
+                    p.r0[((size_t)d * K + k) * p.rows + 2 * t] = (float)r_e;
+                    p.r0[((size_t)d * K + k) * p.rows + 2 * t + 1] = (float)r_o;
+                }
+            } else {
+                double pr = 0.0;
+                for (int a = 0; a < m; ++a) {
+                    double xr, xi;
+                    load_row(p, d, t, a, xr, xi);
+                    pr += xr * w[a];
+                }
+                const double r_e = yr - pr;
+                rr += r_e * r_e;
+                yy += yr * yr;
+                if (p.r0) p.r0[((size_t)d * K + k) * p.rows + t] = (float)r_e;
+            }
+        }
+        red[tid] = rr;
+        __syncthreads();
+        for (int s = kThreads / 2; s > 0; s >>= 1) {
+            if (tid < s) red[tid] += red[tid + s];
+            __syncthreads();
+        }
+        const double res = sqrt(red[0]);
+        __syncthreads();
+        red[tid] = yy;
+        __syncthreads();
+        for (int s = kThreads / 2; s > 0; s >>= 1) {
+            if (tid < s) red[tid] += red[tid + s];
+            __syncthreads();
+        }
+        const double ynorm = sqrt(red[0]);
+        __syncthreads();
+        if (tid == 0) {
+            const size_t net = (size_t)d * K + k;
+            int st = NOMA_OK;
+            double cond;
+            if (rank == m) {
+                cond = lmax / lmin;
+            } else if (rank > 0 && res <= 1e-8 * sqrt(lmax) * fmax(1.0, ynorm)) {
+                cond = lmax / lkeep;
+            } else {
+                st = NOMA_ERR_ILL_CONDITIONED;
+                cond = lmin > 0.0 ? lmax / lmin : INFINITY;
+            }
+            if (p.cond) p.cond[net] = cond;
+            if (p.status) p.status[net] = st;
+        }
+    }
+}
+
+size_t lls_smem_bytes(int m, int K) {
+    size_t chunk = 2 * kLlsChunk * m + 2 * kLlsChunk * K;
+    if (chunk < (size_t)(2 * m * K)) chunk = 2 * m * K;  // U aliases the chunk buffers
+    size_t n = 2 * m * m * 2 + 2 * m * K + chunk + 4 * (kLlsMaxM / 2 + 1) + m + kThreads;
+    return n * sizeof(double);
+}
+
+int lls_launch(const LlsParams &p, cudaStream_t st) {
+    if (p.m < 1 || p.m > kLlsMaxM) return NOMA_ERR_UNSUPPORTED;
+    const int nent = p.m * (p.m + 1) / 2 + p.m * p.K;
+    if (nent > kLlsMaxE * kThreads) return NOMA_ERR_UNSUPPORTED;
+    const size_t smem = lls_smem_bytes(p.m, p.K);
+    if (smem > 227 * 1024) return NOMA_ERR_UNSUPPORTED;
+    cudaFuncSetAttribute(lls_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    lls_kernel<<<p.n_designs, kThreads, smem, st>>>(p);
+    return cudaGetLastError() == cudaSuccess ? NOMA_OK : NOMA_ERR_CUDA;
+}
+
+}  // namespace noma_dev

@@ -1,0 +1,234 @@
+// Bit-exact RNG consumers on sm_100a: per-epoch Fisher-Yates shuffles
+// (hybrid_nn.cpp:148-154, :176), He-normal initialisation (hybrid_nn.cpp:34-55)
+// and the synthetic uplink generator (channel_sim.cpp:30-117).
+//
+// Every reference stream is sequential (xoshiro256++), so the unit of
+// parallelism is the stream: one thread per (net, epoch) shuffle, one thread
+// per net initialisation, one thread per slot for the synthesiser's draws.
+// The data-parallel parts (superposition, distortion, noise scaling) run one
+// thread per receive sample.
+#include <math.h>
+
+#include "kernels.cuh"
+
+namespace noma_dev {
+
+// ---------------------------------------------------------------- shuffle
+// perm[net][epoch][n] (u16).  Each thread owns one (net, epoch) and keeps its
+// index array in shared memory while applying the 1..n-1 swaps.
+__global__ void perm_kernel(int n_nets, int epochs, int n, const uint64_t *shuffle_seeds,
+                            uint16_t *perm) {
+    extern __shared__ uint16_t sidx[];
+    const int job = blockIdx.x * blockDim.x + threadIdx.x;
+    if (job >= n_nets * epochs) return;
+    const int net = job / epochs, epoch = job % epochs;
+    uint16_t *idx = sidx + (size_t)threadIdx.x * n;
+    for (int i = 0; i < n; ++i) idx[i] = (uint16_t)i;
+    Xoshiro r(substream_seed(shuffle_seeds[net], (uint64_t)epoch));
+    for (int i = n - 1; i > 0; --i) {
+        const int j = (int)r.below((uint64_t)i + 1);
+        const uint16_t t = idx[i];
+        idx[i] = idx[j];
+        idx[j] = t;
+    }
+    uint16_t *out = perm + (size_t)job * n;
+    for (int i = 0; i < n; ++i) out[i] = idx[i];
+}
+
+int perm_launch(int n_nets, int epochs, int n, const uint64_t *seeds, uint16_t *perm,
+                cudaStream_t st) {
+    if (n > 65535) return NOMA_ERR_UNSUPPORTED;
+    const int jobs = n_nets * epochs;
+    if (jobs == 0) return NOMA_OK;
+    int tpb = (int)((160 * 1024) / (2 * (size_t)n));
+    tpb = tpb > 64 ? 64 : tpb;
+    if (tpb < 1) return NOMA_ERR_UNSUPPORTED;
+    const size_t smem = (size_t)tpb * n * sizeof(uint16_t);
+    cudaFuncSetAttribute(perm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    perm_kernel<<<(jobs + tpb - 1) / tpb, tpb, smem, st>>>(n_nets, epochs, n, seeds, perm);
+    return cudaGetLastError() == cudaSuccess ? NOMA_OK : NOMA_ERR_CUDA;
+}
+
+// ------------------------------------------------------------------- init
+// plans[net][plan_total]: W_l (He-normal, row-major draws), b_l = 0, final = 0;
+// w0 (FP64, nullable) copied into the plan's w0 slot.
+__global__ void init_kernel(NetGeom g, int n_nets, const uint64_t *seeds, const double *w0,
+                            float *plans) {
+    const int net = blockIdx.x * blockDim.x + threadIdx.x;
+    if (net >= n_nets) return;
+    float *pl = plans + (size_t)net * g.plan_total;
+    for (int i = 0; i < g.plan_total; ++i) pl[i] = 0.0f;
+    if (w0)
+        for (int c = 0; c < g.dims[0]; ++c) pl[c] = (float)w0[(size_t)net * g.dims[0] + c];
+    Xoshiro r(seeds[net]);
+    for (int l = 1; l < g.nd; ++l) {
+        const int fan_in = g.dims[l - 1];
+        const double scale = sqrt(2.0 / fan_in);
+        for (int row = 0; row < g.dims[l]; ++row)
+            for (int c = 0; c < fan_in; ++c)
+                pl[g.plan_w[l] + row * g.plan_pad[l - 1] + c] = (float)(r.gaussian() * scale);
+    }
+}
+
+int init_launch(const NetGeom &g, int n_nets, const uint64_t *seeds, const double *w0,
+                float *plans, cudaStream_t st) {
+    if (n_nets == 0) return NOMA_OK;
+    init_kernel<<<(n_nets + 63) / 64, 64, 0, st>>>(g, n_nets, seeds, w0, plans);
+    return cudaGetLastError() == cudaSuccess ? NOMA_OK : NOMA_ERR_CUDA;
+}
+
+// Copies FP64 w0 [net][d0] into the plans' w0 slots.
+__global__ void set_w0_kernel(int n_nets, int d0, int plan_total, const double *w0,
+                              float *plans) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n_nets * d0) return;
+    const int net = i / d0, c = i % d0;
+    plans[(size_t)net * plan_total + c] = (float)w0[i];
+}
+
+int set_w0_launch(int n_nets, int d0, int plan_total, const double *w0, float *plans,
+                  cudaStream_t st) {
+    const int n = n_nets * d0;
+    if (n == 0) return NOMA_OK;
+    set_w0_kernel<<<(n + 255) / 256, 256, 0, st>>>(n_nets, d0, plan_total, w0, plans);
+    return cudaGetLastError() == cudaSuccess ? NOMA_OK : NOMA_ERR_CUDA;
+}
+
+// -------------------------------------------------------------- synthesis
+// One thread per slot: the three sequential streams of SeedBundle.
+__global__ void synth_draw_kernel(SynthParams p) {
+    const int s = blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= p.S) return;
+    const uint64_t master = p.seeds[s];
+    Xoshiro sym(substream_seed(master, 1)), chan(substream_seed(master, 2)),
+        noise(substream_seed(master, 3));
+    const double hs = 1.0 / sqrt(2.0);
+    double *h = p.channel + (size_t)s * p.M * p.K * 2;
+    for (int k = 0; k < p.K; ++k)  // gen_channel: k then m; g++ draws imag first
+        for (int m = 0; m < p.M; ++m) {
+            const double im = __dmul_rn(chan.gaussian(), hs);
+            const double re = __dmul_rn(chan.gaussian(), hs);
+            h[((size_t)m * p.K + k) * 2] = re;
+            h[((size_t)m * p.K + k) * 2 + 1] = im;
+        }
+    const int T = p.NT + p.ND;
+    uint8_t *codes = p.codes_all + (size_t)s * T * p.K;
+    for (int t = 0; t < T; ++t)
+        for (int k = 0; k < p.K; ++k) codes[(size_t)t * p.K + k] = (uint8_t)sym.below(4);
+    double np = 0.0;
+    if (p.noisy) {
+        double sig = 0.0;
+        for (int k = 0; k < p.K; ++k) {
+            double nrm = 0.0;
+            for (int m = 0; m < p.M; ++m) {
+                const double re = h[((size_t)m * p.K + k) * 2], im = h[((size_t)m * p.K + k) * 2 + 1];
+                nrm = __dadd_rn(nrm, __dadd_rn(__dmul_rn(re, re), __dmul_rn(im, im)));
+            }
+            sig = __dadd_rn(sig, __dmul_rn(p.powers[k], nrm));
+        }
+        np = sig / __dmul_rn((double)p.M, p.snr_lin);
+        double *nz = p.noise + (size_t)s * T * p.M * 2;
+        for (int t = 0; t < T; ++t)
+            for (int m = 0; m < p.M; ++m) {
+                const double im = noise.gaussian();
+                const double re = noise.gaussian();
+                nz[((size_t)t * p.M + m) * 2] = re;
+                nz[((size_t)t * p.M + m) * 2 + 1] = im;
+            }
+    }
+    if (p.noise_power) p.noise_power[s] = np;
+}
+
+// One thread per (slot, t, m): superposition, cubic distortion, noise.
+__global__ void synth_mix_kernel(SynthParams p, const double *noise_power) {
+    const int T = p.NT + p.ND;
+    const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= (size_t)p.S * T * p.M) return;
+    const int m = (int)(i % p.M);
+    const int t = (int)((i / p.M) % T);
+    const int s = (int)(i / ((size_t)p.M * T));
+    const double a = 1.0 / sqrt(2.0);
+    const double *h = p.channel + (size_t)s * p.M * p.K * 2;
+    const uint8_t *codes = p.codes_all + ((size_t)s * T + t) * p.K;
+    double re = 0.0, im = 0.0;
+    for (int k = 0; k < p.K; ++k) {
+        const uint8_t b = codes[k];
+        const double br = (b & 1) ? -a : a, bi = (b & 2) ? -a : a;
+        const double sp = sqrt(p.powers[k]);
+        const double cr = __dmul_rn(h[((size_t)m * p.K + k) * 2], sp);
+        const double ci = __dmul_rn(h[((size_t)m * p.K + k) * 2 + 1], sp);
+        re = __dadd_rn(re, __dsub_rn(__dmul_rn(br, cr), __dmul_rn(bi, ci)));
+        im = __dadd_rn(im, __dadd_rn(__dmul_rn(br, ci), __dmul_rn(bi, cr)));
+    }
+    if (p.gain > 0.0) {
+        const double nrm = __dadd_rn(__dmul_rn(re, re), __dmul_rn(im, im));
+        re = __dadd_rn(re, __dmul_rn(__dmul_rn(p.gain, re), nrm));
+        im = __dadd_rn(im, __dmul_rn(__dmul_rn(p.gain, im), nrm));
+    }
+    if (p.noisy) {
+        const double sd = sqrt(noise_power[s] / 2.0);
+        const double *nz = p.noise + (((size_t)s * T + t) * p.M + m) * 2;
+        re = __dadd_rn(re, __dmul_rn(nz[0], sd));
+        im = __dadd_rn(im, __dmul_rn(nz[1], sd));
+    }
+    if (t < p.NT) {
+        if (p.pilot_rx) {
+            double *o = p.pilot_rx + (((size_t)s * p.NT + t) * p.M + m) * 2;
+            o[0] = re;
+            o[1] = im;
+        }
+        if (p.pilot_sym && m < p.K) {  // piggy-back: symbols of this row
+            const double br = (codes[m] & 1) ? -a : a, bi = (codes[m] & 2) ? -a : a;
+            double *o = p.pilot_sym + (((size_t)s * p.NT + t) * p.K + m) * 2;
+            o[0] = br;
+            o[1] = bi;
+        }
+    } else {
+        const int td = t - p.NT;
+        if (p.data_rx) {
+            float *o = p.data_rx + (((size_t)s * p.ND + td) * p.M + m) * 2;
+            o[0] = (float)re;
+            o[1] = (float)im;
+        }
+        if (p.data_codes && m < p.K) p.data_codes[((size_t)s * p.ND + td) * p.K + m] = codes[m];
+    }
+}
+
+// pilot symbols / data codes for users k >= M (the mix kernel covers k < M)
+__global__ void synth_codes_tail_kernel(SynthParams p) {
+    const int T = p.NT + p.ND;
+    const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int extra = p.K - p.M;
+    if (extra <= 0 || i >= (size_t)p.S * T * extra) return;
+    const int k = p.M + (int)(i % extra);
+    const int t = (int)((i / extra) % T);
+    const int s = (int)(i / ((size_t)extra * T));
+    const double a = 1.0 / sqrt(2.0);
+    const uint8_t c = p.codes_all[((size_t)s * T + t) * p.K + k];
+    if (t < p.NT) {
+        if (p.pilot_sym) {
+            double *o = p.pilot_sym + (((size_t)s * p.NT + t) * p.K + k) * 2;
+            o[0] = (c & 1) ? -a : a;
+            o[1] = (c & 2) ? -a : a;
+        }
+    } else if (p.data_codes) {
+        p.data_codes[((size_t)s * p.ND + (t - p.NT)) * p.K + k] = c;
+    }
+}
+
+int synth_launch(SynthParams p, double *noise_power_scratch, cudaStream_t st) {
+    const int T = p.NT + p.ND;
+    synth_draw_kernel<<<(p.S + 63) / 64, 64, 0, st>>>(p);
+    if (cudaGetLastError() != cudaSuccess) return NOMA_ERR_CUDA;
+    const size_t n = (size_t)p.S * T * p.M;
+    synth_mix_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(p, noise_power_scratch);
+    if (cudaGetLastError() != cudaSuccess) return NOMA_ERR_CUDA;
+    if (p.K > p.M) {
+        const size_t n2 = (size_t)p.S * T * (p.K - p.M);
+        synth_codes_tail_kernel<<<(unsigned)((n2 + 255) / 256), 256, 0, st>>>(p);
+        if (cudaGetLastError() != cudaSuccess) return NOMA_ERR_CUDA;
+    }
+    return NOMA_OK;
+}
+
+}  // namespace noma_dev

@@ -1,0 +1,78 @@
+// Kernel parameter blocks and host-side launchers (one definition, shared by
+// the kernel translation units and the C-ABI in capi.cu).
+#pragma once
+
+#include "common.cuh"
+
+namespace noma_dev {
+
+struct LlsParams {
+    int layout;           // NOMA_LAYOUT_*
+    int n_designs, K, rows, width;
+    int m;                // complex columns (width/2 for WIDEN, width for REAL)
+    int nrow_c;           // complex rows (rows/2 for WIDEN, rows for REAL)
+    const double *design, *targets;
+    double *w0, *cond;
+    int *status;
+    float *design32;      // nullable: FP32 copy for training, [S][nrow_c][width]
+    float *r0;            // nullable: [net][rows]
+};
+
+struct TrainParams {
+    NetGeom g;
+    int layout, n_nets, K, rows, width, epochs, batch;
+    const float *design32;  // WIDEN: [S][rows/2][width] ([Re x_t | Im x_t]); REAL: [S][rows][width]
+    const float *r0;        // [net][rows]
+    const uint16_t *perm;   // [net][epochs][rows]
+    float *plans;           // [net][plan_total] in/out
+    double *trace;          // [net][epochs] nullable
+    const int *status;      // [net] nullable
+    float lr, b1, b2, eps, omb1, omb2;
+    double b1d, b2d;
+    // shared-memory carve-up (floats)
+    int off_x, off_a[NOMA_MAX_DIMS], off_ps, off_gs, off_r0b, off_dy, off_red, off_misc;
+};
+
+struct DetectParams {
+    NetGeom g;
+    int layout, n_nets, K, rows, width;
+    const float *data;      // WIDEN: [S][rows][width/2] c32; REAL: [S][rows][width]
+    const float *plans;     // [net][plan_total]
+    const uint8_t *truth;   // WIDEN: [S][rows][K] codes, nullable
+    float *soft;            // WIDEN: [net][rows] c32; REAL: [net][rows]
+    uint8_t *codes;         // WIDEN: [net][rows]
+    uint32_t *errors;       // [net]
+    const int *status;      // [net] nullable
+    int tiles;              // per net
+    int off_x, off_a0, off_a1, off_ps, off_w0, off_y;
+};
+
+struct SynthParams {
+    int S, K, M, NT, ND;
+    double gain;           // cubic distortion
+    int noisy;             // snr finite
+    double snr_lin;        // 10^(snr/10), computed on the host (glibc pow)
+    const uint64_t *seeds; // master seeds [S]
+    const double *powers;  // [K], host-computed power_profile
+    double *pilot_rx;      // [S][NT][M] c64
+    double *pilot_sym;     // [S][NT][K] c64
+    float *data_rx;        // [S][ND][M] c32
+    uint8_t *data_codes;   // [S][ND][K]
+    double *channel;       // [S][M][K] c64 (scratch or output)
+    double *noise_power;   // [S]
+    uint8_t *codes_all;    // scratch [S][NT+ND][K]
+    double *noise;         // scratch [S][NT+ND][M] c64 (unit gaussians, g++ draw order)
+};
+
+int lls_launch(const LlsParams &p, cudaStream_t st);
+int perm_launch(int n_nets, int epochs, int n, const uint64_t *seeds, uint16_t *perm,
+                cudaStream_t st);
+int init_launch(const NetGeom &g, int n_nets, const uint64_t *seeds, const double *w0,
+                float *plans, cudaStream_t st);
+int set_w0_launch(int n_nets, int d0, int plan_total, const double *w0, float *plans,
+                  cudaStream_t st);
+int train_launch(TrainParams &p, cudaStream_t st);
+int detect_launch(DetectParams &p, cudaStream_t st);
+int synth_launch(SynthParams p, double *noise_power_scratch, cudaStream_t st);
+
+}  // namespace noma_dev

@@ -1,0 +1,110 @@
+"""GPU parity of the whole slot pipeline (noma_pipeline: LLS -> init -> fused
+training -> streaming detection) and of the device channel synthesiser,
+against the FP64 oracle's slot run (noma_cli.cpp:86-160 composition)."""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def A():
+    from paper_2206_05998_b200 import api
+
+    api.context()
+    return api
+
+
+def _seeds(O, seeds, K):
+    init = np.array([[O.substream_seed(s, 0x1000 + k + 1) for k in range(K)] for s in seeds],
+                    np.uint64)
+    shuf = np.array([[O.substream_seed(s, k + 1) for k in range(K)] for s in seeds], np.uint64)
+    return init, shuf
+
+
+@pytest.mark.parametrize("M,K,hidden,snr,epochs,S", [
+    (4, 3, [16], 20.0, 3, 2),
+    (16, 6, [64], 25.0, 50, 2),      # C1
+    (16, 6, [64, 64], 25.0, 10, 1),  # C2 shape (fewer epochs to bound oracle time)
+    (16, 6, [64], 8.0, 20, 2),       # low SNR: non-zero BER
+])
+def test_pipeline_matches_oracle(A, O, M, K, hidden, snr, epochs, S):
+    sc = O.Scenario(num_users=K, num_antennas=M, train_symbols=685 if M > 4 else 64,
+                    data_symbols=3840 if M > 4 else 256, power_step_db=3.0, snr_db=snr,
+                    rx_nonlinearity_gain=0.05)
+    seeds = [1000 + s for s in range(S)]
+    recs = [O.synthesize(sc, O.seed_bundle(s)) for s in seeds]
+    ref = O.run_slots(sc, hidden, seeds, epochs=epochs, threads=8)
+    dims = [2 * M] + hidden
+    init, shuf = _seeds(O, seeds, K)
+    truth = np.stack([A.codes_of(r.data_symbols) for r in recs])
+    out = A.pipeline(dims, np.stack([r.train_rx for r in recs]),
+                     np.stack([r.train_symbols for r in recs]),
+                     np.stack([r.data_rx for r in recs]), truth, init, shuf, epochs=epochs)
+    assert (out.status == 0).all()
+    werr = np.max(np.abs(out.w0 - ref.w0)) / np.max(np.abs(ref.w0))
+    assert werr < 1e-10
+    assert np.all(np.abs(out.gram_condition - ref.gram_condition) <= 1e-6 * ref.gram_condition)
+    scale = max(1.0, np.max(np.abs(ref.soft)))
+    assert np.max(np.abs(out.soft - ref.soft)) / scale < 2e-3
+    rcodes = A.codes_of(ref.soft)
+    flips = int(np.count_nonzero(out.codes != rcodes))
+    assert flips <= 1e-4 * out.codes.size + 0.5, flips
+    assert np.all(np.abs(out.bit_errors.astype(np.int64) - ref.bit_errors) <= 2 * flips)
+    assert np.all(np.abs(out.trace - ref.trace) <= 1e-2 * np.abs(ref.trace) + 1e-7)
+
+
+def test_ill_conditioned_slot_is_flagged(A, O):
+    # duplicate antennas -> rank-deficient complex design; random targets are
+    # inconsistent -> status ILL for every user, no training for them.
+    rng = np.random.default_rng(0)
+    NT, M, K, ND = 64, 4, 2, 32
+    x = rng.normal(size=(NT, M)) + 1j * rng.normal(size=(NT, M))
+    x[:, 1] = x[:, 0]
+    y = rng.normal(size=(NT, K)) + 1j * rng.normal(size=(NT, K))
+    init, shuf = _seeds(O, [5], K)
+    out = A.pipeline([8, 8], x[None], y[None], np.zeros((1, ND, M), np.complex64),
+                     np.zeros((1, ND, K), np.uint8), init, shuf, epochs=2)
+    assert (out.status == 3).all()
+    assert (out.gram_condition > 1e12).all()
+    assert (out.bit_errors == 0xFFFFFFFF).all()
+
+
+@pytest.mark.parametrize("K,M,NT,ND,snr,gain", [(6, 16, 685, 3840, 25.0, 0.05),
+                                               (3, 2, 16, 64, float("inf"), 0.0),
+                                               (8, 4, 32, 100, 10.0, 0.0)])
+def test_device_synthesis_matches_oracle(A, O, K, M, NT, ND, snr, gain):
+    seeds = [7, 1000, 2**40 + 3]
+    sy = A.synthesize(K, M, NT, ND, seeds, power_step_db=3.0, snr_db=snr, rx_nonlinearity_gain=gain)
+    sc = O.Scenario(num_users=K, num_antennas=M, train_symbols=NT, data_symbols=ND,
+                    power_step_db=3.0, snr_db=snr, rx_nonlinearity_gain=gain)
+    for i, s in enumerate(seeds):
+        rec = O.synthesize(sc, O.seed_bundle(s))
+        assert np.array_equal(sy.pilot_sym[i], rec.train_symbols)          # integer stream: exact
+        assert np.array_equal(sy.data_codes[i], A.codes_of(rec.data_symbols))
+        assert np.max(np.abs(sy.channel[i] - rec.channel)) <= 4e-16 * np.max(np.abs(rec.channel))
+        assert np.max(np.abs(sy.pilot_rx[i] - rec.train_rx)) <= 1e-14 * np.max(np.abs(rec.train_rx))
+        assert np.max(np.abs(sy.data_rx[i] - rec.data_rx.astype(np.complex64))) <= \
+            1e-6 * np.max(np.abs(rec.data_rx))
+        assert abs(sy.noise_power[i] - rec.noise_power) <= 1e-14 * max(rec.noise_power, 1e-300)
+
+
+def test_large_detect_self_consistent(A, O):
+    """C3-sized data phase (2^20 symbols): codes are the sign pattern of the
+    soft outputs and the error count equals the code mismatches vs truth."""
+    from tests.helpers import random_net_fused
+
+    onet = random_net_fused([32, 64, 64], 3)
+    layers, final = onet.layers()
+    net = A.net_from_params(onet.dims, onet.w0, layers, final)
+    sy = A.synthesize(6, 16, 32, 1 << 20, [11], snr_db=25.0, rx_nonlinearity_gain=0.05)
+    truth = sy.data_rx[0][:, 0].astype(np.complex128)
+    soft, bits, errs = A.detect(net, sy.data_rx[0], truth_symbols=truth)
+    assert np.array_equal(bits, O.hard_decision_qpsk(soft.astype(np.complex128)))
+    assert errs == int(np.count_nonzero(bits != O.hard_decision_qpsk(truth)))
+    # spot-check a slice against the FP64 reference forward
+    sl = slice(123456, 123456 + 2048)
+    from tests import refimpl as R
+    ref = O.narrow_predictions(R.reference_forward(onet.dims, onet.w0, layers, final,
+                                                   O.widen_design(sy.data_rx[0][sl])))
+    assert np.max(np.abs(soft[sl] - ref)) / max(1.0, np.max(np.abs(ref))) < 1e-5
