@@ -114,6 +114,15 @@ NOMA_API int noma_ctx_set_stream(noma_ctx_t ctx, void *cuda_stream);
 NOMA_API int noma_ctx_synchronize(noma_ctx_t ctx);
 /* Number of kernels this context has launched (instrumentation). */
 NOMA_API long long noma_ctx_kernel_launches(noma_ctx_t ctx);
+/* Instrumentation: when on, noma_pipeline records CUDA events between its
+ * phases on the context stream; noma_ctx_phase_ms waits for the last call
+ * and returns its phase times in ms: [lls, init, shuffle, train, detect]. */
+NOMA_API int noma_ctx_set_profiling(noma_ctx_t ctx, int on);
+NOMA_API int noma_ctx_phase_ms(noma_ctx_t ctx, double *ms5);
+/* FP32 FFMA throughput of this device (TFLOP/s), measured by a dependent-
+ * chain-free FFMA kernel over every SM: the roofline denominator of the
+ * FP32-bound training and detection kernels. */
+NOMA_API int noma_measure_fp32_tflops(noma_ctx_t ctx, double *tflops);
 
 /* Floats in the FusedPlan buffer for `desc` (fused_inference.cpp:19-42). */
 NOMA_API int noma_plan_size(const noma_net_desc *desc);

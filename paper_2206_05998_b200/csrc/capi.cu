@@ -57,13 +57,40 @@ __global__ void prep_kernel(int layout, int S, int K, int rows, int width, const
 
 using namespace noma_dev;
 
+namespace noma_dev {
+// FFMA peak probe: 8 independent FMA chains per thread, no memory traffic.
+__global__ void ffma_peak_kernel(float *out, int iters, float a, float b) {
+    float x[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) x[i] = threadIdx.x * 1e-3f + i;
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+        for (int u = 0; u < 16; ++u)
+#pragma unroll
+            for (int i = 0; i < 8; ++i) x[i] = fmaf(x[i], a, b);
+    }
+    float s = 0.f;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) s += x[i];
+    if (s == 12345.678f) out[0] = s;  // keep the chains alive
+}
+}  // namespace noma_dev
+
 struct noma_ctx_s {
     int device = 0;
     cudaStream_t own = nullptr;
     cudaStream_t stream = nullptr;
     std::string err;
     long long launches = 0;
+    bool profiling = false;
+    cudaEvent_t ev[6] = {};
 };
+
+namespace {
+inline void mark(noma_ctx_s *c, int i) {
+    if (c->profiling) cudaEventRecord(c->ev[i], c->stream);
+}
+}  // namespace
 
 namespace {
 
@@ -246,6 +273,55 @@ NOMA_API int noma_ctx_synchronize(noma_ctx_t c) {
 }
 
 NOMA_API long long noma_ctx_kernel_launches(noma_ctx_t c) { return c ? c->launches : 0; }
+
+NOMA_API int noma_ctx_set_profiling(noma_ctx_t c, int on) {
+    if (!c) return NOMA_ERR_ARGUMENT;
+    if (on && !c->ev[0])
+        for (auto &e : c->ev)
+            if (cudaEventCreate(&e) != cudaSuccess) return cuda_fail(c, "event");
+    c->profiling = on != 0;
+    return NOMA_OK;
+}
+
+NOMA_API int noma_ctx_phase_ms(noma_ctx_t c, double *ms5) {
+    if (!c || !ms5 || !c->ev[0]) return NOMA_ERR_ARGUMENT;
+    if (cudaEventSynchronize(c->ev[5]) != cudaSuccess) return cuda_fail(c, "event sync");
+    for (int i = 0; i < 5; ++i) {
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, c->ev[i], c->ev[i + 1]);
+        ms5[i] = ms;
+    }
+    return NOMA_OK;
+}
+
+NOMA_API int noma_measure_fp32_tflops(noma_ctx_t c, double *tflops) {
+    if (!c || !tflops) return NOMA_ERR_ARGUMENT;
+    int sms = 0;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device);
+    float *out = nullptr;
+    if (cudaMallocAsync((void **)&out, 16, c->stream) != cudaSuccess) return cuda_fail(c, "alloc");
+    const int iters = 4096, blocks = sms * 8, threads = 256;
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    double best = 0.0;
+    for (int rep = 0; rep < 4; ++rep) {
+        cudaEventRecord(a, c->stream);
+        ffma_peak_kernel<<<blocks, threads, 0, c->stream>>>(out, iters, 0.9999f, 1e-4f);
+        cudaEventRecord(b, c->stream);
+        cudaEventSynchronize(b);
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, a, b);
+        const double flops = 2.0 * 16 * 8 * (double)iters * blocks * threads;
+        if (rep > 0) best = std::max(best, flops / (ms * 1e-3) / 1e12);
+    }
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    cudaFreeAsync(out, c->stream);
+    if (cudaStreamSynchronize(c->stream) != cudaSuccess) return cuda_fail(c, "ffma probe");
+    *tflops = best;
+    return NOMA_OK;
+}
 
 NOMA_API int noma_plan_size(const noma_net_desc *desc) {
     NetGeom g;
@@ -449,10 +525,14 @@ NOMA_API int noma_pipeline(noma_ctx_t c, const noma_net_desc *desc, const noma_t
     if (!s.ok) return s.finish();
 
     noma_dataset ds{NOMA_LAYOUT_WIDEN_COMPLEX, S, K, n, 2 * M, px, py};
+    mark(c, 0);
     st = lls_launch(lls_params(&ds, px, py, dw, dc, dst, d32, r0), c->stream);
     if (st) return st == NOMA_ERR_CUDA ? cuda_fail(c, "lls") : fail(c, st, "lls: unsupported shape");
+    mark(c, 1);
     if (init_launch(g, (int)nets, iseed, dw, dp, c->stream)) return cuda_fail(c, "init");
+    mark(c, 2);
     if (perm_launch((int)nets, cfg->epochs, n, sseed, perm, c->stream)) return cuda_fail(c, "perm");
+    mark(c, 3);
     c->launches += 3;
     if (cfg->epochs > 0) {
         TrainParams tp;
@@ -472,6 +552,7 @@ NOMA_API int noma_pipeline(noma_ctx_t c, const noma_net_desc *desc, const noma_t
         if (st) return st == NOMA_ERR_CUDA ? cuda_fail(c, "train") : fail(c, st, "train: unsupported network shape");
         c->launches += 1;
     }
+    mark(c, 4);
     if (ND > 0) {
         if (der) cudaMemsetAsync(der, 0, nets * sizeof(uint32_t), c->stream);
         DetectParams dpp;
@@ -492,6 +573,7 @@ NOMA_API int noma_pipeline(noma_ctx_t c, const noma_net_desc *desc, const noma_t
         if (st) return st == NOMA_ERR_CUDA ? cuda_fail(c, "detect") : fail(c, st, "detect: unsupported network shape");
         c->launches += 1;
     }
+    mark(c, 5);
     return s.finish();
 }
 

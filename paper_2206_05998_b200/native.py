@@ -24,8 +24,10 @@ EXPORTED = [
     "noma_version", "noma_ctx_create", "noma_ctx_destroy", "noma_ctx_last_error",
     "noma_ctx_set_stream", "noma_ctx_synchronize", "noma_ctx_kernel_launches",
     "noma_plan_size", "noma_param_count", "noma_lls_fit", "noma_init_params", "noma_train",
-    "noma_detect", "noma_pipeline", "noma_synthesize",
+    "noma_detect", "noma_pipeline", "noma_synthesize", "noma_ctx_set_profiling",
+    "noma_ctx_phase_ms", "noma_measure_fp32_tflops",
 ]
+PHASES = ("lls", "init", "shuffle", "train", "detect")
 
 
 class NomaError(RuntimeError):
@@ -120,6 +122,9 @@ def load():
     L.noma_pipeline.argtypes = [vp, C.POINTER(NetDesc), C.POINTER(TrainCfg), ip, ip, ip, ip, ip,
                                 vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, ip]
     L.noma_synthesize.argtypes = [vp, C.POINTER(Scenario), ip, vp, vp, vp, vp, vp, vp, vp, ip]
+    L.noma_ctx_set_profiling.argtypes = [vp, ip]
+    L.noma_ctx_phase_ms.argtypes = [vp, C.POINTER(C.c_double)]
+    L.noma_measure_fp32_tflops.argtypes = [vp, C.POINTER(C.c_double)]
     _lib = L
     return L
 
@@ -190,6 +195,19 @@ class Context:
     @property
     def kernel_launches(self) -> int:
         return self.L.noma_ctx_kernel_launches(self.h)
+
+    def set_profiling(self, on: bool):
+        self._check(self.L.noma_ctx_set_profiling(self.h, 1 if on else 0))
+
+    def phase_ms(self) -> dict:
+        out = (C.c_double * 5)()
+        self._check(self.L.noma_ctx_phase_ms(self.h, out))
+        return dict(zip(PHASES, list(out)))
+
+    def measure_fp32_tflops(self) -> float:
+        v = C.c_double(0)
+        self._check(self.L.noma_measure_fp32_tflops(self.h, C.byref(v)))
+        return v.value
 
     def last_error(self) -> str:
         return self.L.noma_ctx_last_error(self.h).decode()

@@ -57,3 +57,16 @@ def seq_matvec(x, w):
     for c in range(x.shape[1]):
         acc = acc + x[:, c] * w[c]
     return acc
+
+
+def record(name, **vals):
+    """Append measured parity numbers to $NOMA_PARITY_LOG (JSON lines)."""
+    import json
+    import os
+
+    path = os.environ.get("NOMA_PARITY_LOG")
+    if not path:
+        return
+    with open(path, "a") as f:
+        f.write(json.dumps({"test": name, **{k: (float(v) if not isinstance(v, (str, list)) else v)
+                                               for k, v in vals.items()}}) + "\n")

@@ -5,19 +5,27 @@ through the C-ABI.
 Tolerances (stated):
   * inference with identical weights: |soft - ref| <= 1e-5 * max(1, max|ref|)
     (test_fused.cpp:128-130, the reference's own FP32 tolerance);
-  * FP32-trained vs FP64-trained (oracle) networks: soft outputs within
-    SOFT_TOL * max(1, max|ref|), hard decisions identical on >= 99.99 % of
-    symbols, |delta BER| <= flips / (2 N_D);
+  * FP32-trained vs FP64-trained (oracle) networks: short trainings (<= 5
+    epochs) soft outputs within SOFT_TOL_SHORT * max(1, max|ref|); full
+    trainings within SOFT_TOL_LONG -- FP32 Adam (lr/eps = 5e5 gain) through
+    ReLU kinks bifurcates from the FP64 trajectory: an independent numpy FP32
+    restatement of the same algorithm deviates from FP64 by up to 1.2e-2 on the
+    C1 weakest user, so SOFT_TOL_LONG = 1e-1; hard
+    decisions identical on >= 99.99 % of symbols, |delta BER| <= flips / (2 N_D),
+    loss trace within TRACE_TOL relative.  Measured on B200 (profiles/parity_r01.md):
+    <= 5e-7 soft deviation up to 20 epochs, 4e-3..4e-2 after 50 epochs, 0 flips at 25 dB;
   * init weights equal to the FP64 draws rounded to FP32 within 1 ulp.
 """
 import numpy as np
 import pytest
 
 from tests import refimpl as R
-from tests.helpers import make_w0, random_mat, random_net_fused
+from tests.helpers import make_w0, random_mat, random_net_fused, record
 
 pytestmark = pytest.mark.gpu
-SOFT_TOL = 2e-3
+SOFT_TOL_SHORT = 1e-4
+SOFT_TOL_LONG = 1e-1
+TRACE_TOL = 1e-1
 INFER_TOL = 1e-5
 
 
@@ -199,25 +207,34 @@ def test_error_paths(A):
 
 @pytest.mark.parametrize("M,K,k,hidden,snr,epochs", [
     (4, 2, 1, [8], 20.0, 5),
-    (16, 6, 5, [64], 25.0, 50),        # C1 shape, weakest user
+    (16, 6, 5, [64], 25.0, 5),         # C1 shape, weakest user, short
+    (16, 6, 5, [64, 64], 25.0, 5),     # C2 shape, short
+    (16, 6, 5, [64], 25.0, 50),        # C1 shape, full training
+    (16, 6, 0, [64], 25.0, 50),        # C1 shape, strongest user
     (16, 6, 5, [64, 64], 25.0, 50),    # C2 shape, weakest user
     (16, 6, 3, [64, 64], 10.0, 20),    # low SNR: decisions stressed
+    (16, 6, 5, [64], 8.0, 20),         # very low SNR: BER > 0
+    (32, 16, 15, [64, 64], 25.0, 5),   # C5 shape
+    (64, 32, 31, [64], 25.0, 2),       # C4 shape (input width 128)
 ])
 def test_fp32_training_tracks_fp64_reference(A, O, M, K, k, hidden, snr, epochs):
     sc = O.Scenario(num_users=K, num_antennas=M, train_symbols=685, data_symbols=3840,
-                    power_step_db=3.0, snr_db=snr, rx_nonlinearity_gain=0.05, seed=1000 + M + k)
+                    power_step_db=3.0 if K <= 6 else 1.0, snr_db=snr, rx_nonlinearity_gain=0.05,
+                    seed=1000 + M + k)
     dims = [2 * M] + hidden
     rec, onet, dnet, otrace, dtrace = _train_pair(A, O, sc, k, dims, epochs, 77, 78)
-    # loss traces
-    assert np.all(np.abs(dtrace - otrace) <= 1e-2 * np.abs(otrace) + 1e-7)
-    # soft outputs and decisions on the data phase
+    trace_dev = float(np.max(np.abs(dtrace - otrace) / np.abs(otrace)))
     ref = O.detect(onet, O.widen_design(rec.data_rx))
     soft, bits, errs = A.detect(dnet, rec.data_rx, truth_symbols=rec.data_symbols[:, k])
     scale = max(1.0, np.max(np.abs(ref)))
     dev = np.max(np.abs(soft - ref)) / scale
-    assert dev < SOFT_TOL, dev
     rbits = O.hard_decision_qpsk(ref)
     flips = int(np.count_nonzero(np.any(bits != rbits, axis=1)))
-    assert flips <= 1e-4 * len(ref) + 0.5, flips
     ref_err = int(np.count_nonzero(rbits != O.hard_decision_qpsk(rec.data_symbols[:, k])))
+    record("fp32_training", config=str((M, K, k, hidden, snr, epochs)), soft_dev=dev,
+           trace_dev=trace_dev, flips=flips, symbols=len(ref), dev_bit_errors=errs,
+           ref_bit_errors=ref_err)
+    assert trace_dev <= (1e-4 if epochs <= 5 else TRACE_TOL), trace_dev
+    assert dev < (SOFT_TOL_SHORT if epochs <= 5 else SOFT_TOL_LONG), dev
+    assert flips <= 1e-4 * len(ref) + 0.5, flips
     assert abs(errs - ref_err) <= 2 * flips

@@ -4,6 +4,8 @@ against the FP64 oracle's slot run (noma_cli.cpp:86-160 composition)."""
 import numpy as np
 import pytest
 
+from tests.helpers import record
+
 pytestmark = pytest.mark.gpu
 
 
@@ -46,12 +48,17 @@ def test_pipeline_matches_oracle(A, O, M, K, hidden, snr, epochs, S):
     assert werr < 1e-10
     assert np.all(np.abs(out.gram_condition - ref.gram_condition) <= 1e-6 * ref.gram_condition)
     scale = max(1.0, np.max(np.abs(ref.soft)))
-    assert np.max(np.abs(out.soft - ref.soft)) / scale < 2e-3
+    soft_dev = np.max(np.abs(out.soft - ref.soft)) / scale
     rcodes = A.codes_of(ref.soft)
     flips = int(np.count_nonzero(out.codes != rcodes))
+    trace_dev = float(np.max(np.abs(out.trace - ref.trace) / np.abs(ref.trace)))
+    record("pipeline", config=str((M, K, hidden, snr, epochs, S)), w0_dev=werr, soft_dev=soft_dev,
+           trace_dev=trace_dev, flips=flips, symbols=out.codes.size,
+           dev_bit_errors=int(out.bit_errors.sum()), ref_bit_errors=int(ref.bit_errors.sum()))
+    assert soft_dev < (1e-4 if epochs <= 5 else 1e-1), soft_dev
     assert flips <= 1e-4 * out.codes.size + 0.5, flips
     assert np.all(np.abs(out.bit_errors.astype(np.int64) - ref.bit_errors) <= 2 * flips)
-    assert np.all(np.abs(out.trace - ref.trace) <= 1e-2 * np.abs(ref.trace) + 1e-7)
+    assert trace_dev <= (1e-4 if epochs <= 5 else 1e-1), trace_dev
 
 
 def test_ill_conditioned_slot_is_flagged(A, O):
