@@ -178,7 +178,8 @@ def main():
     M, K, S = cfg["M"], cfg["K"], cfg["slots"]
     dims = [2 * M] + cfg["hidden"]
     ctx = N.Context(local)
-    stream = torch.cuda.current_stream()
+    stream = torch.cuda.Stream(device=local)  # a real stream (the legacy default is handle 0)
+    torch.cuda.set_stream(stream)
     ctx.set_stream(stream.cuda_stream)
     dev = torch.device("cuda", local)
 

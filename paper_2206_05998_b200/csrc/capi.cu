@@ -226,6 +226,7 @@ void fill_train(TrainParams &tp, const NetGeom &g, const noma_train_cfg *cfg) {
     tp.eps = (float)cfg->eps;
     tp.omb1 = (float)(1.0 - cfg->beta1);
     tp.omb2 = (float)(1.0 - cfg->beta2);
+    tp.lr_d = cfg->lr;
     tp.b1d = cfg->beta1;
     tp.b2d = cfg->beta2;
 }

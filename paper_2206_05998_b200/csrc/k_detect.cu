@@ -24,9 +24,10 @@ __global__ void __launch_bounds__(kThreads) detect_kernel(DetectParams p) {
     const NetGeom &g = p.g;
     const int N = g.nd - 1, d = net / p.K, k = net % p.K;
     float *XT = sm + p.off_x, *PS = sm + p.off_ps, *W0 = sm + p.off_w0, *Y = sm + p.off_y;
+    float *YP = sm + p.off_yp;
     float *buf[2] = {sm + p.off_a0, sm + p.off_a1};
 
-    for (int i = tid; i < p.off_y + kBatchRows; i += kThreads) sm[i] = 0.0f;
+    for (int i = tid; i < p.off_end; i += kThreads) sm[i] = 0.0f;
     __syncthreads();
     const float *pl = p.plans + (size_t)net * g.plan_total;
     for (int c = tid; c < g.dims[0]; c += kThreads) W0[c] = pl[c];
@@ -72,8 +73,9 @@ __global__ void __launch_bounds__(kThreads) detect_kernel(DetectParams p) {
         const float *in = XT;
         for (int l = 1; l <= N; ++l) {
             float *out = buf[(l - 1) & 1];
-            tile_forward<true>(PS + g.pw[l], g.sw[l], PS + g.pb[l], in, out, g.fp[l], g.fp[l - 1],
-                               warp, lane);
+            tile_forward<kThreads / 32>(PS + g.pw[l], g.sw[l], PS + g.pb[l], in, out, g.fp[l],
+                                        g.fp[l - 1], warp, lane, l == N ? PS + g.pf : nullptr,
+                                        l == N ? YP : nullptr);
             __syncthreads();
             in = out;
         }
@@ -82,8 +84,12 @@ __global__ void __launch_bounds__(kThreads) detect_kernel(DetectParams p) {
             float lin = 0.0f;
             for (int c = 0; c < g.fp[0]; ++c) lin = fmaf(W0[c], XT[c * kSR + tid], lin);
             float br = 0.0f;
-            const float *wf = PS + g.pf;
-            for (int j = 0; j < g.fp[N]; ++j) br = fmaf(wf[j], in[j * kSR + tid], br);
+            if (N) {
+                for (int b = 0; b < (g.fp[N] >> 4); ++b) br += YP[b * kBatchRows + tid];
+            } else {
+                const float *wf = PS + g.pf;
+                for (int j = 0; j < g.fp[N]; ++j) br = fmaf(wf[j], in[j * kSR + tid], br);
+            }
             Y[tid] = lin + br;
         }
         __syncthreads();
@@ -133,6 +139,9 @@ int detect_launch(DetectParams &p, cudaStream_t st) {
     off += g.fp[0];
     p.off_y = off;
     off += kBatchRows;
+    p.off_yp = off;
+    off += (g.fp[g.nd - 1] / 16) * kBatchRows;
+    p.off_end = off;
     const size_t smem = (size_t)off * sizeof(float);
     if (smem > 227 * 1024) return NOMA_ERR_UNSUPPORTED;
     const int rows_per_tile = p.layout == NOMA_LAYOUT_WIDEN_COMPLEX ? kBatchRows / 2 : kBatchRows;

@@ -1,7 +1,7 @@
 // Pilot-phase training on sm_100a: replaces hybrid_nn::train
 // (hybrid_nn.cpp:158-195) together with loss_and_grad (:84-114) and
-// adam_step (:118-144) -- one fused kernel, one CTA per user network, for all
-// epochs x minibatches.
+// adam_step (:118-144) -- one fused kernel, one CTA (16 warps) per user
+// network, for all epochs x minibatches.
 //
 // On-chip state for the whole training (never leaves the SM):
 //   * weights, biases, final layer      -- shared memory (FP32)
@@ -11,7 +11,8 @@
 // Per minibatch: gather the shuffled rows straight from the (L2-resident)
 // design -- the IQ-symmetry widening (iq_transform.cpp:17-20) is applied at
 // load: odd widened rows are [Im; -Re] of the stored complex row -- then
-// forward, residual, backward and the Adam update, separated by CTA barriers.
+// forward (final-layer dot fused into the last hidden layer's epilogue),
+// residual, backward and the Adam update, separated by CTA barriers.
 //
 // Frozen linear branch: w0 never changes during training (hybrid_nn.cpp:
 // 129-144 never touches it), so the LLS kernel precomputes r0 = y - X w0 in
@@ -25,8 +26,11 @@
 
 namespace noma_dev {
 
+constexpr int kTrainThreads = 512;
+constexpr int kTrainWarps = kTrainThreads / 32;
+
 template <int NSLOT>
-__global__ void __launch_bounds__(kThreads, 1) train_kernel(TrainParams p) {
+__global__ void __launch_bounds__(kTrainThreads, 1) train_kernel(TrainParams p) {
     extern __shared__ __align__(16) float sm[];
     const int net = blockIdx.x;
     if (p.status && p.status[net] != NOMA_OK) return;
@@ -39,112 +43,126 @@ __global__ void __launch_bounds__(kThreads, 1) train_kernel(TrainParams p) {
     float *GS = sm + p.off_gs;
     float *r0b = sm + p.off_r0b;
     float *dy = sm + p.off_dy;
-    float *red = sm + p.off_red;
-    float *misc = sm + p.off_misc;  // [0]=lr/corr-independent scratch: c1, c2
+    float *red = sm + p.off_red;    // 128 floats: epoch loss reduction
+    float *misc = sm + p.off_misc;  // [0] lr/corr1, [1] 1/corr2
+    float *yp = sm + p.off_yp;      // [fp_N/16][128] final-layer partials
 
-    // zero everything (padding must stay zero for the whole training)
-    for (int i = tid; i < p.off_misc + 8; i += kThreads) sm[i] = 0.0f;
+    for (int i = tid; i < p.off_end; i += kTrainThreads) sm[i] = 0.0f;
     __syncthreads();
     const float *pl = p.plans + (size_t)net * g.plan_total;
     for (int l = 1; l <= N; ++l) {
         const int rowsl = g.dims[l], cols = g.dims[l - 1];
-        for (int i = tid; i < rowsl * cols; i += kThreads) {
+        for (int i = tid; i < rowsl * cols; i += kTrainThreads) {
             const int j = i / cols, c = i % cols;
             PS[g.pw[l] + j * g.sw[l] + c] = pl[g.plan_w[l] + j * g.plan_pad[l - 1] + c];
         }
-        for (int j = tid; j < rowsl; j += kThreads) PS[g.pb[l] + j] = pl[g.plan_b[l] + j];
+        for (int j = tid; j < rowsl; j += kTrainThreads) PS[g.pb[l] + j] = pl[g.plan_b[l] + j];
     }
-    for (int j = tid; j < g.dims[N]; j += kThreads) PS[g.pf + j] = pl[g.plan_f + j];
+    for (int j = tid; j < g.dims[N]; j += kTrainThreads) PS[g.pf + j] = pl[g.plan_f + j];
 
     float mom1[NSLOT], mom2[NSLOT];
 #pragma unroll
     for (int s = 0; s < NSLOT; ++s) mom1[s] = mom2[s] = 0.0f;
     __syncthreads();
 
-    const int width = p.width, half_w = (width + 1) / 2, M = width / 2;
-    const float *AN = N ? sm + p.off_a[N] : XT;
+    const int width = p.width, M = width / 2;
+    const bool vec4 = (width & 3) == 0 && (M & 3) == 0;
     const int fpN = g.fp[N];
+    const int njb = fpN >> 4;  // final-layer partial blocks
+    float *AN = N ? sm + p.off_a[N] : XT;
+    float loss_acc = 0.0f;     // per-row-thread partial of the epoch loss
     long step = 0;
     for (int e = 0; e < p.epochs; ++e) {
-        double loss_sum = 0.0;
         const uint16_t *perm = p.perm + ((size_t)net * p.epochs + e) * n;
         for (int start = 0; start < n; start += p.batch) {
             const int bsz = min(p.batch, n - start);
-            // ---- gather (IQ widening at load) -------------------------------
+            // ---- gather (IQ widening at load): 4 threads per batch row ------
             {
-                const int r = tid & (kBatchRows - 1), h = tid >> 7;
-                const int c0 = h * half_w, c1 = min(width, c0 + half_w);
+                const int r = tid & (kBatchRows - 1), qtr = tid >> 7;
                 if (r < bsz) {
                     const int idx = perm[start + r];
-                    if (h == 0) r0b[r] = p.r0[(size_t)net * n + idx];
-                    if (p.layout == NOMA_LAYOUT_WIDEN_COMPLEX) {
-                        const float *src = p.design32 + ((size_t)d * (n >> 1) + (idx >> 1)) * width;
-                        if (idx & 1) {
-                            for (int c = c0; c < c1; ++c)
-                                XT[c * kSR + r] = c < M ? src[M + c] : -src[c - M];
-                        } else {
-                            for (int c = c0; c < c1; ++c) XT[c * kSR + r] = src[c];
+                    if (qtr == 0) r0b[r] = p.r0[(size_t)net * n + idx];
+                    const bool wid = p.layout == NOMA_LAYOUT_WIDEN_COMPLEX;
+                    const float *src = wid ? p.design32 + ((size_t)d * (n >> 1) + (idx >> 1)) * width
+                                           : p.design32 + ((size_t)d * n + idx) * width;
+                    const bool odd = wid && (idx & 1);
+                    if (vec4) {
+                        for (int c = qtr * 4; c < width; c += 16) {
+                            float4 v;
+                            if (!odd) {
+                                v = *reinterpret_cast<const float4 *>(src + c);
+                            } else if (c < M) {
+                                v = *reinterpret_cast<const float4 *>(src + M + c);
+                            } else {
+                                const float4 t = *reinterpret_cast<const float4 *>(src + c - M);
+                                v = make_float4(-t.x, -t.y, -t.z, -t.w);
+                            }
+                            XT[c * kSR + r] = v.x;
+                            XT[(c + 1) * kSR + r] = v.y;
+                            XT[(c + 2) * kSR + r] = v.z;
+                            XT[(c + 3) * kSR + r] = v.w;
                         }
                     } else {
-                        const float *src = p.design32 + ((size_t)d * n + idx) * width;
-                        for (int c = c0; c < c1; ++c) XT[c * kSR + r] = src[c];
+                        for (int c = qtr; c < width; c += 4)
+                            XT[c * kSR + r] = !odd ? src[c] : (c < M ? src[M + c] : -src[c - M]);
                     }
                 } else {
-                    if (h == 0) r0b[r] = 0.0f;
-                    for (int c = c0; c < c1; ++c) XT[c * kSR + r] = 0.0f;
+                    if (qtr == 0) r0b[r] = 0.0f;
+                    for (int c = qtr; c < width; c += 4) XT[c * kSR + r] = 0.0f;
+                }
+                if (tid == kTrainThreads - 1) {  // Adam constants for this step (FP64 pow)
+                    const double c1 = 1.0 - pow(p.b1d, (double)(step + 1));
+                    const double c2 = 1.0 - pow(p.b2d, (double)(step + 1));
+                    misc[0] = (float)(p.lr_d / c1);
+                    misc[1] = (float)(1.0 / c2);
                 }
             }
             __syncthreads();
-            // ---- forward (hybrid_nn.cpp:60-72) -------------------------------
+            // ---- forward (hybrid_nn.cpp:60-72); last layer also forms yp -----
             for (int l = 1; l <= N; ++l) {
-                tile_forward<true>(PS + g.pw[l], g.sw[l], PS + g.pb[l],
-                                   l == 1 ? XT : sm + p.off_a[l - 1], sm + p.off_a[l], g.fp[l],
-                                   g.fp[l - 1], warp, lane);
+                tile_forward<kTrainWarps>(PS + g.pw[l], g.sw[l], PS + g.pb[l],
+                                          l == 1 ? XT : sm + p.off_a[l - 1], sm + p.off_a[l],
+                                          g.fp[l], g.fp[l - 1], warp, lane,
+                                          l == N ? PS + g.pf : nullptr, l == N ? yp : nullptr);
                 __syncthreads();
             }
-            // ---- residual a_N w - r0, dy = 2 r / B, loss (hybrid_nn.cpp:94-98)
-            {
-                if (tid < kBatchRows) {
+            // ---- residual a_N w - r0, dy = 2 r / B (hybrid_nn.cpp:94-98) ------
+            if (tid < kBatchRows) {
+                float yhat = 0.0f;
+                if (N) {
+                    for (int b = 0; b < njb; ++b) yhat += yp[b * kBatchRows + tid];
+                } else {
                     const float *wf = PS + g.pf;
-                    float acc = 0.0f;
-                    for (int j = 0; j < fpN; ++j) acc = fmaf(AN[j * kSR + tid], wf[j], acc);
-                    const float res = tid < bsz ? acc - r0b[tid] : 0.0f;
-                    dy[tid] = (2.0f / (float)bsz) * res;
-                    float sq = res * res;
-#pragma unroll
-                    for (int o = 16; o > 0; o >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, o);
-                    if (lane == 0) red[warp] = sq;
+                    for (int j = 0; j < fpN; ++j) yhat = fmaf(XT[j * kSR + tid], wf[j], yhat);
                 }
-                if (tid == kThreads - 1) {  // Adam bias corrections for this step (FP64 pow)
-                    misc[0] = (float)(1.0 - pow(p.b1d, (double)(step + 1)));
-                    misc[1] = (float)(1.0 - pow(p.b2d, (double)(step + 1)));
-                }
+                const float res = tid < bsz ? yhat - r0b[tid] : 0.0f;
+                dy[tid] = (2.0f / (float)bsz) * res;
+                loss_acc = fmaf(res, res, loss_acc);
             }
             __syncthreads();
-            if (tid == 0) {
-                const float sq = (red[0] + red[1]) + (red[2] + red[3]);
-                const double lb = (double)sq / (double)bsz;
-                loss_sum += lb * (double)bsz;
-            }
-            // ---- final layer gradient and dZ_N (hybrid_nn.cpp:99-107) -------
+            // ---- final layer gradient and dZ_N (hybrid_nn.cpp:99-107) --------
             {
-                float *A = sm + (N ? p.off_a[N] : p.off_x);
                 const float *wf = PS + g.pf;
-                for (int j = warp; j < fpN; j += kThreads / 32) {
-                    float s = 0.0f;
+                for (int it = tid; it < fpN * 8; it += kTrainThreads) {  // fpN*8 % 256 == 0
+                    const int j = it >> 3, part = it & 7;
+                    float *row = AN + j * kSR + part;  // rows r = part + 8 q
+                    const float *dyp = dy + part;
+                    float s0 = 0.f, s1 = 0.f;
 #pragma unroll
-                    for (int q = 0; q < 4; ++q) s = fmaf(A[j * kSR + lane + 32 * q], dy[lane + 32 * q], s);
-#pragma unroll
-                    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-                    if (lane == 0) GS[g.pf + j] = s;
+                    for (int q = 0; q < 16; q += 2) {
+                        s0 = fmaf(row[8 * q], dyp[8 * q], s0);
+                        s1 = fmaf(row[8 * q + 8], dyp[8 * q + 8], s1);
+                    }
+                    float s = s0 + s1;
+                    s += __shfl_xor_sync(0xffffffffu, s, 1);
+                    s += __shfl_xor_sync(0xffffffffu, s, 2);
+                    s += __shfl_xor_sync(0xffffffffu, s, 4);
+                    if (part == 0) GS[g.pf + j] = s;
                     if (N) {
                         const float wj = wf[j];
 #pragma unroll
-                        for (int q = 0; q < 4; ++q) {
-                            const int r = lane + 32 * q;
-                            const float a = A[j * kSR + r];
-                            A[j * kSR + r] = a > 0.0f ? dy[r] * wj : 0.0f;
-                        }
+                        for (int q = 0; q < 16; ++q)
+                            row[8 * q] = row[8 * q] > 0.0f ? dyp[8 * q] * wj : 0.0f;
                     }
                 }
             }
@@ -152,45 +170,54 @@ __global__ void __launch_bounds__(kThreads, 1) train_kernel(TrainParams p) {
             // ---- backward (hybrid_nn.cpp:105-112) ----------------------------
             for (int l = N; l >= 1; --l) {
                 const float *ain = l == 1 ? XT : sm + p.off_a[l - 1];
-                tile_weight_grad(sm + p.off_a[l], ain, GS + g.pw[l], g.sw[l], GS + g.pb[l],
-                                 g.fp[l], g.fp[l - 1], warp, lane);
+                tile_weight_grad<kTrainWarps>(sm + p.off_a[l], ain, GS + g.pw[l], g.sw[l],
+                                              GS + g.pb[l], g.fp[l], g.fp[l - 1], warp, lane);
                 __syncthreads();
                 if (l > 1) {
-                    tile_backward_data(PS + g.pw[l], g.sw[l], sm + p.off_a[l], sm + p.off_a[l - 1],
-                                       g.fp[l - 1], g.fp[l], warp, lane);
+                    tile_backward_data<kTrainWarps>(PS + g.pw[l], g.sw[l], sm + p.off_a[l],
+                                                    sm + p.off_a[l - 1], g.fp[l - 1], g.fp[l],
+                                                    warp, lane);
                     __syncthreads();
                 }
             }
             // ---- Adam (hybrid_nn.cpp:118-144): FP32 moments in registers ----
             {
-                const float c1 = misc[0], c2 = misc[1];
+                const float lrc = misc[0], ic2 = misc[1];
 #pragma unroll
                 for (int s = 0; s < NSLOT; ++s) {
-                    const int i = tid + s * kThreads;
+                    const int i = tid + s * kTrainThreads;
                     if (i < g.ptotal) {
                         const float gi = GS[i];
                         mom1[s] = p.b1 * mom1[s] + p.omb1 * gi;
                         mom2[s] = p.b2 * mom2[s] + p.omb2 * (gi * gi);
-                        PS[i] -= p.lr * (mom1[s] / c1) / (sqrtf(mom2[s] / c2) + p.eps);
+                        PS[i] -= __fdividef(lrc * mom1[s], sqrtf(mom2[s] * ic2) + p.eps);
                     }
                 }
             }
             ++step;
             __syncthreads();
         }
-        if (tid == 0 && p.trace) p.trace[(size_t)net * p.epochs + e] = loss_sum / (double)n;
+        // ---- epoch loss (hybrid_nn.cpp:190-192): trace[e] = sum r^2 / n ------
+        if (tid < kBatchRows) red[tid] = loss_acc;
+        loss_acc = 0.0f;
+        __syncthreads();
+        if (tid == 0 && p.trace) {
+            double s = 0.0;
+            for (int i = 0; i < kBatchRows; ++i) s += red[i];
+            p.trace[(size_t)net * p.epochs + e] = s / (double)n;
+        }
     }
     // ---- write the trained parameters back in FusedPlan layout -------------
     float *po = p.plans + (size_t)net * g.plan_total;
     for (int l = 1; l <= N; ++l) {
         const int rowsl = g.dims[l], cols = g.dims[l - 1];
-        for (int i = tid; i < rowsl * cols; i += kThreads) {
+        for (int i = tid; i < rowsl * cols; i += kTrainThreads) {
             const int j = i / cols, c = i % cols;
             po[g.plan_w[l] + j * g.plan_pad[l - 1] + c] = PS[g.pw[l] + j * g.sw[l] + c];
         }
-        for (int j = tid; j < rowsl; j += kThreads) po[g.plan_b[l] + j] = PS[g.pb[l] + j];
+        for (int j = tid; j < rowsl; j += kTrainThreads) po[g.plan_b[l] + j] = PS[g.pb[l] + j];
     }
-    for (int j = tid; j < g.dims[N]; j += kThreads) po[g.plan_f + j] = PS[g.pf + j];
+    for (int j = tid; j < g.dims[N]; j += kTrainThreads) po[g.plan_f + j] = PS[g.pf + j];
 }
 
 // host: carve shared memory, pick the moment-slot instantiation, launch.
@@ -215,26 +242,29 @@ int train_launch(TrainParams &p, cudaStream_t st) {
     p.off_dy = off;
     off += kBatchRows;
     p.off_red = off;
-    off += 32;
+    off += kBatchRows;
+    p.off_yp = off;
+    off += (g.fp[g.nd - 1] / 16) * kBatchRows;
     p.off_misc = off;
     off += 8;
+    p.off_end = off;
     const size_t smem = (size_t)off * sizeof(float);
     if (smem > 227 * 1024) return NOMA_ERR_UNSUPPORTED;
-    const int need = (g.ptotal + kThreads - 1) / kThreads;
+    const int need = (g.ptotal + kTrainThreads - 1) / kTrainThreads;
 #define NOMA_TRAIN_CASE(NS)                                                                    \
     if (need <= NS) {                                                                          \
         cudaFuncSetAttribute(train_kernel<NS>, cudaFuncAttributeMaxDynamicSharedMemorySize,    \
                              (int)smem);                                                       \
-        train_kernel<NS><<<p.n_nets, kThreads, smem, st>>>(p);                                 \
+        train_kernel<NS><<<p.n_nets, kTrainThreads, smem, st>>>(p);                            \
         return cudaGetLastError() == cudaSuccess ? NOMA_OK : NOMA_ERR_CUDA;                    \
     }
+    NOMA_TRAIN_CASE(4)
     NOMA_TRAIN_CASE(8)
+    NOMA_TRAIN_CASE(12)
     NOMA_TRAIN_CASE(16)
+    NOMA_TRAIN_CASE(20)
     NOMA_TRAIN_CASE(24)
     NOMA_TRAIN_CASE(32)
-    NOMA_TRAIN_CASE(40)
-    NOMA_TRAIN_CASE(48)
-    NOMA_TRAIN_CASE(64)
 #undef NOMA_TRAIN_CASE
     return NOMA_ERR_UNSUPPORTED;
 }

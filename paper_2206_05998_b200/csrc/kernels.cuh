@@ -28,9 +28,10 @@ struct TrainParams {
     double *trace;          // [net][epochs] nullable
     const int *status;      // [net] nullable
     float lr, b1, b2, eps, omb1, omb2;
-    double b1d, b2d;
+    double lr_d, b1d, b2d;
     // shared-memory carve-up (floats)
-    int off_x, off_a[NOMA_MAX_DIMS], off_ps, off_gs, off_r0b, off_dy, off_red, off_misc;
+    int off_x, off_a[NOMA_MAX_DIMS], off_ps, off_gs, off_r0b, off_dy, off_red, off_yp, off_misc,
+        off_end;
 };
 
 struct DetectParams {
@@ -44,7 +45,7 @@ struct DetectParams {
     uint32_t *errors;       // [net]
     const int *status;      // [net] nullable
     int tiles;              // per net
-    int off_x, off_a0, off_a1, off_ps, off_w0, off_y;
+    int off_x, off_a0, off_a1, off_ps, off_w0, off_y, off_yp, off_end;
 };
 
 struct SynthParams {

@@ -186,8 +186,14 @@ class Context:
         self.L.noma_ctx_set_stream(self.h, C.c_void_p(stream_ptr) if stream_ptr else None)
 
     def use_torch_stream(self):
+        """Bind to torch's current stream (must not be the legacy default
+        stream, whose handle 0 means 'the context's own stream' here)."""
         import torch
-        self.set_stream(torch.cuda.current_stream(self.device).cuda_stream)
+        s = torch.cuda.current_stream(self.device).cuda_stream
+        if not s:
+            raise ValueError("torch's current stream is the legacy default stream; "
+                             "set a torch.cuda.Stream first")
+        self.set_stream(s)
 
     def synchronize(self):
         self._check(self.L.noma_ctx_synchronize(self.h))

@@ -26,7 +26,9 @@ NT, ND = bench.NT, bench.ND
 dims = [2 * M] + cfg["hidden"]
 dev = torch.device("cuda", 0)
 ctx = N.Context(0)
-ctx.set_stream(torch.cuda.current_stream().cuda_stream)
+_stream = torch.cuda.Stream()
+torch.cuda.set_stream(_stream)
+ctx.set_stream(_stream.cuda_stream)
 seeds = np.arange(1000, 1000 + S, dtype=np.uint64)
 px = torch.empty((S, NT, M, 2), dtype=torch.float64, device=dev)
 py = torch.empty((S, NT, K, 2), dtype=torch.float64, device=dev)
