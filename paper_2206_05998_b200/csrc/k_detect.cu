@@ -85,7 +85,7 @@ __global__ void __launch_bounds__(kThreads) detect_kernel(DetectParams p) {
             for (int c = 0; c < g.fp[0]; ++c) lin = fmaf(W0[c], XT[c * kSR + tid], lin);
             float br = 0.0f;
             if (N) {
-                for (int b = 0; b < (g.fp[N] >> 4); ++b) br += YP[b * kBatchRows + tid];
+                for (int b = 0; b < (g.fp[N] >> 5); ++b) br += YP[b * kBatchRows + tid];
             } else {
                 const float *wf = PS + g.pf;
                 for (int j = 0; j < g.fp[N]; ++j) br = fmaf(wf[j], in[j * kSR + tid], br);
@@ -140,7 +140,7 @@ int detect_launch(DetectParams &p, cudaStream_t st) {
     p.off_y = off;
     off += kBatchRows;
     p.off_yp = off;
-    off += (g.fp[g.nd - 1] / 16) * kBatchRows;
+    off += (g.fp[g.nd - 1] / 32) * kBatchRows;
     p.off_end = off;
     const size_t smem = (size_t)off * sizeof(float);
     if (smem > 227 * 1024) return NOMA_ERR_UNSUPPORTED;

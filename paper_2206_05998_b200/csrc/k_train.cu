@@ -1,18 +1,19 @@
 // Pilot-phase training on sm_100a: replaces hybrid_nn::train
 // (hybrid_nn.cpp:158-195) together with loss_and_grad (:84-114) and
-// adam_step (:118-144) -- one fused kernel, one CTA (16 warps) per user
+// adam_step (:118-144) -- one fused kernel, one CTA (8 warps) per user
 // network, for all epochs x minibatches.
 //
 // On-chip state for the whole training (never leaves the SM):
 //   * weights, biases, final layer      -- shared memory (FP32)
-//   * gradients                         -- shared memory (FP32)
+//   * gradients (1-2 split partials)    -- shared memory (FP32)
 //   * Adam first/second moments         -- registers (NSLOT per thread)
 //   * minibatch input and activations   -- shared memory, feature-major
 // Per minibatch: gather the shuffled rows straight from the (L2-resident)
 // design -- the IQ-symmetry widening (iq_transform.cpp:17-20) is applied at
 // load: odd widened rows are [Im; -Re] of the stored complex row -- then
 // forward (final-layer dot fused into the last hidden layer's epilogue),
-// residual, backward and the Adam update, separated by CTA barriers.
+// residual, backward and the Adam update, separated by CTA barriers.  The
+// dense contractions use the 8x4 FFMA register tiles of tiles.cuh.
 //
 // Frozen linear branch: w0 never changes during training (hybrid_nn.cpp:
 // 129-144 never touches it), so the LLS kernel precomputes r0 = y - X w0 in
@@ -26,11 +27,17 @@
 
 namespace noma_dev {
 
-constexpr int kTrainThreads = 512;
+constexpr int kTrainThreads = 256;
 constexpr int kTrainWarps = kTrainThreads / 32;
+constexpr int kMaxSplit = 2;  // weight-gradient split-K partials
 
-template <int NSLOT>
-__global__ void __launch_bounds__(kTrainThreads, 1) train_kernel(TrainParams p) {
+__host__ __device__ inline int grad_splits(int J, int C) {
+    const int tiles = (J >> 5) * (C >> 5);
+    return tiles < kTrainWarps ? kMaxSplit : 1;
+}
+
+template <int NSLOT, int MINB>
+__global__ void __launch_bounds__(kTrainThreads, MINB) train_kernel(TrainParams p) {
     extern __shared__ __align__(16) float sm[];
     const int net = blockIdx.x;
     if (p.status && p.status[net] != NOMA_OK) return;
@@ -38,6 +45,7 @@ __global__ void __launch_bounds__(kTrainThreads, 1) train_kernel(TrainParams p) 
     const NetGeom &g = p.g;
     const int N = g.nd - 1;  // hidden layers
     const int n = p.rows, d = net / p.K;
+    const int gstride = p.gs_stride;  // floats between gradient split partials
     float *XT = sm + p.off_x;
     float *PS = sm + p.off_ps;
     float *GS = sm + p.off_gs;
@@ -45,7 +53,7 @@ __global__ void __launch_bounds__(kTrainThreads, 1) train_kernel(TrainParams p) 
     float *dy = sm + p.off_dy;
     float *red = sm + p.off_red;    // 128 floats: epoch loss reduction
     float *misc = sm + p.off_misc;  // [0] lr/corr1, [1] 1/corr2
-    float *yp = sm + p.off_yp;      // [fp_N/16][128] final-layer partials
+    float *yp = sm + p.off_yp;      // [fp_N/32][128] final-layer partials
 
     for (int i = tid; i < p.off_end; i += kTrainThreads) sm[i] = 0.0f;
     __syncthreads();
@@ -68,7 +76,7 @@ __global__ void __launch_bounds__(kTrainThreads, 1) train_kernel(TrainParams p) 
     const int width = p.width, M = width / 2;
     const bool vec4 = (width & 3) == 0 && (M & 3) == 0;
     const int fpN = g.fp[N];
-    const int njb = fpN >> 4;  // final-layer partial blocks
+    const int njb = fpN >> 5;  // final-layer partial blocks
     float *AN = N ? sm + p.off_a[N] : XT;
     float loss_acc = 0.0f;     // per-row-thread partial of the epoch loss
     long step = 0;
@@ -76,18 +84,18 @@ __global__ void __launch_bounds__(kTrainThreads, 1) train_kernel(TrainParams p) 
         const uint16_t *perm = p.perm + ((size_t)net * p.epochs + e) * n;
         for (int start = 0; start < n; start += p.batch) {
             const int bsz = min(p.batch, n - start);
-            // ---- gather (IQ widening at load): 4 threads per batch row ------
+            // ---- gather (IQ widening at load): 2 threads per batch row ------
             {
-                const int r = tid & (kBatchRows - 1), qtr = tid >> 7;
+                const int r = tid & (kBatchRows - 1), h = tid >> 7;
                 if (r < bsz) {
                     const int idx = perm[start + r];
-                    if (qtr == 0) r0b[r] = p.r0[(size_t)net * n + idx];
+                    if (h == 0) r0b[r] = p.r0[(size_t)net * n + idx];
                     const bool wid = p.layout == NOMA_LAYOUT_WIDEN_COMPLEX;
                     const float *src = wid ? p.design32 + ((size_t)d * (n >> 1) + (idx >> 1)) * width
                                            : p.design32 + ((size_t)d * n + idx) * width;
                     const bool odd = wid && (idx & 1);
                     if (vec4) {
-                        for (int c = qtr * 4; c < width; c += 16) {
+                        for (int c = h * 4; c < width; c += 8) {
                             float4 v;
                             if (!odd) {
                                 v = *reinterpret_cast<const float4 *>(src + c);
@@ -103,12 +111,12 @@ __global__ void __launch_bounds__(kTrainThreads, 1) train_kernel(TrainParams p) 
                             XT[(c + 3) * kSR + r] = v.w;
                         }
                     } else {
-                        for (int c = qtr; c < width; c += 4)
+                        for (int c = h; c < width; c += 2)
                             XT[c * kSR + r] = !odd ? src[c] : (c < M ? src[M + c] : -src[c - M]);
                     }
                 } else {
-                    if (qtr == 0) r0b[r] = 0.0f;
-                    for (int c = qtr; c < width; c += 4) XT[c * kSR + r] = 0.0f;
+                    if (h == 0) r0b[r] = 0.0f;
+                    for (int c = h; c < width; c += 2) XT[c * kSR + r] = 0.0f;
                 }
                 if (tid == kTrainThreads - 1) {  // Adam constants for this step (FP64 pow)
                     const double c1 = 1.0 - pow(p.b1d, (double)(step + 1));
@@ -171,7 +179,9 @@ __global__ void __launch_bounds__(kTrainThreads, 1) train_kernel(TrainParams p) 
             for (int l = N; l >= 1; --l) {
                 const float *ain = l == 1 ? XT : sm + p.off_a[l - 1];
                 tile_weight_grad<kTrainWarps>(sm + p.off_a[l], ain, GS + g.pw[l], g.sw[l],
-                                              GS + g.pb[l], g.fp[l], g.fp[l - 1], warp, lane);
+                                              GS + g.pb[l], g.fp[l], g.fp[l - 1],
+                                              grad_splits(g.fp[l], g.fp[l - 1]), gstride, warp,
+                                              lane);
                 __syncthreads();
                 if (l > 1) {
                     tile_backward_data<kTrainWarps>(PS + g.pw[l], g.sw[l], sm + p.off_a[l],
@@ -187,7 +197,7 @@ __global__ void __launch_bounds__(kTrainThreads, 1) train_kernel(TrainParams p) 
                 for (int s = 0; s < NSLOT; ++s) {
                     const int i = tid + s * kTrainThreads;
                     if (i < g.ptotal) {
-                        const float gi = GS[i];
+                        const float gi = GS[i] + GS[gstride + i];  // fixed-order split sum
                         mom1[s] = p.b1 * mom1[s] + p.omb1 * gi;
                         mom2[s] = p.b2 * mom2[s] + p.omb2 * (gi * gi);
                         PS[i] -= __fdividef(lrc * mom1[s], sqrtf(mom2[s] * ic2) + p.eps);
@@ -235,8 +245,9 @@ int train_launch(TrainParams &p, cudaStream_t st) {
     }
     p.off_ps = off;
     off += pad_to(g.ptotal, 4);
+    p.gs_stride = pad_to(g.ptotal, 4);
     p.off_gs = off;
-    off += pad_to(g.ptotal, 4);
+    off += kMaxSplit * p.gs_stride;
     p.off_r0b = off;
     off += kBatchRows;
     p.off_dy = off;
@@ -244,28 +255,31 @@ int train_launch(TrainParams &p, cudaStream_t st) {
     p.off_red = off;
     off += kBatchRows;
     p.off_yp = off;
-    off += (g.fp[g.nd - 1] / 16) * kBatchRows;
+    off += (g.fp[g.nd - 1] / 32) * kBatchRows;
     p.off_misc = off;
     off += 8;
     p.off_end = off;
     const size_t smem = (size_t)off * sizeof(float);
     if (smem > 227 * 1024) return NOMA_ERR_UNSUPPORTED;
     const int need = (g.ptotal + kTrainThreads - 1) / kTrainThreads;
-#define NOMA_TRAIN_CASE(NS)                                                                    \
-    if (need <= NS) {                                                                          \
-        cudaFuncSetAttribute(train_kernel<NS>, cudaFuncAttributeMaxDynamicSharedMemorySize,    \
-                             (int)smem);                                                       \
-        train_kernel<NS><<<p.n_nets, kTrainThreads, smem, st>>>(p);                            \
-        return cudaGetLastError() == cudaSuccess ? NOMA_OK : NOMA_ERR_CUDA;                    \
+    // two CTAs (nets) per SM when shared memory and the 128-register cap allow
+    const bool two = smem <= 112 * 1024 && need <= 16;
+#define NOMA_TRAIN_LAUNCH(NS, MB)                                                               \
+    {                                                                                           \
+        cudaFuncSetAttribute(train_kernel<NS, MB>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                             (int)smem);                                                        \
+        train_kernel<NS, MB><<<p.n_nets, kTrainThreads, smem, st>>>(p);                         \
+        return cudaGetLastError() == cudaSuccess ? NOMA_OK : NOMA_ERR_CUDA;                     \
     }
-    NOMA_TRAIN_CASE(4)
-    NOMA_TRAIN_CASE(8)
-    NOMA_TRAIN_CASE(12)
-    NOMA_TRAIN_CASE(16)
-    NOMA_TRAIN_CASE(20)
-    NOMA_TRAIN_CASE(24)
-    NOMA_TRAIN_CASE(32)
-#undef NOMA_TRAIN_CASE
+    if (two && need <= 8) NOMA_TRAIN_LAUNCH(8, 2)
+    if (two) NOMA_TRAIN_LAUNCH(16, 2)
+    if (need <= 8) NOMA_TRAIN_LAUNCH(8, 1)
+    if (need <= 16) NOMA_TRAIN_LAUNCH(16, 1)
+    if (need <= 24) NOMA_TRAIN_LAUNCH(24, 1)
+    if (need <= 32) NOMA_TRAIN_LAUNCH(32, 1)
+    if (need <= 48) NOMA_TRAIN_LAUNCH(48, 1)
+    if (need <= 64) NOMA_TRAIN_LAUNCH(64, 1)
+#undef NOMA_TRAIN_LAUNCH
     return NOMA_ERR_UNSUPPORTED;
 }
 
