@@ -248,6 +248,14 @@ NOMA_API int noma_ctx_create(int device, noma_ctx_t *out) {
         return NOMA_ERR_CUDA;
     }
     c->stream = c->own;
+    // Keep freed stream-ordered scratch in the pool: the default release
+    // threshold (0) hands it back to the OS at every synchronisation, which
+    // would put page-mapping latency inside every call.
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+        uint64_t keep = UINT64_MAX;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
     *out = c;
     return NOMA_OK;
 }

@@ -31,9 +31,9 @@ constexpr int kTrainThreads = 256;
 constexpr int kTrainWarps = kTrainThreads / 32;
 constexpr int kMaxSplit = 2;  // weight-gradient split-K partials
 
-__host__ __device__ inline int grad_splits(int J, int C) {
+__host__ __device__ inline int grad_splits(int J, int C, int max_split) {
     const int tiles = (J >> 5) * (C >> 5);
-    return tiles < kTrainWarps ? kMaxSplit : 1;
+    return tiles < kTrainWarps ? max_split : 1;
 }
 
 template <int NSLOT, int MINB>
@@ -180,7 +180,7 @@ __global__ void __launch_bounds__(kTrainThreads, MINB) train_kernel(TrainParams 
                 const float *ain = l == 1 ? XT : sm + p.off_a[l - 1];
                 tile_weight_grad<kTrainWarps>(sm + p.off_a[l], ain, GS + g.pw[l], g.sw[l],
                                               GS + g.pb[l], g.fp[l], g.fp[l - 1],
-                                              grad_splits(g.fp[l], g.fp[l - 1]), gstride, warp,
+                                              grad_splits(g.fp[l], g.fp[l - 1], p.gsplit), gstride, warp,
                                               lane);
                 __syncthreads();
                 if (l > 1) {
@@ -197,7 +197,8 @@ __global__ void __launch_bounds__(kTrainThreads, MINB) train_kernel(TrainParams 
                 for (int s = 0; s < NSLOT; ++s) {
                     const int i = tid + s * kTrainThreads;
                     if (i < g.ptotal) {
-                        const float gi = GS[i] + GS[gstride + i];  // fixed-order split sum
+                        // fixed-order sum of the split-K partials
+                        const float gi = p.gsplit > 1 ? GS[i] + GS[gstride + i] : GS[i];
                         mom1[s] = p.b1 * mom1[s] + p.omb1 * gi;
                         mom2[s] = p.b2 * mom2[s] + p.omb2 * (gi * gi);
                         PS[i] -= __fdividef(lrc * mom1[s], sqrtf(mom2[s] * ic2) + p.eps);
@@ -247,7 +248,10 @@ int train_launch(TrainParams &p, cudaStream_t st) {
     off += pad_to(g.ptotal, 4);
     p.gs_stride = pad_to(g.ptotal, 4);
     p.off_gs = off;
-    off += kMaxSplit * p.gs_stride;
+    // two split-K gradient partials when they fit, else one
+    const int base_rest = off + kBatchRows * 3 + (g.fp[g.nd - 1] / 32) * kBatchRows + 8;
+    p.gsplit = (size_t)(base_rest + kMaxSplit * p.gs_stride) * sizeof(float) <= 227 * 1024 ? kMaxSplit : 1;
+    off += p.gsplit * p.gs_stride;
     p.off_r0b = off;
     off += kBatchRows;
     p.off_dy = off;

@@ -178,17 +178,15 @@ __device__ __forceinline__ void tile_weight_grad(const float *__restrict__ dz,
             for (int i = 0; i < 8; ++i) z[i] = *reinterpret_cast<const float4 *>(dz + (j0 + 4 * i) * kSR + r);
 #pragma unroll
             for (int q = 0; q < 4; ++q) x[q] = *reinterpret_cast<const float4 *>(ain + (c0 + 8 * q) * kSR + r);
-#pragma unroll
-            for (int i = 0; i < 8; ++i)
-#pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                    float s = acc[i][q];
-                    s = fmaf(z[i].x, x[q].x, s);
-                    s = fmaf(z[i].y, x[q].y, s);
-                    s = fmaf(z[i].z, x[q].z, s);
-                    s = fmaf(z[i].w, x[q].w, s);
-                    acc[i][q] = s;
-                }
+            // component-major order: 32 independent FMAs between dependent ones
+#define NOMA_GRAD_C(KK)                                                                 \
+    _Pragma("unroll") for (int i = 0; i < 8; ++i) {                                     \
+        const float zi = f4c<KK>(z[i]);                                                 \
+        _Pragma("unroll") for (int q = 0; q < 4; ++q)                                   \
+            acc[i][q] = fmaf(zi, f4c<KK>(x[q]), acc[i][q]);                             \
+    }
+            NOMA_GRAD_C(0) NOMA_GRAD_C(1) NOMA_GRAD_C(2) NOMA_GRAD_C(3)
+#undef NOMA_GRAD_C
             if (cb == 0) {  // warp-uniform
 #pragma unroll
                 for (int i = 0; i < 8; ++i) sb[i] += (z[i].x + z[i].y) + (z[i].z + z[i].w);
