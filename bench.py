@@ -208,7 +208,8 @@ def main():
         ctx.pipeline(dims, tcfg, S, K, M, NT, ND, px, py, dx, truth, init_d, shuf_d, status,
                      w0=w0, plans=plans, codes=codes, bit_errors=errs)
 
-    peak_fp32 = ctx.measure_fp32_tflops()
+    peak_fp32 = ctx.measure_fp32_tflops(0)
+    peak_tile = ctx.measure_fp32_tflops(1)
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
@@ -331,7 +332,10 @@ def main():
             "phase_ms": {k: statistics.mean(p[k] for p in phases) for k in phases[0]},
             "roofline": {"bound": "fp32", "kernel": "train_kernel", "achieved": achieved,
                          "peak": peak_fp32, "unit": "TFLOP/s", "frac": achieved / peak_fp32,
-                         "peak_source": "measured in this run (noma_measure_fp32_tflops FFMA probe)",
+                         "peak_source": "measured in this run: constant-operand FFMA probe (issue-rate peak)",
+                         "register_tile_ceiling": peak_tile,
+                         "frac_of_register_tile_ceiling": achieved / peak_tile,
+                         "register_tile_ceiling_source": "measured in this run: 8x4 register outer-product FFMA probe (3-register FFMA is RF-read limited on B200)",
                          "traffic": traffic,
                          "algorithmic_flop_per_launch": nets * tr_flops},
             "cpu_baseline": cpu,

@@ -119,10 +119,14 @@ NOMA_API long long noma_ctx_kernel_launches(noma_ctx_t ctx);
  * and returns its phase times in ms: [lls, init, shuffle, train, detect]. */
 NOMA_API int noma_ctx_set_profiling(noma_ctx_t ctx, int on);
 NOMA_API int noma_ctx_phase_ms(noma_ctx_t ctx, double *ms5);
-/* FP32 FFMA throughput of this device (TFLOP/s), measured by a dependent-
- * chain-free FFMA kernel over every SM: the roofline denominator of the
- * FP32-bound training and detection kernels. */
-NOMA_API int noma_measure_fp32_tflops(noma_ctx_t ctx, double *tflops);
+/* FP32 FFMA throughput of this device (TFLOP/s) over every SM, the roofline
+ * denominators of the FP32-bound training and detection kernels.
+ * form 0: FFMA with constant operands (the issue-rate peak);
+ * form 1: an 8x4 register outer product, all operands in registers (the
+ *         ceiling of any register-tiled FP32 GEMM inner loop on this part --
+ *         3-register FFMA is register-file-read limited, profiles/
+ *         r01_microbench_ffma_forms.txt). */
+NOMA_API int noma_measure_fp32_tflops(noma_ctx_t ctx, int form, double *tflops);
 
 /* Floats in the FusedPlan buffer for `desc` (fused_inference.cpp:19-42). */
 NOMA_API int noma_plan_size(const noma_net_desc *desc);

@@ -58,6 +58,35 @@ __global__ void prep_kernel(int layout, int S, int K, int rows, int width, const
 using namespace noma_dev;
 
 namespace noma_dev {
+// Register-tile probe: the 8x4 outer product of the GEMM tiles, operands in
+// registers, no memory traffic (4 * 32 FMAs per iteration).
+__global__ void ffma_outer_kernel(float *out, int iters) {
+    float acc[8][4], w[8], v[4];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        w[i] = 1e-3f * (threadIdx.x + i);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) acc[i][q] = 0.f;
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) v[q] = 0.5f + 1e-4f * (threadIdx.x + q);
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+            for (int i = 0; i < 8; ++i)
+#pragma unroll
+                for (int q = 0; q < 4; ++q) acc[i][q] = fmaf(w[i], v[q], acc[i][q]);
+        w[it & 7] += 1e-7f;
+    }
+    float s = 0.f;
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) s += acc[i][q];
+    if (s == 12345.678f) out[0] = s;
+}
+
 // FFMA peak probe: 8 independent FMA chains per thread, no memory traffic.
 __global__ void ffma_peak_kernel(float *out, int iters, float a, float b) {
     float x[8];
@@ -303,8 +332,8 @@ NOMA_API int noma_ctx_phase_ms(noma_ctx_t c, double *ms5) {
     return NOMA_OK;
 }
 
-NOMA_API int noma_measure_fp32_tflops(noma_ctx_t c, double *tflops) {
-    if (!c || !tflops) return NOMA_ERR_ARGUMENT;
+NOMA_API int noma_measure_fp32_tflops(noma_ctx_t c, int form, double *tflops) {
+    if (!c || !tflops || form < 0 || form > 1) return NOMA_ERR_ARGUMENT;
     int sms = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device);
     float *out = nullptr;
@@ -316,12 +345,16 @@ NOMA_API int noma_measure_fp32_tflops(noma_ctx_t c, double *tflops) {
     double best = 0.0;
     for (int rep = 0; rep < 4; ++rep) {
         cudaEventRecord(a, c->stream);
-        ffma_peak_kernel<<<blocks, threads, 0, c->stream>>>(out, iters, 0.9999f, 1e-4f);
+        if (form == 0)
+            ffma_peak_kernel<<<blocks, threads, 0, c->stream>>>(out, iters, 0.9999f, 1e-4f);
+        else
+            ffma_outer_kernel<<<blocks, threads, 0, c->stream>>>(out, iters);
         cudaEventRecord(b, c->stream);
         cudaEventSynchronize(b);
         float ms = 0.f;
         cudaEventElapsedTime(&ms, a, b);
-        const double flops = 2.0 * 16 * 8 * (double)iters * blocks * threads;
+        const double fma_per_thread = form == 0 ? 16.0 * 8 * iters : 4.0 * 32 * iters;
+        const double flops = 2.0 * fma_per_thread * blocks * threads;
         if (rep > 0) best = std::max(best, flops / (ms * 1e-3) / 1e12);
     }
     cudaEventDestroy(a);

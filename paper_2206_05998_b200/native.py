@@ -124,7 +124,7 @@ def load():
     L.noma_synthesize.argtypes = [vp, C.POINTER(Scenario), ip, vp, vp, vp, vp, vp, vp, vp, ip]
     L.noma_ctx_set_profiling.argtypes = [vp, ip]
     L.noma_ctx_phase_ms.argtypes = [vp, C.POINTER(C.c_double)]
-    L.noma_measure_fp32_tflops.argtypes = [vp, C.POINTER(C.c_double)]
+    L.noma_measure_fp32_tflops.argtypes = [vp, ip, C.POINTER(C.c_double)]
     _lib = L
     return L
 
@@ -210,9 +210,10 @@ class Context:
         self._check(self.L.noma_ctx_phase_ms(self.h, out))
         return dict(zip(PHASES, list(out)))
 
-    def measure_fp32_tflops(self) -> float:
+    def measure_fp32_tflops(self, form: int = 0) -> float:
+        """form 0: constant-operand FFMA peak; 1: 8x4 register outer product."""
         v = C.c_double(0)
-        self._check(self.L.noma_measure_fp32_tflops(self.h, C.byref(v)))
+        self._check(self.L.noma_measure_fp32_tflops(self.h, form, C.byref(v)))
         return v.value
 
     def last_error(self) -> str:
