@@ -149,6 +149,23 @@ NOMA_API int noma_lls_fit(noma_ctx_t ctx, const noma_dataset *ds, double *w0,
 NOMA_API int noma_init_params(noma_ctx_t ctx, const noma_net_desc *desc, int n_nets,
                               const uint64_t *seeds, const double *w0, float *plans, int mem);
 
+/* init_params with the caller's Rng (hybrid_nn.hpp:55: `Rng& rng` is advanced):
+ * states [net][4] hold xoshiro256++ states (rng.hpp:28-45) on entry and the
+ * advanced states on return.  Outputs (nullable): plans [net][plan] f32, and
+ * theta [net][trainable] f64 in the reference parameter order W_1, b_1, ...,
+ * W_N, b_N, final (HybridNetParams, hybrid_nn.hpp:15-23). */
+NOMA_API int noma_init_params_state(noma_ctx_t ctx, const noma_net_desc *desc, int n_nets,
+                                    uint64_t *states, const double *w0, float *plans,
+                                    double *theta, int mem);
+
+/* Replaces lls::predict (lls.hpp:24, lls.cpp:62-66) for every net: FP64
+ * yhat = X w0.  WIDEN_COMPLEX: data [n_designs][rows][width/2] c64, out
+ * [net][rows] c64 (narrow(X_widened w0)); REAL: data [n_designs][rows][width]
+ * f64, out [net][rows] f64. */
+NOMA_API int noma_lls_predict(noma_ctx_t ctx, int layout, int n_designs, int nets_per_design,
+                              int rows, int width, const double *data, const double *w0,
+                              double *out, int mem);
+
 /* Replaces hybrid_nn::train (hybrid_nn.hpp:70-72, hybrid_nn.cpp:158-195)
  * for every net of `ds`: one fused kernel per net runs all epochs x
  * minibatches (forward, backward, Adam) with the weights resident on chip.

@@ -86,6 +86,19 @@ def lls_fit_slots(pilot_rx: np.ndarray, pilot_sym: np.ndarray):
     return w0, cond, status
 
 
+def lls_predict(w: np.ndarray, widened_design: np.ndarray) -> np.ndarray:
+    """lls::predict (lls.cpp:62-66): narrow(X w) in FP64 on device."""
+    x = np.ascontiguousarray(widened_design, dtype=np.float64)
+    w = np.ascontiguousarray(w, dtype=np.float64)
+    if x.shape[1] != w.size:
+        raise N.DimensionError(N.ERR_DIMENSION, "lls::predict: column count does not match weights")
+    if x.shape[0] % 2:
+        raise N.DimensionError(N.ERR_DIMENSION, "narrow_predictions: length must be even")
+    out = np.zeros(x.shape[0])
+    context().lls_predict(N.LAYOUT_REAL, 1, 1, x.shape[0], x.shape[1], x, w.reshape(1, -1), out)
+    return out[0::2] + 1j * out[1::2]
+
+
 # ------------------------------------------------------------ hybrid_nn
 def plan_layout(dims):
     """Offsets of the FusedPlan buffer (fused_inference.cpp:19-42)."""
@@ -131,6 +144,18 @@ def init_params(dims, w0: np.ndarray, seed: int) -> HybridNet:
     plans = np.zeros((1, N.plan_size(dims)), dtype=np.float32)
     context().init_params(dims, np.array([seed], dtype=np.uint64), w0.reshape(1, -1), plans)
     return HybridNet(dims, plans[0], w0.copy())
+
+
+def init_params_state(dims, w0: np.ndarray, state):
+    """init_params(dims, w0, Rng&) with an explicit xoshiro256++ state
+    (4 x u64): returns (HybridNet, flat FP64 theta, advanced state)."""
+    dims = [int(d) for d in dims]
+    w0 = np.ascontiguousarray(w0, dtype=np.float64)
+    st = np.array([list(state)], dtype=np.uint64)
+    plans = np.zeros((1, N.plan_size(dims)), dtype=np.float32)
+    theta = np.zeros((1, N.param_count(dims)))
+    context().init_params_state(dims, st, w0.reshape(1, -1), plans, theta)
+    return HybridNet(dims, plans[0], w0.copy()), theta[0], tuple(int(v) for v in st[0])
 
 
 def net_from_params(dims, w0, layers, final) -> HybridNet:

@@ -426,6 +426,51 @@ NOMA_API int noma_init_params(noma_ctx_t c, const noma_net_desc *desc, int n_net
     return s.finish();
 }
 
+NOMA_API int noma_init_params_state(noma_ctx_t c, const noma_net_desc *desc, int n_nets,
+                                    uint64_t *states, const double *w0, float *plans,
+                                    double *theta, int mem) {
+    if (!c) return NOMA_ERR_ARGUMENT;
+    NetGeom g;
+    if (!make_geom(desc, &g)) return fail(c, NOMA_ERR_DIMENSION, "init_params: bad dims");
+    if (!states) return fail(c, NOMA_ERR_ARGUMENT, "null states");
+    if (n_nets <= 0) return NOMA_OK;
+    const int ptrain = trainable_count(g);
+    Stage s(c, mem);
+    uint64_t *ds = s.inout(states, (size_t)n_nets * 4);
+    const double *dw = s.in(w0, (size_t)n_nets * g.dims[0]);
+    float *dp = s.out(plans, (size_t)n_nets * g.plan_total);
+    double *dt = s.out(theta, (size_t)n_nets * ptrain);
+    if (!s.ok) return s.finish();
+    if (init_state_launch(g, n_nets, ds, dw, dp, dt, ptrain, c->stream)) return cuda_fail(c, "init");
+    c->launches += 1;
+    return s.finish();
+}
+
+NOMA_API int noma_lls_predict(noma_ctx_t c, int layout, int n_designs, int nets_per_design,
+                              int rows, int width, const double *data, const double *w0,
+                              double *out, int mem) {
+    if (!c) return NOMA_ERR_ARGUMENT;
+    if (!data || !w0 || !out) return fail(c, NOMA_ERR_ARGUMENT, "null argument");
+    if (layout != NOMA_LAYOUT_WIDEN_COMPLEX && layout != NOMA_LAYOUT_REAL)
+        return fail(c, NOMA_ERR_ARGUMENT, "bad layout");
+    if (width < 1 || rows < 0 || n_designs < 0 || nets_per_design < 1 ||
+        (layout == NOMA_LAYOUT_WIDEN_COMPLEX && (width & 1)))
+        return fail(c, NOMA_ERR_DIMENSION, "lls::predict: column count does not match weights");
+    const size_t nets = (size_t)n_designs * nets_per_design;
+    if (nets == 0 || rows == 0) return NOMA_OK;
+    const size_t de = (size_t)n_designs * rows * width;  // doubles (complex: rows*(w/2)*2)
+    const size_t oe = nets * rows * (layout == NOMA_LAYOUT_WIDEN_COMPLEX ? 2 : 1);
+    Stage s(c, mem);
+    const double *dd = s.in(data, de);
+    const double *dw = s.in(w0, nets * width);
+    double *dout = s.out(out, oe);
+    if (!s.ok) return s.finish();
+    if (lls_predict_launch(layout, n_designs, nets_per_design, rows, width, dd, dw, dout, c->stream))
+        return cuda_fail(c, "lls predict");
+    c->launches += 1;
+    return s.finish();
+}
+
 NOMA_API int noma_train(noma_ctx_t c, const noma_dataset *ds, const noma_net_desc *desc,
                         const noma_train_cfg *cfg, const double *w0, float *plans_inout,
                         const uint64_t *shuffle_seeds, double *trace, int *status, int mem) {

@@ -34,6 +34,8 @@ __host__ __device__ inline uint64_t substream_seed(uint64_t master, uint64_t tag
 
 struct Xoshiro {
     uint64_t s0, s1, s2, s3;
+    __host__ __device__ Xoshiro(uint64_t a, uint64_t b, uint64_t c, uint64_t d)
+        : s0(a), s1(b), s2(c), s3(d) {}
     __host__ __device__ explicit Xoshiro(uint64_t seed) {
         uint64_t sm = seed;
         s0 = splitmix64(sm);

@@ -360,6 +360,45 @@ __global__ void __launch_bounds__(kThreads) lls_kernel(LlsParams p) {
     }
 }
 
+// lls::predict (lls.cpp:62-66): yhat = narrow(X_widened w0), FP64, one thread
+// per (net, row).  WIDEN: the widened rows 2t / 2t+1 of complex row t give
+// Re / Im of the prediction directly.
+__global__ void lls_predict_kernel(int layout, int S, int K, int rows, int width,
+                                   const double *data, const double *w0, double *out) {
+    const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= (size_t)S * K * rows) return;
+    const int t = (int)(i % rows);
+    const size_t net = i / rows;
+    const int d = (int)(net / K);
+    const double *w = w0 + net * width;
+    if (layout == NOMA_LAYOUT_WIDEN_COMPLEX) {
+        const int m = width / 2;
+        const double *x = data + ((size_t)d * rows + t) * m * 2;
+        double pe = 0.0, po = 0.0;
+        for (int a = 0; a < m; ++a) {
+            const double xr = x[2 * a], xi = x[2 * a + 1];
+            pe += xr * w[a] + xi * w[m + a];
+            po += xi * w[a] - xr * w[m + a];
+        }
+        out[2 * i] = pe;
+        out[2 * i + 1] = po;
+    } else {
+        const double *x = data + ((size_t)d * rows + t) * width;
+        double s = 0.0;
+        for (int c = 0; c < width; ++c) s += x[c] * w[c];
+        out[i] = s;
+    }
+}
+
+int lls_predict_launch(int layout, int S, int K, int rows, int width, const double *data,
+                       const double *w0, double *out, cudaStream_t st) {
+    const size_t n = (size_t)S * K * rows;
+    if (n == 0) return NOMA_OK;
+    lls_predict_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(layout, S, K, rows, width,
+                                                                     data, w0, out);
+    return cudaGetLastError() == cudaSuccess ? NOMA_OK : NOMA_ERR_CUDA;
+}
+
 size_t lls_smem_bytes(int m, int K) {
     size_t chunk = 2 * kLlsChunk * m + 2 * kLlsChunk * K;
     if (chunk < (size_t)(2 * m * K)) chunk = 2 * m * K;  // U aliases the chunk buffers

@@ -70,6 +70,52 @@ __global__ void init_kernel(NetGeom g, int n_nets, const uint64_t *seeds, const 
     }
 }
 
+// Same draws from caller-provided xoshiro states (init_params(dims, w0, Rng&)):
+// states are advanced in place; FP64 weights optionally written in the
+// reference parameter order (W_1, b_1, ..., W_N, b_N, final).
+__global__ void init_state_kernel(NetGeom g, int n_nets, uint64_t *states, const double *w0,
+                                  float *plans, double *theta, int ptrain) {
+    const int net = blockIdx.x * blockDim.x + threadIdx.x;
+    if (net >= n_nets) return;
+    uint64_t *st = states + (size_t)net * 4;
+    Xoshiro r(st[0], st[1], st[2], st[3]);
+    float *pl = plans ? plans + (size_t)net * g.plan_total : nullptr;
+    double *th = theta ? theta + (size_t)net * ptrain : nullptr;
+    if (pl) {
+        for (int i = 0; i < g.plan_total; ++i) pl[i] = 0.0f;
+        if (w0)
+            for (int c = 0; c < g.dims[0]; ++c) pl[c] = (float)w0[(size_t)net * g.dims[0] + c];
+    }
+    int off = 0;
+    for (int l = 1; l < g.nd; ++l) {
+        const int fan_in = g.dims[l - 1];
+        const double scale = sqrt(2.0 / fan_in);
+        for (int row = 0; row < g.dims[l]; ++row)
+            for (int c = 0; c < fan_in; ++c) {
+                const double v = r.gaussian() * scale;
+                if (pl) pl[g.plan_w[l] + row * g.plan_pad[l - 1] + c] = (float)v;
+                if (th) th[off] = v;
+                ++off;
+            }
+        if (th)
+            for (int j = 0; j < g.dims[l]; ++j) th[off + j] = 0.0;
+        off += g.dims[l];
+    }
+    if (th)
+        for (int j = 0; j < g.dims[g.nd - 1]; ++j) th[off + j] = 0.0;
+    st[0] = r.s0;
+    st[1] = r.s1;
+    st[2] = r.s2;
+    st[3] = r.s3;
+}
+
+int init_state_launch(const NetGeom &g, int n_nets, uint64_t *states, const double *w0,
+                      float *plans, double *theta, int ptrain, cudaStream_t st) {
+    if (n_nets == 0) return NOMA_OK;
+    init_state_kernel<<<(n_nets + 63) / 64, 64, 0, st>>>(g, n_nets, states, w0, plans, theta, ptrain);
+    return cudaGetLastError() == cudaSuccess ? NOMA_OK : NOMA_ERR_CUDA;
+}
+
 int init_launch(const NetGeom &g, int n_nets, const uint64_t *seeds, const double *w0,
                 float *plans, cudaStream_t st) {
     if (n_nets == 0) return NOMA_OK;

@@ -72,6 +72,10 @@ int init_launch(const NetGeom &g, int n_nets, const uint64_t *seeds, const doubl
                 float *plans, cudaStream_t st);
 int set_w0_launch(int n_nets, int d0, int plan_total, const double *w0, float *plans,
                   cudaStream_t st);
+int init_state_launch(const NetGeom &g, int n_nets, uint64_t *states, const double *w0,
+                      float *plans, double *theta, int ptrain, cudaStream_t st);
+int lls_predict_launch(int layout, int S, int K, int rows, int width, const double *data,
+                       const double *w0, double *out, cudaStream_t st);
 int train_launch(TrainParams &p, cudaStream_t st);
 int detect_launch(DetectParams &p, cudaStream_t st);
 int synth_launch(SynthParams p, double *noise_power_scratch, cudaStream_t st);

@@ -25,7 +25,8 @@ EXPORTED = [
     "noma_ctx_set_stream", "noma_ctx_synchronize", "noma_ctx_kernel_launches",
     "noma_plan_size", "noma_param_count", "noma_lls_fit", "noma_init_params", "noma_train",
     "noma_detect", "noma_pipeline", "noma_synthesize", "noma_ctx_set_profiling",
-    "noma_ctx_phase_ms", "noma_measure_fp32_tflops",
+    "noma_ctx_phase_ms", "noma_measure_fp32_tflops", "noma_init_params_state",
+    "noma_lls_predict",
 ]
 PHASES = ("lls", "init", "shuffle", "train", "detect")
 
@@ -125,6 +126,8 @@ def load():
     L.noma_ctx_set_profiling.argtypes = [vp, ip]
     L.noma_ctx_phase_ms.argtypes = [vp, C.POINTER(C.c_double)]
     L.noma_measure_fp32_tflops.argtypes = [vp, ip, C.POINTER(C.c_double)]
+    L.noma_init_params_state.argtypes = [vp, C.POINTER(NetDesc), ip, vp, vp, vp, vp, ip]
+    L.noma_lls_predict.argtypes = [vp, ip, ip, ip, ip, ip, vp, vp, vp, ip]
     _lib = L
     return L
 
@@ -244,6 +247,18 @@ class Context:
         n = seeds.shape[0]
         self._check(self.L.noma_init_params(self.h, C.byref(d), n, _ptr(seeds), _ptr(w0),
                                             _ptr(plans), mem))
+
+    def init_params_state(self, dims, states, w0, plans=None, theta=None):
+        mem = _mem_of(states, w0, plans, theta)
+        d = NetDesc.of(dims)
+        self._check(self.L.noma_init_params_state(self.h, C.byref(d), states.shape[0],
+                                                  _ptr(states), _ptr(w0), _ptr(plans),
+                                                  _ptr(theta), mem))
+
+    def lls_predict(self, layout, n_designs, K, rows, width, data, w0, out):
+        mem = _mem_of(data, w0, out)
+        self._check(self.L.noma_lls_predict(self.h, layout, n_designs, K, rows, width,
+                                            _ptr(data), _ptr(w0), _ptr(out), mem))
 
     def train(self, layout, n_designs, K, rows, width, design, targets, dims, cfg: TrainCfg, w0,
               plans, shuffle_seeds, trace=None, status=None):

@@ -245,3 +245,30 @@ def test_fp32_training_tracks_fp64_reference(A, O, M, K, k, hidden, snr, epochs)
         p = max(ref_err, 1) / (2 * len(ref))
         assert flips <= 0.02 * len(ref), flips
         assert abs(errs - ref_err) <= 3 * np.sqrt(2 * len(ref) * p * (1 - p)) + 1
+
+
+def test_init_params_state_advances_the_callers_rng(A, O):
+    """init_params(dims, w0, Rng&) (hybrid_nn.hpp:55): FP64 weights equal the
+    oracle's draws and the caller's stream is advanced identically."""
+    dims = [8, 16, 4]
+    w0 = make_w0(8, 3)
+    r = O.Rng(44)
+    onet = O.init_params(dims, w0, r)
+    net, theta, state = A.init_params_state(dims, w0, O.Rng(44).state())
+    assert state == r.state()
+    assert np.max(np.abs(theta - onet.theta)) <= 4e-16 * np.max(np.abs(onet.theta))
+
+
+def test_lls_predict_fp64(A, O):
+    rec = O.synthesize(O.Scenario(train_symbols=64, data_symbols=300, snr_db=20.0, seed=31))
+    xt = O.widen_design(rec.train_rx)
+    w = O.lls_fit(xt, O.widen_targets(rec.train_symbols[:, 2])).w
+    xd = O.widen_design(rec.data_rx)
+    got = A.lls_predict(w, xd)
+    ref = O.narrow_predictions(xd @ w)
+    assert np.max(np.abs(got - ref)) <= 1e-13 * np.max(np.abs(ref))
+    # coordinate selector / zero weights (test_lls.cpp:58-73)
+    x = np.array([[1 + 2j, 3 + 4j], [-1 + 0.5j, 0 + 1j], [2 - 2j, 1 + 1j]])
+    sel = np.array([1.0, 0, 0, 0])
+    assert np.array_equal(A.lls_predict(sel, O.widen_design(x)), x[:, 0])
+    assert np.array_equal(A.lls_predict(np.zeros(4), O.widen_design(x)), np.zeros(3, complex))
