@@ -173,6 +173,7 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
     from paper_2206_05998_b200 import native as N
+    from paper_2206_05998_b200 import shard
     from paper_2206_05998_b200.seeds import slot_user_seeds
 
     M, K, S = cfg["M"], cfg["K"], cfg["slots"]
@@ -184,7 +185,7 @@ def main():
     dev = torch.device("cuda", local)
 
     # ---- synthetic inputs, generated on device (not timed) ----------------
-    seeds = np.arange(1000 + rank * S, 1000 + (rank + 1) * S, dtype=np.uint64)
+    seeds = shard.slot_seeds(world * S, world, rank)  # this rank's slots, no overlap
     seeds_d = torch.from_numpy(seeds.astype(np.int64)).to(dev)
     px = torch.empty((S, NT, M, 2), dtype=torch.float64, device=dev)
     py = torch.empty((S, NT, K, 2), dtype=torch.float64, device=dev)
@@ -239,11 +240,7 @@ def main():
     launches = ctx.kernel_launches - launches0
     ctx.set_profiling(False)
     step_ms = [a.elapsed_time(b) for a, b in ev]
-    total_ms = sum(step_ms)
-    t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    total_ms = float(t.item())
+    total_ms = shard.max_over_ranks(sum(step_ms), dev)  # the slowest rank
     sym_per_step = S * K * ND * world
     value = sym_per_step * args.steps / (total_ms * 1e-3)
 
@@ -286,11 +283,9 @@ def main():
         b.record(stream)
         b.synchronize()
         e2e_ms.append(a.elapsed_time(b))
-    et = torch.tensor([statistics.mean(e2e_ms)], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(et, op=dist.ReduceOp.MAX)
-    e2e_value = sym_per_step / (float(et.item()) * 1e-3)
-    bit_err_total = int(h_errs.astype(np.int64).sum())
+    e2e_value = sym_per_step / (shard.max_over_ranks(statistics.mean(e2e_ms), dev) * 1e-3)
+    all_errs = shard.gather_to_rank0(h_errs.astype(np.int64))  # per-slot BER counters
+    bit_err_total = int(all_errs.sum()) if all_errs is not None else None
 
     # ---- single-slot latency (C-config, S=1) -------------------------------
     lat = []
