@@ -68,7 +68,7 @@ __global__ void __launch_bounds__(kTrainThreads, MINB) train_kernel(TrainParams 
     }
     for (int j = tid; j < g.dims[N]; j += kTrainThreads) PS[g.pf + j] = pl[g.plan_f + j];
 
-    float mom1[NSLOT], mom2[NSLOT];
+    float mom1[NSLOT > 0 ? NSLOT : 1], mom2[NSLOT > 0 ? NSLOT : 1];
 #pragma unroll
     for (int s = 0; s < NSLOT; ++s) mom1[s] = mom2[s] = 0.0f;
     __syncthreads();
@@ -190,18 +190,30 @@ __global__ void __launch_bounds__(kTrainThreads, MINB) train_kernel(TrainParams 
                     __syncthreads();
                 }
             }
-            // ---- Adam (hybrid_nn.cpp:118-144): FP32 moments in registers ----
+            // ---- Adam (hybrid_nn.cpp:118-144): FP32 moments, registers or smem
             {
                 const float lrc = misc[0], ic2 = misc[1];
+                if constexpr (NSLOT > 0) {
 #pragma unroll
-                for (int s = 0; s < NSLOT; ++s) {
-                    const int i = tid + s * kTrainThreads;
-                    if (i < g.ptotal) {
-                        // fixed-order sum of the split-K partials
+                    for (int s = 0; s < NSLOT; ++s) {
+                        const int i = tid + s * kTrainThreads;
+                        if (i < g.ptotal) {
+                            // fixed-order sum of the split-K partials
+                            const float gi = p.gsplit > 1 ? GS[i] + GS[gstride + i] : GS[i];
+                            mom1[s] = p.b1 * mom1[s] + p.omb1 * gi;
+                            mom2[s] = p.b2 * mom2[s] + p.omb2 * (gi * gi);
+                            PS[i] -= __fdividef(lrc * mom1[s], sqrtf(mom2[s] * ic2) + p.eps);
+                        }
+                    }
+                } else {
+                    float *M1 = sm + p.off_mom, *M2 = M1 + gstride;
+                    for (int i = tid; i < g.ptotal; i += kTrainThreads) {
                         const float gi = p.gsplit > 1 ? GS[i] + GS[gstride + i] : GS[i];
-                        mom1[s] = p.b1 * mom1[s] + p.omb1 * gi;
-                        mom2[s] = p.b2 * mom2[s] + p.omb2 * (gi * gi);
-                        PS[i] -= __fdividef(lrc * mom1[s], sqrtf(mom2[s] * ic2) + p.eps);
+                        const float m1 = p.b1 * M1[i] + p.omb1 * gi;
+                        const float m2 = p.b2 * M2[i] + p.omb2 * (gi * gi);
+                        M1[i] = m1;
+                        M2[i] = m2;
+                        PS[i] -= __fdividef(lrc * m1, sqrtf(m2 * ic2) + p.eps);
                     }
                 }
             }
@@ -248,10 +260,23 @@ int train_launch(TrainParams &p, cudaStream_t st) {
     off += pad_to(g.ptotal, 4);
     p.gs_stride = pad_to(g.ptotal, 4);
     p.off_gs = off;
-    // two split-K gradient partials when they fit, else one
+    // Prefer (a) two split-K gradient partials and (b) Adam moments in shared
+    // memory (frees ~2*ptotal/256 registers per thread for the FFMA2 tiles'
+    // scheduling); drop (b) then (a) until the carve-up fits 227 KB.
     const int base_rest = off + kBatchRows * 3 + (g.fp[g.nd - 1] / 32) * kBatchRows + 8;
-    p.gsplit = (size_t)(base_rest + kMaxSplit * p.gs_stride) * sizeof(float) <= 227 * 1024 ? kMaxSplit : 1;
+    auto fits = [&](int splits, int mom) {
+        return (size_t)(base_rest + (splits + 2 * mom) * p.gs_stride) * sizeof(float) <= 227 * 1024;
+    };
+    int mom_smem = 1;
+    p.gsplit = kMaxSplit;
+    if (!fits(p.gsplit, mom_smem)) p.gsplit = 1;
+    if (!fits(p.gsplit, mom_smem)) {
+        mom_smem = 0;
+        p.gsplit = fits(kMaxSplit, 0) ? kMaxSplit : 1;
+    }
     off += p.gsplit * p.gs_stride;
+    p.off_mom = off;
+    off += 2 * mom_smem * p.gs_stride;
     p.off_r0b = off;
     off += kBatchRows;
     p.off_dy = off;
@@ -275,11 +300,16 @@ int train_launch(TrainParams &p, cudaStream_t st) {
         train_kernel<NS, MB><<<p.n_nets, kTrainThreads, smem, st>>>(p);                         \
         return cudaGetLastError() == cudaSuccess ? NOMA_OK : NOMA_ERR_CUDA;                     \
     }
+    if (mom_smem) {
+        if (smem <= 112 * 1024) NOMA_TRAIN_LAUNCH(0, 2)
+        NOMA_TRAIN_LAUNCH(0, 1)
+    }
     if (two && need <= 8) NOMA_TRAIN_LAUNCH(8, 2)
     if (two) NOMA_TRAIN_LAUNCH(16, 2)
     if (need <= 8) NOMA_TRAIN_LAUNCH(8, 1)
     if (need <= 16) NOMA_TRAIN_LAUNCH(16, 1)
     if (need <= 24) NOMA_TRAIN_LAUNCH(24, 1)
+    if (need <= 28) NOMA_TRAIN_LAUNCH(28, 1)
     if (need <= 32) NOMA_TRAIN_LAUNCH(32, 1)
     if (need <= 48) NOMA_TRAIN_LAUNCH(48, 1)
     if (need <= 64) NOMA_TRAIN_LAUNCH(64, 1)

@@ -31,7 +31,7 @@ struct TrainParams {
     double lr_d, b1d, b2d;
     // shared-memory carve-up (floats)
     int off_x, off_a[NOMA_MAX_DIMS], off_ps, off_gs, off_r0b, off_dy, off_red, off_yp, off_misc,
-        off_end, gs_stride, gsplit;
+        off_end, gs_stride, gsplit, off_mom;
 };
 
 struct DetectParams {

@@ -44,9 +44,12 @@ __device__ __forceinline__ float2 f2_unpack(f2_t v) {
     asm("mov.b64 {%0, %1}, %2;" : "=f"(r.x), "=f"(r.y) : "l"(v));
     return r;
 }
-// d = a * b + d, lane-wise, IEEE rn
+// d = a * b + d, lane-wise, IEEE rn.  `volatile` pins the source order of the
+// FMAs (ptxas otherwise interleaves updates of the same accumulator a few
+// instructions apart and stalls on the FFMA2 latency): every tile below is
+// written accumulator-major so consecutive FMAs are independent.
 __device__ __forceinline__ void f2_fma(f2_t &d, f2_t a, f2_t b) {
-    asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(d) : "l"(a), "l"(b));
+    asm volatile("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(d) : "l"(a), "l"(b));
 }
 
 template <int KK>
@@ -206,16 +209,16 @@ __device__ __forceinline__ void tile_weight_grad(const float *__restrict__ dz,
 #pragma unroll
                 for (int i = 0; i < 4; ++i)
 #pragma unroll
-                    for (int q = 0; q < 4; ++q) {
-                        f2_fma(acc[ih + i][q], z[i].x, x[q].x);
-                        f2_fma(acc[ih + i][q], z[i].y, x[q].y);
-                    }
+                    for (int q = 0; q < 4; ++q) f2_fma(acc[ih + i][q], z[i].x, x[q].x);
+#pragma unroll
+                for (int i = 0; i < 4; ++i)
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) f2_fma(acc[ih + i][q], z[i].y, x[q].y);
                 if (cb == 0) {  // warp-uniform: bias gradient from the same loads
 #pragma unroll
-                    for (int i = 0; i < 4; ++i) {
-                        f2_fma(sb[ih + i], z[i].x, one);
-                        f2_fma(sb[ih + i], z[i].y, one);
-                    }
+                    for (int i = 0; i < 4; ++i) f2_fma(sb[ih + i], z[i].x, one);
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) f2_fma(sb[ih + i], z[i].y, one);
                 }
             }
         }
