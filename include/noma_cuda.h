@@ -114,11 +114,12 @@ NOMA_API int noma_ctx_set_stream(noma_ctx_t ctx, void *cuda_stream);
 NOMA_API int noma_ctx_synchronize(noma_ctx_t ctx);
 /* Number of kernels this context has launched (instrumentation). */
 NOMA_API long long noma_ctx_kernel_launches(noma_ctx_t ctx);
-/* Instrumentation: when on, noma_pipeline records CUDA events between its
- * phases on the context stream; noma_ctx_phase_ms waits for the last call
- * and returns its phase times in ms: [lls, init, shuffle, train, detect]. */
+/* Instrumentation: when on, noma_pipeline records CUDA events around its
+ * phases (init and shuffles run on a side stream, overlapping the LLS);
+ * noma_ctx_phase_ms waits for the last call and returns ms for
+ * [lls, init, shuffle, train, detect, whole pipeline]. */
 NOMA_API int noma_ctx_set_profiling(noma_ctx_t ctx, int on);
-NOMA_API int noma_ctx_phase_ms(noma_ctx_t ctx, double *ms5);
+NOMA_API int noma_ctx_phase_ms(noma_ctx_t ctx, double *ms6);
 /* FP32 FFMA throughput of this device (TFLOP/s) over every SM, the roofline
  * denominators of the FP32-bound training and detection kernels.
  * form 0: FFMA with constant operands (the issue-rate peak);

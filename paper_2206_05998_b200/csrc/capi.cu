@@ -112,12 +112,16 @@ struct noma_ctx_s {
     std::string err;
     long long launches = 0;
     bool profiling = false;
-    cudaEvent_t ev[6] = {};
+    // [0] start, [1] after LLS, [2] side start, [3] after init, [4] after
+    // shuffles (side stream), [5] joined, [6] after train, [7] after detect
+    cudaEvent_t ev[8] = {};
+    cudaStream_t side = nullptr;          // init + shuffles overlap the LLS
+    cudaEvent_t fork = nullptr, join = nullptr;
 };
 
 namespace {
-inline void mark(noma_ctx_s *c, int i) {
-    if (c->profiling) cudaEventRecord(c->ev[i], c->stream);
+inline void mark(noma_ctx_s *c, int i, cudaStream_t s = nullptr) {
+    if (c->profiling) cudaEventRecord(c->ev[i], s ? s : c->stream);
 }
 }  // namespace
 
@@ -277,6 +281,12 @@ NOMA_API int noma_ctx_create(int device, noma_ctx_t *out) {
         return NOMA_ERR_CUDA;
     }
     c->stream = c->own;
+    if (cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&c->fork, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&c->join, cudaEventDisableTiming) != cudaSuccess) {
+        delete c;
+        return NOMA_ERR_CUDA;
+    }
     // Keep freed stream-ordered scratch in the pool: the default release
     // threshold (0) hands it back to the OS at every synchronisation, which
     // would put page-mapping latency inside every call.
@@ -292,6 +302,11 @@ NOMA_API int noma_ctx_create(int device, noma_ctx_t *out) {
 NOMA_API int noma_ctx_destroy(noma_ctx_t c) {
     if (!c) return NOMA_OK;
     cudaStreamSynchronize(c->stream);
+    if (c->side) cudaStreamSynchronize(c->side), cudaStreamDestroy(c->side);
+    if (c->fork) cudaEventDestroy(c->fork);
+    if (c->join) cudaEventDestroy(c->join);
+    for (auto &e : c->ev)
+        if (e) cudaEventDestroy(e);
     if (c->own) cudaStreamDestroy(c->own);
     delete c;
     return NOMA_OK;
@@ -321,14 +336,20 @@ NOMA_API int noma_ctx_set_profiling(noma_ctx_t c, int on) {
     return NOMA_OK;
 }
 
-NOMA_API int noma_ctx_phase_ms(noma_ctx_t c, double *ms5) {
-    if (!c || !ms5 || !c->ev[0]) return NOMA_ERR_ARGUMENT;
-    if (cudaEventSynchronize(c->ev[5]) != cudaSuccess) return cuda_fail(c, "event sync");
-    for (int i = 0; i < 5; ++i) {
+NOMA_API int noma_ctx_phase_ms(noma_ctx_t c, double *ms6) {
+    if (!c || !ms6 || !c->ev[0]) return NOMA_ERR_ARGUMENT;
+    if (cudaEventSynchronize(c->ev[7]) != cudaSuccess) return cuda_fail(c, "event sync");
+    auto el = [&](int a, int b) {
         float ms = 0.f;
-        cudaEventElapsedTime(&ms, c->ev[i], c->ev[i + 1]);
-        ms5[i] = ms;
-    }
+        cudaEventElapsedTime(&ms, c->ev[a], c->ev[b]);
+        return (double)ms;
+    };
+    ms6[0] = el(0, 1);  // lls
+    ms6[1] = el(2, 3);  // init   (side stream, overlaps lls)
+    ms6[2] = el(3, 4);  // shuffle (side stream)
+    ms6[3] = el(5, 6);  // train
+    ms6[4] = el(6, 7);  // detect
+    ms6[5] = el(0, 7);  // whole pipeline
     return NOMA_OK;
 }
 
@@ -612,15 +633,25 @@ NOMA_API int noma_pipeline(noma_ctx_t c, const noma_net_desc *desc, const noma_t
     if (!s.ok) return s.finish();
 
     noma_dataset ds{NOMA_LAYOUT_WIDEN_COMPLEX, S, K, n, 2 * M, px, py};
+    // fork: He-normal init and the per-epoch shuffles depend only on seeds,
+    // so they run on the side stream while the LLS kernel runs; join before
+    // w0 is copied into the plans and training starts.
     mark(c, 0);
+    cudaEventRecord(c->fork, c->stream);
+    cudaStreamWaitEvent(c->side, c->fork, 0);
+    mark(c, 2, c->side);
+    if (init_launch(g, (int)nets, iseed, nullptr, dp, c->side)) return cuda_fail(c, "init");
+    mark(c, 3, c->side);
+    if (perm_launch((int)nets, cfg->epochs, n, sseed, perm, c->side)) return cuda_fail(c, "perm");
+    mark(c, 4, c->side);
+    cudaEventRecord(c->join, c->side);
     st = lls_launch(lls_params(&ds, px, py, dw, dc, dst, d32, r0), c->stream);
     if (st) return st == NOMA_ERR_CUDA ? cuda_fail(c, "lls") : fail(c, st, "lls: unsupported shape");
     mark(c, 1);
-    if (init_launch(g, (int)nets, iseed, dw, dp, c->stream)) return cuda_fail(c, "init");
-    mark(c, 2);
-    if (perm_launch((int)nets, cfg->epochs, n, sseed, perm, c->stream)) return cuda_fail(c, "perm");
-    mark(c, 3);
-    c->launches += 3;
+    cudaStreamWaitEvent(c->stream, c->join, 0);
+    if (set_w0_launch((int)nets, 2 * M, g.plan_total, dw, dp, c->stream)) return cuda_fail(c, "w0");
+    mark(c, 5);
+    c->launches += 4;
     if (cfg->epochs > 0) {
         TrainParams tp;
         fill_train(tp, g, cfg);
@@ -639,7 +670,7 @@ NOMA_API int noma_pipeline(noma_ctx_t c, const noma_net_desc *desc, const noma_t
         if (st) return st == NOMA_ERR_CUDA ? cuda_fail(c, "train") : fail(c, st, "train: unsupported network shape");
         c->launches += 1;
     }
-    mark(c, 4);
+    mark(c, 6);
     if (ND > 0) {
         if (der) cudaMemsetAsync(der, 0, nets * sizeof(uint32_t), c->stream);
         DetectParams dpp;
@@ -660,7 +691,7 @@ NOMA_API int noma_pipeline(noma_ctx_t c, const noma_net_desc *desc, const noma_t
         if (st) return st == NOMA_ERR_CUDA ? cuda_fail(c, "detect") : fail(c, st, "detect: unsupported network shape");
         c->launches += 1;
     }
-    mark(c, 5);
+    mark(c, 7);
     return s.finish();
 }
 

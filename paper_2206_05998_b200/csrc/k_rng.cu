@@ -50,76 +50,99 @@ int perm_launch(int n_nets, int epochs, int n, const uint64_t *seeds, uint16_t *
 }
 
 // ------------------------------------------------------------------- init
-// plans[net][plan_total]: W_l (He-normal, row-major draws), b_l = 0, final = 0;
-// w0 (FP64, nullable) copied into the plan's w0 slot.
-__global__ void init_kernel(NetGeom g, int n_nets, const uint64_t *seeds, const double *w0,
-                            float *plans) {
-    const int net = blockIdx.x * blockDim.x + threadIdx.x;
-    if (net >= n_nets) return;
-    float *pl = plans + (size_t)net * g.plan_total;
-    for (int i = 0; i < g.plan_total; ++i) pl[i] = 0.0f;
-    if (w0)
-        for (int c = 0; c < g.dims[0]; ++c) pl[c] = (float)w0[(size_t)net * g.dims[0] + c];
-    Xoshiro r(seeds[net]);
-    for (int l = 1; l < g.nd; ++l) {
-        const int fan_in = g.dims[l - 1];
-        const double scale = sqrt(2.0 / fan_in);
-        for (int row = 0; row < g.dims[l]; ++row)
-            for (int c = 0; c < fan_in; ++c)
-                pl[g.plan_w[l] + row * g.plan_pad[l - 1] + c] = (float)(r.gaussian() * scale);
-    }
-}
+// He-normal initialisation (hybrid_nn.cpp:43-52), one CTA per net.  The
+// reference stream is sequential, so one producer thread runs xoshiro256++
+// ahead into a double-buffered shared-memory ring of raw u64 pairs while the
+// other threads turn the previous chunk into Box-Muller draws (the FP64
+// log/sqrt/cos dominate the per-draw cost) and scatter them into the plan
+// (FP32, FusedPlan layout) and/or the flat FP64 parameter vector.
+// Seeds come from `seeds` (Rng(seed)) or, when `states` is non-null, from
+// caller xoshiro states that are advanced in place (init_params(..., Rng&)).
+constexpr int kInitThreads = 128;
+constexpr int kInitChunk = 1024;  // gaussians per ring slot
 
-// Same draws from caller-provided xoshiro states (init_params(dims, w0, Rng&)):
-// states are advanced in place; FP64 weights optionally written in the
-// reference parameter order (W_1, b_1, ..., W_N, b_N, final).
-__global__ void init_state_kernel(NetGeom g, int n_nets, uint64_t *states, const double *w0,
-                                  float *plans, double *theta, int ptrain) {
-    const int net = blockIdx.x * blockDim.x + threadIdx.x;
-    if (net >= n_nets) return;
-    uint64_t *st = states + (size_t)net * 4;
-    Xoshiro r(st[0], st[1], st[2], st[3]);
+__global__ void __launch_bounds__(kInitThreads) init_block_kernel(
+    NetGeom g, const uint64_t *seeds, uint64_t *states, const double *w0, float *plans,
+    double *theta, int ptrain) {
+    __shared__ uint64_t ring[2][2 * kInitChunk];
+    const int net = blockIdx.x, tid = threadIdx.x;
     float *pl = plans ? plans + (size_t)net * g.plan_total : nullptr;
     double *th = theta ? theta + (size_t)net * ptrain : nullptr;
+    // zero outputs, w0 slot, biases / final (theta)
     if (pl) {
-        for (int i = 0; i < g.plan_total; ++i) pl[i] = 0.0f;
-        if (w0)
-            for (int c = 0; c < g.dims[0]; ++c) pl[c] = (float)w0[(size_t)net * g.dims[0] + c];
+        for (int i = tid; i < g.plan_total; i += kInitThreads) pl[i] = 0.0f;
     }
-    int off = 0;
+    if (th) {
+        for (int i = tid; i < ptrain; i += kInitThreads) th[i] = 0.0;
+    }
+    __syncthreads();
+    if (pl && w0)
+        for (int c = tid; c < g.dims[0]; c += kInitThreads) pl[c] = (float)w0[(size_t)net * g.dims[0] + c];
+    // gaussian count and per-layer starts (reference draw order)
+    int start[NOMA_MAX_DIMS + 1];
+    int total = 0;
     for (int l = 1; l < g.nd; ++l) {
-        const int fan_in = g.dims[l - 1];
-        const double scale = sqrt(2.0 / fan_in);
-        for (int row = 0; row < g.dims[l]; ++row)
-            for (int c = 0; c < fan_in; ++c) {
-                const double v = r.gaussian() * scale;
-                if (pl) pl[g.plan_w[l] + row * g.plan_pad[l - 1] + c] = (float)v;
-                if (th) th[off] = v;
-                ++off;
-            }
-        if (th)
-            for (int j = 0; j < g.dims[l]; ++j) th[off + j] = 0.0;
-        off += g.dims[l];
+        start[l] = total;
+        total += g.dims[l] * g.dims[l - 1];
     }
-    if (th)
-        for (int j = 0; j < g.dims[g.nd - 1]; ++j) th[off + j] = 0.0;
-    st[0] = r.s0;
-    st[1] = r.s1;
-    st[2] = r.s2;
-    st[3] = r.s3;
+    start[g.nd] = total;
+    Xoshiro r = states ? Xoshiro(states[net * 4], states[net * 4 + 1], states[net * 4 + 2], states[net * 4 + 3])
+                       : Xoshiro(seeds[net]);
+    const int chunks = (total + kInitChunk - 1) / kInitChunk;
+    auto produce = [&](int c) {
+        const int n = min(kInitChunk, total - c * kInitChunk);
+        uint64_t *b = ring[c & 1];
+        for (int i = 0; i < 2 * n; ++i) b[i] = r.next();
+    };
+    if (tid == 0 && chunks > 0) produce(0);
+    __syncthreads();
+    for (int c = 0; c < chunks; ++c) {
+        if (tid == 0) {
+            if (c + 1 < chunks) produce(c + 1);
+        } else {
+            const int n = min(kInitChunk, total - c * kInitChunk);
+            const uint64_t *b = ring[c & 1];
+            for (int i = tid - 1; i < n; i += kInitThreads - 1) {
+                const int w = c * kInitChunk + i;
+                int l = 1;
+                while (w >= start[l + 1]) ++l;
+                const int fan_in = g.dims[l - 1];
+                const int off = w - start[l], row = off / fan_in, col = off % fan_in;
+                // Box-Muller cosine half (rng.hpp:58-62) on the recorded pair
+                const double u1 = 1.0 - static_cast<double>(b[2 * i] >> 11) * 0x1.0p-53;
+                const double u2 = static_cast<double>(b[2 * i + 1] >> 11) * 0x1.0p-53;
+                const double ang = __dmul_rn(2.0 * 3.141592653589793238462643383279502884, u2);
+                const double gauss = __dmul_rn(sqrt(__dmul_rn(-2.0, log(u1))), cos(ang));
+                const double v = gauss * sqrt(2.0 / fan_in);
+                if (pl) pl[g.plan_w[l] + row * g.plan_pad[l - 1] + col] = (float)v;
+                if (th) {
+                    int t = 0;  // flat offset: W_1, b_1, ..., W_l block
+                    for (int q = 1; q < l; ++q) t += g.dims[q] * g.dims[q - 1] + g.dims[q];
+                    th[t + off] = v;
+                }
+            }
+        }
+        __syncthreads();
+    }
+    if (states && tid == 0) {
+        states[net * 4] = r.s0;
+        states[net * 4 + 1] = r.s1;
+        states[net * 4 + 2] = r.s2;
+        states[net * 4 + 3] = r.s3;
+    }
 }
 
 int init_state_launch(const NetGeom &g, int n_nets, uint64_t *states, const double *w0,
                       float *plans, double *theta, int ptrain, cudaStream_t st) {
     if (n_nets == 0) return NOMA_OK;
-    init_state_kernel<<<(n_nets + 63) / 64, 64, 0, st>>>(g, n_nets, states, w0, plans, theta, ptrain);
+    init_block_kernel<<<n_nets, kInitThreads, 0, st>>>(g, nullptr, states, w0, plans, theta, ptrain);
     return cudaGetLastError() == cudaSuccess ? NOMA_OK : NOMA_ERR_CUDA;
 }
 
 int init_launch(const NetGeom &g, int n_nets, const uint64_t *seeds, const double *w0,
                 float *plans, cudaStream_t st) {
     if (n_nets == 0) return NOMA_OK;
-    init_kernel<<<(n_nets + 63) / 64, 64, 0, st>>>(g, n_nets, seeds, w0, plans);
+    init_block_kernel<<<n_nets, kInitThreads, 0, st>>>(g, seeds, nullptr, w0, plans, nullptr, 0);
     return cudaGetLastError() == cudaSuccess ? NOMA_OK : NOMA_ERR_CUDA;
 }
 

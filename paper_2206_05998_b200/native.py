@@ -28,7 +28,7 @@ EXPORTED = [
     "noma_ctx_phase_ms", "noma_measure_fp32_tflops", "noma_init_params_state",
     "noma_lls_predict",
 ]
-PHASES = ("lls", "init", "shuffle", "train", "detect")
+PHASES = ("lls", "init", "shuffle", "train", "detect", "total")
 
 
 class NomaError(RuntimeError):
@@ -209,7 +209,7 @@ class Context:
         self._check(self.L.noma_ctx_set_profiling(self.h, 1 if on else 0))
 
     def phase_ms(self) -> dict:
-        out = (C.c_double * 5)()
+        out = (C.c_double * 6)()
         self._check(self.L.noma_ctx_phase_ms(self.h, out))
         return dict(zip(PHASES, list(out)))
 
