@@ -177,6 +177,15 @@ NOMA_API int noma_train(noma_ctx_t ctx, const noma_dataset *ds, const noma_net_d
                         const noma_train_cfg *cfg, const double *w0, float *plans_inout,
                         const uint64_t *shuffle_seeds, double *loss_trace, int *status, int mem);
 
+/* FP64 parity mode of noma_train: the reference's precision end to end
+ * (residual x w0 + a w - y formed in FP64, FP64 Adam).  theta_inout
+ * [net][trainable] holds HybridNetParams in the reference flat order (W_1,
+ * b_1, ..., W_N, b_N, final) on entry and the trained values on return. */
+NOMA_API int noma_train_f64(noma_ctx_t ctx, const noma_dataset *ds, const noma_net_desc *desc,
+                            const noma_train_cfg *cfg, const double *w0, double *theta_inout,
+                            const uint64_t *shuffle_seeds, double *loss_trace, int *status,
+                            int mem);
+
 /* Replaces hybrid_nn::detect / fused::fused_forward_f32 + hard_decision_qpsk
  * + bit_error_rate (hybrid_nn.cpp:197-199, fused_inference.cpp:222-231,
  * eval.cpp:38-65): streaming inference of every net over its design's data.

@@ -200,6 +200,29 @@ def train(net: HybridNet, design: np.ndarray, targets: np.ndarray, epochs=50, ba
     return trace
 
 
+def train_f64(dims, w0, theta, design, targets, epochs=50, batch_size=128, lr=0.005,
+              shuffle_seed=0, widened_complex=False):
+    """FP64 parity mode of hybrid_nn::train: theta (reference flat order,
+    W_1, b_1, ..., final) is trained in place on device; returns the trace."""
+    cfg = N.TrainCfg.of(epochs, batch_size, lr)
+    if widened_complex:
+        x = np.ascontiguousarray(design, dtype=np.complex128)
+        y = np.ascontiguousarray(np.asarray(targets, dtype=np.complex128).reshape(-1, 1))
+        rows, width, layout = 2 * x.shape[0], 2 * x.shape[1], N.LAYOUT_WIDEN
+        xd, yd = x.view(np.float64), y.view(np.float64)
+    else:
+        xd = np.ascontiguousarray(design, dtype=np.float64)
+        yd = np.ascontiguousarray(targets, dtype=np.float64)
+        rows, width, layout = xd.shape[0], xd.shape[1], N.LAYOUT_REAL
+    th = np.ascontiguousarray(theta, dtype=np.float64).reshape(1, -1)
+    trace = np.zeros(max(epochs, 0))
+    context().train_f64(layout, 1, 1, rows, width, xd, yd, list(dims), cfg,
+                        np.ascontiguousarray(w0, dtype=np.float64).reshape(1, -1), th,
+                        np.array([shuffle_seed], dtype=np.uint64), trace if epochs > 0 else None)
+    theta[...] = th[0]
+    return trace
+
+
 def fused_forward_f32(net: HybridNet, x: np.ndarray) -> np.ndarray:
     """fused::fused_forward_f32 (fused_inference.cpp:222-231): real rows [B, d0]."""
     x = np.ascontiguousarray(x, dtype=np.float32)

@@ -546,6 +546,62 @@ NOMA_API int noma_train(noma_ctx_t c, const noma_dataset *ds, const noma_net_des
     return s.finish();
 }
 
+NOMA_API int noma_train_f64(noma_ctx_t c, const noma_dataset *ds, const noma_net_desc *desc,
+                            const noma_train_cfg *cfg, const double *w0, double *theta_inout,
+                            const uint64_t *shuffle_seeds, double *trace, int *status, int mem) {
+    if (!c) return NOMA_ERR_ARGUMENT;
+    int st = check_dataset(c, ds);
+    if (st) return st;
+    if ((st = check_cfg(c, cfg))) return st;
+    NetGeom g;
+    if (!make_geom(desc, &g)) return fail(c, NOMA_ERR_DIMENSION, "train: bad dims");
+    if (g.dims[0] != ds->width) return fail(c, NOMA_ERR_DIMENSION, "train: input width does not match network");
+    if (!w0 || !theta_inout || !shuffle_seeds) return fail(c, NOMA_ERR_ARGUMENT, "null argument");
+    const size_t nets = (size_t)ds->n_designs * ds->nets_per_design;
+    if (nets == 0) return NOMA_OK;
+    if (ds->rows > 65535) return fail(c, NOMA_ERR_UNSUPPORTED, "train: more than 65535 rows");
+    const int ptrain = trainable_count(g);
+    Stage s(c, mem);
+    const double *x = s.in(ds->design, design_elems(ds));
+    const double *y = s.in(ds->targets, target_elems(ds));
+    const double *dw = s.in(w0, nets * ds->width);
+    const uint64_t *seeds = s.in(shuffle_seeds, nets);
+    double *dth = s.inout(theta_inout, nets * ptrain);
+    double *dt = s.out(trace, nets * (size_t)cfg->epochs);
+    const int *dst = s.in(status, nets);
+    double *mom = s.scratch<double>(nets * 2 * ptrain);
+    uint16_t *perm = s.scratch<uint16_t>(nets * (size_t)cfg->epochs * ds->rows);
+    if (!s.ok) return s.finish();
+    if (perm_launch((int)nets, cfg->epochs, ds->rows, seeds, perm, c->stream)) return cuda_fail(c, "perm");
+    TrainF64Params tp;
+    tp.g = g;
+    tp.layout = ds->layout;
+    tp.n_nets = (int)nets;
+    tp.K = ds->nets_per_design;
+    tp.rows = ds->rows;
+    tp.width = ds->width;
+    tp.epochs = cfg->epochs;
+    tp.batch = cfg->batch_size;
+    tp.design = x;
+    tp.targets = y;
+    tp.w0 = dw;
+    tp.perm = perm;
+    tp.theta = dth;
+    tp.moments = mom;
+    tp.trace = dt;
+    tp.status = dst;
+    tp.lr = cfg->lr;
+    tp.b1 = cfg->beta1;
+    tp.b2 = cfg->beta2;
+    tp.eps = cfg->eps;
+    if (cfg->epochs > 0) {
+        st = train_f64_launch(tp, c->stream);
+        if (st) return st == NOMA_ERR_CUDA ? cuda_fail(c, "train f64") : fail(c, st, "train f64: unsupported shape");
+    }
+    c->launches += 2;
+    return s.finish();
+}
+
 NOMA_API int noma_detect(noma_ctx_t c, const noma_net_desc *desc, int layout, int n_designs,
                          int nets_per_design, int rows, const float *data, const float *plans,
                          const uint8_t *truth, float *soft, uint8_t *codes, uint32_t *bit_errors,

@@ -1,0 +1,208 @@
+// FP64 parity mode of the pilot-phase training (hybrid_nn::train,
+// hybrid_nn.cpp:158-195, with loss_and_grad :84-114 and adam_step :118-144)
+// -- the reference's own precision.  Same fused structure as the FP32 kernel
+// (one CTA per user network for all epochs, weights/gradients on chip, the
+// IQ widening applied at load) but every value is FP64 and the residual is
+// formed exactly as the reference does (x w0 + a_N w - y, hybrid_nn.cpp:94).
+// Used to show that the device path reproduces the FP64 reference trajectory;
+// the FP32 kernel is the throughput path.
+//
+// The 128-row minibatch is processed in chunks of CH rows (CH = 64 or 32 so
+// the FP64 activations fit next to the FP64 weights and gradients); gradients
+// accumulate over the chunks before the single Adam update of the step.  Adam
+// moments live in global memory (L2-resident), two FP64 per parameter.
+#include <math.h>
+
+#include "kernels.cuh"
+
+namespace noma_dev {
+
+constexpr int kT64 = 256;
+
+__global__ void __launch_bounds__(kT64) train_f64_kernel(TrainF64Params p) {
+    extern __shared__ __align__(16) double smd[];
+    const int net = blockIdx.x, tid = threadIdx.x;
+    if (p.status && p.status[net] != NOMA_OK) return;
+    const NetGeom &g = p.g;
+    const int N = g.nd - 1, n = p.rows, d = net / p.K, CH = p.chunk;
+    const int width = p.width, M = width / 2;
+    // theta layout (reference flat order): W_1 (L1 x L0), b_1, ..., final
+    double *TH = smd;                      // ptrain
+    double *GR = TH + p.ptrain;            // ptrain
+    double *ACT = GR + p.ptrain;           // activations [layer][CH][L_l], layer 0 = input
+    double *DA = ACT + p.act_total;        // dA scratch [CH][maxw]
+    double *DZ = DA + CH * p.maxw;         // dZ scratch [CH][maxw]
+    double *YB = DZ + CH * p.maxw;         // targets of the chunk [CH]
+    double *RED = YB + CH;                 // kT64 reduction scratch
+    int *IDX = reinterpret_cast<int *>(RED + kT64);  // CH row indices
+
+    double *gtheta = p.theta + (size_t)net * p.ptrain;
+    double *m1 = p.moments + (size_t)net * 2 * p.ptrain, *m2 = m1 + p.ptrain;
+    for (int i = tid; i < p.ptrain; i += kT64) {
+        TH[i] = gtheta[i];
+        m1[i] = 0.0;
+        m2[i] = 0.0;
+    }
+    const double *w0 = p.w0 + (size_t)net * width;
+    int woff[NOMA_MAX_DIMS], boff[NOMA_MAX_DIMS], aoff[NOMA_MAX_DIMS];
+    {
+        int o = 0, a = 0;
+        for (int l = 1; l <= N; ++l) {
+            woff[l] = o;
+            o += g.dims[l] * g.dims[l - 1];
+            boff[l] = o;
+            o += g.dims[l];
+        }
+        for (int l = 0; l <= N; ++l) {
+            aoff[l] = a;
+            a += CH * g.dims[l];
+        }
+    }
+    const int foff = p.ptrain - g.dims[N];
+    __syncthreads();
+    long step = 0;
+    for (int e = 0; e < p.epochs; ++e) {
+        const uint16_t *perm = p.perm + ((size_t)net * p.epochs + e) * n;
+        double loss_sum = 0.0;  // thread 0
+        for (int start = 0; start < n; start += p.batch) {
+            const int bsz = min(p.batch, n - start);
+            for (int i = tid; i < p.ptrain; i += kT64) GR[i] = 0.0;
+            double sq = 0.0;  // per-thread partial of ||residual||^2
+            __syncthreads();
+            for (int c0 = 0; c0 < bsz; c0 += CH) {
+                const int cn = min(CH, bsz - c0);
+                // ---- gather + widen (iq_transform.cpp:17-20), targets -------
+                for (int r = tid; r < cn; r += kT64) IDX[r] = perm[start + c0 + r];
+                __syncthreads();
+                for (int i = tid; i < cn * width; i += kT64) {
+                    const int r = i / width, c = i % width, idx = IDX[r];
+                    double v;
+                    if (p.layout == NOMA_LAYOUT_WIDEN_COMPLEX) {
+                        const double *x = p.design + ((size_t)d * (n / 2) + (idx >> 1)) * M * 2;
+                        if (!(idx & 1)) v = c < M ? x[2 * c] : x[2 * (c - M) + 1];
+                        else v = c < M ? x[2 * c + 1] : -x[2 * (c - M)];
+                    } else {
+                        v = p.design[((size_t)d * n + idx) * width + c];
+                    }
+                    ACT[aoff[0] + r * width + c] = v;
+                }
+                for (int r = tid; r < cn; r += kT64) {
+                    const int idx = IDX[r];
+                    YB[r] = p.layout == NOMA_LAYOUT_WIDEN_COMPLEX
+                                ? p.targets[(((size_t)d * (n / 2) + (idx >> 1)) * p.K + net % p.K) * 2 + (idx & 1)]
+                                : p.targets[((size_t)d * p.K + net % p.K) * n + idx];
+                }
+                __syncthreads();
+                // ---- forward (hybrid_nn.cpp:60-72) ---------------------------
+                for (int l = 1; l <= N; ++l) {
+                    const int in = g.dims[l - 1], out = g.dims[l];
+                    const double *A = ACT + aoff[l - 1], *W = TH + woff[l], *B = TH + boff[l];
+                    double *Z = ACT + aoff[l];
+                    for (int i = tid; i < cn * out; i += kT64) {
+                        const int r = i / out, j = i % out;
+                        double s = 0.0;
+                        for (int k = 0; k < in; ++k) s += A[r * in + k] * W[j * in + k];
+                        s += B[j];
+                        Z[r * out + j] = s > 0.0 ? s : 0.0;
+                    }
+                    __syncthreads();
+                }
+                // ---- residual x w0 + a_N w - y, dy = 2 r / B (hybrid_nn.cpp:94-98)
+                const int LN = g.dims[N];
+                const double *AN = ACT + aoff[N];
+                for (int r = tid; r < cn; r += kT64) {
+                    double lin = 0.0, br = 0.0;
+                    for (int c = 0; c < width; ++c) lin += ACT[aoff[0] + r * width + c] * w0[c];
+                    for (int c = 0; c < LN; ++c) br += AN[r * LN + c] * TH[foff + c];
+                    const double res = lin + br - YB[r];
+                    sq += res * res;
+                    YB[r] = (2.0 / (double)bsz) * res;  // dy
+                }
+                __syncthreads();
+                // ---- final layer gradient, da = dy wf^T (hybrid_nn.cpp:99-102)
+                for (int j = tid; j < LN; j += kT64) {
+                    double s = 0.0;
+                    for (int r = 0; r < cn; ++r) s += AN[r * LN + j] * YB[r];
+                    GR[foff + j] += s;
+                }
+                for (int i = tid; i < cn * LN; i += kT64) DA[i] = YB[i / LN] * TH[foff + i % LN];
+                __syncthreads();
+                // ---- hidden layers backward (hybrid_nn.cpp:105-112) ------------
+                for (int l = N; l >= 1; --l) {
+                    const int out = g.dims[l], in = g.dims[l - 1];
+                    const double *A = ACT + aoff[l], *Ab = ACT + aoff[l - 1];
+                    for (int i = tid; i < cn * out; i += kT64) DZ[i] = A[i] > 0.0 ? DA[i] : 0.0;
+                    __syncthreads();
+                    for (int i = tid; i < out * in; i += kT64) {  // gW = dz^T below
+                        const int j = i / in, c = i % in;
+                        double s = 0.0;
+                        for (int r = 0; r < cn; ++r) s += DZ[r * out + j] * Ab[r * in + c];
+                        GR[woff[l] + i] += s;
+                    }
+                    for (int j = tid; j < out; j += kT64) {  // gb = colsum dz
+                        double s = 0.0;
+                        for (int r = 0; r < cn; ++r) s += DZ[r * out + j];
+                        GR[boff[l] + j] += s;
+                    }
+                    if (l > 1) {  // da = dz W_l
+                        for (int i = tid; i < cn * in; i += kT64) {
+                            const int r = i / in, c = i % in;
+                            double s = 0.0;
+                            for (int j = 0; j < out; ++j) s += DZ[r * out + j] * TH[woff[l] + j * in + c];
+                            DA[i] = s;
+                        }
+                    }
+                    __syncthreads();
+                }
+            }
+            // ---- loss of the step and Adam (hybrid_nn.cpp:118-144) ------------
+            RED[tid] = sq;
+            __syncthreads();
+            if (tid == 0) {
+                double s = 0.0;
+                for (int i = 0; i < kT64; ++i) s += RED[i];
+                const double loss = s / (double)bsz;
+                loss_sum += loss * (double)bsz;
+            }
+            ++step;
+            const double corr1 = 1.0 - pow(p.b1, (double)step);
+            const double corr2 = 1.0 - pow(p.b2, (double)step);
+            for (int i = tid; i < p.ptrain; i += kT64) {
+                const double gi = GR[i];
+                const double a = p.b1 * m1[i] + (1.0 - p.b1) * gi;
+                const double b = p.b2 * m2[i] + (1.0 - p.b2) * (gi * gi);
+                m1[i] = a;
+                m2[i] = b;
+                TH[i] -= p.lr * (a / corr1) / (sqrt(b / corr2) + p.eps);
+            }
+            __syncthreads();
+        }
+        if (tid == 0 && p.trace) p.trace[(size_t)net * p.epochs + e] = loss_sum / (double)n;
+    }
+    for (int i = tid; i < p.ptrain; i += kT64) gtheta[i] = TH[i];
+}
+
+int train_f64_launch(TrainF64Params &p, cudaStream_t st) {
+    const NetGeom &g = p.g;
+    if (p.batch < 1) return NOMA_ERR_CONFIG;
+    int maxw = 0;
+    for (int l = 0; l < g.nd; ++l) maxw = g.dims[l] > maxw ? g.dims[l] : maxw;
+    p.maxw = maxw;
+    p.ptrain = trainable_count(g);
+    for (int ch = 128; ch >= 8; ch /= 2) {
+        int act = 0;
+        for (int l = 0; l < g.nd; ++l) act += ch * g.dims[l];
+        const size_t smem = (size_t)(2 * p.ptrain + act + 2 * ch * maxw + ch + kT64) * sizeof(double) +
+                            ch * sizeof(int);
+        if (smem <= 227 * 1024) {
+            p.chunk = ch;
+            p.act_total = act;
+            cudaFuncSetAttribute(train_f64_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            train_f64_kernel<<<p.n_nets, kT64, smem, st>>>(p);
+            return cudaGetLastError() == cudaSuccess ? NOMA_OK : NOMA_ERR_CUDA;
+        }
+    }
+    return NOMA_ERR_UNSUPPORTED;
+}
+
+}  // namespace noma_dev

@@ -34,6 +34,21 @@ struct TrainParams {
         off_end, gs_stride, gsplit, off_mom;
 };
 
+struct TrainF64Params {
+    NetGeom g;
+    int layout, n_nets, K, rows, width, epochs, batch;
+    const double *design;   // as noma_dataset (FP64)
+    const double *targets;
+    const double *w0;       // [net][width]
+    const uint16_t *perm;   // [net][epochs][rows]
+    double *theta;          // [net][ptrain] in/out, reference flat order
+    double *moments;        // [net][2][ptrain] scratch
+    double *trace;          // [net][epochs] nullable
+    const int *status;
+    double lr, b1, b2, eps;
+    int ptrain, maxw, chunk, act_total;
+};
+
 struct DetectParams {
     NetGeom g;
     int layout, n_nets, K, rows, width;
@@ -77,6 +92,7 @@ int init_state_launch(const NetGeom &g, int n_nets, uint64_t *states, const doub
 int lls_predict_launch(int layout, int S, int K, int rows, int width, const double *data,
                        const double *w0, double *out, cudaStream_t st);
 int train_launch(TrainParams &p, cudaStream_t st);
+int train_f64_launch(TrainF64Params &p, cudaStream_t st);
 int detect_launch(DetectParams &p, cudaStream_t st);
 int synth_launch(SynthParams p, double *noise_power_scratch, cudaStream_t st);
 

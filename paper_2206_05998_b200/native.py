@@ -26,7 +26,7 @@ EXPORTED = [
     "noma_plan_size", "noma_param_count", "noma_lls_fit", "noma_init_params", "noma_train",
     "noma_detect", "noma_pipeline", "noma_synthesize", "noma_ctx_set_profiling",
     "noma_ctx_phase_ms", "noma_measure_fp32_tflops", "noma_init_params_state",
-    "noma_lls_predict",
+    "noma_lls_predict", "noma_train_f64",
 ]
 PHASES = ("lls", "init", "shuffle", "train", "detect", "total")
 
@@ -128,6 +128,8 @@ def load():
     L.noma_measure_fp32_tflops.argtypes = [vp, ip, C.POINTER(C.c_double)]
     L.noma_init_params_state.argtypes = [vp, C.POINTER(NetDesc), ip, vp, vp, vp, vp, ip]
     L.noma_lls_predict.argtypes = [vp, ip, ip, ip, ip, ip, vp, vp, vp, ip]
+    L.noma_train_f64.argtypes = [vp, C.POINTER(Dataset), C.POINTER(NetDesc), C.POINTER(TrainCfg),
+                                 vp, vp, vp, vp, vp, ip]
     _lib = L
     return L
 
@@ -268,6 +270,15 @@ class Context:
         self._check(self.L.noma_train(self.h, C.byref(ds), C.byref(d), C.byref(cfg), _ptr(w0),
                                       _ptr(plans), _ptr(shuffle_seeds), _ptr(trace),
                                       _ptr(status), mem))
+
+    def train_f64(self, layout, n_designs, K, rows, width, design, targets, dims, cfg: TrainCfg,
+                  w0, theta, shuffle_seeds, trace=None, status=None):
+        mem = _mem_of(design, targets, w0, theta, shuffle_seeds)
+        ds = Dataset(layout, n_designs, K, rows, width, _ptr(design), _ptr(targets))
+        d = NetDesc.of(dims)
+        self._check(self.L.noma_train_f64(self.h, C.byref(ds), C.byref(d), C.byref(cfg), _ptr(w0),
+                                          _ptr(theta), _ptr(shuffle_seeds), _ptr(trace),
+                                          _ptr(status), mem))
 
     def detect(self, dims, layout, n_designs, K, rows, data, plans, truth=None, soft=None,
                codes=None, bit_errors=None):

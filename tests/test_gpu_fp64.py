@@ -1,0 +1,74 @@
+"""GPU parity of the FP64 training mode (noma_train_f64) against the FP64
+oracle: the reference's own precision end to end, so the device must follow
+the reference trajectory through all 50 epochs -- weights, loss trace, soft
+outputs and hard decisions (bit-identical decisions is the north-star bar)."""
+import numpy as np
+import pytest
+
+from tests.helpers import record
+
+pytestmark = pytest.mark.gpu
+
+THETA_TOL = 1e-8   # relative to max |theta| after 50 epochs of FP64 Adam
+TRACE_TOL = 1e-9   # relative, per epoch
+
+
+@pytest.fixture(scope="module")
+def A():
+    from paper_2206_05998_b200 import api
+
+    api.context()
+    return api
+
+
+@pytest.mark.parametrize("M,K,k,hidden,snr,epochs", [
+    (4, 2, 1, [64, 64, 64], float("inf"), 50),  # test_hybrid_nn.cpp:253-271 scenario
+    (16, 6, 5, [64], 25.0, 50),                 # C1, weakest user
+    (16, 6, 0, [64], 25.0, 50),                 # C1, strongest user
+    (16, 6, 5, [64, 64], 25.0, 50),             # C2
+    (16, 6, 5, [64], 8.0, 50),                  # low SNR, BER > 0
+    (32, 16, 15, [64], 25.0, 10),               # C5 shape
+])
+def test_fp64_training_follows_the_reference(A, O, M, K, k, hidden, snr, epochs):
+    sc = O.Scenario(num_users=K, num_antennas=M, train_symbols=685, data_symbols=3840,
+                    power_step_db=3.0 if K <= 6 else 1.0, snr_db=snr,
+                    rx_nonlinearity_gain=0.0 if np.isinf(snr) else 0.05, seed=91 + M + k)
+    rec = O.synthesize(sc)
+    x = O.widen_design(rec.train_rx)
+    y = O.widen_targets(rec.train_symbols[:, k])
+    w0 = O.lls_fit(x, y).w
+    dims = [2 * M] + hidden
+    onet = O.init_params(dims, w0, O.Rng(92))
+    theta = onet.theta.copy()
+    otrace = O.train(onet, x, y, epochs=epochs, shuffle_seed=93)
+    dtrace = A.train_f64(dims, w0, theta, rec.train_rx, rec.train_symbols[:, k], epochs=epochs,
+                         shuffle_seed=93, widened_complex=True)
+    th_dev = float(np.max(np.abs(theta - onet.theta)) / np.max(np.abs(onet.theta)))
+    tr_dev = float(np.max(np.abs(dtrace - otrace) / np.abs(otrace)))
+    xd = O.widen_design(rec.data_rx)
+    dnet = O.HybridNet(dims, w0, theta)
+    soft_ref = O.detect(onet, xd)
+    soft_dev = O.detect(dnet, xd)
+    sdev = float(np.max(np.abs(soft_dev - soft_ref)) / max(1.0, np.max(np.abs(soft_ref))))
+    flips = int(np.count_nonzero(np.any(O.hard_decision_qpsk(soft_dev) != O.hard_decision_qpsk(soft_ref), axis=1)))
+    record("fp64_training", config=str((M, K, k, hidden, snr, epochs)), theta_dev=th_dev,
+           trace_dev=tr_dev, soft_dev=sdev, flips=flips, symbols=len(soft_ref))
+    assert tr_dev <= TRACE_TOL, tr_dev
+    assert th_dev <= THETA_TOL, th_dev
+    assert flips == 0
+
+
+def test_fp64_real_layout_and_determinism(A, O):
+    rec = O.synthesize(O.Scenario(num_users=2, num_antennas=4, train_symbols=128, data_symbols=8,
+                                  snr_db=20.0, seed=5))
+    x = O.widen_design(rec.train_rx)
+    y = O.widen_targets(rec.train_symbols[:, 0])
+    w0 = O.lls_fit(x, y).w
+    onet = O.init_params([8, 16, 16], w0, O.Rng(4))
+    t1, t2 = onet.theta.copy(), onet.theta.copy()
+    tr1 = A.train_f64([8, 16, 16], w0, t1, x, y, epochs=6, shuffle_seed=7)
+    tr2 = A.train_f64([8, 16, 16], w0, t2, x, y, epochs=6, shuffle_seed=7)
+    assert np.array_equal(t1, t2) and np.array_equal(tr1, tr2)
+    otr = O.train(onet, x, y, epochs=6, shuffle_seed=7)
+    assert np.max(np.abs(t1 - onet.theta)) <= 1e-12 * np.max(np.abs(onet.theta))
+    assert np.max(np.abs(tr1 - otr) / otr) <= 1e-12
