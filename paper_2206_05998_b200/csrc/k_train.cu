@@ -27,12 +27,12 @@
 
 namespace noma_dev {
 
-constexpr int kTrainThreads = 256;
+constexpr int kTrainThreads = 512;
 constexpr int kTrainWarps = kTrainThreads / 32;
 constexpr int kMaxSplit = 2;  // weight-gradient split-K partials
 
 __host__ __device__ inline int grad_splits(int J, int C, int max_split) {
-    const int tiles = (J >> 5) * (C >> 5);
+    const int tiles = (J >> 5) * (C >> 4);
     return tiles < kTrainWarps ? max_split : 1;
 }
 
@@ -76,7 +76,7 @@ __global__ void __launch_bounds__(kTrainThreads, MINB) train_kernel(TrainParams 
     const int width = p.width, M = width / 2;
     const bool vec4 = (width & 3) == 0 && (M & 3) == 0;
     const int fpN = g.fp[N];
-    const int njb = fpN >> 5;  // final-layer partial blocks
+    const int njb = fpN >> 4;  // final-layer partial blocks (16 j each)
     float *AN = N ? sm + p.off_a[N] : XT;
     float loss_acc = 0.0f;     // per-row-thread partial of the epoch loss
     long step = 0;
@@ -84,7 +84,7 @@ __global__ void __launch_bounds__(kTrainThreads, MINB) train_kernel(TrainParams 
         const uint16_t *perm = p.perm + ((size_t)net * p.epochs + e) * n;
         for (int start = 0; start < n; start += p.batch) {
             const int bsz = min(p.batch, n - start);
-            // ---- gather (IQ widening at load): 2 threads per batch row ------
+            // ---- gather (IQ widening at load): 4 threads per batch row ------
             {
                 const int r = tid & (kBatchRows - 1), h = tid >> 7;
                 if (r < bsz) {
@@ -95,7 +95,7 @@ __global__ void __launch_bounds__(kTrainThreads, MINB) train_kernel(TrainParams 
                                            : p.design32 + ((size_t)d * n + idx) * width;
                     const bool odd = wid && (idx & 1);
                     if (vec4) {
-                        for (int c = h * 4; c < width; c += 8) {
+                        for (int c = h * 4; c < width; c += 16) {
                             float4 v;
                             if (!odd) {
                                 v = *reinterpret_cast<const float4 *>(src + c);
@@ -111,12 +111,12 @@ __global__ void __launch_bounds__(kTrainThreads, MINB) train_kernel(TrainParams 
                             XT[(c + 3) * kSR + r] = v.w;
                         }
                     } else {
-                        for (int c = h; c < width; c += 2)
+                        for (int c = h; c < width; c += 4)
                             XT[c * kSR + r] = !odd ? src[c] : (c < M ? src[M + c] : -src[c - M]);
                     }
                 } else {
                     if (h == 0) r0b[r] = 0.0f;
-                    for (int c = h; c < width; c += 2) XT[c * kSR + r] = 0.0f;
+                    for (int c = h; c < width; c += 4) XT[c * kSR + r] = 0.0f;
                 }
                 if (tid == kTrainThreads - 1) {  // Adam constants for this step (FP64 pow)
                     const double c1 = 1.0 - pow(p.b1d, (double)(step + 1));
@@ -128,7 +128,7 @@ __global__ void __launch_bounds__(kTrainThreads, MINB) train_kernel(TrainParams 
             __syncthreads();
             // ---- forward (hybrid_nn.cpp:60-72); last layer also forms yp -----
             for (int l = 1; l <= N; ++l) {
-                tile_forward<kTrainWarps>(PS + g.pw[l], g.sw[l], PS + g.pb[l],
+                tile_forward44<kTrainWarps>(PS + g.pw[l], g.sw[l], PS + g.pb[l],
                                           l == 1 ? XT : sm + p.off_a[l - 1], sm + p.off_a[l],
                                           g.fp[l], g.fp[l - 1], warp, lane,
                                           l == N ? PS + g.pf : nullptr, l == N ? yp : nullptr);
@@ -178,13 +178,13 @@ __global__ void __launch_bounds__(kTrainThreads, MINB) train_kernel(TrainParams 
             // ---- backward (hybrid_nn.cpp:105-112) ----------------------------
             for (int l = N; l >= 1; --l) {
                 const float *ain = l == 1 ? XT : sm + p.off_a[l - 1];
-                tile_weight_grad<kTrainWarps>(sm + p.off_a[l], ain, GS + g.pw[l], g.sw[l],
+                tile_weight_grad44<kTrainWarps>(sm + p.off_a[l], ain, GS + g.pw[l], g.sw[l],
                                               GS + g.pb[l], g.fp[l], g.fp[l - 1],
                                               grad_splits(g.fp[l], g.fp[l - 1], p.gsplit), gstride, warp,
                                               lane);
                 __syncthreads();
                 if (l > 1) {
-                    tile_backward_data<kTrainWarps>(PS + g.pw[l], g.sw[l], sm + p.off_a[l],
+                    tile_backward_data44<kTrainWarps>(PS + g.pw[l], g.sw[l], sm + p.off_a[l],
                                                     sm + p.off_a[l - 1], g.fp[l - 1], g.fp[l],
                                                     warp, lane);
                     __syncthreads();
@@ -263,7 +263,7 @@ int train_launch(TrainParams &p, cudaStream_t st) {
     // Prefer (a) two split-K gradient partials and (b) Adam moments in shared
     // memory (frees ~2*ptotal/256 registers per thread for the FFMA2 tiles'
     // scheduling); drop (b) then (a) until the carve-up fits 227 KB.
-    const int base_rest = off + kBatchRows * 3 + (g.fp[g.nd - 1] / 32) * kBatchRows + 8;
+    const int base_rest = off + kBatchRows * 3 + (g.fp[g.nd - 1] / 16) * kBatchRows + 8;
     auto fits = [&](int splits, int mom) {
         return (size_t)(base_rest + (splits + 2 * mom) * p.gs_stride) * sizeof(float) <= 227 * 1024;
     };
@@ -284,7 +284,7 @@ int train_launch(TrainParams &p, cudaStream_t st) {
     p.off_red = off;
     off += kBatchRows;
     p.off_yp = off;
-    off += (g.fp[g.nd - 1] / 32) * kBatchRows;
+    off += (g.fp[g.nd - 1] / 16) * kBatchRows;
     p.off_misc = off;
     off += 8;
     p.off_end = off;
@@ -300,12 +300,8 @@ int train_launch(TrainParams &p, cudaStream_t st) {
         train_kernel<NS, MB><<<p.n_nets, kTrainThreads, smem, st>>>(p);                         \
         return cudaGetLastError() == cudaSuccess ? NOMA_OK : NOMA_ERR_CUDA;                     \
     }
-    if (mom_smem) {
-        if (smem <= 112 * 1024) NOMA_TRAIN_LAUNCH(0, 2)
-        NOMA_TRAIN_LAUNCH(0, 1)
-    }
-    if (two && need <= 8) NOMA_TRAIN_LAUNCH(8, 2)
-    if (two) NOMA_TRAIN_LAUNCH(16, 2)
+    (void)two;
+    if (mom_smem) NOMA_TRAIN_LAUNCH(0, 1)
     if (need <= 8) NOMA_TRAIN_LAUNCH(8, 1)
     if (need <= 16) NOMA_TRAIN_LAUNCH(16, 1)
     if (need <= 24) NOMA_TRAIN_LAUNCH(24, 1)

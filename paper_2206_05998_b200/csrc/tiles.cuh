@@ -242,3 +242,180 @@ __device__ __forceinline__ void tile_weight_grad(const float *__restrict__ dz,
 }
 
 }  // namespace noma_dev
+
+namespace noma_dev {
+
+// ---------------------------------------------------------------------------
+// 4 x 4 FFMA2 tiles for the 16-warp training CTA (more warps per scheduler to
+// hide the FFMA2 dependency latency; 24 shared-memory wavefronts per 32
+// FFMA2 per thread).  Same layouts and contracts as the 8 x 4 tiles above.
+
+// out[j][r]: J % 16 == 0; thread tile 4 j (j0 + 4 i, quarter-uniform W reads)
+// x 4 r (two FP32x2 pairs); warp tile 16 j x 32 r.  yp blocks are 16 j wide.
+template <int NW>
+__device__ __forceinline__ void tile_forward44(const float *__restrict__ W, int sw,
+                                               const float *__restrict__ bias,
+                                               const float *__restrict__ in,
+                                               float *__restrict__ out, int J, int Kin, int warp,
+                                               int lane, const float *__restrict__ wf = nullptr,
+                                               float *__restrict__ yp = nullptr) {
+    const int rg = lane & 7, jg = lane >> 3;
+    const int ntile = (J >> 4) * 4;
+    for (int wt = warp; wt < ntile; wt += NW) {
+        const int jb = wt >> 2;
+        const int j0 = jb * 16 + jg;
+        const int r0 = (wt & 3) * 32 + 4 * rg;
+        f2_t acc[4][2];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) acc[i][0] = acc[i][1] = f2_bcast(bias[j0 + 4 * i]);
+        const float *wp = W + j0 * sw;
+        const float *ip = in + r0;
+#pragma unroll 2
+        for (int k = 0; k < Kin; k += 4) {
+            float4 w[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) w[i] = *reinterpret_cast<const float4 *>(wp + 4 * i * sw + k);
+            ulonglong2 x[4];
+#pragma unroll
+            for (int kk = 0; kk < 4; ++kk) x[kk] = *reinterpret_cast<const ulonglong2 *>(ip + (k + kk) * kSR);
+#define NOMA_FWD44_K(KK)                                                                \
+    _Pragma("unroll") for (int i = 0; i < 4; ++i) {                                     \
+        const f2_t wk = f2_bcast(f4c<KK>(w[i]));                                        \
+        f2_fma(acc[i][0], wk, x[KK].x);                                                 \
+        f2_fma(acc[i][1], wk, x[KK].y);                                                 \
+    }
+            NOMA_FWD44_K(0) NOMA_FWD44_K(1) NOMA_FWD44_K(2) NOMA_FWD44_K(3)
+#undef NOMA_FWD44_K
+        }
+        float y[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const float2 a = f2_unpack(acc[i][0]), b = f2_unpack(acc[i][1]);
+            const float v[4] = {fmaxf(a.x, 0.f), fmaxf(a.y, 0.f), fmaxf(b.x, 0.f), fmaxf(b.y, 0.f)};
+            *reinterpret_cast<float4 *>(out + (j0 + 4 * i) * kSR + r0) = make_float4(v[0], v[1], v[2], v[3]);
+            if (yp) {
+                const float f = wf[j0 + 4 * i];
+#pragma unroll
+                for (int q = 0; q < 4; ++q) y[q] = fmaf(f, v[q], y[q]);
+            }
+        }
+        if (yp) {
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                y[q] += __shfl_xor_sync(0xffffffffu, y[q], 8);
+                y[q] += __shfl_xor_sync(0xffffffffu, y[q], 16);
+            }
+            if (jg == 0)
+                *reinterpret_cast<float4 *>(yp + jb * kBatchRows + r0) = make_float4(y[0], y[1], y[2], y[3]);
+        }
+    }
+}
+
+// dA[c][r] = sum_j W[j][c] dz[j][r], masked in place; C % 16 == 0.  Thread
+// tile 4 c (one float4 of a W row, quarter-uniform) x 4 r.
+template <int NW>
+__device__ __forceinline__ void tile_backward_data44(const float *__restrict__ W, int sw,
+                                                     const float *__restrict__ dz,
+                                                     float *__restrict__ a, int C, int J,
+                                                     int warp, int lane) {
+    const int rg = lane & 7, cg = lane >> 3;
+    const int ntile = (C >> 4) * 4;
+    for (int wt = warp; wt < ntile; wt += NW) {
+        const int c0 = (wt >> 2) * 16 + 4 * cg;
+        const int r0 = (wt & 3) * 32 + 4 * rg;
+        f2_t acc[4][2];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) acc[i][0] = acc[i][1] = 0ull;
+#pragma unroll 4
+        for (int j = 0; j < J; ++j) {
+            const float4 w = *reinterpret_cast<const float4 *>(W + j * sw + c0);
+            const ulonglong2 z = *reinterpret_cast<const ulonglong2 *>(dz + j * kSR + r0);
+            const float wc[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const f2_t wi = f2_bcast(wc[i]);
+                f2_fma(acc[i][0], wi, z.x);
+                f2_fma(acc[i][1], wi, z.y);
+            }
+        }
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            float *ap = a + (c0 + i) * kSR + r0;
+            const float4 x = *reinterpret_cast<const float4 *>(ap);
+            const float2 p = f2_unpack(acc[i][0]), q = f2_unpack(acc[i][1]);
+            *reinterpret_cast<float4 *>(ap) =
+                make_float4(x.x > 0.f ? p.x : 0.f, x.y > 0.f ? p.y : 0.f,
+                            x.z > 0.f ? q.x : 0.f, x.w > 0.f ? q.y : 0.f);
+        }
+    }
+}
+
+// gW / gb partials over row splits; J % 32 == 0, C % 16 == 0.  Thread tile
+// 4 j (j0 + 8 i; 8-distinct dz reads) x 4 c (c0 + 4 q; quarter-uniform ain
+// reads); warp tile 32 j x 16 c; FP32x2 lanes carry even / odd rows.
+template <int NW>
+__device__ __forceinline__ void tile_weight_grad44(const float *__restrict__ dz,
+                                                   const float *__restrict__ ain,
+                                                   float *__restrict__ gW, int sw,
+                                                   float *__restrict__ gb, int J, int C,
+                                                   int splits, int split_stride, int warp,
+                                                   int lane) {
+    const int jg = lane & 7, cg = lane >> 3;
+    const int ncb = C >> 4;
+    const int ntile = (J >> 5) * ncb;
+    const int rows_per_split = kBatchRows / splits;
+    for (int task = warp; task < ntile * splits; task += NW) {
+        const int wt = task / splits, sp = task % splits;
+        const int jb = wt / ncb, cb = wt % ncb;
+        const int j0 = jb * 32 + jg, c0 = cb * 16 + cg;
+        const int rb = sp * rows_per_split, re = rb + rows_per_split;
+        f2_t acc[4][4], sb[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            sb[i] = 0ull;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) acc[i][q] = 0ull;
+        }
+        const f2_t one = f2_bcast(1.0f);
+#pragma unroll 2
+        for (int r = rb; r < re; r += 4) {
+            ulonglong2 z[4], x[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) z[i] = *reinterpret_cast<const ulonglong2 *>(dz + (j0 + 8 * i) * kSR + r);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) x[q] = *reinterpret_cast<const ulonglong2 *>(ain + (c0 + 4 * q) * kSR + r);
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int q = 0; q < 4; ++q) f2_fma(acc[i][q], z[i].x, x[q].x);
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int q = 0; q < 4; ++q) f2_fma(acc[i][q], z[i].y, x[q].y);
+            if (cb == 0) {
+#pragma unroll
+                for (int i = 0; i < 4; ++i) f2_fma(sb[i], z[i].x, one);
+#pragma unroll
+                for (int i = 0; i < 4; ++i) f2_fma(sb[i], z[i].y, one);
+            }
+        }
+        float *gWs = gW + sp * split_stride;
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const float2 v = f2_unpack(acc[i][q]);
+                gWs[(j0 + 8 * i) * sw + c0 + 4 * q] = v.x + v.y;
+            }
+        if (cb == 0 && cg == 0) {
+            float *gbs = gb + sp * split_stride;
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const float2 v = f2_unpack(sb[i]);
+                gbs[j0 + 8 * i] = v.x + v.y;
+            }
+        }
+    }
+}
+
+}  // namespace noma_dev
