@@ -6,7 +6,7 @@
 // On-chip state for the whole training (never leaves the SM):
 //   * weights, biases, final layer      -- shared memory (FP32)
 //   * gradients (1-2 split partials)    -- shared memory (FP32)
-//   * Adam first/second moments         -- registers (NSLOT per thread)
+//   * Adam first/second moments         -- shared memory (registers if short)
 //   * minibatch input and activations   -- shared memory, feature-major
 // Per minibatch: gather the shuffled rows straight from the (L2-resident)
 // design -- the IQ-symmetry widening (iq_transform.cpp:17-20) is applied at
@@ -27,17 +27,24 @@
 
 namespace noma_dev {
 
-constexpr int kTrainThreads = 512;
-constexpr int kTrainWarps = kTrainThreads / 32;
 constexpr int kMaxSplit = 2;  // weight-gradient split-K partials
 
+// Two CTA shapes: 16 warps with 4x4 FFMA2 tiles (one net per SM: large nets)
+// and 8 warps with 8x4 FFMA2 tiles (two nets per SM when they fit: small
+// nets); the tile width picks the final-layer partial block (16 / 32 j).
+template <int NT>
+__host__ __device__ constexpr int yp_block() { return NT == 512 ? 16 : 32; }
+
+template <int NT>
 __host__ __device__ inline int grad_splits(int J, int C, int max_split) {
-    const int tiles = (J >> 5) * (C >> 4);
-    return tiles < kTrainWarps ? max_split : 1;
+    const int tiles = NT == 512 ? (J >> 5) * (C >> 4) : (J >> 5) * (C >> 5);
+    return tiles < NT / 32 ? max_split : 1;
 }
 
-template <int NSLOT, int MINB>
-__global__ void __launch_bounds__(kTrainThreads, MINB) train_kernel(TrainParams p) {
+template <int NT, int NSLOT, int MINB>
+__global__ void __launch_bounds__(NT, MINB) train_kernel(TrainParams p) {
+    constexpr int kTrainThreads = NT;
+    constexpr int kTrainWarps = NT / 32;
     extern __shared__ __align__(16) float sm[];
     const int net = blockIdx.x;
     if (p.status && p.status[net] != NOMA_OK) return;
@@ -76,7 +83,7 @@ __global__ void __launch_bounds__(kTrainThreads, MINB) train_kernel(TrainParams 
     const int width = p.width, M = width / 2;
     const bool vec4 = (width & 3) == 0 && (M & 3) == 0;
     const int fpN = g.fp[N];
-    const int njb = fpN >> 4;  // final-layer partial blocks (16 j each)
+    const int njb = fpN / yp_block<NT>();  // final-layer partial blocks
     float *AN = N ? sm + p.off_a[N] : XT;
     float loss_acc = 0.0f;     // per-row-thread partial of the epoch loss
     long step = 0;
@@ -84,8 +91,9 @@ __global__ void __launch_bounds__(kTrainThreads, MINB) train_kernel(TrainParams 
         const uint16_t *perm = p.perm + ((size_t)net * p.epochs + e) * n;
         for (int start = 0; start < n; start += p.batch) {
             const int bsz = min(p.batch, n - start);
-            // ---- gather (IQ widening at load): 4 threads per batch row ------
+            // ---- gather (IQ widening at load): NT/128 threads per batch row -
             {
+                constexpr int TPR = NT / kBatchRows;
                 const int r = tid & (kBatchRows - 1), h = tid >> 7;
                 if (r < bsz) {
                     const int idx = perm[start + r];
@@ -95,7 +103,7 @@ __global__ void __launch_bounds__(kTrainThreads, MINB) train_kernel(TrainParams 
                                            : p.design32 + ((size_t)d * n + idx) * width;
                     const bool odd = wid && (idx & 1);
                     if (vec4) {
-                        for (int c = h * 4; c < width; c += 16) {
+                        for (int c = h * 4; c < width; c += 4 * TPR) {
                             float4 v;
                             if (!odd) {
                                 v = *reinterpret_cast<const float4 *>(src + c);
@@ -111,12 +119,12 @@ __global__ void __launch_bounds__(kTrainThreads, MINB) train_kernel(TrainParams 
                             XT[(c + 3) * kSR + r] = v.w;
                         }
                     } else {
-                        for (int c = h; c < width; c += 4)
+                        for (int c = h; c < width; c += TPR)
                             XT[c * kSR + r] = !odd ? src[c] : (c < M ? src[M + c] : -src[c - M]);
                     }
                 } else {
                     if (h == 0) r0b[r] = 0.0f;
-                    for (int c = h; c < width; c += 4) XT[c * kSR + r] = 0.0f;
+                    for (int c = h; c < width; c += TPR) XT[c * kSR + r] = 0.0f;
                 }
                 if (tid == kTrainThreads - 1) {  // Adam constants for this step (FP64 pow)
                     const double c1 = 1.0 - pow(p.b1d, (double)(step + 1));
@@ -128,10 +136,17 @@ __global__ void __launch_bounds__(kTrainThreads, MINB) train_kernel(TrainParams 
             __syncthreads();
             // ---- forward (hybrid_nn.cpp:60-72); last layer also forms yp -----
             for (int l = 1; l <= N; ++l) {
-                tile_forward44<kTrainWarps>(PS + g.pw[l], g.sw[l], PS + g.pb[l],
-                                          l == 1 ? XT : sm + p.off_a[l - 1], sm + p.off_a[l],
-                                          g.fp[l], g.fp[l - 1], warp, lane,
-                                          l == N ? PS + g.pf : nullptr, l == N ? yp : nullptr);
+                const float *ain = l == 1 ? XT : sm + p.off_a[l - 1];
+                const float *wfp = l == N ? PS + g.pf : nullptr;
+                float *ypp = l == N ? yp : nullptr;
+                if constexpr (NT == 512)
+                    tile_forward44<kTrainWarps>(PS + g.pw[l], g.sw[l], PS + g.pb[l], ain,
+                                                sm + p.off_a[l], g.fp[l], g.fp[l - 1], warp, lane,
+                                                wfp, ypp);
+                else
+                    tile_forward<kTrainWarps>(PS + g.pw[l], g.sw[l], PS + g.pb[l], ain,
+                                              sm + p.off_a[l], g.fp[l], g.fp[l - 1], warp, lane,
+                                              wfp, ypp);
                 __syncthreads();
             }
             // ---- residual a_N w - r0, dy = 2 r / B (hybrid_nn.cpp:94-98) ------
@@ -178,15 +193,25 @@ __global__ void __launch_bounds__(kTrainThreads, MINB) train_kernel(TrainParams 
             // ---- backward (hybrid_nn.cpp:105-112) ----------------------------
             for (int l = N; l >= 1; --l) {
                 const float *ain = l == 1 ? XT : sm + p.off_a[l - 1];
-                tile_weight_grad44<kTrainWarps>(sm + p.off_a[l], ain, GS + g.pw[l], g.sw[l],
-                                              GS + g.pb[l], g.fp[l], g.fp[l - 1],
-                                              grad_splits(g.fp[l], g.fp[l - 1], p.gsplit), gstride, warp,
-                                              lane);
+                const int splits = grad_splits<NT>(g.fp[l], g.fp[l - 1], p.gsplit);
+                if constexpr (NT == 512)
+                    tile_weight_grad44<kTrainWarps>(sm + p.off_a[l], ain, GS + g.pw[l], g.sw[l],
+                                                    GS + g.pb[l], g.fp[l], g.fp[l - 1], splits,
+                                                    gstride, warp, lane);
+                else
+                    tile_weight_grad<kTrainWarps>(sm + p.off_a[l], ain, GS + g.pw[l], g.sw[l],
+                                                  GS + g.pb[l], g.fp[l], g.fp[l - 1], splits,
+                                                  gstride, warp, lane);
                 __syncthreads();
                 if (l > 1) {
-                    tile_backward_data44<kTrainWarps>(PS + g.pw[l], g.sw[l], sm + p.off_a[l],
-                                                    sm + p.off_a[l - 1], g.fp[l - 1], g.fp[l],
-                                                    warp, lane);
+                    if constexpr (NT == 512)
+                        tile_backward_data44<kTrainWarps>(PS + g.pw[l], g.sw[l], sm + p.off_a[l],
+                                                          sm + p.off_a[l - 1], g.fp[l - 1],
+                                                          g.fp[l], warp, lane);
+                    else
+                        tile_backward_data<kTrainWarps>(PS + g.pw[l], g.sw[l], sm + p.off_a[l],
+                                                        sm + p.off_a[l - 1], g.fp[l - 1], g.fp[l],
+                                                        warp, lane);
                     __syncthreads();
                 }
             }
@@ -290,25 +315,21 @@ int train_launch(TrainParams &p, cudaStream_t st) {
     p.off_end = off;
     const size_t smem = (size_t)off * sizeof(float);
     if (smem > 227 * 1024) return NOMA_ERR_UNSUPPORTED;
-    const int need = (g.ptotal + kTrainThreads - 1) / kTrainThreads;
-    // two CTAs (nets) per SM when shared memory and the 128-register cap allow
-    const bool two = smem <= 112 * 1024 && need <= 16;
-#define NOMA_TRAIN_LAUNCH(NS, MB)                                                               \
+    const int need = (g.ptotal + 511) / 512;
+#define NOMA_TRAIN_LAUNCH(NT, NS, MB)                                                           \
     {                                                                                           \
-        cudaFuncSetAttribute(train_kernel<NS, MB>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
-                             (int)smem);                                                        \
-        train_kernel<NS, MB><<<p.n_nets, kTrainThreads, smem, st>>>(p);                         \
+        cudaFuncSetAttribute(train_kernel<NT, NS, MB>,                                          \
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);           \
+        train_kernel<NT, NS, MB><<<p.n_nets, NT, smem, st>>>(p);                                \
         return cudaGetLastError() == cudaSuccess ? NOMA_OK : NOMA_ERR_CUDA;                     \
     }
-    (void)two;
-    if (mom_smem) NOMA_TRAIN_LAUNCH(0, 1)
-    if (need <= 8) NOMA_TRAIN_LAUNCH(8, 1)
-    if (need <= 16) NOMA_TRAIN_LAUNCH(16, 1)
-    if (need <= 24) NOMA_TRAIN_LAUNCH(24, 1)
-    if (need <= 28) NOMA_TRAIN_LAUNCH(28, 1)
-    if (need <= 32) NOMA_TRAIN_LAUNCH(32, 1)
-    if (need <= 48) NOMA_TRAIN_LAUNCH(48, 1)
-    if (need <= 64) NOMA_TRAIN_LAUNCH(64, 1)
+    // small nets: two 8-warp CTAs (two nets) per SM; else one 16-warp CTA
+    if (mom_smem && smem <= 112 * 1024) NOMA_TRAIN_LAUNCH(256, 0, 2)
+    if (mom_smem) NOMA_TRAIN_LAUNCH(512, 0, 1)
+    if (need <= 8) NOMA_TRAIN_LAUNCH(512, 8, 1)
+    if (need <= 16) NOMA_TRAIN_LAUNCH(512, 16, 1)
+    if (need <= 24) NOMA_TRAIN_LAUNCH(512, 24, 1)
+    if (need <= 32) NOMA_TRAIN_LAUNCH(512, 32, 1)
 #undef NOMA_TRAIN_LAUNCH
     return NOMA_ERR_UNSUPPORTED;
 }
