@@ -1,5 +1,7 @@
 // C-ABI (include/noma_cuda.h): context, staging and the batched entry points.
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -251,6 +253,7 @@ int check_cfg(noma_ctx_t c, const noma_train_cfg *cfg) {
 
 void fill_train(TrainParams &tp, const NetGeom &g, const noma_train_cfg *cfg) {
     tp.g = g;
+    tp.clocks = nullptr;
     tp.epochs = cfg->epochs;
     tp.batch = cfg->batch_size;
     tp.lr = (float)cfg->lr;
@@ -722,9 +725,18 @@ NOMA_API int noma_pipeline(noma_ctx_t c, const noma_net_desc *desc, const noma_t
         tp.plans = dp;
         tp.trace = dt;
         tp.status = dst;
+        const bool clocks = std::getenv("NOMA_PHASE_CLOCKS") != nullptr;
+        if (clocks) tp.clocks = s.scratch<long long>(8);
         st = train_launch(tp, c->stream);
         if (st) return st == NOMA_ERR_CUDA ? cuda_fail(c, "train") : fail(c, st, "train: unsupported network shape");
         c->launches += 1;
+        if (clocks) {  // instrumentation only: per-phase cycles of net 0
+            long long h[6];
+            cudaMemcpyAsync(h, tp.clocks, sizeof(h), cudaMemcpyDeviceToHost, c->stream);
+            cudaStreamSynchronize(c->stream);
+            std::fprintf(stderr, "NOMA_PHASE_CLOCKS gather %lld forward %lld residual %lld final %lld backward %lld adam %lld\n",
+                         h[0], h[1], h[2], h[3], h[4], h[5]);
+        }
     }
     mark(c, 6);
     if (ND > 0) {

@@ -61,6 +61,15 @@ __global__ void __launch_bounds__(NT, MINB) train_kernel(TrainParams p) {
     float *red = sm + p.off_red;    // 128 floats: epoch loss reduction
     float *misc = sm + p.off_misc;  // [0] lr/corr1, [1] 1/corr2
     float *yp = sm + p.off_yp;      // [fp_N/32][128] final-layer partials
+    // optional phase-cycle instrumentation (block 0, thread 0; NOMA_PHASE_CLOCKS)
+    const bool clk_on = p.clocks && blockIdx.x == 0 && threadIdx.x == 0;
+    long long clk_acc[6] = {0, 0, 0, 0, 0, 0}, clk_prev = clk_on ? clock64() : 0;
+#define NOMA_PHASE(I)                                \
+    if (clk_on) {                                    \
+        const long long now = clock64();             \
+        clk_acc[I] += now - clk_prev;                \
+        clk_prev = now;                              \
+    }
 
     for (int i = tid; i < p.off_end; i += kTrainThreads) sm[i] = 0.0f;
     __syncthreads();
@@ -91,6 +100,7 @@ __global__ void __launch_bounds__(NT, MINB) train_kernel(TrainParams p) {
         const uint16_t *perm = p.perm + ((size_t)net * p.epochs + e) * n;
         for (int start = 0; start < n; start += p.batch) {
             const int bsz = min(p.batch, n - start);
+            NOMA_PHASE(5)
             // ---- gather (IQ widening at load): NT/128 threads per batch row -
             {
                 constexpr int TPR = NT / kBatchRows;
@@ -134,6 +144,7 @@ __global__ void __launch_bounds__(NT, MINB) train_kernel(TrainParams p) {
                 }
             }
             __syncthreads();
+            NOMA_PHASE(0)
             // ---- forward (hybrid_nn.cpp:60-72); last layer also forms yp -----
             for (int l = 1; l <= N; ++l) {
                 const float *ain = l == 1 ? XT : sm + p.off_a[l - 1];
@@ -149,6 +160,7 @@ __global__ void __launch_bounds__(NT, MINB) train_kernel(TrainParams p) {
                                               wfp, ypp);
                 __syncthreads();
             }
+            NOMA_PHASE(1)
             // ---- residual a_N w - r0, dy = 2 r / B (hybrid_nn.cpp:94-98) ------
             if (tid < kBatchRows) {
                 float yhat = 0.0f;
@@ -163,6 +175,7 @@ __global__ void __launch_bounds__(NT, MINB) train_kernel(TrainParams p) {
                 loss_acc = fmaf(res, res, loss_acc);
             }
             __syncthreads();
+            NOMA_PHASE(2)
             // ---- final layer gradient and dZ_N (hybrid_nn.cpp:99-107) --------
             {
                 const float *wf = PS + g.pf;
@@ -190,6 +203,7 @@ __global__ void __launch_bounds__(NT, MINB) train_kernel(TrainParams p) {
                 }
             }
             __syncthreads();
+            NOMA_PHASE(3)
             // ---- backward (hybrid_nn.cpp:105-112) ----------------------------
             for (int l = N; l >= 1; --l) {
                 const float *ain = l == 1 ? XT : sm + p.off_a[l - 1];
@@ -215,6 +229,7 @@ __global__ void __launch_bounds__(NT, MINB) train_kernel(TrainParams p) {
                     __syncthreads();
                 }
             }
+            NOMA_PHASE(4)
             // ---- Adam (hybrid_nn.cpp:118-144): FP32 moments, registers or smem
             {
                 const float lrc = misc[0], ic2 = misc[1];
@@ -255,6 +270,10 @@ __global__ void __launch_bounds__(NT, MINB) train_kernel(TrainParams p) {
             p.trace[(size_t)net * p.epochs + e] = s / (double)n;
         }
     }
+    NOMA_PHASE(5)
+    if (clk_on)
+        for (int i = 0; i < 6; ++i) p.clocks[i] = clk_acc[i];
+#undef NOMA_PHASE
     // ---- write the trained parameters back in FusedPlan layout -------------
     float *po = p.plans + (size_t)net * g.plan_total;
     for (int l = 1; l <= N; ++l) {
@@ -324,7 +343,8 @@ int train_launch(TrainParams &p, cudaStream_t st) {
         return cudaGetLastError() == cudaSuccess ? NOMA_OK : NOMA_ERR_CUDA;                     \
     }
     // small nets: two 8-warp CTAs (two nets) per SM; else one 16-warp CTA
-    if (mom_smem && smem <= 112 * 1024) NOMA_TRAIN_LAUNCH(256, 0, 2)
+    // (the 2-per-SM shape only pays when there are more nets than SMs)
+    if (mom_smem && smem <= 112 * 1024 && p.n_nets > 148) NOMA_TRAIN_LAUNCH(256, 0, 2)
     if (mom_smem) NOMA_TRAIN_LAUNCH(512, 0, 1)
     if (need <= 8) NOMA_TRAIN_LAUNCH(512, 8, 1)
     if (need <= 16) NOMA_TRAIN_LAUNCH(512, 16, 1)

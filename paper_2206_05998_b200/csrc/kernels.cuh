@@ -32,6 +32,7 @@ struct TrainParams {
     // shared-memory carve-up (floats)
     int off_x, off_a[NOMA_MAX_DIMS], off_ps, off_gs, off_r0b, off_dy, off_red, off_yp, off_misc,
         off_end, gs_stride, gsplit, off_mom;
+    long long *clocks;      // nullable: phase cycles of block 0 (NOMA_PHASE_CLOCKS)
 };
 
 struct TrainF64Params {
