@@ -21,9 +21,13 @@
 // This is the reference loss exactly (residual = x w0 + a_N w - y,
 // hybrid_nn.cpp:94) without the FP32 cancellation of x w0 - y.
 #include <math.h>
+#include <cstdlib>
 
 #include "kernels.cuh"
 #include "tiles.cuh"
+
+#include <cooperative_groups.h>
+namespace cg = cooperative_groups;
 
 namespace noma_dev {
 
@@ -41,12 +45,21 @@ __host__ __device__ inline int grad_splits(int J, int C, int max_split) {
     return tiles < NT / 32 ? max_split : 1;
 }
 
-template <int NT, int NSLOT, int MINB>
+// CS > 1: latency mode -- a thread-block cluster of CS CTAs trains one net.
+// CTA `rank` owns minibatch rows [rank*RB, (rank+1)*RB), RB = 128/CS; each
+// step the CTAs' weight-gradient partials are reduce-scattered through
+// distributed shared memory (fixed summation order: deterministic), every CTA
+// runs Adam on its 1/CS parameter slice and pushes the updated slice into all
+// CTAs' weight copies, bracketed by two cluster barriers.
+template <int NT, int NSLOT, int MINB, int CS>
 __global__ void __launch_bounds__(NT, MINB) train_kernel(TrainParams p) {
     constexpr int kTrainThreads = NT;
     constexpr int kTrainWarps = NT / 32;
+    constexpr int RB = kBatchRows / CS;  // minibatch rows per CTA
     extern __shared__ __align__(16) float sm[];
-    const int net = blockIdx.x;
+    cg::cluster_group cluster = cg::this_cluster();
+    const int rank = CS > 1 ? (int)cluster.block_rank() : 0;
+    const int net = blockIdx.x / CS;
     if (p.status && p.status[net] != NOMA_OK) return;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const NetGeom &g = p.g;
@@ -105,8 +118,9 @@ __global__ void __launch_bounds__(NT, MINB) train_kernel(TrainParams p) {
             {
                 constexpr int TPR = NT / kBatchRows;
                 const int r = tid & (kBatchRows - 1), h = tid >> 7;
-                if (r < bsz) {
-                    const int idx = perm[start + r];
+                const int rg = rank * RB + r;  // row of the minibatch (CS > 1: r < RB local)
+                if (r < RB && rg < bsz) {
+                    const int idx = perm[start + rg];
                     if (h == 0) r0b[r] = p.r0[(size_t)net * n + idx];
                     const bool wid = p.layout == NOMA_LAYOUT_WIDEN_COMPLEX;
                     const float *src = wid ? p.design32 + ((size_t)d * (n >> 1) + (idx >> 1)) * width
@@ -153,7 +167,7 @@ __global__ void __launch_bounds__(NT, MINB) train_kernel(TrainParams p) {
                 if constexpr (NT == 512)
                     tile_forward44<kTrainWarps>(PS + g.pw[l], g.sw[l], PS + g.pb[l], ain,
                                                 sm + p.off_a[l], g.fp[l], g.fp[l - 1], warp, lane,
-                                                wfp, ypp);
+                                                wfp, ypp, RB);
                 else
                     tile_forward<kTrainWarps>(PS + g.pw[l], g.sw[l], PS + g.pb[l], ain,
                                               sm + p.off_a[l], g.fp[l], g.fp[l - 1], warp, lane,
@@ -170,7 +184,7 @@ __global__ void __launch_bounds__(NT, MINB) train_kernel(TrainParams p) {
                     const float *wf = PS + g.pf;
                     for (int j = 0; j < fpN; ++j) yhat = fmaf(XT[j * kSR + tid], wf[j], yhat);
                 }
-                const float res = tid < bsz ? yhat - r0b[tid] : 0.0f;
+                const float res = (tid < RB && rank * RB + tid < bsz) ? yhat - r0b[tid] : 0.0f;
                 dy[tid] = (2.0f / (float)bsz) * res;
                 loss_acc = fmaf(res, res, loss_acc);
             }
@@ -211,7 +225,7 @@ __global__ void __launch_bounds__(NT, MINB) train_kernel(TrainParams p) {
                 if constexpr (NT == 512)
                     tile_weight_grad44<kTrainWarps>(sm + p.off_a[l], ain, GS + g.pw[l], g.sw[l],
                                                     GS + g.pb[l], g.fp[l], g.fp[l - 1], splits,
-                                                    gstride, warp, lane);
+                                                    gstride, warp, lane, RB);
                 else
                     tile_weight_grad<kTrainWarps>(sm + p.off_a[l], ain, GS + g.pw[l], g.sw[l],
                                                   GS + g.pb[l], g.fp[l], g.fp[l - 1], splits,
@@ -221,7 +235,7 @@ __global__ void __launch_bounds__(NT, MINB) train_kernel(TrainParams p) {
                     if constexpr (NT == 512)
                         tile_backward_data44<kTrainWarps>(PS + g.pw[l], g.sw[l], sm + p.off_a[l],
                                                           sm + p.off_a[l - 1], g.fp[l - 1],
-                                                          g.fp[l], warp, lane);
+                                                          g.fp[l], warp, lane, RB);
                     else
                         tile_backward_data<kTrainWarps>(PS + g.pw[l], g.sw[l], sm + p.off_a[l],
                                                         sm + p.off_a[l - 1], g.fp[l - 1], g.fp[l],
@@ -233,7 +247,37 @@ __global__ void __launch_bounds__(NT, MINB) train_kernel(TrainParams p) {
             // ---- Adam (hybrid_nn.cpp:118-144): FP32 moments, registers or smem
             {
                 const float lrc = misc[0], ic2 = misc[1];
-                if constexpr (NSLOT > 0) {
+                if constexpr (CS > 1) {
+                    // reduce-scatter the CS gradient partials over DSMEM, Adam on
+                    // this CTA's slice, push the slice into every CTA's weights
+                    cluster.sync();
+                    float *M1 = sm + p.off_mom, *M2 = M1 + gstride;
+                    const int slice = pad_to((g.ptotal + CS - 1) / CS, 4);
+                    const int lo = rank * slice, hi = min(g.ptotal, lo + slice);
+                    const float *gsr[CS];
+                    float *psr[CS];
+#pragma unroll
+                    for (int q = 0; q < CS; ++q) {
+                        gsr[q] = cluster.map_shared_rank(GS, q);
+                        psr[q] = cluster.map_shared_rank(PS, q);
+                    }
+                    for (int i = lo + tid; i < hi; i += kTrainThreads) {
+                        float gi = 0.0f;
+#pragma unroll
+                        for (int q = 0; q < CS; ++q) {
+                            gi += gsr[q][i];
+                            if (p.gsplit > 1) gi += gsr[q][gstride + i];
+                        }
+                        const float m1 = p.b1 * M1[i] + p.omb1 * gi;
+                        const float m2 = p.b2 * M2[i] + p.omb2 * (gi * gi);
+                        M1[i] = m1;
+                        M2[i] = m2;
+                        const float th = PS[i] - __fdividef(lrc * m1, sqrtf(m2 * ic2) + p.eps);
+#pragma unroll
+                        for (int q = 0; q < CS; ++q) psr[q][i] = th;
+                    }
+                    cluster.sync();
+                } else if constexpr (NSLOT > 0) {
 #pragma unroll
                     for (int s = 0; s < NSLOT; ++s) {
                         const int i = tid + s * kTrainThreads;
@@ -263,11 +307,24 @@ __global__ void __launch_bounds__(NT, MINB) train_kernel(TrainParams p) {
         // ---- epoch loss (hybrid_nn.cpp:190-192): trace[e] = sum r^2 / n ------
         if (tid < kBatchRows) red[tid] = loss_acc;
         loss_acc = 0.0f;
-        __syncthreads();
-        if (tid == 0 && p.trace) {
-            double s = 0.0;
-            for (int i = 0; i < kBatchRows; ++i) s += red[i];
-            p.trace[(size_t)net * p.epochs + e] = s / (double)n;
+        if constexpr (CS > 1) {
+            cluster.sync();
+            if (rank == 0 && tid == 0 && p.trace) {
+                double s = 0.0;
+                for (int q = 0; q < CS; ++q) {
+                    const float *rq = cluster.map_shared_rank(red, q);
+                    for (int i = 0; i < RB; ++i) s += rq[i];
+                }
+                p.trace[(size_t)net * p.epochs + e] = s / (double)n;
+            }
+            cluster.sync();
+        } else {
+            __syncthreads();
+            if (tid == 0 && p.trace) {
+                double s = 0.0;
+                for (int i = 0; i < kBatchRows; ++i) s += red[i];
+                p.trace[(size_t)net * p.epochs + e] = s / (double)n;
+            }
         }
     }
     NOMA_PHASE(5)
@@ -275,6 +332,7 @@ __global__ void __launch_bounds__(NT, MINB) train_kernel(TrainParams p) {
         for (int i = 0; i < 6; ++i) p.clocks[i] = clk_acc[i];
 #undef NOMA_PHASE
     // ---- write the trained parameters back in FusedPlan layout -------------
+    if (CS > 1 && rank != 0) return;  // every CTA of the cluster holds the same weights
     float *po = p.plans + (size_t)net * g.plan_total;
     for (int l = 1; l <= N; ++l) {
         const int rowsl = g.dims[l], cols = g.dims[l - 1];
@@ -337,10 +395,41 @@ int train_launch(TrainParams &p, cudaStream_t st) {
     const int need = (g.ptotal + 511) / 512;
 #define NOMA_TRAIN_LAUNCH(NT, NS, MB)                                                           \
     {                                                                                           \
-        cudaFuncSetAttribute(train_kernel<NT, NS, MB>,                                          \
+        cudaFuncSetAttribute(train_kernel<NT, NS, MB, 1>,                                       \
                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);           \
-        train_kernel<NT, NS, MB><<<p.n_nets, NT, smem, st>>>(p);                                \
+        train_kernel<NT, NS, MB, 1><<<p.n_nets, NT, smem, st>>>(p);                             \
         return cudaGetLastError() == cudaSuccess ? NOMA_OK : NOMA_ERR_CUDA;                     \
+    }
+    // latency mode: fewer nets than SMs -> a cluster of CS CTAs per net
+    int sms = 148;
+    {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    }
+    int cs = !mom_smem ? 1 : p.n_nets * 4 <= sms ? 4 : p.n_nets * 2 <= sms ? 2 : 1;
+    if (const char *force = std::getenv("NOMA_TRAIN_CLUSTER"))  // A/B testing: 1, 2 or 4
+        cs = mom_smem && (std::atoi(force) == 2 || std::atoi(force) == 4) ? std::atoi(force) : 1;
+    if (cs > 1) {
+        auto launch = [&](auto kern) {
+            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            cudaLaunchConfig_t cfg = {};
+            cfg.gridDim = dim3(p.n_nets * cs);
+            cfg.blockDim = dim3(512);
+            cfg.dynamicSmemBytes = smem;
+            cfg.stream = st;
+            cudaLaunchAttribute attr[1];
+            attr[0].id = cudaLaunchAttributeClusterDimension;
+            attr[0].val.clusterDim.x = cs;
+            attr[0].val.clusterDim.y = 1;
+            attr[0].val.clusterDim.z = 1;
+            cfg.attrs = attr;
+            cfg.numAttrs = 1;
+            return cudaLaunchKernelEx(&cfg, kern, p) == cudaSuccess;
+        };
+        const bool ok = cs == 4 ? launch(train_kernel<512, 0, 1, 4>) : launch(train_kernel<512, 0, 1, 2>);
+        if (ok) return NOMA_OK;
+        cudaGetLastError();  // cluster launch refused: fall through to one CTA per net
     }
     // small nets: two 8-warp CTAs (two nets) per SM; else one 16-warp CTA
     // (the 2-per-SM shape only pays when there are more nets than SMs)

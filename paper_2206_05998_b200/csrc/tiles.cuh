@@ -258,13 +258,15 @@ __device__ __forceinline__ void tile_forward44(const float *__restrict__ W, int 
                                                const float *__restrict__ in,
                                                float *__restrict__ out, int J, int Kin, int warp,
                                                int lane, const float *__restrict__ wf = nullptr,
-                                               float *__restrict__ yp = nullptr) {
+                                               float *__restrict__ yp = nullptr,
+                                               int R = kBatchRows) {
     const int rg = lane & 7, jg = lane >> 3;
-    const int ntile = (J >> 4) * 4;
+    const int nrb = R >> 5;  // 32-row blocks (R % 32 == 0)
+    const int ntile = (J >> 4) * nrb;
     for (int wt = warp; wt < ntile; wt += NW) {
-        const int jb = wt >> 2;
+        const int jb = wt / nrb;
         const int j0 = jb * 16 + jg;
-        const int r0 = (wt & 3) * 32 + 4 * rg;
+        const int r0 = (wt % nrb) * 32 + 4 * rg;
         f2_t acc[4][2];
 #pragma unroll
         for (int i = 0; i < 4; ++i) acc[i][0] = acc[i][1] = f2_bcast(bias[j0 + 4 * i]);
@@ -317,12 +319,13 @@ template <int NW>
 __device__ __forceinline__ void tile_backward_data44(const float *__restrict__ W, int sw,
                                                      const float *__restrict__ dz,
                                                      float *__restrict__ a, int C, int J,
-                                                     int warp, int lane) {
+                                                     int warp, int lane, int R = kBatchRows) {
     const int rg = lane & 7, cg = lane >> 3;
-    const int ntile = (C >> 4) * 4;
+    const int nrb = R >> 5;
+    const int ntile = (C >> 4) * nrb;
     for (int wt = warp; wt < ntile; wt += NW) {
-        const int c0 = (wt >> 2) * 16 + 4 * cg;
-        const int r0 = (wt & 3) * 32 + 4 * rg;
+        const int c0 = (wt / nrb) * 16 + 4 * cg;
+        const int r0 = (wt % nrb) * 32 + 4 * rg;
         f2_t acc[4][2];
 #pragma unroll
         for (int i = 0; i < 4; ++i) acc[i][0] = acc[i][1] = 0ull;
@@ -359,11 +362,11 @@ __device__ __forceinline__ void tile_weight_grad44(const float *__restrict__ dz,
                                                    float *__restrict__ gW, int sw,
                                                    float *__restrict__ gb, int J, int C,
                                                    int splits, int split_stride, int warp,
-                                                   int lane) {
+                                                   int lane, int R = kBatchRows) {
     const int jg = lane & 7, cg = lane >> 3;
     const int ncb = C >> 4;
     const int ntile = (J >> 5) * ncb;
-    const int rows_per_split = kBatchRows / splits;
+    const int rows_per_split = R / splits;
     for (int task = warp; task < ntile * splits; task += NW) {
         const int wt = task / splits, sp = task % splits;
         const int jb = wt / ncb, cb = wt % ncb;

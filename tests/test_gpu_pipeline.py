@@ -115,3 +115,27 @@ def test_large_detect_self_consistent(A, O):
     ref = O.narrow_predictions(R.reference_forward(onet.dims, onet.w0, layers, final,
                                                    O.widen_design(sy.data_rx[0][sl])))
     assert np.max(np.abs(soft[sl] - ref)) / max(1.0, np.max(np.abs(ref))) < 1e-5
+
+
+@pytest.mark.parametrize("mode", ["1", "2", "4"])
+def test_train_modes_agree(A, O, mode, monkeypatch):
+    """The one-CTA-per-net kernel (throughput mode) and the cluster kernels
+    (latency mode: 2 or 4 CTAs per net, gradients reduced over DSMEM) follow
+    the FP64 oracle for short trainings; >74 nets also exercise the
+    many-nets launch path."""
+    monkeypatch.setenv("NOMA_TRAIN_CLUSTER", mode)
+    sc = O.Scenario(num_users=6, num_antennas=4, train_symbols=64, data_symbols=128,
+                    power_step_db=3.0, snr_db=20.0, rx_nonlinearity_gain=0.05)
+    S = 13  # 78 nets
+    seeds = [2000 + s for s in range(S)]
+    recs = [O.synthesize(sc, O.seed_bundle(s)) for s in seeds]
+    ref = O.run_slots(sc, [16, 16], seeds, epochs=3, threads=8)
+    init, shuf = _seeds(O, seeds, 6)
+    out = A.pipeline([8, 16, 16], np.stack([r.train_rx for r in recs]),
+                     np.stack([r.train_symbols for r in recs]), np.stack([r.data_rx for r in recs]),
+                     np.stack([A.codes_of(r.data_symbols) for r in recs]), init, shuf, epochs=3)
+    assert (out.status == 0).all()
+    soft_dev = np.max(np.abs(out.soft - ref.soft)) / max(1.0, np.max(np.abs(ref.soft)))
+    trace_dev = float(np.max(np.abs(out.trace - ref.trace) / np.abs(ref.trace)))
+    record("train_modes", config=f"cluster={mode}", soft_dev=soft_dev, trace_dev=trace_dev)
+    assert soft_dev < 1e-4 and trace_dev < 1e-4
