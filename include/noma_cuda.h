@@ -114,6 +114,12 @@ NOMA_API int noma_ctx_set_stream(noma_ctx_t ctx, void *cuda_stream);
 NOMA_API int noma_ctx_synchronize(noma_ctx_t ctx);
 /* Number of kernels this context has launched (instrumentation). */
 NOMA_API long long noma_ctx_kernel_launches(noma_ctx_t ctx);
+/* Which training kernel the last noma_train / noma_pipeline call launched:
+ * 1 = one CTA per net (16 warps), 2 = two 8-warp CTAs per SM,
+ * 10 + c = row-split cluster of c CTAs per net (DSMEM gradient reduce),
+ * 100 + c = neuron-split latency cluster of c CTAs per net (k_train_lat.cu),
+ * 0 = none yet. */
+NOMA_API int noma_ctx_train_mode(noma_ctx_t ctx);
 /* Instrumentation: when on, noma_pipeline records CUDA events around its
  * phases (init and shuffles run on a side stream, overlapping the LLS);
  * noma_ctx_phase_ms waits for the last call and returns ms for

@@ -113,6 +113,7 @@ struct noma_ctx_s {
     cudaStream_t stream = nullptr;
     std::string err;
     long long launches = 0;
+    int train_mode = 0;
     bool profiling = false;
     // [0] start, [1] after LLS, [2] side start, [3] after init, [4] after
     // shuffles (side stream), [5] joined, [6] after train, [7] after detect
@@ -254,6 +255,7 @@ int check_cfg(noma_ctx_t c, const noma_train_cfg *cfg) {
 void fill_train(TrainParams &tp, const NetGeom &g, const noma_train_cfg *cfg) {
     tp.g = g;
     tp.clocks = nullptr;
+    tp.mode = 0;
     tp.epochs = cfg->epochs;
     tp.batch = cfg->batch_size;
     tp.lr = (float)cfg->lr;
@@ -329,6 +331,8 @@ NOMA_API int noma_ctx_synchronize(noma_ctx_t c) {
 }
 
 NOMA_API long long noma_ctx_kernel_launches(noma_ctx_t c) { return c ? c->launches : 0; }
+
+NOMA_API int noma_ctx_train_mode(noma_ctx_t c) { return c ? c->train_mode : 0; }
 
 NOMA_API int noma_ctx_set_profiling(noma_ctx_t c, int on) {
     if (!c) return NOMA_ERR_ARGUMENT;
@@ -543,6 +547,7 @@ NOMA_API int noma_train(noma_ctx_t c, const noma_dataset *ds, const noma_net_des
     tp.status = dst;
     if (cfg->epochs > 0) {
         st = train_launch(tp, c->stream);
+        c->train_mode = tp.mode;
         if (st) return st == NOMA_ERR_CUDA ? cuda_fail(c, "train") : fail(c, st, "train: unsupported network shape");
     }
     c->launches += 3;
@@ -728,6 +733,7 @@ NOMA_API int noma_pipeline(noma_ctx_t c, const noma_net_desc *desc, const noma_t
         const bool clocks = std::getenv("NOMA_PHASE_CLOCKS") != nullptr;
         if (clocks) tp.clocks = s.scratch<long long>(8);
         st = train_launch(tp, c->stream);
+        c->train_mode = tp.mode;
         if (st) return st == NOMA_ERR_CUDA ? cuda_fail(c, "train") : fail(c, st, "train: unsupported network shape");
         c->launches += 1;
         if (clocks) {  // instrumentation only: per-phase cycles of net 0

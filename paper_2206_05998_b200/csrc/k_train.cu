@@ -397,10 +397,21 @@ int train_launch(TrainParams &p, cudaStream_t st) {
     {                                                                                           \
         cudaFuncSetAttribute(train_kernel<NT, NS, MB, 1>,                                       \
                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);           \
+        p.mode = NT == 256 ? 2 : 1;                                                             \
         train_kernel<NT, NS, MB, 1><<<p.n_nets, NT, smem, st>>>(p);                             \
         return cudaGetLastError() == cudaSuccess ? NOMA_OK : NOMA_ERR_CUDA;                     \
     }
-    // latency mode: fewer nets than SMs -> a cluster of CS CTAs per net
+    // latency mode (few nets, e.g. one slot): a neuron-split cluster per net
+    // (k_train_lat.cu); NOMA_LAT_CLUSTER=1 disables it for A/B runs.
+    {
+        int sms_l = 148, dev_l = 0;
+        cudaGetDevice(&dev_l);
+        cudaDeviceGetAttribute(&sms_l, cudaDevAttrMultiProcessorCount, dev_l);
+        if (p.n_nets * 2 <= sms_l || std::getenv("NOMA_LAT_CLUSTER")) {
+            if (train_lat_launch(p, st) == NOMA_OK) return NOMA_OK;
+        }
+    }
+    // row-split cluster: fewer nets than SMs -> a cluster of CS CTAs per net
     int sms = 148;
     {
         int dev = 0;
@@ -428,7 +439,10 @@ int train_launch(TrainParams &p, cudaStream_t st) {
             return cudaLaunchKernelEx(&cfg, kern, p) == cudaSuccess;
         };
         const bool ok = cs == 4 ? launch(train_kernel<512, 0, 1, 4>) : launch(train_kernel<512, 0, 1, 2>);
-        if (ok) return NOMA_OK;
+        if (ok) {
+            p.mode = 10 + cs;
+            return NOMA_OK;
+        }
         cudaGetLastError();  // cluster launch refused: fall through to one CTA per net
     }
     // small nets: two 8-warp CTAs (two nets) per SM; else one 16-warp CTA

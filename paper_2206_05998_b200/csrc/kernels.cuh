@@ -33,6 +33,7 @@ struct TrainParams {
     int off_x, off_a[NOMA_MAX_DIMS], off_ps, off_gs, off_r0b, off_dy, off_red, off_yp, off_misc,
         off_end, gs_stride, gsplit, off_mom;
     long long *clocks;      // nullable: phase cycles of block 0 (NOMA_PHASE_CLOCKS)
+    int mode;               // out: kernel shape launched (noma_ctx_train_mode codes)
 };
 
 struct TrainF64Params {
@@ -93,6 +94,7 @@ int init_state_launch(const NetGeom &g, int n_nets, uint64_t *states, const doub
 int lls_predict_launch(int layout, int S, int K, int rows, int width, const double *data,
                        const double *w0, double *out, cudaStream_t st);
 int train_launch(TrainParams &p, cudaStream_t st);
+int train_lat_launch(TrainParams &p, cudaStream_t st);
 int train_f64_launch(TrainF64Params &p, cudaStream_t st);
 int detect_launch(DetectParams &p, cudaStream_t st);
 int synth_launch(SynthParams p, double *noise_power_scratch, cudaStream_t st);

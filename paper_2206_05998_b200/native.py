@@ -26,7 +26,7 @@ EXPORTED = [
     "noma_plan_size", "noma_param_count", "noma_lls_fit", "noma_init_params", "noma_train",
     "noma_detect", "noma_pipeline", "noma_synthesize", "noma_ctx_set_profiling",
     "noma_ctx_phase_ms", "noma_measure_fp32_tflops", "noma_init_params_state",
-    "noma_lls_predict", "noma_train_f64",
+    "noma_lls_predict", "noma_train_f64", "noma_ctx_train_mode",
 ]
 PHASES = ("lls", "init", "shuffle", "train", "detect", "total")
 
@@ -113,6 +113,7 @@ def load():
     L.noma_ctx_synchronize.argtypes = [vp]
     L.noma_ctx_kernel_launches.restype = C.c_longlong
     L.noma_ctx_kernel_launches.argtypes = [vp]
+    L.noma_ctx_train_mode.argtypes = [vp]
     L.noma_plan_size.argtypes = [C.POINTER(NetDesc)]
     L.noma_param_count.argtypes = [C.POINTER(NetDesc)]
     L.noma_lls_fit.argtypes = [vp, C.POINTER(Dataset), vp, vp, vp, ip]
@@ -206,6 +207,11 @@ class Context:
     @property
     def kernel_launches(self) -> int:
         return self.L.noma_ctx_kernel_launches(self.h)
+
+    @property
+    def train_mode(self) -> int:
+        """Kernel shape of the last training launch (noma_ctx_train_mode)."""
+        return self.L.noma_ctx_train_mode(self.h)
 
     def set_profiling(self, on: bool):
         self._check(self.L.noma_ctx_set_profiling(self.h, 1 if on else 0))
