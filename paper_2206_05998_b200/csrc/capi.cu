@@ -732,16 +732,17 @@ NOMA_API int noma_pipeline(noma_ctx_t c, const noma_net_desc *desc, const noma_t
         tp.status = dst;
         const bool clocks = std::getenv("NOMA_PHASE_CLOCKS") != nullptr;
         if (clocks) tp.clocks = s.scratch<long long>(8);
+        if (clocks && tp.clocks) cudaMemsetAsync(tp.clocks, 0, 8 * sizeof(long long), c->stream);
         st = train_launch(tp, c->stream);
         c->train_mode = tp.mode;
         if (st) return st == NOMA_ERR_CUDA ? cuda_fail(c, "train") : fail(c, st, "train: unsupported network shape");
         c->launches += 1;
         if (clocks) {  // instrumentation only: per-phase cycles of net 0
-            long long h[6];
+            long long h[8] = {0, 0, 0, 0, 0, 0, 0, 0};
             cudaMemcpyAsync(h, tp.clocks, sizeof(h), cudaMemcpyDeviceToHost, c->stream);
             cudaStreamSynchronize(c->stream);
-            std::fprintf(stderr, "NOMA_PHASE_CLOCKS gather %lld forward %lld residual %lld final %lld backward %lld adam %lld\n",
-                         h[0], h[1], h[2], h[3], h[4], h[5]);
+            std::fprintf(stderr, "NOMA_PHASE_CLOCKS mode %d: %lld %lld %lld %lld %lld %lld %lld %lld\n",
+                         tp.mode, h[0], h[1], h[2], h[3], h[4], h[5], h[6], h[7]);
         }
     }
     mark(c, 6);

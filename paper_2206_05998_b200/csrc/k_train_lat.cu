@@ -27,6 +27,7 @@
 #include <math.h>
 
 #include <cstdlib>
+#include <type_traits>
 
 #include "kernels.cuh"
 #include "tiles.cuh"
@@ -36,7 +37,6 @@ namespace noma_dev {
 namespace {
 
 constexpr int kLT = 512;      // threads per CTA
-constexpr int kLatMaxV = 4;   // float4 per gather thread: input width <= 64
 
 __device__ __forceinline__ uint32_t s2u(const void *p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -83,43 +83,103 @@ __device__ __forceinline__ void ffma2(f2_t &d, f2_t a, f2_t b) { f2_fma(d, a, b)
 
 }  // namespace
 
-// Shared-memory carve-up (floats), identical on host and device.
+namespace {
+
+__device__ __forceinline__ void st_async2(uint32_t raddr, float a, float b, uint32_t rbar) {
+    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f32 [%0], {%1, %2}, [%3];" ::"r"(raddr),
+                 "f"(a), "f"(b), "r"(rbar)
+                 : "memory");
+}
+__device__ __forceinline__ void st_async1(uint32_t raddr, float a, uint32_t rbar) {
+    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.f32 [%0], %1, [%2];" ::"r"(raddr), "f"(a),
+                 "r"(rbar)
+                 : "memory");
+}
+// Send the first NV floats of v (NV = 1, 2 or 4, contiguous in the target).
+template <int NV>
+__device__ __forceinline__ void st_async_n(uint32_t raddr, const float *v, uint32_t rbar) {
+    if constexpr (NV == 4) st_async4(raddr, make_float4(v[0], v[1], v[2], v[3]), rbar);
+    else if constexpr (NV == 2) st_async2(raddr, v[0], v[1], rbar);
+    else st_async1(raddr, v[0], rbar);
+}
+template <int NV>
+__device__ __forceinline__ void sts_n(float *p, const float *v) {
+    if constexpr (NV == 4) *reinterpret_cast<float4 *>(p) = make_float4(v[0], v[1], v[2], v[3]);
+    else if constexpr (NV == 2) *reinterpret_cast<float2 *>(p) = make_float2(v[0], v[1]);
+    else *p = v[0];
+}
+
+// In-register reduce-scatter of V values (v[0..V)) over a group of LANES
+// lanes (aligned, xor offsets LANES/2 .. 1).  Halving rounds split the value
+// range on the lane bits from the top; once one value is left the remaining
+// rounds are xor sums.  Afterwards v[0 .. max(1, V/LANES)) hold the lane's
+// values: block (lane & (LANES-1)) of V/LANES values if V >= LANES, else the
+// full sum of value index (lane & (LANES-1)) >> log2(LANES/V), replicated on
+// LANES/V lanes.  Fixed summation tree: deterministic.
+template <int N, int V, int LANES>
+__device__ __forceinline__ void reduce_scatter(float (&v)[N], int lane) {
+    if constexpr (LANES > 1) {
+        constexpr int O = LANES / 2;
+        if constexpr (V > 1) {
+            const bool h = lane & O;
+#pragma unroll
+            for (int i = 0; i < V / 2; ++i) {
+                const float snd = h ? v[i] : v[i + V / 2];
+                const float keep = h ? v[i + V / 2] : v[i];
+                v[i] = keep + __shfl_xor_sync(0xffffffffu, snd, O);
+            }
+            reduce_scatter<N, V / 2, O>(v, lane);
+        } else {
+            v[0] += __shfl_xor_sync(0xffffffffu, v[0], O);
+            reduce_scatter<N, 1, O>(v, lane);
+        }
+    }
+}
+
+constexpr int ilog2c(int v) { return v <= 1 ? 0 : 1 + ilog2c(v / 2); }
+
+}  // namespace
+
+constexpr int kLatMaxV = 4;         // float4 per gather thread: input width <= 64
+constexpr int kLatMaxLayers = 2;    // hidden layers handled by the latency kernel
+constexpr int kLatMaxSteps = 4096;  // Adam bias-correction table in shared memory
+
+// Shared-memory carve-up (floats), identical on host and device.  Own
+// parameters are double-buffered by step parity: step s reads copy s&1 and
+// Adam writes copy (s+1)&1, so the update needs no barrier against readers.
 struct LatCarve {
-    int cs, N, J[NOMA_MAX_DIMS], cin[NOMA_MAX_DIMS], sw[NOMA_MAX_DIMS], rsp[NOMA_MAX_DIMS];
-    int xt, r0b, yall, dy, red, misc;
-    int w[NOMA_MAX_DIMS], b[NOMA_MAX_DIMS], wf, npar;  // own parameters
-    int m1, m2;                                        // Adam moments
-    int aN;                                            // own a_N [J_N][kSR]
+    int cs, jt, N, total, width;
+    int sw[NOMA_MAX_DIMS];
+    int xt, r0b, yall, dy, red, atab;
+    int w[NOMA_MAX_DIMS], b[NOMA_MAX_DIMS], wf, npar;  // copy 0; copy 1 at +npar
+    int aN;                                            // own a_N [JT][kSR]
     int aloc[NOMA_MAX_DIMS], af[NOMA_MAX_DIMS], rsb[NOMA_MAX_DIMS];  // l < N
-    int part[NOMA_MAX_DIMS], partb[NOMA_MAX_DIMS];     // weight-gradient partials
     int bars;                                          // mbarriers (8-byte aligned)
     int nbars, end;
 };
 
-__host__ __device__ inline int lat_pow2_floor(int v) {
-    int p = 1;
-    while (p * 2 <= v) p *= 2;
-    return p;
-}
-
-// Returns false when the shape is outside this kernel (caller falls back).
-__host__ __device__ inline bool lat_carve(const NetGeom &g, int cs, int width, LatCarve *c) {
+// Shapes the latency kernel handles (else the caller falls back): 1-2 hidden
+// layers of one width H = cs * jt with jt in {2, 4, 8} (jt >= 4 with two
+// layers), input width 2M in {32, 64} (k split over 8 lanes, column tiles
+// over at most 16 warps), at most kLatMaxSteps Adam steps.
+__host__ __device__ inline bool lat_carve(const NetGeom &g, int cs, int width, int total_steps,
+                                          LatCarve *c) {
     const int N = g.nd - 1;
-    if (N < 1 || cs < 2 || cs > 16) return false;
-    if (width != g.dims[0] || width % 8 || width > 4 * 4 * kLatMaxV) return false;
+    if (N < 1 || N > kLatMaxLayers || cs < 2 || cs > 16) return false;
+    if (width != g.dims[0] || (width != 32 && width != 64)) return false;
+    if (total_steps > kLatMaxSteps) return false;
+    const int H = g.dims[1];
+    for (int l = 1; l <= N; ++l)
+        if (g.dims[l] != H) return false;
+    if (H % cs) return false;
+    const int jt = H / cs;
+    if (jt != 2 && jt != 4 && jt != 8) return false;
+    if (N > 1 && (jt < 4 || H > 64)) return false;
     c->cs = cs;
+    c->jt = jt;
     c->N = N;
-    for (int l = 1; l <= N; ++l) {
-        if (g.dims[l] % cs) return false;
-        c->J[l] = g.dims[l] / cs;
-        c->cin[l] = g.dims[l - 1];
-        if (c->J[l] % 2 || c->cin[l] % 4) return false;
-        if (l < N && c->J[l] % 4) return false;
-        c->sw[l] = c->cin[l] + 4;
-        const int ntile = (c->J[l] / 2) * (c->cin[l] / 4);
-        int r = ntile >= kLT ? 1 : lat_pow2_floor(kLT / ntile);
-        c->rsp[l] = r > 32 ? 32 : r;
-    }
+    c->total = total_steps;
+    c->width = width;
     int off = 0;
     c->xt = off;
     off += 2 * width * kSR;
@@ -130,40 +190,30 @@ __host__ __device__ inline bool lat_carve(const NetGeom &g, int cs, int width, L
     c->dy = off;
     off += kBatchRows;
     c->red = off;
-    off += kBatchRows;
-    c->misc = off;
-    off += 4;
+    off += 32;
+    c->atab = off;
+    off += pad_to(2 * total_steps, 4);
     int np = 0;
     for (int l = 1; l <= N; ++l) {
+        c->sw[l] = g.dims[l - 1] + 4;
         c->w[l] = off + np;
-        np += c->J[l] * c->sw[l];
+        np += jt * c->sw[l];
         c->b[l] = off + np;
-        np += c->J[l];
+        np += pad_to(jt, 4);
     }
     c->wf = off + np;
-    np += c->J[N];
-    np = pad_to(np, 4);
+    np += pad_to(jt, 4);
     c->npar = np;
-    off += np;
-    c->m1 = off;
-    off += np;
-    c->m2 = off;
-    off += np;
+    off += 2 * np;
     c->aN = off;
-    off += c->J[N] * kSR;
+    off += jt * kSR;
     for (int l = 1; l < N; ++l) {
         c->aloc[l] = off;
-        off += c->J[l] * kSR;
+        off += jt * kSR;
         c->af[l] = off;
-        off += g.dims[l] * kSR;
+        off += H * kSR;
         c->rsb[l] = off;
-        off += cs * c->J[l] * kSR;
-    }
-    for (int l = 1; l <= N; ++l) {
-        c->part[l] = off;
-        off += c->rsp[l] * c->J[l] * c->cin[l];
-        c->partb[l] = off;
-        off += c->rsp[l] * c->J[l] * 2;
+        off += cs * jt * kSR;
     }
     off = pad_to(off, 2);
     c->bars = off;
@@ -173,188 +223,224 @@ __host__ __device__ inline bool lat_carve(const NetGeom &g, int cs, int width, L
     return (size_t)off * sizeof(float) <= 227 * 1024;
 }
 
-template <int CS>
+template <int CS, int JT, int NL, int VW>
 __global__ void __launch_bounds__(kLT, 1) train_lat_kernel(TrainParams p, LatCarve c) {
     extern __shared__ __align__(16) float sm[];
+    constexpr int H = CS * JT;
     const int net = blockIdx.x / CS;
     if (p.status && p.status[net] != NOMA_OK) return;  // uniform over the cluster
     const uint32_t rank = cl_rank();
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const NetGeom &g = p.g;
-    const int N = c.N;
-    const int n = p.rows, d = net / p.K, width = p.width, M = width / 2;
+    const int n = p.rows, d = net / p.K, width = c.width, M = width / 2;
     const bool wid = p.layout == NOMA_LAYOUT_WIDEN_COMPLEX;
     uint64_t *bars = reinterpret_cast<uint64_t *>(sm + c.bars);
     // barrier indices: Y[0], Y[1], then AG_l = 2 + 2(l-1), RS_l = 3 + 2(l-1)
+    // phase cycles (NOMA_PHASE_CLOCKS, block 0 thread 0): 0 forward, 1 its
+    // barrier, 2 yp send + gather, 3 yp wait, 4 residual + barrier, 5 backward
+    // + Adam, 6 end-of-step barrier, 7 prologue / epilogue.  After a barrier a
+    // volatile shared load blocks until the barrier has actually released.
     const bool clk_on = p.clocks && blockIdx.x == 0 && tid == 0;
-    long long clk_acc[6] = {0, 0, 0, 0, 0, 0}, clk_prev = clk_on ? clock64() : 0;
-#define NOMA_LPHASE(I)                               \
-    if (clk_on) {                                    \
-        const long long now = clock64();             \
-        clk_acc[I] += now - clk_prev;                \
-        clk_prev = now;                              \
+    long long clk_acc[8] = {0, 0, 0, 0, 0, 0, 0, 0}, clk_prev = clk_on ? clock64() : 0;
+#define NOMA_LPHASE(I)                                            \
+    if (clk_on) {                                                 \
+        (void)*reinterpret_cast<volatile float *>(sm + c.dy);     \
+        const long long now = clock64();                          \
+        clk_acc[I] += now - clk_prev;                             \
+        clk_prev = now;                                           \
     }
 
     for (int i = tid; i < c.bars; i += kLT) sm[i] = 0.0f;
-    // own parameters from the FusedPlan buffer (fused_inference.cpp:19-42)
+    __syncthreads();
+    // own parameters (copy 0) from the FusedPlan buffer (fused_inference.cpp:19-42)
     const float *pl = p.plans + (size_t)net * g.plan_total;
-    for (int l = 1; l <= N; ++l) {
-        const int J = c.J[l], C = c.cin[l];
-        for (int i = tid; i < J * C; i += kLT) {
-            const int j = i / C, k = i % C;
-            sm[c.w[l] + j * c.sw[l] + k] = pl[g.plan_w[l] + (rank * J + j) * g.plan_pad[l - 1] + k];
+#pragma unroll
+    for (int l = 1; l <= NL; ++l) {
+        const int C = g.dims[l - 1];
+        for (int i = tid; i < JT * C; i += kLT) {
+            const int j = i / C, k = i - j * C;
+            sm[c.w[l] + j * c.sw[l] + k] = pl[g.plan_w[l] + (rank * JT + j) * g.plan_pad[l - 1] + k];
         }
-        for (int j = tid; j < J; j += kLT) sm[c.b[l] + j] = pl[g.plan_b[l] + rank * J + j];
+        if (tid < JT) sm[c.b[l] + tid] = pl[g.plan_b[l] + rank * JT + tid];
     }
-    for (int j = tid; j < c.J[N]; j += kLT) sm[c.wf + j] = pl[g.plan_f + rank * c.J[N] + j];
-    const uint32_t ybytes = CS * kBatchRows * 4;
+    if (tid < JT) sm[c.wf + tid] = pl[g.plan_f + rank * JT + tid];
+    // Adam bias corrections per step, FP64 pow like hybrid_nn.cpp:133-135
+    for (int i = tid; i < c.total; i += kLT) {
+        const double c1 = 1.0 - pow(p.b1d, (double)(i + 1));
+        const double c2 = 1.0 - pow(p.b2d, (double)(i + 1));
+        sm[c.atab + 2 * i] = (float)(p.lr_d / c1);
+        sm[c.atab + 2 * i + 1] = (float)(1.0 / c2);
+    }
+    constexpr uint32_t ybytes = CS * kBatchRows * 4;
+    constexpr uint32_t agbytes = H * kBatchRows * 4;
+    constexpr uint32_t rsbytes = CS * JT * kBatchRows * 4;
     if (tid == 0) {
         for (int b = 0; b < c.nbars; ++b) mbar_init(s2u(bars + b), 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         mbar_arm(s2u(bars + 0), ybytes);
         mbar_arm(s2u(bars + 1), ybytes);
-        for (int l = 1; l < N; ++l) {
-            mbar_arm(s2u(bars + 2 + 2 * (l - 1)), g.dims[l] * kBatchRows * 4);
-            mbar_arm(s2u(bars + 3 + 2 * (l - 1)), CS * c.J[l] * kBatchRows * 4);
+#pragma unroll
+        for (int l = 1; l < NL; ++l) {
+            mbar_arm(s2u(bars + 2 + 2 * (l - 1)), agbytes);
+            mbar_arm(s2u(bars + 3 + 2 * (l - 1)), rsbytes);
         }
     }
 
     // ---- step schedule and the two-stage gather prefetch --------------------
+    // Thread t gathers float4 columns 4(t/128 + 4v) of minibatch row t%128:
+    // the complex row idx/2 of slot d; odd widened rows read the other half
+    // (offset +-M) and negate Re (iq_transform.cpp:17-20).
     const int spe = (n + p.batch - 1) / p.batch;  // steps per epoch
-    const long total = (long)spe * p.epochs;
-    const int gr = tid >> 2, gh = tid & 3;         // gather: 4 threads per row
-    const int nv = width / 4;                       // float4 per row
-    auto step_row = [&](long s, int r, int &bsz) -> int {  // perm index or -1
-        const int e = (int)(s / spe), start = (int)(s % spe) * p.batch;
-        bsz = min(p.batch, n - start);
-        if (r >= bsz) return -1;
-        return p.perm[((size_t)net * p.epochs + e) * n + start + r];
+    const int total = c.total;
+    const int gr = tid & (kBatchRows - 1), gh = tid >> 7;
+    const float *dsrc = p.design32 + (wid ? (size_t)d * (n >> 1) : (size_t)d * n) * width;
+    const float *r0src = p.r0 + (size_t)net * n;
+    const uint16_t *psrc = p.perm + (size_t)net * p.epochs * n;
+    int colv[VW], offo[VW];
+    bool okv[VW], negv[VW];
+#pragma unroll
+    for (int v = 0; v < VW; ++v) {
+        const int col = 4 * (gh + 4 * v);
+        okv[v] = col < width;
+        colv[v] = okv[v] ? col : 0;
+        offo[v] = wid ? (col < M ? M : -M) : 0;
+        negv[v] = wid && col >= M;
+    }
+    auto perm_at = [&](int e, int st, int r) -> int {  // perm index, or -1 past the batch
+        const int start = st * p.batch;
+        return r < min(p.batch, n - start) ? (int)psrc[e * n + start + r] : -1;
     };
-    float4 rowv[kLatMaxV];
+    float4 rowv[VW];
     float rowr0 = 0.0f;
     auto load_row = [&](int idx) {
+        const bool valid = idx >= 0;
+        const int ii = valid ? idx : 0;
+        const bool odd = wid && (ii & 1);
+        const float *src = dsrc + (wid ? ii >> 1 : ii) * width;
 #pragma unroll
-        for (int v = 0; v < kLatMaxV; ++v) {
-            const int f = gh + 4 * v;
+        for (int v = 0; v < VW; ++v) {
             float4 x = make_float4(0.f, 0.f, 0.f, 0.f);
-            if (idx >= 0 && f < nv) {
-                const int col = 4 * f;
-                const float *src = wid ? p.design32 + ((size_t)d * (n >> 1) + (idx >> 1)) * width
-                                       : p.design32 + ((size_t)d * n + idx) * width;
-                if (!wid || !(idx & 1)) {
-                    x = *reinterpret_cast<const float4 *>(src + col);
-                } else if (col < M) {
-                    x = *reinterpret_cast<const float4 *>(src + M + col);
-                } else {
-                    const float4 t = *reinterpret_cast<const float4 *>(src + col - M);
-                    x = make_float4(-t.x, -t.y, -t.z, -t.w);
-                }
-            }
-            rowv[v] = x;
+            if (okv[v]) x = *reinterpret_cast<const float4 *>(src + colv[v] + (odd ? offo[v] : 0));
+            const float sg = !valid ? 0.f : (odd && negv[v]) ? -1.f : 1.f;
+            rowv[v] = make_float4(sg * x.x, sg * x.y, sg * x.z, sg * x.w);
         }
-        rowr0 = (idx >= 0 && gh == 0) ? p.r0[(size_t)net * n + idx] : 0.0f;
+        rowr0 = (valid && gh == 0) ? r0src[ii] : 0.0f;
     };
     auto store_row = [&](int buf) {
-        float *xt = sm + c.xt + buf * width * kSR;
+        float *xt = sm + c.xt + buf * width * kSR + gr;
 #pragma unroll
-        for (int v = 0; v < kLatMaxV; ++v) {
-            const int f = gh + 4 * v;
-            if (f < nv) {
-                xt[(4 * f + 0) * kSR + gr] = rowv[v].x;
-                xt[(4 * f + 1) * kSR + gr] = rowv[v].y;
-                xt[(4 * f + 2) * kSR + gr] = rowv[v].z;
-                xt[(4 * f + 3) * kSR + gr] = rowv[v].w;
+        for (int v = 0; v < VW; ++v) {
+            if (okv[v]) {
+                float *q = xt + colv[v] * kSR;
+                q[0] = rowv[v].x;
+                q[kSR] = rowv[v].y;
+                q[2 * kSR] = rowv[v].z;
+                q[3 * kSR] = rowv[v].w;
             }
         }
         if (gh == 0) sm[c.r0b + buf * kBatchRows + gr] = rowr0;
     };
-    int bsz_dummy;
-    load_row(total > 0 ? step_row(0, gr, bsz_dummy) : -1);
+    load_row(total > 0 ? perm_at(0, 0, gr) : -1);
     store_row(0);
-    int idx_next = total > 1 ? step_row(1, gr, bsz_dummy) : -1;
-    load_row(idx_next);                              // rows of step 1
-    idx_next = total > 2 ? step_row(2, gr, bsz_dummy) : -1;  // indices of step 2
+    int idx_next = total > 1 ? perm_at(1 / spe, 1 % spe, gr) : -1;
+    load_row(idx_next);                                      // rows of step 1
+    idx_next = total > 2 ? perm_at(2 / spe, 2 % spe, gr) : -1;  // indices of step 2
+    int e3 = 3 / spe, st3 = 3 % spe;                          // schedule of step s+3
     __syncthreads();
     cl_sync();  // every CTA's barriers initialised before any st.async lands
 
+    // Adam moments of the parameters this thread updates (registers; fixed
+    // thread -> parameter map for the whole training): per layer one weight
+    // and one bias-or-final-weight.
+    float mw[NL + 1], vw[NL + 1], mb[NL + 1], vb[NL + 1];
+#pragma unroll
+    for (int l = 0; l <= NL; ++l) mw[l] = vw[l] = mb[l] = vb[l] = 0.f;
+
+    // forward thread map: 8 k-split lanes x 32 row quads (threads < 256)
+    const int fkq = tid & 7, frq = (tid >> 3) & 31;
+    constexpr int FV = JT / 2;                     // values per lane after the k reduce
+    const int fj = (fkq * FV) >> 2, fr = (fkq * FV) & 3;  // neuron, first row of them
+
     float loss_acc = 0.0f;
-    long s = 0;
-    NOMA_LPHASE(5)
+    int s = 0;
+    NOMA_LPHASE(7)
     for (int e = 0; e < p.epochs; ++e) {
         for (int st = 0; st < spe; ++st, ++s) {
-            const int buf = (int)(s & 1);
+            const int buf = s & 1;
             const int start = st * p.batch, bsz = min(p.batch, n - start);
             const float *XT = sm + c.xt + buf * width * kSR;
-            // ---- forward (hybrid_nn.cpp:60-72), own neurons ------------------
-            for (int l = 1; l <= N; ++l) {
-                const int J = c.J[l], C = c.cin[l];
+            const int po = buf * c.npar, pn = (buf ^ 1) * c.npar;  // param copy: read, write
+            // ---- forward (hybrid_nn.cpp:60-72): all JT own neurons x 4 rows per
+            // thread, k split over 8 lanes, lane reduce-scatter --------------
+#pragma unroll
+            for (int l = 1; l <= NL; ++l) {
+                const int NC = (l == 1 ? width : H) >> 2;
                 const float *in = l == 1 ? XT : sm + c.af[l - 1];
-                const float *W = sm + c.w[l], *bias = sm + c.b[l];
-                float *out = l == N ? sm + c.aN : sm + c.aloc[l];
-                const int items = J * 32;
-                int ks = items >= kLT ? 1 : lat_pow2_floor(kLT / items);
-                if (ks > C / 4) ks = lat_pow2_floor(C / 4);
-                const int kchunks = C / 4;
-                for (int t = tid; t < items * ks; t += kLT) {
-                    const int kq = t % ks, rq = (t / ks) & 31, j = t / (ks * 32);
-                    const int r0 = 4 * rq;
-                    f2_t a0 = 0ull, a1 = 0ull;
-                    const float *wr = W + j * c.sw[l];
-                    for (int kc = kq; kc < kchunks; kc += ks) {
-                        const float4 w4 = *reinterpret_cast<const float4 *>(wr + 4 * kc);
-                        const float *ip = in + 4 * kc * kSR + r0;
-                        const ulonglong2 x0 = *reinterpret_cast<const ulonglong2 *>(ip);
-                        const ulonglong2 x1 = *reinterpret_cast<const ulonglong2 *>(ip + kSR);
-                        const ulonglong2 x2 = *reinterpret_cast<const ulonglong2 *>(ip + 2 * kSR);
-                        const ulonglong2 x3 = *reinterpret_cast<const ulonglong2 *>(ip + 3 * kSR);
-                        f2_t wb = f2_bcast(w4.x);
-                        ffma2(a0, wb, x0.x);
-                        ffma2(a1, wb, x0.y);
-                        wb = f2_bcast(w4.y);
-                        ffma2(a0, wb, x1.x);
-                        ffma2(a1, wb, x1.y);
-                        wb = f2_bcast(w4.z);
-                        ffma2(a0, wb, x2.x);
-                        ffma2(a1, wb, x2.y);
-                        wb = f2_bcast(w4.w);
-                        ffma2(a0, wb, x3.x);
-                        ffma2(a1, wb, x3.y);
+                const float *W = sm + po + c.w[l];
+                const int sw = c.sw[l];
+                if (tid < 256) {
+                    f2_t acc[JT][2];
+#pragma unroll
+                    for (int j = 0; j < JT; ++j) acc[j][0] = acc[j][1] = 0ull;
+                    for (int kc = fkq; kc < NC; kc += 8) {
+                        const float *ip = in + 4 * kc * kSR + 4 * frq;
+                        ulonglong2 x[4];
+#pragma unroll
+                        for (int kk = 0; kk < 4; ++kk) x[kk] = *reinterpret_cast<const ulonglong2 *>(ip + kk * kSR);
+#pragma unroll
+                        for (int j = 0; j < JT; ++j) {
+                            const float4 w4 = *reinterpret_cast<const float4 *>(W + j * sw + 4 * kc);
+                            const float wk[4] = {w4.x, w4.y, w4.z, w4.w};
+#pragma unroll
+                            for (int kk = 0; kk < 4; ++kk) {
+                                const f2_t wb = f2_bcast(wk[kk]);
+                                ffma2(acc[j][0], wb, x[kk].x);
+                                ffma2(acc[j][1], wb, x[kk].y);
+                            }
+                        }
                     }
-                    float2 u = f2_unpack(a0), v = f2_unpack(a1);
-                    for (int o = 1; o < ks; o <<= 1) {  // butterfly over the k split
-                        u.x += __shfl_xor_sync(0xffffffffu, u.x, o);
-                        u.y += __shfl_xor_sync(0xffffffffu, u.y, o);
-                        v.x += __shfl_xor_sync(0xffffffffu, v.x, o);
-                        v.y += __shfl_xor_sync(0xffffffffu, v.y, o);
+                    float v[4 * JT];
+#pragma unroll
+                    for (int j = 0; j < JT; ++j) {
+                        const float2 a = f2_unpack(acc[j][0]), b = f2_unpack(acc[j][1]);
+                        v[4 * j] = a.x;
+                        v[4 * j + 1] = a.y;
+                        v[4 * j + 2] = b.x;
+                        v[4 * j + 3] = b.y;
                     }
-                    const float bj = bias[j];
-                    const float4 y = make_float4(fmaxf(u.x + bj, 0.f), fmaxf(u.y + bj, 0.f),
-                                                 fmaxf(v.x + bj, 0.f), fmaxf(v.y + bj, 0.f));
-                    if (kq == 0) *reinterpret_cast<float4 *>(out + j * kSR + r0) = y;
-                    if (l < N) {  // all-gather: lane kq sends to ranks kq, kq+ks, ...
-                        const uint32_t la = s2u(sm + c.af[l] + (rank * J + j) * kSR + r0);
+                    reduce_scatter<4 * JT, 4 * JT, 8>(v, lane);
+                    const float bj = sm[po + c.b[l] + fj];
+#pragma unroll
+                    for (int i = 0; i < FV; ++i) v[i] = fmaxf(v[i] + bj, 0.f);
+                    const int r = 4 * frq + fr;
+                    sts_n<FV>((l == NL ? sm + c.aN : sm + c.aloc[l]) + fj * kSR + r, v);
+                    if (l < NL) {  // all-gather a_l into every CTA (incl. this one)
+                        const uint32_t la = s2u(sm + c.af[l] + (rank * JT + fj) * kSR + r);
                         const uint32_t lb = s2u(bars + 2 + 2 * (l - 1));
-                        for (int q = kq; q < CS; q += ks) st_async4(mapa(la, q), y, mapa(lb, q));
+#pragma unroll
+                        for (int q = 0; q < CS; ++q) st_async_n<FV>(mapa(la, q), v, mapa(lb, q));
                     }
                 }
-                if (l < N) {
+                if (l < NL) {
                     const uint32_t lb = s2u(bars + 2 + 2 * (l - 1));
                     mbar_wait(lb, (uint32_t)(s & 1));
                     // re-arm for step s+1 (its bytes cannot land before every
                     // CTA has finished step s)
-                    if (tid == 0) mbar_arm(lb, g.dims[l] * kBatchRows * 4);
+                    if (tid == 0) mbar_arm(lb, agbytes);
                 }
             }
-            __syncthreads();
             NOMA_LPHASE(0)
-            // ---- final-layer partials to every CTA; gather the next tile ------
+            __syncthreads();
+            NOMA_LPHASE(1)
+            // ---- final-layer partials yp (hybrid_nn.cpp:81): warps 0-3 send --
             const uint32_t ybar = s2u(bars + buf);
-            if (warp == 0) {
+            if (warp < 4) {
                 const int r0 = 4 * lane;
                 const float *aN = sm + c.aN;
-                const float *wf = sm + c.wf;
+                const float *wf = sm + po + c.wf;
                 float4 y = make_float4(0.f, 0.f, 0.f, 0.f);
-                for (int j = 0; j < c.J[N]; ++j) {
+#pragma unroll
+                for (int j = 0; j < JT; ++j) {
                     const float4 a = *reinterpret_cast<const float4 *>(aN + j * kSR + r0);
                     const float f = wf[j];
                     y.x = fmaf(f, a.x, y.x);
@@ -364,239 +450,236 @@ __global__ void __launch_bounds__(kLT, 1) train_lat_kernel(TrainParams p, LatCar
                 }
                 const uint32_t la = s2u(sm + c.yall + (buf * CS + rank) * kBatchRows + r0);
 #pragma unroll
-                for (int q = 0; q < CS; ++q) st_async4(mapa(la, q), y, mapa(ybar, q));
+                for (int q = warp; q < CS; q += 4) st_async4(mapa(la, q), y, mapa(ybar, q));
             }
+            // ---- gather: store the rows of step s+1, load step s+2's ----------
             if (s + 1 < total) {
-                store_row(buf ^ 1);  // rows of step s+1 (loaded one step ago)
-                load_row(idx_next);  // rows of step s+2
-                idx_next = s + 3 < total ? step_row(s + 3, gr, bsz_dummy) : -1;
+                store_row(buf ^ 1);
+                load_row(idx_next);
+                idx_next = s + 3 < total ? perm_at(e3, st3, gr) : -1;
             }
-            if (tid == kLT - 1) {  // Adam bias corrections (FP64 pow, hybrid_nn.cpp:133-135)
-                const double c1 = 1.0 - pow(p.b1d, (double)(s + 1));
-                const double c2 = 1.0 - pow(p.b2d, (double)(s + 1));
-                sm[c.misc + 0] = (float)(p.lr_d / c1);
-                sm[c.misc + 1] = (float)(1.0 / c2);
+            if (++st3 == spe) {
+                st3 = 0;
+                ++e3;
             }
-            NOMA_LPHASE(1)
-            // ---- residual a_N w - r0, dy = 2 r / B (hybrid_nn.cpp:94-98) --------
-            if (tid < kBatchRows) {
+            NOMA_LPHASE(2)
+            // ---- residual a_N w - r0, dy = 2 r / B (hybrid_nn.cpp:94-98): warp 0,
+            // 4 rows per lane, partials summed in rank order ------------------
+            if (warp == 0) {
                 mbar_wait(ybar, (uint32_t)((s >> 1) & 1));
-                const float *ya = sm + c.yall + buf * CS * kBatchRows + tid;
-                float yh = 0.0f;
+                NOMA_LPHASE(3)
+                const int r0 = 4 * lane;
+                const float *ya = sm + c.yall + buf * CS * kBatchRows + r0;
+                float4 yh = *reinterpret_cast<const float4 *>(ya);
 #pragma unroll
-                for (int q = 0; q < CS; ++q) yh += ya[q * kBatchRows];
-                const float res = tid < bsz ? yh - sm[c.r0b + buf * kBatchRows + tid] : 0.0f;
-                sm[c.dy + tid] = (2.0f / (float)bsz) * res;
-                loss_acc = fmaf(res, res, loss_acc);
+                for (int q = 1; q < CS; ++q) {
+                    const float4 v = *reinterpret_cast<const float4 *>(ya + q * kBatchRows);
+                    yh.x += v.x;
+                    yh.y += v.y;
+                    yh.z += v.z;
+                    yh.w += v.w;
+                }
+                const float4 rr = *reinterpret_cast<const float4 *>(sm + c.r0b + buf * kBatchRows + r0);
+                const float4 res = make_float4(r0 < bsz ? yh.x - rr.x : 0.f, r0 + 1 < bsz ? yh.y - rr.y : 0.f,
+                                               r0 + 2 < bsz ? yh.z - rr.z : 0.f, r0 + 3 < bsz ? yh.w - rr.w : 0.f);
+                const float sc = 2.0f / (float)bsz;
+                *reinterpret_cast<float4 *>(sm + c.dy + r0) = make_float4(sc * res.x, sc * res.y, sc * res.z, sc * res.w);
+                loss_acc = fmaf(res.x, res.x, loss_acc);
+                loss_acc = fmaf(res.y, res.y, loss_acc);
+                loss_acc = fmaf(res.z, res.z, loss_acc);
+                loss_acc = fmaf(res.w, res.w, loss_acc);
             }
             __syncthreads();
             if (tid == 0) mbar_arm(ybar, ybytes);  // phase for step s+2
-            NOMA_LPHASE(2)
-            // ---- backward (hybrid_nn.cpp:99-112), own neurons ---------------
-            for (int l = N; l >= 1; --l) {
-                const int J = c.J[l], C = c.cin[l];
-                const bool top = l == N;
+            NOMA_LPHASE(4)
+            // ---- backward (hybrid_nn.cpp:99-112) fused with Adam (:118-144) ---
+            const float lrc = sm[c.atab + 2 * s], ic2 = sm[c.atab + 2 * s + 1];
+#pragma unroll
+            for (int l = NL; l >= 1; --l) {
+                constexpr int dummy = 0;
+                (void)dummy;
+                const bool top = l == NL;
+                const int NC = (l == 1 ? width : H) >> 2;
                 const float *zsrc = top ? sm + c.aN : sm + c.aloc[l];  // a_N, or dZ_l in place
-                const float *dyp = sm + c.dy, *wf = sm + c.wf;
+                const float *dyp = sm + c.dy, *wfp = sm + po + c.wf;
                 const float *in = l == 1 ? XT : sm + c.af[l - 1];
-                const int rsp = c.rsp[l], nct = C / 4;
-                const int ntile = (J / 2) * nct;
-                float *part = sm + c.part[l], *partb = sm + c.partb[l];
-                for (int t = tid; t < ntile * rsp; t += kLT) {
-                    const int rs = t % rsp, tile = t / rsp;
-                    const int it = tile / nct, ct = tile % nct;
-                    const int i0 = 2 * it, c0 = 4 * ct;
-                    f2_t acc[2][4], sb[2], sf[2];
+                const int sw = c.sw[l];
+                if (l > 1 && tid < (H / 4) * 32) {
+                    // dA_{l-1} partial = sum_{j own} W_l[j][c] dZ_l[j][r] (:111) for
+                    // every c (4 c x 4 r per thread), sent to the owner of c.
+                    const float *W = sm + po + c.w[l];
+                    const uint32_t rb = s2u(bars + 3 + 2 * (l - 2));
+                    const int cq = tid >> 5, r = 4 * lane, cc = 4 * cq;  // H/4 = 16 warps
+                    f2_t acc[4][2];
 #pragma unroll
-                    for (int a = 0; a < 2; ++a) {
-                        sb[a] = sf[a] = 0ull;
+                    for (int q = 0; q < 4; ++q) acc[q][0] = acc[q][1] = 0ull;
+                    float4 y4 = make_float4(0.f, 0.f, 0.f, 0.f);
+                    if (top) y4 = *reinterpret_cast<const float4 *>(dyp + r);
 #pragma unroll
-                        for (int q = 0; q < 4; ++q) acc[a][q] = 0ull;
+                    for (int j = 0; j < JT; ++j) {
+                        const float4 w4 = *reinterpret_cast<const float4 *>(W + j * sw + cc);
+                        float4 z = *reinterpret_cast<const float4 *>(zsrc + j * kSR + r);
+                        if (top) {
+                            const float f = wfp[j];
+                            z = make_float4(z.x > 0.f ? y4.x * f : 0.f, z.y > 0.f ? y4.y * f : 0.f,
+                                            z.z > 0.f ? y4.z * f : 0.f, z.w > 0.f ? y4.w * f : 0.f);
+                        }
+                        const f2_t za = f2_pack(z.x, z.y), zb = f2_pack(z.z, z.w);
+                        const float wc[4] = {w4.x, w4.y, w4.z, w4.w};
+#pragma unroll
+                        for (int q = 0; q < 4; ++q) {
+                            const f2_t wq = f2_bcast(wc[q]);
+                            ffma2(acc[q][0], wq, za);
+                            ffma2(acc[q][1], wq, zb);
+                        }
                     }
-                    const float wf0 = top ? wf[i0] : 0.f, wf1 = top ? wf[i0 + 1] : 0.f;
+                    const int owner = cc / JT, lc = cc - owner * JT;
+                    const uint32_t la = s2u(sm + c.rsb[l - 1] + (rank * JT + lc) * kSR + r);
+                    const uint32_t ra = mapa(la, owner), rbar = mapa(rb, owner);
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        const float2 u = f2_unpack(acc[q][0]), v = f2_unpack(acc[q][1]);
+                        st_async4(ra + q * kSR * 4, make_float4(u.x, u.y, v.x, v.y), rbar);
+                    }
+                }
+                // weight gradient dZ^T A (:109), bias colsum (:110), final a_N^T dy
+                // (:99): warp ct owns column tile 4ct..4ct+3 for all JT neurons,
+                // lane = row quad; lane reduce-scatter, then Adam in registers.
+                if (warp < NC) {
+                    const int ct = warp, r = 4 * lane;
+                    f2_t acc[JT][4], sb[JT], sf[JT];
+#pragma unroll
+                    for (int j = 0; j < JT; ++j) {
+                        sb[j] = sf[j] = 0ull;
+#pragma unroll
+                        for (int q = 0; q < 4; ++q) acc[j][q] = 0ull;
+                    }
+                    ulonglong2 x[4];
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) x[q] = *reinterpret_cast<const ulonglong2 *>(in + (4 * ct + q) * kSR + r);
+                    float4 y4 = make_float4(0.f, 0.f, 0.f, 0.f);
+                    if (top) y4 = *reinterpret_cast<const float4 *>(dyp + r);
                     const f2_t one = f2_bcast(1.0f);
-                    for (int rq = rs; rq < 32; rq += rsp) {
-                        const int r = 4 * rq;
-                        float4 z0 = *reinterpret_cast<const float4 *>(zsrc + i0 * kSR + r);
-                        float4 z1 = *reinterpret_cast<const float4 *>(zsrc + (i0 + 1) * kSR + r);
-                        if (top) {  // dZ_N = (a_N > 0) dy w_j, formed on the fly (:102-107)
-                            const float4 y = *reinterpret_cast<const float4 *>(dyp + r);
-                            if (ct == 0) {  // final-layer gradient a_N^T dy (:99)
-                                ffma2(sf[0], f2_pack(z0.x, z0.y), f2_pack(y.x, y.y));
-                                ffma2(sf[0], f2_pack(z0.z, z0.w), f2_pack(y.z, y.w));
-                                ffma2(sf[1], f2_pack(z1.x, z1.y), f2_pack(y.x, y.y));
-                                ffma2(sf[1], f2_pack(z1.z, z1.w), f2_pack(y.z, y.w));
-                            }
-                            z0 = make_float4(z0.x > 0.f ? y.x * wf0 : 0.f, z0.y > 0.f ? y.y * wf0 : 0.f,
-                                             z0.z > 0.f ? y.z * wf0 : 0.f, z0.w > 0.f ? y.w * wf0 : 0.f);
-                            z1 = make_float4(z1.x > 0.f ? y.x * wf1 : 0.f, z1.y > 0.f ? y.y * wf1 : 0.f,
-                                             z1.z > 0.f ? y.z * wf1 : 0.f, z1.w > 0.f ? y.w * wf1 : 0.f);
+#pragma unroll
+                    for (int j = 0; j < JT; ++j) {
+                        float4 z = *reinterpret_cast<const float4 *>(zsrc + j * kSR + r);
+                        if (top) {  // dZ_N = (a_N > 0) dy w_j on the fly (:102-107)
+                            ffma2(sf[j], f2_pack(z.x, z.y), f2_pack(y4.x, y4.y));
+                            ffma2(sf[j], f2_pack(z.z, z.w), f2_pack(y4.z, y4.w));
+                            const float f = wfp[j];
+                            z = make_float4(z.x > 0.f ? y4.x * f : 0.f, z.y > 0.f ? y4.y * f : 0.f,
+                                            z.z > 0.f ? y4.z * f : 0.f, z.w > 0.f ? y4.w * f : 0.f);
                         }
-                        const f2_t z0a = f2_pack(z0.x, z0.y), z0b = f2_pack(z0.z, z0.w);
-                        const f2_t z1a = f2_pack(z1.x, z1.y), z1b = f2_pack(z1.z, z1.w);
+                        const f2_t za = f2_pack(z.x, z.y), zb = f2_pack(z.z, z.w);
+                        ffma2(sb[j], za, one);
+                        ffma2(sb[j], zb, one);
 #pragma unroll
                         for (int q = 0; q < 4; ++q) {
-                            const ulonglong2 x = *reinterpret_cast<const ulonglong2 *>(in + (c0 + q) * kSR + r);
-                            ffma2(acc[0][q], z0a, x.x);
-                            ffma2(acc[0][q], z0b, x.y);
-                            ffma2(acc[1][q], z1a, x.x);
-                            ffma2(acc[1][q], z1b, x.y);
-                        }
-                        if (ct == 0) {  // bias gradient colsum dZ (:110)
-                            ffma2(sb[0], z0a, one);
-                            ffma2(sb[0], z0b, one);
-                            ffma2(sb[1], z1a, one);
-                            ffma2(sb[1], z1b, one);
+                            ffma2(acc[j][q], za, x[q].x);
+                            ffma2(acc[j][q], zb, x[q].y);
                         }
                     }
+                    float gv[4 * JT];
 #pragma unroll
-                    for (int a = 0; a < 2; ++a) {
-                        float v[4];
+                    for (int j = 0; j < JT; ++j)
 #pragma unroll
                         for (int q = 0; q < 4; ++q) {
-                            const float2 h = f2_unpack(acc[a][q]);
-                            v[q] = h.x + h.y;
+                            const float2 h = f2_unpack(acc[j][q]);
+                            gv[4 * j + q] = h.x + h.y;
                         }
-                        *reinterpret_cast<float4 *>(part + (rs * J + i0 + a) * C + c0) =
-                            make_float4(v[0], v[1], v[2], v[3]);
-                        if (ct == 0) {
-                            const float2 hb = f2_unpack(sb[a]), hf = f2_unpack(sf[a]);
-                            partb[(rs * J + i0 + a) * 2 + 0] = hb.x + hb.y;
-                            partb[(rs * J + i0 + a) * 2 + 1] = hf.x + hf.y;
+                    reduce_scatter<4 * JT, 4 * JT, 32>(gv, lane);
+                    constexpr int GSH = 5 - ilog2c(4 * JT);  // replicas: 2^GSH lanes per weight
+                    const int gi = lane >> GSH;               // j * 4 + q
+                    if ((lane & ((1 << GSH) - 1)) == 0) {
+                        const int off = (gi >> 2) * sw + 4 * ct + (gi & 3);
+                        const float gsum = gv[0];
+                        const float m1 = p.b1 * mw[l] + p.omb1 * gsum;
+                        const float m2 = p.b2 * vw[l] + p.omb2 * (gsum * gsum);
+                        mw[l] = m1;
+                        vw[l] = m2;
+                        sm[pn + c.w[l] + off] = sm[po + c.w[l] + off] - __fdividef(lrc * m1, sqrtf(m2 * ic2) + p.eps);
+                    }
+                    if (ct == 0) {  // biases, then final weights (top layer)
+                        float bv[2 * JT];
+#pragma unroll
+                        for (int j = 0; j < JT; ++j) {
+                            const float2 hb = f2_unpack(sb[j]), hf = f2_unpack(sf[j]);
+                            bv[j] = hb.x + hb.y;
+                            bv[JT + j] = hf.x + hf.y;
+                        }
+                        reduce_scatter<2 * JT, 2 * JT, 32>(bv, lane);
+                        constexpr int BSH = 5 - ilog2c(2 * JT);
+                        const int bi = lane >> BSH;
+                        if ((lane & ((1 << BSH) - 1)) == 0 && (top || bi < JT)) {
+                            const int off = bi < JT ? c.b[l] + bi : c.wf + bi - JT;
+                            const float gsum = bv[0];
+                            const float m1 = p.b1 * mb[l] + p.omb1 * gsum;
+                            const float m2 = p.b2 * vb[l] + p.omb2 * (gsum * gsum);
+                            mb[l] = m1;
+                            vb[l] = m2;
+                            sm[pn + off] = sm[po + off] - __fdividef(lrc * m1, sqrtf(m2 * ic2) + p.eps);
                         }
                     }
                 }
                 if (l > 1) {
-                    // dA_{l-1} partial = sum_{j own} W_l[j][c] dZ_l[j][r] (:111) for
-                    // every c, reduce-scattered to the owner of c.
-                    const int Jd = c.J[l - 1];
-                    const float *W = sm + c.w[l];
-                    const uint32_t rb = s2u(bars + 3 + 2 * (l - 2));
-                    for (int t = tid; t < (C / 4) * 32; t += kLT) {
-                        const int rq = t & 31, cq = t >> 5;
-                        const int r = 4 * rq, cc = 4 * cq;
-                        f2_t acc[4][2];
-#pragma unroll
-                        for (int q = 0; q < 4; ++q) acc[q][0] = acc[q][1] = 0ull;
-                        for (int j = 0; j < J; ++j) {
-                            const float4 w4 = *reinterpret_cast<const float4 *>(W + j * c.sw[l] + cc);
-                            float4 z = *reinterpret_cast<const float4 *>(zsrc + j * kSR + r);
-                            if (top) {
-                                const float4 y = *reinterpret_cast<const float4 *>(dyp + r);
-                                const float f = wf[j];
-                                z = make_float4(z.x > 0.f ? y.x * f : 0.f, z.y > 0.f ? y.y * f : 0.f,
-                                                z.z > 0.f ? y.z * f : 0.f, z.w > 0.f ? y.w * f : 0.f);
-                            }
-                            const f2_t za = f2_pack(z.x, z.y), zb = f2_pack(z.z, z.w);
-                            const float wc[4] = {w4.x, w4.y, w4.z, w4.w};
-#pragma unroll
-                            for (int q = 0; q < 4; ++q) {
-                                const f2_t wq = f2_bcast(wc[q]);
-                                ffma2(acc[q][0], wq, za);
-                                ffma2(acc[q][1], wq, zb);
-                            }
-                        }
-                        const int owner = cc / Jd, lc = cc - owner * Jd;
-                        const uint32_t la = s2u(sm + c.rsb[l - 1] + (rank * Jd + lc) * kSR + r);
-                        const uint32_t ra = mapa(la, owner), rbar = mapa(rb, owner);
-#pragma unroll
-                        for (int q = 0; q < 4; ++q) {
-                            const float2 u = f2_unpack(acc[q][0]), v = f2_unpack(acc[q][1]);
-                            st_async4(ra + q * kSR * 4, make_float4(u.x, u.y, v.x, v.y), rbar);
-                        }
-                    }
                     // receive: dZ_{l-1} own = (a_{l-1} > 0) * sum_q partial_q (:107)
+                    const uint32_t rb = s2u(bars + 3 + 2 * (l - 2));
                     mbar_wait(rb, (uint32_t)(s & 1));
-                    const float *rs_ = sm + c.rsb[l - 1];
-                    float *al = sm + c.aloc[l - 1];
-                    for (int t = tid; t < Jd * 32; t += kLT) {
-                        const int j = t >> 5, r = 4 * (t & 31);
-                        float4 sum = *reinterpret_cast<const float4 *>(rs_ + j * kSR + r);
+                    if (tid < JT * 32) {
+                        const int j = tid >> 5, r = 4 * lane;
+                        const float *rs_ = sm + c.rsb[l - 1] + j * kSR + r;
+                        float4 sum = *reinterpret_cast<const float4 *>(rs_);
+#pragma unroll
                         for (int q = 1; q < CS; ++q) {
-                            const float4 v = *reinterpret_cast<const float4 *>(rs_ + (q * Jd + j) * kSR + r);
+                            const float4 v = *reinterpret_cast<const float4 *>(rs_ + q * JT * kSR);
                             sum.x += v.x;
                             sum.y += v.y;
                             sum.z += v.z;
                             sum.w += v.w;
                         }
-                        float4 *ap = reinterpret_cast<float4 *>(al + j * kSR + r);
+                        float4 *ap = reinterpret_cast<float4 *>(sm + c.aloc[l - 1] + j * kSR + r);
                         const float4 a = *ap;
                         *ap = make_float4(a.x > 0.f ? sum.x : 0.f, a.y > 0.f ? sum.y : 0.f,
                                           a.z > 0.f ? sum.z : 0.f, a.w > 0.f ? sum.w : 0.f);
                     }
                     __syncthreads();
-                    if (tid == 0) mbar_arm(rb, CS * Jd * kBatchRows * 4);
+                    if (tid == 0) mbar_arm(rb, rsbytes);
                 }
             }
+            NOMA_LPHASE(5)
             __syncthreads();
-            NOMA_LPHASE(3)
-            // ---- Adam (hybrid_nn.cpp:118-144) over the own parameters ---------
-            {
-                const float lrc = sm[c.misc + 0], ic2 = sm[c.misc + 1];
-                float *M1 = sm + c.m1, *M2 = sm + c.m2;
-                int base = 0;
-                for (int l = 1; l <= N + 1; ++l) {
-                    const bool fin = l == N + 1;
-                    const int L = fin ? N : l;
-                    const int J = c.J[L], C = c.cin[L], rsp = c.rsp[L];
-                    const int cnt = fin ? J : J * C + J;
-                    const float *part = sm + c.part[L], *partb = sm + c.partb[L];
-                    for (int i = tid; i < cnt; i += kLT) {
-                        float gsum = 0.0f;
-                        float *th;
-                        if (fin) {
-                            for (int q = 0; q < rsp; ++q) gsum += partb[(q * J + i) * 2 + 1];
-                            th = sm + c.wf + i;
-                        } else if (i < J * C) {
-                            const int j = i / C, k = i % C;
-                            for (int q = 0; q < rsp; ++q) gsum += part[(q * J + j) * C + k];
-                            th = sm + c.w[L] + j * c.sw[L] + k;
-                        } else {
-                            const int j = i - J * C;
-                            for (int q = 0; q < rsp; ++q) gsum += partb[(q * J + j) * 2 + 0];
-                            th = sm + c.b[L] + j;
-                        }
-                        const int pi = base + i;
-                        const float m1 = p.b1 * M1[pi] + p.omb1 * gsum;
-                        const float m2 = p.b2 * M2[pi] + p.omb2 * (gsum * gsum);
-                        M1[pi] = m1;
-                        M2[pi] = m2;
-                        *th -= __fdividef(lrc * m1, sqrtf(m2 * ic2) + p.eps);
-                    }
-                    base += cnt;
-                }
-            }
-            __syncthreads();
-            NOMA_LPHASE(4)
+            NOMA_LPHASE(6)
         }
         // ---- epoch loss (hybrid_nn.cpp:190-192): trace[e] = sum r^2 / n -------
         if (rank == 0 && p.trace) {
-            if (tid < kBatchRows) sm[c.red + tid] = loss_acc;
+            if (tid < 32) sm[c.red + tid] = loss_acc;
             __syncthreads();
             if (tid == 0) {
                 double t = 0.0;
-                for (int i = 0; i < kBatchRows; ++i) t += sm[c.red + i];
+                for (int i = 0; i < 32; ++i) t += sm[c.red + i];
                 p.trace[(size_t)net * p.epochs + e] = t / (double)n;
             }
             __syncthreads();
         }
         loss_acc = 0.0f;
     }
-    NOMA_LPHASE(5)
+    NOMA_LPHASE(7)
     if (clk_on)
-        for (int i = 0; i < 6; ++i) p.clocks[i] = clk_acc[i];
+        for (int i = 0; i < 8; ++i) p.clocks[i] = clk_acc[i];
 #undef NOMA_LPHASE
     // ---- own slice of the trained parameters back to the FusedPlan layout ----
-    float *po = p.plans + (size_t)net * g.plan_total;
-    for (int l = 1; l <= N; ++l) {
-        const int J = c.J[l], C = c.cin[l];
-        for (int i = tid; i < J * C; i += kLT) {
-            const int j = i / C, k = i % C;
-            po[g.plan_w[l] + (rank * J + j) * g.plan_pad[l - 1] + k] = sm[c.w[l] + j * c.sw[l] + k];
+    const int pf = (total & 1) * c.npar;  // copy written by the last step
+    float *pout = p.plans + (size_t)net * g.plan_total;
+#pragma unroll
+    for (int l = 1; l <= NL; ++l) {
+        const int C = g.dims[l - 1];
+        for (int i = tid; i < JT * C; i += kLT) {
+            const int j = i / C, k = i - j * C;
+            pout[g.plan_w[l] + (rank * JT + j) * g.plan_pad[l - 1] + k] = sm[pf + c.w[l] + j * c.sw[l] + k];
         }
-        for (int j = tid; j < J; j += kLT) po[g.plan_b[l] + rank * J + j] = sm[c.b[l] + j];
+        if (tid < JT) pout[g.plan_b[l] + rank * JT + tid] = sm[pf + c.b[l] + tid];
     }
-    for (int j = tid; j < c.J[N]; j += kLT) po[g.plan_f + rank * c.J[N] + j] = sm[c.wf + j];
+    if (tid < JT) pout[g.plan_f + rank * JT + tid] = sm[pf + c.wf + tid];
     cl_sync();  // no CTA leaves while a peer could still address its shared memory
 }
 
@@ -610,13 +693,15 @@ int train_lat_launch(TrainParams &p, cudaStream_t st) {
     int want = 0;
     if (const char *f = std::getenv("NOMA_LAT_CLUSTER")) want = std::atoi(f);
     if (want == 1) return NOMA_ERR_UNSUPPORTED;
-    const int cand[4] = {16, 8, 4, 2};
-    for (int ci = 0; ci < 4; ++ci) {
+    const long total = (long)((p.rows + p.batch - 1) / p.batch) * p.epochs;
+    if (total < 1 || total > kLatMaxSteps) return NOMA_ERR_UNSUPPORTED;
+    const int cand[3] = {16, 8, 4};
+    for (int ci = 0; ci < 3; ++ci) {
         const int cs = cand[ci];
         if (want && cs != want) continue;
         if (!want && p.n_nets * cs > sms) continue;
         LatCarve c;
-        if (!lat_carve(p.g, cs, p.width, &c)) continue;
+        if (!lat_carve(p.g, cs, p.width, (int)total, &c)) continue;
         const size_t smem = (size_t)c.end * sizeof(float);
         auto launch = [&](auto kern) -> int {
             cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -644,13 +729,25 @@ int train_lat_launch(TrainParams &p, cudaStream_t st) {
             }
             return NOMA_OK;
         };
+        const int vw = p.width <= 32 ? 2 : 4;  // float4 per gather thread
+        auto pick = [&](auto cs_t, auto jt_t) -> int {
+            constexpr int CS = decltype(cs_t)::value, JT = decltype(jt_t)::value;
+            if (c.N == 1) return vw == 2 ? launch(train_lat_kernel<CS, JT, 1, 2>) : launch(train_lat_kernel<CS, JT, 1, 4>);
+            if constexpr (JT >= 4 && CS * JT <= 64)
+                return vw == 2 ? launch(train_lat_kernel<CS, JT, 2, 2>) : launch(train_lat_kernel<CS, JT, 2, 4>);
+            return NOMA_ERR_UNSUPPORTED;
+        };
+        using I16 = std::integral_constant<int, 16>;
+        using I8 = std::integral_constant<int, 8>;
+        using I4 = std::integral_constant<int, 4>;
+        using I2 = std::integral_constant<int, 2>;
         int r = NOMA_ERR_UNSUPPORTED;
-        switch (cs) {
-            case 16: r = launch(train_lat_kernel<16>); break;
-            case 8: r = launch(train_lat_kernel<8>); break;
-            case 4: r = launch(train_lat_kernel<4>); break;
-            default: r = launch(train_lat_kernel<2>); break;
-        }
+        if (cs == 16 && c.jt == 2) r = pick(I16(), I2());
+        else if (cs == 16 && c.jt == 4) r = pick(I16(), I4());
+        else if (cs == 16 && c.jt == 8) r = pick(I16(), I8());
+        else if (cs == 8 && c.jt == 4) r = pick(I8(), I4());
+        else if (cs == 8 && c.jt == 8) r = pick(I8(), I8());
+        else if (cs == 4 && c.jt == 8) r = pick(I4(), I8());
         if (r == NOMA_OK) {
             p.mode = 100 + cs;
             return NOMA_OK;

@@ -42,29 +42,41 @@ def _devs(out, ref):
     return soft, trace
 
 
-@pytest.mark.parametrize("cs,hidden", [
-    (2, [32]), (4, [32]), (8, [32]), (16, [32]),
-    (2, [32, 32]), (4, [32, 32]), (8, [32, 32]),
-    (4, [32, 32, 32]), (2, [64, 32]),
+@pytest.mark.parametrize("cs,M,hidden", [
+    (16, 16, [32]), (16, 16, [64]), (16, 16, [128]), (8, 16, [32]), (8, 16, [64]), (4, 16, [32]),
+    (16, 16, [64, 64]), (8, 16, [32, 32]), (8, 16, [64, 64]), (4, 16, [32, 32]),
+    (16, 32, [64]), (16, 32, [64, 64]),
 ])
-def test_latency_cluster_matches_oracle(A, O, cs, hidden, monkeypatch):
+def test_latency_cluster_matches_oracle(A, O, cs, M, hidden, monkeypatch):
+    """Every (cluster size, own neurons per CTA, layers, input width) instance
+    of the latency kernel against the FP64 oracle (short training)."""
     monkeypatch.setenv("NOMA_LAT_CLUSTER", str(cs))
-    out, ref = _run(A, O, M=4, K=3, hidden=hidden, NT=100, ND=256, epochs=3)
+    out, ref = _run(A, O, M=M, K=3, hidden=hidden, NT=100, ND=256, epochs=3)
     assert A.context().train_mode == 100 + cs
     assert (out.status == 0).all()
     soft, trace = _devs(out, ref)
-    record("latency_cluster", config=f"cs={cs} hidden={hidden}", soft_dev=soft, trace_dev=trace)
+    record("latency_cluster", config=f"cs={cs} M={M} hidden={hidden}", soft_dev=soft, trace_dev=trace)
     assert soft < 1e-4 and trace < 1e-4, (soft, trace)
 
 
 @pytest.mark.parametrize("NT", [64, 100, 129])
 def test_latency_ragged_minibatches(A, O, NT, monkeypatch):
     """2 N_T = 128 (one full batch per epoch), 200 (128 + 72), 258 (128+128+2)."""
-    monkeypatch.setenv("NOMA_LAT_CLUSTER", "8")
-    out, ref = _run(A, O, M=4, K=2, hidden=[16], NT=NT, ND=64, epochs=4)
-    assert A.context().train_mode == 108
+    monkeypatch.setenv("NOMA_LAT_CLUSTER", "16")
+    out, ref = _run(A, O, M=16, K=2, hidden=[64], NT=NT, ND=64, epochs=4)
+    assert A.context().train_mode == 116
     soft, trace = _devs(out, ref)
     assert soft < 1e-4 and trace < 1e-4, (NT, soft, trace)
+
+
+def test_latency_unsupported_shape_falls_back(A, O, monkeypatch):
+    """Unequal hidden widths are outside the latency kernel: the pipeline
+    runs the one-CTA-per-net kernel instead, with the same results."""
+    monkeypatch.setenv("NOMA_LAT_CLUSTER", "16")
+    out, ref = _run(A, O, M=16, K=2, hidden=[64, 32], NT=100, ND=64, epochs=3)
+    assert A.context().train_mode < 100
+    soft, trace = _devs(out, ref)
+    assert soft < 1e-4 and trace < 1e-4
 
 
 def test_latency_c1_single_slot(A, O):
@@ -84,7 +96,7 @@ def test_latency_c1_single_slot(A, O):
 
 def test_latency_deterministic(A, O, monkeypatch):
     monkeypatch.setenv("NOMA_LAT_CLUSTER", "16")
-    a, _ = _run(A, O, M=4, K=3, hidden=[32], NT=100, ND=64, epochs=5)
-    b, _ = _run(A, O, M=4, K=3, hidden=[32], NT=100, ND=64, epochs=5)
+    a, _ = _run(A, O, M=16, K=3, hidden=[64, 64], NT=100, ND=64, epochs=5)
+    b, _ = _run(A, O, M=16, K=3, hidden=[64, 64], NT=100, ND=64, epochs=5)
     assert np.array_equal(a.plans, b.plans)
     assert np.array_equal(a.trace, b.trace)

@@ -22,6 +22,7 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--configs", default="c1,c2")
 ap.add_argument("--clusters", default="1,2,4")
 ap.add_argument("--reps", type=int, default=6)
+ap.add_argument("--lat", default="", help="NOMA_LAT_CLUSTER values to sweep (latency kernel)")
 args = ap.parse_args()
 dev = torch.device("cuda", 0)
 ctx = N.Context(0)
@@ -46,8 +47,13 @@ for tag in args.configs.split(","):
     errs = torch.empty((1, K), dtype=torch.int32, device=dev)
     codes = torch.empty((1, K, ND), dtype=torch.uint8, device=dev)
     tcfg = N.TrainCfg.of(bench.EPOCHS, bench.BATCH, bench.LR)
-    for cs in args.clusters.split(","):
-        os.environ["NOMA_TRAIN_CLUSTER"] = cs
+    sweep = [("lat", v) for v in args.lat.split(",") if v] or [("row", v) for v in args.clusters.split(",")]
+    for kind, cs in sweep:
+        os.environ.pop("NOMA_LAT_CLUSTER", None)
+        if kind == "lat":
+            os.environ["NOMA_LAT_CLUSTER"] = cs
+        else:
+            os.environ["NOMA_TRAIN_CLUSTER"] = cs
         os.environ.pop("NOMA_PHASE_CLOCKS", None)
         tot, ph = [], []
         ctx.set_profiling(True)
@@ -68,7 +74,7 @@ for tag in args.configs.split(","):
                      codes=codes, bit_errors=errs)
         torch.cuda.synchronize()
         os.environ.pop("NOMA_PHASE_CLOCKS", None)
-        print(json.dumps({"config": tag, "cluster": cs, "latency_us": statistics.median(tot),
+        print(json.dumps({"config": tag, "cluster": f"{kind}{cs}", "train_mode": ctx.train_mode, "latency_us": statistics.median(tot),
                           "phase_us": {k: round(1e3 * statistics.median(p[k] for p in ph), 1)
                                        for k in ph[0]},
                           "bit_errors": errs.cpu().tolist()}), flush=True)
