@@ -731,18 +731,26 @@ NOMA_API int noma_pipeline(noma_ctx_t c, const noma_net_desc *desc, const noma_t
         tp.trace = dt;
         tp.status = dst;
         const bool clocks = std::getenv("NOMA_PHASE_CLOCKS") != nullptr;
-        if (clocks) tp.clocks = s.scratch<long long>(8);
-        if (clocks && tp.clocks) cudaMemsetAsync(tp.clocks, 0, 8 * sizeof(long long), c->stream);
+        // [0..8) phase totals, [8..) per-warp timeline of 4 steps (latency kernel)
+        constexpr int kClk = 8 + 4 * 16 * 10;
+        if (clocks) tp.clocks = s.scratch<long long>(kClk);
+        if (clocks && tp.clocks) cudaMemsetAsync(tp.clocks, 0, kClk * sizeof(long long), c->stream);
         st = train_launch(tp, c->stream);
         c->train_mode = tp.mode;
         if (st) return st == NOMA_ERR_CUDA ? cuda_fail(c, "train") : fail(c, st, "train: unsupported network shape");
         c->launches += 1;
         if (clocks) {  // instrumentation only: per-phase cycles of net 0
-            long long h[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-            cudaMemcpyAsync(h, tp.clocks, sizeof(h), cudaMemcpyDeviceToHost, c->stream);
+            std::vector<long long> h(kClk, 0);
+            cudaMemcpyAsync(h.data(), tp.clocks, kClk * sizeof(long long), cudaMemcpyDeviceToHost, c->stream);
             cudaStreamSynchronize(c->stream);
             std::fprintf(stderr, "NOMA_PHASE_CLOCKS mode %d: %lld %lld %lld %lld %lld %lld %lld %lld\n",
                          tp.mode, h[0], h[1], h[2], h[3], h[4], h[5], h[6], h[7]);
+            if (const char *path = std::getenv("NOMA_PHASE_TRACE")) {
+                if (FILE *f = std::fopen(path, "w")) {
+                    for (int i = 8; i < kClk; ++i) std::fprintf(f, "%lld\n", h[i]);
+                    std::fclose(f);
+                }
+            }
         }
     }
     mark(c, 6);

@@ -138,6 +138,16 @@ __device__ __forceinline__ void reduce_scatter(float (&v)[N], int lane) {
 
 constexpr int ilog2c(int v) { return v <= 1 ? 0 : 1 + ilog2c(v / 2); }
 
+// Compile-time loop B, B+S, ... (exclusive E): the body sees an
+// integral_constant, so layer-dependent tile shapes are constants.
+template <int B, int E, int S, typename F>
+__device__ __forceinline__ void static_for(F &&f) {
+    if constexpr ((S > 0 && B < E) || (S < 0 && B > E)) {
+        f(std::integral_constant<int, B>());
+        static_for<B + S, E, S>(f);
+    }
+}
+
 }  // namespace
 
 constexpr int kLatMaxV = 4;         // float4 per gather thread: input width <= 64
@@ -249,6 +259,10 @@ __global__ void __launch_bounds__(kLT, 1) train_lat_kernel(TrainParams p, LatCar
         clk_acc[I] += now - clk_prev;                             \
         clk_prev = now;                                           \
     }
+    // per-warp timeline of steps 100-103 (lane 0 of every warp of block 0)
+    long long *tl = p.clocks && blockIdx.x == 0 && lane == 0 ? p.clocks + 8 + warp * 10 : nullptr;
+#define NOMA_TL(PT)                                                              \
+    if (tl && s >= 100 && s < 104) tl[(s - 100) * 160 + (PT)] = clock64();
 
     for (int i = tid; i < c.bars; i += kLT) sm[i] = 0.0f;
     __syncthreads();
@@ -287,58 +301,66 @@ __global__ void __launch_bounds__(kLT, 1) train_lat_kernel(TrainParams p, LatCar
     }
 
     // ---- step schedule and the two-stage gather prefetch --------------------
-    // Thread t gathers float4 columns 4(t/128 + 4v) of minibatch row t%128:
-    // the complex row idx/2 of slot d; odd widened rows read the other half
-    // (offset +-M) and negate Re (iq_transform.cpp:17-20).
+    // Warps 4-15 gather (warps 0-3 are on the critical yp/residual path):
+    // thread t' = tid - 128 owns minibatch row t' % 128 and float4 columns
+    // f = t'/128 + 3m of it -- the complex row idx/2 of slot d; odd widened
+    // rows read the other half (offset +-M) and negate Re (iq_transform.cpp:17-20).
+    constexpr int W0 = 16 * VW;       // input width 2M
+    constexpr int NV = W0 / 4;        // float4 per widened row
+    constexpr int GI = (NV + 2) / 3;  // float4 per gather thread
     const int spe = (n + p.batch - 1) / p.batch;  // steps per epoch
     const int total = c.total;
-    const int gr = tid & (kBatchRows - 1), gh = tid >> 7;
-    const float *dsrc = p.design32 + (wid ? (size_t)d * (n >> 1) : (size_t)d * n) * width;
+    const bool gatherer = tid >= 128;
+    const int gt = gatherer ? tid - 128 : 0;
+    const int gr = gt & (kBatchRows - 1), gq = gt >> 7;
+    const float *dsrc = p.design32 + (wid ? (size_t)d * (n >> 1) : (size_t)d * n) * W0;
     const float *r0src = p.r0 + (size_t)net * n;
     const uint16_t *psrc = p.perm + (size_t)net * p.epochs * n;
-    int colv[VW], offo[VW];
-    bool okv[VW], negv[VW];
+    int colv[GI], offo[GI];
+    bool okv[GI], negv[GI];
 #pragma unroll
-    for (int v = 0; v < VW; ++v) {
-        const int col = 4 * (gh + 4 * v);
-        okv[v] = col < width;
+    for (int v = 0; v < GI; ++v) {
+        const int col = 4 * (gq + 3 * v);
+        okv[v] = gatherer && col < W0;
         colv[v] = okv[v] ? col : 0;
         offo[v] = wid ? (col < M ? M : -M) : 0;
         negv[v] = wid && col >= M;
     }
     auto perm_at = [&](int e, int st, int r) -> int {  // perm index, or -1 past the batch
         const int start = st * p.batch;
-        return r < min(p.batch, n - start) ? (int)psrc[e * n + start + r] : -1;
+        return gatherer && r < min(p.batch, n - start) ? (int)psrc[e * n + start + r] : -1;
     };
-    float4 rowv[VW];
-    float rowr0 = 0.0f;
+    // raw loads stay in registers until store_row one step later (the sign of
+    // odd rows is applied there, so nothing waits on the loads here)
+    float4 rowv[GI];
+    float rowr0 = 0.0f, rowsg = 0.0f, rowsgn = 0.0f;  // sign: even / odd-row Re half
     auto load_row = [&](int idx) {
         const bool valid = idx >= 0;
         const int ii = valid ? idx : 0;
         const bool odd = wid && (ii & 1);
-        const float *src = dsrc + (wid ? ii >> 1 : ii) * width;
+        const float *src = dsrc + (wid ? ii >> 1 : ii) * W0;
 #pragma unroll
-        for (int v = 0; v < VW; ++v) {
-            float4 x = make_float4(0.f, 0.f, 0.f, 0.f);
-            if (okv[v]) x = *reinterpret_cast<const float4 *>(src + colv[v] + (odd ? offo[v] : 0));
-            const float sg = !valid ? 0.f : (odd && negv[v]) ? -1.f : 1.f;
-            rowv[v] = make_float4(sg * x.x, sg * x.y, sg * x.z, sg * x.w);
-        }
-        rowr0 = (valid && gh == 0) ? r0src[ii] : 0.0f;
+        for (int v = 0; v < GI; ++v)
+            rowv[v] = okv[v] ? *reinterpret_cast<const float4 *>(src + colv[v] + (odd ? offo[v] : 0))
+                             : make_float4(0.f, 0.f, 0.f, 0.f);
+        rowsg = valid ? 1.0f : 0.0f;
+        rowsgn = odd ? -rowsg : rowsg;
+        rowr0 = gatherer && gq == 0 ? r0src[ii] : 0.0f;
     };
     auto store_row = [&](int buf) {
-        float *xt = sm + c.xt + buf * width * kSR + gr;
+        float *xt = sm + c.xt + buf * W0 * kSR + gr;
 #pragma unroll
-        for (int v = 0; v < VW; ++v) {
+        for (int v = 0; v < GI; ++v) {
             if (okv[v]) {
+                const float sg = negv[v] ? rowsgn : rowsg;
                 float *q = xt + colv[v] * kSR;
-                q[0] = rowv[v].x;
-                q[kSR] = rowv[v].y;
-                q[2 * kSR] = rowv[v].z;
-                q[3 * kSR] = rowv[v].w;
+                q[0] = sg * rowv[v].x;
+                q[kSR] = sg * rowv[v].y;
+                q[2 * kSR] = sg * rowv[v].z;
+                q[3 * kSR] = sg * rowv[v].w;
             }
         }
-        if (gh == 0) sm[c.r0b + buf * kBatchRows + gr] = rowr0;
+        if (gatherer && gq == 0) sm[c.r0b + buf * kBatchRows + gr] = rowsg * rowr0;
     };
     load_row(total > 0 ? perm_at(0, 0, gr) : -1);
     store_row(0);
@@ -356,10 +378,16 @@ __global__ void __launch_bounds__(kLT, 1) train_lat_kernel(TrainParams p, LatCar
 #pragma unroll
     for (int l = 0; l <= NL; ++l) mw[l] = vw[l] = mb[l] = vb[l] = 0.f;
 
-    // forward thread map: 8 k-split lanes x 32 row quads (threads < 256)
-    const int fkq = tid & 7, frq = (tid >> 3) & 31;
-    constexpr int FV = JT / 2;                     // values per lane after the k reduce
-    const int fj = (fkq * FV) >> 2, fr = (fkq * FV) & 3;  // neuron, first row of them
+    // forward thread map: 8 k-split lanes x 32 row quads x 2 neuron halves;
+    // after the k reduce-scatter a lane holds FV values (neuron fj, rows
+    // 4 frq + fr ..), or -- with one neuron per half -- one value on 2 lanes
+    constexpr int JPF = JT / 2;                  // neurons per forward thread
+    constexpr int FVV = 4 * JPF;                 // values before the reduce
+    constexpr int FV = FVV >= 8 ? FVV / 8 : 1;   // values per lane after it
+    const int fkq = tid & 7, frq = (tid >> 3) & 31, fjh = tid >> 8;
+    const int fbase = FVV >= 8 ? fkq * FV : fkq >> (3 - ilog2c(FVV));
+    const bool fown = FVV >= 8 || (fkq & ((8 / FVV) - 1)) == 0;
+    const int fj = fjh * JPF + (fbase >> 2), fr = fbase & 3;
 
     float loss_acc = 0.0f;
     int s = 0;
@@ -370,25 +398,27 @@ __global__ void __launch_bounds__(kLT, 1) train_lat_kernel(TrainParams p, LatCar
             const int start = st * p.batch, bsz = min(p.batch, n - start);
             const float *XT = sm + c.xt + buf * width * kSR;
             const int po = buf * c.npar, pn = (buf ^ 1) * c.npar;  // param copy: read, write
+            NOMA_TL(0)
             // ---- forward (hybrid_nn.cpp:60-72): all JT own neurons x 4 rows per
             // thread, k split over 8 lanes, lane reduce-scatter --------------
-#pragma unroll
-            for (int l = 1; l <= NL; ++l) {
-                const int NC = (l == 1 ? width : H) >> 2;
+static_for<1, NL + 1, 1>([&](auto LC) {
+                constexpr int l = decltype(LC)::value;
+                const int NC = (l == 1 ? W0 : H) >> 2;
                 const float *in = l == 1 ? XT : sm + c.af[l - 1];
-                const float *W = sm + po + c.w[l];
+                const float *W = sm + po + c.w[l] + fjh * JPF * c.sw[l];
                 const int sw = c.sw[l];
-                if (tid < 256) {
-                    f2_t acc[JT][2];
+                {
+                    f2_t acc[JPF][2];
 #pragma unroll
-                    for (int j = 0; j < JT; ++j) acc[j][0] = acc[j][1] = 0ull;
+                    for (int j = 0; j < JPF; ++j) acc[j][0] = acc[j][1] = 0ull;
+#pragma unroll
                     for (int kc = fkq; kc < NC; kc += 8) {
                         const float *ip = in + 4 * kc * kSR + 4 * frq;
                         ulonglong2 x[4];
 #pragma unroll
                         for (int kk = 0; kk < 4; ++kk) x[kk] = *reinterpret_cast<const ulonglong2 *>(ip + kk * kSR);
 #pragma unroll
-                        for (int j = 0; j < JT; ++j) {
+                        for (int j = 0; j < JPF; ++j) {
                             const float4 w4 = *reinterpret_cast<const float4 *>(W + j * sw + 4 * kc);
                             const float wk[4] = {w4.x, w4.y, w4.z, w4.w};
 #pragma unroll
@@ -399,26 +429,28 @@ __global__ void __launch_bounds__(kLT, 1) train_lat_kernel(TrainParams p, LatCar
                             }
                         }
                     }
-                    float v[4 * JT];
+                    float v[FVV];
 #pragma unroll
-                    for (int j = 0; j < JT; ++j) {
+                    for (int j = 0; j < JPF; ++j) {
                         const float2 a = f2_unpack(acc[j][0]), b = f2_unpack(acc[j][1]);
                         v[4 * j] = a.x;
                         v[4 * j + 1] = a.y;
                         v[4 * j + 2] = b.x;
                         v[4 * j + 3] = b.y;
                     }
-                    reduce_scatter<4 * JT, 4 * JT, 8>(v, lane);
+                    reduce_scatter<FVV, FVV, 8>(v, lane);
                     const float bj = sm[po + c.b[l] + fj];
 #pragma unroll
                     for (int i = 0; i < FV; ++i) v[i] = fmaxf(v[i] + bj, 0.f);
                     const int r = 4 * frq + fr;
-                    sts_n<FV>((l == NL ? sm + c.aN : sm + c.aloc[l]) + fj * kSR + r, v);
-                    if (l < NL) {  // all-gather a_l into every CTA (incl. this one)
-                        const uint32_t la = s2u(sm + c.af[l] + (rank * JT + fj) * kSR + r);
-                        const uint32_t lb = s2u(bars + 2 + 2 * (l - 1));
+                    if (fown) {
+                        sts_n<FV>((l == NL ? sm + c.aN : sm + c.aloc[l]) + fj * kSR + r, v);
+                        if (l < NL) {  // all-gather a_l into every CTA (incl. this one)
+                            const uint32_t la = s2u(sm + c.af[l] + (rank * JT + fj) * kSR + r);
+                            const uint32_t lb = s2u(bars + 2 + 2 * (l - 1));
 #pragma unroll
-                        for (int q = 0; q < CS; ++q) st_async_n<FV>(mapa(la, q), v, mapa(lb, q));
+                            for (int q = 0; q < CS; ++q) st_async_n<FV>(mapa(la, q), v, mapa(lb, q));
+                        }
                     }
                 }
                 if (l < NL) {
@@ -428,10 +460,12 @@ __global__ void __launch_bounds__(kLT, 1) train_lat_kernel(TrainParams p, LatCar
                     // CTA has finished step s)
                     if (tid == 0) mbar_arm(lb, agbytes);
                 }
-            }
+            });
             NOMA_LPHASE(0)
+            NOMA_TL(1)
             __syncthreads();
             NOMA_LPHASE(1)
+            NOMA_TL(2)
             // ---- final-layer partials yp (hybrid_nn.cpp:81): warps 0-3 send --
             const uint32_t ybar = s2u(bars + buf);
             if (warp < 4) {
@@ -452,6 +486,7 @@ __global__ void __launch_bounds__(kLT, 1) train_lat_kernel(TrainParams p, LatCar
 #pragma unroll
                 for (int q = warp; q < CS; q += 4) st_async4(mapa(la, q), y, mapa(ybar, q));
             }
+            NOMA_TL(3)
             // ---- gather: store the rows of step s+1, load step s+2's ----------
             if (s + 1 < total) {
                 store_row(buf ^ 1);
@@ -463,11 +498,13 @@ __global__ void __launch_bounds__(kLT, 1) train_lat_kernel(TrainParams p, LatCar
                 ++e3;
             }
             NOMA_LPHASE(2)
+            NOMA_TL(4)
             // ---- residual a_N w - r0, dy = 2 r / B (hybrid_nn.cpp:94-98): warp 0,
             // 4 rows per lane, partials summed in rank order ------------------
             if (warp == 0) {
                 mbar_wait(ybar, (uint32_t)((s >> 1) & 1));
                 NOMA_LPHASE(3)
+                NOMA_TL(5)
                 const int r0 = 4 * lane;
                 const float *ya = sm + c.yall + buf * CS * kBatchRows + r0;
                 float4 yh = *reinterpret_cast<const float4 *>(ya);
@@ -489,17 +526,17 @@ __global__ void __launch_bounds__(kLT, 1) train_lat_kernel(TrainParams p, LatCar
                 loss_acc = fmaf(res.z, res.z, loss_acc);
                 loss_acc = fmaf(res.w, res.w, loss_acc);
             }
+            NOMA_TL(6)
             __syncthreads();
             if (tid == 0) mbar_arm(ybar, ybytes);  // phase for step s+2
             NOMA_LPHASE(4)
+            NOMA_TL(7)
             // ---- backward (hybrid_nn.cpp:99-112) fused with Adam (:118-144) ---
             const float lrc = sm[c.atab + 2 * s], ic2 = sm[c.atab + 2 * s + 1];
-#pragma unroll
-            for (int l = NL; l >= 1; --l) {
-                constexpr int dummy = 0;
-                (void)dummy;
+static_for<NL, 0, -1>([&](auto LC) {
+                constexpr int l = decltype(LC)::value;
                 const bool top = l == NL;
-                const int NC = (l == 1 ? width : H) >> 2;
+                const int NC = (l == 1 ? W0 : H) >> 2;
                 const float *zsrc = top ? sm + c.aN : sm + c.aloc[l];  // a_N, or dZ_l in place
                 const float *dyp = sm + c.dy, *wfp = sm + po + c.wf;
                 const float *in = l == 1 ? XT : sm + c.af[l - 1];
@@ -545,11 +582,17 @@ __global__ void __launch_bounds__(kLT, 1) train_lat_kernel(TrainParams p, LatCar
                 // weight gradient dZ^T A (:109), bias colsum (:110), final a_N^T dy
                 // (:99): warp ct owns column tile 4ct..4ct+3 for all JT neurons,
                 // lane = row quad; lane reduce-scatter, then Adam in registers.
-                if (warp < NC) {
-                    const int ct = warp, r = 4 * lane;
-                    f2_t acc[JT][4], sb[JT], sf[JT];
+                {
+                    // warp -> column tile ct (4 columns) x neuron group jg
+                    // (JPB neurons): JS = 16 / NC groups cover all 16 warps
+                    constexpr int NCL = (l == 1 ? W0 : H) / 4;
+                    constexpr int JS = NCL >= 16 ? 1 : 16 / NCL;
+                    constexpr int JPB = JT / JS;
+                    const int ct = warp % NCL, jg = warp / NCL, r = 4 * lane;
+                    const int j0 = jg * JPB;
+                    f2_t acc[JPB][4], sb[JPB], sf[JPB];
 #pragma unroll
-                    for (int j = 0; j < JT; ++j) {
+                    for (int j = 0; j < JPB; ++j) {
                         sb[j] = sf[j] = 0ull;
 #pragma unroll
                         for (int q = 0; q < 4; ++q) acc[j][q] = 0ull;
@@ -561,12 +604,12 @@ __global__ void __launch_bounds__(kLT, 1) train_lat_kernel(TrainParams p, LatCar
                     if (top) y4 = *reinterpret_cast<const float4 *>(dyp + r);
                     const f2_t one = f2_bcast(1.0f);
 #pragma unroll
-                    for (int j = 0; j < JT; ++j) {
-                        float4 z = *reinterpret_cast<const float4 *>(zsrc + j * kSR + r);
+                    for (int j = 0; j < JPB; ++j) {
+                        float4 z = *reinterpret_cast<const float4 *>(zsrc + (j0 + j) * kSR + r);
                         if (top) {  // dZ_N = (a_N > 0) dy w_j on the fly (:102-107)
                             ffma2(sf[j], f2_pack(z.x, z.y), f2_pack(y4.x, y4.y));
                             ffma2(sf[j], f2_pack(z.z, z.w), f2_pack(y4.z, y4.w));
-                            const float f = wfp[j];
+                            const float f = wfp[j0 + j];
                             z = make_float4(z.x > 0.f ? y4.x * f : 0.f, z.y > 0.f ? y4.y * f : 0.f,
                                             z.z > 0.f ? y4.z * f : 0.f, z.w > 0.f ? y4.w * f : 0.f);
                         }
@@ -579,19 +622,19 @@ __global__ void __launch_bounds__(kLT, 1) train_lat_kernel(TrainParams p, LatCar
                             ffma2(acc[j][q], zb, x[q].y);
                         }
                     }
-                    float gv[4 * JT];
+                    float gv[4 * JPB];
 #pragma unroll
-                    for (int j = 0; j < JT; ++j)
+                    for (int j = 0; j < JPB; ++j)
 #pragma unroll
                         for (int q = 0; q < 4; ++q) {
                             const float2 h = f2_unpack(acc[j][q]);
                             gv[4 * j + q] = h.x + h.y;
                         }
-                    reduce_scatter<4 * JT, 4 * JT, 32>(gv, lane);
-                    constexpr int GSH = 5 - ilog2c(4 * JT);  // replicas: 2^GSH lanes per weight
-                    const int gi = lane >> GSH;               // j * 4 + q
+                    reduce_scatter<4 * JPB, 4 * JPB, 32>(gv, lane);
+                    constexpr int GSH = 5 - ilog2c(4 * JPB);  // replicas: 2^GSH lanes per weight
+                    const int gi = lane >> GSH;                // j * 4 + q within the group
                     if ((lane & ((1 << GSH) - 1)) == 0) {
-                        const int off = (gi >> 2) * sw + 4 * ct + (gi & 3);
+                        const int off = (j0 + (gi >> 2)) * sw + 4 * ct + (gi & 3);
                         const float gsum = gv[0];
                         const float m1 = p.b1 * mw[l] + p.omb1 * gsum;
                         const float m2 = p.b2 * vw[l] + p.omb2 * (gsum * gsum);
@@ -600,18 +643,18 @@ __global__ void __launch_bounds__(kLT, 1) train_lat_kernel(TrainParams p, LatCar
                         sm[pn + c.w[l] + off] = sm[po + c.w[l] + off] - __fdividef(lrc * m1, sqrtf(m2 * ic2) + p.eps);
                     }
                     if (ct == 0) {  // biases, then final weights (top layer)
-                        float bv[2 * JT];
+                        float bv[2 * JPB];
 #pragma unroll
-                        for (int j = 0; j < JT; ++j) {
+                        for (int j = 0; j < JPB; ++j) {
                             const float2 hb = f2_unpack(sb[j]), hf = f2_unpack(sf[j]);
                             bv[j] = hb.x + hb.y;
-                            bv[JT + j] = hf.x + hf.y;
+                            bv[JPB + j] = hf.x + hf.y;
                         }
-                        reduce_scatter<2 * JT, 2 * JT, 32>(bv, lane);
-                        constexpr int BSH = 5 - ilog2c(2 * JT);
+                        reduce_scatter<2 * JPB, 2 * JPB, 32>(bv, lane);
+                        constexpr int BSH = 5 - ilog2c(2 * JPB);
                         const int bi = lane >> BSH;
-                        if ((lane & ((1 << BSH) - 1)) == 0 && (top || bi < JT)) {
-                            const int off = bi < JT ? c.b[l] + bi : c.wf + bi - JT;
+                        if ((lane & ((1 << BSH) - 1)) == 0 && (top || bi < JPB)) {
+                            const int off = bi < JPB ? c.b[l] + j0 + bi : c.wf + j0 + bi - JPB;
                             const float gsum = bv[0];
                             const float m1 = p.b1 * mb[l] + p.omb1 * gsum;
                             const float m2 = p.b2 * vb[l] + p.omb2 * (gsum * gsum);
@@ -645,10 +688,12 @@ __global__ void __launch_bounds__(kLT, 1) train_lat_kernel(TrainParams p, LatCar
                     __syncthreads();
                     if (tid == 0) mbar_arm(rb, rsbytes);
                 }
-            }
+            });
             NOMA_LPHASE(5)
+            NOMA_TL(8)
             __syncthreads();
             NOMA_LPHASE(6)
+            NOMA_TL(9)
         }
         // ---- epoch loss (hybrid_nn.cpp:190-192): trace[e] = sum r^2 / n -------
         if (rank == 0 && p.trace) {
