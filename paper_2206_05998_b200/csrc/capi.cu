@@ -242,6 +242,7 @@ LlsParams lls_params(const noma_dataset *ds, const double *x, const double *y, d
     p.status = status;
     p.design32 = d32;
     p.r0 = r0;
+    p.clocks = nullptr;
     return p;
 }
 
@@ -709,7 +710,20 @@ NOMA_API int noma_pipeline(noma_ctx_t c, const noma_net_desc *desc, const noma_t
     if (perm_launch((int)nets, cfg->epochs, n, sseed, perm, c->side)) return cuda_fail(c, "perm");
     mark(c, 4, c->side);
     cudaEventRecord(c->join, c->side);
-    st = lls_launch(lls_params(&ds, px, py, dw, dc, dst, d32, r0), c->stream);
+    LlsParams lp = lls_params(&ds, px, py, dw, dc, dst, d32, r0);
+    const bool lclk = std::getenv("NOMA_PHASE_CLOCKS") != nullptr;
+    if (lclk) {
+        lp.clocks = s.scratch<long long>(8);
+        if (lp.clocks) cudaMemsetAsync(lp.clocks, 0, 8 * sizeof(long long), c->stream);
+    }
+    st = lls_launch(lp, c->stream);
+    if (lclk && lp.clocks && !st) {
+        long long h[8];
+        cudaMemcpyAsync(h, lp.clocks, sizeof(h), cudaMemcpyDeviceToHost, c->stream);
+        cudaStreamSynchronize(c->stream);
+        std::fprintf(stderr, "NOMA_LLS_CLOCKS gram %lld frob %lld jacobi %lld solve %lld residual %lld sweeps %lld\n",
+                     h[0], h[1], h[2], h[3], h[4], h[5]);
+    }
     if (st) return st == NOMA_ERR_CUDA ? cuda_fail(c, "lls") : fail(c, st, "lls: unsupported shape");
     mark(c, 1);
     cudaStreamWaitEvent(c->stream, c->join, 0);
@@ -732,7 +746,7 @@ NOMA_API int noma_pipeline(noma_ctx_t c, const noma_net_desc *desc, const noma_t
         tp.status = dst;
         const bool clocks = std::getenv("NOMA_PHASE_CLOCKS") != nullptr;
         // [0..8) phase totals, [8..) per-warp timeline of 4 steps (latency kernel)
-        constexpr int kClk = 8 + 4 * 16 * 10;
+        constexpr int kClk = 8 + 4 * 16 * 16;
         if (clocks) tp.clocks = s.scratch<long long>(kClk);
         if (clocks && tp.clocks) cudaMemsetAsync(tp.clocks, 0, kClk * sizeof(long long), c->stream);
         st = train_launch(tp, c->stream);

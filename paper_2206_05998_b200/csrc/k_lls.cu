@@ -26,57 +26,85 @@
 namespace noma_dev {
 
 constexpr int kLlsMaxM = 64;     // complex columns (widened width <= 128)
-constexpr int kLlsChunk = 32;    // rows staged per chunk
 constexpr int kLlsMaxE = 18;     // Gram/RHS entries per thread (registers)
 
-struct cplx { double re, im; };
+__host__ __device__ inline int lls_chunk(int m) { return m <= 16 ? 64 : m <= 32 ? 32 : 16; }
 
-__device__ inline void load_row(const LlsParams &p, int d, int t, int a, double &re, double &im) {
-    if (p.layout == NOMA_LAYOUT_WIDEN_COMPLEX) {
-        const double *x = p.design + (((size_t)d * p.nrow_c + t) * p.m + a) * 2;
-        re = x[0];
-        im = x[1];
-    } else {
-        re = p.design[((size_t)d * p.nrow_c + t) * p.m + a];
-        im = 0.0;
-    }
+__device__ __forceinline__ void cp_async16(void *dst, const void *src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((unsigned)__cvta_generic_to_shared(dst)),
+                 "l"(src)
+                 : "memory");
 }
-
-__device__ inline void load_target(const LlsParams &p, int d, int t, int k, double &re,
-                                   double &im) {
-    if (p.layout == NOMA_LAYOUT_WIDEN_COMPLEX) {
-        const double *y = p.targets + (((size_t)d * p.nrow_c + t) * p.K + k) * 2;
-        re = y[0];
-        im = y[1];
-    } else {
-        re = p.targets[((size_t)d * p.K + k) * p.rows + t];
-        im = 0.0;
-    }
+__device__ __forceinline__ void cp_async8(void *dst, const void *src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"((unsigned)__cvta_generic_to_shared(dst)),
+                 "l"(src)
+                 : "memory");
 }
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
+// MAXE Gram/RHS entries per thread; ILP independent partial sums per entry
+// (small problems: one entry per thread, split over ILP row phases).
+template <int MAXE, int ILP>
 __global__ void __launch_bounds__(kThreads) lls_kernel(LlsParams p) {
     extern __shared__ __align__(16) double smem[];
     const int m = p.m, K = p.K, d = blockIdx.x, tid = threadIdx.x;
+    const int CH = lls_chunk(m);
+    const bool cplx_layout = p.layout == NOMA_LAYOUT_WIDEN_COMPLEX;
     double *A = smem;                       // m*m complex (Gram -> eigenvalues)
     double *V = A + 2 * m * m;              // m*m complex eigenvectors
-    double *D = V + 2 * m * m;              // m*K complex RHS X^H y
-    double *xs = D + 2 * m * K;             // chunk rows: kLlsChunk*m complex
-    double *ys = xs + 2 * kLlsChunk * m;    // chunk targets: kLlsChunk*K complex
-    const int chunk = max(2 * kLlsChunk * m + 2 * kLlsChunk * K, 2 * m * K);
-    double *rot = xs + chunk;               // per pair: c, s, e_re, e_im
+    double *D = V + 2 * m * m;              // m*K complex RHS X^H y, later the solutions c_k
+    double *bufs = D + 2 * m * K;           // 2 x (CH rows of x | CH rows of y), complex
+    const int bstride = 2 * CH * m + 2 * CH * K;
+    double *rot = bufs + 2 * bstride;       // per pair: c, s, e_re, e_im
     double *lam = rot + 4 * (kLlsMaxM / 2 + 1);  // m eigenvalues
-    double *U = xs;                         // m*K complex: V^H d / lambda (reuses chunk)
-    double *red = lam + m;                  // reduction scratch (kThreads)
+    double *red = lam + m;                  // 2 * kThreads reduction scratch
+    double *U = bufs;                       // m*K complex: V^H d / lambda (reuses bufs)
     __shared__ int pair_p[kLlsMaxM / 2 + 1], pair_q[kLlsMaxM / 2 + 1];
-    __shared__ int any_rot;
+    __shared__ int any_rot[2];  // by sweep parity; reset one sweep ahead
 
+    // Staging of CH rows of the design and the targets into buffer b with
+    // cp.async (row-major complex rows are contiguous; REAL rows fill the Re
+    // slots of zeroed buffers).
+    for (int i = tid; i < 2 * bstride; i += kThreads) bufs[i] = 0.0;
+    __syncthreads();
+    const int nch = (p.nrow_c + CH - 1) / CH;
+    auto issue = [&](int ch, int b) {
+        const int t0 = ch * CH, tn = min(CH, p.nrow_c - t0);
+        double *xb = bufs + b * bstride, *yb = xb + 2 * CH * m;
+        if (cplx_layout) {
+            const double *xs = p.design + ((size_t)d * p.nrow_c + t0) * m * 2;
+            const double *ys = p.targets + ((size_t)d * p.nrow_c + t0) * K * 2;
+            for (int i = tid; i < tn * m; i += kThreads) cp_async16(xb + 2 * i, xs + 2 * i);
+            for (int i = tid; i < tn * K; i += kThreads) cp_async16(yb + 2 * i, ys + 2 * i);
+        } else {
+            const double *xs = p.design + ((size_t)d * p.nrow_c + t0) * m;
+            for (int i = tid; i < tn * m; i += kThreads) cp_async8(xb + 2 * i, xs + i);
+            for (int i = tid; i < tn * K; i += kThreads) {
+                const int t = i / K, k = i - t * K;
+                cp_async8(yb + 2 * i, p.targets + ((size_t)d * K + k) * p.rows + t0 + t);
+            }
+        }
+        cp_async_commit();
+    };
+
+    const bool clk = p.clocks && d == 0 && tid == 0;
+    long long ck = clk ? clock64() : 0;
+#define NOMA_LLS_CLK(I)                      \
+    if (clk) {                               \
+        const long long now = clock64();     \
+        p.clocks[I] += now - ck;             \
+        ck = now;                            \
+    }
     // ---- phase A: Gram (upper triangle) and RHS, accumulated in registers.
     const int ngram = m * (m + 1) / 2, nent = ngram + m * K;
-    double acc_re[kLlsMaxE], acc_im[kLlsMaxE];
-    int ea[kLlsMaxE], eb[kLlsMaxE];
+    double acc_re[MAXE][ILP], acc_im[MAXE][ILP];
+    int ea[MAXE], eb[MAXE];
 #pragma unroll
-    for (int e = 0; e < kLlsMaxE; ++e) {
-        acc_re[e] = acc_im[e] = 0.0;
+    for (int e = 0; e < MAXE; ++e) {
+#pragma unroll
+        for (int u = 0; u < ILP; ++u) acc_re[e][u] = acc_im[e][u] = 0.0;
         const int id = tid + e * kThreads;
         ea[e] = eb[e] = -1;
         if (id < ngram) {  // map id -> (a <= b)
@@ -89,82 +117,102 @@ __global__ void __launch_bounds__(kThreads) lls_kernel(LlsParams p) {
             eb[e] = m + (id - ngram) % K;  // b >= m encodes target k = b - m
         }
     }
-    for (int t0 = 0; t0 < p.nrow_c; t0 += kLlsChunk) {
-        const int tn = min(kLlsChunk, p.nrow_c - t0);
-        for (int i = tid; i < tn * m; i += kThreads) {
-            const int t = i / m, a = i % m;
-            double re, im;
-            load_row(p, d, t0 + t, a, re, im);
-            xs[2 * i] = re;
-            xs[2 * i + 1] = im;
-            if (p.design32) {
-                if (p.layout == NOMA_LAYOUT_WIDEN_COMPLEX) {
+    issue(0, 0);
+    for (int ch = 0; ch < nch; ++ch) {
+        if (ch + 1 < nch) {
+            issue(ch + 1, (ch + 1) & 1);
+            cp_async_wait<1>();
+        } else {
+            cp_async_wait<0>();
+        }
+        __syncthreads();
+        const int t0 = ch * CH, tn = min(CH, p.nrow_c - t0);
+        const double *xs = bufs + (ch & 1) * bstride, *ys = xs + 2 * CH * m;
+        if (p.design32) {  // FP32 copy of the design for the training kernels
+            for (int i = tid; i < tn * m; i += kThreads) {
+                const int t = i / m, a = i - t * m;
+                if (cplx_layout) {
                     float *o = p.design32 + ((size_t)d * p.nrow_c + t0 + t) * p.width;
-                    o[a] = (float)re;
-                    o[m + a] = (float)im;
+                    o[a] = (float)xs[2 * i];
+                    o[m + a] = (float)xs[2 * i + 1];
                 } else {
-                    p.design32[((size_t)d * p.nrow_c + t0 + t) * p.width + a] = (float)re;
+                    p.design32[((size_t)d * p.nrow_c + t0 + t) * p.width + a] = (float)xs[2 * i];
                 }
             }
         }
-        for (int i = tid; i < tn * K; i += kThreads) {
-            double re, im;
-            load_target(p, d, t0 + i / K, i % K, re, im);
-            ys[2 * i] = re;
-            ys[2 * i + 1] = im;
-        }
-        __syncthreads();
 #pragma unroll
-        for (int e = 0; e < kLlsMaxE; ++e) {
+        for (int e = 0; e < MAXE; ++e) {
             if (ea[e] < 0) continue;
             const int a = ea[e], b = eb[e];
             const bool rhs = b >= m;
-            double sr = acc_re[e], si = acc_im[e];
-            for (int t = 0; t < tn; ++t) {
-                const double xr = xs[2 * (t * m + a)], xi = xs[2 * (t * m + a) + 1];
-                double br, bi;
-                if (rhs) {
-                    br = ys[2 * (t * K + b - m)];
-                    bi = ys[2 * (t * K + b - m) + 1];
-                } else {
-                    br = xs[2 * (t * m + b)];
-                    bi = xs[2 * (t * m + b) + 1];
-                }
-                sr += xr * br + xi * bi;  // conj(x_a) * b
-                si += xr * bi - xi * br;
-            }
-            acc_re[e] = sr;
-            acc_im[e] = si;
-        }
-        __syncthreads();
-    }
+            const double *bp = rhs ? ys + 2 * (b - m) : xs + 2 * b;
+            const int bst = rhs ? 2 * K : 2 * m;
+            // rows t = u, u + ILP, ...: ILP independent accumulation chains
+            for (int t = 0; t < tn; t += ILP) {
 #pragma unroll
-    for (int e = 0; e < kLlsMaxE; ++e) {
+                for (int u = 0; u < ILP; ++u) {
+                    if (t + u < tn) {
+                        const double xr = xs[2 * ((t + u) * m + a)], xi = xs[2 * ((t + u) * m + a) + 1];
+                        const double br = bp[(t + u) * bst], bi = bp[(t + u) * bst + 1];
+                        acc_re[e][u] += xr * br + xi * bi;  // conj(x_a) * b
+                        acc_im[e][u] += xr * bi - xi * br;
+                    }
+                }
+            }
+        }
+        __syncthreads();  // buffer (ch & 1) is refilled by the next issue
+    }
+    NOMA_LLS_CLK(0)
+    double fro = 0.0;  // squared Frobenius norm of the Gram (rotation invariant)
+#pragma unroll
+    for (int e = 0; e < MAXE; ++e) {
         if (ea[e] < 0) continue;
         const int a = ea[e], b = eb[e];
+        double sre = acc_re[e][0], sim = acc_im[e][0];
+#pragma unroll
+        for (int u = 1; u < ILP; ++u) {  // fixed-order combine of the chains
+            sre += acc_re[e][u];
+            sim += acc_im[e][u];
+        }
+        acc_re[e][0] = sre;
+        acc_im[e][0] = sim;
         if (b >= m) {
-            D[2 * (a * K + b - m)] = acc_re[e];
-            D[2 * (a * K + b - m) + 1] = acc_im[e];
+            D[2 * (a * K + b - m)] = sre;
+            D[2 * (a * K + b - m) + 1] = sim;
         } else {
-            A[2 * (a * m + b)] = acc_re[e];
-            A[2 * (a * m + b) + 1] = acc_im[e];
-            A[2 * (b * m + a)] = acc_re[e];       // Hermitian mirror
-            A[2 * (b * m + a) + 1] = -acc_im[e];
+            A[2 * (a * m + b)] = sre;
+            A[2 * (a * m + b) + 1] = sim;
+            A[2 * (b * m + a)] = sre;       // Hermitian mirror
+            A[2 * (b * m + a) + 1] = -sim;
             if (a == b) A[2 * (a * m + a) + 1] = 0.0;
+            const double sq = sre * sre + (a == b ? 0.0 : sim * sim);
+            fro += a == b ? sq : 2.0 * sq;
         }
     }
     for (int i = tid; i < m * m; i += kThreads) {
         V[2 * i] = (i / m == i % m) ? 1.0 : 0.0;
         V[2 * i + 1] = 0.0;
     }
+    red[tid] = fro;
     __syncthreads();
+    for (int s2 = kThreads / 2; s2 > 0; s2 >>= 1) {
+        if (tid < s2) red[tid] += red[tid + s2];
+        __syncthreads();
+    }
+    // Two-sided Jacobi leaves rounding-level off-diagonals of ~eps ||A||_F, so
+    // that is the rotation threshold (a relative test against sqrt(a_pp a_qq)
+    // never settles for the small noise eigenvalues of a near-far design).
+    const double tol_rot = DBL_EPSILON * sqrt(red[0]);
+    if (tid == 0) any_rot[0] = any_rot[1] = 0;
+    __syncthreads();
+    NOMA_LLS_CLK(1)
 
-    // ---- phase B: cyclic Jacobi, round-robin pairs (circle method).
+    // ---- phase B: cyclic Jacobi, round-robin pairs (circle method); each
+    // round applies A <- U^H A U as independent 2x2 blocks (in place) and
+    // V <- V U, two barriers per round.
     const int mm = m + (m & 1);
     const int npairs = mm / 2;
-    for (int sweep = 0; sweep < 40; ++sweep) {
-        if (tid == 0) any_rot = 0;
-        __syncthreads();
+    for (int sweep = 0; sweep < 30; ++sweep) {
         for (int r = 0; r < mm - 1; ++r) {
             if (tid < npairs) {
                 const int i = tid;
@@ -176,65 +224,103 @@ __global__ void __launch_bounds__(kThreads) lls_kernel(LlsParams p) {
                 if (qq < m) {
                     const double a = A[2 * (pp * m + pp)], b = A[2 * (qq * m + qq)];
                     const double hr = A[2 * (pp * m + qq)], hi = A[2 * (pp * m + qq) + 1];
-                    const double habs = hypot(hr, hi);
-                    if (habs > 0.0 && habs > DBL_EPSILON * 0.5 * sqrt(fabs(a) * fabs(b))) {
-                        er = hr / habs;
-                        ei = hi / habs;
-                        const double th = (b - a) / (2.0 * habs);
-                        const double t = (th >= 0.0 ? 1.0 : -1.0) / (fabs(th) + sqrt(th * th + 1.0));
-                        c = 1.0 / sqrt(t * t + 1.0);
+                    const double h2 = hr * hr + hi * hi;
+                    if (h2 > tol_rot * tol_rot) {
+                        // short dependent chain of FP64 special functions:
+                        // e = h/|h|, th = (b-a)/(2|h|), t = sgn/(|th|+sqrt(th^2+1)),
+                        // c = 1/sqrt(1+t^2), s = t c
+                        const double ih = rsqrt(h2);
+                        er = hr * ih;
+                        ei = hi * ih;
+                        const double th = 0.5 * (b - a) * ih;
+                        const double t = (th >= 0.0 ? 1.0 : -1.0) / (fabs(th) + sqrt(fma(th, th, 1.0)));
+                        c = rsqrt(fma(t, t, 1.0));
                         s = t * c;
-                        any_rot = 1;
+                        any_rot[sweep & 1] = 1;
                     }
-                } else {
-                    pp = qq = -1;
                 }
                 pair_p[i] = pp;
-                pair_q[i] = qq;
+                pair_q[i] = qq;  // qq == m: p is unpaired this round (m odd)
                 rot[4 * i] = c;
                 rot[4 * i + 1] = s;
                 rot[4 * i + 2] = er;
                 rot[4 * i + 3] = ei;
             }
             __syncthreads();
-            // columns: A <- A U, V <- V U
-            for (int it = tid; it < npairs * m * 2; it += kThreads) {
-                const int mat = it / (npairs * m), rem = it % (npairs * m);
-                const int i = rem / m, row = rem % m;
-                const int pp = pair_p[i], qq = pair_q[i];
-                if (pp < 0) continue;
-                const double c = rot[4 * i], s = rot[4 * i + 1];
-                const double er = rot[4 * i + 2], ei = -rot[4 * i + 3];  // e^{-i phi}
-                double *Mx = mat ? V : A;
-                const double xr = Mx[2 * (row * m + pp)], xi = Mx[2 * (row * m + pp) + 1];
-                const double yr = Mx[2 * (row * m + qq)], yi = Mx[2 * (row * m + qq) + 1];
-                const double zr = er * yr - ei * yi, zi = er * yi + ei * yr;  // e^{-i phi} y
-                Mx[2 * (row * m + pp)] = c * xr - s * zr;
-                Mx[2 * (row * m + pp) + 1] = c * xi - s * zi;
-                Mx[2 * (row * m + qq)] = s * xr + c * zr;
-                Mx[2 * (row * m + qq) + 1] = s * xi + c * zi;
-            }
-            __syncthreads();
-            // rows: A <- U^H A
-            for (int it = tid; it < npairs * m; it += kThreads) {
-                const int i = it / m, col = it % m;
-                const int pp = pair_p[i], qq = pair_q[i];
-                if (pp < 0) continue;
-                const double c = rot[4 * i], s = rot[4 * i + 1];
-                const double er = rot[4 * i + 2], ei = rot[4 * i + 3];  // e^{+i phi}
-                const double xr = A[2 * (pp * m + col)], xi = A[2 * (pp * m + col) + 1];
-                const double yr = A[2 * (qq * m + col)], yi = A[2 * (qq * m + col) + 1];
-                const double zr = er * yr - ei * yi, zi = er * yi + ei * yr;
-                A[2 * (pp * m + col)] = c * xr - s * zr;
-                A[2 * (pp * m + col) + 1] = c * xi - s * zi;
-                A[2 * (qq * m + col)] = s * xr + c * zr;
-                A[2 * (qq * m + col) + 1] = s * xi + c * zi;
+            // every thread has passed the previous sweep's break test
+            if (r == 0 && tid == 0) any_rot[(sweep + 1) & 1] = 0;
+            // A block (row pair I, column pair J): rows get U^H, columns U
+            for (int it = tid; it < npairs * npairs + npairs * m; it += kThreads) {
+                if (it < npairs * npairs) {
+                    const int I = it / npairs, J = it - I * npairs;
+                    const int r0 = pair_p[I], r1 = pair_q[I], c0 = pair_p[J], c1 = pair_q[J];
+                    const double ci = rot[4 * I], si = rot[4 * I + 1], eri = rot[4 * I + 2], eii = rot[4 * I + 3];
+                    const double cj = rot[4 * J], sj = rot[4 * J + 1], erj = rot[4 * J + 2], eij = -rot[4 * J + 3];
+                    const bool h1 = r1 < m, k1 = c1 < m;
+                    double x[2][2][2];  // [row][col][re/im]
+                    x[0][0][0] = A[2 * (r0 * m + c0)];
+                    x[0][0][1] = A[2 * (r0 * m + c0) + 1];
+                    x[0][1][0] = k1 ? A[2 * (r0 * m + c1)] : 0.0;
+                    x[0][1][1] = k1 ? A[2 * (r0 * m + c1) + 1] : 0.0;
+                    x[1][0][0] = h1 ? A[2 * (r1 * m + c0)] : 0.0;
+                    x[1][0][1] = h1 ? A[2 * (r1 * m + c0) + 1] : 0.0;
+                    x[1][1][0] = h1 && k1 ? A[2 * (r1 * m + c1)] : 0.0;
+                    x[1][1][1] = h1 && k1 ? A[2 * (r1 * m + c1) + 1] : 0.0;
+                    // rows: (x0, x1) <- (c x0 - s e x1, s x0 + c e x1), e = e^{+i phi_I}
+                    double y[2][2][2];
+                    for (int cc = 0; cc < 2; ++cc) {
+                        const double zr = eri * x[1][cc][0] - eii * x[1][cc][1];
+                        const double zi = eri * x[1][cc][1] + eii * x[1][cc][0];
+                        y[0][cc][0] = ci * x[0][cc][0] - si * zr;
+                        y[0][cc][1] = ci * x[0][cc][1] - si * zi;
+                        y[1][cc][0] = si * x[0][cc][0] + ci * zr;
+                        y[1][cc][1] = si * x[0][cc][1] + ci * zi;
+                    }
+                    // columns: (y0, y1) <- (c y0 - s e' y1, s y0 + c e' y1), e' = e^{-i phi_J}
+                    for (int rr = 0; rr < 2; ++rr) {
+                        const double zr = erj * y[rr][1][0] - eij * y[rr][1][1];
+                        const double zi = erj * y[rr][1][1] + eij * y[rr][1][0];
+                        x[rr][0][0] = cj * y[rr][0][0] - sj * zr;
+                        x[rr][0][1] = cj * y[rr][0][1] - sj * zi;
+                        x[rr][1][0] = sj * y[rr][0][0] + cj * zr;
+                        x[rr][1][1] = sj * y[rr][0][1] + cj * zi;
+                    }
+                    A[2 * (r0 * m + c0)] = x[0][0][0];
+                    A[2 * (r0 * m + c0) + 1] = x[0][0][1];
+                    if (k1) {
+                        A[2 * (r0 * m + c1)] = x[0][1][0];
+                        A[2 * (r0 * m + c1) + 1] = x[0][1][1];
+                    }
+                    if (h1) {
+                        A[2 * (r1 * m + c0)] = x[1][0][0];
+                        A[2 * (r1 * m + c0) + 1] = x[1][0][1];
+                    }
+                    if (h1 && k1) {
+                        A[2 * (r1 * m + c1)] = x[1][1][0];
+                        A[2 * (r1 * m + c1) + 1] = x[1][1][1];
+                    }
+                } else {  // V <- V U on row `row`, column pair i
+                    const int rem = it - npairs * npairs;
+                    const int i = rem / m, row = rem - i * m;
+                    const int pp = pair_p[i], qq = pair_q[i];
+                    if (qq >= m) continue;
+                    const double c = rot[4 * i], s = rot[4 * i + 1];
+                    const double er = rot[4 * i + 2], ei = -rot[4 * i + 3];  // e^{-i phi}
+                    const double xr = V[2 * (row * m + pp)], xi = V[2 * (row * m + pp) + 1];
+                    const double yr = V[2 * (row * m + qq)], yi = V[2 * (row * m + qq) + 1];
+                    const double zr = er * yr - ei * yi, zi = er * yi + ei * yr;
+                    V[2 * (row * m + pp)] = c * xr - s * zr;
+                    V[2 * (row * m + pp) + 1] = c * xi - s * zi;
+                    V[2 * (row * m + qq)] = s * xr + c * zr;
+                    V[2 * (row * m + qq) + 1] = s * xi + c * zi;
+                }
             }
             __syncthreads();
         }
-        if (!any_rot) break;
-        __syncthreads();
+        if (clk) p.clocks[5] = sweep + 1;
+        if (!any_rot[sweep & 1]) break;
     }
+    NOMA_LLS_CLK(2)
 
     // ---- phase C: eigenvalues, rank, pseudo-inverse solve.
     for (int i = tid; i < m; i += kThreads) lam[i] = A[2 * (i * m + i)];
@@ -271,7 +357,7 @@ __global__ void __launch_bounds__(kThreads) lls_kernel(LlsParams p) {
         U[2 * it + 1] = si;
     }
     __syncthreads();
-    // c_k[a] = sum_i V[a][i] U[i][k]; w0 written FP64
+    // c_k[a] = sum_i V[a][i] U[i][k] -> D (complex), w0 written FP64
     for (int it = tid; it < m * K; it += kThreads) {
         const int a = it / K, k = it % K;
         double sr = 0.0, si = 0.0;
@@ -281,82 +367,97 @@ __global__ void __launch_bounds__(kThreads) lls_kernel(LlsParams p) {
             sr += vr * ur - vi * ui;
             si += vr * ui + vi * ur;
         }
+        D[2 * it] = sr;
+        D[2 * it + 1] = si;
         double *w = p.w0 + ((size_t)d * K + k) * p.width;
-        if (p.layout == NOMA_LAYOUT_WIDEN_COMPLEX) {
+        if (cplx_layout) {
             w[a] = sr;
             w[m + a] = -si;
         } else {
             w[a] = sr;
         }
     }
-    __syncthreads();  // w0 (global) visible to the block below
+    __syncthreads();
 
-    // ---- phase D: residuals r0 = y - X w0 (FP64), norms, status.
-    for (int k = 0; k < K; ++k) {
-        const double *w = p.w0 + ((size_t)d * K + k) * p.width;
-        double rr = 0.0, yy = 0.0;
-        for (int t = tid; t < p.nrow_c; t += kThreads) {
-            double yr, yi;
-            load_target(p, d, t, k, yr, yi);
-            if (p.layout == NOMA_LAYOUT_WIDEN_COMPLEX) {
-                double pe = 0.0, po = 0.0;
-                for (int a = 0; a < m; ++a) {
-                    double xr, xi;
-                    load_row(p, d, t, a, xr, xi);
-                    pe += xr * w[a] + xi * w[m + a];  // row 2t = [Re x; Im x]
-                    po += xi * w[a] - xr * w[m + a];  // row 2t+1 = [Im x; -Re x]
+    NOMA_LLS_CLK(3)
+    // ---- phase D: residuals r0 = y - X w0 (FP64) and norms, one pass over
+    // the staged rows; thread = (user k, row group), fixed-order reductions.
+    const int ngrp = kThreads / K;  // K <= kThreads
+    const int rk = tid % K, rg = tid / K;
+    const bool rthread = rg < ngrp;
+    double rr = 0.0, yy = 0.0;
+    issue(0, 0);
+    for (int ch = 0; ch < nch; ++ch) {
+        if (ch + 1 < nch) {
+            issue(ch + 1, (ch + 1) & 1);
+            cp_async_wait<1>();
+        } else {
+            cp_async_wait<0>();
+        }
+        __syncthreads();
+        const int t0 = ch * CH, tn = min(CH, p.nrow_c - t0);
+        const double *xs = bufs + (ch & 1) * bstride, *ys = xs + 2 * CH * m;
+        if (rthread) {
+            for (int t = rg; t < tn; t += ngrp) {
+                const double yr = ys[2 * (t * K + rk)], yi = ys[2 * (t * K + rk) + 1];
+                double pe0 = 0.0, po0 = 0.0, pe1 = 0.0, po1 = 0.0;
+                for (int a = 0; a < m; a += 2) {  // m even (widened) or odd tail below
+                    const double xr = xs[2 * (t * m + a)], xi = xs[2 * (t * m + a) + 1];
+                    const double w0a = D[2 * (a * K + rk)], w1a = -D[2 * (a * K + rk) + 1];
+                    pe0 += xr * w0a + xi * w1a;  // row 2t = [Re x; Im x]
+                    po0 += xi * w0a - xr * w1a;  // row 2t+1 = [Im x; -Re x]
+                    if (a + 1 < m) {
+                        const double yr1 = xs[2 * (t * m + a + 1)], yi1 = xs[2 * (t * m + a + 1) + 1];
+                        const double v0 = D[2 * ((a + 1) * K + rk)], v1 = -D[2 * ((a + 1) * K + rk) + 1];
+                        pe1 += yr1 * v0 + yi1 * v1;
+                        po1 += yi1 * v0 - yr1 * v1;
+                    }
                 }
-                const double r_e = yr - pe, r_o = yi - po;
-                rr += r_e * r_e + r_o * r_o;
-                yy += yr * yr + yi * yi;
-                if (p.r0) {
-                    p.r0[((size_t)d * K + k) * p.rows + 2 * t] = (float)r_e;
-                    p.r0[((size_t)d * K + k) * p.rows + 2 * t + 1] = (float)r_o;
+                const double pe = pe0 + pe1, po = po0 + po1;
+                const size_t net = (size_t)d * K + rk;
+                if (cplx_layout) {
+                    const double r_e = yr - pe, r_o = yi - po;
+                    rr += r_e * r_e + r_o * r_o;
+                    yy += yr * yr + yi * yi;
+                    if (p.r0) {
+                        p.r0[net * p.rows + 2 * (t0 + t)] = (float)r_e;
+                        p.r0[net * p.rows + 2 * (t0 + t) + 1] = (float)r_o;
+                    }
+                } else {
+                    const double r_e = yr - pe;
+                    rr += r_e * r_e;
+                    yy += yr * yr;
+                    if (p.r0) p.r0[net * p.rows + t0 + t] = (float)r_e;
                 }
-            } else {
-                double pr = 0.0;
-                for (int a = 0; a < m; ++a) {
-                    double xr, xi;
-                    load_row(p, d, t, a, xr, xi);
-                    pr += xr * w[a];
-                }
-                const double r_e = yr - pr;
-                rr += r_e * r_e;
-                yy += yr * yr;
-                if (p.r0) p.r0[((size_t)d * K + k) * p.rows + t] = (float)r_e;
             }
         }
-        red[tid] = rr;
         __syncthreads();
-        for (int s = kThreads / 2; s > 0; s >>= 1) {
-            if (tid < s) red[tid] += red[tid + s];
-            __syncthreads();
+    }
+    NOMA_LLS_CLK(4)
+#undef NOMA_LLS_CLK
+    red[tid] = rr;
+    red[kThreads + tid] = yy;
+    __syncthreads();
+    if (tid < K) {
+        double sr = 0.0, sy = 0.0;
+        for (int g = 0; g < ngrp; ++g) {
+            sr += red[g * K + tid];
+            sy += red[kThreads + g * K + tid];
         }
-        const double res = sqrt(red[0]);
-        __syncthreads();
-        red[tid] = yy;
-        __syncthreads();
-        for (int s = kThreads / 2; s > 0; s >>= 1) {
-            if (tid < s) red[tid] += red[tid + s];
-            __syncthreads();
+        const double res = sqrt(sr), ynorm = sqrt(sy);
+        const size_t net = (size_t)d * K + tid;
+        int st = NOMA_OK;
+        double cond;
+        if (rank == m) {
+            cond = lmax / lmin;
+        } else if (rank > 0 && res <= 1e-8 * sqrt(lmax) * fmax(1.0, ynorm)) {
+            cond = lmax / lkeep;
+        } else {
+            st = NOMA_ERR_ILL_CONDITIONED;
+            cond = lmin > 0.0 ? lmax / lmin : INFINITY;
         }
-        const double ynorm = sqrt(red[0]);
-        __syncthreads();
-        if (tid == 0) {
-            const size_t net = (size_t)d * K + k;
-            int st = NOMA_OK;
-            double cond;
-            if (rank == m) {
-                cond = lmax / lmin;
-            } else if (rank > 0 && res <= 1e-8 * sqrt(lmax) * fmax(1.0, ynorm)) {
-                cond = lmax / lkeep;
-            } else {
-                st = NOMA_ERR_ILL_CONDITIONED;
-                cond = lmin > 0.0 ? lmax / lmin : INFINITY;
-            }
-            if (p.cond) p.cond[net] = cond;
-            if (p.status) p.status[net] = st;
-        }
+        if (p.cond) p.cond[net] = cond;
+        if (p.status) p.status[net] = st;
     }
 }
 
@@ -400,20 +501,26 @@ int lls_predict_launch(int layout, int S, int K, int rows, int width, const doub
 }
 
 size_t lls_smem_bytes(int m, int K) {
-    size_t chunk = 2 * kLlsChunk * m + 2 * kLlsChunk * K;
-    if (chunk < (size_t)(2 * m * K)) chunk = 2 * m * K;  // U aliases the chunk buffers
-    size_t n = 2 * m * m * 2 + 2 * m * K + chunk + 4 * (kLlsMaxM / 2 + 1) + m + kThreads;
+    const size_t bstride = 2 * (size_t)lls_chunk(m) * m + 2 * (size_t)lls_chunk(m) * K;
+    size_t n = 2 * (size_t)m * m * 2 + 2 * (size_t)m * K + 2 * bstride + 4 * (kLlsMaxM / 2 + 1) + m +
+               2 * kThreads;
     return n * sizeof(double);
 }
 
 int lls_launch(const LlsParams &p, cudaStream_t st) {
     if (p.m < 1 || p.m > kLlsMaxM) return NOMA_ERR_UNSUPPORTED;
     const int nent = p.m * (p.m + 1) / 2 + p.m * p.K;
-    if (nent > kLlsMaxE * kThreads) return NOMA_ERR_UNSUPPORTED;
+    if (nent > kLlsMaxE * kThreads || p.K > kThreads) return NOMA_ERR_UNSUPPORTED;
+    if (2 * p.m * p.K > 2 * (2 * lls_chunk(p.m) * p.m + 2 * lls_chunk(p.m) * p.K)) return NOMA_ERR_UNSUPPORTED;
     const size_t smem = lls_smem_bytes(p.m, p.K);
     if (smem > 227 * 1024) return NOMA_ERR_UNSUPPORTED;
-    cudaFuncSetAttribute(lls_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    lls_kernel<<<p.n_designs, kThreads, smem, st>>>(p);
+    if (nent <= kThreads) {
+        cudaFuncSetAttribute(lls_kernel<1, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        lls_kernel<1, 4><<<p.n_designs, kThreads, smem, st>>>(p);
+    } else {
+        cudaFuncSetAttribute(lls_kernel<kLlsMaxE, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        lls_kernel<kLlsMaxE, 1><<<p.n_designs, kThreads, smem, st>>>(p);
+    }
     return cudaGetLastError() == cudaSuccess ? NOMA_OK : NOMA_ERR_CUDA;
 }
 

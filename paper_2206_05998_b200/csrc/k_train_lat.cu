@@ -81,6 +81,20 @@ __device__ __forceinline__ void st_async4(uint32_t raddr, float4 v, uint32_t rba
 
 __device__ __forceinline__ void ffma2(f2_t &d, f2_t a, f2_t b) { f2_fma(d, a, b); }
 
+// Bulk async copy of `bytes` (multiple of 16) from this CTA's shared memory to
+// a (possibly remote) CTA's shared memory, completing on that CTA's mbarrier.
+// The issuing thread must have ordered the source writes (barrier) and made
+// them visible to the async proxy (fence_proxy_async) first.
+__device__ __forceinline__ void bulk_s2s(uint32_t rdst, uint32_t src, uint32_t bytes, uint32_t rbar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(rdst),
+        "r"(src), "r"(bytes), "r"(rbar)
+        : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
 }  // namespace
 
 namespace {
@@ -164,6 +178,7 @@ struct LatCarve {
     int w[NOMA_MAX_DIMS], b[NOMA_MAX_DIMS], wf, npar;  // copy 0; copy 1 at +npar
     int aN;                                            // own a_N [JT][kSR]
     int aloc[NOMA_MAX_DIMS], af[NOMA_MAX_DIMS], rsb[NOMA_MAX_DIMS];  // l < N
+    int rsst;                                          // dA partial staging [H][kSR]
     int bars;                                          // mbarriers (8-byte aligned)
     int nbars, end;
 };
@@ -220,11 +235,13 @@ __host__ __device__ inline bool lat_carve(const NetGeom &g, int cs, int width, i
     for (int l = 1; l < N; ++l) {
         c->aloc[l] = off;
         off += jt * kSR;
-        c->af[l] = off;
-        off += H * kSR;
+        c->af[l] = off;  // double-buffered by step parity
+        off += 2 * H * kSR;
         c->rsb[l] = off;
         off += cs * jt * kSR;
     }
+    c->rsst = off;
+    if (N > 1) off += H * kSR;
     off = pad_to(off, 2);
     c->bars = off;
     c->nbars = 2 + 2 * (N - 1);  // Y[2], AG_l, RS_l
@@ -260,9 +277,9 @@ __global__ void __launch_bounds__(kLT, 1) train_lat_kernel(TrainParams p, LatCar
         clk_prev = now;                                           \
     }
     // per-warp timeline of steps 100-103 (lane 0 of every warp of block 0)
-    long long *tl = p.clocks && blockIdx.x == 0 && lane == 0 ? p.clocks + 8 + warp * 10 : nullptr;
+    long long *tl = p.clocks && blockIdx.x == 0 && lane == 0 ? p.clocks + 8 + warp * 16 : nullptr;
 #define NOMA_TL(PT)                                                              \
-    if (tl && s >= 100 && s < 104) tl[(s - 100) * 160 + (PT)] = clock64();
+    if (tl && s >= 100 && s < 104) tl[(s - 100) * 256 + (PT)] = clock64();
 
     for (int i = tid; i < c.bars; i += kLT) sm[i] = 0.0f;
     __syncthreads();
@@ -286,8 +303,9 @@ __global__ void __launch_bounds__(kLT, 1) train_lat_kernel(TrainParams p, LatCar
         sm[c.atab + 2 * i + 1] = (float)(1.0 / c2);
     }
     constexpr uint32_t ybytes = CS * kBatchRows * 4;
-    constexpr uint32_t agbytes = H * kBatchRows * 4;
-    constexpr uint32_t rsbytes = CS * JT * kBatchRows * 4;
+    // all-gather / reduce-scatter move whole [JT][kSR] tiles by bulk copy
+    constexpr uint32_t agbytes = H * kSR * 4;
+    constexpr uint32_t rsbytes = CS * JT * kSR * 4;
     if (tid == 0) {
         for (int b = 0; b < c.nbars; ++b) mbar_init(s2u(bars + b), 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -404,7 +422,7 @@ __global__ void __launch_bounds__(kLT, 1) train_lat_kernel(TrainParams p, LatCar
 static_for<1, NL + 1, 1>([&](auto LC) {
                 constexpr int l = decltype(LC)::value;
                 const int NC = (l == 1 ? W0 : H) >> 2;
-                const float *in = l == 1 ? XT : sm + c.af[l - 1];
+                const float *in = l == 1 ? XT : sm + c.af[l - 1] + buf * H * kSR;
                 const float *W = sm + po + c.w[l] + fjh * JPF * c.sw[l];
                 const int sw = c.sw[l];
                 {
@@ -443,19 +461,25 @@ static_for<1, NL + 1, 1>([&](auto LC) {
 #pragma unroll
                     for (int i = 0; i < FV; ++i) v[i] = fmaxf(v[i] + bj, 0.f);
                     const int r = 4 * frq + fr;
-                    if (fown) {
-                        sts_n<FV>((l == NL ? sm + c.aN : sm + c.aloc[l]) + fj * kSR + r, v);
-                        if (l < NL) {  // all-gather a_l into every CTA (incl. this one)
-                            const uint32_t la = s2u(sm + c.af[l] + (rank * JT + fj) * kSR + r);
-                            const uint32_t lb = s2u(bars + 2 + 2 * (l - 1));
-#pragma unroll
-                            for (int q = 0; q < CS; ++q) st_async_n<FV>(mapa(la, q), v, mapa(lb, q));
-                        }
-                    }
+                    if (fown) sts_n<FV>((l == NL ? sm + c.aN : sm + c.aloc[l]) + fj * kSR + r, v);
                 }
                 if (l < NL) {
+                    // all-gather a_l: the own [JT][kSR] tile to every CTA (incl.
+                    // this one) by bulk copy, rows rank*JT.. of af_l[s&1].  The
+                    // source is rewritten only at step s+1, after every copy
+                    // of step s has landed (peers' RS of step s waits on it);
+                    // af is double-buffered because the RS copies are issued
+                    // before this CTA's last read of af (the weight gradient).
                     const uint32_t lb = s2u(bars + 2 + 2 * (l - 1));
+                    NOMA_TL(10)
+                    __syncthreads();
+                    if (tid < CS) {
+                        fence_proxy_async();
+                        bulk_s2s(mapa(s2u(sm + c.af[l] + (buf * H + rank * JT) * kSR), tid), s2u(sm + c.aloc[l]),
+                                 JT * kSR * 4, mapa(lb, tid));
+                    }
                     mbar_wait(lb, (uint32_t)(s & 1));
+                    NOMA_TL(11)
                     // re-arm for step s+1 (its bytes cannot land before every
                     // CTA has finished step s)
                     if (tid == 0) mbar_arm(lb, agbytes);
@@ -539,7 +563,7 @@ static_for<NL, 0, -1>([&](auto LC) {
                 const int NC = (l == 1 ? W0 : H) >> 2;
                 const float *zsrc = top ? sm + c.aN : sm + c.aloc[l];  // a_N, or dZ_l in place
                 const float *dyp = sm + c.dy, *wfp = sm + po + c.wf;
-                const float *in = l == 1 ? XT : sm + c.af[l - 1];
+                const float *in = l == 1 ? XT : sm + c.af[l - 1] + buf * H * kSR;
                 const int sw = c.sw[l];
                 if (l > 1 && tid < (H / 4) * 32) {
                     // dA_{l-1} partial = sum_{j own} W_l[j][c] dZ_l[j][r] (:111) for
@@ -570,14 +594,25 @@ static_for<NL, 0, -1>([&](auto LC) {
                             ffma2(acc[q][1], wq, zb);
                         }
                     }
-                    const int owner = cc / JT, lc = cc - owner * JT;
-                    const uint32_t la = s2u(sm + c.rsb[l - 1] + (rank * JT + lc) * kSR + r);
-                    const uint32_t ra = mapa(la, owner), rbar = mapa(rb, owner);
+                    (void)rb;
 #pragma unroll
                     for (int q = 0; q < 4; ++q) {
                         const float2 u = f2_unpack(acc[q][0]), v = f2_unpack(acc[q][1]);
-                        st_async4(ra + q * kSR * 4, make_float4(u.x, u.y, v.x, v.y), rbar);
+                        *reinterpret_cast<float4 *>(sm + c.rsst + (cc + q) * kSR + r) = make_float4(u.x, u.y, v.x, v.y);
                     }
+                }
+                if (l > 1) {
+                    // reduce-scatter: rows [q*JT, (q+1)*JT) of the partial to CTA
+                    // q's slot `rank` (single-buffered: rewritten at step s+1 only
+                    // after every peer has consumed step s, see the Y exchange)
+                    const uint32_t rb = s2u(bars + 3 + 2 * (l - 2));
+                    __syncthreads();
+                    if (tid < CS) {
+                        fence_proxy_async();
+                        bulk_s2s(mapa(s2u(sm + c.rsb[l - 1] + rank * JT * kSR), tid),
+                                 s2u(sm + c.rsst + tid * JT * kSR), JT * kSR * 4, mapa(rb, tid));
+                    }
+                    NOMA_TL(12)
                 }
                 // weight gradient dZ^T A (:109), bias colsum (:110), final a_N^T dy
                 // (:99): warp ct owns column tile 4ct..4ct+3 for all JT neurons,
@@ -667,7 +702,9 @@ static_for<NL, 0, -1>([&](auto LC) {
                 if (l > 1) {
                     // receive: dZ_{l-1} own = (a_{l-1} > 0) * sum_q partial_q (:107)
                     const uint32_t rb = s2u(bars + 3 + 2 * (l - 2));
+                    NOMA_TL(13)
                     mbar_wait(rb, (uint32_t)(s & 1));
+                    NOMA_TL(14)
                     if (tid < JT * 32) {
                         const int j = tid >> 5, r = 4 * lane;
                         const float *rs_ = sm + c.rsb[l - 1] + j * kSR + r;

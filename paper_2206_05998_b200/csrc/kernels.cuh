@@ -16,6 +16,7 @@ struct LlsParams {
     int *status;
     float *design32;      // nullable: FP32 copy for training, [S][nrow_c][width]
     float *r0;            // nullable: [net][rows]
+    long long *clocks;    // nullable: phase cycles of block 0 (NOMA_PHASE_CLOCKS)
 };
 
 struct TrainParams {
