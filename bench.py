@@ -300,6 +300,37 @@ def main():
         if i >= 2:
             lat.append(a.elapsed_time(b) * 1e3)
 
+    # ---- single-slot latency at C1 (the north star's sub-ms target config) --
+    lat_c1 = None
+    if args.config != "c1":
+        c1 = CONFIGS["c1"]
+        M1, K1 = c1["M"], c1["K"]
+        dims1 = [2 * M1] + c1["hidden"]
+        s1 = torch.from_numpy(seeds[:1].astype(np.int64)).to(dev)
+        px1 = torch.empty((1, NT, M1, 2), dtype=torch.float64, device=dev)
+        py1 = torch.empty((1, NT, K1, 2), dtype=torch.float64, device=dev)
+        dx1 = torch.empty((1, ND, M1, 2), dtype=torch.float32, device=dev)
+        tr1 = torch.empty((1, ND, K1), dtype=torch.uint8, device=dev)
+        ctx.synthesize(N.Scenario(K1, M1, NT, ND, c1["step"], SNR, GAIN), s1, px1, py1, dx1, tr1)
+        i1, h1 = slot_user_seeds(seeds[:1], K1)
+        i1 = torch.from_numpy(i1.astype(np.int64)).to(dev)
+        h1 = torch.from_numpy(h1.astype(np.int64)).to(dev)
+        st1 = torch.empty((1, K1), dtype=torch.int32, device=dev)
+        er1 = torch.empty((1, K1), dtype=torch.int32, device=dev)
+        co1 = torch.empty((1, K1, ND), dtype=torch.uint8, device=dev)
+        l1 = []
+        for i in range(5):
+            a = torch.cuda.Event(enable_timing=True)
+            b = torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            ctx.pipeline(dims1, tcfg, 1, K1, M1, NT, ND, px1, py1, dx1, tr1, i1, h1, st1,
+                         codes=co1, bit_errors=er1)
+            b.record(stream)
+            b.synchronize()
+            if i >= 2:
+                l1.append(a.elapsed_time(b) * 1e3)
+        lat_c1 = statistics.median(l1)
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         threads = os.cpu_count() or 1
@@ -324,6 +355,9 @@ def main():
                        "slots_per_gpu": S, "parallelism": f"slot-sharded x{world}, no collective",
                        "l2": "flushed (256 MiB write) between timed steps"},
             "latency_us_per_slot": statistics.mean(lat),
+            "latency_note": "one slot (all K user nets) LLS+init+shuffles+50-epoch training+detection, "
+                            "device time; training in the neuron-split cluster kernel (16 CTAs per net)",
+            "latency_c1_us_per_slot": lat_c1,
             "phase_ms": {k: statistics.mean(p[k] for p in phases) for k in phases[0]},
             "roofline": {"bound": "fp32", "kernel": "train_kernel", "achieved": achieved,
                          "peak": peak_fp32, "unit": "TFLOP/s", "frac": achieved / peak_fp32,
