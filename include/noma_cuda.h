@@ -120,6 +120,11 @@ NOMA_API long long noma_ctx_kernel_launches(noma_ctx_t ctx);
  * 100 + c = neuron-split latency cluster of c CTAs per net (k_train_lat.cu),
  * 0 = none yet. */
 NOMA_API int noma_ctx_train_mode(noma_ctx_t ctx);
+/* Which detection kernel the last noma_detect / noma_pipeline call used:
+ * 1 = FP32 FFMA register tiles (k_detect.cu), 2 = tcgen05 3xTF32 tensor-core
+ * kernel (k_detect_tc.cu; widened input 32/64, hidden layers of 64),
+ * 0 = none yet.  NOMA_DETECT_TC=0 in the environment forces the FFMA kernel. */
+NOMA_API int noma_ctx_detect_mode(noma_ctx_t ctx);
 /* Instrumentation: when on, noma_pipeline records CUDA events around its
  * phases (init and shuffles run on a side stream, overlapping the LLS);
  * noma_ctx_phase_ms waits for the last call and returns ms for

@@ -114,6 +114,7 @@ struct noma_ctx_s {
     std::string err;
     long long launches = 0;
     int train_mode = 0;
+    int detect_mode = 0;
     bool profiling = false;
     // [0] start, [1] after LLS, [2] side start, [3] after init, [4] after
     // shuffles (side stream), [5] joined, [6] after train, [7] after detect
@@ -334,6 +335,8 @@ NOMA_API int noma_ctx_synchronize(noma_ctx_t c) {
 NOMA_API long long noma_ctx_kernel_launches(noma_ctx_t c) { return c ? c->launches : 0; }
 
 NOMA_API int noma_ctx_train_mode(noma_ctx_t c) { return c ? c->train_mode : 0; }
+
+NOMA_API int noma_ctx_detect_mode(noma_ctx_t c) { return c ? c->detect_mode : 0; }
 
 NOMA_API int noma_ctx_set_profiling(noma_ctx_t c, int on) {
     if (!c) return NOMA_ERR_ARGUMENT;
@@ -651,7 +654,9 @@ NOMA_API int noma_detect(noma_ctx_t c, const noma_net_desc *desc, int layout, in
     dpp.codes = dco;
     dpp.errors = der;
     dpp.status = nullptr;
+    dpp.mode = 0;
     int st = detect_launch(dpp, c->stream);
+    c->detect_mode = dpp.mode;
     if (st) return st == NOMA_ERR_CUDA ? cuda_fail(c, "detect") : fail(c, st, "detect: unsupported network shape");
     c->launches += 1;
     return s.finish();
@@ -784,7 +789,9 @@ NOMA_API int noma_pipeline(noma_ctx_t c, const noma_net_desc *desc, const noma_t
         dpp.codes = dco;
         dpp.errors = der;
         dpp.status = dst;
+        dpp.mode = 0;
         st = detect_launch(dpp, c->stream);
+        c->detect_mode = dpp.mode;
         if (st) return st == NOMA_ERR_CUDA ? cuda_fail(c, "detect") : fail(c, st, "detect: unsupported network shape");
         c->launches += 1;
     }

@@ -9,6 +9,8 @@
 // the feature-major tile, the same FP32 register-tile forward as training,
 // then the linear branch, the QPSK sign decision and a warp-reduced bit-error
 // count (one atomic per warp per tile).
+#include <cstdlib>
+
 #include "kernels.cuh"
 #include "tiles.cuh"
 
@@ -122,6 +124,17 @@ __global__ void __launch_bounds__(kThreads) detect_kernel(DetectParams p) {
 
 int detect_launch(DetectParams &p, cudaStream_t st) {
     const NetGeom &g = p.g;
+    // tensor-core path (k_detect_tc.cu) for the shapes it covers, unless
+    // NOMA_DETECT_TC=0 (A/B and parity runs of the FFMA kernel)
+    const char *tc_env = std::getenv("NOMA_DETECT_TC");
+    if (!(tc_env && tc_env[0] == '0')) {
+        const int r = detect_tc_launch(p, st);
+        if (r != NOMA_ERR_UNSUPPORTED) {
+            p.mode = 2;
+            return r;
+        }
+    }
+    p.mode = 1;
     for (int l = 0; l < g.nd; ++l)
         if (g.dims[l] > NOMA_MAX_WIDTH) return NOMA_ERR_UNSUPPORTED;
     int maxh = 32;

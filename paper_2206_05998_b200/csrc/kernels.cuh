@@ -64,6 +64,7 @@ struct DetectParams {
     const int *status;      // [net] nullable
     int tiles;              // per net
     int off_x, off_a0, off_a1, off_ps, off_w0, off_y, off_yp, off_end;
+    int mode;               // out: 1 = FFMA kernel, 2 = tcgen05 3xTF32 kernel
 };
 
 struct SynthParams {
@@ -98,6 +99,7 @@ int train_launch(TrainParams &p, cudaStream_t st);
 int train_lat_launch(TrainParams &p, cudaStream_t st);
 int train_f64_launch(TrainF64Params &p, cudaStream_t st);
 int detect_launch(DetectParams &p, cudaStream_t st);
+int detect_tc_launch(const DetectParams &p, cudaStream_t st);
 int synth_launch(SynthParams p, double *noise_power_scratch, cudaStream_t st);
 
 }  // namespace noma_dev

@@ -26,7 +26,7 @@ EXPORTED = [
     "noma_plan_size", "noma_param_count", "noma_lls_fit", "noma_init_params", "noma_train",
     "noma_detect", "noma_pipeline", "noma_synthesize", "noma_ctx_set_profiling",
     "noma_ctx_phase_ms", "noma_measure_fp32_tflops", "noma_init_params_state",
-    "noma_lls_predict", "noma_train_f64", "noma_ctx_train_mode",
+    "noma_lls_predict", "noma_train_f64", "noma_ctx_train_mode", "noma_ctx_detect_mode",
 ]
 PHASES = ("lls", "init", "shuffle", "train", "detect", "total")
 
@@ -114,6 +114,7 @@ def load():
     L.noma_ctx_kernel_launches.restype = C.c_longlong
     L.noma_ctx_kernel_launches.argtypes = [vp]
     L.noma_ctx_train_mode.argtypes = [vp]
+    L.noma_ctx_detect_mode.argtypes = [vp]
     L.noma_plan_size.argtypes = [C.POINTER(NetDesc)]
     L.noma_param_count.argtypes = [C.POINTER(NetDesc)]
     L.noma_lls_fit.argtypes = [vp, C.POINTER(Dataset), vp, vp, vp, ip]
@@ -212,6 +213,11 @@ class Context:
     def train_mode(self) -> int:
         """Kernel shape of the last training launch (noma_ctx_train_mode)."""
         return self.L.noma_ctx_train_mode(self.h)
+
+    @property
+    def detect_mode(self) -> int:
+        """Kernel of the last detection (noma_ctx_detect_mode): 1 FFMA, 2 tcgen05."""
+        return self.L.noma_ctx_detect_mode(self.h)
 
     def set_profiling(self, on: bool):
         self._check(self.L.noma_ctx_set_profiling(self.h, 1 if on else 0))

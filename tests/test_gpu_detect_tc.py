@@ -1,0 +1,53 @@
+"""GPU parity of the tcgen05 (3xTF32) detection kernel, k_detect_tc.cu, for
+every shape it covers: soft outputs against the FP64 reference forward at the
+reference's FP32 inference tolerance (test_fused.cpp:128-130), hard decisions
+against the reference's sign pattern, and bit-for-bit agreement of decisions
+and error counters with the FFMA kernel (the north star's gate for putting
+the data phase on tensor cores)."""
+import numpy as np
+import pytest
+
+from tests.helpers import random_net_fused, record
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def A():
+    from paper_2206_05998_b200 import api
+
+    api.context()
+    return api
+
+
+@pytest.mark.parametrize("dims", [[32, 64], [32, 64, 64], [64, 64], [64, 64, 64]])
+@pytest.mark.parametrize("nsym", [4096, 1000])  # 1000: ragged last tile
+def test_detect_tc_matches_reference(A, O, dims, nsym, monkeypatch):
+    from tests import refimpl as R
+
+    M = dims[0] // 2
+    onet = random_net_fused(dims, 7 + len(dims))
+    layers, final = onet.layers()
+    net = A.net_from_params(onet.dims, onet.w0, layers, final)
+    sy = A.synthesize(6, M, 2 * M, nsym, [23], snr_db=8.0, rx_nonlinearity_gain=0.05)
+    x = sy.data_rx[0]
+    truth = sy.data_rx[0][:, 0].astype(np.complex128)  # any symbols: only the count is compared
+    soft, bits, errs = A.detect(net, x, truth_symbols=truth)
+    assert A.context().detect_mode == 2
+    ref = O.narrow_predictions(R.reference_forward(onet.dims, onet.w0, layers, final,
+                                                   O.widen_design(x.astype(np.complex128))))
+    scale = max(1.0, float(np.max(np.abs(ref))))
+    dev = float(np.max(np.abs(soft - ref))) / scale
+    ref_bits = O.hard_decision_qpsk(ref)
+    margin = np.minimum(np.abs(ref.real), np.abs(ref.imag)) > 1e-5 * scale
+    flips = int(np.count_nonzero((bits != ref_bits).any(axis=-1) & margin))
+    record("detect_tc", config=str(dims), symbols=nsym, soft_dev=dev, flips=flips)
+    assert dev < 1e-5, dev
+    assert flips == 0
+    # identical decisions and counters to the FFMA kernel
+    monkeypatch.setenv("NOMA_DETECT_TC", "0")
+    soft_f, bits_f, errs_f = A.detect(net, x, truth_symbols=truth)
+    assert A.context().detect_mode == 1
+    assert np.max(np.abs(soft_f - soft)) / scale < 2e-6
+    assert np.array_equal(bits, bits_f)
+    assert errs == errs_f
