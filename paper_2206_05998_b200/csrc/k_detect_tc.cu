@@ -31,7 +31,8 @@ namespace noma_dev {
 
 namespace {
 
-constexpr int kTcThreads = 128;
+constexpr int kTcGroups = 2;    // independent 128-thread tile streams per CTA
+constexpr int kTcThreads = 128 * kTcGroups;
 constexpr int kTcRows = 128;
 
 __device__ __forceinline__ uint32_t tc_s2u(const void *p) {
@@ -110,7 +111,14 @@ struct DetectTcParams {
     const int *status;
 };
 
-// W0 = input width 2M, H = hidden width, NL = hidden layers (1 or 2)
+// W0 = input width 2M, H = hidden width, NL = hidden layers (1 or 2).
+// kTcGroups groups of 128 threads each run their own tile stream (own A
+// buffers, TMEM columns and mbarrier; group-local named barriers), so one
+// group's MMAs overlap another group's epilogue; the weights are shared.
+template <int W0, int H, int NL>
+constexpr uint32_t tc_abuf_bytes() {  // per group: A1 (hi, lo), aliased by A2 (hi, lo)
+    return (uint32_t)(2 * kTcRows * (NL > 1 && H > W0 ? H : W0) * 4);
+}
 template <int W0, int H, int NL>
 __global__ void __launch_bounds__(kTcThreads, 1) detect_tc_kernel(DetectTcParams p) {
     constexpr int M = W0 / 2;
@@ -118,17 +126,22 @@ __global__ void __launch_bounds__(kTcThreads, 1) detect_tc_kernel(DetectTcParams
     constexpr int KB0 = W0 / 4, KBH = H / 4;   // k-blocks per row group
     constexpr uint32_t A1B = kTcRows * W0 * 4, B1B = N1 * W0 * 4;
     constexpr uint32_t A2B = kTcRows * H * 4, B2B = H * H * 4;
+    constexpr uint32_t ABUF = tc_abuf_bytes<W0, H, NL>();
     extern __shared__ __align__(1024) char smem[];
-    char *a1h = smem, *a1l = a1h + A1B;
-    char *b1h = a1l + A1B, *b1l = b1h + B1B;
-    char *a2h = b1l + B1B, *a2l = a2h + (NL > 1 ? A2B : 0);
-    char *b2h = a2l + (NL > 1 ? A2B : 0), *b2l = b2h + (NL > 1 ? B2B : 0);
-    float *bias = reinterpret_cast<float *>(b2l + (NL > 1 ? B2B : 0));  // [NL][H]
-    float *wf = bias + NL * H;                                             // [H]
-    uint64_t *mbar = reinterpret_cast<uint64_t *>(wf + H);
-    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(mbar + 1);
+    char *b1h = smem, *b1l = b1h + B1B;
+    char *b2h = b1l + B1B, *b2l = b2h + (NL > 1 ? B2B : 0);
+    char *abase = b2l + (NL > 1 ? B2B : 0);
+    float *bias = reinterpret_cast<float *>(abase + kTcGroups * ABUF);  // [NL][H]
+    float *wf = bias + NL * H;                                           // [H]
+    uint64_t *mbars = reinterpret_cast<uint64_t *>(wf + H);              // [kTcGroups]
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(mbars + kTcGroups);
 
-    const int net = blockIdx.y, tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int net = blockIdx.y, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int grp = threadIdx.x >> 7, tid = threadIdx.x & 127;  // group, thread in group
+    char *a1h = abase + grp * ABUF, *a1l = a1h + A1B;
+    char *a2h = a1h, *a2l = a1h + A2B;  // layer-2 operand reuses the group's A1 space
+    (void)A2B;
+    auto gsync = [&]() { asm volatile("bar.sync %0, 128;" ::"r"(1 + grp) : "memory"); };
     if (p.status && p.status[net] != NOMA_OK) {
         if (blockIdx.x == 0 && tid == 0 && p.errors) p.errors[net] = 0xFFFFFFFFu;
         return;
@@ -138,7 +151,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) detect_tc_kernel(DetectTcParams
     const float *pl = p.plans + (size_t)net * g.plan_total;
 
     // ---- weights: hi/lo planes in the K-major core layout (FusedPlan order) --
-    for (int i = tid; i < N1 * KB0; i += kTcThreads) {
+    for (int i = threadIdx.x; i < N1 * KB0; i += kTcThreads) {
         const int j = i / KB0, kq = (i - j * KB0) * 4;
         float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
         if (j < H) v = *reinterpret_cast<const float4 *>(pl + g.plan_w[1] + j * g.plan_pad[0] + kq);
@@ -146,27 +159,29 @@ __global__ void __launch_bounds__(kTcThreads, 1) detect_tc_kernel(DetectTcParams
         put4(b1h, b1l, j, kq, KB0, v);
     }
     if constexpr (NL > 1) {
-        for (int i = tid; i < H * KBH; i += kTcThreads) {
+        for (int i = threadIdx.x; i < H * KBH; i += kTcThreads) {
             const int j = i / KBH, kq = (i - j * KBH) * 4;
             put4(b2h, b2l, j, kq, KBH, *reinterpret_cast<const float4 *>(pl + g.plan_w[2] + j * g.plan_pad[1] + kq));
         }
     }
-    for (int i = tid; i < NL * H; i += kTcThreads) bias[i] = pl[g.plan_b[1 + i / H] + i % H];
-    for (int i = tid; i < H; i += kTcThreads) wf[i] = pl[g.plan_f + i];
+    for (int i = threadIdx.x; i < NL * H; i += kTcThreads) bias[i] = pl[g.plan_b[1 + i / H] + i % H];
+    for (int i = threadIdx.x; i < H; i += kTcThreads) wf[i] = pl[g.plan_f + i];
     if (warp == 0) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(tc_s2u(tmem_slot)));
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(tc_s2u(tmem_slot)),
+                     "n"(256 * kTcGroups));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
-    if (tid == 0) {
-        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(tc_s2u(mbar)));
+    if (threadIdx.x < kTcGroups) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(tc_s2u(mbars + threadIdx.x)));
         asm volatile("fence.mbarrier_init.release.cluster;");
     }
     asm volatile("tcgen05.fence::before_thread_sync;");
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;");
-    const uint32_t tmem = *tmem_slot;
-    const uint32_t trow = tmem + ((uint32_t)(warp * 32) << 16);  // this warp's TMEM lanes
-    const uint32_t bar = tc_s2u(mbar);
+    // group grp: TMEM columns [256 grp, 256 grp + 256); lanes = the group's rows
+    const uint32_t tmem = *tmem_slot + 256 * grp;
+    const uint32_t trow = tmem + ((uint32_t)((warp & 3) * 32) << 16);  // this warp's TMEM lanes
+    const uint32_t bar = tc_s2u(mbars + grp);
     uint32_t phase = 0;
 
     // ---- tile loop: thread t = widened row t = symbol t/2, Re/Im half t&1 --
@@ -174,9 +189,11 @@ __global__ void __launch_bounds__(kTcThreads, 1) detect_tc_kernel(DetectTcParams
     const bool odd = tid & 1;
     const float2 *src = reinterpret_cast<const float2 *>(p.data) + (size_t)d * p.rows * M;
     float2 xs[M];
+    uint8_t truth_next = 0;  // the tile's truth code, loaded with its samples
     auto load_tile = [&](int tile) {
         const int s = tile * 64 + sym;
         const bool ok = tile < p.tiles && s < p.rows;
+        truth_next = ok && p.truth && !odd ? p.truth[((size_t)d * p.rows + s) * p.K + k] : (uint8_t)0;
 #pragma unroll
         for (int m = 0; m < M; m += 2) {
             const float4 v = ok ? *reinterpret_cast<const float4 *>(src + (size_t)s * M + m)
@@ -186,9 +203,11 @@ __global__ void __launch_bounds__(kTcThreads, 1) detect_tc_kernel(DetectTcParams
         }
     };
     uint32_t my_err = 0;
-    int tile = blockIdx.x;
+    const int tstride = gridDim.x * kTcGroups;
+    int tile = blockIdx.x * kTcGroups + grp;
     load_tile(tile);
-    for (; tile < p.tiles; tile += gridDim.x) {
+    for (; tile < p.tiles; tile += tstride) {
+        const uint8_t truth_cur = truth_next;
         // widened row -> A operand (hi/lo)
 #pragma unroll
         for (int m = 0; m < M; m += 4) {
@@ -202,10 +221,10 @@ __global__ void __launch_bounds__(kTcThreads, 1) detect_tc_kernel(DetectTcParams
                 put4(a1h, a1l, tid, M + m, KB0, make_float4(-re.x, -re.y, -re.z, -re.w));
             }
         }
-        load_tile(tile + gridDim.x);  // next tile's samples, in flight during the MMAs
+        load_tile(tile + tstride);  // next tile's samples, in flight during the MMAs
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         asm volatile("tcgen05.fence::before_thread_sync;");
-        __syncthreads();
+        gsync();
         asm volatile("tcgen05.fence::after_thread_sync;");
         if (tid == 0) {  // layer 1 (+ linear branch): D1[128 x N1] in TMEM columns 0..N1
             constexpr uint32_t id1 = umma_idesc_tf32(N1);
@@ -254,7 +273,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) detect_tc_kernel(DetectTcParams
             }
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             asm volatile("tcgen05.fence::before_thread_sync;");
-            __syncthreads();
+            gsync();
             asm volatile("tcgen05.fence::after_thread_sync;");
             if (tid == 0) {  // layer 2: D2[128 x H] in TMEM columns 128..
                 constexpr uint32_t id2 = umma_idesc_tf32(H);
@@ -290,10 +309,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) detect_tc_kernel(DetectTcParams
             const uint8_t code = (uint8_t)((y < 0.f ? 1 : 0) | (yo < 0.f ? 2 : 0));  // eval.cpp:41-42
             if (p.codes) p.codes[(size_t)net * p.rows + s] = code;
             if (p.soft) *reinterpret_cast<float2 *>(p.soft + ((size_t)net * p.rows + s) * 2) = make_float2(y, yo);
-            if (p.truth) {
-                const uint8_t t = p.truth[((size_t)d * p.rows + s) * p.K + k];
-                my_err += __popc((unsigned)(t ^ code) & 3u);
-            }
+            if (p.truth) my_err += __popc((unsigned)(truth_cur ^ code) & 3u);
         }
         // the next tile's A stores must not overtake this tile's TMEM reads
         asm volatile("tcgen05.fence::before_thread_sync;");
@@ -305,13 +321,14 @@ __global__ void __launch_bounds__(kTcThreads, 1) detect_tc_kernel(DetectTcParams
     }
     asm volatile("tcgen05.fence::before_thread_sync;");
     __syncthreads();
-    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem));
+    if (warp == 0)
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(*tmem_slot), "n"(256 * kTcGroups));
 }
 
 template <int W0, int H, int NL>
 constexpr size_t detect_tc_smem() {
-    return 2 * (size_t)kTcRows * W0 * 4 + 2 * (size_t)(H + 16) * W0 * 4 +
-           (NL > 1 ? 2 * (size_t)kTcRows * H * 4 + 2 * (size_t)H * H * 4 : 0) + (size_t)(NL + 1) * H * 4 + 16;
+    return 2 * (size_t)(H + 16) * W0 * 4 + (NL > 1 ? 2 * (size_t)H * H * 4 : 0) +
+           (size_t)kTcGroups * tc_abuf_bytes<W0, H, NL>() + (size_t)(NL + 1) * H * 4 + 8 * kTcGroups + 8;
 }
 
 // Supported shapes: widened input 32 or 64 wide, one or two hidden layers of
