@@ -258,6 +258,8 @@ void fill_train(TrainParams &tp, const NetGeom &g, const noma_train_cfg *cfg) {
     tp.g = g;
     tp.clocks = nullptr;
     tp.mode = 0;
+    tp.xprep = tp.r0prep = nullptr;
+    tp.prep_floats = 0;
     tp.epochs = cfg->epochs;
     tp.batch = cfg->batch_size;
     tp.lr = (float)cfg->lr;
@@ -269,6 +271,22 @@ void fill_train(TrainParams &tp, const NetGeom &g, const noma_train_cfg *cfg) {
     tp.lr_d = cfg->lr;
     tp.b1d = cfg->beta1;
     tp.b2d = cfg->beta2;
+}
+
+// Latency-mode minibatch tiles (k_train_lat.cu lat_prep_kernel): scratch
+// for few nets only (the latency kernel's regime), capped at 256 Mi floats.
+template <class StageT>
+void prep_scratch(StageT &s, TrainParams &tp) {
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (tp.n_nets * 2 > sms && !std::getenv("NOMA_LAT_CLUSTER")) return;
+    const size_t steps = (size_t)((tp.rows + tp.batch - 1) / tp.batch) * tp.epochs;
+    const size_t xf = (size_t)tp.n_nets * steps * tp.width * noma_dev::kSR;
+    if (steps == 0 || xf > ((size_t)256 << 20)) return;
+    tp.xprep = s.template scratch<float>(xf);
+    tp.r0prep = s.template scratch<float>((size_t)tp.n_nets * steps * noma_dev::kBatchRows);
+    tp.prep_floats = tp.xprep && tp.r0prep ? xf : 0;
 }
 
 }  // namespace
@@ -550,6 +568,7 @@ NOMA_API int noma_train(noma_ctx_t c, const noma_dataset *ds, const noma_net_des
     tp.trace = dt;
     tp.status = dst;
     if (cfg->epochs > 0) {
+        prep_scratch(s, tp);
         st = train_launch(tp, c->stream);
         c->train_mode = tp.mode;
         if (st) return st == NOMA_ERR_CUDA ? cuda_fail(c, "train") : fail(c, st, "train: unsupported network shape");
@@ -754,6 +773,7 @@ NOMA_API int noma_pipeline(noma_ctx_t c, const noma_net_desc *desc, const noma_t
         constexpr int kClk = 8 + 4 * 16 * 16;
         if (clocks) tp.clocks = s.scratch<long long>(kClk);
         if (clocks && tp.clocks) cudaMemsetAsync(tp.clocks, 0, kClk * sizeof(long long), c->stream);
+        prep_scratch(s, tp);
         st = train_launch(tp, c->stream);
         c->train_mode = tp.mode;
         if (st) return st == NOMA_ERR_CUDA ? cuda_fail(c, "train") : fail(c, st, "train: unsupported network shape");

@@ -36,7 +36,6 @@ namespace noma_dev {
 
 namespace {
 
-constexpr int kLT = 512;      // threads per CTA
 
 __device__ __forceinline__ uint32_t s2u(const void *p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -61,11 +60,15 @@ __device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
 __device__ __forceinline__ void mbar_arm(uint32_t bar, uint32_t bytes) {
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
 }
+// Acquire at CTA scope: the awaited bytes are st.async / bulk-copy writes
+// into THIS CTA's shared memory, completed on this CTA's mbarrier (the same
+// contract as TMA loads).  A cluster-scope acquire would add an L1
+// invalidate-all (CCTL.IVALL) after every wait.
 __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
     asm volatile(
         "{\n\t.reg .pred p;\n"
         "NOMA_MBW_%=:\n\t"
-        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
         "@!p bra NOMA_MBW_%=;\n}" ::"r"(bar),
         "r"(parity)
         : "memory");
@@ -89,6 +92,13 @@ __device__ __forceinline__ void bulk_s2s(uint32_t rdst, uint32_t src, uint32_t b
     asm volatile(
         "cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(rdst),
         "r"(src), "r"(bytes), "r"(rbar)
+        : "memory");
+}
+// Bulk async copy global -> this CTA's shared memory, completing on `mbar`.
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void *src, uint32_t bytes, uint32_t mbar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+        "l"(src), "r"(bytes), "r"(mbar)
         : "memory");
 }
 __device__ __forceinline__ void fence_proxy_async() {
@@ -215,7 +225,7 @@ __host__ __device__ inline bool lat_carve(const NetGeom &g, int cs, int width, i
     c->dy = off;
     off += kBatchRows;
     c->red = off;
-    off += 32;
+    off += kBatchRows;
     c->atab = off;
     off += pad_to(2 * total_steps, 4);
     int np = 0;
@@ -244,14 +254,15 @@ __host__ __device__ inline bool lat_carve(const NetGeom &g, int cs, int width, i
     if (N > 1) off += H * kSR;
     off = pad_to(off, 2);
     c->bars = off;
-    c->nbars = 2 + 2 * (N - 1);  // Y[2], AG_l, RS_l
+    c->nbars = 2 + 2 * (N - 1) + 2;  // Y[2], AG_l, RS_l, G[2] (minibatch tiles)
     off += 2 * c->nbars;
     c->end = off;
     return (size_t)off * sizeof(float) <= 227 * 1024;
 }
 
-template <int CS, int JT, int NL, int VW>
-__global__ void __launch_bounds__(kLT, 1) train_lat_kernel(TrainParams p, LatCarve c) {
+template <int CS, int JT, int NL, int VW, int NW>
+__global__ void __launch_bounds__(NW * 32, 1) train_lat_kernel(TrainParams p, LatCarve c) {
+    constexpr int kLT = NW * 32;  // threads per CTA (16 warps, or 8 for one 32-input layer)
     extern __shared__ __align__(16) float sm[];
     constexpr int H = CS * JT;
     const int net = blockIdx.x / CS;
@@ -318,75 +329,30 @@ __global__ void __launch_bounds__(kLT, 1) train_lat_kernel(TrainParams p, LatCar
         }
     }
 
-    // ---- step schedule and the two-stage gather prefetch --------------------
-    // Warps 4-15 gather (warps 0-3 are on the critical yp/residual path):
-    // thread t' = tid - 128 owns minibatch row t' % 128 and float4 columns
-    // f = t'/128 + 3m of it -- the complex row idx/2 of slot d; odd widened
-    // rows read the other half (offset +-M) and negate Re (iq_transform.cpp:17-20).
-    constexpr int W0 = 16 * VW;       // input width 2M
-    constexpr int NV = W0 / 4;        // float4 per widened row
-    constexpr int GI = (NV + 2) / 3;  // float4 per gather thread
+    // ---- step schedule: minibatch tiles by bulk copy --------------------------
+    // lat_prep_kernel has materialised every step's permuted, IQ-widened,
+    // feature-major tile X[W0][kSR] and its r0 column (hybrid_nn.cpp:176-187,
+    // iq_transform.cpp:17-20); one thread copies step s+1's tile into the other
+    // buffer during step s, completing on barrier G[(s+1)&1].
+    constexpr int W0 = 16 * VW;  // input width 2M
     const int spe = (n + p.batch - 1) / p.batch;  // steps per epoch
     const int total = c.total;
-    const bool gatherer = tid >= 128;
-    const int gt = gatherer ? tid - 128 : 0;
-    const int gr = gt & (kBatchRows - 1), gq = gt >> 7;
-    const float *dsrc = p.design32 + (wid ? (size_t)d * (n >> 1) : (size_t)d * n) * W0;
-    const float *r0src = p.r0 + (size_t)net * n;
-    const uint16_t *psrc = p.perm + (size_t)net * p.epochs * n;
-    int colv[GI], offo[GI];
-    bool okv[GI], negv[GI];
-#pragma unroll
-    for (int v = 0; v < GI; ++v) {
-        const int col = 4 * (gq + 3 * v);
-        okv[v] = gatherer && col < W0;
-        colv[v] = okv[v] ? col : 0;
-        offo[v] = wid ? (col < M ? M : -M) : 0;
-        negv[v] = wid && col >= M;
-    }
-    auto perm_at = [&](int e, int st, int r) -> int {  // perm index, or -1 past the batch
-        const int start = st * p.batch;
-        return gatherer && r < min(p.batch, n - start) ? (int)psrc[e * n + start + r] : -1;
+    constexpr uint32_t xbytes = W0 * kSR * 4, rbytes = kBatchRows * 4;
+    const int gbar0 = c.nbars - 2;
+    const float *xsrc = p.xprep + (size_t)net * total * W0 * kSR;
+    const float *rsrc = p.r0prep + (size_t)net * total * kBatchRows;
+    auto fetch = [&](int step) {  // one thread
+        const int b = step & 1;
+        const uint32_t gb = s2u(bars + gbar0 + b);
+        mbar_arm(gb, xbytes + rbytes);
+        bulk_g2s(s2u(sm + c.xt + b * W0 * kSR), xsrc + (size_t)step * W0 * kSR, xbytes, gb);
+        bulk_g2s(s2u(sm + c.r0b + b * kBatchRows), rsrc + (size_t)step * kBatchRows, rbytes, gb);
     };
-    // raw loads stay in registers until store_row one step later (the sign of
-    // odd rows is applied there, so nothing waits on the loads here)
-    float4 rowv[GI];
-    float rowr0 = 0.0f, rowsg = 0.0f, rowsgn = 0.0f;  // sign: even / odd-row Re half
-    auto load_row = [&](int idx) {
-        const bool valid = idx >= 0;
-        const int ii = valid ? idx : 0;
-        const bool odd = wid && (ii & 1);
-        const float *src = dsrc + (wid ? ii >> 1 : ii) * W0;
-#pragma unroll
-        for (int v = 0; v < GI; ++v)
-            rowv[v] = okv[v] ? *reinterpret_cast<const float4 *>(src + colv[v] + (odd ? offo[v] : 0))
-                             : make_float4(0.f, 0.f, 0.f, 0.f);
-        rowsg = valid ? 1.0f : 0.0f;
-        rowsgn = odd ? -rowsg : rowsg;
-        rowr0 = gatherer && gq == 0 ? r0src[ii] : 0.0f;
-    };
-    auto store_row = [&](int buf) {
-        float *xt = sm + c.xt + buf * W0 * kSR + gr;
-#pragma unroll
-        for (int v = 0; v < GI; ++v) {
-            if (okv[v]) {
-                const float sg = negv[v] ? rowsgn : rowsg;
-                float *q = xt + colv[v] * kSR;
-                q[0] = sg * rowv[v].x;
-                q[kSR] = sg * rowv[v].y;
-                q[2 * kSR] = sg * rowv[v].z;
-                q[3 * kSR] = sg * rowv[v].w;
-            }
-        }
-        if (gatherer && gq == 0) sm[c.r0b + buf * kBatchRows + gr] = rowsg * rowr0;
-    };
-    load_row(total > 0 ? perm_at(0, 0, gr) : -1);
-    store_row(0);
-    int idx_next = total > 1 ? perm_at(1 / spe, 1 % spe, gr) : -1;
-    load_row(idx_next);                                      // rows of step 1
-    idx_next = total > 2 ? perm_at(2 / spe, 2 % spe, gr) : -1;  // indices of step 2
-    int e3 = 3 / spe, st3 = 3 % spe;                          // schedule of step s+3
+    (void)wid;
+    (void)d;
+    (void)M;
     __syncthreads();
+    if (tid == 0 && total > 0) fetch(0);
     cl_sync();  // every CTA's barriers initialised before any st.async lands
 
     // Adam moments of the parameters this thread updates (registers; fixed
@@ -399,10 +365,10 @@ __global__ void __launch_bounds__(kLT, 1) train_lat_kernel(TrainParams p, LatCar
     // forward thread map: 8 k-split lanes x 32 row quads x 2 neuron halves;
     // after the k reduce-scatter a lane holds FV values (neuron fj, rows
     // 4 frq + fr ..), or -- with one neuron per half -- one value on 2 lanes
-    constexpr int JPF = JT / 2;                  // neurons per forward thread
+    constexpr int JPF = NW == 16 ? JT / 2 : JT;  // neurons per forward thread
     constexpr int FVV = 4 * JPF;                 // values before the reduce
     constexpr int FV = FVV >= 8 ? FVV / 8 : 1;   // values per lane after it
-    const int fkq = tid & 7, frq = (tid >> 3) & 31, fjh = tid >> 8;
+    const int fkq = tid & 7, frq = (tid >> 3) & 31, fjh = NW == 16 ? tid >> 8 : 0;
     const int fbase = FVV >= 8 ? fkq * FV : fkq >> (3 - ilog2c(FVV));
     const bool fown = FVV >= 8 || (fkq & ((8 / FVV) - 1)) == 0;
     const int fj = fjh * JPF + (fbase >> 2), fr = fbase & 3;
@@ -416,6 +382,7 @@ __global__ void __launch_bounds__(kLT, 1) train_lat_kernel(TrainParams p, LatCar
             const int start = st * p.batch, bsz = min(p.batch, n - start);
             const float *XT = sm + c.xt + buf * width * kSR;
             const int po = buf * c.npar, pn = (buf ^ 1) * c.npar;  // param copy: read, write
+            mbar_wait(s2u(bars + gbar0 + buf), (uint32_t)((s >> 1) & 1));  // this step's tile
             NOMA_TL(0)
             // ---- forward (hybrid_nn.cpp:60-72): all JT own neurons x 4 rows per
             // thread, k split over 8 lanes, lane reduce-scatter --------------
@@ -511,44 +478,28 @@ static_for<1, NL + 1, 1>([&](auto LC) {
                 for (int q = warp; q < CS; q += 4) st_async4(mapa(la, q), y, mapa(ybar, q));
             }
             NOMA_TL(3)
-            // ---- gather: store the rows of step s+1, load step s+2's ----------
-            if (s + 1 < total) {
-                store_row(buf ^ 1);
-                load_row(idx_next);
-                idx_next = s + 3 < total ? perm_at(e3, st3, gr) : -1;
-            }
-            if (++st3 == spe) {
-                st3 = 0;
-                ++e3;
-            }
+            // ---- next step's minibatch tile (bulk copy, one thread off the
+            // critical warps; XT[buf^1] was last read in step s-1) ------------
+            if (tid == kLT - 32 && s + 1 < total) fetch(s + 1);
             NOMA_LPHASE(2)
             NOMA_TL(4)
-            // ---- residual a_N w - r0, dy = 2 r / B (hybrid_nn.cpp:94-98): warp 0,
-            // 4 rows per lane, partials summed in rank order ------------------
-            if (warp == 0) {
+            // ---- residual a_N w - r0, dy = 2 r / B (hybrid_nn.cpp:94-98): warps
+            // 0-3, one row per lane, partials summed in rank order ------------
+            if (warp < 4) {
                 mbar_wait(ybar, (uint32_t)((s >> 1) & 1));
                 NOMA_LPHASE(3)
                 NOMA_TL(5)
-                const int r0 = 4 * lane;
-                const float *ya = sm + c.yall + buf * CS * kBatchRows + r0;
-                float4 yh = *reinterpret_cast<const float4 *>(ya);
+                const int r = tid;  // 0..127
+                const float *ya = sm + c.yall + buf * CS * kBatchRows + r;
+                float yq[CS];
 #pragma unroll
-                for (int q = 1; q < CS; ++q) {
-                    const float4 v = *reinterpret_cast<const float4 *>(ya + q * kBatchRows);
-                    yh.x += v.x;
-                    yh.y += v.y;
-                    yh.z += v.z;
-                    yh.w += v.w;
-                }
-                const float4 rr = *reinterpret_cast<const float4 *>(sm + c.r0b + buf * kBatchRows + r0);
-                const float4 res = make_float4(r0 < bsz ? yh.x - rr.x : 0.f, r0 + 1 < bsz ? yh.y - rr.y : 0.f,
-                                               r0 + 2 < bsz ? yh.z - rr.z : 0.f, r0 + 3 < bsz ? yh.w - rr.w : 0.f);
-                const float sc = 2.0f / (float)bsz;
-                *reinterpret_cast<float4 *>(sm + c.dy + r0) = make_float4(sc * res.x, sc * res.y, sc * res.z, sc * res.w);
-                loss_acc = fmaf(res.x, res.x, loss_acc);
-                loss_acc = fmaf(res.y, res.y, loss_acc);
-                loss_acc = fmaf(res.z, res.z, loss_acc);
-                loss_acc = fmaf(res.w, res.w, loss_acc);
+                for (int q = 0; q < CS; ++q) yq[q] = ya[q * kBatchRows];
+                float yh = yq[0];
+#pragma unroll
+                for (int q = 1; q < CS; ++q) yh += yq[q];
+                const float res = r < bsz ? yh - sm[c.r0b + buf * kBatchRows + r] : 0.0f;
+                sm[c.dy + r] = (2.0f / (float)bsz) * res;
+                loss_acc = fmaf(res, res, loss_acc);
             }
             NOMA_TL(6)
             __syncthreads();
@@ -621,7 +572,8 @@ static_for<NL, 0, -1>([&](auto LC) {
                     // warp -> column tile ct (4 columns) x neuron group jg
                     // (JPB neurons): JS = 16 / NC groups cover all 16 warps
                     constexpr int NCL = (l == 1 ? W0 : H) / 4;
-                    constexpr int JS = NCL >= 16 ? 1 : 16 / NCL;
+                    constexpr int JS = NCL >= NW ? 1 : NW / NCL;
+                    static_assert(NCL <= NW, "one column tile per warp");
                     constexpr int JPB = JT / JS;
                     const int ct = warp % NCL, jg = warp / NCL, r = 4 * lane;
                     const int j0 = jg * JPB;
@@ -677,19 +629,20 @@ static_for<NL, 0, -1>([&](auto LC) {
                         vw[l] = m2;
                         sm[pn + c.w[l] + off] = sm[po + c.w[l] + off] - __fdividef(lrc * m1, sqrtf(m2 * ic2) + p.eps);
                     }
-                    if (ct == 0) {  // biases, then final weights (top layer)
-                        float bv[2 * JPB];
+                    // biases on the column-tile-0 warps, final weights (top layer)
+                    // on the column-tile-1 warps: the extra reductions are spread
+                    if (ct == 0 || (top && ct == 1)) {
+                        float bv[JPB];
 #pragma unroll
                         for (int j = 0; j < JPB; ++j) {
-                            const float2 hb = f2_unpack(sb[j]), hf = f2_unpack(sf[j]);
-                            bv[j] = hb.x + hb.y;
-                            bv[JPB + j] = hf.x + hf.y;
+                            const float2 h = f2_unpack(ct == 0 ? sb[j] : sf[j]);
+                            bv[j] = h.x + h.y;
                         }
-                        reduce_scatter<2 * JPB, 2 * JPB, 32>(bv, lane);
-                        constexpr int BSH = 5 - ilog2c(2 * JPB);
+                        reduce_scatter<JPB, JPB, 32>(bv, lane);
+                        constexpr int BSH = 5 - ilog2c(JPB);
                         const int bi = lane >> BSH;
-                        if ((lane & ((1 << BSH) - 1)) == 0 && (top || bi < JPB)) {
-                            const int off = bi < JPB ? c.b[l] + j0 + bi : c.wf + j0 + bi - JPB;
+                        if ((lane & ((1 << BSH) - 1)) == 0) {
+                            const int off = (ct == 0 ? c.b[l] : c.wf) + j0 + bi;
                             const float gsum = bv[0];
                             const float m1 = p.b1 * mb[l] + p.omb1 * gsum;
                             const float m2 = p.b2 * vb[l] + p.omb2 * (gsum * gsum);
@@ -734,11 +687,11 @@ static_for<NL, 0, -1>([&](auto LC) {
         }
         // ---- epoch loss (hybrid_nn.cpp:190-192): trace[e] = sum r^2 / n -------
         if (rank == 0 && p.trace) {
-            if (tid < 32) sm[c.red + tid] = loss_acc;
+            if (tid < kBatchRows) sm[c.red + tid] = loss_acc;
             __syncthreads();
             if (tid == 0) {
                 double t = 0.0;
-                for (int i = 0; i < 32; ++i) t += sm[c.red + i];
+                for (int i = 0; i < kBatchRows; ++i) t += sm[c.red + i];
                 p.trace[(size_t)net * p.epochs + e] = t / (double)n;
             }
             __syncthreads();
@@ -765,10 +718,37 @@ static_for<NL, 0, -1>([&](auto LC) {
     cl_sync();  // no CTA leaves while a peer could still address its shared memory
 }
 
+// Per-step minibatch tiles for the latency kernel: block (net, step) writes
+// the feature-major tile X[width][kSR] of the rows perm[e][start..start+bsz)
+// (zero rows past the batch), IQ-widened (iq_transform.cpp:17-20), and their
+// r0 targets; the training kernel then moves a whole tile with one bulk copy.
+__global__ void __launch_bounds__(kBatchRows) lat_prep_kernel(TrainParams p, int total) {
+    const int job = blockIdx.x, net = job / total, step = job - net * total;
+    const int spe = (p.rows + p.batch - 1) / p.batch;
+    const int e = step / spe, start = (step - e * spe) * p.batch, bsz = min(p.batch, p.rows - start);
+    const int r = threadIdx.x, n = p.rows, width = p.width, M = width / 2, d = net / p.K;
+    const bool wid = p.layout == NOMA_LAYOUT_WIDEN_COMPLEX;
+    const int idx = r < bsz ? (int)p.perm[((size_t)net * p.epochs + e) * n + start + r] : -1;
+    float *xo = p.xprep + (size_t)job * width * kSR;
+    p.r0prep[(size_t)job * kBatchRows + r] = idx >= 0 ? p.r0[(size_t)net * n + idx] : 0.0f;
+    const float *src = idx < 0 ? nullptr
+                       : wid ? p.design32 + ((size_t)d * (n >> 1) + (idx >> 1)) * width
+                             : p.design32 + ((size_t)d * n + idx) * width;
+    const bool odd = wid && idx >= 0 && (idx & 1);
+    for (int k = 0; k < width; ++k) {
+        float v = 0.0f;
+        if (src) v = !odd ? src[k] : (k < M ? src[M + k] : -src[k - M]);
+        xo[k * kSR + r] = v;
+    }
+    if (r < kSR - kBatchRows)
+        for (int k = 0; k < width; ++k) xo[k * kSR + kBatchRows + r] = 0.0f;
+}
+
 // host: pick the cluster size, carve shared memory, launch.  Returns
 // NOMA_ERR_UNSUPPORTED when latency mode does not apply (caller falls back).
 int train_lat_launch(TrainParams &p, cudaStream_t st) {
     if (p.batch < 1 || p.batch > kBatchRows || p.n_nets < 1) return NOMA_ERR_UNSUPPORTED;
+    if (!p.xprep || !p.r0prep) return NOMA_ERR_UNSUPPORTED;
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -777,6 +757,8 @@ int train_lat_launch(TrainParams &p, cudaStream_t st) {
     if (want == 1) return NOMA_ERR_UNSUPPORTED;
     const long total = (long)((p.rows + p.batch - 1) / p.batch) * p.epochs;
     if (total < 1 || total > kLatMaxSteps) return NOMA_ERR_UNSUPPORTED;
+    if ((size_t)p.n_nets * total * p.width * kSR > p.prep_floats) return NOMA_ERR_UNSUPPORTED;
+    bool prepped = false;  // the tiles are built once, for the first shape that fits
     const int cand[3] = {16, 8, 4};
     for (int ci = 0; ci < 3; ++ci) {
         const int cs = cand[ci];
@@ -785,12 +767,17 @@ int train_lat_launch(TrainParams &p, cudaStream_t st) {
         LatCarve c;
         if (!lat_carve(p.g, cs, p.width, (int)total, &c)) continue;
         const size_t smem = (size_t)c.end * sizeof(float);
-        auto launch = [&](auto kern) -> int {
+        if (!prepped) {
+            lat_prep_kernel<<<(unsigned)(p.n_nets * total), kBatchRows, 0, st>>>(p, (int)total);
+            if (cudaGetLastError() != cudaSuccess) return NOMA_ERR_CUDA;
+            prepped = true;
+        }
+        auto launch = [&](auto kern, int nwarps) -> int {
             cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
             if (cs > 8) cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
             cudaLaunchConfig_t cfg = {};
             cfg.gridDim = dim3(p.n_nets * cs);
-            cfg.blockDim = dim3(kLT);
+            cfg.blockDim = dim3(nwarps * 32);
             cfg.dynamicSmemBytes = smem;
             cfg.stream = st;
             cudaLaunchAttribute attr[1];
@@ -812,11 +799,20 @@ int train_lat_launch(TrainParams &p, cudaStream_t st) {
             return NOMA_OK;
         };
         const int vw = p.width <= 32 ? 2 : 4;  // float4 per gather thread
+        // 8 warps for one hidden layer over a 32-wide input (less issue
+        // contention on the critical path); NOMA_LAT_WARPS=16 overrides
+        int nw = (c.N == 1 && vw == 2) ? 8 : 16;
+        if (const char *f = std::getenv("NOMA_LAT_WARPS")) nw = std::atoi(f) == 8 && c.N == 1 && vw == 2 ? 8 : 16;
         auto pick = [&](auto cs_t, auto jt_t) -> int {
             constexpr int CS = decltype(cs_t)::value, JT = decltype(jt_t)::value;
-            if (c.N == 1) return vw == 2 ? launch(train_lat_kernel<CS, JT, 1, 2>) : launch(train_lat_kernel<CS, JT, 1, 4>);
+            if (c.N == 1) {
+                if (vw == 2) return nw == 8 ? launch(train_lat_kernel<CS, JT, 1, 2, 8>, 8)
+                                            : launch(train_lat_kernel<CS, JT, 1, 2, 16>, 16);
+                return launch(train_lat_kernel<CS, JT, 1, 4, 16>, 16);
+            }
             if constexpr (JT >= 4 && CS * JT <= 64)
-                return vw == 2 ? launch(train_lat_kernel<CS, JT, 2, 2>) : launch(train_lat_kernel<CS, JT, 2, 4>);
+                return vw == 2 ? launch(train_lat_kernel<CS, JT, 2, 2, 16>, 16)
+                               : launch(train_lat_kernel<CS, JT, 2, 4, 16>, 16);
             return NOMA_ERR_UNSUPPORTED;
         };
         using I16 = std::integral_constant<int, 16>;

@@ -35,6 +35,8 @@ struct TrainParams {
         off_end, gs_stride, gsplit, off_mom;
     long long *clocks;      // nullable: phase cycles of block 0 (NOMA_PHASE_CLOCKS)
     int mode;               // out: kernel shape launched (noma_ctx_train_mode codes)
+    float *xprep, *r0prep;  // latency kernel: per-step minibatch tiles (scratch, nullable)
+    size_t prep_floats;     // capacity of xprep (floats)
 };
 
 struct TrainF64Params {
