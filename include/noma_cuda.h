@@ -231,6 +231,13 @@ NOMA_API int noma_synthesize(noma_ctx_t ctx, const noma_scenario *sc, int S,
                              const uint64_t *master_seeds, double *pilot_rx, double *pilot_sym,
                              float *data_rx, uint8_t *data_codes, double *channel,
                              double *noise_power, int mem);
+/* As noma_synthesize with explicit SeedBundles [S][3] = {symbols, channel,
+ * noise} (synthesize(cfg, seeds), channel_sim.cpp:76-117) -- the per-trial
+ * seeds of run_noise_sweep (eval.cpp:212-219). */
+NOMA_API int noma_synthesize_bundles(noma_ctx_t ctx, const noma_scenario *sc, int S,
+                                     const uint64_t *bundles, double *pilot_rx, double *pilot_sym,
+                                     float *data_rx, uint8_t *data_codes, double *channel,
+                                     double *noise_power, int mem);
 
 #ifdef __cplusplus
 }

@@ -514,3 +514,73 @@ def run_slots(sc: Scenario, hidden, seeds, epochs=50, batch=128, lr=0.005, threa
                                  errs.ctypes.data_as(_lp))
     soft_c = soft[..., 0::2] + 1j * soft[..., 1::2] if soft is not None else None
     return SlotResult(w0, cond, status, plans, trace[..., :epochs], soft_c, errs)
+
+
+# ---------------------------------------------------------------- sweep
+# TEST INFRASTRUCTURE: FP64 restatement of detect_user / run_noise_sweep
+# (eval.cpp:100-254) over the primitives above, the checker for
+# paper_2206_05998_b200.sweep (small sizes only).
+def real_design(x: np.ndarray) -> np.ndarray:
+    """eval.cpp:69-74: one row [Re r; Im r] per symbol."""
+    return np.concatenate([x.real, x.imag], axis=1)
+
+
+def detect_user_ref(opts, rec, user, det, abl, trial_tag):
+    """eval.cpp:100-166 (det in {"LLS", "HybridNN"}; abl in {"symmetry_on",
+    "symmetry_off", "symmetry_on_half_data"})."""
+    ms = opts.master_seed
+    dims_h = list(opts.hidden_dims)
+    y = rec.train_symbols[:, user - 1]
+    wd = widen_design(rec.data_rx)
+    if abl != "symmetry_off":
+        if abl == "symmetry_on":
+            design, targets = widen_design(rec.train_rx), widen_targets(y)
+        else:
+            half = rec.train_rx.shape[0] // 2
+            design, targets = widen_design(rec.train_rx[:half]), widen_targets(y[:half])
+        w = lls_fit(design, targets, user)
+        if det == "LLS":
+            return narrow_predictions(wd @ w.w)
+        net = init_params([design.shape[1]] + dims_h, w.w,
+                          Rng(substream_seed(ms, mix_tag(trial_tag, 11))))
+        train(net, design, targets, opts.epochs, opts.batch_size, opts.lr,
+              substream_seed(ms, mix_tag(trial_tag, 12)))
+        return detect(net, wd)
+    rt, rd = real_design(rec.train_rx), real_design(rec.data_rx)
+    preds = []
+    for slot, yy in ((1, y.real.copy()), (2, y.imag.copy())):
+        w = lls_fit(rt, yy, user)
+        if det == "LLS":
+            preds.append(rd @ w.w)
+            continue
+        net = init_params([rt.shape[1]] + dims_h, w.w,
+                          Rng(substream_seed(ms, mix_tag(trial_tag, 11, slot))))
+        train(net, rt, yy, opts.epochs, opts.batch_size, opts.lr,
+              substream_seed(ms, mix_tag(trial_tag, 12, slot)))
+        preds.append(forward(net, rd))
+    return preds[0] + 1j * preds[1]
+
+
+def run_noise_sweep_ref(opts):
+    """eval.cpp:170-254 -> {(snr_index, detector, ablation, user): [ber per trial]}."""
+    sc = opts.scenario
+    users = list(opts.users) or list(range(1, sc.num_users + 1))
+    out = {}
+    for si, snr in enumerate(opts.snr_list):
+        scn = Scenario(sc.num_users, sc.num_antennas, sc.train_symbols, sc.data_symbols,
+                       sc.power_step_db, snr, sc.rx_nonlinearity_gain)
+        for t in range(opts.trials):
+            seeds = (substream_seed(opts.master_seed, 1),
+                     substream_seed(opts.master_seed, mix_tag(2, t)) if opts.fresh_channel_per_trial
+                     else substream_seed(opts.master_seed, 2),
+                     substream_seed(opts.master_seed, mix_tag(3, si, t)))
+            rec = synthesize(scn, seeds)
+            for di, det in enumerate(opts.detectors):
+                for ai, abl in enumerate(opts.ablations):
+                    for u in users:
+                        tag = mix_tag(si, t, u, (di << 8) | ai)
+                        pred = detect_user_ref(opts, rec, u, det, abl, tag)
+                        ber = bit_error_rate(hard_decision_qpsk(pred),
+                                             hard_decision_qpsk(rec.data_symbols[:, u - 1]))
+                        out.setdefault((si, det, abl, u), []).append(ber)
+    return out

@@ -819,10 +819,12 @@ NOMA_API int noma_pipeline(noma_ctx_t c, const noma_net_desc *desc, const noma_t
     return s.finish();
 }
 
-NOMA_API int noma_synthesize(noma_ctx_t c, const noma_scenario *sc, int S,
-                             const uint64_t *master_seeds, double *pilot_rx, double *pilot_sym,
-                             float *data_rx, uint8_t *data_codes, double *channel,
-                             double *noise_power, int mem) {
+}  // extern "C"
+
+namespace {
+int synthesize_impl(noma_ctx_t c, const noma_scenario *sc, int S, const uint64_t *master_seeds,
+                    int bundles, double *pilot_rx, double *pilot_sym, float *data_rx,
+                    uint8_t *data_codes, double *channel, double *noise_power, int mem) {
     if (!c) return NOMA_ERR_ARGUMENT;
     if (!sc || !master_seeds) return fail(c, NOMA_ERR_ARGUMENT, "null argument");
     // ScenarioConfig::validate (channel_sim.cpp:9-21)
@@ -836,7 +838,7 @@ NOMA_API int noma_synthesize(noma_ctx_t c, const noma_scenario *sc, int S,
     std::vector<double> powers(K);
     for (int k = 0; k < K; ++k) powers[k] = std::pow(10.0, (double)(-k) * sc->power_step_db / 10.0);
     Stage s(c, NOMA_MEM_HOST == mem ? NOMA_MEM_HOST : NOMA_MEM_DEVICE);
-    const uint64_t *dseeds = s.in(master_seeds, (size_t)S);
+    const uint64_t *dseeds = s.in(master_seeds, (size_t)S * (bundles ? 3 : 1));
     double *dpow = s.scratch<double>(K);
     SynthParams p;
     p.S = S;
@@ -848,6 +850,7 @@ NOMA_API int noma_synthesize(noma_ctx_t c, const noma_scenario *sc, int S,
     p.noisy = std::isinf(sc->snr_db) ? 0 : 1;
     p.snr_lin = std::pow(10.0, sc->snr_db / 10.0);
     p.seeds = dseeds;
+    p.bundles = bundles;
     p.powers = dpow;
     p.pilot_rx = s.out(pilot_rx, (size_t)S * NT * M * 2);
     p.pilot_sym = s.out(pilot_sym, (size_t)S * NT * K * 2);
@@ -867,6 +870,25 @@ NOMA_API int noma_synthesize(noma_ctx_t c, const noma_scenario *sc, int S,
     int st = s.finish();
     if (mem == NOMA_MEM_DEVICE) cudaStreamSynchronize(c->stream);  // keep `powers` alive
     return st;
+}
+}  // namespace
+
+extern "C" {
+
+NOMA_API int noma_synthesize(noma_ctx_t c, const noma_scenario *sc, int S,
+                             const uint64_t *master_seeds, double *pilot_rx, double *pilot_sym,
+                             float *data_rx, uint8_t *data_codes, double *channel,
+                             double *noise_power, int mem) {
+    return synthesize_impl(c, sc, S, master_seeds, 0, pilot_rx, pilot_sym, data_rx, data_codes,
+                           channel, noise_power, mem);
+}
+
+NOMA_API int noma_synthesize_bundles(noma_ctx_t c, const noma_scenario *sc, int S,
+                                     const uint64_t *bundles, double *pilot_rx, double *pilot_sym,
+                                     float *data_rx, uint8_t *data_codes, double *channel,
+                                     double *noise_power, int mem) {
+    return synthesize_impl(c, sc, S, bundles, 1, pilot_rx, pilot_sym, data_rx, data_codes,
+                           channel, noise_power, mem);
 }
 
 }  // extern "C"

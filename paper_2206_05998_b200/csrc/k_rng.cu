@@ -168,9 +168,10 @@ int set_w0_launch(int n_nets, int d0, int plan_total, const double *w0, float *p
 __global__ void synth_draw_kernel(SynthParams p) {
     const int s = blockIdx.x * blockDim.x + threadIdx.x;
     if (s >= p.S) return;
-    const uint64_t master = p.seeds[s];
-    Xoshiro sym(substream_seed(master, 1)), chan(substream_seed(master, 2)),
-        noise(substream_seed(master, 3));
+    const uint64_t master = p.bundles ? 0 : p.seeds[s];
+    Xoshiro sym(p.bundles ? p.seeds[3 * s] : substream_seed(master, 1)),
+        chan(p.bundles ? p.seeds[3 * s + 1] : substream_seed(master, 2)),
+        noise(p.bundles ? p.seeds[3 * s + 2] : substream_seed(master, 3));
     const double hs = 1.0 / sqrt(2.0);
     double *h = p.channel + (size_t)s * p.M * p.K * 2;
     for (int k = 0; k < p.K; ++k)  // gen_channel: k then m; g++ draws imag first

@@ -74,7 +74,8 @@ struct SynthParams {
     double gain;           // cubic distortion
     int noisy;             // snr finite
     double snr_lin;        // 10^(snr/10), computed on the host (glibc pow)
-    const uint64_t *seeds; // master seeds [S]
+    const uint64_t *seeds; // master seeds [S], or [S][3] {symbols, channel, noise} if bundles
+    int bundles;           // 1: seeds are explicit SeedBundles (eval.cpp:212-219 sweep seeds)
     const double *powers;  // [K], host-computed power_profile
     double *pilot_rx;      // [S][NT][M] c64
     double *pilot_sym;     // [S][NT][K] c64

@@ -26,7 +26,7 @@ EXPORTED = [
     "noma_plan_size", "noma_param_count", "noma_lls_fit", "noma_init_params", "noma_train",
     "noma_detect", "noma_pipeline", "noma_synthesize", "noma_ctx_set_profiling",
     "noma_ctx_phase_ms", "noma_measure_fp32_tflops", "noma_init_params_state",
-    "noma_lls_predict", "noma_train_f64", "noma_ctx_train_mode", "noma_ctx_detect_mode",
+    "noma_lls_predict", "noma_train_f64", "noma_ctx_train_mode", "noma_ctx_detect_mode", "noma_synthesize_bundles",
 ]
 PHASES = ("lls", "init", "shuffle", "train", "detect", "total")
 
@@ -125,6 +125,7 @@ def load():
     L.noma_pipeline.argtypes = [vp, C.POINTER(NetDesc), C.POINTER(TrainCfg), ip, ip, ip, ip, ip,
                                 vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, ip]
     L.noma_synthesize.argtypes = [vp, C.POINTER(Scenario), ip, vp, vp, vp, vp, vp, vp, vp, ip]
+    L.noma_synthesize_bundles.argtypes = [vp, C.POINTER(Scenario), ip, vp, vp, vp, vp, vp, vp, vp, ip]
     L.noma_ctx_set_profiling.argtypes = [vp, ip]
     L.noma_ctx_phase_ms.argtypes = [vp, C.POINTER(C.c_double)]
     L.noma_measure_fp32_tflops.argtypes = [vp, ip, C.POINTER(C.c_double)]
@@ -310,6 +311,15 @@ class Context:
             _ptr(data_rx), _ptr(truth), _ptr(init_seeds), _ptr(shuffle_seeds), _ptr(w0),
             _ptr(cond), _ptr(plans), _ptr(trace), _ptr(soft), _ptr(codes), _ptr(bit_errors),
             _ptr(status), mem))
+
+    def synthesize_bundles(self, sc: Scenario, bundles, pilot_rx=None, pilot_sym=None, data_rx=None,
+                           data_codes=None, channel=None, noise_power=None):
+        """synthesize(cfg, SeedBundle{symbols, channel, noise}) per row of bundles [S, 3]."""
+        mem = _mem_of(bundles, pilot_rx, pilot_sym, data_rx, data_codes, channel, noise_power)
+        S = bundles.shape[0]
+        self._check(self.L.noma_synthesize_bundles(self.h, C.byref(sc), S, _ptr(bundles), _ptr(pilot_rx),
+                                                   _ptr(pilot_sym), _ptr(data_rx), _ptr(data_codes),
+                                                   _ptr(channel), _ptr(noise_power), mem))
 
     def synthesize(self, sc: Scenario, seeds, pilot_rx=None, pilot_sym=None, data_rx=None,
                    data_codes=None, channel=None, noise_power=None):

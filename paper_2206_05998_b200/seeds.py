@@ -26,6 +26,17 @@ def substream_seed(master: int, tag: int) -> int:
     return _splitmix64(s)[0]
 
 
+def mix_tag(a: int, b: int, c: int = 0, d: int = 0) -> int:
+    """eval.cpp:77-84.  splitmix64 advances `s` in place inside the right
+    operand of `s ^= splitmix64(s) + x`; C++17 sequences that operand first,
+    so the XOR applies to the advanced state."""
+    s = (a * 0x9E3779B97F4A7C15 + 1) & _MASK
+    for x in (b, c, d):
+        r, s = _splitmix64(s)
+        s = s ^ ((r + x) & _MASK)
+    return _splitmix64(s)[0]
+
+
 def slot_user_seeds(slot_seeds, K):
     """-> (init_seeds [S,K], shuffle_seeds [S,K]) uint64 for 1-based users."""
     init = np.array([[substream_seed(int(s), 0x1000 + u) for u in range(1, K + 1)]
