@@ -325,3 +325,78 @@ def synthesize(num_users, num_antennas, train_symbols, data_symbols, seeds, powe
                          out.data_rx.view(np.float32), out.data_codes, out.channel.view(np.float64),
                          out.noise_power)
     return out
+
+
+# -------------------------------------------------------------- bench rows
+def bench_rows(net: HybridNet, batch: int, repeats: int = 20, naive_ns_per_sample=None) -> str:
+    """GPU rows for the `noma bench` CSV (fused_inference.cpp:282-338, schema
+    path,dims,batch,ns_per_sample,speedup_vs_naive): the device forward over
+    `batch` rows of the plan, timed with CUDA events (median of `repeats`,
+    like time_median_ns), for the FP32 FFMA kernel ("gpu_ffma") and, when the
+    shape is on the tensor-core path, the tcgen05 3xTF32 kernel
+    ("gpu_tcgen05").  Inputs are widened complex rows (batch/2 symbols), the
+    data-phase layout; the rows are gated against the plan's FP64 forward at
+    the reference FP32 tolerance (test_fused.cpp:128-130) before any timing
+    is reported, as bench_compare gates its paths (:291-301).  The speedup
+    column is filled when the caller supplies the CPU naive ns/sample."""
+    import os
+
+    import torch
+
+    dims = list(net.dims)
+    if batch < 2 or batch % 2 or repeats < 1:
+        raise N.DimensionError(N.ERR_DIMENSION, "bench_rows: batch must be even >= 2, repeats >= 1")
+    if dims[0] % 2:
+        raise N.UnsupportedError(N.ERR_UNSUPPORTED, "bench_rows: widened input width must be even")
+    rng = np.random.default_rng(0x9E24A)
+    nsym, M = batch // 2, dims[0] // 2
+    x = (rng.normal(size=(nsym, M)) + 1j * rng.normal(size=(nsym, M))).astype(np.complex64)
+    # FP64 forward of the plan (the gate)
+    layers, final = net.unpack()
+    wd = np.empty((batch, dims[0]))
+    xr, xi = x.real.astype(np.float64), x.imag.astype(np.float64)
+    wd[0::2, :M], wd[0::2, M:], wd[1::2, :M], wd[1::2, M:] = xr, xi, xi, -xr
+    a = wd
+    for W, b in layers:
+        a = np.maximum(a @ W.T + b, 0.0)
+    ref = wd @ net.plan[:dims[0]].astype(np.float64) + a @ final
+    ref_c = ref[0::2] + 1j * ref[1::2]
+    dev = torch.device("cuda", 0)
+    ctx = context()
+    dx = torch.from_numpy(x.view(np.float32).copy()).to(dev)
+    plan = torch.from_numpy(np.ascontiguousarray(net.plan.reshape(1, -1))).to(dev)
+    soft = torch.empty((nsym, 2), dtype=torch.float32, device=dev)
+    rows = []
+    old = os.environ.get("NOMA_DETECT_TC")
+    try:
+        for path, env in (("gpu_tcgen05", None), ("gpu_ffma", "0")):
+            if env is None:
+                os.environ.pop("NOMA_DETECT_TC", None)
+            else:
+                os.environ["NOMA_DETECT_TC"] = env
+            ctx.detect(dims, N.LAYOUT_WIDEN, 1, 1, nsym, dx, plan, soft=soft)
+            torch.cuda.synchronize()
+            if path == "gpu_tcgen05" and ctx.detect_mode != 2:
+                continue
+            got = soft.cpu().numpy().view(np.complex64).ravel()
+            scale = max(1.0, float(np.max(np.abs(ref_c))))
+            if np.max(np.abs(got - ref_c)) / scale > 1e-5:
+                raise RuntimeError("bench_rows: device path disagrees with the FP64 forward")
+            ns = []
+            for _ in range(repeats):
+                e0 = torch.cuda.Event(enable_timing=True)
+                e1 = torch.cuda.Event(enable_timing=True)
+                e0.record()
+                ctx.detect(dims, N.LAYOUT_WIDEN, 1, 1, nsym, dx, plan, soft=soft)
+                e1.record()
+                e1.synchronize()
+                ns.append(e0.elapsed_time(e1) * 1e6)
+            per = sorted(ns)[len(ns) // 2] / batch
+            sp = "" if naive_ns_per_sample is None else repr(naive_ns_per_sample / per)
+            rows.append(f"{path},{'x'.join(str(d) for d in dims)},{batch},{per!r},{sp}")
+    finally:
+        if old is None:
+            os.environ.pop("NOMA_DETECT_TC", None)
+        else:
+            os.environ["NOMA_DETECT_TC"] = old
+    return "\n".join(rows) + "\n"

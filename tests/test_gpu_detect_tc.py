@@ -51,3 +51,23 @@ def test_detect_tc_matches_reference(A, O, dims, nsym, monkeypatch):
     assert np.max(np.abs(soft_f - soft)) / scale < 2e-6
     assert np.array_equal(bits, bits_f)
     assert errs == errs_f
+
+
+def test_bench_rows(A, O):
+    """`noma bench` GPU rows (fused_inference.cpp:325-338 schema), gated
+    against the FP64 forward; the CPU naive row comes from the oracle here."""
+    import time
+
+    onet = random_net_fused([32, 64, 64], 5)
+    layers, final = onet.layers()
+    net = A.net_from_params(onet.dims, onet.w0, layers, final)
+    x = np.random.default_rng(1).normal(size=(4096, 32))
+    t0 = time.perf_counter()
+    O.fused_forward(onet.dims, O.build_plan(onet), x)
+    naive = (time.perf_counter() - t0) * 1e9 / 4096
+    rows = A.bench_rows(net, 1 << 16, repeats=5, naive_ns_per_sample=naive).splitlines()
+    assert [r.split(",")[0] for r in rows] == ["gpu_tcgen05", "gpu_ffma"]
+    for r in rows:
+        path, dims, batch, ns, sp = r.split(",")
+        assert dims == "32x64x64" and batch == str(1 << 16)
+        assert float(ns) > 0 and float(sp) > 1
