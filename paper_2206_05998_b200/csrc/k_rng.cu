@@ -9,62 +9,183 @@
 // thread per receive sample.
 #include <math.h>
 
+#include <mutex>
+#include <vector>
+
 #include "kernels.cuh"
 
 namespace noma_dev {
 
-// ---------------------------------------------------------------- shuffle
-// perm[net][epoch][n] (u16).  Each thread owns one (net, epoch) and keeps its
-// index array in shared memory while applying the 1..n-1 swaps.
-__global__ void perm_kernel(int n_nets, int epochs, int n, const uint64_t *shuffle_seeds,
-                            uint16_t *perm) {
-    extern __shared__ uint16_t sidx[];
-    const int job = blockIdx.x * blockDim.x + threadIdx.x;
-    if (job >= n_nets * epochs) return;
-    const int net = job / epochs, epoch = job % epochs;
-    uint16_t *idx = sidx + (size_t)threadIdx.x * n;
-    for (int i = 0; i < n; ++i) idx[i] = (uint16_t)i;
-    Xoshiro r(substream_seed(shuffle_seeds[net], (uint64_t)epoch));
-    for (int i = n - 1; i > 0; --i) {
-        const int j = (int)r.below((uint64_t)i + 1);
-        const uint16_t t = idx[i];
-        idx[i] = idx[j];
-        idx[j] = t;
+// ------------------------------------------------------------ jump-ahead
+// xoshiro256's state update (rng.hpp:35-45, without the ++ output scrambler)
+// is linear over GF(2): s' = T s with T a 256x256 bit matrix.  With
+// J = T^kJumpDraws precomputed, the state before draw c*kJumpDraws is J^c s0,
+// so independent threads can generate consecutive blocks of one reference
+// stream -- bit-identical draws, in parallel.  Tables (rows = 4 x u64 per
+// output bit): lo[b] = J^b (b < kJumpLo), hi[a] = J^(kJumpLo a) (a < kJumpHi),
+// built once per device on the host.
+constexpr int kJumpDraws = 128;
+constexpr int kJumpLo = 64, kJumpHi = 64;  // up to 4096 blocks = 524288 draws
+
+namespace {
+struct Gf2 {
+    uint64_t r[256][4];
+};
+void gf2_mul(const Gf2 &a, const Gf2 &b, Gf2 &out) {  // out = a . b (row form)
+    for (int i = 0; i < 256; ++i) {
+        uint64_t acc[4] = {0, 0, 0, 0};
+        for (int k = 0; k < 256; ++k)
+            if ((a.r[i][k >> 6] >> (k & 63)) & 1)
+                for (int w = 0; w < 4; ++w) acc[w] ^= b.r[k][w];
+        for (int w = 0; w < 4; ++w) out.r[i][w] = acc[w];
     }
+}
+void gf2_step_matrix(Gf2 &t) {  // T: column j = one xoshiro step of e_j
+    for (int i = 0; i < 256; ++i)
+        for (int w = 0; w < 4; ++w) t.r[i][w] = 0;
+    for (int j = 0; j < 256; ++j) {
+        uint64_t s[4] = {0, 0, 0, 0};
+        s[j >> 6] = 1ull << (j & 63);
+        Xoshiro x(s[0], s[1], s[2], s[3]);
+        x.next();
+        const uint64_t o[4] = {x.s0, x.s1, x.s2, x.s3};
+        for (int i = 0; i < 256; ++i)
+            if ((o[i >> 6] >> (i & 63)) & 1) t.r[i][j >> 6] |= 1ull << (j & 63);
+    }
+}
+std::mutex g_jump_mu;
+const uint64_t *g_jump[64] = {};  // per device: lo tables then hi tables
+}  // namespace
+
+// Device table [kJumpLo + kJumpHi][256][4] for the current device (cached).
+const uint64_t *jump_table() {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lk(g_jump_mu);
+    if (dev < 0 || dev >= 64) return nullptr;
+    if (g_jump[dev]) return g_jump[dev];
+    std::vector<Gf2> tab(kJumpLo + kJumpHi);
+    Gf2 t, j, tmp;
+    gf2_step_matrix(t);
+    j = t;  // J = T^128 by squaring (128 = 2^7)
+    for (int k = 0; k < 7; ++k) {
+        gf2_mul(j, j, tmp);
+        j = tmp;
+    }
+    for (int i = 0; i < 256; ++i)
+        for (int w = 0; w < 4; ++w) tab[0].r[i][w] = (w == (i >> 6)) ? 1ull << (i & 63) : 0;
+    for (int b = 1; b < kJumpLo; ++b) gf2_mul(tab[b - 1], j, tab[b]);
+    Gf2 big;
+    gf2_mul(tab[kJumpLo - 1], j, big);  // J^kJumpLo
+    tab[kJumpLo] = tab[0];
+    for (int a = 1; a < kJumpHi; ++a) gf2_mul(tab[kJumpLo + a - 1], big, tab[kJumpLo + a]);
+    uint64_t *d = nullptr;
+    const size_t bytes = tab.size() * sizeof(Gf2);
+    if (cudaMalloc(&d, bytes) != cudaSuccess) return nullptr;
+    if (cudaMemcpy(d, tab.data(), bytes, cudaMemcpyHostToDevice) != cudaSuccess) {
+        cudaFree(d);
+        return nullptr;
+    }
+    g_jump[dev] = d;
+    return d;
+}
+
+// s <- M s over GF(2) (M in row form, 256 x 4 u64)
+__device__ __forceinline__ void gf2_apply(const uint64_t *__restrict__ m, Xoshiro &x) {
+    uint64_t o[4] = {0, 0, 0, 0};
+#pragma unroll 4
+    for (int i = 0; i < 256; ++i) {
+        const uint64_t *row = m + 4 * i;
+        const uint64_t v = (__ldg(row) & x.s0) ^ (__ldg(row + 1) & x.s1) ^ (__ldg(row + 2) & x.s2) ^
+                           (__ldg(row + 3) & x.s3);
+        o[i >> 6] |= (uint64_t)(__popcll(v) & 1) << (i & 63);
+    }
+    x.s0 = o[0];
+    x.s1 = o[1];
+    x.s2 = o[2];
+    x.s3 = o[3];
+}
+// advance x by `block` blocks of kJumpDraws draws
+__device__ __forceinline__ void jump_blocks(const uint64_t *tab, int block, Xoshiro &x) {
+    const int lo = block % kJumpLo, hi = block / kJumpLo;
+    if (lo) gf2_apply(tab + (size_t)lo * 1024, x);
+    if (hi) gf2_apply(tab + (size_t)(kJumpLo + hi) * 1024, x);
+}
+
+// ---------------------------------------------------------------- shuffle
+// perm[net][epoch][n] (u16), Fisher-Yates of hybrid_nn.cpp:148-154 with
+// Rng(substream_seed(shuffle_seed, epoch)) (:176).  One warp per (net,
+// epoch): the n-1 draws below(i+1), i = n-1..1, are generated in blocks of
+// kJumpDraws by the lanes in parallel (jump-ahead, bit-identical stream) into
+// shared memory; lane 0 then applies the swap chain, which is inherently
+// sequential, and the warp writes the permutation out.
+constexpr int kPermWarps = 4;
+
+__global__ void __launch_bounds__(32 * kPermWarps) perm_kernel(int n_nets, int epochs, int n,
+                                                               const uint64_t *shuffle_seeds,
+                                                               uint16_t *perm, const uint64_t *jtab) {
+    extern __shared__ uint16_t sbuf[];  // per warp: idx[n], draws[n]
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int job = blockIdx.x * kPermWarps + warp;
+    if (job >= n_nets * epochs) return;  // warp-uniform
+    const int net = job / epochs, epoch = job % epochs;
+    uint16_t *idx = sbuf + (size_t)warp * 2 * n, *jd = idx + n;
+    const Xoshiro r0(substream_seed(shuffle_seeds[net], (uint64_t)epoch));
+    const int draws = n - 1, nblk = (draws + kJumpDraws - 1) / kJumpDraws;
+    for (int bk = lane; bk < nblk; bk += 32) {
+        Xoshiro r = r0;
+        jump_blocks(jtab, bk, r);
+        const int k_end = min(draws, (bk + 1) * kJumpDraws);
+        for (int k = bk * kJumpDraws; k < k_end; ++k) {  // draw k is for i = n-1-k
+            const int i = n - 1 - k;
+            jd[k] = (uint16_t)r.below((uint64_t)i + 1);
+        }
+    }
+    for (int i = lane; i < n; i += 32) idx[i] = (uint16_t)i;
+    __syncwarp();
+    if (lane == 0) {
+        for (int k = 0; k < draws; ++k) {
+            const int i = n - 1 - k, j = jd[k];
+            const uint16_t t = idx[i];
+            idx[i] = idx[j];
+            idx[j] = t;
+        }
+    }
+    __syncwarp();
     uint16_t *out = perm + (size_t)job * n;
-    for (int i = 0; i < n; ++i) out[i] = idx[i];
+    for (int i = lane; i < n; i += 32) out[i] = idx[i];
 }
 
 int perm_launch(int n_nets, int epochs, int n, const uint64_t *seeds, uint16_t *perm,
                 cudaStream_t st) {
     if (n > 65535) return NOMA_ERR_UNSUPPORTED;
     const int jobs = n_nets * epochs;
-    if (jobs == 0) return NOMA_OK;
-    int tpb = (int)((160 * 1024) / (2 * (size_t)n));
-    tpb = tpb > 64 ? 64 : tpb;
-    if (tpb < 1) return NOMA_ERR_UNSUPPORTED;
-    const size_t smem = (size_t)tpb * n * sizeof(uint16_t);
+    if (jobs == 0 || n < 1) return NOMA_OK;
+    if ((n - 1 + kJumpDraws - 1) / kJumpDraws > kJumpLo * kJumpHi) return NOMA_ERR_UNSUPPORTED;
+    const uint64_t *jt = jump_table();
+    if (!jt) return NOMA_ERR_CUDA;
+    const size_t smem = (size_t)kPermWarps * 2 * n * sizeof(uint16_t);
+    if (smem > 227 * 1024) return NOMA_ERR_UNSUPPORTED;
     cudaFuncSetAttribute(perm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    perm_kernel<<<(jobs + tpb - 1) / tpb, tpb, smem, st>>>(n_nets, epochs, n, seeds, perm);
+    perm_kernel<<<(jobs + kPermWarps - 1) / kPermWarps, 32 * kPermWarps, smem, st>>>(n_nets, epochs, n,
+                                                                                    seeds, perm, jt);
     return cudaGetLastError() == cudaSuccess ? NOMA_OK : NOMA_ERR_CUDA;
 }
 
 // ------------------------------------------------------------------- init
 // He-normal initialisation (hybrid_nn.cpp:43-52), one CTA per net.  The
-// reference stream is sequential, so one producer thread runs xoshiro256++
-// ahead into a double-buffered shared-memory ring of raw u64 pairs while the
-// other threads turn the previous chunk into Box-Muller draws (the FP64
-// log/sqrt/cos dominate the per-draw cost) and scatter them into the plan
-// (FP32, FusedPlan layout) and/or the flat FP64 parameter vector.
-// Seeds come from `seeds` (Rng(seed)) or, when `states` is non-null, from
-// caller xoshiro states that are advanced in place (init_params(..., Rng&)).
+// reference stream (2 u64 per gaussian, row-major per layer) is cut into
+// blocks of kJumpDraws draws; thread b jumps its own xoshiro copy to block b
+// (jump_blocks) and turns the block's 64 pairs into Box-Muller draws (the FP64
+// log/sqrt/cos dominate), scattered into the plan (FP32, FusedPlan layout)
+// and/or the flat FP64 parameter vector.  Seeds come from `seeds`
+// (Rng(seed)) or, when `states` is non-null, from caller xoshiro states that
+// are advanced in place past all draws (init_params(..., Rng&)).
 constexpr int kInitThreads = 128;
-constexpr int kInitChunk = 1024;  // gaussians per ring slot
 
 __global__ void __launch_bounds__(kInitThreads) init_block_kernel(
     NetGeom g, const uint64_t *seeds, uint64_t *states, const double *w0, float *plans,
-    double *theta, int ptrain) {
-    __shared__ uint64_t ring[2][2 * kInitChunk];
+    double *theta, int ptrain, const uint64_t *jtab) {
     const int net = blockIdx.x, tid = threadIdx.x;
     float *pl = plans ? plans + (size_t)net * g.plan_total : nullptr;
     double *th = theta ? theta + (size_t)net * ptrain : nullptr;
@@ -86,63 +207,63 @@ __global__ void __launch_bounds__(kInitThreads) init_block_kernel(
         total += g.dims[l] * g.dims[l - 1];
     }
     start[g.nd] = total;
-    Xoshiro r = states ? Xoshiro(states[net * 4], states[net * 4 + 1], states[net * 4 + 2], states[net * 4 + 3])
-                       : Xoshiro(seeds[net]);
-    const int chunks = (total + kInitChunk - 1) / kInitChunk;
-    auto produce = [&](int c) {
-        const int n = min(kInitChunk, total - c * kInitChunk);
-        uint64_t *b = ring[c & 1];
-        for (int i = 0; i < 2 * n; ++i) b[i] = r.next();
-    };
-    if (tid == 0 && chunks > 0) produce(0);
-    __syncthreads();
-    for (int c = 0; c < chunks; ++c) {
-        if (tid == 0) {
-            if (c + 1 < chunks) produce(c + 1);
-        } else {
-            const int n = min(kInitChunk, total - c * kInitChunk);
-            const uint64_t *b = ring[c & 1];
-            for (int i = tid - 1; i < n; i += kInitThreads - 1) {
-                const int w = c * kInitChunk + i;
-                int l = 1;
-                while (w >= start[l + 1]) ++l;
-                const int fan_in = g.dims[l - 1];
-                const int off = w - start[l], row = off / fan_in, col = off % fan_in;
-                // Box-Muller cosine half (rng.hpp:58-62) on the recorded pair
-                const double u1 = 1.0 - static_cast<double>(b[2 * i] >> 11) * 0x1.0p-53;
-                const double u2 = static_cast<double>(b[2 * i + 1] >> 11) * 0x1.0p-53;
-                const double ang = __dmul_rn(2.0 * 3.141592653589793238462643383279502884, u2);
-                const double gauss = __dmul_rn(sqrt(__dmul_rn(-2.0, log(u1))), cos(ang));
-                const double v = gauss * sqrt(2.0 / fan_in);
-                if (pl) pl[g.plan_w[l] + row * g.plan_pad[l - 1] + col] = (float)v;
-                if (th) {
-                    int t = 0;  // flat offset: W_1, b_1, ..., W_l block
-                    for (int q = 1; q < l; ++q) t += g.dims[q] * g.dims[q - 1] + g.dims[q];
-                    th[t + off] = v;
-                }
+    const Xoshiro r0 = states ? Xoshiro(states[net * 4], states[net * 4 + 1], states[net * 4 + 2], states[net * 4 + 3])
+                              : Xoshiro(seeds[net]);
+    constexpr int G = kJumpDraws / 2;  // gaussians per block
+    const int blocks = (total + G - 1) / G;
+    for (int b = tid; b < blocks; b += kInitThreads) {
+        Xoshiro r = r0;
+        jump_blocks(jtab, b, r);
+        const int w_end = min(total, (b + 1) * G);
+        int l = 1;
+        for (int w = b * G; w < w_end; ++w) {
+            const uint64_t a1 = r.next(), a2 = r.next();
+            while (w >= start[l + 1]) ++l;
+            const int fan_in = g.dims[l - 1];
+            const int off = w - start[l], row = off / fan_in, col = off % fan_in;
+            // Box-Muller cosine half (rng.hpp:58-62)
+            const double u1 = 1.0 - static_cast<double>(a1 >> 11) * 0x1.0p-53;
+            const double u2 = static_cast<double>(a2 >> 11) * 0x1.0p-53;
+            const double ang = __dmul_rn(2.0 * 3.141592653589793238462643383279502884, u2);
+            const double gauss = __dmul_rn(sqrt(__dmul_rn(-2.0, log(u1))), cos(ang));
+            const double v = gauss * sqrt(2.0 / fan_in);
+            if (pl) pl[g.plan_w[l] + row * g.plan_pad[l - 1] + col] = (float)v;
+            if (th) {
+                int t = 0;  // flat offset: W_1, b_1, ..., W_l block
+                for (int q = 1; q < l; ++q) t += g.dims[q] * g.dims[q - 1] + g.dims[q];
+                th[t + off] = v;
             }
         }
-        __syncthreads();
-    }
-    if (states && tid == 0) {
-        states[net * 4] = r.s0;
-        states[net * 4 + 1] = r.s1;
-        states[net * 4 + 2] = r.s2;
-        states[net * 4 + 3] = r.s3;
+        if (states && w_end == total) {  // the last block leaves the stream past every draw
+            states[net * 4] = r.s0;
+            states[net * 4 + 1] = r.s1;
+            states[net * 4 + 2] = r.s2;
+            states[net * 4 + 3] = r.s3;
+        }
     }
 }
 
 int init_state_launch(const NetGeom &g, int n_nets, uint64_t *states, const double *w0,
                       float *plans, double *theta, int ptrain, cudaStream_t st) {
     if (n_nets == 0) return NOMA_OK;
-    init_block_kernel<<<n_nets, kInitThreads, 0, st>>>(g, nullptr, states, w0, plans, theta, ptrain);
+    const uint64_t *jt = jump_table();
+    if (!jt) return NOMA_ERR_CUDA;
+    int total = 0;
+    for (int l = 1; l < g.nd; ++l) total += g.dims[l] * g.dims[l - 1];
+    if ((total + kJumpDraws / 2 - 1) / (kJumpDraws / 2) > kJumpLo * kJumpHi) return NOMA_ERR_UNSUPPORTED;
+    init_block_kernel<<<n_nets, kInitThreads, 0, st>>>(g, nullptr, states, w0, plans, theta, ptrain, jt);
     return cudaGetLastError() == cudaSuccess ? NOMA_OK : NOMA_ERR_CUDA;
 }
 
 int init_launch(const NetGeom &g, int n_nets, const uint64_t *seeds, const double *w0,
                 float *plans, cudaStream_t st) {
     if (n_nets == 0) return NOMA_OK;
-    init_block_kernel<<<n_nets, kInitThreads, 0, st>>>(g, seeds, nullptr, w0, plans, nullptr, 0);
+    const uint64_t *jt = jump_table();
+    if (!jt) return NOMA_ERR_CUDA;
+    int total = 0;
+    for (int l = 1; l < g.nd; ++l) total += g.dims[l] * g.dims[l - 1];
+    if ((total + kJumpDraws / 2 - 1) / (kJumpDraws / 2) > kJumpLo * kJumpHi) return NOMA_ERR_UNSUPPORTED;
+    init_block_kernel<<<n_nets, kInitThreads, 0, st>>>(g, seeds, nullptr, w0, plans, nullptr, 0, jt);
     return cudaGetLastError() == cudaSuccess ? NOMA_OK : NOMA_ERR_CUDA;
 }
 
