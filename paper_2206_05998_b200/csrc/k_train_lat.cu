@@ -358,9 +358,10 @@ __global__ void __launch_bounds__(NW * 32, 1) train_lat_kernel(TrainParams p, La
     // Adam moments of the parameters this thread updates (registers; fixed
     // thread -> parameter map for the whole training): per layer one weight
     // and one bias-or-final-weight.
-    float mw[NL + 1], vw[NL + 1], mb[NL + 1], vb[NL + 1];
+    // (up to 2 column tiles per warp when a layer has more tiles than warps)
+    float mw[NL + 1][2], vw[NL + 1][2], mb[NL + 1], vb[NL + 1];
 #pragma unroll
-    for (int l = 0; l <= NL; ++l) mw[l] = vw[l] = mb[l] = vb[l] = 0.f;
+    for (int l = 0; l <= NL; ++l) mw[l][0] = vw[l][0] = mw[l][1] = vw[l][1] = mb[l] = vb[l] = 0.f;
 
     // forward thread map: 8 k-split lanes x 32 row quads x 2 neuron halves;
     // after the k reduce-scatter a lane holds FV values (neuron fj, rows
@@ -516,12 +517,13 @@ static_for<NL, 0, -1>([&](auto LC) {
                 const float *dyp = sm + c.dy, *wfp = sm + po + c.wf;
                 const float *in = l == 1 ? XT : sm + c.af[l - 1] + buf * H * kSR;
                 const int sw = c.sw[l];
-                if (l > 1 && tid < (H / 4) * 32) {
+                if (l > 1)
+                for (int tt = tid; tt < (H / 4) * 32; tt += kLT) {
                     // dA_{l-1} partial = sum_{j own} W_l[j][c] dZ_l[j][r] (:111) for
                     // every c (4 c x 4 r per thread), sent to the owner of c.
                     const float *W = sm + po + c.w[l];
                     const uint32_t rb = s2u(bars + 3 + 2 * (l - 2));
-                    const int cq = tid >> 5, r = 4 * lane, cc = 4 * cq;  // H/4 = 16 warps
+                    const int cq = tt >> 5, r = 4 * lane, cc = 4 * cq;
                     f2_t acc[4][2];
 #pragma unroll
                     for (int q = 0; q < 4; ++q) acc[q][0] = acc[q][1] = 0ull;
@@ -568,14 +570,17 @@ static_for<NL, 0, -1>([&](auto LC) {
                 // weight gradient dZ^T A (:109), bias colsum (:110), final a_N^T dy
                 // (:99): warp ct owns column tile 4ct..4ct+3 for all JT neurons,
                 // lane = row quad; lane reduce-scatter, then Adam in registers.
-                {
+                constexpr int NCL = (l == 1 ? W0 : H) / 4;
+                constexpr int TPW = NCL > NW ? NCL / NW : 1;  // column tiles per warp
+                static_assert(TPW <= 2 && (NCL <= NW || NCL % NW == 0), "tile map");
+#pragma unroll
+                for (int tw = 0; tw < TPW; ++tw) {
                     // warp -> column tile ct (4 columns) x neuron group jg
-                    // (JPB neurons): JS = 16 / NC groups cover all 16 warps
-                    constexpr int NCL = (l == 1 ? W0 : H) / 4;
+                    // (JPB neurons): JS = NW / NC groups cover all warps
                     constexpr int JS = NCL >= NW ? 1 : NW / NCL;
-                    static_assert(NCL <= NW, "one column tile per warp");
                     constexpr int JPB = JT / JS;
-                    const int ct = warp % NCL, jg = warp / NCL, r = 4 * lane;
+                    const int ct = NCL > NW ? warp + NW * tw : warp % NCL;
+                    const int jg = NCL > NW ? 0 : warp / NCL, r = 4 * lane;
                     const int j0 = jg * JPB;
                     f2_t acc[JPB][4], sb[JPB], sf[JPB];
 #pragma unroll
@@ -623,10 +628,10 @@ static_for<NL, 0, -1>([&](auto LC) {
                     if ((lane & ((1 << GSH) - 1)) == 0) {
                         const int off = (j0 + (gi >> 2)) * sw + 4 * ct + (gi & 3);
                         const float gsum = gv[0];
-                        const float m1 = p.b1 * mw[l] + p.omb1 * gsum;
-                        const float m2 = p.b2 * vw[l] + p.omb2 * (gsum * gsum);
-                        mw[l] = m1;
-                        vw[l] = m2;
+                        const float m1 = p.b1 * mw[l][tw] + p.omb1 * gsum;
+                        const float m2 = p.b2 * vw[l][tw] + p.omb2 * (gsum * gsum);
+                        mw[l][tw] = m1;
+                        vw[l][tw] = m2;
                         sm[pn + c.w[l] + off] = sm[po + c.w[l] + off] - __fdividef(lrc * m1, sqrtf(m2 * ic2) + p.eps);
                     }
                     // biases on the column-tile-0 warps, final weights (top layer)
@@ -801,8 +806,9 @@ int train_lat_launch(TrainParams &p, cudaStream_t st) {
         const int vw = p.width <= 32 ? 2 : 4;  // float4 per gather thread
         // 8 warps for one hidden layer over a 32-wide input (less issue
         // contention on the critical path); NOMA_LAT_WARPS=16 overrides
-        int nw = (c.N == 1 && vw == 2) ? 8 : 16;
-        if (const char *f = std::getenv("NOMA_LAT_WARPS")) nw = std::atoi(f) == 8 && c.N == 1 && vw == 2 ? 8 : 16;
+        const bool nw8_ok = vw == 2;  // 32-wide input: k split and column tiles fit 8 warps
+        int nw = nw8_ok ? 8 : 16;
+        if (const char *f = std::getenv("NOMA_LAT_WARPS")) nw = std::atoi(f) == 8 && nw8_ok ? 8 : 16;
         auto pick = [&](auto cs_t, auto jt_t) -> int {
             constexpr int CS = decltype(cs_t)::value, JT = decltype(jt_t)::value;
             if (c.N == 1) {
@@ -810,9 +816,11 @@ int train_lat_launch(TrainParams &p, cudaStream_t st) {
                                             : launch(train_lat_kernel<CS, JT, 1, 2, 16>, 16);
                 return launch(train_lat_kernel<CS, JT, 1, 4, 16>, 16);
             }
-            if constexpr (JT >= 4 && CS * JT <= 64)
-                return vw == 2 ? launch(train_lat_kernel<CS, JT, 2, 2, 16>, 16)
-                               : launch(train_lat_kernel<CS, JT, 2, 4, 16>, 16);
+            if constexpr (JT >= 4 && CS * JT <= 64) {
+                if (vw == 2) return nw == 8 ? launch(train_lat_kernel<CS, JT, 2, 2, 8>, 8)
+                                            : launch(train_lat_kernel<CS, JT, 2, 2, 16>, 16);
+                return launch(train_lat_kernel<CS, JT, 2, 4, 16>, 16);
+            }
             return NOMA_ERR_UNSUPPORTED;
         };
         using I16 = std::integral_constant<int, 16>;
