@@ -29,6 +29,8 @@ constexpr int kLlsMaxM = 64;     // complex columns (widened width <= 128)
 constexpr int kLlsMaxE = 18;     // Gram/RHS entries per thread (registers)
 
 __host__ __device__ inline int lls_chunk(int m) { return m <= 16 ? 64 : m <= 32 ? 32 : 16; }
+// Gram row groups (a function of m only: see phase A)
+__host__ __device__ inline int lls_row_groups(int m) { return m <= 16 ? 4 : m <= 32 ? 2 : 1; }
 
 __device__ __forceinline__ void cp_async16(void *dst, const void *src) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((unsigned)__cvta_generic_to_shared(dst)),
@@ -44,12 +46,15 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
-// MAXE Gram/RHS entries per thread; ILP independent partial sums per entry
-// (small problems: one entry per thread, split over ILP row phases).
-template <int MAXE, int ILP>
+// Phase A register blocking: a thread accumulates 2 x 2 complex blocks
+// (columns a, a+1 against columns b, b+1 of the design, or targets k, k+1) --
+// four complex operands per row feed four MACs -- over the rows of its row
+// group; MB = blocks per thread, row groups fill the CTA when blocks are few.
+template <int MB>
 __global__ void __launch_bounds__(kThreads) lls_kernel(LlsParams p) {
     extern __shared__ __align__(16) double smem[];
     const int m = p.m, K = p.K, d = blockIdx.x, tid = threadIdx.x;
+    const int warp = tid >> 5, lane = tid & 31;
     const int CH = lls_chunk(m);
     const bool cplx_layout = p.layout == NOMA_LAYOUT_WIDEN_COMPLEX;
     double *A = smem;                       // m*m complex (Gram -> eigenvalues)
@@ -62,7 +67,8 @@ __global__ void __launch_bounds__(kThreads) lls_kernel(LlsParams p) {
     double *red = lam + m;                  // 2 * kThreads reduction scratch
     double *U = bufs;                       // m*K complex: V^H d / lambda (reuses bufs)
     __shared__ int pair_p[kLlsMaxM / 2 + 1], pair_q[kLlsMaxM / 2 + 1];
-    __shared__ int any_rot[2];  // by sweep parity; reset one sweep ahead
+    __shared__ int any_rot[2];    // by sweep parity; reset one sweep ahead
+    __shared__ int round_rot[2];  // by round parity: some pair rotates
 
     // Staging of CH rows of the design and the targets into buffer b with
     // cp.async (row-major complex rows are contiguous; REAL rows fill the Re
@@ -97,25 +103,36 @@ __global__ void __launch_bounds__(kThreads) lls_kernel(LlsParams p) {
         p.clocks[I] += now - ck;             \
         ck = now;                            \
     }
-    // ---- phase A: Gram (upper triangle) and RHS, accumulated in registers.
-    const int ngram = m * (m + 1) / 2, nent = ngram + m * K;
-    double acc_re[MAXE][ILP], acc_im[MAXE][ILP];
-    int ea[MAXE], eb[MAXE];
+    // ---- phase A: Gram (upper 2x2 blocks) and RHS blocks in registers ------
+    // Task = (row group g, block): rows t == g (mod RG) in order; the RG
+    // partials are summed in group order.  RG depends on m only, so every
+    // entry's arithmetic is independent of how many users share the fit --
+    // batched and single-user fits agree bitwise (test_lls.cpp:120-134).
+    const int nb = (m + 1) / 2, nk = (K + 1) / 2;
+    const int ngb = nb * (nb + 1) / 2, nblk = ngb + nb * nk;
+    const int RG = lls_row_groups(m);
+    const int ntask = RG * nblk;
+    int tg[MB], ba[MB], bb[MB];  // task row group, block coordinates (bb >= nb: targets)
+    double acc[MB][4][2];
 #pragma unroll
-    for (int e = 0; e < MAXE; ++e) {
-#pragma unroll
-        for (int u = 0; u < ILP; ++u) acc_re[e][u] = acc_im[e][u] = 0.0;
-        const int id = tid + e * kThreads;
-        ea[e] = eb[e] = -1;
-        if (id < ngram) {  // map id -> (a <= b)
-            int a = 0, rem = id;
-            while (rem >= m - a) { rem -= m - a; ++a; }
-            ea[e] = a;
-            eb[e] = a + rem;
-        } else if (id < nent) {
-            ea[e] = (id - ngram) / K;
-            eb[e] = m + (id - ngram) % K;  // b >= m encodes target k = b - m
+    for (int e = 0; e < MB; ++e) {
+        const int task = tid + e * kThreads;
+        tg[e] = ba[e] = bb[e] = -1;
+        if (task < ntask) {
+            const int g = task / nblk, id = task - g * nblk;
+            tg[e] = g;
+            if (id < ngb) {
+                int A_ = 0, rem = id;
+                while (rem >= nb - A_) { rem -= nb - A_; ++A_; }
+                ba[e] = A_;
+                bb[e] = A_ + rem;
+            } else {
+                ba[e] = (id - ngb) / nk;
+                bb[e] = nb + (id - ngb) % nk;
+            }
         }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) acc[e][q][0] = acc[e][q][1] = 0.0;
     }
     issue(0, 0);
     for (int ch = 0; ch < nch; ++ch) {
@@ -141,53 +158,91 @@ __global__ void __launch_bounds__(kThreads) lls_kernel(LlsParams p) {
             }
         }
 #pragma unroll
-        for (int e = 0; e < MAXE; ++e) {
-            if (ea[e] < 0) continue;
-            const int a = ea[e], b = eb[e];
-            const bool rhs = b >= m;
-            const double *bp = rhs ? ys + 2 * (b - m) : xs + 2 * b;
-            const int bst = rhs ? 2 * K : 2 * m;
-            // rows t = u, u + ILP, ...: ILP independent accumulation chains
-            for (int t = 0; t < tn; t += ILP) {
-#pragma unroll
-                for (int u = 0; u < ILP; ++u) {
-                    if (t + u < tn) {
-                        const double xr = xs[2 * ((t + u) * m + a)], xi = xs[2 * ((t + u) * m + a) + 1];
-                        const double br = bp[(t + u) * bst], bi = bp[(t + u) * bst + 1];
-                        acc_re[e][u] += xr * br + xi * bi;  // conj(x_a) * b
-                        acc_im[e][u] += xr * bi - xi * br;
-                    }
-                }
+        for (int e = 0; e < MB; ++e) {
+            if (tg[e] < 0) continue;
+            const int a0 = 2 * ba[e], a1 = min(a0 + 1, m - 1);
+            const bool rhs = bb[e] >= nb;
+            const int c0 = rhs ? 2 * (bb[e] - nb) : 2 * bb[e];
+            const int c1 = min(c0 + 1, (rhs ? K : m) - 1);
+            const double *bp = rhs ? ys : xs;
+            const int bst = rhs ? K : m;
+            for (int t = tg[e]; t < tn; t += RG) {  // CH % RG == 0: global row parity kept
+                const double2 x0 = *reinterpret_cast<const double2 *>(xs + 2 * (t * m + a0));
+                const double2 x1 = *reinterpret_cast<const double2 *>(xs + 2 * (t * m + a1));
+                const double2 y0 = *reinterpret_cast<const double2 *>(bp + 2 * (t * bst + c0));
+                const double2 y1 = *reinterpret_cast<const double2 *>(bp + 2 * (t * bst + c1));
+                // conj(x) * y: (xr yr + xi yi) + i (xr yi - xi yr)
+                acc[e][0][0] += x0.x * y0.x + x0.y * y0.y;
+                acc[e][0][1] += x0.x * y0.y - x0.y * y0.x;
+                acc[e][1][0] += x0.x * y1.x + x0.y * y1.y;
+                acc[e][1][1] += x0.x * y1.y - x0.y * y1.x;
+                acc[e][2][0] += x1.x * y0.x + x1.y * y0.y;
+                acc[e][2][1] += x1.x * y0.y - x1.y * y0.x;
+                acc[e][3][0] += x1.x * y1.x + x1.y * y1.y;
+                acc[e][3][1] += x1.x * y1.y - x1.y * y1.x;
             }
         }
         __syncthreads();  // buffer (ch & 1) is refilled by the next issue
     }
     NOMA_LLS_CLK(0)
+    // group partials -> shared memory (bufs is free), summed in group order
+    // (RG == 1: the thread's own sums are already final; stage them the same way
+    // only when they fit, else write them directly below)
+    double *part = bufs;  // [task][4][2]
+    const bool staged = RG > 1 || (size_t)ntask * 8 <= (size_t)2 * bstride;
+#pragma unroll
+    for (int e = 0; e < MB; ++e)
+        if (tg[e] >= 0 && staged)
+            for (int q = 0; q < 4; ++q) {
+                const int task = tid + e * kThreads;
+                part[(task * 4 + q) * 2] = acc[e][q][0];
+                part[(task * 4 + q) * 2 + 1] = acc[e][q][1];
+            }
+    __syncthreads();
     double fro = 0.0;  // squared Frobenius norm of the Gram (rotation invariant)
+    // staged: thread -> blocks tid, tid + kThreads, ...; direct (RG == 1 and
+    // too many blocks to stage): thread -> its own tasks (task == block).
 #pragma unroll
-    for (int e = 0; e < MAXE; ++e) {
-        if (ea[e] < 0) continue;
-        const int a = ea[e], b = eb[e];
-        double sre = acc_re[e][0], sim = acc_im[e][0];
-#pragma unroll
-        for (int u = 1; u < ILP; ++u) {  // fixed-order combine of the chains
-            sre += acc_re[e][u];
-            sim += acc_im[e][u];
-        }
-        acc_re[e][0] = sre;
-        acc_im[e][0] = sim;
-        if (b >= m) {
-            D[2 * (a * K + b - m)] = sre;
-            D[2 * (a * K + b - m) + 1] = sim;
+    for (int e = 0; e < MB; ++e) {
+    if (staged && e > 0) break;
+    for (int id = staged ? tid : (tg[e] >= 0 ? tid + e * kThreads : nblk); id < nblk;
+         id += staged ? kThreads : nblk) {
+        int A_, B_;
+        if (id < ngb) {
+            int rem = id;
+            A_ = 0;
+            while (rem >= nb - A_) { rem -= nb - A_; ++A_; }
+            B_ = A_ + rem;
         } else {
-            A[2 * (a * m + b)] = sre;
-            A[2 * (a * m + b) + 1] = sim;
-            A[2 * (b * m + a)] = sre;       // Hermitian mirror
-            A[2 * (b * m + a) + 1] = -sim;
-            if (a == b) A[2 * (a * m + a) + 1] = 0.0;
-            const double sq = sre * sre + (a == b ? 0.0 : sim * sim);
-            fro += a == b ? sq : 2.0 * sq;
+            A_ = (id - ngb) / nk;
+            B_ = nb + (id - ngb) % nk;
         }
+        const bool rhs = B_ >= nb;
+        for (int q = 0; q < 4; ++q) {
+            double sre = staged ? part[(id * 4 + q) * 2] : acc[e][q][0];
+            double sim = staged ? part[(id * 4 + q) * 2 + 1] : acc[e][q][1];
+            for (int g = 1; g < RG; ++g) {
+                sre += part[((g * nblk + id) * 4 + q) * 2];
+                sim += part[((g * nblk + id) * 4 + q) * 2 + 1];
+            }
+            const int a = 2 * A_ + (q >> 1);
+            const int cidx = (rhs ? 2 * (B_ - nb) : 2 * B_) + (q & 1);
+            if (a >= m) continue;
+            if (rhs) {
+                if (cidx < K) {
+                    D[2 * (a * K + cidx)] = sre;
+                    D[2 * (a * K + cidx) + 1] = sim;
+                }
+            } else if (cidx < m && cidx >= a) {
+                A[2 * (a * m + cidx)] = sre;
+                A[2 * (a * m + cidx) + 1] = cidx == a ? 0.0 : sim;
+                A[2 * (cidx * m + a)] = sre;  // Hermitian mirror
+                A[2 * (cidx * m + a) + 1] = cidx == a ? 0.0 : -sim;
+                const double sq = sre * sre + (cidx == a ? 0.0 : sim * sim);
+                fro += cidx == a ? sq : 2.0 * sq;
+            }
+        }
+    }
     }
     for (int i = tid; i < m * m; i += kThreads) {
         V[2 * i] = (i / m == i % m) ? 1.0 : 0.0;
@@ -203,7 +258,7 @@ __global__ void __launch_bounds__(kThreads) lls_kernel(LlsParams p) {
     // that is the rotation threshold (a relative test against sqrt(a_pp a_qq)
     // never settles for the small noise eigenvalues of a near-far design).
     const double tol_rot = DBL_EPSILON * sqrt(red[0]);
-    if (tid == 0) any_rot[0] = any_rot[1] = 0;
+    if (tid == 0) any_rot[0] = any_rot[1] = round_rot[0] = round_rot[1] = 0;
     __syncthreads();
     NOMA_LLS_CLK(1)
 
@@ -237,6 +292,7 @@ __global__ void __launch_bounds__(kThreads) lls_kernel(LlsParams p) {
                         c = rsqrt(fma(t, t, 1.0));
                         s = t * c;
                         any_rot[sweep & 1] = 1;
+                        round_rot[r & 1] = 1;
                     }
                 }
                 pair_p[i] = pp;
@@ -249,6 +305,9 @@ __global__ void __launch_bounds__(kThreads) lls_kernel(LlsParams p) {
             __syncthreads();
             // every thread has passed the previous sweep's break test
             if (r == 0 && tid == 0) any_rot[(sweep + 1) & 1] = 0;
+            if (!round_rot[r & 1]) continue;  // no pair rotates: identity round
+            __syncthreads();
+            if (tid == 0) round_rot[r & 1] = 0;  // reset for round r + 2
             // A block (row pair I, column pair J): rows get U^H, columns U
             for (int it = tid; it < npairs * npairs + npairs * m; it += kThreads) {
                 if (it < npairs * npairs) {
@@ -256,6 +315,7 @@ __global__ void __launch_bounds__(kThreads) lls_kernel(LlsParams p) {
                     const int r0 = pair_p[I], r1 = pair_q[I], c0 = pair_p[J], c1 = pair_q[J];
                     const double ci = rot[4 * I], si = rot[4 * I + 1], eri = rot[4 * I + 2], eii = rot[4 * I + 3];
                     const double cj = rot[4 * J], sj = rot[4 * J + 1], erj = rot[4 * J + 2], eij = -rot[4 * J + 3];
+                    if (si == 0.0 && sj == 0.0) continue;  // both rotations identity
                     const bool h1 = r1 < m, k1 = c1 < m;
                     double x[2][2][2];  // [row][col][re/im]
                     x[0][0][0] = A[2 * (r0 * m + c0)];
@@ -305,6 +365,7 @@ __global__ void __launch_bounds__(kThreads) lls_kernel(LlsParams p) {
                     const int pp = pair_p[i], qq = pair_q[i];
                     if (qq >= m) continue;
                     const double c = rot[4 * i], s = rot[4 * i + 1];
+                    if (s == 0.0) continue;
                     const double er = rot[4 * i + 2], ei = -rot[4 * i + 3];  // e^{-i phi}
                     const double xr = V[2 * (row * m + pp)], xi = V[2 * (row * m + pp) + 1];
                     const double yr = V[2 * (row * m + qq)], yi = V[2 * (row * m + qq) + 1];
@@ -378,87 +439,101 @@ __global__ void __launch_bounds__(kThreads) lls_kernel(LlsParams p) {
         }
     }
     __syncthreads();
-
     NOMA_LLS_CLK(3)
-    // ---- phase D: residuals r0 = y - X w0 (FP64) and norms, one pass over
-    // the staged rows; thread = (user k, row group), fixed-order reductions.
-    const int ngrp = kThreads / K;  // K <= kThreads
-    const int rk = tid % K, rg = tid / K;
-    const bool rthread = rg < ngrp;
-    double rr = 0.0, yy = 0.0;
-    issue(0, 0);
-    for (int ch = 0; ch < nch; ++ch) {
-        if (ch + 1 < nch) {
-            issue(ch + 1, (ch + 1) & 1);
-            cp_async_wait<1>();
-        } else {
-            cp_async_wait<0>();
-        }
-        __syncthreads();
-        const int t0 = ch * CH, tn = min(CH, p.nrow_c - t0);
-        const double *xs = bufs + (ch & 1) * bstride, *ys = xs + 2 * CH * m;
-        if (rthread) {
-            for (int t = rg; t < tn; t += ngrp) {
-                const double yr = ys[2 * (t * K + rk)], yi = ys[2 * (t * K + rk) + 1];
-                double pe0 = 0.0, po0 = 0.0, pe1 = 0.0, po1 = 0.0;
-                for (int a = 0; a < m; a += 2) {  // m even (widened) or odd tail below
-                    const double xr = xs[2 * (t * m + a)], xi = xs[2 * (t * m + a) + 1];
-                    const double w0a = D[2 * (a * K + rk)], w1a = -D[2 * (a * K + rk) + 1];
-                    pe0 += xr * w0a + xi * w1a;  // row 2t = [Re x; Im x]
-                    po0 += xi * w0a - xr * w1a;  // row 2t+1 = [Im x; -Re x]
-                    if (a + 1 < m) {
-                        const double yr1 = xs[2 * (t * m + a + 1)], yi1 = xs[2 * (t * m + a + 1) + 1];
-                        const double v0 = D[2 * ((a + 1) * K + rk)], v1 = -D[2 * ((a + 1) * K + rk) + 1];
-                        pe1 += yr1 * v0 + yi1 * v1;
-                        po1 += yi1 * v0 - yr1 * v1;
-                    }
-                }
-                const double pe = pe0 + pe1, po = po0 + po1;
-                const size_t net = (size_t)d * K + rk;
+
+    // ---- phase D: residuals r0 = y - X w0 (FP64) and norms: thread per row
+    // (rows read once from global / L2), users in groups of 8; per-user sums
+    // in fixed order (warp tree, then warps in order).
+    double *sums = red;  // [8 warps][8 users][2]
+    for (int k0 = 0; k0 < K; k0 += 8) {
+        const int kn = min(8, K - k0);
+        double rr[8], yy[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) rr[k] = yy[k] = 0.0;
+        for (int t = tid; t < p.nrow_c; t += kThreads) {
+            double pe[8], po[8];
+#pragma unroll
+            for (int k = 0; k < 8; ++k) pe[k] = po[k] = 0.0;
+            for (int a = 0; a < m; ++a) {
+                double xr, xi;
                 if (cplx_layout) {
-                    const double r_e = yr - pe, r_o = yi - po;
-                    rr += r_e * r_e + r_o * r_o;
-                    yy += yr * yr + yi * yi;
-                    if (p.r0) {
-                        p.r0[net * p.rows + 2 * (t0 + t)] = (float)r_e;
-                        p.r0[net * p.rows + 2 * (t0 + t) + 1] = (float)r_o;
-                    }
+                    const double2 x = *reinterpret_cast<const double2 *>(p.design + (((size_t)d * p.nrow_c + t) * m + a) * 2);
+                    xr = x.x;
+                    xi = x.y;
                 } else {
-                    const double r_e = yr - pe;
-                    rr += r_e * r_e;
-                    yy += yr * yr;
-                    if (p.r0) p.r0[net * p.rows + t0 + t] = (float)r_e;
+                    xr = p.design[((size_t)d * p.nrow_c + t) * m + a];
+                    xi = 0.0;
+                }
+#pragma unroll
+                for (int k = 0; k < 8; ++k) {
+                    if (k < kn) {
+                        const double w0a = D[2 * (a * K + k0 + k)], w1a = -D[2 * (a * K + k0 + k) + 1];
+                        pe[k] += xr * w0a + xi * w1a;  // row 2t = [Re x; Im x]
+                        po[k] += xi * w0a - xr * w1a;  // row 2t+1 = [Im x; -Re x]
+                    }
                 }
             }
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                if (k >= kn) continue;
+                const size_t net = (size_t)d * K + k0 + k;
+                if (cplx_layout) {
+                    const double2 y = *reinterpret_cast<const double2 *>(p.targets + (((size_t)d * p.nrow_c + t) * K + k0 + k) * 2);
+                    const double r_e = y.x - pe[k], r_o = y.y - po[k];
+                    rr[k] += r_e * r_e + r_o * r_o;
+                    yy[k] += y.x * y.x + y.y * y.y;
+                    if (p.r0) {
+                        p.r0[net * p.rows + 2 * t] = (float)r_e;
+                        p.r0[net * p.rows + 2 * t + 1] = (float)r_o;
+                    }
+                } else {
+                    const double y = p.targets[((size_t)d * K + k0 + k) * p.rows + t];
+                    const double r_e = y - pe[k];
+                    rr[k] += r_e * r_e;
+                    yy[k] += y * y;
+                    if (p.r0) p.r0[net * p.rows + t] = (float)r_e;
+                }
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                rr[k] += __shfl_xor_sync(0xffffffffu, rr[k], o);
+                yy[k] += __shfl_xor_sync(0xffffffffu, yy[k], o);
+            }
+        if (lane == 0)
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                sums[(warp * 8 + k) * 2] = rr[k];
+                sums[(warp * 8 + k) * 2 + 1] = yy[k];
+            }
+        __syncthreads();
+        if (tid < kn) {
+            double sr = 0.0, sy = 0.0;
+            for (int w = 0; w < kThreads / 32; ++w) {
+                sr += sums[(w * 8 + tid) * 2];
+                sy += sums[(w * 8 + tid) * 2 + 1];
+            }
+            const double res = sqrt(sr), ynorm = sqrt(sy);
+            const size_t net = (size_t)d * K + k0 + tid;
+            int st = NOMA_OK;
+            double cond;
+            if (rank == m) {
+                cond = lmax / lmin;
+            } else if (rank > 0 && res <= 1e-8 * sqrt(lmax) * fmax(1.0, ynorm)) {
+                cond = lmax / lkeep;
+            } else {
+                st = NOMA_ERR_ILL_CONDITIONED;
+                cond = lmin > 0.0 ? lmax / lmin : INFINITY;
+            }
+            if (p.cond) p.cond[net] = cond;
+            if (p.status) p.status[net] = st;
         }
         __syncthreads();
     }
     NOMA_LLS_CLK(4)
 #undef NOMA_LLS_CLK
-    red[tid] = rr;
-    red[kThreads + tid] = yy;
-    __syncthreads();
-    if (tid < K) {
-        double sr = 0.0, sy = 0.0;
-        for (int g = 0; g < ngrp; ++g) {
-            sr += red[g * K + tid];
-            sy += red[kThreads + g * K + tid];
-        }
-        const double res = sqrt(sr), ynorm = sqrt(sy);
-        const size_t net = (size_t)d * K + tid;
-        int st = NOMA_OK;
-        double cond;
-        if (rank == m) {
-            cond = lmax / lmin;
-        } else if (rank > 0 && res <= 1e-8 * sqrt(lmax) * fmax(1.0, ynorm)) {
-            cond = lmax / lkeep;
-        } else {
-            st = NOMA_ERR_ILL_CONDITIONED;
-            cond = lmin > 0.0 ? lmax / lmin : INFINITY;
-        }
-        if (p.cond) p.cond[net] = cond;
-        if (p.status) p.status[net] = st;
-    }
 }
 
 // lls::predict (lls.cpp:62-66): yhat = narrow(X_widened w0), FP64, one thread
@@ -514,13 +589,23 @@ int lls_launch(const LlsParams &p, cudaStream_t st) {
     if (2 * p.m * p.K > 2 * (2 * lls_chunk(p.m) * p.m + 2 * lls_chunk(p.m) * p.K)) return NOMA_ERR_UNSUPPORTED;
     const size_t smem = lls_smem_bytes(p.m, p.K);
     if (smem > 227 * 1024) return NOMA_ERR_UNSUPPORTED;
-    if (nent <= kThreads) {
-        cudaFuncSetAttribute(lls_kernel<1, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        lls_kernel<1, 4><<<p.n_designs, kThreads, smem, st>>>(p);
-    } else {
-        cudaFuncSetAttribute(lls_kernel<kLlsMaxE, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        lls_kernel<kLlsMaxE, 1><<<p.n_designs, kThreads, smem, st>>>(p);
-    }
+    const int nb = (p.m + 1) / 2, nk = (p.K + 1) / 2;
+    const int nblk = nb * (nb + 1) / 2 + nb * nk;
+    const int ntask = lls_row_groups(p.m) * nblk;
+    const int mb = (ntask + kThreads - 1) / kThreads;
+    if (mb > 8) return NOMA_ERR_UNSUPPORTED;
+    // task partials [task][4][2] reuse the staging buffers when RG > 1
+    if (lls_row_groups(p.m) > 1 &&
+        (size_t)ntask * 8 > (size_t)2 * (2 * lls_chunk(p.m) * p.m + 2 * lls_chunk(p.m) * p.K))
+        return NOMA_ERR_UNSUPPORTED;
+    auto go = [&](auto kern) {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        kern<<<p.n_designs, kThreads, smem, st>>>(p);
+    };
+    if (mb == 1) go(lls_kernel<1>);
+    else if (mb == 2) go(lls_kernel<2>);
+    else if (mb <= 4) go(lls_kernel<4>);
+    else go(lls_kernel<8>);
     return cudaGetLastError() == cudaSuccess ? NOMA_OK : NOMA_ERR_CUDA;
 }
 
