@@ -352,7 +352,7 @@ __global__ void __launch_bounds__(NW * 32, 1) train_lat_kernel(TrainParams p, La
     (void)d;
     (void)M;
     __syncthreads();
-    if (tid == 0 && total > 0) fetch(0);
+    if (tid == kLT - 32 && total > 0) fetch(0);  // same issuer as every later fetch
     cl_sync();  // every CTA's barriers initialised before any st.async lands
 
     // Adam moments of the parameters this thread updates (registers; fixed

@@ -1,0 +1,35 @@
+"""Small invocations of every device kernel for compute-sanitizer runs:
+LLS, init, shuffles, synthesis, the throughput and latency training kernels,
+FFMA and tcgen05 detection (one slot, short training)."""
+import os
+import sys
+
+import numpy as np
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2206_05998_b200 import api  # noqa: E402
+from paper_2206_05998_b200.seeds import slot_user_seeds  # noqa: E402
+
+mode = sys.argv[1] if len(sys.argv) > 1 else "all"
+sy = api.synthesize(3, 16, 100, 256, [5], snr_db=15.0, rx_nonlinearity_gain=0.05)
+init, shuf = slot_user_seeds(np.array([5], np.uint64), 3)
+for hidden in ([64], [64, 64]):
+    if mode in ("all", "lat"):  # latency cluster kernel (default for few nets)
+        out = api.pipeline([32] + hidden, sy.pilot_rx, sy.pilot_sym, sy.data_rx, sy.data_codes,
+                           init, shuf, epochs=2)
+        print("lat", hidden, api.context().train_mode, api.context().detect_mode, out.bit_errors.ravel())
+    if mode in ("all", "tc"):  # throughput kernel + tcgen05 detect
+        os.environ["NOMA_LAT_CLUSTER"] = "1"
+        out = api.pipeline([32] + hidden, sy.pilot_rx, sy.pilot_sym, sy.data_rx, sy.data_codes,
+                           init, shuf, epochs=2)
+        print("tc", hidden, api.context().train_mode, api.context().detect_mode, out.bit_errors.ravel())
+        os.environ.pop("NOMA_LAT_CLUSTER")
+    if mode in ("all", "thr"):  # throughput kernel + FFMA detect
+        os.environ["NOMA_LAT_CLUSTER"] = "1"
+        os.environ["NOMA_DETECT_TC"] = "0"
+        out = api.pipeline([32] + hidden, sy.pilot_rx, sy.pilot_sym, sy.data_rx, sy.data_codes,
+                           init, shuf, epochs=2)
+        print("thr", hidden, api.context().train_mode, api.context().detect_mode, out.bit_errors.ravel())
+        os.environ.pop("NOMA_LAT_CLUSTER")
+        os.environ.pop("NOMA_DETECT_TC")
+print("done")
