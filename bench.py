@@ -288,6 +288,21 @@ def detect_only(args, cfg):
         if i:
             e2e.append(a.elapsed_time(b))
     e2e_value = sym / (shard.max_over_ranks(statistics.mean(e2e), dev) * 1e-3)
+    if mode == 2:
+        roofline = {"bound": "tensor", "kernel": "detect_tc_kernel", "achieved": achieved,
+                    "peak": tf32_peak, "unit": "TFLOP/s", "frac": achieved / tf32_peak,
+                    "peak_source": "TF32 dense = measured BF16 (MEASURED_PEAKS.json) / 2",
+                    "tensor_work_factor": 3,
+                    "frac_of_3xtf32_ceiling": 3 * achieved / tf32_peak,
+                    "hbm_bound_ms": bytes_step / (hbm * 1e9) * 1e3,
+                    "algorithmic_flop_per_launch": flop_step, "traffic": None}
+    else:
+        fp32_peak = ctx.measure_fp32_tflops(0)
+        roofline = {"bound": "fp32", "kernel": "detect_kernel", "achieved": achieved,
+                    "peak": fp32_peak, "unit": "TFLOP/s", "frac": achieved / fp32_peak,
+                    "peak_source": "measured in this run: constant-operand FFMA probe (issue-rate peak)",
+                    "hbm_bound_ms": bytes_step / (hbm * 1e9) * 1e3,
+                    "algorithmic_flop_per_launch": flop_step, "traffic": None}
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         dt, rows = cpu_detect_sample(cfg)
@@ -298,20 +313,15 @@ def detect_only(args, cfg):
         print(json.dumps({
             "metric": "detected symbols/sec (data-phase detection)", "value": value, "unit": "symbols/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32 (3xTF32 tensor cores)",
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f32 (3xTF32 tensor cores)" if mode == 2 else "f32",
             "data": "synthetic (device channel simulator; weights trained on the slot's pilots, untimed)",
             "config": {"workload": f"c3: M={M} K={K} dims={dims} N_D={nd} per slot, {S} slot(s) per GPU, "
                                    f"frozen trained weights", "l2": "flushed (256 MiB write) between steps; "
                                    f"inputs {bytes_step / 2**20:.0f} MiB per step > L2",
                        "parallelism": f"slot-sharded x{world}, no collective"},
             "detect_kernel": {1: "FFMA register tiles", 2: "tcgen05 3xTF32"}.get(mode, str(mode)),
-            "roofline": {"bound": "tensor", "kernel": "detect_tc_kernel", "achieved": achieved,
-                         "peak": tf32_peak, "unit": "TFLOP/s", "frac": achieved / tf32_peak,
-                         "peak_source": "TF32 dense = measured BF16 (MEASURED_PEAKS.json) / 2",
-                         "tensor_work_factor": 3,
-                         "frac_of_3xtf32_ceiling": 3 * achieved / tf32_peak,
-                         "hbm_bound_ms": bytes_step / (hbm * 1e9) * 1e3,
-                         "algorithmic_flop_per_launch": flop_step, "traffic": None},
+            "roofline": roofline,
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_value, "unit": "symbols/s", "h2d_bytes_per_step": h_dx.numel() * 4 + h_truth.numel()
                     + h_plans.nbytes, "d2h_bytes_per_step": h_codes.nbytes + h_errs.nbytes,

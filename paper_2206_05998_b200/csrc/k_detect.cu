@@ -160,11 +160,20 @@ int detect_launch(DetectParams &p, cudaStream_t st) {
     const int rows_per_tile = p.layout == NOMA_LAYOUT_WIDEN_COMPLEX ? kBatchRows / 2 : kBatchRows;
     p.tiles = (p.rows + rows_per_tile - 1) / rows_per_tile;
     if (p.tiles == 0 || p.n_nets == 0) return NOMA_OK;
-    // ~2 resident CTAs per SM over the whole grid
-    int ctas = (2 * 148 + p.n_nets - 1) / p.n_nets;
+    // one wave of resident CTAs split evenly over the nets (rounded down: a
+    // partial second wave would double the time of a few-net launch)
+    cudaFuncSetAttribute(detect_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    int sms = 148, dev = 0, per_sm = 1;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, detect_kernel, kThreads, smem) != cudaSuccess ||
+        per_sm < 1) {
+        cudaGetLastError();
+        per_sm = 1;
+    }
+    int ctas = sms * per_sm / p.n_nets;
     ctas = ctas < 1 ? 1 : ctas;
     ctas = ctas > p.tiles ? p.tiles : ctas;
-    cudaFuncSetAttribute(detect_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     detect_kernel<<<dim3(ctas, p.n_nets), kThreads, smem, st>>>(p);
     return cudaGetLastError() == cudaSuccess ? NOMA_OK : NOMA_ERR_CUDA;
 }

@@ -19,12 +19,15 @@
 //   * one thread issues tcgen05.mma kind::tf32 (M=128): layer 1 with
 //     N = H + 16, the extra B row being the linear-branch weight w0, so the
 //     TMEM accumulator column H holds x . w0; layer 2 (if any) with N = H;
-//   * each thread reads its row's accumulators (tcgen05.ld 32x32b), adds the
-//     bias, applies ReLU, and either stages the next layer's A operand or
-//     forms yhat = x.w0 + a_N . w_final; lane pairs (2s, 2s+1) give Re/Im of
-//     symbol s, whose sign bits are the QPSK decision (ties -> 0); errors
-//     against the truth codes are warp-reduced into one atomic per warp.
-// The next tile's samples are prefetched into registers during the MMAs.
+//   * each thread reads its row's accumulators (tcgen05.ld 32x32b, all in
+//     flight, one wait), adds the bias, applies ReLU, and either writes the
+//     layer-2 A operand (hi/lo) into TMEM with tcgen05.st -- the layer-2
+//     MMAs read A from TMEM -- or forms yhat = x.w0 + a_N . w_final; lane
+//     pairs (2s, 2s+1) give Re/Im of symbol s, whose sign bits are the QPSK
+//     decision (ties -> 0); errors against the truth codes are warp-reduced
+//     into one atomic per warp.
+// The next tile's samples are prefetched into registers a tile ahead and
+// staged into the (then free) smem A1 buffer while layer 2 runs.
 #include "kernels.cuh"
 
 namespace noma_dev {
@@ -70,16 +73,34 @@ __device__ __forceinline__ void tc_mbar_wait(uint32_t bar, uint32_t parity) {
         "r"(parity)
         : "memory");
 }
-__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
-    uint32_t r[16];
+// tcgen05.ld without the wait: several loads in flight, one tmem_wait_ld()
+__device__ __forceinline__ void tmem_ld16_nw(uint32_t taddr, uint32_t (&r)[16]) {
     asm volatile(
         "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
         : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
           "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
         : "r"(taddr));
-    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-#pragma unroll
-    for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+// 16 columns of this thread's TMEM lane (the layer-2 A operand row)
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const float (&v)[16]) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(
+            taddr),
+        "r"(__float_as_uint(v[0])), "r"(__float_as_uint(v[1])), "r"(__float_as_uint(v[2])),
+        "r"(__float_as_uint(v[3])), "r"(__float_as_uint(v[4])), "r"(__float_as_uint(v[5])),
+        "r"(__float_as_uint(v[6])), "r"(__float_as_uint(v[7])), "r"(__float_as_uint(v[8])),
+        "r"(__float_as_uint(v[9])), "r"(__float_as_uint(v[10])), "r"(__float_as_uint(v[11])),
+        "r"(__float_as_uint(v[12])), "r"(__float_as_uint(v[13])), "r"(__float_as_uint(v[14])),
+        "r"(__float_as_uint(v[15])));
+}
+// A operand from TMEM (a_tmem: column address of the K-step), B from smem
+__device__ __forceinline__ void umma_tf32_ta(uint32_t tmem_d, uint32_t a_tmem, uint64_t bd, uint32_t idesc,
+                                             uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "r"(a_tmem), "l"(bd), "r"(idesc), "r"(accumulate));
 }
 __device__ __forceinline__ float tf32_hi(float x) { return __uint_as_float(__float_as_uint(x) & 0xFFFFE000u); }
 
@@ -112,12 +133,18 @@ struct DetectTcParams {
 };
 
 // W0 = input width 2M, H = hidden width, NL = hidden layers (1 or 2).
-// kTcGroups groups of 128 threads each run their own tile stream (own A
-// buffers, TMEM columns and mbarrier; group-local named barriers), so one
+// kTcGroups groups of 128 threads each run their own tile stream (own A1
+// buffer, TMEM columns and mbarrier; group-local named barriers), so one
 // group's MMAs overlap another group's epilogue; the weights are shared.
+// TMEM per group (256 columns): D1 = [x W1^T | x w0] in columns 0..N1, D2
+// reuses columns 0..H once D1 has been read; the layer-2 A operand a1 (hi,
+// lo) is written by the epilogue into columns 128.. and 192.. with
+// tcgen05.st and read from there by the layer-2 MMAs, so the group's smem A1
+// buffer is free as soon as layer 1 completes and the next tile is staged
+// into it while layer 2 runs.
 template <int W0, int H, int NL>
-constexpr uint32_t tc_abuf_bytes() {  // per group: A1 (hi, lo), aliased by A2 (hi, lo)
-    return (uint32_t)(2 * kTcRows * (NL > 1 && H > W0 ? H : W0) * 4);
+constexpr uint32_t tc_abuf_bytes() {  // per group: the layer-1 A operand (hi, lo)
+    return (uint32_t)(2 * kTcRows * W0 * 4);
 }
 template <int W0, int H, int NL>
 __global__ void __launch_bounds__(kTcThreads, 1) detect_tc_kernel(DetectTcParams p) {
@@ -125,8 +152,10 @@ __global__ void __launch_bounds__(kTcThreads, 1) detect_tc_kernel(DetectTcParams
     constexpr int N1 = H + 16;                 // layer-1 B rows: W1 | w0 | zeros
     constexpr int KB0 = W0 / 4, KBH = H / 4;   // k-blocks per row group
     constexpr uint32_t A1B = kTcRows * W0 * 4, B1B = N1 * W0 * 4;
-    constexpr uint32_t A2B = kTcRows * H * 4, B2B = H * H * 4;
+    constexpr uint32_t B2B = H * H * 4;
     constexpr uint32_t ABUF = tc_abuf_bytes<W0, H, NL>();
+    constexpr uint32_t kA2Hi = 128, kA2Lo = 192;  // TMEM columns of the layer-2 A operand
+    static_assert(N1 <= 128 && H <= 64, "TMEM column plan: D1 < 128, A2 hi/lo 64 columns each");
     extern __shared__ __align__(1024) char smem[];
     char *b1h = smem, *b1l = b1h + B1B;
     char *b2h = b1l + B1B, *b2l = b2h + (NL > 1 ? B2B : 0);
@@ -139,8 +168,6 @@ __global__ void __launch_bounds__(kTcThreads, 1) detect_tc_kernel(DetectTcParams
     const int net = blockIdx.y, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int grp = threadIdx.x >> 7, tid = threadIdx.x & 127;  // group, thread in group
     char *a1h = abase + grp * ABUF, *a1l = a1h + A1B;
-    char *a2h = a1h, *a2l = a1h + A2B;  // layer-2 operand reuses the group's A1 space
-    (void)A2B;
     auto gsync = [&]() { asm volatile("bar.sync %0, 128;" ::"r"(1 + grp) : "memory"); };
     if (p.status && p.status[net] != NOMA_OK) {
         if (blockIdx.x == 0 && tid == 0 && p.errors) p.errors[net] = 0xFFFFFFFFu;
@@ -189,7 +216,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) detect_tc_kernel(DetectTcParams
     const bool odd = tid & 1;
     const float2 *src = reinterpret_cast<const float2 *>(p.data) + (size_t)d * p.rows * M;
     float2 xs[M];
-    uint8_t truth_next = 0;  // the tile's truth code, loaded with its samples
+    uint8_t truth_next = 0;  // truth code of the tile whose samples are in xs
     auto load_tile = [&](int tile) {
         const int s = tile * 64 + sym;
         const bool ok = tile < p.tiles && s < p.rows;
@@ -202,13 +229,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) detect_tc_kernel(DetectTcParams
             xs[m + 1] = make_float2(v.z, v.w);
         }
     };
-    uint32_t my_err = 0;
-    const int tstride = gridDim.x * kTcGroups;
-    int tile = blockIdx.x * kTcGroups + grp;
-    load_tile(tile);
-    for (; tile < p.tiles; tile += tstride) {
-        const uint8_t truth_cur = truth_next;
-        // widened row -> A operand (hi/lo)
+    // widened row (iq_transform.cpp:17-20) -> layer-1 A operand (hi/lo) in smem
+    auto stage_a1 = [&]() {
 #pragma unroll
         for (int m = 0; m < M; m += 4) {
             float4 re = make_float4(xs[m].x, xs[m + 1].x, xs[m + 2].x, xs[m + 3].x);
@@ -221,7 +243,28 @@ __global__ void __launch_bounds__(kTcThreads, 1) detect_tc_kernel(DetectTcParams
                 put4(a1h, a1l, tid, M + m, KB0, make_float4(-re.x, -re.y, -re.z, -re.w));
             }
         }
-        load_tile(tile + tstride);  // next tile's samples, in flight during the MMAs
+    };
+    // sum_c relu(v_c + b_c) w_c over 16 columns into 4 partial sums
+    auto dot16 = [&](const uint32_t (&v)[16], const float *b, const float *w, float (&acc)[4]) {
+#pragma unroll
+        for (int q = 0; q < 16; q += 4) {
+            const float4 b4 = *reinterpret_cast<const float4 *>(b + q);
+            const float4 w4 = *reinterpret_cast<const float4 *>(w + q);
+            acc[0] = fmaf(fmaxf(__uint_as_float(v[q]) + b4.x, 0.f), w4.x, acc[0]);
+            acc[1] = fmaf(fmaxf(__uint_as_float(v[q + 1]) + b4.y, 0.f), w4.y, acc[1]);
+            acc[2] = fmaf(fmaxf(__uint_as_float(v[q + 2]) + b4.z, 0.f), w4.z, acc[2]);
+            acc[3] = fmaf(fmaxf(__uint_as_float(v[q + 3]) + b4.w, 0.f), w4.w, acc[3]);
+        }
+    };
+    uint32_t my_err = 0;
+    const int tstride = gridDim.x * kTcGroups;
+    int tile = blockIdx.x * kTcGroups + grp;
+    load_tile(tile);
+    stage_a1();
+    uint8_t truth_a1 = truth_next;  // truth of the tile staged in A1
+    load_tile(tile + tstride);
+    for (; tile < p.tiles; tile += tstride) {
+        const uint8_t truth_cur = truth_a1;
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         asm volatile("tcgen05.fence::before_thread_sync;");
         gsync();
@@ -244,65 +287,72 @@ __global__ void __launch_bounds__(kTcThreads, 1) detect_tc_kernel(DetectTcParams
         tc_mbar_wait(bar, phase);
         phase ^= 1;
         asm volatile("tcgen05.fence::after_thread_sync;");
-        float lin, yh = 0.0f;
-        {
-            float v[16];
-            tmem_ld16(trow + H, v);  // column H: x . w0
-            lin = v[0];
-        }
+        // D1 -> registers: all H + 16 columns in flight, one wait
+        uint32_t v1[H / 16 + 1][16];
+#pragma unroll
+        for (int c = 0; c <= H / 16; ++c) tmem_ld16_nw(trow + 16 * c, v1[c]);
+        tmem_wait_ld();
+        const float lin = __uint_as_float(v1[H / 16][0]);  // column H: x . w0
+        float acc[4] = {0.f, 0.f, 0.f, 0.f};
         if constexpr (NL == 1) {
+            // layer 1 done: A1 is free for the next tile
+            stage_a1();
+            truth_a1 = truth_next;
+            load_tile(tile + 2 * tstride);
 #pragma unroll
-            for (int c0 = 0; c0 < H; c0 += 16) {
-                float v[16];
-                tmem_ld16(trow + c0, v);
-#pragma unroll
-                for (int i = 0; i < 16; ++i) yh = fmaf(fmaxf(v[i] + bias[c0 + i], 0.f), wf[c0 + i], yh);
-            }
+            for (int c = 0; c < H / 16; ++c) dot16(v1[c], bias + 16 * c, wf + 16 * c, acc);
         } else {
-            // a1 = relu(D1 + b1) -> layer-2 A operand (hi/lo)
+            // a1 = relu(D1 + b1) -> layer-2 A operand (hi/lo) in TMEM
 #pragma unroll
-            for (int c0 = 0; c0 < H; c0 += 16) {
-                float v[16];
-                tmem_ld16(trow + c0, v);
+            for (int c = 0; c < H / 16; ++c) {
+                float hi[16], lo[16];
 #pragma unroll
-                for (int q = 0; q < 16; q += 4)
-                    put4(a2h, a2l, tid, c0 + q,
-                         KBH, make_float4(fmaxf(v[q] + bias[c0 + q], 0.f), fmaxf(v[q + 1] + bias[c0 + q + 1], 0.f),
-                                          fmaxf(v[q + 2] + bias[c0 + q + 2], 0.f),
-                                          fmaxf(v[q + 3] + bias[c0 + q + 3], 0.f)));
+                for (int q = 0; q < 16; q += 4) {
+                    const float4 b4 = *reinterpret_cast<const float4 *>(bias + 16 * c + q);
+                    const float bq[4] = {b4.x, b4.y, b4.z, b4.w};
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        const float a = fmaxf(__uint_as_float(v1[c][q + e]) + bq[e], 0.f);
+                        hi[q + e] = tf32_hi(a);
+                        lo[q + e] = a - hi[q + e];
+                    }
+                }
+                tmem_st16(trow + kA2Hi + 16 * c, hi);
+                tmem_st16(trow + kA2Lo + 16 * c, lo);
             }
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
             asm volatile("tcgen05.fence::before_thread_sync;");
             gsync();
             asm volatile("tcgen05.fence::after_thread_sync;");
-            if (tid == 0) {  // layer 2: D2[128 x H] in TMEM columns 128..
+            if (tid == 0) {  // layer 2: D2[128 x H] in TMEM columns 0..H, A from TMEM
                 constexpr uint32_t id2 = umma_idesc_tf32(H);
 #pragma unroll
                 for (int kk = 0; kk < H / 8; ++kk) {
                     const uint32_t ko = kk * 256;
-                    const uint64_t ah = umma_desc(tc_s2u(a2h) + ko, 128, KBH * 128);
-                    const uint64_t al = umma_desc(tc_s2u(a2l) + ko, 128, KBH * 128);
                     const uint64_t bh = umma_desc(tc_s2u(b2h) + ko, 128, KBH * 128);
                     const uint64_t bl = umma_desc(tc_s2u(b2l) + ko, 128, KBH * 128);
-                    umma_tf32(tmem + 128, ah, bh, id2, kk > 0);
-                    umma_tf32(tmem + 128, ah, bl, id2, 1);
-                    umma_tf32(tmem + 128, al, bh, id2, 1);
+                    umma_tf32_ta(tmem, tmem + kA2Hi + 8 * kk, bh, id2, kk > 0);
+                    umma_tf32_ta(tmem, tmem + kA2Hi + 8 * kk, bl, id2, 1);
+                    umma_tf32_ta(tmem, tmem + kA2Lo + 8 * kk, bh, id2, 1);
                 }
                 umma_commit(bar);
             }
+            // next tile's A1 while layer 2 runs (layer 1 has completed)
+            stage_a1();
+            truth_a1 = truth_next;
+            load_tile(tile + 2 * tstride);
             tc_mbar_wait(bar, phase);
             phase ^= 1;
             asm volatile("tcgen05.fence::after_thread_sync;");
+            uint32_t v2[H / 16][16];
 #pragma unroll
-            for (int c0 = 0; c0 < H; c0 += 16) {
-                float v[16];
-                tmem_ld16(trow + 128 + c0, v);
+            for (int c = 0; c < H / 16; ++c) tmem_ld16_nw(trow + 16 * c, v2[c]);
+            tmem_wait_ld();
 #pragma unroll
-                for (int i = 0; i < 16; ++i) yh = fmaf(fmaxf(v[i] + bias[H + c0 + i], 0.f), wf[c0 + i], yh);
-            }
+            for (int c = 0; c < H / 16; ++c) dot16(v2[c], bias + H + 16 * c, wf + 16 * c, acc);
         }
         // yhat = x.w0 + a_N . w (hybrid_nn.cpp:81); Re/Im of symbol `sym`
-        const float y = lin + yh;
+        const float y = lin + ((acc[0] + acc[1]) + (acc[2] + acc[3]));
         const float yo = __shfl_xor_sync(0xffffffffu, y, 1);
         const int s = tile * 64 + sym;
         if (!odd && s < p.rows) {
@@ -311,7 +361,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) detect_tc_kernel(DetectTcParams
             if (p.soft) *reinterpret_cast<float2 *>(p.soft + ((size_t)net * p.rows + s) * 2) = make_float2(y, yo);
             if (p.truth) my_err += __popc((unsigned)(truth_cur ^ code) & 3u);
         }
-        // the next tile's A stores must not overtake this tile's TMEM reads
+        // this tile's TMEM reads before the next tile's layer-1 MMA overwrites D
         asm volatile("tcgen05.fence::before_thread_sync;");
     }
     if (p.errors && p.truth) {
@@ -359,7 +409,9 @@ int detect_tc_launch(const DetectParams &dp, cudaStream_t st) {
     int sms = 148, dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    int ctas = (sms + p.n_nets - 1) / p.n_nets;  // one wave: a CTA per SM
+    // one wave, one CTA per SM (the smem footprint allows one): rounding up
+    // would leave a second wave of CTAs that doubles the kernel time
+    int ctas = sms / p.n_nets;
     ctas = ctas < 1 ? 1 : ctas > p.tiles ? p.tiles : ctas;
     auto launch = [&](auto kern, size_t smem) -> int {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

@@ -1,0 +1,5 @@
+mkdir -p gpurun_out
+timeout 300 python -m pytest tests/test_gpu_detect_tc.py -x -q 2>&1 | tail -3
+timeout 600 python bench.py --config c3 --steps 5 --warmup 3 --no-cpu-baseline 2>&1 | tail -1 > gpurun_out/bench_c3_tc4.json
+python -c "
+import json;d=json.load(open('gpurun_out/bench_c3_tc4.json'));print('%.3g'%d['value'], d['ms_per_step'], d['roofline'], d.get('bit_errors'))"
