@@ -289,11 +289,29 @@ def detect_only(args, cfg):
             e2e.append(a.elapsed_time(b))
     e2e_value = sym / (shard.max_over_ranks(statistics.mean(e2e), dev) * 1e-3)
     if mode == 2:
-        roofline = {"bound": "tensor", "kernel": "detect_tc_kernel", "achieved": achieved,
-                    "peak": tf32_peak, "unit": "TFLOP/s", "frac": achieved / tf32_peak,
-                    "peak_source": "TF32 dense = measured BF16 (MEASURED_PEAKS.json) / 2",
+        # tcgen05 kind::tf32 (M=128, N>=128) measured by tools/microbench/umma_rate.cu
+        # on this pool's B200 at 1965 MHz (profiles/r01_microbench_umma_rate.txt)
+        tf32_mma = 1190.0
+        clk_ghz = 1.965
+        sms = torch.cuda.get_device_properties(dev).multi_processor_count
+        ctas_per_net = max(1, sms // (S * K))  # detect launcher: one wave, one CTA per SM
+        tiles_per_cta = -(-((nd + 63) // 64) // ctas_per_net)
+        # per 128-row tile: 3 x W0/8 layer-1 MMAs with A in smem, bound by the
+        # shared-memory operand read (~48 cycles each at N=64), + 3 x H/8 per
+        # further layer with A in TMEM at the M*N/256 = 32-cycle pipe floor
+        tile_cyc = 3 * (dims[0] // 8) * 48 + sum(3 * (dims[l - 1] // 8) * 32 for l in range(2, len(dims)))
+        attain_ms = tiles_per_cta * tile_cyc / (clk_ghz * 1e6) * max(1, -(-(S * K) // sms))
+        roofline = {"bound": "tensor", "kernel": "detect_ws_kernel", "achieved": achieved,
+                    "peak": tf32_mma / 3, "unit": "TFLOP/s", "frac": 3 * achieved / tf32_mma,
+                    "peak_source": "3xTF32 = 1/3 of the measured tcgen05 kind::tf32 MMA rate (1190 TF/s, "
+                                   "tools/microbench/umma_rate.cu); every product is 3 TF32 MMAs",
                     "tensor_work_factor": 3,
-                    "frac_of_3xtf32_ceiling": 3 * achieved / tf32_peak,
+                    "frac_vs_bf16_half": 3 * achieved / tf32_peak,
+                    "bf16_half_peak": tf32_peak,
+                    "attainable_ms": attain_ms,
+                    "frac_of_attainable": attain_ms / kern_ms,
+                    "attainable_note": "MMA floor per tile: layer 1 A-from-smem MMAs bound by smem "
+                                       "operand bandwidth (48 cyc), later layers A-from-TMEM at 32 cyc",
                     "hbm_bound_ms": bytes_step / (hbm * 1e9) * 1e3,
                     "algorithmic_flop_per_launch": flop_step, "traffic": None}
     else:

@@ -10,33 +10,27 @@
 // level and the hard decisions match the FFMA path (the north star's gate
 // for using tensor cores on the data phase).
 //
-// Per CTA (128 threads, one user network, a persistent loop over 128-row
-// tiles = 64 QPSK symbols of the user's slot):
-//   * thread t forms widened row t of the tile (row 2s = [Re x_s; Im x_s],
-//     2s+1 = [Im x_s; -Re x_s], iq_transform.cpp:17-20) straight from the
-//     complex samples, splits it hi/lo and stores it in the no-swizzle
-//     K-major core-matrix layout (8 rows x 16 B per core matrix);
-//   * one thread issues tcgen05.mma kind::tf32 (M=128): layer 1 with
-//     N = H + 16, the extra B row being the linear-branch weight w0, so the
-//     TMEM accumulator column H holds x . w0; layer 2 (if any) with N = H;
-//   * each thread reads its row's accumulators (tcgen05.ld 32x32b, all in
-//     flight, one wait), adds the bias, applies ReLU, and either writes the
-//     layer-2 A operand (hi/lo) into TMEM with tcgen05.st -- the layer-2
-//     MMAs read A from TMEM -- or forms yhat = x.w0 + a_N . w_final; lane
-//     pairs (2s, 2s+1) give Re/Im of symbol s, whose sign bits are the QPSK
-//     decision (ties -> 0); errors against the truth codes are warp-reduced
-//     into one atomic per warp.
-// The next tile's samples are prefetched into registers a tile ahead and
-// staged into the (then free) smem A1 buffer while layer 2 runs.
+// Per CTA: one user network, one CTA per SM, a persistent warp-specialised
+// pipeline over 128-row tiles (64 QPSK symbols); see detect_ws_kernel below.
+// Each tile's widened rows (row 2s = [Re x_s; Im x_s], 2s+1 = [Im x_s;
+// -Re x_s], iq_transform.cpp:17-20) are formed straight from the complex
+// samples and stored hi/lo in the no-swizzle K-major core-matrix layout
+// (8 rows x 16 B per core matrix); tcgen05.mma kind::tf32 (M=128) runs the
+// hidden layers with FP32 accumulators in TMEM; the epilogues add the bias,
+// apply ReLU, stage the next layer's A operand in TMEM (tcgen05.st) or form
+// yhat = x.w0 + a_N . w_final; lane pairs (2s, 2s+1) give Re/Im of symbol s,
+// whose sign bits are the QPSK decision (ties -> 0); errors against the truth
+// codes are warp-reduced into one atomic per warp.
+#include <cstdio>
+#include <cstdlib>
+
 #include "kernels.cuh"
 
 namespace noma_dev {
 
 namespace {
 
-constexpr int kTcGroups = 2;    // independent 128-thread tile streams per CTA
-constexpr int kTcThreads = 128 * kTcGroups;
-constexpr int kTcRows = 128;
+constexpr int kTcRows = 128;  // rows per tile = TMEM lanes = M of every MMA
 
 __device__ __forceinline__ uint32_t tc_s2u(const void *p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -66,10 +60,12 @@ __device__ __forceinline__ void umma_commit(uint32_t mbar) {
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(mbar)
                  : "memory");
 }
+// the suspend-time hint lets a waiting warp sleep until the phase completes
+// instead of re-polling (the pipeline roles spend much of their time here)
 __device__ __forceinline__ void tc_mbar_wait(uint32_t bar, uint32_t parity) {
     asm volatile(
         "{\n\t.reg .pred p;\nTCW_%=:\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t@!p bra TCW_%=;\n}" ::"r"(bar),
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, 1000000;\n\t@!p bra TCW_%=;\n}" ::"r"(bar),
         "r"(parity)
         : "memory");
 }
@@ -103,6 +99,38 @@ __device__ __forceinline__ void umma_tf32_ta(uint32_t tmem_d, uint32_t a_tmem, u
         "r"(a_tmem), "l"(bd), "r"(idesc), "r"(accumulate));
 }
 __device__ __forceinline__ float tf32_hi(float x) { return __uint_as_float(__float_as_uint(x) & 0xFFFFE000u); }
+// packed FP32x2 arithmetic (sm_100a FADD2 / FFMA2): per lane identical to the
+// scalar operation, half the instructions
+typedef unsigned long long p2_t;
+__device__ __forceinline__ p2_t pk2(float a, float b) {
+    p2_t r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+    return r;
+}
+__device__ __forceinline__ float2 up2(p2_t v) {
+    float2 r;
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(r.x), "=f"(r.y) : "l"(v));
+    return r;
+}
+__device__ __forceinline__ p2_t add2(p2_t a, p2_t b) {
+    p2_t d;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+    return d;
+}
+__device__ __forceinline__ p2_t sub2(p2_t a, p2_t b) {
+    p2_t d;
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+    return d;
+}
+__device__ __forceinline__ p2_t fma2(p2_t a, p2_t b, p2_t c) {
+    p2_t d;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+    return d;
+}
+__device__ __forceinline__ p2_t relu2(p2_t v) {
+    const float2 f = up2(v);
+    return pk2(fmaxf(f.x, 0.f), fmaxf(f.y, 0.f));
+}
 
 // byte offset of element (row r, k) in a K-major no-swizzle operand with
 // `kb` 4-element k-blocks per row group: core (r/8, k/4) at
@@ -115,7 +143,8 @@ __device__ __forceinline__ void put4(char *hi, char *lo, int r, int k, int kb, f
     const float4 h = make_float4(tf32_hi(v.x), tf32_hi(v.y), tf32_hi(v.z), tf32_hi(v.w));
     const int o = core_off(r, k, kb);
     *reinterpret_cast<float4 *>(hi + o) = h;
-    *reinterpret_cast<float4 *>(lo + o) = make_float4(v.x - h.x, v.y - h.y, v.z - h.z, v.w - h.w);
+    const float2 l01 = up2(sub2(pk2(v.x, v.y), pk2(h.x, h.y))), l23 = up2(sub2(pk2(v.z, v.w), pk2(h.z, h.w)));
+    *reinterpret_cast<float4 *>(lo + o) = make_float4(l01.x, l01.y, l23.x, l23.y);
 }
 
 }  // namespace
@@ -130,255 +159,375 @@ struct DetectTcParams {
     uint8_t *codes;              // [net][rows], nullable
     uint32_t *errors;            // [net], nullable
     const int *status;
+    long long *clocks;           // NOMA_DETECT_CLK: per-role cycles of CTA (0, 0), nullable
 };
 
 // W0 = input width 2M, H = hidden width, NL = hidden layers (1 or 2).
-// kTcGroups groups of 128 threads each run their own tile stream (own A1
-// buffer, TMEM columns and mbarrier; group-local named barriers), so one
-// group's MMAs overlap another group's epilogue; the weights are shared.
-// TMEM per group (256 columns): D1 = [x W1^T | x w0] in columns 0..N1, D2
-// reuses columns 0..H once D1 has been read; the layer-2 A operand a1 (hi,
-// lo) is written by the epilogue into columns 128.. and 192.. with
-// tcgen05.st and read from there by the layer-2 MMAs, so the group's smem A1
-// buffer is free as soon as layer 1 completes and the next tile is staged
-// into it while layer 2 runs.
-template <int W0, int H, int NL>
-constexpr uint32_t tc_abuf_bytes() {  // per group: the layer-1 A operand (hi, lo)
-    return (uint32_t)(2 * kTcRows * W0 * 4);
+// ---------------------------------------------------------------------------
+// Warp-specialised pipeline (one CTA per SM, persistent over the net's tiles):
+//   warps 0-3   loaders: thread r forms widened row r of a tile from global
+//               samples, computes the linear branch lin = x . w0 in FP32,
+//               stages the row (hi/lo) into smem A1[slot] (slot = tile parity)
+//               and lin into lin_s[slot];
+//   warps 4-7   epilogue 1: D1[slot] -> a1 = relu(D1 + b1), split hi/lo into
+//               TMEM A2[slot] (the layer-2 A operand); with one hidden layer
+//               the output directly;
+//   warps 8-11  epilogue 2 (two layers): D2[slot] -> yhat = lin + a2 . w ->
+//               QPSK decision and bit errors;
+//   warp 12 (8) issues the layer-1 tcgen05.mma chains (elected lane);
+//   warps 13-14 issue the layer-2 chains of even / odd tiles.
+// Every hand-off is an mbarrier: *_FULL / *_EMPTY by the 4 warps of the
+// producing / consuming role, MMA completion by tcgen05.commit.  TMEM (all 512
+// columns): D1[2] at 0 / 64, D2[2] at 128 / 192, A2[2] (hi, lo) at 256 / 384.
+// Issue costs measured by tools/microbench/umma_rate.cu (M=128, K=8 tf32):
+// one issuing thread needs ~47 cycles per N=64 MMA, two concurrent issuers
+// reach the 32-cycle pipe floor when A is in TMEM; with A in smem the MMA is
+// bound by shared-memory operand bandwidth (~48 cycles at N=64) -- hence A2
+// in TMEM, two layer-2 issuers, and x . w0 on the CUDA cores (which also
+// keeps D1 at 64 columns so that everything fits in TMEM).
+template <int NL>
+struct WsRoles {
+    static constexpr int kMma1Warp = NL > 1 ? 12 : 8;  // layer-1 issuer; layer-2 issuers follow
+    static constexpr int kWarps = NL > 1 ? 15 : 9;
+    static constexpr int kThreads = 32 * kWarps;
+};
+// lin = x . w0 travels from the loaders to the last stage through a ring of
+// kLinSlots slots: with only two, the loaders would be held to within two
+// tiles of the final epilogue and starve the whole pipeline
+constexpr int kLinSlots = 8;
+enum WsBar { kA1Full = 0, kM1Done = 2, kD1Empty = 4, kA2Full = 6, kM2Done = 8, kD2Empty = 10, kLinFull = 12,
+             kLinEmpty = 12 + kLinSlots, kWsBars = 12 + 2 * kLinSlots };
+
+// one arrival per warp (barrier count = 4 warps per role): 128 per-thread
+// arrivals on one mbarrier serialise and cost more than the stage's work.
+// __syncwarp orders the lanes' prior shared-memory / tcgen05 writes (each lane
+// has fenced them) before lane 0's release-arrive.
+__device__ __forceinline__ void ws_arrive(uint32_t bar) {
+    __syncwarp();
+    if ((threadIdx.x & 31) == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
 }
+
 template <int W0, int H, int NL>
-__global__ void __launch_bounds__(kTcThreads, 1) detect_tc_kernel(DetectTcParams p) {
+constexpr size_t detect_ws_smem() {
+    return 2 * (size_t)H * W0 * 4 + (NL > 1 ? 2 * (size_t)H * H * 4 : 0) + 4 * (size_t)kTcRows * W0 * 4 +
+           (size_t)(NL + 1) * H * 4 + (size_t)W0 * 4 + kLinSlots * kTcRows * 4 + 8 * kWsBars + 16;
+}
+
+template <int W0, int H, int NL>
+__global__ void __launch_bounds__(WsRoles<NL>::kThreads, 1) detect_ws_kernel(DetectTcParams p) {
+    using R = WsRoles<NL>;
     constexpr int M = W0 / 2;
-    constexpr int N1 = H + 16;                 // layer-1 B rows: W1 | w0 | zeros
-    constexpr int KB0 = W0 / 4, KBH = H / 4;   // k-blocks per row group
-    constexpr uint32_t A1B = kTcRows * W0 * 4, B1B = N1 * W0 * 4;
-    constexpr uint32_t B2B = H * H * 4;
-    constexpr uint32_t ABUF = tc_abuf_bytes<W0, H, NL>();
-    constexpr uint32_t kA2Hi = 128, kA2Lo = 192;  // TMEM columns of the layer-2 A operand
-    static_assert(N1 <= 128 && H <= 64, "TMEM column plan: D1 < 128, A2 hi/lo 64 columns each");
+    constexpr int KB0 = W0 / 4, KBH = H / 4;  // k-blocks per row group
+    constexpr uint32_t A1B = kTcRows * W0 * 4, B1B = H * W0 * 4, B2B = H * H * 4;
+    constexpr uint32_t kD1 = 0, kD2 = 128, kA2 = 256, kA2S = 128;  // TMEM columns; A2 slot = hi | lo
+    static_assert(H == 64, "TMEM column plan assumes 64-wide hidden layers");
     extern __shared__ __align__(1024) char smem[];
     char *b1h = smem, *b1l = b1h + B1B;
     char *b2h = b1l + B1B, *b2l = b2h + (NL > 1 ? B2B : 0);
-    char *abase = b2l + (NL > 1 ? B2B : 0);
-    float *bias = reinterpret_cast<float *>(abase + kTcGroups * ABUF);  // [NL][H]
-    float *wf = bias + NL * H;                                           // [H]
-    uint64_t *mbars = reinterpret_cast<uint64_t *>(wf + H);              // [kTcGroups]
-    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(mbars + kTcGroups);
+    char *a1 = b2l + (NL > 1 ? B2B : 0);                 // [slot][hi | lo]
+    float *bias = reinterpret_cast<float *>(a1 + 4 * A1B);  // [NL][H]
+    float *wf = bias + NL * H;                              // [H]
+    float *w0s = wf + H;                                    // [W0]
+    float *lin_s = w0s + W0;                                // [kLinSlots][128]
+    uint64_t *bars = reinterpret_cast<uint64_t *>(lin_s + kLinSlots * kTcRows);
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + kWsBars);
+    auto bar = [&](int i) { return tc_s2u(bars + i); };
+    // NOMA_DETECT_CLK: lane 0 of each role's first warp in CTA (0, 0) records
+    // [total loop cycles, cycles waiting at site 0, at site 1, TMEM loads, dot,
+    // emit] per role
+    const int role = (threadIdx.x >> 7) < 3 ? (int)(threadIdx.x >> 7) : 3 + (int)(threadIdx.x >> 5) - 4 * 3;
+    long long *ck = p.clocks && blockIdx.x == 0 && blockIdx.y == 0 && (threadIdx.x & (threadIdx.x < 384 ? 127 : 31)) == 0
+                        ? p.clocks + 6 * role
+                        : nullptr;
+    auto wait = [&](int site, uint32_t b, uint32_t ph) {
+        if (ck) {
+            const long long t0 = clock64();
+            tc_mbar_wait(b, ph);
+            ck[1 + site] += clock64() - t0;
+        } else {
+            tc_mbar_wait(b, ph);
+        }
+    };
+    const long long tstart = ck ? clock64() : 0;
 
     const int net = blockIdx.y, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int grp = threadIdx.x >> 7, tid = threadIdx.x & 127;  // group, thread in group
-    char *a1h = abase + grp * ABUF, *a1l = a1h + A1B;
-    auto gsync = [&]() { asm volatile("bar.sync %0, 128;" ::"r"(1 + grp) : "memory"); };
     if (p.status && p.status[net] != NOMA_OK) {
-        if (blockIdx.x == 0 && tid == 0 && p.errors) p.errors[net] = 0xFFFFFFFFu;
+        if (blockIdx.x == 0 && threadIdx.x == 0 && p.errors) p.errors[net] = 0xFFFFFFFFu;
         return;
     }
     const NetGeom &g = p.g;
     const int d = net / p.K, k = net % p.K;
     const float *pl = p.plans + (size_t)net * g.plan_total;
-
     // ---- weights: hi/lo planes in the K-major core layout (FusedPlan order) --
-    for (int i = threadIdx.x; i < N1 * KB0; i += kTcThreads) {
+    for (int i = threadIdx.x; i < H * KB0; i += R::kThreads) {
         const int j = i / KB0, kq = (i - j * KB0) * 4;
-        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (j < H) v = *reinterpret_cast<const float4 *>(pl + g.plan_w[1] + j * g.plan_pad[0] + kq);
-        else if (j == H) v = *reinterpret_cast<const float4 *>(pl + g.plan_w0 + kq);
-        put4(b1h, b1l, j, kq, KB0, v);
+        put4(b1h, b1l, j, kq, KB0, *reinterpret_cast<const float4 *>(pl + g.plan_w[1] + j * g.plan_pad[0] + kq));
     }
     if constexpr (NL > 1) {
-        for (int i = threadIdx.x; i < H * KBH; i += kTcThreads) {
+        for (int i = threadIdx.x; i < H * KBH; i += R::kThreads) {
             const int j = i / KBH, kq = (i - j * KBH) * 4;
             put4(b2h, b2l, j, kq, KBH, *reinterpret_cast<const float4 *>(pl + g.plan_w[2] + j * g.plan_pad[1] + kq));
         }
     }
-    for (int i = threadIdx.x; i < NL * H; i += kTcThreads) bias[i] = pl[g.plan_b[1 + i / H] + i % H];
-    for (int i = threadIdx.x; i < H; i += kTcThreads) wf[i] = pl[g.plan_f + i];
+    for (int i = threadIdx.x; i < NL * H; i += R::kThreads) bias[i] = pl[g.plan_b[1 + i / H] + i % H];
+    for (int i = threadIdx.x; i < H; i += R::kThreads) wf[i] = pl[g.plan_f + i];
+    for (int i = threadIdx.x; i < W0; i += R::kThreads) w0s[i] = pl[g.plan_w0 + i];
     if (warp == 0) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(tc_s2u(tmem_slot)),
-                     "n"(256 * kTcGroups));
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(tc_s2u(tmem_slot)));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
-    if (threadIdx.x < kTcGroups) {
-        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(tc_s2u(mbars + threadIdx.x)));
+    if (threadIdx.x == 32) {
+        for (int i = 0; i < kWsBars; ++i) {
+            const bool commit = (i >= kM1Done && i < kM1Done + 2) || (i >= kM2Done && i < kM2Done + 2);
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar(i)), "r"(commit ? 1 : kTcRows / 32));
+        }
         asm volatile("fence.mbarrier_init.release.cluster;");
     }
     asm volatile("tcgen05.fence::before_thread_sync;");
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;");
-    // group grp: TMEM columns [256 grp, 256 grp + 256); lanes = the group's rows
-    const uint32_t tmem = *tmem_slot + 256 * grp;
-    const uint32_t trow = tmem + ((uint32_t)((warp & 3) * 32) << 16);  // this warp's TMEM lanes
-    const uint32_t bar = tc_s2u(mbars + grp);
-    uint32_t phase = 0;
+    const uint32_t tmem = *tmem_slot;
+    const int first = blockIdx.x, stride = gridDim.x;
+    const int ntile = first < p.tiles ? (p.tiles - first + stride - 1) / stride : 0;
 
-    // ---- tile loop: thread t = widened row t = symbol t/2, Re/Im half t&1 --
-    const int sym = tid >> 1;
-    const bool odd = tid & 1;
-    const float2 *src = reinterpret_cast<const float2 *>(p.data) + (size_t)d * p.rows * M;
-    float2 xs[M];
-    uint8_t truth_next = 0;  // truth code of the tile whose samples are in xs
-    auto load_tile = [&](int tile) {
-        const int s = tile * 64 + sym;
-        const bool ok = tile < p.tiles && s < p.rows;
-        truth_next = ok && p.truth && !odd ? p.truth[((size_t)d * p.rows + s) * p.K + k] : (uint8_t)0;
-#pragma unroll
-        for (int m = 0; m < M; m += 2) {
-            const float4 v = ok ? *reinterpret_cast<const float4 *>(src + (size_t)s * M + m)
-                                : make_float4(0.f, 0.f, 0.f, 0.f);
-            xs[m] = make_float2(v.x, v.y);
-            xs[m + 1] = make_float2(v.z, v.w);
+    // decision + bit errors of widened row r (lane pairs = Re/Im of a symbol)
+    uint32_t my_err = 0;
+    auto emit = [&](int tile, int r, float y, uint8_t truth) {
+        const float yo = __shfl_xor_sync(0xffffffffu, y, 1);
+        const int s = tile * 64 + (r >> 1);
+        if (!(r & 1) && s < p.rows) {
+            const uint8_t code = (uint8_t)((y < 0.f ? 1 : 0) | (yo < 0.f ? 2 : 0));  // eval.cpp:41-42
+            if (p.codes) p.codes[(size_t)net * p.rows + s] = code;
+            if (p.soft) *reinterpret_cast<float2 *>(p.soft + ((size_t)net * p.rows + s) * 2) = make_float2(y, yo);
+            if (p.truth) my_err += __popc((unsigned)(truth ^ code) & 3u);
         }
     };
-    // widened row (iq_transform.cpp:17-20) -> layer-1 A operand (hi/lo) in smem
-    auto stage_a1 = [&]() {
-#pragma unroll
-        for (int m = 0; m < M; m += 4) {
-            float4 re = make_float4(xs[m].x, xs[m + 1].x, xs[m + 2].x, xs[m + 3].x);
-            float4 im = make_float4(xs[m].y, xs[m + 1].y, xs[m + 2].y, xs[m + 3].y);
-            if (!odd) {
-                put4(a1h, a1l, tid, m, KB0, re);
-                put4(a1h, a1l, tid, M + m, KB0, im);
-            } else {
-                put4(a1h, a1l, tid, m, KB0, im);
-                put4(a1h, a1l, tid, M + m, KB0, make_float4(-re.x, -re.y, -re.z, -re.w));
-            }
-        }
+    auto truth_of = [&](int tile, int r) -> uint8_t {
+        const int s = tile * 64 + (r >> 1);
+        return p.truth && !(r & 1) && s < p.rows ? p.truth[((size_t)d * p.rows + s) * p.K + k] : (uint8_t)0;
     };
     // sum_c relu(v_c + b_c) w_c over 16 columns into 4 partial sums
-    auto dot16 = [&](const uint32_t (&v)[16], const float *b, const float *w, float (&acc)[4]) {
+    // (partials: acc2[0] = columns 4j, 4j+1; acc2[1] = 4j+2, 4j+3)
+    auto dot16 = [&](const uint32_t (&v)[16], const float *b, const float *w, p2_t (&acc2)[2]) {
 #pragma unroll
         for (int q = 0; q < 16; q += 4) {
             const float4 b4 = *reinterpret_cast<const float4 *>(b + q);
             const float4 w4 = *reinterpret_cast<const float4 *>(w + q);
-            acc[0] = fmaf(fmaxf(__uint_as_float(v[q]) + b4.x, 0.f), w4.x, acc[0]);
-            acc[1] = fmaf(fmaxf(__uint_as_float(v[q + 1]) + b4.y, 0.f), w4.y, acc[1]);
-            acc[2] = fmaf(fmaxf(__uint_as_float(v[q + 2]) + b4.z, 0.f), w4.z, acc[2]);
-            acc[3] = fmaf(fmaxf(__uint_as_float(v[q + 3]) + b4.w, 0.f), w4.w, acc[3]);
+            const p2_t a01 = relu2(add2(pk2(__uint_as_float(v[q]), __uint_as_float(v[q + 1])), pk2(b4.x, b4.y)));
+            const p2_t a23 = relu2(add2(pk2(__uint_as_float(v[q + 2]), __uint_as_float(v[q + 3])), pk2(b4.z, b4.w)));
+            acc2[0] = fma2(a01, pk2(w4.x, w4.y), acc2[0]);
+            acc2[1] = fma2(a23, pk2(w4.z, w4.w), acc2[1]);
         }
     };
-    uint32_t my_err = 0;
-    const int tstride = gridDim.x * kTcGroups;
-    int tile = blockIdx.x * kTcGroups + grp;
-    load_tile(tile);
-    stage_a1();
-    uint8_t truth_a1 = truth_next;  // truth of the tile staged in A1
-    load_tile(tile + tstride);
-    for (; tile < p.tiles; tile += tstride) {
-        const uint8_t truth_cur = truth_a1;
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        asm volatile("tcgen05.fence::before_thread_sync;");
-        gsync();
-        asm volatile("tcgen05.fence::after_thread_sync;");
-        if (tid == 0) {  // layer 1 (+ linear branch): D1[128 x N1] in TMEM columns 0..N1
-            constexpr uint32_t id1 = umma_idesc_tf32(N1);
+    // the final stage: D_N[slot] + lin -> decision (epilogue 1 or 2)
+    auto finish = [&](int i, int r, const uint32_t (&v)[H / 16][16], const float *bN, uint8_t truth) {
+        const int ls = i % kLinSlots;
+        wait(1, bar(kLinFull + ls), (i / kLinSlots) & 1);
+        const float lin = lin_s[ls * kTcRows + r];
+        ws_arrive(bar(kLinEmpty + ls));
+        const long long td0 = ck ? clock64() : 0;
+        p2_t acc2[2] = {0ull, 0ull};
 #pragma unroll
-            for (int kk = 0; kk < W0 / 8; ++kk) {
-                const uint32_t ko = kk * 256;
-                const uint64_t ah = umma_desc(tc_s2u(a1h) + ko, 128, KB0 * 128);
-                const uint64_t al = umma_desc(tc_s2u(a1l) + ko, 128, KB0 * 128);
-                const uint64_t bh = umma_desc(tc_s2u(b1h) + ko, 128, KB0 * 128);
-                const uint64_t bl = umma_desc(tc_s2u(b1l) + ko, 128, KB0 * 128);
-                umma_tf32(tmem, ah, bh, id1, kk > 0);
-                umma_tf32(tmem, ah, bl, id1, 1);
-                umma_tf32(tmem, al, bh, id1, 1);
-            }
-            umma_commit(bar);
+        for (int c = 0; c < H / 16; ++c) dot16(v[c], bN + 16 * c, wf + 16 * c, acc2);
+        const float2 s01 = up2(acc2[0]), s23 = up2(acc2[1]);
+        const float y = lin + ((s01.x + s01.y) + (s23.x + s23.y));  // hybrid_nn.cpp:81
+        const long long td1 = ck ? clock64() : 0;
+        emit(first + i * stride, r, y, truth);
+        if (ck) {
+            ck[4] += td1 - td0;
+            ck[5] += clock64() - td1;
         }
-        tc_mbar_wait(bar, phase);
-        phase ^= 1;
-        asm volatile("tcgen05.fence::after_thread_sync;");
-        // D1 -> registers: all H + 16 columns in flight, one wait
-        uint32_t v1[H / 16 + 1][16];
+    };
+
+    if (warp < 4) {
+        // ---------------- loaders: widened rows -> A1[slot] (hi/lo), lin ---------
+        const int r = threadIdx.x, sym = r >> 1;
+        const bool odd = r & 1;
+        const float2 *src = reinterpret_cast<const float2 *>(p.data) + (size_t)d * p.rows * M;
+        float2 xs[M];
+        auto load = [&](int tile) {
+            const int s = tile * 64 + sym;
+            const bool ok = s < p.rows;
 #pragma unroll
-        for (int c = 0; c <= H / 16; ++c) tmem_ld16_nw(trow + 16 * c, v1[c]);
-        tmem_wait_ld();
-        const float lin = __uint_as_float(v1[H / 16][0]);  // column H: x . w0
-        float acc[4] = {0.f, 0.f, 0.f, 0.f};
-        if constexpr (NL == 1) {
-            // layer 1 done: A1 is free for the next tile
-            stage_a1();
-            truth_a1 = truth_next;
-            load_tile(tile + 2 * tstride);
-#pragma unroll
-            for (int c = 0; c < H / 16; ++c) dot16(v1[c], bias + 16 * c, wf + 16 * c, acc);
-        } else {
-            // a1 = relu(D1 + b1) -> layer-2 A operand (hi/lo) in TMEM
-#pragma unroll
-            for (int c = 0; c < H / 16; ++c) {
-                float hi[16], lo[16];
-#pragma unroll
-                for (int q = 0; q < 16; q += 4) {
-                    const float4 b4 = *reinterpret_cast<const float4 *>(bias + 16 * c + q);
-                    const float bq[4] = {b4.x, b4.y, b4.z, b4.w};
-#pragma unroll
-                    for (int e = 0; e < 4; ++e) {
-                        const float a = fmaxf(__uint_as_float(v1[c][q + e]) + bq[e], 0.f);
-                        hi[q + e] = tf32_hi(a);
-                        lo[q + e] = a - hi[q + e];
-                    }
-                }
-                tmem_st16(trow + kA2Hi + 16 * c, hi);
-                tmem_st16(trow + kA2Lo + 16 * c, lo);
+            for (int m = 0; m < M; m += 2) {
+                const float4 v = ok ? *reinterpret_cast<const float4 *>(src + (size_t)s * M + m)
+                                    : make_float4(0.f, 0.f, 0.f, 0.f);
+                xs[m] = make_float2(v.x, v.y);
+                xs[m + 1] = make_float2(v.z, v.w);
             }
-            asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
-            asm volatile("tcgen05.fence::before_thread_sync;");
-            gsync();
+        };
+        if (ntile > 0) load(first);
+        for (int i = 0; i < ntile; ++i) {
+            const int sl = i & 1;
+            const uint32_t ph = (i >> 1) & 1;
+            char *ah = a1 + sl * 2 * A1B, *al = ah + A1B;
+            p2_t l2[2] = {0ull, 0ull};  // x . w0 (hybrid_nn.cpp:81, linear branch), 4 partials
+            wait(0, bar(kM1Done + sl), ph ^ 1);  // A1[sl] read by tile i-2's MMAs
+#pragma unroll
+            for (int m = 0; m < M; m += 4) {
+                const float4 re = make_float4(xs[m].x, xs[m + 1].x, xs[m + 2].x, xs[m + 3].x);
+                const float4 im = make_float4(xs[m].y, xs[m + 1].y, xs[m + 2].y, xs[m + 3].y);
+                // widened row (iq_transform.cpp:17-20): [Re; Im] or [Im; -Re]
+                const float4 lo4 = odd ? im : re;
+                const float4 hi4 = odd ? make_float4(-re.x, -re.y, -re.z, -re.w) : im;
+                put4(ah, al, r, m, KB0, lo4);
+                put4(ah, al, r, M + m, KB0, hi4);
+                const float4 wa = *reinterpret_cast<const float4 *>(w0s + m);
+                const float4 wb = *reinterpret_cast<const float4 *>(w0s + M + m);
+                l2[0] = fma2(pk2(lo4.x, lo4.y), pk2(wa.x, wa.y), l2[0]);
+                l2[1] = fma2(pk2(lo4.z, lo4.w), pk2(wa.z, wa.w), l2[1]);
+                l2[0] = fma2(pk2(hi4.x, hi4.y), pk2(wb.x, wb.y), l2[0]);
+                l2[1] = fma2(pk2(hi4.z, hi4.w), pk2(wb.z, wb.w), l2[1]);
+            }
+            if (i + 1 < ntile) load(first + (i + 1) * stride);  // in flight until the next stage
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            ws_arrive(bar(kA1Full + sl));
+            const int ls = i % kLinSlots;
+            wait(1, bar(kLinEmpty + ls), ((i / kLinSlots) & 1) ^ 1);
+            const float2 q01 = up2(l2[0]), q23 = up2(l2[1]);
+            lin_s[ls * kTcRows + r] = (q01.x + q01.y) + (q23.x + q23.y);
+            ws_arrive(bar(kLinFull + ls));
+        }
+    } else if (warp < 8) {
+        // ---------------- epilogue 1 --------------------------------------------
+        const int q = warp - 4, r = q * 32 + lane;
+        const uint32_t trow = tmem + ((uint32_t)(q * 32) << 16);
+        // truth codes two tiles ahead (a global load per tile would otherwise
+        // sit exposed on this stage's critical path)
+        uint8_t tq0 = NL == 1 ? truth_of(first, r) : 0, tq1 = NL == 1 ? truth_of(first + stride, r) : 0;
+        for (int i = 0; i < ntile; ++i) {
+            const int sl = i & 1;
+            const uint32_t ph = (i >> 1) & 1;
+            uint8_t truth = 0;
+            if constexpr (NL == 1) {
+                truth = tq0;
+                tq0 = tq1;
+                tq1 = truth_of(first + (i + 2) * stride, r);
+            }
+            wait(0, bar(kM1Done + sl), ph);
             asm volatile("tcgen05.fence::after_thread_sync;");
-            if (tid == 0) {  // layer 2: D2[128 x H] in TMEM columns 0..H, A from TMEM
-                constexpr uint32_t id2 = umma_idesc_tf32(H);
+            uint32_t v1[H / 16][16];
+            const long long tl0 = ck ? clock64() : 0;
 #pragma unroll
-                for (int kk = 0; kk < H / 8; ++kk) {
-                    const uint32_t ko = kk * 256;
-                    const uint64_t bh = umma_desc(tc_s2u(b2h) + ko, 128, KBH * 128);
-                    const uint64_t bl = umma_desc(tc_s2u(b2l) + ko, 128, KBH * 128);
-                    umma_tf32_ta(tmem, tmem + kA2Hi + 8 * kk, bh, id2, kk > 0);
-                    umma_tf32_ta(tmem, tmem + kA2Hi + 8 * kk, bl, id2, 1);
-                    umma_tf32_ta(tmem, tmem + kA2Lo + 8 * kk, bh, id2, 1);
+            for (int c = 0; c < H / 16; ++c) tmem_ld16_nw(trow + kD1 + sl * H + 16 * c, v1[c]);
+            tmem_wait_ld();
+            if (ck) ck[3] += clock64() - tl0;
+            asm volatile("tcgen05.fence::before_thread_sync;");
+            ws_arrive(bar(kD1Empty + sl));
+            if constexpr (NL == 1) {
+                finish(i, r, v1, bias, truth);
+            } else {
+                // A2[sl] is free once tile i-2's layer-2 MMAs are done
+                wait(1, bar(kM2Done + sl), ph ^ 1);
+                asm volatile("tcgen05.fence::after_thread_sync;");
+                const uint32_t a2 = trow + kA2 + sl * kA2S;
+#pragma unroll
+                for (int c = 0; c < H / 16; ++c) {
+                    float hi[16], lo[16];
+#pragma unroll
+                    for (int e4 = 0; e4 < 16; e4 += 4) {
+                        const float4 b4 = *reinterpret_cast<const float4 *>(bias + 16 * c + e4);
+#pragma unroll
+                        for (int e = 0; e < 4; e += 2) {
+                            const p2_t a = relu2(add2(pk2(__uint_as_float(v1[c][e4 + e]), __uint_as_float(v1[c][e4 + e + 1])),
+                                                      e ? pk2(b4.z, b4.w) : pk2(b4.x, b4.y)));
+                            const float2 af = up2(a);
+                            hi[e4 + e] = tf32_hi(af.x);
+                            hi[e4 + e + 1] = tf32_hi(af.y);
+                            const float2 lf = up2(sub2(a, pk2(hi[e4 + e], hi[e4 + e + 1])));
+                            lo[e4 + e] = lf.x;
+                            lo[e4 + e + 1] = lf.y;
+                        }
+                    }
+                    tmem_st16(a2 + 16 * c, hi);
+                    tmem_st16(a2 + H + 16 * c, lo);
                 }
-                umma_commit(bar);
+                asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+                asm volatile("tcgen05.fence::before_thread_sync;");
+                ws_arrive(bar(kA2Full + sl));
             }
-            // next tile's A1 while layer 2 runs (layer 1 has completed)
-            stage_a1();
-            truth_a1 = truth_next;
-            load_tile(tile + 2 * tstride);
-            tc_mbar_wait(bar, phase);
-            phase ^= 1;
+        }
+    } else if (NL > 1 && warp < 12) {
+        // ---------------- epilogue 2 --------------------------------------------
+        const int q = warp - 8, r = q * 32 + lane;
+        const uint32_t trow = tmem + ((uint32_t)(q * 32) << 16);
+        uint8_t tq0 = truth_of(first, r), tq1 = truth_of(first + stride, r);  // two tiles ahead
+        for (int i = 0; i < ntile; ++i) {
+            const int sl = i & 1;
+            const uint32_t ph = (i >> 1) & 1;
+            const uint8_t truth = tq0;
+            tq0 = tq1;
+            tq1 = truth_of(first + (i + 2) * stride, r);
+            wait(0, bar(kM2Done + sl), ph);
             asm volatile("tcgen05.fence::after_thread_sync;");
             uint32_t v2[H / 16][16];
+            const long long tl0 = ck ? clock64() : 0;
 #pragma unroll
-            for (int c = 0; c < H / 16; ++c) tmem_ld16_nw(trow + 16 * c, v2[c]);
+            for (int c = 0; c < H / 16; ++c) tmem_ld16_nw(trow + kD2 + sl * H + 16 * c, v2[c]);
             tmem_wait_ld();
+            if (ck) ck[3] += clock64() - tl0;
+            asm volatile("tcgen05.fence::before_thread_sync;");
+            ws_arrive(bar(kD2Empty + sl));
+            finish(i, r, v2, bias + H, truth);
+        }
+    } else if (warp == R::kMma1Warp) {
+        // ---------------- layer-1 issuer (whole warp, elected lane issues) -------
+        constexpr uint32_t id1 = umma_idesc_tf32(H);
+        const uint64_t b1hd = umma_desc(tc_s2u(b1h), 128, KB0 * 128), b1ld = umma_desc(tc_s2u(b1l), 128, KB0 * 128);
+        const uint64_t a0hd = umma_desc(tc_s2u(a1), 128, KB0 * 128);
+        for (int i = 0; i < ntile; ++i) {
+            const int sl = i & 1;
+            const uint32_t ph = (i >> 1) & 1;
+            wait(0, bar(kA1Full + sl), ph);
+            wait(1, bar(kD1Empty + sl), ph ^ 1);
+            asm volatile("tcgen05.fence::after_thread_sync;");
+            const uint64_t ahd = a0hd + (uint64_t)((sl * 2 * A1B) >> 4), ald = ahd + (A1B >> 4);
+            const uint32_t dcol = tmem + kD1 + sl * H;
+            if (lane == 0) {
 #pragma unroll
-            for (int c = 0; c < H / 16; ++c) dot16(v2[c], bias + H + 16 * c, wf + 16 * c, acc);
+                for (int kk = 0; kk < W0 / 8; ++kk) {
+                    const uint64_t ko = (uint64_t)(kk * 16);  // 256 B per k-step, in 16-byte units
+                    umma_tf32(dcol, ahd + ko, b1hd + ko, id1, kk > 0);
+                    umma_tf32(dcol, ahd + ko, b1ld + ko, id1, 1);
+                    umma_tf32(dcol, ald + ko, b1hd + ko, id1, 1);
+                }
+                umma_commit(bar(kM1Done + sl));
+            }
+            __syncwarp();
         }
-        // yhat = x.w0 + a_N . w (hybrid_nn.cpp:81); Re/Im of symbol `sym`
-        const float y = lin + ((acc[0] + acc[1]) + (acc[2] + acc[3]));
-        const float yo = __shfl_xor_sync(0xffffffffu, y, 1);
-        const int s = tile * 64 + sym;
-        if (!odd && s < p.rows) {
-            const uint8_t code = (uint8_t)((y < 0.f ? 1 : 0) | (yo < 0.f ? 2 : 0));  // eval.cpp:41-42
-            if (p.codes) p.codes[(size_t)net * p.rows + s] = code;
-            if (p.soft) *reinterpret_cast<float2 *>(p.soft + ((size_t)net * p.rows + s) * 2) = make_float2(y, yo);
-            if (p.truth) my_err += __popc((unsigned)(truth_cur ^ code) & 3u);
+    } else if (NL > 1 && warp > R::kMma1Warp) {
+        // ---------------- layer-2 issuers: warp 13 even tiles, 14 odd tiles ------
+        constexpr uint32_t id2 = umma_idesc_tf32(H);
+        const uint64_t b2hd = umma_desc(tc_s2u(b2h), 128, KBH * 128), b2ld = umma_desc(tc_s2u(b2l), 128, KBH * 128);
+        const int sl = warp - R::kMma1Warp - 1;
+        const uint32_t a2 = tmem + kA2 + sl * kA2S, dcol = tmem + kD2 + sl * H;
+        for (int i = sl; i < ntile; i += 2) {
+            const uint32_t ph = (i >> 1) & 1;
+            wait(0, bar(kA2Full + sl), ph);
+            wait(1, bar(kD2Empty + sl), ph ^ 1);  // epilogue 2 has read tile i-2's D2
+            asm volatile("tcgen05.fence::after_thread_sync;");
+            if (lane == 0) {
+#pragma unroll
+                for (int kk = 0; kk < H / 8; ++kk) {
+                    const uint64_t ko = (uint64_t)(kk * 16);
+                    umma_tf32_ta(dcol, a2 + 8 * kk, b2hd + ko, id2, kk > 0);
+                    umma_tf32_ta(dcol, a2 + 8 * kk, b2ld + ko, id2, 1);
+                    umma_tf32_ta(dcol, a2 + H + 8 * kk, b2hd + ko, id2, 1);
+                }
+                umma_commit(bar(kM2Done + sl));
+            }
+            __syncwarp();
         }
-        // this tile's TMEM reads before the next tile's layer-1 MMA overwrites D
-        asm volatile("tcgen05.fence::before_thread_sync;");
     }
-    if (p.errors && p.truth) {
+    if (ck) ck[0] = clock64() - tstart;
+    if ((NL == 1 ? (warp >= 4 && warp < 8) : (warp >= 8 && warp < 12)) && p.errors && p.truth) {
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) my_err += __shfl_xor_sync(0xffffffffu, my_err, o);
         if (lane == 0 && my_err) atomicAdd(p.errors + net, my_err);
     }
     asm volatile("tcgen05.fence::before_thread_sync;");
     __syncthreads();
-    if (warp == 0)
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(*tmem_slot), "n"(256 * kTcGroups));
-}
-
-template <int W0, int H, int NL>
-constexpr size_t detect_tc_smem() {
-    return 2 * (size_t)(H + 16) * W0 * 4 + (NL > 1 ? 2 * (size_t)H * H * 4 : 0) +
-           (size_t)kTcGroups * tc_abuf_bytes<W0, H, NL>() + (size_t)(NL + 1) * H * 4 + 8 * kTcGroups + 8;
+    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
 }
 
 // Supported shapes: widened input 32 or 64 wide, one or two hidden layers of
@@ -405,6 +554,14 @@ int detect_tc_launch(const DetectParams &dp, cudaStream_t st) {
     p.codes = dp.codes;
     p.errors = dp.errors;
     p.status = dp.status;
+    p.clocks = nullptr;
+    static long long *clk_buf = nullptr;
+    const bool clk = std::getenv("NOMA_DETECT_CLK") != nullptr;
+    if (clk) {
+        if (!clk_buf) cudaMalloc(&clk_buf, 64 * sizeof(long long));
+        cudaMemsetAsync(clk_buf, 0, 64 * sizeof(long long), st);
+        p.clocks = clk_buf;
+    }
     if (p.tiles == 0 || p.n_nets == 0) return NOMA_OK;
     int sms = 148, dev = 0;
     cudaGetDevice(&dev);
@@ -413,15 +570,26 @@ int detect_tc_launch(const DetectParams &dp, cudaStream_t st) {
     // would leave a second wave of CTAs that doubles the kernel time
     int ctas = sms / p.n_nets;
     ctas = ctas < 1 ? 1 : ctas > p.tiles ? p.tiles : ctas;
-    auto launch = [&](auto kern, size_t smem) -> int {
+    auto launch = [&](auto kern, size_t smem, int threads) -> int {
+        // one CTA per SM: each allocates all 512 TMEM columns
+        smem = smem < 116 * 1024 ? 116 * 1024 : smem;
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        kern<<<dim3(ctas, p.n_nets), kTcThreads, smem, st>>>(p);
-        return cudaGetLastError() == cudaSuccess ? NOMA_OK : NOMA_ERR_CUDA;
+        kern<<<dim3(ctas, p.n_nets), threads, smem, st>>>(p);
+        if (cudaGetLastError() != cudaSuccess) return NOMA_ERR_CUDA;
+        if (clk) {  // roles: loader, epilogue 1, epilogue 2, L1 issuer, L2 issuers (even, odd)
+            long long h[36];
+            cudaMemcpyAsync(h, clk_buf, sizeof h, cudaMemcpyDeviceToHost, st);
+            cudaStreamSynchronize(st);
+            std::fprintf(stderr, "NOMA_DETECT_CLK tiles/CTA %d:", (p.tiles + ctas - 1) / ctas);
+            for (int i = 0; i < 36; ++i) std::fprintf(stderr, " %lld", h[i]);
+            std::fprintf(stderr, "\n");
+        }
+        return NOMA_OK;
     };
-    if (W0 == 32 && NL == 1) return launch(detect_tc_kernel<32, 64, 1>, detect_tc_smem<32, 64, 1>());
-    if (W0 == 32 && NL == 2) return launch(detect_tc_kernel<32, 64, 2>, detect_tc_smem<32, 64, 2>());
-    if (W0 == 64 && NL == 1) return launch(detect_tc_kernel<64, 64, 1>, detect_tc_smem<64, 64, 1>());
-    return launch(detect_tc_kernel<64, 64, 2>, detect_tc_smem<64, 64, 2>());
+    if (W0 == 32 && NL == 1) return launch(detect_ws_kernel<32, 64, 1>, detect_ws_smem<32, 64, 1>(), WsRoles<1>::kThreads);
+    if (W0 == 32 && NL == 2) return launch(detect_ws_kernel<32, 64, 2>, detect_ws_smem<32, 64, 2>(), WsRoles<2>::kThreads);
+    if (W0 == 64 && NL == 1) return launch(detect_ws_kernel<64, 64, 1>, detect_ws_smem<64, 64, 1>(), WsRoles<1>::kThreads);
+    return launch(detect_ws_kernel<64, 64, 2>, detect_ws_smem<64, 64, 2>(), WsRoles<2>::kThreads);
 }
 
 }  // namespace noma_dev

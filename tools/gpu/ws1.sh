@@ -1,0 +1,7 @@
+mkdir -p gpurun_out
+timeout 300 python -m pytest tests/test_gpu_detect_tc.py -x -q 2>&1 | tail -3
+for ws in 1 0; do
+  NOMA_DETECT_WS=$ws timeout 300 python bench.py --config c3 --steps 5 --warmup 3 --no-cpu-baseline 2>&1 | tail -1 > gpurun_out/bench_c3_ws$ws.json
+  python -c "
+import json;d=json.load(open('gpurun_out/bench_c3_ws$ws.json'));print('ws$ws', '%.3g'%d['value'], d['ms_per_step'], d['roofline'].get('frac_of_3xtf32_ceiling'), d.get('bit_errors'))"
+done
