@@ -296,10 +296,11 @@ def detect_only(args, cfg):
         sms = torch.cuda.get_device_properties(dev).multi_processor_count
         ctas_per_net = max(1, sms // (S * K))  # detect launcher: one wave, one CTA per SM
         tiles_per_cta = -(-((nd + 63) // 64) // ctas_per_net)
-        # per 128-row tile: 3 x W0/8 layer-1 MMAs with A in smem, bound by the
-        # shared-memory operand read (~48 cycles each at N=64), + 3 x H/8 per
-        # further layer with A in TMEM at the M*N/256 = 32-cycle pipe floor
-        tile_cyc = 3 * (dims[0] // 8) * 48 + sum(3 * (dims[l - 1] // 8) * 32 for l in range(2, len(dims)))
+        # per 128-row tile: 3 MMAs per k-step of 8; A from TMEM runs at the
+        # M*N/256 = 32-cycle pipe floor (N=64), A from smem (layer 1 of a
+        # 64-wide input) is bound by the shared-memory operand read (~48 cycles)
+        tile_cyc = 3 * (dims[0] // 8) * (32 if dims[0] <= 32 else 48) + \
+            sum(3 * (dims[l - 1] // 8) * 32 for l in range(2, len(dims)))
         attain_ms = tiles_per_cta * tile_cyc / (clk_ghz * 1e6) * max(1, -(-(S * K) // sms))
         roofline = {"bound": "tensor", "kernel": "detect_ws_kernel", "achieved": achieved,
                     "peak": tf32_mma / 3, "unit": "TFLOP/s", "frac": 3 * achieved / tf32_mma,
@@ -310,8 +311,8 @@ def detect_only(args, cfg):
                     "bf16_half_peak": tf32_peak,
                     "attainable_ms": attain_ms,
                     "frac_of_attainable": attain_ms / kern_ms,
-                    "attainable_note": "MMA floor per tile: layer 1 A-from-smem MMAs bound by smem "
-                                       "operand bandwidth (48 cyc), later layers A-from-TMEM at 32 cyc",
+                    "attainable_note": "MMA floor per 128-row tile: 3 MMAs per k-step, 32 cycles each with "
+                                       "A in TMEM (48 with A in smem, 64-wide inputs)",
                     "hbm_bound_ms": bytes_step / (hbm * 1e9) * 1e3,
                     "algorithmic_flop_per_launch": flop_step, "traffic": None}
     else:

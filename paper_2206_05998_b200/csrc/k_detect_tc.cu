@@ -165,43 +165,50 @@ struct DetectTcParams {
 // W0 = input width 2M, H = hidden width, NL = hidden layers (1 or 2).
 // ---------------------------------------------------------------------------
 // Warp-specialised pipeline (one CTA per SM, persistent over the net's tiles):
-//   warps 0-3   loaders: thread r forms widened row r of a tile from global
-//               samples, computes the linear branch lin = x . w0 in FP32,
-//               stages the row (hi/lo) into smem A1[slot] (slot = tile parity)
-//               and lin into lin_s[slot];
-//   warps 4-7   epilogue 1: D1[slot] -> a1 = relu(D1 + b1), split hi/lo into
-//               TMEM A2[slot] (the layer-2 A operand); with one hidden layer
-//               the output directly;
-//   warps 8-11  epilogue 2 (two layers): D2[slot] -> yhat = lin + a2 . w ->
-//               QPSK decision and bit errors;
-//   warp 12 (8) issues the layer-1 tcgen05.mma chains (elected lane);
-//   warps 13-14 issue the layer-2 chains of even / odd tiles.
-// Every hand-off is an mbarrier: *_FULL / *_EMPTY by the 4 warps of the
-// producing / consuming role, MMA completion by tcgen05.commit.  TMEM (all 512
-// columns): D1[2] at 0 / 64, D2[2] at 128 / 192, A2[2] (hi, lo) at 256 / 384.
-// Issue costs measured by tools/microbench/umma_rate.cu (M=128, K=8 tf32):
-// one issuing thread needs ~47 cycles per N=64 MMA, two concurrent issuers
-// reach the 32-cycle pipe floor when A is in TMEM; with A in smem the MMA is
-// bound by shared-memory operand bandwidth (~48 cycles at N=64) -- hence A2
-// in TMEM, two layer-2 issuers, and x . w0 on the CUDA cores (which also
-// keeps D1 at 64 columns so that everything fits in TMEM).
-template <int NL>
+//   warps 0-3    loaders: thread r forms widened row r of a tile from global
+//                samples, computes the linear branch lin = x . w0 in FP32, and
+//                stages the row hi/lo as the layer-1 A operand of slot
+//                (tile parity): in TMEM with tcgen05.st for a 32-wide input,
+//                in smem (K-major core layout) for a 64-wide one; lin goes to
+//                an 8-slot smem ring;
+//   warps 4-7    epilogue 1: D[slot] -> a1 = relu(D + b1), split hi/lo into
+//                TMEM A2[slot] (the layer-2 A operand); with one hidden layer
+//                the output directly;
+//   warps 8-11   epilogue 2 (two layers): D[slot] -> yhat = lin + a2 . w ->
+//                QPSK decision and bit errors;
+//   next 2 warps issue the layer-1 tcgen05.mma chains of even / odd tiles;
+//   last 2 warps issue the layer-2 chains of even / odd tiles.
+// Every hand-off is an mbarrier with one arrival per producing warp; MMA
+// completion by tcgen05.commit.  TMEM (512 columns): D[2] at 0 / 64 -- the
+// layer-2 accumulator reuses its slot's layer-1 columns, which epilogue 1 has
+// drained before it releases A2, and the next layer-1 MMA into the slot waits
+// for the final epilogue; A2[2] (hi, lo) at 128 / 256; A1[2] (hi, lo) at
+// 384 / 448 for a 32-wide input.
+// Why (tools/microbench/umma_rate.cu, tmem_bw.cu, NOMA_DETECT_CLK): an M=128,
+// N=64 tf32 MMA reaches the 32-cycle pipe floor only with A in TMEM and two
+// concurrent issuers (one issuer: ~47 cycles; A in smem: ~48 cycles, bound by
+// the smem operand read); TMEM loads/stores are cheap (~300-800 B/cycle), and
+// shared memory is the contended resource -- while the tensor core streams
+// operands from it, epilogue LDS / mbarrier latency grows ~10x.
+template <int W0, int NL>
 struct WsRoles {
-    static constexpr int kMma1Warp = NL > 1 ? 12 : 8;  // layer-1 issuer; layer-2 issuers follow
-    static constexpr int kWarps = NL > 1 ? 15 : 9;
+    static constexpr bool kA1Tmem = W0 <= 32;            // layer-1 A operand in TMEM
+    static constexpr int kMma1Warp = NL > 1 ? 12 : 8;    // layer-1 issuers: kMma1Warp, +1
+    static constexpr int kMma2Warp = kMma1Warp + 2;      // layer-2 issuers (two layers): +0, +1
+    static constexpr int kWarps = NL > 1 ? 16 : 10;
     static constexpr int kThreads = 32 * kWarps;
 };
 // lin = x . w0 travels from the loaders to the last stage through a ring of
 // kLinSlots slots: with only two, the loaders would be held to within two
 // tiles of the final epilogue and starve the whole pipeline
 constexpr int kLinSlots = 8;
-enum WsBar { kA1Full = 0, kM1Done = 2, kD1Empty = 4, kA2Full = 6, kM2Done = 8, kD2Empty = 10, kLinFull = 12,
-             kLinEmpty = 12 + kLinSlots, kWsBars = 12 + 2 * kLinSlots };
+enum WsBar { kA1Full = 0, kM1Done = 2, kDEmpty = 4, kA2Full = 6, kM2Done = 8, kLinFull = 10,
+             kLinEmpty = 10 + kLinSlots, kWsBars = 10 + 2 * kLinSlots };
 
 // one arrival per warp (barrier count = 4 warps per role): 128 per-thread
-// arrivals on one mbarrier serialise and cost more than the stage's work.
-// __syncwarp orders the lanes' prior shared-memory / tcgen05 writes (each lane
-// has fenced them) before lane 0's release-arrive.
+// arrivals on one mbarrier serialise.  __syncwarp orders the lanes' prior
+// shared-memory / tcgen05 writes (each lane has fenced them) before lane 0's
+// release-arrive.
 __device__ __forceinline__ void ws_arrive(uint32_t bar) {
     __syncwarp();
     if ((threadIdx.x & 31) == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
@@ -209,33 +216,36 @@ __device__ __forceinline__ void ws_arrive(uint32_t bar) {
 
 template <int W0, int H, int NL>
 constexpr size_t detect_ws_smem() {
-    return 2 * (size_t)H * W0 * 4 + (NL > 1 ? 2 * (size_t)H * H * 4 : 0) + 4 * (size_t)kTcRows * W0 * 4 +
-           (size_t)(NL + 1) * H * 4 + (size_t)W0 * 4 + kLinSlots * kTcRows * 4 + 8 * kWsBars + 16;
+    return 2 * (size_t)H * W0 * 4 + (NL > 1 ? 2 * (size_t)H * H * 4 : 0) +
+           (WsRoles<W0, NL>::kA1Tmem ? 0 : 4 * (size_t)kTcRows * W0 * 4) + (size_t)(NL + 1) * H * 4 +
+           (size_t)W0 * 4 + kLinSlots * kTcRows * 4 + 8 * kWsBars + 16;
 }
 
 template <int W0, int H, int NL>
-__global__ void __launch_bounds__(WsRoles<NL>::kThreads, 1) detect_ws_kernel(DetectTcParams p) {
-    using R = WsRoles<NL>;
+__global__ void __launch_bounds__(WsRoles<W0, NL>::kThreads, 1) detect_ws_kernel(DetectTcParams p) {
+    using R = WsRoles<W0, NL>;
+    constexpr bool kA1T = R::kA1Tmem;
     constexpr int M = W0 / 2;
     constexpr int KB0 = W0 / 4, KBH = H / 4;  // k-blocks per row group
     constexpr uint32_t A1B = kTcRows * W0 * 4, B1B = H * W0 * 4, B2B = H * H * 4;
-    constexpr uint32_t kD1 = 0, kD2 = 128, kA2 = 256, kA2S = 128;  // TMEM columns; A2 slot = hi | lo
+    constexpr uint32_t kD = 0, kA2 = 128, kA2S = 128, kA1 = 384, kA1S = 64;  // TMEM columns
     static_assert(H == 64, "TMEM column plan assumes 64-wide hidden layers");
     extern __shared__ __align__(1024) char smem[];
     char *b1h = smem, *b1l = b1h + B1B;
     char *b2h = b1l + B1B, *b2l = b2h + (NL > 1 ? B2B : 0);
-    char *a1 = b2l + (NL > 1 ? B2B : 0);                 // [slot][hi | lo]
-    float *bias = reinterpret_cast<float *>(a1 + 4 * A1B);  // [NL][H]
-    float *wf = bias + NL * H;                              // [H]
-    float *w0s = wf + H;                                    // [W0]
-    float *lin_s = w0s + W0;                                // [kLinSlots][128]
+    char *a1 = b2l + (NL > 1 ? B2B : 0);                                 // smem A1 [slot][hi | lo] (W0 = 64)
+    float *bias = reinterpret_cast<float *>(a1 + (kA1T ? 0 : 4 * A1B));  // [NL][H]
+    float *wf = bias + NL * H;                                           // [H]
+    float *w0s = wf + H;                                                 // [W0]
+    float *lin_s = w0s + W0;                                             // [kLinSlots][128]
     uint64_t *bars = reinterpret_cast<uint64_t *>(lin_s + kLinSlots * kTcRows);
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + kWsBars);
     auto bar = [&](int i) { return tc_s2u(bars + i); };
     // NOMA_DETECT_CLK: lane 0 of each role's first warp in CTA (0, 0) records
     // [total loop cycles, cycles waiting at site 0, at site 1, TMEM loads, dot,
-    // emit] per role
-    const int role = (threadIdx.x >> 7) < 3 ? (int)(threadIdx.x >> 7) : 3 + (int)(threadIdx.x >> 5) - 4 * 3;
+    // emit] per role (roles: loaders, epilogue 1, epilogue 2, then one per
+    // issuing warp)
+    const int role = (threadIdx.x >> 7) < 3 ? (int)(threadIdx.x >> 7) : 3 + (int)(threadIdx.x >> 5) - 12;
     long long *ck = p.clocks && blockIdx.x == 0 && blockIdx.y == 0 && (threadIdx.x & (threadIdx.x < 384 ? 127 : 31)) == 0
                         ? p.clocks + 6 * role
                         : nullptr;
@@ -306,7 +316,7 @@ __global__ void __launch_bounds__(WsRoles<NL>::kThreads, 1) detect_ws_kernel(Det
         const int s = tile * 64 + (r >> 1);
         return p.truth && !(r & 1) && s < p.rows ? p.truth[((size_t)d * p.rows + s) * p.K + k] : (uint8_t)0;
     };
-    // sum_c relu(v_c + b_c) w_c over 16 columns into 4 partial sums
+    // sum_c relu(v_c + b_c) w_c over 16 columns
     // (partials: acc2[0] = columns 4j, 4j+1; acc2[1] = 4j+2, 4j+3)
     auto dot16 = [&](const uint32_t (&v)[16], const float *b, const float *w, p2_t (&acc2)[2]) {
 #pragma unroll
@@ -319,7 +329,7 @@ __global__ void __launch_bounds__(WsRoles<NL>::kThreads, 1) detect_ws_kernel(Det
             acc2[1] = fma2(a23, pk2(w4.z, w4.w), acc2[1]);
         }
     };
-    // the final stage: D_N[slot] + lin -> decision (epilogue 1 or 2)
+    // the final stage: D[slot] (drained) + lin -> decision (epilogue 1 or 2)
     auto finish = [&](int i, int r, const uint32_t (&v)[H / 16][16], const float *bN, uint8_t truth) {
         const int ls = i % kLinSlots;
         wait(1, bar(kLinFull + ls), (i / kLinSlots) & 1);
@@ -338,11 +348,21 @@ __global__ void __launch_bounds__(WsRoles<NL>::kThreads, 1) detect_ws_kernel(Det
             ck[5] += clock64() - td1;
         }
     };
+    // drain D[slot] of tile i into registers and release the slot / columns
+    auto drain = [&](int i, uint32_t trow, uint32_t (&v)[H / 16][16]) {
+        const long long tl0 = ck ? clock64() : 0;
+#pragma unroll
+        for (int c = 0; c < H / 16; ++c) tmem_ld16_nw(trow + kD + (i & 1) * H + 16 * c, v[c]);
+        tmem_wait_ld();
+        if (ck) ck[3] += clock64() - tl0;
+        asm volatile("tcgen05.fence::before_thread_sync;");
+    };
 
     if (warp < 4) {
         // ---------------- loaders: widened rows -> A1[slot] (hi/lo), lin ---------
         const int r = threadIdx.x, sym = r >> 1;
         const bool odd = r & 1;
+        const uint32_t trow = tmem + ((uint32_t)(warp * 32) << 16);
         const float2 *src = reinterpret_cast<const float2 *>(p.data) + (size_t)d * p.rows * M;
         float2 xs[M];
         auto load = [&](int tile) {
@@ -360,9 +380,12 @@ __global__ void __launch_bounds__(WsRoles<NL>::kThreads, 1) detect_ws_kernel(Det
         for (int i = 0; i < ntile; ++i) {
             const int sl = i & 1;
             const uint32_t ph = (i >> 1) & 1;
-            char *ah = a1 + sl * 2 * A1B, *al = ah + A1B;
             p2_t l2[2] = {0ull, 0ull};  // x . w0 (hybrid_nn.cpp:81, linear branch), 4 partials
             wait(0, bar(kM1Done + sl), ph ^ 1);  // A1[sl] read by tile i-2's MMAs
+            asm volatile("tcgen05.fence::after_thread_sync;");
+            float rh[kA1T ? W0 : 1], rl[kA1T ? W0 : 1];  // the row, hi / lo (TMEM staging)
+            (void)rh;
+            (void)rl;
 #pragma unroll
             for (int m = 0; m < M; m += 4) {
                 const float4 re = make_float4(xs[m].x, xs[m + 1].x, xs[m + 2].x, xs[m + 3].x);
@@ -370,8 +393,19 @@ __global__ void __launch_bounds__(WsRoles<NL>::kThreads, 1) detect_ws_kernel(Det
                 // widened row (iq_transform.cpp:17-20): [Re; Im] or [Im; -Re]
                 const float4 lo4 = odd ? im : re;
                 const float4 hi4 = odd ? make_float4(-re.x, -re.y, -re.z, -re.w) : im;
-                put4(ah, al, r, m, KB0, lo4);
-                put4(ah, al, r, M + m, KB0, hi4);
+                if constexpr (kA1T) {
+                    const float v8[8] = {lo4.x, lo4.y, lo4.z, lo4.w, hi4.x, hi4.y, hi4.z, hi4.w};
+#pragma unroll
+                    for (int e = 0; e < 8; ++e) {
+                        const int kk = e < 4 ? m + e : M + m + e - 4;
+                        rh[kk] = tf32_hi(v8[e]);
+                        rl[kk] = v8[e] - rh[kk];
+                    }
+                } else {
+                    char *ah = a1 + sl * 2 * A1B, *al = ah + A1B;
+                    put4(ah, al, r, m, KB0, lo4);
+                    put4(ah, al, r, M + m, KB0, hi4);
+                }
                 const float4 wa = *reinterpret_cast<const float4 *>(w0s + m);
                 const float4 wb = *reinterpret_cast<const float4 *>(w0s + M + m);
                 l2[0] = fma2(pk2(lo4.x, lo4.y), pk2(wa.x, wa.y), l2[0]);
@@ -379,8 +413,26 @@ __global__ void __launch_bounds__(WsRoles<NL>::kThreads, 1) detect_ws_kernel(Det
                 l2[0] = fma2(pk2(hi4.x, hi4.y), pk2(wb.x, wb.y), l2[0]);
                 l2[1] = fma2(pk2(hi4.z, hi4.w), pk2(wb.z, wb.w), l2[1]);
             }
+            if constexpr (kA1T) {
+#pragma unroll
+                for (int c = 0; c < W0 / 16; ++c) {
+                    float h16[16], l16[16];
+#pragma unroll
+                    for (int e = 0; e < 16; ++e) {
+                        h16[e] = rh[16 * c + e];
+                        l16[e] = rl[16 * c + e];
+                    }
+                    tmem_st16(trow + kA1 + sl * kA1S + 16 * c, h16);
+                    tmem_st16(trow + kA1 + sl * kA1S + W0 + 16 * c, l16);
+                }
+            }
             if (i + 1 < ntile) load(first + (i + 1) * stride);  // in flight until the next stage
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            if constexpr (kA1T) {
+                asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+                asm volatile("tcgen05.fence::before_thread_sync;");
+            } else {
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            }
             ws_arrive(bar(kA1Full + sl));
             const int ls = i % kLinSlots;
             wait(1, bar(kLinEmpty + ls), ((i / kLinSlots) & 1) ^ 1);
@@ -407,14 +459,9 @@ __global__ void __launch_bounds__(WsRoles<NL>::kThreads, 1) detect_ws_kernel(Det
             wait(0, bar(kM1Done + sl), ph);
             asm volatile("tcgen05.fence::after_thread_sync;");
             uint32_t v1[H / 16][16];
-            const long long tl0 = ck ? clock64() : 0;
-#pragma unroll
-            for (int c = 0; c < H / 16; ++c) tmem_ld16_nw(trow + kD1 + sl * H + 16 * c, v1[c]);
-            tmem_wait_ld();
-            if (ck) ck[3] += clock64() - tl0;
-            asm volatile("tcgen05.fence::before_thread_sync;");
-            ws_arrive(bar(kD1Empty + sl));
+            drain(i, trow, v1);
             if constexpr (NL == 1) {
+                ws_arrive(bar(kDEmpty + sl));
                 finish(i, r, v1, bias, truth);
             } else {
                 // A2[sl] is free once tile i-2's layer-2 MMAs are done
@@ -444,7 +491,7 @@ __global__ void __launch_bounds__(WsRoles<NL>::kThreads, 1) detect_ws_kernel(Det
                 }
                 asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
                 asm volatile("tcgen05.fence::before_thread_sync;");
-                ws_arrive(bar(kA2Full + sl));
+                ws_arrive(bar(kA2Full + sl));  // also: D[sl] drained, layer 2 may overwrite it
             }
         }
     } else if (NL > 1 && warp < 12) {
@@ -461,50 +508,54 @@ __global__ void __launch_bounds__(WsRoles<NL>::kThreads, 1) detect_ws_kernel(Det
             wait(0, bar(kM2Done + sl), ph);
             asm volatile("tcgen05.fence::after_thread_sync;");
             uint32_t v2[H / 16][16];
-            const long long tl0 = ck ? clock64() : 0;
-#pragma unroll
-            for (int c = 0; c < H / 16; ++c) tmem_ld16_nw(trow + kD2 + sl * H + 16 * c, v2[c]);
-            tmem_wait_ld();
-            if (ck) ck[3] += clock64() - tl0;
-            asm volatile("tcgen05.fence::before_thread_sync;");
-            ws_arrive(bar(kD2Empty + sl));
+            drain(i, trow, v2);
+            ws_arrive(bar(kDEmpty + sl));
             finish(i, r, v2, bias + H, truth);
         }
-    } else if (warp == R::kMma1Warp) {
-        // ---------------- layer-1 issuer (whole warp, elected lane issues) -------
+    } else if (warp == R::kMma1Warp || warp == R::kMma1Warp + 1) {
+        // ---------------- layer-1 issuers: even / odd tiles (elected lane) -------
         constexpr uint32_t id1 = umma_idesc_tf32(H);
         const uint64_t b1hd = umma_desc(tc_s2u(b1h), 128, KB0 * 128), b1ld = umma_desc(tc_s2u(b1l), 128, KB0 * 128);
-        const uint64_t a0hd = umma_desc(tc_s2u(a1), 128, KB0 * 128);
-        for (int i = 0; i < ntile; ++i) {
-            const int sl = i & 1;
+        const int sl = warp - R::kMma1Warp;
+        const uint32_t dcol = tmem + kD + sl * H;
+        for (int i = sl; i < ntile; i += 2) {
             const uint32_t ph = (i >> 1) & 1;
             wait(0, bar(kA1Full + sl), ph);
-            wait(1, bar(kD1Empty + sl), ph ^ 1);
+            wait(1, bar(kDEmpty + sl), ph ^ 1);  // the final epilogue has drained tile i-2
             asm volatile("tcgen05.fence::after_thread_sync;");
-            const uint64_t ahd = a0hd + (uint64_t)((sl * 2 * A1B) >> 4), ald = ahd + (A1B >> 4);
-            const uint32_t dcol = tmem + kD1 + sl * H;
             if (lane == 0) {
+                if constexpr (kA1T) {
+                    const uint32_t ah = tmem + kA1 + sl * kA1S;
 #pragma unroll
-                for (int kk = 0; kk < W0 / 8; ++kk) {
-                    const uint64_t ko = (uint64_t)(kk * 16);  // 256 B per k-step, in 16-byte units
-                    umma_tf32(dcol, ahd + ko, b1hd + ko, id1, kk > 0);
-                    umma_tf32(dcol, ahd + ko, b1ld + ko, id1, 1);
-                    umma_tf32(dcol, ald + ko, b1hd + ko, id1, 1);
+                    for (int kk = 0; kk < W0 / 8; ++kk) {
+                        const uint64_t ko = (uint64_t)(kk * 16);  // 256 B per k-step, in 16-byte units
+                        umma_tf32_ta(dcol, ah + 8 * kk, b1hd + ko, id1, kk > 0);
+                        umma_tf32_ta(dcol, ah + 8 * kk, b1ld + ko, id1, 1);
+                        umma_tf32_ta(dcol, ah + W0 + 8 * kk, b1hd + ko, id1, 1);
+                    }
+                } else {
+                    const uint64_t ahd = umma_desc(tc_s2u(a1 + sl * 2 * A1B), 128, KB0 * 128);
+                    const uint64_t ald = ahd + (A1B >> 4);
+#pragma unroll
+                    for (int kk = 0; kk < W0 / 8; ++kk) {
+                        const uint64_t ko = (uint64_t)(kk * 16);
+                        umma_tf32(dcol, ahd + ko, b1hd + ko, id1, kk > 0);
+                        umma_tf32(dcol, ahd + ko, b1ld + ko, id1, 1);
+                        umma_tf32(dcol, ald + ko, b1hd + ko, id1, 1);
+                    }
                 }
                 umma_commit(bar(kM1Done + sl));
             }
             __syncwarp();
         }
-    } else if (NL > 1 && warp > R::kMma1Warp) {
-        // ---------------- layer-2 issuers: warp 13 even tiles, 14 odd tiles ------
+    } else if (NL > 1 && (warp == R::kMma2Warp || warp == R::kMma2Warp + 1)) {
+        // ---------------- layer-2 issuers: even / odd tiles, A from TMEM --------
         constexpr uint32_t id2 = umma_idesc_tf32(H);
         const uint64_t b2hd = umma_desc(tc_s2u(b2h), 128, KBH * 128), b2ld = umma_desc(tc_s2u(b2l), 128, KBH * 128);
-        const int sl = warp - R::kMma1Warp - 1;
-        const uint32_t a2 = tmem + kA2 + sl * kA2S, dcol = tmem + kD2 + sl * H;
+        const int sl = warp - R::kMma2Warp;
+        const uint32_t a2 = tmem + kA2 + sl * kA2S, dcol = tmem + kD + sl * H;
         for (int i = sl; i < ntile; i += 2) {
-            const uint32_t ph = (i >> 1) & 1;
-            wait(0, bar(kA2Full + sl), ph);
-            wait(1, bar(kD2Empty + sl), ph ^ 1);  // epilogue 2 has read tile i-2's D2
+            wait(0, bar(kA2Full + sl), (i >> 1) & 1);  // epilogue 1 has drained D[sl] and filled A2[sl]
             asm volatile("tcgen05.fence::after_thread_sync;");
             if (lane == 0) {
 #pragma unroll
@@ -576,20 +627,20 @@ int detect_tc_launch(const DetectParams &dp, cudaStream_t st) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         kern<<<dim3(ctas, p.n_nets), threads, smem, st>>>(p);
         if (cudaGetLastError() != cudaSuccess) return NOMA_ERR_CUDA;
-        if (clk) {  // roles: loader, epilogue 1, epilogue 2, L1 issuer, L2 issuers (even, odd)
-            long long h[36];
+        if (clk) {  // roles: loaders, epilogue 1, epilogue 2, L1 issuers (even, odd), L2 issuers (even, odd)
+            long long h[48];
             cudaMemcpyAsync(h, clk_buf, sizeof h, cudaMemcpyDeviceToHost, st);
             cudaStreamSynchronize(st);
             std::fprintf(stderr, "NOMA_DETECT_CLK tiles/CTA %d:", (p.tiles + ctas - 1) / ctas);
-            for (int i = 0; i < 36; ++i) std::fprintf(stderr, " %lld", h[i]);
+            for (int i = 0; i < 48; ++i) std::fprintf(stderr, " %lld", h[i]);
             std::fprintf(stderr, "\n");
         }
         return NOMA_OK;
     };
-    if (W0 == 32 && NL == 1) return launch(detect_ws_kernel<32, 64, 1>, detect_ws_smem<32, 64, 1>(), WsRoles<1>::kThreads);
-    if (W0 == 32 && NL == 2) return launch(detect_ws_kernel<32, 64, 2>, detect_ws_smem<32, 64, 2>(), WsRoles<2>::kThreads);
-    if (W0 == 64 && NL == 1) return launch(detect_ws_kernel<64, 64, 1>, detect_ws_smem<64, 64, 1>(), WsRoles<1>::kThreads);
-    return launch(detect_ws_kernel<64, 64, 2>, detect_ws_smem<64, 64, 2>(), WsRoles<2>::kThreads);
+    if (W0 == 32 && NL == 1) return launch(detect_ws_kernel<32, 64, 1>, detect_ws_smem<32, 64, 1>(), WsRoles<32, 1>::kThreads);
+    if (W0 == 32 && NL == 2) return launch(detect_ws_kernel<32, 64, 2>, detect_ws_smem<32, 64, 2>(), WsRoles<32, 2>::kThreads);
+    if (W0 == 64 && NL == 1) return launch(detect_ws_kernel<64, 64, 1>, detect_ws_smem<64, 64, 1>(), WsRoles<64, 1>::kThreads);
+    return launch(detect_ws_kernel<64, 64, 2>, detect_ws_smem<64, 64, 2>(), WsRoles<64, 2>::kThreads);
 }
 
 }  // namespace noma_dev
