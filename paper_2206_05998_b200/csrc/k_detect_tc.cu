@@ -606,14 +606,16 @@ int detect_tc_launch(const DetectParams &dp, cudaStream_t st) {
     p.errors = dp.errors;
     p.status = dp.status;
     p.clocks = nullptr;
-    static long long *clk_buf = nullptr;
-    const bool clk = std::getenv("NOMA_DETECT_CLK") != nullptr;
+    if (p.tiles == 0 || p.n_nets == 0) return NOMA_OK;
+    // NOMA_DETECT_CLK (diagnostics): per-role cycle counters, printed after a
+    // synchronising launch; the buffer lives for this call only
+    long long *clk_buf = nullptr;
+    const bool clk = std::getenv("NOMA_DETECT_CLK") != nullptr &&
+                     cudaMallocAsync(&clk_buf, 64 * sizeof(long long), st) == cudaSuccess;
     if (clk) {
-        if (!clk_buf) cudaMalloc(&clk_buf, 64 * sizeof(long long));
         cudaMemsetAsync(clk_buf, 0, 64 * sizeof(long long), st);
         p.clocks = clk_buf;
     }
-    if (p.tiles == 0 || p.n_nets == 0) return NOMA_OK;
     int sms = 148, dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -626,7 +628,7 @@ int detect_tc_launch(const DetectParams &dp, cudaStream_t st) {
         smem = smem < 116 * 1024 ? 116 * 1024 : smem;
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         kern<<<dim3(ctas, p.n_nets), threads, smem, st>>>(p);
-        if (cudaGetLastError() != cudaSuccess) return NOMA_ERR_CUDA;
+        const bool launched = cudaGetLastError() == cudaSuccess;
         if (clk) {  // roles: loaders, epilogue 1, epilogue 2, L1 issuers (even, odd), L2 issuers (even, odd)
             long long h[48];
             cudaMemcpyAsync(h, clk_buf, sizeof h, cudaMemcpyDeviceToHost, st);
@@ -634,8 +636,9 @@ int detect_tc_launch(const DetectParams &dp, cudaStream_t st) {
             std::fprintf(stderr, "NOMA_DETECT_CLK tiles/CTA %d:", (p.tiles + ctas - 1) / ctas);
             for (int i = 0; i < 48; ++i) std::fprintf(stderr, " %lld", h[i]);
             std::fprintf(stderr, "\n");
+            cudaFreeAsync(clk_buf, st);
         }
-        return NOMA_OK;
+        return launched ? NOMA_OK : NOMA_ERR_CUDA;
     };
     if (W0 == 32 && NL == 1) return launch(detect_ws_kernel<32, 64, 1>, detect_ws_smem<32, 64, 1>(), WsRoles<32, 1>::kThreads);
     if (W0 == 32 && NL == 2) return launch(detect_ws_kernel<32, 64, 2>, detect_ws_smem<32, 64, 2>(), WsRoles<32, 2>::kThreads);
