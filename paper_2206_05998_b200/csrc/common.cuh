@@ -15,6 +15,19 @@ constexpr int kFeatPad = 32;      // every feature dim padded to 32 on chip
 
 __host__ __device__ inline int pad_to(int w, int m) { return ((w + m - 1) / m) * m; }
 
+#ifdef __CUDACC__
+// Adam parameter step lr_t m / (sqrt(v / (1 - b2^t)) + eps) (hybrid_nn.cpp:133-139)
+// with the single-instruction approximate square root (MUFU.SQRT, ~1 ulp):
+// the IEEE sqrtf sequence cost ~8 instructions per parameter update, a
+// visible share of the training kernels; the difference is far below the
+// FP32 training's own rounding against the FP64 reference
+__device__ __forceinline__ float adam_step(float lr_m1, float m2_ic2, float eps) {
+    float r;
+    asm("sqrt.approx.f32 %0, %1;" : "=f"(r) : "f"(m2_ic2));
+    return __fdividef(lr_m1, r + eps);
+}
+#endif
+
 // ------------------------------------------------------------------ RNG
 // rng.hpp:10-62, bit-exact: splitmix64, substream_seed, xoshiro256++,
 // 53-bit uniform, multiply-shift below(), Box-Muller cosine half.

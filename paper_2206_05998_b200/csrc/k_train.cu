@@ -272,7 +272,7 @@ __global__ void __launch_bounds__(NT, MINB) train_kernel(TrainParams p) {
                         const float m2 = p.b2 * M2[i] + p.omb2 * (gi * gi);
                         M1[i] = m1;
                         M2[i] = m2;
-                        const float th = PS[i] - __fdividef(lrc * m1, sqrtf(m2 * ic2) + p.eps);
+                        const float th = PS[i] - adam_step(lrc * m1, m2 * ic2, p.eps);
 #pragma unroll
                         for (int q = 0; q < CS; ++q) psr[q][i] = th;
                     }
@@ -286,7 +286,7 @@ __global__ void __launch_bounds__(NT, MINB) train_kernel(TrainParams p) {
                             const float gi = p.gsplit > 1 ? GS[i] + GS[gstride + i] : GS[i];
                             mom1[s] = p.b1 * mom1[s] + p.omb1 * gi;
                             mom2[s] = p.b2 * mom2[s] + p.omb2 * (gi * gi);
-                            PS[i] -= __fdividef(lrc * mom1[s], sqrtf(mom2[s] * ic2) + p.eps);
+                            PS[i] -= adam_step(lrc * mom1[s], mom2[s] * ic2, p.eps);
                         }
                     }
                 } else {
@@ -297,7 +297,7 @@ __global__ void __launch_bounds__(NT, MINB) train_kernel(TrainParams p) {
                         const float m2 = p.b2 * M2[i] + p.omb2 * (gi * gi);
                         M1[i] = m1;
                         M2[i] = m2;
-                        PS[i] -= __fdividef(lrc * m1, sqrtf(m2 * ic2) + p.eps);
+                        PS[i] -= adam_step(lrc * m1, m2 * ic2, p.eps);
                     }
                 }
             }

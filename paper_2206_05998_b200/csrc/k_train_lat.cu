@@ -632,7 +632,7 @@ static_for<NL, 0, -1>([&](auto LC) {
                         const float m2 = p.b2 * vw[l][tw] + p.omb2 * (gsum * gsum);
                         mw[l][tw] = m1;
                         vw[l][tw] = m2;
-                        sm[pn + c.w[l] + off] = sm[po + c.w[l] + off] - __fdividef(lrc * m1, sqrtf(m2 * ic2) + p.eps);
+                        sm[pn + c.w[l] + off] = sm[po + c.w[l] + off] - adam_step(lrc * m1, m2 * ic2, p.eps);
                     }
                     // biases on the column-tile-0 warps, final weights (top layer)
                     // on the column-tile-1 warps: the extra reductions are spread
@@ -653,7 +653,7 @@ static_for<NL, 0, -1>([&](auto LC) {
                             const float m2 = p.b2 * vb[l] + p.omb2 * (gsum * gsum);
                             mb[l] = m1;
                             vb[l] = m2;
-                            sm[pn + off] = sm[po + off] - __fdividef(lrc * m1, sqrtf(m2 * ic2) + p.eps);
+                            sm[pn + off] = sm[po + off] - adam_step(lrc * m1, m2 * ic2, p.eps);
                         }
                     }
                 }
