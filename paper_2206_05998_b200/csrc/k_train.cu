@@ -290,13 +290,36 @@ __global__ void __launch_bounds__(NT, MINB) train_kernel(TrainParams p) {
                         }
                     }
                 } else {
-                    float *M1 = sm + p.off_mom, *M2 = M1 + gstride;
-                    for (int i = tid; i < g.ptotal; i += kTrainThreads) {
+                    // moments interleaved (m1, m2) per parameter; two parameters
+                    // per iteration: float2 gradients / parameters, float4
+                    // moments (the regions are 16-byte aligned, padded to 4)
+                    float *M12 = sm + p.off_mom;
+                    const int npair = g.ptotal >> 1;
+                    for (int t = tid; t < npair; t += kTrainThreads) {
+                        float2 gi = *reinterpret_cast<const float2 *>(GS + 2 * t);
+                        if (p.gsplit > 1) {
+                            const float2 g2 = *reinterpret_cast<const float2 *>(GS + gstride + 2 * t);
+                            gi.x += g2.x;
+                            gi.y += g2.y;
+                        }
+                        float4 m = *reinterpret_cast<const float4 *>(M12 + 4 * t);
+                        m.x = p.b1 * m.x + p.omb1 * gi.x;
+                        m.y = p.b2 * m.y + p.omb2 * (gi.x * gi.x);
+                        m.z = p.b1 * m.z + p.omb1 * gi.y;
+                        m.w = p.b2 * m.w + p.omb2 * (gi.y * gi.y);
+                        *reinterpret_cast<float4 *>(M12 + 4 * t) = m;
+                        float2 th = *reinterpret_cast<const float2 *>(PS + 2 * t);
+                        th.x -= adam_step(lrc * m.x, m.y * ic2, p.eps);
+                        th.y -= adam_step(lrc * m.z, m.w * ic2, p.eps);
+                        *reinterpret_cast<float2 *>(PS + 2 * t) = th;
+                    }
+                    if ((g.ptotal & 1) && tid == 0) {  // odd count: the last parameter
+                        const int i = g.ptotal - 1;
                         const float gi = p.gsplit > 1 ? GS[i] + GS[gstride + i] : GS[i];
-                        const float m1 = p.b1 * M1[i] + p.omb1 * gi;
-                        const float m2 = p.b2 * M2[i] + p.omb2 * (gi * gi);
-                        M1[i] = m1;
-                        M2[i] = m2;
+                        const float m1 = p.b1 * M12[2 * i] + p.omb1 * gi;
+                        const float m2 = p.b2 * M12[2 * i + 1] + p.omb2 * (gi * gi);
+                        M12[2 * i] = m1;
+                        M12[2 * i + 1] = m2;
                         PS[i] -= adam_step(lrc * m1, m2 * ic2, p.eps);
                     }
                 }
