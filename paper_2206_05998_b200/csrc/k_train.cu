@@ -192,18 +192,30 @@ __global__ void __launch_bounds__(NT, MINB) train_kernel(TrainParams p) {
             NOMA_PHASE(2)
             // ---- final layer gradient and dZ_N (hybrid_nn.cpp:99-107) --------
             {
+                // item (j, part): neuron j, rows 4 part + 32 c + e (c, e < 4) as
+                // four float4 chunks -- a quarter-warp reads 128 contiguous
+                // bytes (conflict-free), the 16 values stay in registers for
+                // both the gradient sum and dZ_N
                 const float *wf = PS + g.pf;
                 for (int it = tid; it < fpN * 8; it += kTrainThreads) {  // fpN*8 % 256 == 0
                     const int j = it >> 3, part = it & 7;
-                    float *row = AN + j * kSR + part;  // rows r = part + 8 q
-                    const float *dyp = dy + part;
-                    float s0 = 0.f, s1 = 0.f;
+                    float4 *row = reinterpret_cast<float4 *>(AN + j * kSR + 4 * part);
+                    const float4 *dyp = reinterpret_cast<const float4 *>(dy + 4 * part);
+                    float4 a[4], y[4];
 #pragma unroll
-                    for (int q = 0; q < 16; q += 2) {
-                        s0 = fmaf(row[8 * q], dyp[8 * q], s0);
-                        s1 = fmaf(row[8 * q + 8], dyp[8 * q + 8], s1);
+                    for (int c = 0; c < 4; ++c) {
+                        a[c] = row[8 * c];
+                        y[c] = dyp[8 * c];
                     }
-                    float s = s0 + s1;
+                    float s4[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) {
+                        s4[0] = fmaf(a[c].x, y[c].x, s4[0]);
+                        s4[1] = fmaf(a[c].y, y[c].y, s4[1]);
+                        s4[2] = fmaf(a[c].z, y[c].z, s4[2]);
+                        s4[3] = fmaf(a[c].w, y[c].w, s4[3]);
+                    }
+                    float s = (s4[0] + s4[1]) + (s4[2] + s4[3]);
                     s += __shfl_xor_sync(0xffffffffu, s, 1);
                     s += __shfl_xor_sync(0xffffffffu, s, 2);
                     s += __shfl_xor_sync(0xffffffffu, s, 4);
@@ -211,8 +223,9 @@ __global__ void __launch_bounds__(NT, MINB) train_kernel(TrainParams p) {
                     if (N) {
                         const float wj = wf[j];
 #pragma unroll
-                        for (int q = 0; q < 16; ++q)
-                            row[8 * q] = row[8 * q] > 0.0f ? dyp[8 * q] * wj : 0.0f;
+                        for (int c = 0; c < 4; ++c)
+                            row[8 * c] = make_float4(a[c].x > 0.0f ? y[c].x * wj : 0.0f, a[c].y > 0.0f ? y[c].y * wj : 0.0f,
+                                                     a[c].z > 0.0f ? y[c].z * wj : 0.0f, a[c].w > 0.0f ? y[c].w * wj : 0.0f);
                     }
                 }
             }
