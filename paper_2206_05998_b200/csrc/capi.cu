@@ -261,6 +261,7 @@ void fill_train(TrainParams &tp, const NetGeom &g, const noma_train_cfg *cfg) {
     tp.clocks = nullptr;
     tp.mode = 0;
     tp.xprep = tp.r0prep = nullptr;
+    tp.atab = nullptr;
     tp.prep_floats = 0;
     tp.epochs = cfg->epochs;
     tp.batch = cfg->batch_size;

@@ -150,11 +150,16 @@ __global__ void __launch_bounds__(NT, MINB) train_kernel(TrainParams p) {
                     if (h == 0) r0b[r] = 0.0f;
                     for (int c = h; c < width; c += TPR) XT[c * kSR + r] = 0.0f;
                 }
-                if (tid == kTrainThreads - 1) {  // Adam constants for this step (FP64 pow)
-                    const double c1 = 1.0 - pow(p.b1d, (double)(step + 1));
-                    const double c2 = 1.0 - pow(p.b2d, (double)(step + 1));
-                    misc[0] = (float)(p.lr_d / c1);
-                    misc[1] = (float)(1.0 / c2);
+                if (tid == kTrainThreads - 1) {  // Adam constants for this step
+                    if (p.atab) {  // precomputed (adam_table_kernel)
+                        misc[0] = p.atab[2 * step];
+                        misc[1] = p.atab[2 * step + 1];
+                    } else {       // FP64 pow, hybrid_nn.cpp:133-135
+                        const double c1 = 1.0 - pow(p.b1d, (double)(step + 1));
+                        const double c2 = 1.0 - pow(p.b2d, (double)(step + 1));
+                        misc[0] = (float)(p.lr_d / c1);
+                        misc[1] = (float)(1.0 / c2);
+                    }
                 }
             }
             __syncthreads();
@@ -382,6 +387,21 @@ __global__ void __launch_bounds__(NT, MINB) train_kernel(TrainParams p) {
 }
 
 // host: carve shared memory, pick the moment-slot instantiation, launch.
+int train_thr_launch(TrainParams &p, cudaStream_t st, size_t smem, int mom_smem, int need);
+
+// Adam bias-correction constants of every step, FP64 pow as hybrid_nn.cpp:133-135:
+// one FP64 pow pair per step in the training kernel sat on the minibatch
+// gather's barrier (a long dependent FP64 chain on one thread)
+__global__ void adam_table_kernel(double lr, double b1, double b2, int total, float *t) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < total) {
+        const double c1 = 1.0 - pow(b1, (double)(i + 1));
+        const double c2 = 1.0 - pow(b2, (double)(i + 1));
+        t[2 * i] = (float)(lr / c1);
+        t[2 * i + 1] = (float)(1.0 / c2);
+    }
+}
+
 int train_launch(TrainParams &p, cudaStream_t st) {
     const NetGeom &g = p.g;
     for (int l = 0; l < g.nd; ++l)
@@ -447,6 +467,24 @@ int train_launch(TrainParams &p, cudaStream_t st) {
             if (train_lat_launch(p, st) == NOMA_OK) return NOMA_OK;
         }
     }
+    // throughput kernels: per-step Adam constants precomputed once per launch
+    float *tab = nullptr;
+    const int total = p.epochs * ((p.rows + p.batch - 1) / p.batch);
+    if (total > 0 && cudaMallocAsync(&tab, 2 * (size_t)total * sizeof(float), st) == cudaSuccess) {
+        adam_table_kernel<<<(total + 255) / 256, 256, 0, st>>>(p.lr_d, p.b1d, p.b2d, total, tab);
+        if (cudaGetLastError() == cudaSuccess) p.atab = tab;
+    } else {
+        cudaGetLastError();
+        tab = nullptr;
+    }
+    const int r = train_thr_launch(p, st, smem, mom_smem, need);
+    if (tab) cudaFreeAsync(tab, st);
+    p.atab = nullptr;
+    return r;
+}
+
+// the throughput kernels (row-split cluster or one CTA per net)
+int train_thr_launch(TrainParams &p, cudaStream_t st, size_t smem, int mom_smem, int need) {
     // row-split cluster: fewer nets than SMs -> a cluster of CS CTAs per net
     int sms = 148;
     {
