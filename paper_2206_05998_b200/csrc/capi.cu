@@ -123,6 +123,7 @@ struct noma_ctx_s {
     cudaStream_t side2 = nullptr;         // shuffles overlap the LLS and the init
     cudaEvent_t fork = nullptr, join = nullptr, join2 = nullptr;
     cudaEvent_t ev_perm0 = nullptr;       // profiling: shuffle start on side2
+    cudaEvent_t join3 = nullptr;          // LLS condition numbers (side2, joined at the end)
 };
 
 namespace {
@@ -246,6 +247,7 @@ LlsParams lls_params(const noma_dataset *ds, const double *x, const double *y, d
     p.design32 = d32;
     p.r0 = r0;
     p.clocks = nullptr;
+    p.mode = 0;
     return p;
 }
 
@@ -314,6 +316,7 @@ NOMA_API int noma_ctx_create(int device, noma_ctx_t *out) {
         cudaEventCreateWithFlags(&c->fork, cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&c->join, cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&c->join2, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&c->join3, cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreate(&c->ev_perm0) != cudaSuccess) {
         delete c;
         return NOMA_ERR_CUDA;
@@ -336,6 +339,7 @@ NOMA_API int noma_ctx_destroy(noma_ctx_t c) {
     if (c->side) cudaStreamSynchronize(c->side), cudaStreamDestroy(c->side);
     if (c->side2) cudaStreamSynchronize(c->side2), cudaStreamDestroy(c->side2);
     if (c->join2) cudaEventDestroy(c->join2);
+    if (c->join3) cudaEventDestroy(c->join3);
     if (c->ev_perm0) cudaEventDestroy(c->ev_perm0);
     if (c->fork) cudaEventDestroy(c->fork);
     if (c->join) cudaEventDestroy(c->join);
@@ -750,7 +754,12 @@ NOMA_API int noma_pipeline(noma_ctx_t c, const noma_net_desc *desc, const noma_t
     if (perm_launch((int)nets, cfg->epochs, n, sseed, perm, c->side2)) return cuda_fail(c, "perm");
     mark(c, 4, c->side2);
     cudaEventRecord(c->join2, c->side2);
+    // critical path: Gram + Cholesky solve (Jacobi only for slots whose
+    // Cholesky pivots fall near the rank threshold); the condition numbers
+    // of the other slots come from a Jacobi launch on side2 that overlaps
+    // training and joins before the outputs
     LlsParams lp = lls_params(&ds, px, py, dw, dc, dst, d32, r0);
+    lp.mode = 1;
     const bool lclk = std::getenv("NOMA_PHASE_CLOCKS") != nullptr;
     if (lclk) {
         lp.clocks = s.scratch<long long>(8);
@@ -765,6 +774,13 @@ NOMA_API int noma_pipeline(noma_ctx_t c, const noma_net_desc *desc, const noma_t
                      h[0], h[1], h[2], h[3], h[4], h[5]);
     }
     if (st) return st == NOMA_ERR_CUDA ? cuda_fail(c, "lls") : fail(c, st, "lls: unsupported shape");
+    const bool cond_side = dc != nullptr;
+    if (cond_side) {
+        LlsParams lc = lls_params(&ds, px, py, nullptr, dc, nullptr, nullptr, nullptr);
+        lc.mode = 2;
+        if (lls_launch(lc, c->side2)) return cuda_fail(c, "lls condition");
+        cudaEventRecord(c->join3, c->side2);
+    }
     mark(c, 1);
     cudaStreamWaitEvent(c->stream, c->join, 0);
     cudaStreamWaitEvent(c->stream, c->join2, 0);
@@ -832,6 +848,7 @@ NOMA_API int noma_pipeline(noma_ctx_t c, const noma_net_desc *desc, const noma_t
         if (st) return st == NOMA_ERR_CUDA ? cuda_fail(c, "detect") : fail(c, st, "detect: unsupported network shape");
         c->launches += 1;
     }
+    if (cond_side) cudaStreamWaitEvent(c->stream, c->join3, 0);
     mark(c, 7);
     return s.finish();
 }

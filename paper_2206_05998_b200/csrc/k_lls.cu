@@ -69,6 +69,7 @@ __global__ void __launch_bounds__(kThreads) lls_kernel(LlsParams p) {
     __shared__ int pair_p[kLlsMaxM / 2 + 1], pair_q[kLlsMaxM / 2 + 1];
     __shared__ int any_rot[2];    // by sweep parity; reset one sweep ahead
     __shared__ int round_rot[2];  // by round parity: some pair rotates
+    __shared__ int chol_ok;       // fast path: every Cholesky pivot above the floor
 
     // Staging of CH rows of the design and the targets into buffer b with
     // cp.async (row-major complex rows are contiguous; REAL rows fill the Re
@@ -262,6 +263,100 @@ __global__ void __launch_bounds__(kThreads) lls_kernel(LlsParams p) {
     __syncthreads();
     NOMA_LLS_CLK(1)
 
+    // ---- fast path (mode 1): Cholesky of the Hermitian Gram C = L L^H in the
+    // idle staging buffer, then L y = d, L^H c = y for every user in place.
+    // A pivot below 1e-10 ||C||_F -- far above the rank threshold of phase C --
+    // sends the slot down the Jacobi path instead, so the rank / status
+    // decisions are those of the Jacobi path; the full-rank solution agrees
+    // with the pseudo-inverse one to rounding.  The condition number is left
+    // to a mode-2 launch (off the critical path).
+    bool fast = false;
+    if (p.mode == 1 && 2 * m * m <= 2 * bstride) {
+        double *L = bufs;  // m x m complex, lower triangle used
+        for (int i = tid; i < m * m; i += kThreads) {
+            L[2 * i] = A[2 * i];
+            L[2 * i + 1] = A[2 * i + 1];
+        }
+        if (tid == 0) chol_ok = 1;
+        const double floor_piv = 1e-10 * sqrt(red[0]);
+        __syncthreads();
+        for (int k = 0; k < m; ++k) {
+            const double dkk = L[2 * (k * m + k)];
+            if (!(dkk > floor_piv)) {  // uniform: every thread read the same pivot
+                if (tid == 0) chol_ok = 0;
+                break;
+            }
+            const double lkk = sqrt(dkk), il = 1.0 / lkk;
+            __syncthreads();
+            for (int i = k + 1 + tid; i < m; i += kThreads) {
+                L[2 * (i * m + k)] *= il;
+                L[2 * (i * m + k) + 1] *= il;
+            }
+            if (tid == 0) L[2 * (k * m + k)] = lkk;
+            __syncthreads();
+            const int nt = m - k - 1;  // trailing update C[i][j] -= L[i][k] conj(L[j][k])
+            for (int t = tid; t < nt * nt; t += kThreads) {
+                const int i = k + 1 + t / nt, j = k + 1 + t % nt;
+                if (j <= i) {
+                    const double ar = L[2 * (i * m + k)], ai = L[2 * (i * m + k) + 1];
+                    const double br = L[2 * (j * m + k)], bi = L[2 * (j * m + k) + 1];
+                    L[2 * (i * m + j)] -= ar * br + ai * bi;
+                    L[2 * (i * m + j) + 1] -= ai * br - ar * bi;
+                }
+            }
+            __syncthreads();
+        }
+        __syncthreads();
+        fast = chol_ok != 0;
+        if (fast) {
+            for (int j = 0; j < m; ++j) {  // forward: L y = d
+                const double ij = 1.0 / L[2 * (j * m + j)];
+                for (int k = tid; k < K; k += kThreads) {
+                    D[2 * (j * K + k)] *= ij;
+                    D[2 * (j * K + k) + 1] *= ij;
+                }
+                __syncthreads();
+                for (int t = tid; t < (m - j - 1) * K; t += kThreads) {
+                    const int i = j + 1 + t / K, k = t % K;
+                    const double lr = L[2 * (i * m + j)], li = L[2 * (i * m + j) + 1];
+                    const double yr = D[2 * (j * K + k)], yi = D[2 * (j * K + k) + 1];
+                    D[2 * (i * K + k)] -= lr * yr - li * yi;
+                    D[2 * (i * K + k) + 1] -= lr * yi + li * yr;
+                }
+                __syncthreads();
+            }
+            for (int j = m - 1; j >= 0; --j) {  // backward: L^H c = y
+                const double ij = 1.0 / L[2 * (j * m + j)];
+                for (int k = tid; k < K; k += kThreads) {
+                    D[2 * (j * K + k)] *= ij;
+                    D[2 * (j * K + k) + 1] *= ij;
+                }
+                __syncthreads();
+                for (int t = tid; t < j * K; t += kThreads) {
+                    const int i = t / K, k = t % K;  // c_i -= conj(L[j][i]) c_j
+                    const double lr = L[2 * (j * m + i)], li = -L[2 * (j * m + i) + 1];
+                    const double cr = D[2 * (j * K + k)], ci = D[2 * (j * K + k) + 1];
+                    D[2 * (i * K + k)] -= lr * cr - li * ci;
+                    D[2 * (i * K + k) + 1] -= lr * ci + li * cr;
+                }
+                __syncthreads();
+            }
+            for (int it = tid; it < m * K; it += kThreads) {  // w0, as phase C
+                const int a = it / K, k = it % K;
+                double *w = p.w0 + ((size_t)d * K + k) * p.width;
+                if (cplx_layout) {
+                    w[a] = D[2 * it];
+                    w[m + a] = -D[2 * it + 1];
+                } else {
+                    w[a] = D[2 * it];
+                }
+            }
+            __syncthreads();
+        }
+    }
+    double lmax = 0.0, lmin = INFINITY, lkeep = INFINITY;
+    int rank = m;
+    if (!fast) {
     // ---- phase B: cyclic Jacobi, round-robin pairs (circle method); each
     // round applies A <- U^H A U as independent 2x2 blocks (in place) and
     // V <- V U, two barriers per round.
@@ -386,20 +481,24 @@ __global__ void __launch_bounds__(kThreads) lls_kernel(LlsParams p) {
     // ---- phase C: eigenvalues, rank, pseudo-inverse solve.
     for (int i = tid; i < m; i += kThreads) lam[i] = A[2 * (i * m + i)];
     __syncthreads();
-    double lmax = 0.0, lmin = INFINITY;
     for (int i = 0; i < m; ++i) {
         lmax = fmax(lmax, lam[i]);
         lmin = fmin(lmin, lam[i]);
     }
     const int big = p.rows > p.width ? p.rows : p.width;
     const double tol = lmax * 16.0 * DBL_EPSILON * (double)big;
-    int rank = 0;
-    double lkeep = INFINITY;
+    rank = 0;
     for (int i = 0; i < m; ++i)
         if (lam[i] > tol) {
             ++rank;
             lkeep = fmin(lkeep, lam[i]);
         }
+    if (p.mode == 2) {  // condition numbers only: full-rank nets (the others get
+                        // theirs from the solving launch, which takes this path)
+        if (rank == m && p.cond)
+            for (int k = tid; k < K; k += kThreads) p.cond[(size_t)d * K + k] = lmax / lmin;
+        return;
+    }
     // U[i][k] = (V_i^H d_k) / lambda_i for kept i, else 0
     for (int it = tid; it < m * K; it += kThreads) {
         const int i = it / K, k = it % K;
@@ -439,6 +538,7 @@ __global__ void __launch_bounds__(kThreads) lls_kernel(LlsParams p) {
         }
     }
     __syncthreads();
+    }  // !fast
     NOMA_LLS_CLK(3)
 
     // ---- phase D: residuals r0 = y - X w0 (FP64) and norms: thread per row
@@ -527,7 +627,7 @@ __global__ void __launch_bounds__(kThreads) lls_kernel(LlsParams p) {
                 st = NOMA_ERR_ILL_CONDITIONED;
                 cond = lmin > 0.0 ? lmax / lmin : INFINITY;
             }
-            if (p.cond) p.cond[net] = cond;
+            if (p.cond && !fast) p.cond[net] = cond;
             if (p.status) p.status[net] = st;
         }
         __syncthreads();

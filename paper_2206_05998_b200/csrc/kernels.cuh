@@ -17,6 +17,8 @@ struct LlsParams {
     float *design32;      // nullable: FP32 copy for training, [S][nrow_c][width]
     float *r0;            // nullable: [net][rows]
     long long *clocks;    // nullable: phase cycles of block 0 (NOMA_PHASE_CLOCKS)
+    int mode;             // 0: Jacobi path; 1: Cholesky fast path (Jacobi fallback), no
+                          // cond for fast-path nets; 2: condition numbers only
 };
 
 struct TrainParams {
