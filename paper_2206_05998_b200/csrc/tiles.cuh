@@ -366,10 +366,15 @@ __device__ __forceinline__ void tile_weight_grad44(const float *__restrict__ dz,
     const int jg = lane & 7, cg = lane >> 3;
     const int ncb = C >> 4;
     const int ntile = (J >> 5) * ncb;
-    const int rows_per_split = R / splits;
+    // task -> (tile, split) and tile -> (jb, cb) by shifts when the counts are
+    // powers of two (splits is 1 or 2; ncb = C / 16), which they are for every
+    // padded width here; integer division per task cost ~3 % of the kernel
+    const bool pow2 = (ncb & (ncb - 1)) == 0 && (splits & (splits - 1)) == 0;
+    const int ss = __ffs(splits) - 1, cs = __ffs(ncb) - 1;
+    const int rows_per_split = pow2 ? R >> ss : R / splits;
     for (int task = warp; task < ntile * splits; task += NW) {
-        const int wt = task / splits, sp = task % splits;
-        const int jb = wt / ncb, cb = wt % ncb;
+        const int wt = pow2 ? task >> ss : task / splits, sp = pow2 ? task & (splits - 1) : task % splits;
+        const int jb = pow2 ? wt >> cs : wt / ncb, cb = pow2 ? wt & (ncb - 1) : wt % ncb;
         const int j0 = jb * 32 + jg, c0 = cb * 16 + cg;
         const int rb = sp * rows_per_split, re = rb + rows_per_split;
         f2_t acc[4][4], sb[4];
