@@ -181,10 +181,13 @@ __device__ __forceinline__ void tile_weight_grad(const float *__restrict__ dz,
     const int cl = lane & 7, jg = lane >> 3;
     const int ncb = C >> 5;
     const int ntile = (J >> 5) * ncb;
-    const int rows_per_split = kBatchRows / splits;
+    // shifts instead of per-task integer division (powers of two here)
+    const bool pow2 = (ncb & (ncb - 1)) == 0 && (splits & (splits - 1)) == 0;
+    const int ss = __ffs(splits) - 1, cs = __ffs(ncb) - 1;
+    const int rows_per_split = pow2 ? kBatchRows >> ss : kBatchRows / splits;
     for (int task = warp; task < ntile * splits; task += NW) {
-        const int wt = task / splits, sp = task % splits;
-        const int jb = wt / ncb, cb = wt % ncb;
+        const int wt = pow2 ? task >> ss : task / splits, sp = pow2 ? task & (splits - 1) : task % splits;
+        const int jb = pow2 ? wt >> cs : wt / ncb, cb = pow2 ? wt & (ncb - 1) : wt % ncb;
         const int j0 = jb * 32 + jg, c0 = cb * 32 + cl;
         const int rb = sp * rows_per_split, re = rb + rows_per_split;
         f2_t acc[8][4], sb[8];
@@ -261,12 +264,14 @@ __device__ __forceinline__ void tile_forward44(const float *__restrict__ W, int 
                                                float *__restrict__ yp = nullptr,
                                                int R = kBatchRows) {
     const int rg = lane & 7, jg = lane >> 3;
-    const int nrb = R >> 5;  // 32-row blocks (R % 32 == 0)
+    const int nrb = R >> 5;  // 32-row blocks (R % 32 == 0): 1, 2 or 4
     const int ntile = (J >> 4) * nrb;
+    const bool pow2 = (nrb & (nrb - 1)) == 0;
+    const int rs = __ffs(nrb) - 1;
     for (int wt = warp; wt < ntile; wt += NW) {
-        const int jb = wt / nrb;
+        const int jb = pow2 ? wt >> rs : wt / nrb;
         const int j0 = jb * 16 + jg;
-        const int r0 = (wt % nrb) * 32 + 4 * rg;
+        const int r0 = (pow2 ? wt & (nrb - 1) : wt % nrb) * 32 + 4 * rg;
         f2_t acc[4][2];
 #pragma unroll
         for (int i = 0; i < 4; ++i) acc[i][0] = acc[i][1] = f2_bcast(bias[j0 + 4 * i]);
@@ -323,9 +328,11 @@ __device__ __forceinline__ void tile_backward_data44(const float *__restrict__ W
     const int rg = lane & 7, cg = lane >> 3;
     const int nrb = R >> 5;
     const int ntile = (C >> 4) * nrb;
+    const bool pow2 = (nrb & (nrb - 1)) == 0;
+    const int rs = __ffs(nrb) - 1;
     for (int wt = warp; wt < ntile; wt += NW) {
-        const int c0 = (wt / nrb) * 16 + 4 * cg;
-        const int r0 = (wt % nrb) * 32 + 4 * rg;
+        const int c0 = (pow2 ? wt >> rs : wt / nrb) * 16 + 4 * cg;
+        const int r0 = (pow2 ? wt & (nrb - 1) : wt % nrb) * 32 + 4 * rg;
         f2_t acc[4][2];
 #pragma unroll
         for (int i = 0; i < 4; ++i) acc[i][0] = acc[i][1] = 0ull;
