@@ -226,11 +226,29 @@ __global__ void __launch_bounds__(NT, MINB) train_kernel(TrainParams p) {
                     s += __shfl_xor_sync(0xffffffffu, s, 4);
                     if (part == 0) GS[g.pf + j] = s;
                     if (N) {
+                        // dZ_N, and its row sum = the top layer's bias gradient
+                        // (:110; the top layer's weight-gradient tiles skip it,
+                        // which evens their per-warp work)
                         const float wj = wf[j];
+                        float b4[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-                        for (int c = 0; c < 4; ++c)
-                            row[8 * c] = make_float4(a[c].x > 0.0f ? y[c].x * wj : 0.0f, a[c].y > 0.0f ? y[c].y * wj : 0.0f,
-                                                     a[c].z > 0.0f ? y[c].z * wj : 0.0f, a[c].w > 0.0f ? y[c].w * wj : 0.0f);
+                        for (int c = 0; c < 4; ++c) {
+                            const float4 z = make_float4(a[c].x > 0.0f ? y[c].x * wj : 0.0f, a[c].y > 0.0f ? y[c].y * wj : 0.0f,
+                                                         a[c].z > 0.0f ? y[c].z * wj : 0.0f, a[c].w > 0.0f ? y[c].w * wj : 0.0f);
+                            row[8 * c] = z;
+                            b4[0] += z.x;
+                            b4[1] += z.y;
+                            b4[2] += z.z;
+                            b4[3] += z.w;
+                        }
+                        float b = (b4[0] + b4[1]) + (b4[2] + b4[3]);
+                        b += __shfl_xor_sync(0xffffffffu, b, 1);
+                        b += __shfl_xor_sync(0xffffffffu, b, 2);
+                        b += __shfl_xor_sync(0xffffffffu, b, 4);
+                        if (part == 0) {
+                            GS[g.pb[N] + j] = b;
+                            if (p.gsplit > 1) GS[gstride + g.pb[N] + j] = 0.0f;
+                        }
                     }
                 }
             }
@@ -243,11 +261,11 @@ __global__ void __launch_bounds__(NT, MINB) train_kernel(TrainParams p) {
                 if constexpr (NT == 512)
                     tile_weight_grad44<kTrainWarps>(sm + p.off_a[l], ain, GS + g.pw[l], g.sw[l],
                                                     GS + g.pb[l], g.fp[l], g.fp[l - 1], splits,
-                                                    gstride, warp, lane, RB);
+                                                    gstride, warp, lane, RB, l != N);
                 else
                     tile_weight_grad<kTrainWarps>(sm + p.off_a[l], ain, GS + g.pw[l], g.sw[l],
                                                   GS + g.pb[l], g.fp[l], g.fp[l - 1], splits,
-                                                  gstride, warp, lane);
+                                                  gstride, warp, lane, l != N);
                 __syncthreads();
                 if (l > 1) {
                     if constexpr (NT == 512)

@@ -177,7 +177,7 @@ __device__ __forceinline__ void tile_weight_grad(const float *__restrict__ dz,
                                                  float *__restrict__ gW, int sw,
                                                  float *__restrict__ gb, int J, int C,
                                                  int splits, int split_stride, int warp,
-                                                 int lane) {
+                                                 int lane, bool bias = true) {
     const int cl = lane & 7, jg = lane >> 3;
     const int ncb = C >> 5;
     const int ntile = (J >> 5) * ncb;
@@ -217,7 +217,7 @@ __device__ __forceinline__ void tile_weight_grad(const float *__restrict__ dz,
                 for (int i = 0; i < 4; ++i)
 #pragma unroll
                     for (int q = 0; q < 4; ++q) f2_fma(acc[ih + i][q], z[i].y, x[q].y);
-                if (cb == 0) {  // warp-uniform: bias gradient from the same loads
+                if (bias && cb == 0) {  // warp-uniform: bias gradient from the same loads
 #pragma unroll
                     for (int i = 0; i < 4; ++i) f2_fma(sb[ih + i], z[i].x, one);
 #pragma unroll
@@ -233,7 +233,7 @@ __device__ __forceinline__ void tile_weight_grad(const float *__restrict__ dz,
                 const float2 v = f2_unpack(acc[i][q]);
                 gWs[(j0 + 4 * i) * sw + c0 + 8 * q] = v.x + v.y;
             }
-        if (cb == 0 && cl == 0) {
+        if (bias && cb == 0 && cl == 0) {
             float *gbs = gb + sp * split_stride;
 #pragma unroll
             for (int i = 0; i < 8; ++i) {
@@ -369,7 +369,7 @@ __device__ __forceinline__ void tile_weight_grad44(const float *__restrict__ dz,
                                                    float *__restrict__ gW, int sw,
                                                    float *__restrict__ gb, int J, int C,
                                                    int splits, int split_stride, int warp,
-                                                   int lane, int R = kBatchRows) {
+                                                   int lane, int R = kBatchRows, bool bias = true) {
     const int jg = lane & 7, cg = lane >> 3;
     const int ncb = C >> 4;
     const int ntile = (J >> 5) * ncb;
@@ -407,7 +407,7 @@ __device__ __forceinline__ void tile_weight_grad44(const float *__restrict__ dz,
             for (int i = 0; i < 4; ++i)
 #pragma unroll
                 for (int q = 0; q < 4; ++q) f2_fma(acc[i][q], z[i].y, x[q].y);
-            if (cb == 0) {
+            if (bias && cb == 0) {
 #pragma unroll
                 for (int i = 0; i < 4; ++i) f2_fma(sb[i], z[i].x, one);
 #pragma unroll
@@ -422,7 +422,7 @@ __device__ __forceinline__ void tile_weight_grad44(const float *__restrict__ dz,
                 const float2 v = f2_unpack(acc[i][q]);
                 gWs[(j0 + 8 * i) * sw + c0 + 4 * q] = v.x + v.y;
             }
-        if (cb == 0 && cg == 0) {
+        if (bias && cb == 0 && cg == 0) {
             float *gbs = gb + sp * split_stride;
 #pragma unroll
             for (int i = 0; i < 4; ++i) {
