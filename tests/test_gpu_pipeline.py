@@ -61,6 +61,31 @@ def test_pipeline_matches_oracle(A, O, M, K, hidden, snr, epochs, S):
     assert trace_dev <= (1e-4 if epochs <= 5 else 1e-1), trace_dev
 
 
+def test_pipeline_lls_paths_match_lls_fit(A, O):
+    # The pipeline's LLS solves by Cholesky (Jacobi fallback for slots whose
+    # pivots approach the rank threshold) and takes the condition numbers
+    # from a Jacobi-only launch overlapping training; noma_lls_fit runs the
+    # Jacobi path throughout.  Same slots -> same status, bitwise-equal
+    # condition numbers, w0 within 1e-10 relative (test_lls.cpp:40).
+    rng = np.random.default_rng(11)
+    S, NT, M, K, ND = 4, 96, 4, 3, 32
+    x = rng.normal(size=(S, NT, M)) + 1j * rng.normal(size=(S, NT, M))
+    x[1] *= np.array([1.0, 0.1, 0.03, 1.0])           # near-far columns: larger condition
+    x[2, :, 3] = x[2, :, 0]                            # exactly rank deficient (Jacobi fallback) ...
+    c = rng.normal(size=(S, M, K)) + 1j * rng.normal(size=(S, M, K))
+    y = np.einsum("stm,smk->stk", x, c)                # ... but consistent: min-norm, status OK
+    y[[0, 1, 3]] += 0.01 * (rng.normal(size=(3, NT, K)) + 1j * rng.normal(size=(3, NT, K)))
+    init, shuf = _seeds(O, [1, 2, 3, 4], K)
+    out = A.pipeline([2 * M, 8], x, y, np.zeros((S, ND, M), np.complex64),
+                     np.zeros((S, ND, K), np.uint8), init, shuf, epochs=0)
+    w0, cond, status = A.lls_fit_slots(x, y)
+    assert np.array_equal(out.status, status) and (status == 0).all()
+    assert np.array_equal(out.gram_condition, cond)
+    assert cond[1].min() > 10 * cond[0].max()          # the near-far slot is the worse conditioned
+    werr = np.abs(out.w0 - w0).max(axis=-1) / np.abs(w0).max(axis=-1)
+    assert werr.max() <= 1e-10, werr
+
+
 def test_ill_conditioned_slot_is_flagged(A, O):
     # duplicate antennas -> rank-deficient complex design; random targets are
     # inconsistent -> status ILL for every user, no training for them.
