@@ -293,6 +293,8 @@ __global__ void __launch_bounds__(WsRoles<W0, NL>::kThreads, 1) detect_ws_kernel
         }
         asm volatile("fence.mbarrier_init.release.cluster;");
     }
+    // the weight planes are read by the tensor core (async proxy)
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     asm volatile("tcgen05.fence::before_thread_sync;");
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;");
