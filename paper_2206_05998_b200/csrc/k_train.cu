@@ -258,11 +258,33 @@ __global__ void __launch_bounds__(NT, MINB) train_kernel(TrainParams p) {
             for (int l = N; l >= 1; --l) {
                 const float *ain = l == 1 ? XT : sm + p.off_a[l - 1];
                 const int splits = grad_splits<NT>(g.fp[l], g.fp[l - 1], p.gsplit);
-                if constexpr (NT == 512)
+                if constexpr (NT == 512) {
+                    // fewer tasks than warps (C2's first layer: 8 for 16): the idle
+                    // warps sum the bias gradient (row sums of dZ_l, :110), so the
+                    // tile tasks carry no bias work and finish together
+                    const int ntask = (g.fp[l] >> 5) * (g.fp[l - 1] >> 4) * splits;
+                    const bool idle_bias = l != N && ntask < kTrainWarps;
                     tile_weight_grad44<kTrainWarps>(sm + p.off_a[l], ain, GS + g.pw[l], g.sw[l],
                                                     GS + g.pb[l], g.fp[l], g.fp[l - 1], splits,
-                                                    gstride, warp, lane, RB, l != N);
-                else
+                                                    gstride, warp, lane, RB, l != N && !idle_bias);
+                    if (idle_bias && warp >= ntask) {
+                        const int nth = (kTrainWarps - ntask) * 32, t0 = tid - ntask * 32;
+                        const float *dzl = sm + p.off_a[l];
+                        for (int j = t0; j < g.fp[l]; j += nth) {
+                            float4 s4 = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll 4
+                            for (int r = 0; r < RB; r += 4) {
+                                const float4 z = *reinterpret_cast<const float4 *>(dzl + j * kSR + r);
+                                s4.x += z.x;
+                                s4.y += z.y;
+                                s4.z += z.z;
+                                s4.w += z.w;
+                            }
+                            GS[g.pb[l] + j] = (s4.x + s4.y) + (s4.z + s4.w);
+                            if (p.gsplit > 1) GS[gstride + g.pb[l] + j] = 0.0f;
+                        }
+                    }
+                } else
                     tile_weight_grad<kTrainWarps>(sm + p.off_a[l], ain, GS + g.pw[l], g.sw[l],
                                                   GS + g.pb[l], g.fp[l], g.fp[l - 1], splits,
                                                   gstride, warp, lane, l != N);
