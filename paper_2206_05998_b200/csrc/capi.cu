@@ -124,6 +124,8 @@ struct noma_ctx_s {
     cudaEvent_t fork = nullptr, join = nullptr, join2 = nullptr;
     cudaEvent_t ev_perm0 = nullptr;       // profiling: shuffle start on side2
     cudaEvent_t join3 = nullptr;          // LLS condition numbers (side2, joined at the end)
+    cudaStream_t copy = nullptr;          // late host->device input copies (data phase)
+    cudaEvent_t ev_alloc = nullptr, copied = nullptr;
 };
 
 namespace {
@@ -153,9 +155,31 @@ struct Stage {
     struct Back { void *host; const void *dev; size_t bytes; };
     std::vector<Back> backs;
     bool ok = true;
+    bool late = false;  // host->device copies pending on c->copy
     Stage(noma_ctx_t c_, int mem_) : c(c_), mem(mem_) {}
     ~Stage() {
+        late_join();  // no buffer is freed under an in-flight copy
         for (void *p : allocs) cudaFreeAsync(p, c->stream);
+    }
+    // an input needed only late in the call (the data phase): allocated on the
+    // context stream, copied on the copy stream so the transfer overlaps the
+    // LLS and training; late_join() orders the context stream after it
+    template <class T> const T *in_late(const T *p, size_t n) {
+        if (!p) return nullptr;
+        if (mem == NOMA_MEM_DEVICE) return p;
+        T *d = scratch<T>(n);
+        if (!d) return nullptr;
+        cudaEventRecord(c->ev_alloc, c->stream);
+        cudaStreamWaitEvent(c->copy, c->ev_alloc, 0);
+        if (cudaMemcpyAsync(d, p, n * sizeof(T), cudaMemcpyHostToDevice, c->copy) != cudaSuccess) ok = false;
+        late = true;
+        return d;
+    }
+    void late_join() {
+        if (!late) return;
+        cudaEventRecord(c->copied, c->copy);
+        cudaStreamWaitEvent(c->stream, c->copied, 0);
+        late = false;
     }
     void *alloc(size_t bytes) {
         if (bytes == 0) bytes = 16;
@@ -317,6 +341,9 @@ NOMA_API int noma_ctx_create(int device, noma_ctx_t *out) {
         cudaEventCreateWithFlags(&c->join, cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&c->join2, cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&c->join3, cudaEventDisableTiming) != cudaSuccess ||
+        cudaStreamCreateWithFlags(&c->copy, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&c->ev_alloc, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&c->copied, cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreate(&c->ev_perm0) != cudaSuccess) {
         delete c;
         return NOMA_ERR_CUDA;
@@ -340,6 +367,9 @@ NOMA_API int noma_ctx_destroy(noma_ctx_t c) {
     if (c->side2) cudaStreamSynchronize(c->side2), cudaStreamDestroy(c->side2);
     if (c->join2) cudaEventDestroy(c->join2);
     if (c->join3) cudaEventDestroy(c->join3);
+    if (c->copy) cudaStreamSynchronize(c->copy), cudaStreamDestroy(c->copy);
+    if (c->ev_alloc) cudaEventDestroy(c->ev_alloc);
+    if (c->copied) cudaEventDestroy(c->copied);
     if (c->ev_perm0) cudaEventDestroy(c->ev_perm0);
     if (c->fork) cudaEventDestroy(c->fork);
     if (c->join) cudaEventDestroy(c->join);
@@ -721,8 +751,6 @@ NOMA_API int noma_pipeline(noma_ctx_t c, const noma_net_desc *desc, const noma_t
     Stage s(c, mem);
     const double *px = s.in(pilot_rx, (size_t)S * NT * M * 2);
     const double *py = s.in(pilot_sym, (size_t)S * NT * K * 2);
-    const float *dx = s.in(data_rx, (size_t)S * ND * M * 2);
-    const uint8_t *dtr = s.in(truth, (size_t)S * ND * K);
     const uint64_t *iseed = s.in(init_seeds, nets);
     const uint64_t *sseed = s.in(shuffle_seeds, nets);
     double *dw = w0 ? s.out(w0, nets * 2 * M) : s.scratch<double>(nets * 2 * M);
@@ -736,6 +764,10 @@ NOMA_API int noma_pipeline(noma_ctx_t c, const noma_net_desc *desc, const noma_t
     float *d32 = s.scratch<float>((size_t)S * NT * 2 * M);
     float *r0 = s.scratch<float>(nets * n);
     uint16_t *perm = s.scratch<uint16_t>(nets * (size_t)cfg->epochs * n);
+    // data-phase inputs (~2/3 of the host->device bytes) travel while the LLS
+    // and training run; the detection launch waits for them
+    const float *dx = s.in_late(data_rx, (size_t)S * ND * M * 2);
+    const uint8_t *dtr = s.in_late(truth, (size_t)S * ND * K);
     if (!s.ok) return s.finish();
 
     noma_dataset ds{NOMA_LAYOUT_WIDEN_COMPLEX, S, K, n, 2 * M, px, py};
@@ -826,6 +858,7 @@ NOMA_API int noma_pipeline(noma_ctx_t c, const noma_net_desc *desc, const noma_t
         }
     }
     mark(c, 6);
+    s.late_join();
     if (ND > 0) {
         if (der) cudaMemsetAsync(der, 0, nets * sizeof(uint32_t), c->stream);
         DetectParams dpp;
