@@ -109,23 +109,6 @@ __device__ __forceinline__ void fence_proxy_async() {
 
 namespace {
 
-__device__ __forceinline__ void st_async2(uint32_t raddr, float a, float b, uint32_t rbar) {
-    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f32 [%0], {%1, %2}, [%3];" ::"r"(raddr),
-                 "f"(a), "f"(b), "r"(rbar)
-                 : "memory");
-}
-__device__ __forceinline__ void st_async1(uint32_t raddr, float a, uint32_t rbar) {
-    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.f32 [%0], %1, [%2];" ::"r"(raddr), "f"(a),
-                 "r"(rbar)
-                 : "memory");
-}
-// Send the first NV floats of v (NV = 1, 2 or 4, contiguous in the target).
-template <int NV>
-__device__ __forceinline__ void st_async_n(uint32_t raddr, const float *v, uint32_t rbar) {
-    if constexpr (NV == 4) st_async4(raddr, make_float4(v[0], v[1], v[2], v[3]), rbar);
-    else if constexpr (NV == 2) st_async2(raddr, v[0], v[1], rbar);
-    else st_async1(raddr, v[0], rbar);
-}
 template <int NV>
 __device__ __forceinline__ void sts_n(float *p, const float *v) {
     if constexpr (NV == 4) *reinterpret_cast<float4 *>(p) = make_float4(v[0], v[1], v[2], v[3]);
@@ -174,7 +157,6 @@ __device__ __forceinline__ void static_for(F &&f) {
 
 }  // namespace
 
-constexpr int kLatMaxV = 4;         // float4 per gather thread: input width <= 64
 constexpr int kLatMaxLayers = 2;    // hidden layers handled by the latency kernel
 constexpr int kLatMaxSteps = 4096;  // Adam bias-correction table in shared memory
 
@@ -512,7 +494,6 @@ static_for<1, NL + 1, 1>([&](auto LC) {
 static_for<NL, 0, -1>([&](auto LC) {
                 constexpr int l = decltype(LC)::value;
                 const bool top = l == NL;
-                const int NC = (l == 1 ? W0 : H) >> 2;
                 const float *zsrc = top ? sm + c.aN : sm + c.aloc[l];  // a_N, or dZ_l in place
                 const float *dyp = sm + c.dy, *wfp = sm + po + c.wf;
                 const float *in = l == 1 ? XT : sm + c.af[l - 1] + buf * H * kSR;
