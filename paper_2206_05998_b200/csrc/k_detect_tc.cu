@@ -213,6 +213,13 @@ __device__ __forceinline__ void ws_arrive(uint32_t bar) {
     __syncwarp();
     if ((threadIdx.x & 31) == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
 }
+// per-thread arrival (barrier count 128) for the x . w0 ring, whose payload is
+// ordinary shared memory: compute-sanitizer racecheck does not credit
+// __syncwarp's memory ordering to a lane-0 arrival
+// (tools/microbench/warp_arrive_repro.cu), so this hand-off stays per lane
+__device__ __forceinline__ void ws_arrive_lane(uint32_t bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
 
 template <int W0, int H, int NL>
 constexpr size_t detect_ws_smem() {
@@ -289,7 +296,9 @@ __global__ void __launch_bounds__(WsRoles<W0, NL>::kThreads, 1) detect_ws_kernel
     if (threadIdx.x == 32) {
         for (int i = 0; i < kWsBars; ++i) {
             const bool commit = (i >= kM1Done && i < kM1Done + 2) || (i >= kM2Done && i < kM2Done + 2);
-            asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar(i)), "r"(commit ? 1 : kTcRows / 32));
+            const bool lin = i >= kLinFull;  // x . w0 ring: per-thread arrivals
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar(i)),
+                         "r"(commit ? 1 : lin ? kTcRows : kTcRows / 32));
         }
         asm volatile("fence.mbarrier_init.release.cluster;");
     }
@@ -336,7 +345,7 @@ __global__ void __launch_bounds__(WsRoles<W0, NL>::kThreads, 1) detect_ws_kernel
         const int ls = i % kLinSlots;
         wait(1, bar(kLinFull + ls), (i / kLinSlots) & 1);
         const float lin = lin_s[ls * kTcRows + r];
-        ws_arrive(bar(kLinEmpty + ls));
+        ws_arrive_lane(bar(kLinEmpty + ls));
         const long long td0 = ck ? clock64() : 0;
         p2_t acc2[2] = {0ull, 0ull};
 #pragma unroll
@@ -440,7 +449,7 @@ __global__ void __launch_bounds__(WsRoles<W0, NL>::kThreads, 1) detect_ws_kernel
             wait(1, bar(kLinEmpty + ls), ((i / kLinSlots) & 1) ^ 1);
             const float2 q01 = up2(l2[0]), q23 = up2(l2[1]);
             lin_s[ls * kTcRows + r] = (q01.x + q01.y) + (q23.x + q23.y);
-            ws_arrive(bar(kLinFull + ls));
+            ws_arrive_lane(bar(kLinFull + ls));
         }
     } else if (warp < 8) {
         // ---------------- epilogue 1 --------------------------------------------
