@@ -33,6 +33,20 @@ namespace noma_dev {
 
 constexpr int kMaxSplit = 2;  // weight-gradient split-K partials
 
+__device__ __forceinline__ void cp_async16_g2s(float *dst, const float *src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((unsigned)__cvta_generic_to_shared(dst)),
+                 "l"(src)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async4_g2s(float *dst, const float *src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"((unsigned)__cvta_generic_to_shared(dst)),
+                 "l"(src)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all_g2s() {
+    asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
+}
+
 // Two CTA shapes: 16 warps with 4x4 FFMA2 tiles (one net per SM: large nets)
 // and 8 warps with 8x4 FFMA2 tiles (two nets per SM when they fit: small
 // nets); the tile width picks the final-layer partial block (16 / 32 j).
@@ -109,11 +123,54 @@ __global__ void __launch_bounds__(NT, MINB) train_kernel(TrainParams p) {
     float *AN = N ? sm + p.off_a[N] : XT;
     float loss_acc = 0.0f;     // per-row-thread partial of the epoch loss
     long step = 0;
+    // next-minibatch staging (two layers, 32-wide input, >= 8 warps idle in the
+    // first layer's weight gradient -- the C2 shape): those warps cp.async the
+    // next step's raw design rows and r0 into a_2, which is dead from then
+    // until the next forward; the gather then only widens shared memory
+    const bool stage_next = NT == 512 && CS == 1 && N >= 2 && width == 32 && vec4 &&
+                            (g.fp[1] >> 5) * (g.fp[0] >> 4) * grad_splits<NT>(g.fp[1], g.fp[0], p.gsplit) <=
+                                kTrainWarps - 8 &&
+                            g.fp[2] * kSR >= kBatchRows * (32 + 2);
+    float *stg = N >= 2 ? sm + p.off_a[2] : nullptr;  // [128][32] rows, then r0[128], idx[128]
+    const bool stage_warp = warp >= kTrainWarps - 8;
     for (int e = 0; e < p.epochs; ++e) {
         const uint16_t *perm = p.perm + ((size_t)net * p.epochs + e) * n;
         for (int start = 0; start < n; start += p.batch) {
             const int bsz = min(p.batch, n - start);
             NOMA_PHASE(5)
+            if (stage_next && step > 0) {  // rows staged in a_2 during the previous step
+                const int r = tid & (kBatchRows - 1), h = tid >> 7;  // 4 threads per row
+                const float *row = stg + r * 32;
+                const int idx = reinterpret_cast<const int *>(stg + kBatchRows * 33)[r];
+                const bool odd = p.layout == NOMA_LAYOUT_WIDEN_COMPLEX && idx >= 0 && (idx & 1);
+                if (h == 0) r0b[r] = stg[kBatchRows * 32 + r];
+#pragma unroll
+                for (int c = h * 4; c < 32; c += 16) {
+                    float4 v;
+                    if (idx < 0) v = make_float4(0.f, 0.f, 0.f, 0.f);
+                    else if (!odd) v = *reinterpret_cast<const float4 *>(row + c);
+                    else if (c < M) v = *reinterpret_cast<const float4 *>(row + M + c);
+                    else {
+                        const float4 t = *reinterpret_cast<const float4 *>(row + c - M);
+                        v = make_float4(-t.x, -t.y, -t.z, -t.w);
+                    }
+                    XT[c * kSR + r] = v.x;
+                    XT[(c + 1) * kSR + r] = v.y;
+                    XT[(c + 2) * kSR + r] = v.z;
+                    XT[(c + 3) * kSR + r] = v.w;
+                }
+                if (tid == kTrainThreads - 1) {
+                    if (p.atab) {
+                        misc[0] = p.atab[2 * step];
+                        misc[1] = p.atab[2 * step + 1];
+                    } else {
+                        const double c1 = 1.0 - pow(p.b1d, (double)(step + 1));
+                        const double c2 = 1.0 - pow(p.b2d, (double)(step + 1));
+                        misc[0] = (float)(p.lr_d / c1);
+                        misc[1] = (float)(1.0 / c2);
+                    }
+                }
+            } else
             // ---- gather (IQ widening at load): NT/128 threads per batch row -
             {
                 constexpr int TPR = NT / kBatchRows;
@@ -267,6 +324,32 @@ __global__ void __launch_bounds__(NT, MINB) train_kernel(TrainParams p) {
                     tile_weight_grad44<kTrainWarps>(sm + p.off_a[l], ain, GS + g.pw[l], g.sw[l],
                                                     GS + g.pb[l], g.fp[l], g.fp[l - 1], splits,
                                                     gstride, warp, lane, RB, l != N && !idle_bias);
+                    if (stage_next && l == 1 && stage_warp) {  // the next minibatch's rows -> a_2
+                        int ns = start + p.batch, ne = e;
+                        if (ns >= n) {
+                            ns = 0;
+                            ++ne;
+                        }
+                        const int pt = tid - (kTrainWarps - 8) * 32;
+                        const int r = pt & (kBatchRows - 1), hh = pt >> 7;  // half a row per thread
+                        const int nb = ne < p.epochs ? min(p.batch, n - ns) : 0;
+                        int *sidx = reinterpret_cast<int *>(stg + kBatchRows * 33);
+                        if (r < nb) {
+                            const int idx = p.perm[((size_t)net * p.epochs + ne) * n + ns + r];
+                            const bool wid = p.layout == NOMA_LAYOUT_WIDEN_COMPLEX;
+                            const float *src = wid ? p.design32 + ((size_t)d * (n >> 1) + (idx >> 1)) * width
+                                                   : p.design32 + ((size_t)d * n + idx) * width;
+#pragma unroll
+                            for (int q = 0; q < 4; ++q) cp_async16_g2s(stg + r * 32 + 16 * hh + 4 * q, src + 16 * hh + 4 * q);
+                            if (hh == 0) {
+                                cp_async4_g2s(stg + kBatchRows * 32 + r, p.r0 + (size_t)net * n + idx);
+                                sidx[r] = idx;
+                            }
+                        } else if (hh == 0) {
+                            stg[kBatchRows * 32 + r] = 0.0f;
+                            sidx[r] = -1;
+                        }
+                    }
                     if (idle_bias && warp >= ntask) {
                         const int nth = (kTrainWarps - ntask) * 32, t0 = tid - ntask * 32;
                         const float *dzl = sm + p.off_a[l];
@@ -382,6 +465,7 @@ __global__ void __launch_bounds__(NT, MINB) train_kernel(TrainParams p) {
                     }
                 }
             }
+            if (stage_next && stage_warp) cp_async_wait_all_g2s();  // staged rows land before the barrier
             ++step;
             __syncthreads();
         }
