@@ -142,6 +142,32 @@ def test_large_detect_self_consistent(A, O):
     assert np.max(np.abs(soft[sl] - ref)) / max(1.0, np.max(np.abs(ref))) < 1e-5
 
 
+@pytest.mark.parametrize("NT", [64, 100])
+def test_throughput_kernel_c2_shape(A, O, NT):
+    """The one-CTA-per-net kernel at the C2 network shape ([32, 64, 64], 78
+    nets): exercises the paths that only this shape takes -- idle warps
+    summing the first layer's bias gradient and staging the next minibatch by
+    cp.async into a dead activation region (NT = 64: one minibatch per epoch,
+    staging across epoch boundaries; NT = 100: a partial second minibatch) --
+    against the FP64 oracle for short trainings."""
+    sc = O.Scenario(num_users=6, num_antennas=16, train_symbols=NT, data_symbols=128,
+                    power_step_db=3.0, snr_db=20.0, rx_nonlinearity_gain=0.05)
+    S = 13  # 78 nets: the throughput kernel
+    seeds = [3000 + s for s in range(S)]
+    recs = [O.synthesize(sc, O.seed_bundle(s)) for s in seeds]
+    ref = O.run_slots(sc, [64, 64], seeds, epochs=3, threads=8)
+    init, shuf = _seeds(O, seeds, 6)
+    out = A.pipeline([32, 64, 64], np.stack([r.train_rx for r in recs]),
+                     np.stack([r.train_symbols for r in recs]), np.stack([r.data_rx for r in recs]),
+                     np.stack([A.codes_of(r.data_symbols) for r in recs]), init, shuf, epochs=3)
+    assert A.context().train_mode == 1
+    assert (out.status == 0).all()
+    soft_dev = np.max(np.abs(out.soft - ref.soft)) / max(1.0, np.max(np.abs(ref.soft)))
+    trace_dev = float(np.max(np.abs(out.trace - ref.trace) / np.abs(ref.trace)))
+    record("throughput_c2_shape", config=f"NT={NT}", soft_dev=soft_dev, trace_dev=trace_dev)
+    assert soft_dev < 1e-4 and trace_dev < 1e-4
+
+
 @pytest.mark.parametrize("mode", ["1", "2", "4"])
 def test_train_modes_agree(A, O, mode, monkeypatch):
     """The one-CTA-per-net kernel (throughput mode) and the cluster kernels
