@@ -253,7 +253,7 @@ __global__ void __launch_bounds__(WsRoles<W0, NL>::kThreads, 1) detect_ws_kernel
     // emit] per role (roles: loaders, epilogue 1, epilogue 2, then one per
     // issuing warp)
     const int role = (threadIdx.x >> 7) < 3 ? (int)(threadIdx.x >> 7) : 3 + (int)(threadIdx.x >> 5) - 12;
-    long long *ck = p.clocks && blockIdx.x == 0 && blockIdx.y == 0 && (threadIdx.x & (threadIdx.x < 384 ? 127 : 31)) == 0
+    long long *ck = p.clocks && blockIdx.x == 0 && (threadIdx.x & (threadIdx.x < 384 ? 127 : 31)) == 0
                         ? p.clocks + 6 * role
                         : nullptr;
     auto wait = [&](int site, uint32_t b, uint32_t ph) {
@@ -267,28 +267,8 @@ __global__ void __launch_bounds__(WsRoles<W0, NL>::kThreads, 1) detect_ws_kernel
     };
     const long long tstart = ck ? clock64() : 0;
 
-    const int net = blockIdx.y, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    if (p.status && p.status[net] != NOMA_OK) {
-        if (blockIdx.x == 0 && threadIdx.x == 0 && p.errors) p.errors[net] = 0xFFFFFFFFu;
-        return;
-    }
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const NetGeom &g = p.g;
-    const int d = net / p.K, k = net % p.K;
-    const float *pl = p.plans + (size_t)net * g.plan_total;
-    // ---- weights: hi/lo planes in the K-major core layout (FusedPlan order) --
-    for (int i = threadIdx.x; i < H * KB0; i += R::kThreads) {
-        const int j = i / KB0, kq = (i - j * KB0) * 4;
-        put4(b1h, b1l, j, kq, KB0, *reinterpret_cast<const float4 *>(pl + g.plan_w[1] + j * g.plan_pad[0] + kq));
-    }
-    if constexpr (NL > 1) {
-        for (int i = threadIdx.x; i < H * KBH; i += R::kThreads) {
-            const int j = i / KBH, kq = (i - j * KBH) * 4;
-            put4(b2h, b2l, j, kq, KBH, *reinterpret_cast<const float4 *>(pl + g.plan_w[2] + j * g.plan_pad[1] + kq));
-        }
-    }
-    for (int i = threadIdx.x; i < NL * H; i += R::kThreads) bias[i] = pl[g.plan_b[1 + i / H] + i % H];
-    for (int i = threadIdx.x; i < H; i += R::kThreads) wf[i] = pl[g.plan_f + i];
-    for (int i = threadIdx.x; i < W0; i += R::kThreads) w0s[i] = pl[g.plan_w0 + i];
     if (warp == 0) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(tc_s2u(tmem_slot)));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
@@ -302,15 +282,15 @@ __global__ void __launch_bounds__(WsRoles<W0, NL>::kThreads, 1) detect_ws_kernel
         }
         asm volatile("fence.mbarrier_init.release.cluster;");
     }
-    // the weight planes are read by the tensor core (async proxy)
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     asm volatile("tcgen05.fence::before_thread_sync;");
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;");
     const uint32_t tmem = *tmem_slot;
-    const int first = blockIdx.x, stride = gridDim.x;
-    const int ntile = first < p.tiles ? (p.tiles - first + stride - 1) / stride : 0;
-
+    // this CTA's share of the global (net, tile) range; one pipeline segment
+    // per net it touches, the mbarrier phases running on across segments (ib)
+    const long long T = (long long)p.n_nets * p.tiles;
+    const long long t_lo = T * blockIdx.x / gridDim.x, t_hi = T * (blockIdx.x + 1) / gridDim.x;
+    int net = 0, d = 0, k = 0, first = 0, ntile = 0, ib = 0;
     // decision + bit errors of widened row r (lane pairs = Re/Im of a symbol)
     uint32_t my_err = 0;
     auto emit = [&](int tile, int r, float y, uint8_t truth) {
@@ -341,7 +321,7 @@ __global__ void __launch_bounds__(WsRoles<W0, NL>::kThreads, 1) detect_ws_kernel
         }
     };
     // the final stage: D[slot] (drained) + lin -> decision (epilogue 1 or 2)
-    auto finish = [&](int i, int r, const uint32_t (&v)[H / 16][16], const float *bN, uint8_t truth) {
+    auto finish = [&](int i, int tile, int r, const uint32_t (&v)[H / 16][16], const float *bN, uint8_t truth) {
         const int ls = i % kLinSlots;
         wait(1, bar(kLinFull + ls), (i / kLinSlots) & 1);
         const float lin = lin_s[ls * kTcRows + r];
@@ -353,7 +333,7 @@ __global__ void __launch_bounds__(WsRoles<W0, NL>::kThreads, 1) detect_ws_kernel
         const float2 s01 = up2(acc2[0]), s23 = up2(acc2[1]);
         const float y = lin + ((s01.x + s01.y) + (s23.x + s23.y));  // hybrid_nn.cpp:81
         const long long td1 = ck ? clock64() : 0;
-        emit(first + i * stride, r, y, truth);
+        emit(tile, r, y, truth);
         if (ck) {
             ck[4] += td1 - td0;
             ck[5] += clock64() - td1;
@@ -369,6 +349,36 @@ __global__ void __launch_bounds__(WsRoles<W0, NL>::kThreads, 1) detect_ws_kernel
         asm volatile("tcgen05.fence::before_thread_sync;");
     };
 
+    for (long long t0 = t_lo; t0 < t_hi; t0 += ntile) {
+    net = (int)(t0 / p.tiles);
+    first = (int)(t0 - (long long)net * p.tiles);
+    ntile = (int)((t_hi < (long long)(net + 1) * p.tiles ? t_hi : (long long)(net + 1) * p.tiles) - t0);
+    d = net / p.K;
+    k = net % p.K;
+    if (p.status && p.status[net] != NOMA_OK) {
+        if (first == 0 && threadIdx.x == 0 && p.errors) p.errors[net] = 0xFFFFFFFFu;
+        continue;
+    }
+    // ---- the net's weights: hi/lo planes in the K-major core layout (FusedPlan
+    // order); the previous segment's MMAs have all completed (every one was
+    // waited on by an epilogue before the closing barrier)
+    const float *pl = p.plans + (size_t)net * g.plan_total;
+    for (int i = threadIdx.x; i < H * KB0; i += R::kThreads) {
+        const int j = i / KB0, kq = (i - j * KB0) * 4;
+        put4(b1h, b1l, j, kq, KB0, *reinterpret_cast<const float4 *>(pl + g.plan_w[1] + j * g.plan_pad[0] + kq));
+    }
+    if constexpr (NL > 1) {
+        for (int i = threadIdx.x; i < H * KBH; i += R::kThreads) {
+            const int j = i / KBH, kq = (i - j * KBH) * 4;
+            put4(b2h, b2l, j, kq, KBH, *reinterpret_cast<const float4 *>(pl + g.plan_w[2] + j * g.plan_pad[1] + kq));
+        }
+    }
+    for (int i = threadIdx.x; i < NL * H; i += R::kThreads) bias[i] = pl[g.plan_b[1 + i / H] + i % H];
+    for (int i = threadIdx.x; i < H; i += R::kThreads) wf[i] = pl[g.plan_f + i];
+    for (int i = threadIdx.x; i < W0; i += R::kThreads) w0s[i] = pl[g.plan_w0 + i];
+    // the weight planes are read by the tensor core (async proxy)
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncthreads();
     if (warp < 4) {
         // ---------------- loaders: widened rows -> A1[slot] (hi/lo), lin ---------
         const int r = threadIdx.x, sym = r >> 1;
@@ -387,8 +397,9 @@ __global__ void __launch_bounds__(WsRoles<W0, NL>::kThreads, 1) detect_ws_kernel
                 xs[m + 1] = make_float2(v.z, v.w);
             }
         };
-        if (ntile > 0) load(first);
-        for (int i = 0; i < ntile; ++i) {
+        load(first);
+        for (int j = 0; j < ntile; ++j) {
+            const int i = ib + j;
             const int sl = i & 1;
             const uint32_t ph = (i >> 1) & 1;
             p2_t l2[2] = {0ull, 0ull};  // x . w0 (hybrid_nn.cpp:81, linear branch), 4 partials
@@ -437,7 +448,7 @@ __global__ void __launch_bounds__(WsRoles<W0, NL>::kThreads, 1) detect_ws_kernel
                     tmem_st16(trow + kA1 + sl * kA1S + W0 + 16 * c, l16);
                 }
             }
-            if (i + 1 < ntile) load(first + (i + 1) * stride);  // in flight until the next stage
+            if (j + 1 < ntile) load(first + j + 1);  // in flight until the next stage
             if constexpr (kA1T) {
                 asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
                 asm volatile("tcgen05.fence::before_thread_sync;");
@@ -457,15 +468,16 @@ __global__ void __launch_bounds__(WsRoles<W0, NL>::kThreads, 1) detect_ws_kernel
         const uint32_t trow = tmem + ((uint32_t)(q * 32) << 16);
         // truth codes two tiles ahead (a global load per tile would otherwise
         // sit exposed on this stage's critical path)
-        uint8_t tq0 = NL == 1 ? truth_of(first, r) : 0, tq1 = NL == 1 ? truth_of(first + stride, r) : 0;
-        for (int i = 0; i < ntile; ++i) {
+        uint8_t tq0 = NL == 1 ? truth_of(first, r) : 0, tq1 = NL == 1 ? truth_of(first + 1, r) : 0;
+        for (int j = 0; j < ntile; ++j) {
+            const int i = ib + j;
             const int sl = i & 1;
             const uint32_t ph = (i >> 1) & 1;
             uint8_t truth = 0;
             if constexpr (NL == 1) {
                 truth = tq0;
                 tq0 = tq1;
-                tq1 = truth_of(first + (i + 2) * stride, r);
+                tq1 = truth_of(first + j + 2, r);
             }
             wait(0, bar(kM1Done + sl), ph);
             asm volatile("tcgen05.fence::after_thread_sync;");
@@ -473,7 +485,7 @@ __global__ void __launch_bounds__(WsRoles<W0, NL>::kThreads, 1) detect_ws_kernel
             drain(i, trow, v1);
             if constexpr (NL == 1) {
                 ws_arrive(bar(kDEmpty + sl));
-                finish(i, r, v1, bias, truth);
+                finish(i, first + j, r, v1, bias, truth);
             } else {
                 // A2[sl] is free once tile i-2's layer-2 MMAs are done
                 wait(1, bar(kM2Done + sl), ph ^ 1);
@@ -509,19 +521,20 @@ __global__ void __launch_bounds__(WsRoles<W0, NL>::kThreads, 1) detect_ws_kernel
         // ---------------- epilogue 2 --------------------------------------------
         const int q = warp - 8, r = q * 32 + lane;
         const uint32_t trow = tmem + ((uint32_t)(q * 32) << 16);
-        uint8_t tq0 = truth_of(first, r), tq1 = truth_of(first + stride, r);  // two tiles ahead
-        for (int i = 0; i < ntile; ++i) {
+        uint8_t tq0 = truth_of(first, r), tq1 = truth_of(first + 1, r);  // two tiles ahead
+        for (int j = 0; j < ntile; ++j) {
+            const int i = ib + j;
             const int sl = i & 1;
             const uint32_t ph = (i >> 1) & 1;
             const uint8_t truth = tq0;
             tq0 = tq1;
-            tq1 = truth_of(first + (i + 2) * stride, r);
+            tq1 = truth_of(first + j + 2, r);
             wait(0, bar(kM2Done + sl), ph);
             asm volatile("tcgen05.fence::after_thread_sync;");
             uint32_t v2[H / 16][16];
             drain(i, trow, v2);
             ws_arrive(bar(kDEmpty + sl));
-            finish(i, r, v2, bias + H, truth);
+            finish(i, first + j, r, v2, bias + H, truth);
         }
     } else if (warp == R::kMma1Warp || warp == R::kMma1Warp + 1) {
         // ---------------- layer-1 issuers: even / odd tiles (elected lane) -------
@@ -529,7 +542,7 @@ __global__ void __launch_bounds__(WsRoles<W0, NL>::kThreads, 1) detect_ws_kernel
         const uint64_t b1hd = umma_desc(tc_s2u(b1h), 128, KB0 * 128), b1ld = umma_desc(tc_s2u(b1l), 128, KB0 * 128);
         const int sl = warp - R::kMma1Warp;
         const uint32_t dcol = tmem + kD + sl * H;
-        for (int i = sl; i < ntile; i += 2) {
+        for (int i = ib + ((sl ^ ib) & 1); i < ib + ntile; i += 2) {
             const uint32_t ph = (i >> 1) & 1;
             wait(0, bar(kA1Full + sl), ph);
             wait(1, bar(kDEmpty + sl), ph ^ 1);  // the final epilogue has drained tile i-2
@@ -565,7 +578,7 @@ __global__ void __launch_bounds__(WsRoles<W0, NL>::kThreads, 1) detect_ws_kernel
         const uint64_t b2hd = umma_desc(tc_s2u(b2h), 128, KBH * 128), b2ld = umma_desc(tc_s2u(b2l), 128, KBH * 128);
         const int sl = warp - R::kMma2Warp;
         const uint32_t a2 = tmem + kA2 + sl * kA2S, dcol = tmem + kD + sl * H;
-        for (int i = sl; i < ntile; i += 2) {
+        for (int i = ib + ((sl ^ ib) & 1); i < ib + ntile; i += 2) {
             wait(0, bar(kA2Full + sl), (i >> 1) & 1);  // epilogue 1 has drained D[sl] and filled A2[sl]
             asm volatile("tcgen05.fence::after_thread_sync;");
             if (lane == 0) {
@@ -581,14 +594,18 @@ __global__ void __launch_bounds__(WsRoles<W0, NL>::kThreads, 1) detect_ws_kernel
             __syncwarp();
         }
     }
-    if (ck) ck[0] = clock64() - tstart;
     if ((NL == 1 ? (warp >= 4 && warp < 8) : (warp >= 8 && warp < 12)) && p.errors && p.truth) {
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) my_err += __shfl_xor_sync(0xffffffffu, my_err, o);
         if (lane == 0 && my_err) atomicAdd(p.errors + net, my_err);
+        my_err = 0;
     }
     asm volatile("tcgen05.fence::before_thread_sync;");
     __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    ib += ntile;  // (a skipped net's segment leaves the phases alone)
+    }  // segments
+    if (ck) ck[0] = clock64() - tstart;
     if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
 }
 
@@ -630,21 +647,23 @@ int detect_tc_launch(const DetectParams &dp, cudaStream_t st) {
     int sms = 148, dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    // one wave, one CTA per SM (the smem footprint allows one): rounding up
-    // would leave a second wave of CTAs that doubles the kernel time
-    int ctas = sms / p.n_nets;
-    ctas = ctas < 1 ? 1 : ctas > p.tiles ? p.tiles : ctas;
+    // one wave, one persistent CTA per SM (the smem footprint allows one),
+    // each taking an equal contiguous share of all nets' tiles: a grid of
+    // (SMs / nets) x nets would leave SMs idle (C3: 144 of 148) and rounding
+    // up would add a second wave that doubles the kernel time
+    const long long total = (long long)p.n_nets * p.tiles;
+    const int ctas = total < sms ? (int)total : sms;
     auto launch = [&](auto kern, size_t smem, int threads) -> int {
         // one CTA per SM: each allocates all 512 TMEM columns
         smem = smem < 116 * 1024 ? 116 * 1024 : smem;
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        kern<<<dim3(ctas, p.n_nets), threads, smem, st>>>(p);
+        kern<<<ctas, threads, smem, st>>>(p);
         const bool launched = cudaGetLastError() == cudaSuccess;
         if (clk) {  // roles: loaders, epilogue 1, epilogue 2, L1 issuers (even, odd), L2 issuers (even, odd)
             long long h[48];
             cudaMemcpyAsync(h, clk_buf, sizeof h, cudaMemcpyDeviceToHost, st);
             cudaStreamSynchronize(st);
-            std::fprintf(stderr, "NOMA_DETECT_CLK tiles/CTA %d:", (p.tiles + ctas - 1) / ctas);
+            std::fprintf(stderr, "NOMA_DETECT_CLK tiles/CTA %lld:", (total + ctas - 1) / ctas);
             for (int i = 0; i < 48; ++i) std::fprintf(stderr, " %lld", h[i]);
             std::fprintf(stderr, "\n");
             cudaFreeAsync(clk_buf, st);
