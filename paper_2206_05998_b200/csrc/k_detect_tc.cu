@@ -202,8 +202,10 @@ struct WsRoles {
 // kLinSlots slots: with only two, the loaders would be held to within two
 // tiles of the final epilogue and starve the whole pipeline
 constexpr int kLinSlots = 8;
-enum WsBar { kA1Full = 0, kM1Done = 2, kDEmpty = 4, kA2Full = 6, kM2Done = 8, kLinFull = 10,
-             kLinEmpty = 10 + kLinSlots, kWsBars = 10 + 2 * kLinSlots };
+// A2Full is per (slot, column half): layer 2's first four k-steps read only
+// columns 0-31 of A2, so they start while epilogue 1 still works on 32-63
+enum WsBar { kA1Full = 0, kM1Done = 2, kDEmpty = 4, kA2Full = 6, kM2Done = 10, kLinFull = 12,
+             kLinEmpty = 12 + kLinSlots, kWsBars = 12 + 2 * kLinSlots };
 
 // one arrival per warp (barrier count = 4 warps per role): 128 per-thread
 // arrivals on one mbarrier serialise.  __syncwarp orders the lanes' prior
@@ -256,11 +258,16 @@ __global__ void __launch_bounds__(WsRoles<W0, NL>::kThreads, 1) detect_ws_kernel
     long long *ck = p.clocks && blockIdx.x == 0 && (threadIdx.x & (threadIdx.x < 384 ? 127 : 31)) == 0
                         ? p.clocks + 6 * role
                         : nullptr;
+    // accumulated in shared memory: a global += per tile would distort the stage
+    __shared__ long long ck_s[8 * 6];
+    long long *cv = ck ? ck_s + 6 * role : nullptr;
+    if (cv)
+        for (int c = 0; c < 6; ++c) cv[c] = 0;
     auto wait = [&](int site, uint32_t b, uint32_t ph) {
         if (ck) {
             const long long t0 = clock64();
             tc_mbar_wait(b, ph);
-            ck[1 + site] += clock64() - t0;
+            cv[1 + site] += clock64() - t0;
         } else {
             tc_mbar_wait(b, ph);
         }
@@ -335,8 +342,8 @@ __global__ void __launch_bounds__(WsRoles<W0, NL>::kThreads, 1) detect_ws_kernel
         const long long td1 = ck ? clock64() : 0;
         emit(tile, r, y, truth);
         if (ck) {
-            ck[4] += td1 - td0;
-            ck[5] += clock64() - td1;
+            cv[4] += td1 - td0;
+            cv[5] += clock64() - td1;
         }
     };
     // drain D[slot] of tile i into registers and release the slot / columns
@@ -345,7 +352,7 @@ __global__ void __launch_bounds__(WsRoles<W0, NL>::kThreads, 1) detect_ws_kernel
 #pragma unroll
         for (int c = 0; c < H / 16; ++c) tmem_ld16_nw(trow + kD + (i & 1) * H + 16 * c, v[c]);
         tmem_wait_ld();
-        if (ck) ck[3] += clock64() - tl0;
+        if (ck) cv[3] += clock64() - tl0;
         asm volatile("tcgen05.fence::before_thread_sync;");
     };
 
@@ -491,8 +498,10 @@ __global__ void __launch_bounds__(WsRoles<W0, NL>::kThreads, 1) detect_ws_kernel
                 wait(1, bar(kM2Done + sl), ph ^ 1);
                 asm volatile("tcgen05.fence::after_thread_sync;");
                 const uint32_t a2 = trow + kA2 + sl * kA2S;
+                long long te0 = ck ? clock64() : 0;
 #pragma unroll
                 for (int c = 0; c < H / 16; ++c) {
+                    if (ck && c == 2) te0 = clock64();
                     float hi[16], lo[16];
 #pragma unroll
                     for (int e4 = 0; e4 < 16; e4 += 4) {
@@ -511,10 +520,18 @@ __global__ void __launch_bounds__(WsRoles<W0, NL>::kThreads, 1) detect_ws_kernel
                     }
                     tmem_st16(a2 + 16 * c, hi);
                     tmem_st16(a2 + H + 16 * c, lo);
+                    if (c % 2 == 1) {  // a column half of A2 (hi and lo) is in TMEM
+                        const long long te1 = ck ? clock64() : 0;
+                        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+                        asm volatile("tcgen05.fence::before_thread_sync;");
+                        if (ck) {  // epilogue 1: [4] compute + store issue, [5] store wait
+                            cv[4] += te1 - te0;
+                            cv[5] += clock64() - te1;
+                        }
+                        // (the first half also says: D[sl] drained, layer 2 may overwrite it)
+                        ws_arrive(bar(kA2Full + 2 * sl + c / 2));
+                    }
                 }
-                asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
-                asm volatile("tcgen05.fence::before_thread_sync;");
-                ws_arrive(bar(kA2Full + sl));  // also: D[sl] drained, layer 2 may overwrite it
             }
         }
     } else if (NL > 1 && warp < 12) {
@@ -579,19 +596,23 @@ __global__ void __launch_bounds__(WsRoles<W0, NL>::kThreads, 1) detect_ws_kernel
         const int sl = warp - R::kMma2Warp;
         const uint32_t a2 = tmem + kA2 + sl * kA2S, dcol = tmem + kD + sl * H;
         for (int i = ib + ((sl ^ ib) & 1); i < ib + ntile; i += 2) {
-            wait(0, bar(kA2Full + sl), (i >> 1) & 1);  // epilogue 1 has drained D[sl] and filled A2[sl]
-            asm volatile("tcgen05.fence::after_thread_sync;");
-            if (lane == 0) {
 #pragma unroll
-                for (int kk = 0; kk < H / 8; ++kk) {
-                    const uint64_t ko = (uint64_t)(kk * 16);
-                    umma_tf32_ta(dcol, a2 + 8 * kk, b2hd + ko, id2, kk > 0);
-                    umma_tf32_ta(dcol, a2 + 8 * kk, b2ld + ko, id2, 1);
-                    umma_tf32_ta(dcol, a2 + H + 8 * kk, b2hd + ko, id2, 1);
+            for (int half = 0; half < 2; ++half) {
+                // epilogue 1 has drained D[sl] and filled this column half of A2[sl]
+                wait(0, bar(kA2Full + 2 * sl + half), (i >> 1) & 1);
+                asm volatile("tcgen05.fence::after_thread_sync;");
+                if (lane == 0) {
+#pragma unroll
+                    for (int kk = half * H / 16; kk < (half + 1) * H / 16; ++kk) {
+                        const uint64_t ko = (uint64_t)(kk * 16);
+                        umma_tf32_ta(dcol, a2 + 8 * kk, b2hd + ko, id2, kk > 0);
+                        umma_tf32_ta(dcol, a2 + 8 * kk, b2ld + ko, id2, 1);
+                        umma_tf32_ta(dcol, a2 + H + 8 * kk, b2hd + ko, id2, 1);
+                    }
+                    if (half) umma_commit(bar(kM2Done + sl));
                 }
-                umma_commit(bar(kM2Done + sl));
+                __syncwarp();
             }
-            __syncwarp();
         }
     }
     if ((NL == 1 ? (warp >= 4 && warp < 8) : (warp >= 8 && warp < 12)) && p.errors && p.truth) {
@@ -605,7 +626,10 @@ __global__ void __launch_bounds__(WsRoles<W0, NL>::kThreads, 1) detect_ws_kernel
     asm volatile("tcgen05.fence::after_thread_sync;");
     ib += ntile;  // (a skipped net's segment leaves the phases alone)
     }  // segments
-    if (ck) ck[0] = clock64() - tstart;
+    if (ck) {
+        cv[0] = clock64() - tstart;
+        for (int c = 0; c < 6; ++c) ck[c] = cv[c];
+    }
     if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
 }
 
