@@ -71,3 +71,52 @@ def test_bench_rows(A, O):
         path, dims, batch, ns, sp = r.split(",")
         assert dims == "32x64x64" and batch == str(1 << 16)
         assert float(ns) > 0 and float(sp) > 1
+
+
+@pytest.mark.parametrize("dims", [[32, 64, 64], [64, 64]])
+@pytest.mark.parametrize("rows", [1000, 9000])  # ragged tiles; CTAs whose share spans several nets
+def test_detect_tc_many_nets(A, dims, rows, monkeypatch):
+    """A batch of designs x users through noma_detect: the persistent
+    detection grid splits all nets' tiles evenly over the SMs, so a CTA runs
+    several nets back to back (weights reloaded, barrier phases carried on).
+    Every net must give what it gives alone, and the same decisions, soft
+    outputs and bit-error counters as the FFMA kernel."""
+    from paper_2206_05998_b200 import native as N
+
+    M, n_designs, K = dims[0] // 2, 5, 6
+    nets = [A.net_from_params(o.dims, o.w0, *o.layers())
+            for o in (random_net_fused(dims, 100 + i) for i in range(n_designs * K))]
+    plans = np.ascontiguousarray(np.stack([n.plan.reshape(-1) for n in nets]))
+    rng = np.random.default_rng(5)
+    x = (rng.normal(size=(n_designs, rows, M)) + 1j * rng.normal(size=(n_designs, rows, M))).astype(np.complex64)
+    truth = rng.integers(0, 4, size=(n_designs, rows, K), dtype=np.uint8)
+
+    def run():
+        soft = np.zeros((n_designs * K, rows), np.complex64)
+        codes = np.zeros((n_designs * K, rows), np.uint8)
+        errs = np.zeros(n_designs * K, np.uint32)
+        A.context().detect(nets[0].dims, N.LAYOUT_WIDEN, n_designs, K, rows, x.view(np.float32), plans,
+                           truth=truth, soft=soft.view(np.float32), codes=codes, bit_errors=errs)
+        return soft, codes, errs, A.context().detect_mode
+
+    soft, codes, errs, mode = run()
+    assert mode == 2
+    for net in (0, K + 1, n_designs * K - 1):  # alone: the same kernel on one net
+        d, k = divmod(net, K)
+        s1, b1, e1 = A.detect(nets[net], x[d])
+        assert np.array_equal(s1, soft[net])
+        assert np.array_equal(b1[:, 0] | (b1[:, 1] << 1), codes[net])
+    want = np.array([np.count_nonzero((codes[n] ^ truth[n // K, :, n % K]) & 1)
+                     + np.count_nonzero((codes[n] ^ truth[n // K, :, n % K]) & 2) for n in range(n_designs * K)])
+    assert np.array_equal(errs, want)
+    monkeypatch.setenv("NOMA_DETECT_TC", "0")
+    soft_f, codes_f, errs_f, mode_f = run()
+    assert mode_f == 1
+    scale = max(1.0, float(np.max(np.abs(soft_f))))
+    assert np.max(np.abs(soft_f - soft)) / scale < 2e-6
+    # random data puts a few of the 2 x nets x rows soft values within
+    # rounding of zero, where the two kernels' FP32 sums may take either sign
+    # (the synthetic channels of the shape tests above have none)
+    near = (np.abs(soft.real) < 1e-5 * scale) | (np.abs(soft.imag) < 1e-5 * scale)
+    assert np.array_equal(codes[~near], codes_f[~near])
+    assert np.all(np.abs(errs.astype(np.int64) - errs_f.astype(np.int64)) <= 2 * near.sum(axis=1))
