@@ -294,14 +294,20 @@ def detect_only(args, cfg):
         tf32_mma = 1190.0
         clk_ghz = 1.965
         sms = torch.cuda.get_device_properties(dev).multi_processor_count
-        ctas_per_net = max(1, sms // (S * K))  # detect launcher: one wave, one CTA per SM
-        tiles_per_cta = -(-((nd + 63) // 64) // ctas_per_net)
+        # detect launcher: one wave of persistent CTAs (one per SM), each an
+        # equal contiguous share of all nets' 64-symbol tiles
+        total_tiles = S * K * ((nd + 63) // 64)
+        tiles_per_cta = -(-total_tiles // min(sms, total_tiles))
         # per 128-row tile: 3 MMAs per k-step of 8; A from TMEM runs at the
         # M*N/256 = 32-cycle pipe floor (N=64), A from smem (layer 1 of a
         # 64-wide input) is bound by the shared-memory operand read (~48 cycles)
         tile_cyc = 3 * (dims[0] // 8) * (32 if dims[0] <= 32 else 48) + \
             sum(3 * (dims[l - 1] // 8) * 32 for l in range(2, len(dims)))
-        attain_ms = tiles_per_cta * tile_cyc / (clk_ghz * 1e6) * max(1, -(-(S * K) // sms))
+        attain_ms = tiles_per_cta * tile_cyc / (clk_ghz * 1e6)
+        tc_traffic = None  # DRAM bytes per launch from one ncu --set full capture
+        tc_tpath = os.path.join(ROOT, "profiles", f"traffic_{args.config}_tc.json")
+        if os.path.exists(tc_tpath):
+            tc_traffic = json.load(open(tc_tpath)).get("bytes_per_launch")
         roofline = {"bound": "tensor", "kernel": "detect_ws_kernel", "achieved": achieved,
                     "peak": tf32_mma / 3, "unit": "TFLOP/s", "frac": 3 * achieved / tf32_mma,
                     "peak_source": "3xTF32 = 1/3 of the measured tcgen05 kind::tf32 MMA rate (1190 TF/s, "
@@ -314,7 +320,7 @@ def detect_only(args, cfg):
                     "attainable_note": "MMA floor per 128-row tile: 3 MMAs per k-step, 32 cycles each with "
                                        "A in TMEM (48 with A in smem, 64-wide inputs)",
                     "hbm_bound_ms": bytes_step / (hbm * 1e9) * 1e3,
-                    "algorithmic_flop_per_launch": flop_step, "traffic": None}
+                    "algorithmic_flop_per_launch": flop_step, "traffic": tc_traffic}
     else:
         fp32_peak = ctx.measure_fp32_tflops(0)
         roofline = {"bound": "fp32", "kernel": "detect_kernel", "achieved": achieved,
