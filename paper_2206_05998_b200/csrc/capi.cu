@@ -698,7 +698,12 @@ NOMA_API int noma_detect(noma_ctx_t c, const noma_net_desc *desc, int layout, in
                                   ? (size_t)n_designs * rows * g.dims[0]
                                   : (size_t)n_designs * rows * g.dims[0];
     Stage s(c, mem);
-    const float *dd = s.in(data, data_elems);
+    // host samples of tens of MB: uploaded in row chunks on the copy stream,
+    // each chunk detected as soon as it has landed, so a host-buffer call
+    // costs about the transfer rather than transfer + kernel
+    const int chunks = mem == NOMA_MEM_HOST && data_elems * sizeof(float) >= (32u << 20) ? 8 : 1;
+    float *dd_chunked = chunks > 1 ? s.scratch<float>(data_elems) : nullptr;
+    const float *dd = chunks > 1 ? dd_chunked : s.in(data, data_elems);
     const float *dp = s.in(plans, nets * g.plan_total);
     const uint8_t *dtr = s.in(truth, (size_t)n_designs * rows * nets_per_design);
     float *dso = s.out(soft, nets * rows * (layout == NOMA_LAYOUT_WIDEN_COMPLEX ? 2 : 1));
@@ -721,10 +726,39 @@ NOMA_API int noma_detect(noma_ctx_t c, const noma_net_desc *desc, int layout, in
     dpp.errors = der;
     dpp.status = nullptr;
     dpp.mode = 0;
-    int st = detect_launch(dpp, c->stream);
-    c->detect_mode = dpp.mode;
-    if (st) return st == NOMA_ERR_CUDA ? cuda_fail(c, "detect") : fail(c, st, "detect: unsupported network shape");
-    c->launches += 1;
+    dpp.stride = rows;
+    if (chunks == 1) {
+        const int st = detect_launch(dpp, c->stream);
+        c->detect_mode = dpp.mode;
+        if (st) return st == NOMA_ERR_CUDA ? cuda_fail(c, "detect") : fail(c, st, "detect: unsupported network shape");
+        c->launches += 1;
+        return s.finish();
+    }
+    // chunks of whole 64-symbol tiles; launch i views rows [r0, r0 + n) of
+    // every design through offset pointers and the full row stride
+    const size_t row_f = g.dims[0], soft_f = layout == NOMA_LAYOUT_WIDEN_COMPLEX ? 2 : 1;
+    const int per = ((rows + chunks - 1) / chunks + 63) / 64 * 64;
+    cudaEventRecord(c->ev_alloc, c->stream);  // the buffer is allocated on the context stream
+    cudaStreamWaitEvent(c->copy, c->ev_alloc, 0);
+    for (int r0 = 0; r0 < rows; r0 += per) {
+        const int n = rows - r0 < per ? rows - r0 : per;
+        if (cudaMemcpy2DAsync(dd_chunked + r0 * row_f, rows * row_f * sizeof(float), data + r0 * row_f,
+                              rows * row_f * sizeof(float), n * row_f * sizeof(float), n_designs,
+                              cudaMemcpyHostToDevice, c->copy) != cudaSuccess)
+            return cuda_fail(c, "detect: chunk upload");
+        cudaEventRecord(c->copied, c->copy);
+        cudaStreamWaitEvent(c->stream, c->copied, 0);
+        DetectParams dc = dpp;
+        dc.rows = n;
+        dc.data = dd + r0 * row_f;
+        dc.truth = dtr ? dtr + (size_t)r0 * nets_per_design : nullptr;
+        dc.soft = dso ? dso + r0 * soft_f : nullptr;
+        dc.codes = dco ? dco + r0 : nullptr;
+        const int st = detect_launch(dc, c->stream);
+        c->detect_mode = dc.mode;
+        if (st) return st == NOMA_ERR_CUDA ? cuda_fail(c, "detect") : fail(c, st, "detect: unsupported network shape");
+        c->launches += 1;
+    }
     return s.finish();
 }
 

@@ -53,7 +53,7 @@ __global__ void __launch_bounds__(kThreads) detect_kernel(DetectParams p) {
         const int tn = min(rows_per_tile, p.rows - t0);
         // ---- gather + widen ------------------------------------------------
         if (widen) {
-            const float2 *src = reinterpret_cast<const float2 *>(p.data) + ((size_t)d * p.rows + t0) * M;
+            const float2 *src = reinterpret_cast<const float2 *>(p.data) + ((size_t)d * p.stride + t0) * M;
             for (int i = tid; i < rows_per_tile * M; i += kThreads) {
                 const int tl = i / M, m = i % M;
                 float2 v = make_float2(0.f, 0.f);
@@ -64,7 +64,7 @@ __global__ void __launch_bounds__(kThreads) detect_kernel(DetectParams p) {
                 XT[(M + m) * kSR + 2 * tl + 1] = -v.x;
             }
         } else {
-            const float *src = p.data + ((size_t)d * p.rows + t0) * p.width;
+            const float *src = p.data + ((size_t)d * p.stride + t0) * p.width;
             for (int i = tid; i < rows_per_tile * p.width; i += kThreads) {
                 const int r = i / p.width, c = i % p.width;
                 XT[c * kSR + r] = r < tn ? src[i] : 0.0f;
@@ -104,14 +104,14 @@ __global__ void __launch_bounds__(kThreads) detect_kernel(DetectParams p) {
                     const float re = Y[2 * tid], im = Y[2 * tid + 1];
                     const uint8_t code = (uint8_t)((re < 0.0f ? 1 : 0) | (im < 0.0f ? 2 : 0));
                     if (p.soft)
-                        reinterpret_cast<float2 *>(p.soft)[(size_t)net * p.rows + t] = make_float2(re, im);
-                    if (p.codes) p.codes[(size_t)net * p.rows + t] = code;
-                    if (p.truth) e = __popc((code ^ p.truth[((size_t)d * p.rows + t) * p.K + k]) & 3u);
+                        reinterpret_cast<float2 *>(p.soft)[(size_t)net * p.stride + t] = make_float2(re, im);
+                    if (p.codes) p.codes[(size_t)net * p.stride + t] = code;
+                    if (p.truth) e = __popc((code ^ p.truth[((size_t)d * p.stride + t) * p.K + k]) & 3u);
                 }
                 my_err += e;
             }
         } else if (tid < tn && p.soft) {
-            p.soft[(size_t)net * p.rows + t0 + tid] = Y[tid];
+            p.soft[(size_t)net * p.stride + t0 + tid] = Y[tid];
         }
         __syncthreads();
     }
@@ -159,6 +159,7 @@ int detect_launch(DetectParams &p, cudaStream_t st) {
     if (smem > 227 * 1024) return NOMA_ERR_UNSUPPORTED;
     const int rows_per_tile = p.layout == NOMA_LAYOUT_WIDEN_COMPLEX ? kBatchRows / 2 : kBatchRows;
     p.tiles = (p.rows + rows_per_tile - 1) / rows_per_tile;
+    if (p.stride == 0) p.stride = p.rows;
     if (p.tiles == 0 || p.n_nets == 0) return NOMA_OK;
     // one wave of resident CTAs split evenly over the nets (rounded down: a
     // partial second wave would double the time of a few-net launch)

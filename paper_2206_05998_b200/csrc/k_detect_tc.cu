@@ -152,6 +152,7 @@ __device__ __forceinline__ void put4(char *hi, char *lo, int r, int k, int kb, f
 struct DetectTcParams {
     NetGeom g;
     int n_nets, K, rows, tiles;  // rows = data symbols per slot; tiles of 64 symbols
+    int stride;                  // row stride of data / truth / soft / codes
     const float *data;           // [S][rows][M] complex f32
     const float *plans;
     const uint8_t *truth;        // [S][rows][K] codes, nullable
@@ -305,14 +306,14 @@ __global__ void __launch_bounds__(WsRoles<W0, NL>::kThreads, 1) detect_ws_kernel
         const int s = tile * 64 + (r >> 1);
         if (!(r & 1) && s < p.rows) {
             const uint8_t code = (uint8_t)((y < 0.f ? 1 : 0) | (yo < 0.f ? 2 : 0));  // eval.cpp:41-42
-            if (p.codes) p.codes[(size_t)net * p.rows + s] = code;
-            if (p.soft) *reinterpret_cast<float2 *>(p.soft + ((size_t)net * p.rows + s) * 2) = make_float2(y, yo);
+            if (p.codes) p.codes[(size_t)net * p.stride + s] = code;
+            if (p.soft) *reinterpret_cast<float2 *>(p.soft + ((size_t)net * p.stride + s) * 2) = make_float2(y, yo);
             if (p.truth) my_err += __popc((unsigned)(truth ^ code) & 3u);
         }
     };
     auto truth_of = [&](int tile, int r) -> uint8_t {
         const int s = tile * 64 + (r >> 1);
-        return p.truth && !(r & 1) && s < p.rows ? p.truth[((size_t)d * p.rows + s) * p.K + k] : (uint8_t)0;
+        return p.truth && !(r & 1) && s < p.rows ? p.truth[((size_t)d * p.stride + s) * p.K + k] : (uint8_t)0;
     };
     // sum_c relu(v_c + b_c) w_c over 16 columns
     // (partials: acc2[0] = columns 4j, 4j+1; acc2[1] = 4j+2, 4j+3)
@@ -391,7 +392,7 @@ __global__ void __launch_bounds__(WsRoles<W0, NL>::kThreads, 1) detect_ws_kernel
         const int r = threadIdx.x, sym = r >> 1;
         const bool odd = r & 1;
         const uint32_t trow = tmem + ((uint32_t)(warp * 32) << 16);
-        const float2 *src = reinterpret_cast<const float2 *>(p.data) + (size_t)d * p.rows * M;
+        const float2 *src = reinterpret_cast<const float2 *>(p.data) + (size_t)d * p.stride * M;
         float2 xs[M];
         auto load = [&](int tile) {
             const int s = tile * 64 + sym;
@@ -649,6 +650,7 @@ int detect_tc_launch(const DetectParams &dp, cudaStream_t st) {
     p.n_nets = dp.n_nets;
     p.K = dp.K;
     p.rows = dp.rows;
+    p.stride = dp.stride ? dp.stride : dp.rows;
     p.tiles = (dp.rows + 63) / 64;
     p.data = dp.data;
     p.plans = dp.plans;

@@ -68,6 +68,8 @@ struct DetectParams {
     uint32_t *errors;       // [net]
     const int *status;      // [net] nullable
     int tiles;              // per net
+    int stride = 0;         // row stride of data / truth / soft / codes (0: rows); a
+                            // launch over rows [r0, r0 + rows) passes offset pointers
     int off_x, off_a0, off_a1, off_ps, off_w0, off_y, off_yp, off_end;
     int mode;               // out: 1 = FFMA kernel, 2 = tcgen05 3xTF32 kernel
 };

@@ -120,3 +120,44 @@ def test_detect_tc_many_nets(A, dims, rows, monkeypatch):
     near = (np.abs(soft.real) < 1e-5 * scale) | (np.abs(soft.imag) < 1e-5 * scale)
     assert np.array_equal(codes[~near], codes_f[~near])
     assert np.all(np.abs(errs.astype(np.int64) - errs_f.astype(np.int64)) <= 2 * near.sum(axis=1))
+
+
+@pytest.mark.parametrize("tc", ["1", "0"])
+def test_detect_host_chunked_upload(A, tc, monkeypatch):
+    """Host buffers of >= 32 MB are uploaded in row chunks on the copy stream,
+    each chunk detected as it lands (strided 2-D copies across designs, ragged
+    last chunk).  Outputs must be bit-identical to the same call on device
+    buffers, which runs one launch."""
+    import torch
+
+    from paper_2206_05998_b200 import native as N
+
+    monkeypatch.setenv("NOMA_DETECT_TC", tc)
+    dims, n_designs, K, rows = [32, 64, 64], 2, 3, 150001
+    M = dims[0] // 2
+    nets = [A.net_from_params(o.dims, o.w0, *o.layers())
+            for o in (random_net_fused(dims, 200 + i) for i in range(n_designs * K))]
+    plans = np.ascontiguousarray(np.stack([n.plan.reshape(-1) for n in nets]))
+    rng = np.random.default_rng(9)
+    x = (rng.normal(size=(n_designs, rows, M)) + 1j * rng.normal(size=(n_designs, rows, M))).astype(np.complex64)
+    assert x.nbytes >= 32 << 20
+    truth = rng.integers(0, 4, size=(n_designs, rows, K), dtype=np.uint8)
+    ctx = A.context()
+    soft = np.zeros((n_designs * K, rows), np.complex64)
+    codes = np.zeros((n_designs * K, rows), np.uint8)
+    errs = np.zeros(n_designs * K, np.uint32)
+    ctx.detect(dims, N.LAYOUT_WIDEN, n_designs, K, rows, x.view(np.float32), plans, truth=truth,
+               soft=soft.view(np.float32), codes=codes, bit_errors=errs)
+    dev = torch.device("cuda", 0)
+    xd = torch.from_numpy(x.view(np.float32)).to(dev)
+    pd = torch.from_numpy(plans).to(dev)
+    td = torch.from_numpy(truth).to(dev)
+    sd = torch.zeros((n_designs * K, rows, 2), dtype=torch.float32, device=dev)
+    cd = torch.zeros((n_designs * K, rows), dtype=torch.uint8, device=dev)
+    ed = torch.zeros(n_designs * K, dtype=torch.int32, device=dev)
+    ctx.detect(dims, N.LAYOUT_WIDEN, n_designs, K, rows, xd, pd, truth=td, soft=sd, codes=cd, bit_errors=ed)
+    torch.cuda.synchronize()
+    assert ctx.detect_mode == (2 if tc == "1" else 1)
+    assert np.array_equal(soft.view(np.float32).reshape(n_designs * K, rows, 2), sd.cpu().numpy())
+    assert np.array_equal(codes, cd.cpu().numpy())
+    assert np.array_equal(errs.astype(np.int64), ed.cpu().numpy().astype(np.int64))
