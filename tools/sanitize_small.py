@@ -32,4 +32,22 @@ for hidden in ([64], [64, 64]):
         print("thr", hidden, api.context().train_mode, api.context().detect_mode, out.bit_errors.ravel())
         os.environ.pop("NOMA_LAT_CLUSTER")
         os.environ.pop("NOMA_DETECT_TC")
+if mode in ("all", "tcmulti"):  # detection CTAs spanning several nets (persistent grid)
+    from paper_2206_05998_b200 import native as N
+    from tests.helpers import random_net_fused
+
+    for dims in ([32, 64, 64], [64, 64]):
+        nd, K, rows = 2, 3, 8000  # 125 tiles per net, 750 over 148 CTAs
+        nets = [api.net_from_params(o.dims, o.w0, *o.layers())
+                for o in (random_net_fused(dims, 300 + i) for i in range(nd * K))]
+        plans = np.ascontiguousarray(np.stack([n.plan.reshape(-1) for n in nets]))
+        rng = np.random.default_rng(3)
+        x = (rng.normal(size=(nd, rows, dims[0] // 2))
+             + 1j * rng.normal(size=(nd, rows, dims[0] // 2))).astype(np.complex64)
+        truth = rng.integers(0, 4, size=(nd, rows, K), dtype=np.uint8)
+        codes = np.zeros((nd * K, rows), np.uint8)
+        errs = np.zeros(nd * K, np.uint32)
+        api.context().detect(dims, N.LAYOUT_WIDEN, nd, K, rows, x.view(np.float32), plans, truth=truth,
+                             codes=codes, bit_errors=errs)
+        print("tcmulti", dims, api.context().detect_mode, errs)
 print("done")
