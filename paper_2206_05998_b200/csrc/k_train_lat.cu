@@ -708,6 +708,10 @@ static_for<NL, 0, -1>([&](auto LC) {
 // the feature-major tile X[width][kSR] of the rows perm[e][start..start+bsz)
 // (zero rows past the batch), IQ-widened (iq_transform.cpp:17-20), and their
 // r0 targets; the training kernel then moves a whole tile with one bulk copy.
+// W = compile-time width (32, 64): the thread's row is read as W/4
+// independent float4 loads and the odd rows' IQ rotation is applied from
+// registers (W = 0: any width, one scalar load per element)
+template <int W>
 __global__ void __launch_bounds__(kBatchRows) lat_prep_kernel(TrainParams p, int total) {
     const int job = blockIdx.x, net = job / total, step = job - net * total;
     const int spe = (p.rows + p.batch - 1) / p.batch;
@@ -721,10 +725,25 @@ __global__ void __launch_bounds__(kBatchRows) lat_prep_kernel(TrainParams p, int
                        : wid ? p.design32 + ((size_t)d * (n >> 1) + (idx >> 1)) * width
                              : p.design32 + ((size_t)d * n + idx) * width;
     const bool odd = wid && idx >= 0 && (idx & 1);
-    for (int k = 0; k < width; ++k) {
-        float v = 0.0f;
-        if (src) v = !odd ? src[k] : (k < M ? src[M + k] : -src[k - M]);
-        xo[k * kSR + r] = v;
+    if constexpr (W > 0) {
+        float v[W];
+#pragma unroll
+        for (int q = 0; q < W / 4; ++q) {
+            const float4 f = src ? reinterpret_cast<const float4 *>(src)[q] : make_float4(0.f, 0.f, 0.f, 0.f);
+            v[4 * q] = f.x;
+            v[4 * q + 1] = f.y;
+            v[4 * q + 2] = f.z;
+            v[4 * q + 3] = f.w;
+        }
+#pragma unroll
+        for (int k = 0; k < W; ++k)  // widened odd row (iq_transform.cpp:17-20): [Im; -Re]
+            xo[k * kSR + r] = !odd ? v[k] : (k < W / 2 ? v[W / 2 + k] : -v[k - W / 2]);
+    } else {
+        for (int k = 0; k < width; ++k) {
+            float v = 0.0f;
+            if (src) v = !odd ? src[k] : (k < M ? src[M + k] : -src[k - M]);
+            xo[k * kSR + r] = v;
+        }
     }
     if (r < kSR - kBatchRows)
         for (int k = 0; k < width; ++k) xo[k * kSR + kBatchRows + r] = 0.0f;
@@ -754,7 +773,13 @@ int train_lat_launch(TrainParams &p, cudaStream_t st) {
         if (!lat_carve(p.g, cs, p.width, (int)total, &c)) continue;
         const size_t smem = (size_t)c.end * sizeof(float);
         if (!prepped) {
-            lat_prep_kernel<<<(unsigned)(p.n_nets * total), kBatchRows, 0, st>>>(p, (int)total);
+            const unsigned jobs = (unsigned)(p.n_nets * total);
+            if (p.width == 32)
+                lat_prep_kernel<32><<<jobs, kBatchRows, 0, st>>>(p, (int)total);
+            else if (p.width == 64)
+                lat_prep_kernel<64><<<jobs, kBatchRows, 0, st>>>(p, (int)total);
+            else
+                lat_prep_kernel<0><<<jobs, kBatchRows, 0, st>>>(p, (int)total);
             if (cudaGetLastError() != cudaSuccess) return NOMA_ERR_CUDA;
             prepped = true;
         }
