@@ -124,12 +124,13 @@ constexpr int kPermWarps = 4;
 __global__ void __launch_bounds__(32 * kPermWarps) perm_kernel(int n_nets, int epochs, int n,
                                                                const uint64_t *shuffle_seeds,
                                                                uint16_t *perm, const uint64_t *jtab) {
-    extern __shared__ uint16_t sbuf[];  // per warp: idx[n], draws[n]
+    extern __shared__ __align__(16) uint16_t sbuf[];  // per warp: idx[n8], draws[n8]
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int job = blockIdx.x * kPermWarps + warp;
     if (job >= n_nets * epochs) return;  // warp-uniform
     const int net = job / epochs, epoch = job % epochs;
-    uint16_t *idx = sbuf + (size_t)warp * 2 * n, *jd = idx + n;
+    const int n8 = (n + 7) & ~7;  // 16-byte aligned arrays
+    uint16_t *idx = sbuf + (size_t)warp * 2 * n8, *jd = idx + n8;
     const Xoshiro r0(substream_seed(shuffle_seeds[net], (uint64_t)epoch));
     const int draws = n - 1, nblk = (draws + kJumpDraws - 1) / kJumpDraws;
     for (int bk = lane; bk < nblk; bk += 32) {
@@ -144,12 +145,26 @@ __global__ void __launch_bounds__(32 * kPermWarps) perm_kernel(int n_nets, int e
     for (int i = lane; i < n; i += 32) idx[i] = (uint16_t)i;
     __syncwarp();
     if (lane == 0) {
-        for (int k = 0; k < draws; ++k) {
-            const int i = n - 1 - k, j = jd[k];
+        // the draws are read eight at a time, one group ahead: loaded inside
+        // the chain they would wait behind the previous swap's stores (same
+        // shared array), doubling the per-step latency
+        auto swap = [&](int k, uint32_t j) {
+            const int i = n - 1 - k;
             const uint16_t t = idx[i];
             idx[i] = idx[j];
             idx[j] = t;
+        };
+        const uint4 *jd4 = reinterpret_cast<const uint4 *>(jd);
+        const int full = draws >> 3;
+        uint4 q = full > 0 ? jd4[0] : make_uint4(0, 0, 0, 0);
+        for (int g = 0; g < full; ++g) {
+            const uint4 cur = q;
+            if (g + 1 < full) q = jd4[g + 1];
+            const uint32_t w[4] = {cur.x, cur.y, cur.z, cur.w};
+#pragma unroll
+            for (int e = 0; e < 8; ++e) swap(8 * g + e, (w[e >> 1] >> (16 * (e & 1))) & 0xFFFFu);
         }
+        for (int k = 8 * full; k < draws; ++k) swap(k, jd[k]);
     }
     __syncwarp();
     uint16_t *out = perm + (size_t)job * n;
@@ -198,7 +213,7 @@ int perm_launch(int n_nets, int epochs, int n, const uint64_t *seeds, uint16_t *
     if ((n - 1 + kJumpDraws - 1) / kJumpDraws > kJumpLo * kJumpHi) return NOMA_ERR_UNSUPPORTED;
     const uint64_t *jt = jump_table();
     if (!jt) return NOMA_ERR_CUDA;
-    const size_t smem = (size_t)kPermWarps * 2 * n * sizeof(uint16_t);
+    const size_t smem = (size_t)kPermWarps * 2 * ((n + 7) & ~7) * sizeof(uint16_t);
     if (smem > 227 * 1024) return NOMA_ERR_UNSUPPORTED;
     cudaFuncSetAttribute(perm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     perm_kernel<<<(jobs + kPermWarps - 1) / kPermWarps, 32 * kPermWarps, smem, st>>>(n_nets, epochs, n,
