@@ -554,22 +554,31 @@ __global__ void __launch_bounds__(kThreads) lls_kernel(LlsParams p) {
             double pe[8], po[8];
 #pragma unroll
             for (int k = 0; k < 8; ++k) pe[k] = po[k] = 0.0;
-            for (int a = 0; a < m; ++a) {
-                double xr, xi;
-                if (cplx_layout) {
-                    const double2 x = *reinterpret_cast<const double2 *>(p.design + (((size_t)d * p.nrow_c + t) * m + a) * 2);
-                    xr = x.x;
-                    xi = x.y;
-                } else {
-                    xr = p.design[((size_t)d * p.nrow_c + t) * m + a];
-                    xi = 0.0;
+            // the row's samples are loaded four at a time, all in flight
+            // before the FMAs (one dependent L2 load per column made this
+            // phase latency-bound); the sums keep the column order
+            for (int a0 = 0; a0 < m; a0 += 4) {
+                double2 xv[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int a = a0 + u;
+                    xv[u] = a >= m ? make_double2(0.0, 0.0)
+                            : cplx_layout
+                                ? *reinterpret_cast<const double2 *>(p.design + (((size_t)d * p.nrow_c + t) * m + a) * 2)
+                                : make_double2(p.design[((size_t)d * p.nrow_c + t) * m + a], 0.0);
                 }
 #pragma unroll
-                for (int k = 0; k < 8; ++k) {
-                    if (k < kn) {
-                        const double w0a = D[2 * (a * K + k0 + k)], w1a = -D[2 * (a * K + k0 + k) + 1];
-                        pe[k] += xr * w0a + xi * w1a;  // row 2t = [Re x; Im x]
-                        po[k] += xi * w0a - xr * w1a;  // row 2t+1 = [Im x; -Re x]
+                for (int u = 0; u < 4; ++u) {
+                    const int a = a0 + u;
+                    if (a >= m) break;
+                    const double xr = xv[u].x, xi = xv[u].y;
+#pragma unroll
+                    for (int k = 0; k < 8; ++k) {
+                        if (k < kn) {
+                            const double w0a = D[2 * (a * K + k0 + k)], w1a = -D[2 * (a * K + k0 + k) + 1];
+                            pe[k] += xr * w0a + xi * w1a;  // row 2t = [Re x; Im x]
+                            po[k] += xi * w0a - xr * w1a;  // row 2t+1 = [Im x; -Re x]
+                        }
                     }
                 }
             }
