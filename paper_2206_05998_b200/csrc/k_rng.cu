@@ -105,6 +105,24 @@ __device__ __forceinline__ void gf2_apply(const uint64_t *__restrict__ m, Xoshir
     x.s2 = o[2];
     x.s3 = o[3];
 }
+// Warp-cooperative y = M x (all 32 lanes, uniform x; every lane gets y):
+// lane l takes rows l + 32 q (coalesced: the warp reads 1 KB of contiguous
+// rows per q), each row's parity is a ballot bit, and row 64 w + 32 h + l is
+// bit 32 h + l of word w.  Stepping one state through J = T^kJumpDraws this
+// way replaces per-lane table jumps, whose lanes each walked a different
+// 8 KB matrix (32 cache lines per load instruction, latency-bound chains).
+__device__ __forceinline__ Xoshiro gf2_warp_apply(const uint64_t *M, const Xoshiro &x, int lane) {
+    uint32_t m[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+        const uint64_t *row = M + 4 * (lane + 32 * q);
+        const uint64_t v = (__ldg(row) & x.s0) ^ (__ldg(row + 1) & x.s1) ^ (__ldg(row + 2) & x.s2) ^
+                           (__ldg(row + 3) & x.s3);
+        m[q] = __ballot_sync(0xffffffffu, __popcll(v) & 1);
+    }
+    return Xoshiro(m[0] | ((uint64_t)m[1] << 32), m[2] | ((uint64_t)m[3] << 32), m[4] | ((uint64_t)m[5] << 32),
+                   m[6] | ((uint64_t)m[7] << 32));
+}
 // advance x by `block` blocks of kJumpDraws draws
 __device__ __forceinline__ void jump_blocks(const uint64_t *tab, int block, Xoshiro &x) {
     const int lo = block % kJumpLo, hi = block / kJumpLo;
@@ -133,9 +151,17 @@ __global__ void __launch_bounds__(32 * kPermWarps) perm_kernel(int n_nets, int e
     uint16_t *idx = sbuf + (size_t)warp * 2 * n8, *jd = idx + n8;
     const Xoshiro r0(substream_seed(shuffle_seeds[net], (uint64_t)epoch));
     const int draws = n - 1, nblk = (draws + kJumpDraws - 1) / kJumpDraws;
-    for (int bk = lane; bk < nblk; bk += 32) {
-        Xoshiro r = r0;
-        jump_blocks(jtab, bk, r);
+    // block bk's state is J^bk r0 (J = lo[1] of the jump table): the warp steps
+    // one state through J and lane t keeps the t-th of each 32
+    Xoshiro x = r0;
+    for (int base = 0; base < nblk; base += 32) {
+        Xoshiro r = x;
+        for (int t = 0; t < 32 && base + t < nblk; ++t) {
+            if (lane == t) r = x;
+            x = gf2_warp_apply(jtab + 1024, x, lane);
+        }
+        const int bk = base + lane;
+        if (bk >= nblk) continue;
         const int k_end = min(draws, (bk + 1) * kJumpDraws);
         for (int k = bk * kJumpDraws; k < k_end; ++k) {  // draw k is for i = n-1-k
             const int i = n - 1 - k;
@@ -260,9 +286,20 @@ __global__ void __launch_bounds__(kInitThreads) init_block_kernel(
                               : Xoshiro(seeds[net]);
     constexpr int G = kJumpDraws / 2;  // gaussians per block
     const int blocks = (total + G - 1) / G;
-    for (int b = tid; b < blocks; b += kInitThreads) {
-        Xoshiro r = r0;
-        jump_blocks(jtab, b, r);
+    // chunks of 32 blocks per warp: the chunk's first state by c steps of
+    // J^32 (lo[32]), then the warp steps through J (lo[1]) and lane t keeps
+    // block 32 c + t (gf2_warp_apply)
+    const int warp = tid >> 5, lane = tid & 31;
+    for (int c = warp; 32 * c < blocks; c += kInitThreads / 32) {
+        Xoshiro x = r0;
+        for (int i = 0; i < c; ++i) x = gf2_warp_apply(jtab + 32 * 1024, x, lane);
+        Xoshiro r = x;
+        for (int t = 0; t < 32 && 32 * c + t < blocks; ++t) {
+            if (lane == t) r = x;
+            x = gf2_warp_apply(jtab + 1024, x, lane);
+        }
+        const int b = 32 * c + lane;
+        if (b >= blocks) continue;
         const int w_end = min(total, (b + 1) * G);
         int l = 1;
         for (int w = b * G; w < w_end; ++w) {
