@@ -348,10 +348,10 @@ __global__ void __launch_bounds__(WsRoles<W0, NL>::kThreads, 1) detect_ws_kernel
         }
     };
     // drain D[slot] of tile i into registers and release the slot / columns
-    auto drain = [&](int i, uint32_t trow, uint32_t (&v)[H / 16][16]) {
+    auto drain = [&](uint32_t col, uint32_t trow, uint32_t (&v)[H / 16][16]) {
         const long long tl0 = ck ? clock64() : 0;
 #pragma unroll
-        for (int c = 0; c < H / 16; ++c) tmem_ld16_nw(trow + kD + (i & 1) * H + 16 * c, v[c]);
+        for (int c = 0; c < H / 16; ++c) tmem_ld16_nw(trow + col + 16 * c, v[c]);
         tmem_wait_ld();
         if (ck) cv[3] += clock64() - tl0;
         asm volatile("tcgen05.fence::before_thread_sync;");
@@ -490,7 +490,8 @@ __global__ void __launch_bounds__(WsRoles<W0, NL>::kThreads, 1) detect_ws_kernel
             wait(0, bar(kM1Done + sl), ph);
             asm volatile("tcgen05.fence::after_thread_sync;");
             uint32_t v1[H / 16][16];
-            drain(i, trow, v1);
+            // two layers: the layer-1 accumulator lives in A2[sl]'s hi half
+            drain(NL > 1 ? kA2 + sl * kA2S : kD + sl * H, trow, v1);
             if constexpr (NL == 1) {
                 ws_arrive(bar(kDEmpty + sl));
                 finish(i, first + j, r, v1, bias, truth);
@@ -529,7 +530,6 @@ __global__ void __launch_bounds__(WsRoles<W0, NL>::kThreads, 1) detect_ws_kernel
                             cv[4] += te1 - te0;
                             cv[5] += clock64() - te1;
                         }
-                        // (the first half also says: D[sl] drained, layer 2 may overwrite it)
                         ws_arrive(bar(kA2Full + 2 * sl + c / 2));
                     }
                 }
@@ -550,7 +550,7 @@ __global__ void __launch_bounds__(WsRoles<W0, NL>::kThreads, 1) detect_ws_kernel
             wait(0, bar(kM2Done + sl), ph);
             asm volatile("tcgen05.fence::after_thread_sync;");
             uint32_t v2[H / 16][16];
-            drain(i, trow, v2);
+            drain(kD + sl * H, trow, v2);
             ws_arrive(bar(kDEmpty + sl));
             finish(i, first + j, r, v2, bias + H, truth);
         }
@@ -559,11 +559,14 @@ __global__ void __launch_bounds__(WsRoles<W0, NL>::kThreads, 1) detect_ws_kernel
         constexpr uint32_t id1 = umma_idesc_tf32(H);
         const uint64_t b1hd = umma_desc(tc_s2u(b1h), 128, KB0 * 128), b1ld = umma_desc(tc_s2u(b1l), 128, KB0 * 128);
         const int sl = warp - R::kMma1Warp;
-        const uint32_t dcol = tmem + kD + sl * H;
+        // two layers: accumulate into A2[sl]'s hi half, free once tile i-2's
+        // layer-2 MMAs are done -- one hand-off earlier than D, which waits
+        // for the final epilogue's drain (one hidden layer: D)
+        const uint32_t dcol = NL > 1 ? tmem + kA2 + sl * kA2S : tmem + kD + sl * H;
         for (int i = ib + ((sl ^ ib) & 1); i < ib + ntile; i += 2) {
             const uint32_t ph = (i >> 1) & 1;
             wait(0, bar(kA1Full + sl), ph);
-            wait(1, bar(kDEmpty + sl), ph ^ 1);  // the final epilogue has drained tile i-2
+            wait(1, bar(NL > 1 ? kM2Done + sl : kDEmpty + sl), ph ^ 1);  // tile i-2's slot is free
             asm volatile("tcgen05.fence::after_thread_sync;");
             if (lane == 0) {
                 if constexpr (kA1T) {
@@ -597,6 +600,7 @@ __global__ void __launch_bounds__(WsRoles<W0, NL>::kThreads, 1) detect_ws_kernel
         const int sl = warp - R::kMma2Warp;
         const uint32_t a2 = tmem + kA2 + sl * kA2S, dcol = tmem + kD + sl * H;
         for (int i = ib + ((sl ^ ib) & 1); i < ib + ntile; i += 2) {
+            wait(1, bar(kDEmpty + sl), ((i >> 1) & 1) ^ 1);  // the final epilogue has drained D (tile i-2)
 #pragma unroll
             for (int half = 0; half < 2; ++half) {
                 // epilogue 1 has drained D[sl] and filled this column half of A2[sl]
