@@ -1,24 +1,31 @@
 #!/usr/bin/env python
 """Benchmark of the B200-native NOMA detector hot path (one JSON line).
 
-Metric (BASELINE.json): detected symbols/sec of per-slot train+detect, with
-the per-slot latency (us) of a single slot reported beside it.  A step is one
-pass of the whole hot path -- LLS init, fused pilot training (50 epochs,
-batch 128, Adam), data-phase detection with hard decisions and BER counters --
-over one batch of synthetic slots resident in HBM.  Default workload:
-BASELINE configs[1] (C2: M=16, K=6 QPSK, dims [32,64,64], IQ symmetry on,
-N_T=685, N_D=3840, 25 dB, near-far 3 dB steps, cubic distortion 0.05),
-S slots per GPU (weak scaling over GPUs; slots are independent -- no
-collective on the data path).
+Metric (BASELINE.json): detected symbols/sec of per-slot train+detect at
+1/2/4/8 B200, with the per-slot train+detect latency (us) of a single slot
+(C1 and C2, the north star's sub-millisecond configs) in the same line.  A
+step is one pass of the whole hot path -- LLS init, fused pilot training (50
+epochs, batch 128, Adam), data-phase detection with hard decisions and
+BER/SER counters -- over the workload's slots, resident in HBM.
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2] [--slots S]
+Default workload: BASELINE configs[4] (C5: M=32 antennas, K=16 QPSK users,
+dims [64,64], N_T=685, N_D=3840, 25 dB, 1 dB near-far steps, cubic distortion
+0.05), 32768 slots in total, split contiguously over the N ranks (strong
+scaling; slots are independent -- no collective on the data path, SURVEY
+8(e)).  --config c4 is BASELINE configs[3] (4096 slots of M=64, K=32).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config c5] [--slots S]
   python bench.py --impl reference ...   # the CPU path (oracle port) on host cores
+
+--gpus N without a torchrun environment re-launches itself under
+torch.distributed.run with N ranks (one per GPU, NCCL).
 """
 from __future__ import annotations
 
 import argparse
 import json
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -32,13 +39,13 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 CONFIGS = {
-    # tag: (M, K, hidden, power step dB, default slots per GPU)
-    "c1": dict(M=16, K=6, hidden=[64], step=3.0, slots=148),
-    "c2": dict(M=16, K=6, hidden=[64, 64], step=3.0, slots=148),
-    "c4": dict(M=64, K=32, hidden=[64], step=1.0, slots=148),
-    "c5": dict(M=32, K=16, hidden=[64], step=1.0, slots=148),
+    # tag: M, K, hidden, power step dB, slots (total over all ranks), scaling
+    "c1": dict(M=16, K=6, hidden=[64], step=3.0, slots=148, scaling="weak"),
+    "c2": dict(M=16, K=6, hidden=[64, 64], step=3.0, slots=148, scaling="weak"),
+    "c4": dict(M=64, K=32, hidden=[64], step=1.0, slots=4096, scaling="strong"),
+    "c5": dict(M=32, K=16, hidden=[64], step=1.0, slots=32768, scaling="strong"),
     # data phase only: frozen trained weights, 2^20 data symbols x K users per slot
-    "c3": dict(M=16, K=6, hidden=[64, 64], step=3.0, slots=1, nd=1 << 20),
+    "c3": dict(M=16, K=6, hidden=[64, 64], step=3.0, slots=1, nd=1 << 20, scaling="weak"),
 }
 NT, ND, SNR, GAIN, EPOCHS, BATCH, LR = 685, 3840, 25.0, 0.05, 50, 128, 0.005
 
@@ -51,6 +58,48 @@ def flops_per_net(dims, rows=2 * NT, epochs=EPOCHS, nd=ND):
     train = (fwd + bwd) * rows * epochs
     detect = (2 * dims[0] + fwd) * 2 * nd
     return train, detect
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def relaunch_under_torchrun(nproc):
+    """--gpus N outside torchrun: one rank per GPU via torch.distributed.run."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={nproc}",
+           "--master-addr", "127.0.0.1", f"--master-port={_free_port()}", os.path.abspath(__file__),
+           *sys.argv[1:]]
+    return subprocess.call(cmd)
+
+
+def dist_env():
+    return (int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("RANK", "0")),
+            int(os.environ.get("LOCAL_RANK", "0")))
+
+
+def dry_run(args, cfg):
+    """Launcher / partition / MAX-reduction check without a GPU (gloo): every
+    rank computes its slot range; rank 0 prints the partition as JSON."""
+    import torch.distributed as dist
+
+    from paper_2206_05998_b200 import shard
+
+    world, rank, _ = dist_env()
+    if world > 1:
+        dist.init_process_group("gloo")
+    total = cfg["slots"]
+    ranges = shard.gather_to_rank0(np.array([shard.slot_range(total, world, rank)], dtype=np.int64))
+    tmax = shard.max_over_ranks(1.0 + rank)
+    if rank == 0:
+        print(json.dumps({"dry_run": True, "n_gpus": world, "total_slots": total,
+                          "ranges": ranges.tolist(), "max_over_ranks": tmax}), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
 
 
 # ----------------------------------------------------------------- clocks
@@ -117,33 +166,57 @@ def run_cpu_sample(cfg, n_slots, threads, seed0=1000):
     return time.perf_counter() - t0
 
 
+def cpu_model():
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for line in out.splitlines():
+            if line.startswith("Model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return None
+
+
+def cpu_latency_us(tag, runs=5):
+    """Single-core per-slot train+detect latency of the CPU path (one slot,
+    the K users trained and detected one after another, eval.cpp:228-241):
+    median of `runs`."""
+    cfg = CONFIGS[tag]
+    return 1e6 * statistics.median(run_cpu_sample(cfg, 1, 1, 7000 + i) for i in range(runs))
+
+
 def reference_arm(args, cfg, tag):
     """The reference's CPU path (FP64 oracle port; the reference itself needs
-    Eigen 3.4, absent here) on the host cores: rank 0 only."""
-    rank = int(os.environ.get("RANK", "0"))
+    Eigen 3.4, absent here) on all host cores: rank 0 only.  A step is a
+    bounded sample of the workload: 4 x nproc slots, one slot per thread."""
+    _, rank, _ = dist_env()
     if rank != 0:
         return
     threads = os.cpu_count() or 1
-    n_slots = threads
-    for _ in range(args.warmup):
-        run_cpu_sample(cfg, n_slots, threads)
+    n_slots = 4 * threads
+    for i in range(args.warmup):
+        run_cpu_sample(cfg, n_slots, threads, 90000 + i * n_slots)
     times = [run_cpu_sample(cfg, n_slots, threads, 5000 + i * n_slots) for i in range(args.steps)]
     sym = n_slots * cfg["K"] * ND
     value = sym / statistics.mean(times)
+    lat = {f"latency_{t}_us_per_slot_1core": cpu_latency_us(t) for t in ("c1", "c2")}
     print(json.dumps({
         "impl": "reference", "metric": "detected symbols/sec (per-slot train+detect)",
         "value": value, "unit": "symbols/s", "n_gpus": args.gpus, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": 1e3 * statistics.mean(times),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (reference channel simulator, seeds 5000+)",
+        "higher_is_better": True, "scaling": cfg["scaling"], "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (reference channel simulator restated in the oracle, seeds 5000+)",
         "config": {"workload": f"{tag}: M={cfg['M']} K={cfg['K']} dims={[2 * cfg['M']] + cfg['hidden']} "
-                               f"N_T={NT} N_D={ND} {EPOCHS} epochs batch {BATCH}; {n_slots} slots per step",
+                               f"N_T={NT} N_D={ND} {EPOCHS} epochs batch {BATCH}; bounded sample of "
+                               f"{n_slots} slots per step (4 x {threads} host threads)",
                    "parallelism": f"{threads} host threads, one slot per thread"},
         "cpu_baseline": {"value": value, "unit": "symbols/s", "cores": threads, "kind": "port",
-                         "sample": f"{n_slots} slots x {cfg['K']} users per step"},
+                         "sample": f"{n_slots} slots x {cfg['K']} users per step, FP64 oracle port "
+                                   f"(reference unbuildable: Eigen 3.4 absent)", "cpu_model": cpu_model()},
         "e2e": {"value": value, "unit": "symbols/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
-        "latency_us_per_slot_1core": None,
+        **lat,
+        "latency_note": "single core, one slot (K users trained + detected in turn), median of 5",
     }), flush=True)
 
 
@@ -360,15 +433,54 @@ def detect_only(args, cfg):
 
 
 # ----------------------------------------------------------------- ours
+def slot_latency_us(ctx, N, tag, seed, dev, stream, runs=5, warm=2):
+    """Single-slot train+detect latency (one slot, all K user nets), device
+    time on the launching stream: median of `runs` after `warm` calls."""
+    import torch
+    from paper_2206_05998_b200.seeds import slot_user_seeds
+
+    c = CONFIGS[tag]
+    M, K = c["M"], c["K"]
+    dims = [2 * M] + c["hidden"]
+    s1 = torch.tensor([seed], dtype=torch.int64, device=dev)
+    px = torch.empty((1, NT, M, 2), dtype=torch.float64, device=dev)
+    py = torch.empty((1, NT, K, 2), dtype=torch.float64, device=dev)
+    dx = torch.empty((1, ND, M, 2), dtype=torch.float32, device=dev)
+    tr = torch.empty((1, ND, K), dtype=torch.uint8, device=dev)
+    ctx.synthesize(N.Scenario(K, M, NT, ND, c["step"], SNR, GAIN), s1, px, py, dx, tr)
+    i1, h1 = slot_user_seeds(np.array([seed], np.uint64), K)
+    i1 = torch.from_numpy(i1.view(np.int64)).to(dev)
+    h1 = torch.from_numpy(h1.view(np.int64)).to(dev)
+    st = torch.empty((1, K), dtype=torch.int32, device=dev)
+    er = torch.empty((1, K), dtype=torch.int32, device=dev)
+    se = torch.empty((1, K), dtype=torch.int32, device=dev)
+    co = torch.empty((1, K, ND), dtype=torch.uint8, device=dev)
+    tcfg = N.TrainCfg.of(EPOCHS, BATCH, LR)
+    lat = []
+    for i in range(warm + runs):
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        ctx.pipeline(dims, tcfg, 1, K, M, NT, ND, px, py, dx, tr, i1, h1, st, codes=co, bit_errors=er,
+                     symbol_errors=se)
+        b.record(stream)
+        b.synchronize()
+        if i >= warm:
+            lat.append(a.elapsed_time(b) * 1e3)
+    return statistics.median(lat), ctx.train_mode
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
-    ap.add_argument("--slots", type=int, default=0, help="slots per GPU (default per config)")
+    ap.add_argument("--config", default="c5", choices=sorted(CONFIGS))
+    ap.add_argument("--slots", type=int, default=0, help="total slots over all ranks (default per config)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--dry-run", action="store_true", help="launcher/partition check without a GPU")
     args = ap.parse_args()
     cfg = dict(CONFIGS[args.config])
     if args.slots:
@@ -377,15 +489,17 @@ def main():
         if args.config == "c3":
             return reference_detect_arm(args, cfg)
         return reference_arm(args, cfg, args.config)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(relaunch_under_torchrun(args.gpus))
+    if args.dry_run:
+        return dry_run(args, cfg)
     if args.config == "c3":
         return detect_only(args, cfg)
 
     import torch
     import torch.distributed as dist
 
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
+    world, rank, local = dist_env()
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
@@ -394,7 +508,9 @@ def main():
     from paper_2206_05998_b200 import shard
     from paper_2206_05998_b200.seeds import slot_user_seeds
 
-    M, K, S = cfg["M"], cfg["K"], cfg["slots"]
+    M, K = cfg["M"], cfg["K"]
+    total = cfg["slots"] * (world if cfg["scaling"] == "weak" else 1)
+    S = shard.slot_range(total, world, rank)[1] - shard.slot_range(total, world, rank)[0]
     dims = [2 * M] + cfg["hidden"]
     ctx = N.Context(local)
     stream = torch.cuda.Stream(device=local)  # a real stream (the legacy default is handle 0)
@@ -403,20 +519,23 @@ def main():
     dev = torch.device("cuda", local)
 
     # ---- synthetic inputs, generated on device (not timed) ----------------
-    seeds = shard.slot_seeds(world * S, world, rank)  # this rank's slots, no overlap
-    seeds_d = torch.from_numpy(seeds.astype(np.int64)).to(dev)
+    seeds = shard.slot_seeds(total, world, rank)  # this rank's slots, no overlap
     px = torch.empty((S, NT, M, 2), dtype=torch.float64, device=dev)
     py = torch.empty((S, NT, K, 2), dtype=torch.float64, device=dev)
     dx = torch.empty((S, ND, M, 2), dtype=torch.float32, device=dev)
     truth = torch.empty((S, ND, K), dtype=torch.uint8, device=dev)
     sc = N.Scenario(K, M, NT, ND, cfg["step"], SNR, GAIN)
-    ctx.synthesize(sc, seeds_d, px, py, dx, truth)
+    for a in range(0, S, 4096):  # bounded synthesis scratch
+        b = min(S, a + 4096)
+        ctx.synthesize(sc, torch.from_numpy(seeds[a:b].view(np.int64)).to(dev), px[a:b], py[a:b], dx[a:b],
+                       truth[a:b])
     init_s, shuf_s = slot_user_seeds(seeds, K)
-    init_d = torch.from_numpy(init_s.astype(np.int64)).to(dev)
-    shuf_d = torch.from_numpy(shuf_s.astype(np.int64)).to(dev)
+    init_d = torch.from_numpy(init_s.view(np.int64)).to(dev)
+    shuf_d = torch.from_numpy(shuf_s.view(np.int64)).to(dev)
     nets = S * K
     status = torch.empty((S, K), dtype=torch.int32, device=dev)
     errs = torch.empty((S, K), dtype=torch.int32, device=dev)
+    sers = torch.empty((S, K), dtype=torch.int32, device=dev)
     codes = torch.empty((S, K, ND), dtype=torch.uint8, device=dev)
     plans = torch.empty((S, K, N.plan_size(dims)), dtype=torch.float32, device=dev)
     w0 = torch.empty((S, K, 2 * M), dtype=torch.float64, device=dev)
@@ -425,16 +544,17 @@ def main():
 
     def step():
         ctx.pipeline(dims, tcfg, S, K, M, NT, ND, px, py, dx, truth, init_d, shuf_d, status,
-                     w0=w0, plans=plans, codes=codes, bit_errors=errs)
+                     w0=w0, plans=plans, codes=codes, bit_errors=errs, symbol_errors=sers)
 
     peak_fp32 = ctx.measure_fp32_tflops(0)
-    peak_tile = ctx.measure_fp32_tflops(1)
+    peak_tile = ctx.measure_fp32_tflops(2)
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
     assert int((status != 0).sum()) == 0, "LLS flagged an ill-conditioned slot"
 
-    # ---- timed region: device time per step (CUDA events), L2 flushed between
+    # ---- timed region: device time per step (CUDA events on the launching
+    # stream), L2 flushed between steps (inputs are far larger than L2 too)
     ctx.set_profiling(True)
     launches0 = ctx.kernel_launches
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
@@ -456,10 +576,12 @@ def main():
     if world > 1:
         dist.barrier()
     launches = ctx.kernel_launches - launches0
+    train_mode = ctx.train_mode
+    nchunks = ctx.pipeline_chunks
     ctx.set_profiling(False)
     step_ms = [a.elapsed_time(b) for a, b in ev]
     total_ms = shard.max_over_ranks(sum(step_ms), dev)  # the slowest rank
-    sym_per_step = S * K * ND * world
+    sym_per_step = total * K * ND
     value = sym_per_step * args.steps / (total_ms * 1e-3)
 
     train_ms = statistics.mean(p["train"] for p in phases)
@@ -472,28 +594,32 @@ def main():
 
     # ---- e2e: public C-ABI with pinned HOST buffers, copies inside -------
     def pinned(tensor):
-        h = torch.empty(tensor.shape, dtype=tensor.dtype, pin_memory=True)
-        h.copy_(tensor)
-        return h.numpy()
+        h = N.pinned_empty(tuple(tensor.shape), {torch.float64: np.float64, torch.float32: np.float32,
+                                                 torch.uint8: np.uint8, torch.int32: np.int32}[tensor.dtype])
+        torch.from_numpy(h).copy_(tensor)
+        return h
 
     h_px, h_py, h_dx, h_truth = pinned(px), pinned(py), pinned(dx), pinned(truth)
     h_init, h_shuf = init_s.copy(), shuf_s.copy()
-    h_status = pinned(status)
-    h_errs = np.empty((S, K), dtype=np.uint32)
-    h_codes = pinned(codes)
+    h_status = N.pinned_empty((S, K), np.int32)
+    h_errs = N.pinned_empty((S, K), np.uint32)
+    h_sers = N.pinned_empty((S, K), np.uint32)
+    h_codes = N.pinned_empty((S, K, ND), np.uint8)
     h2d = h_px.nbytes + h_py.nbytes + h_dx.nbytes + h_truth.nbytes + h_init.nbytes + h_shuf.nbytes
-    d2h = h_status.nbytes + h_errs.nbytes + h_codes.nbytes
+    d2h = h_status.nbytes + h_errs.nbytes + h_sers.nbytes + h_codes.nbytes
 
     def step_host():
         ctx.pipeline(dims, tcfg, S, K, M, NT, ND, h_px.view(np.float64), h_py.view(np.float64),
                      h_dx.view(np.float32), h_truth, h_init, h_shuf, h_status, codes=h_codes,
-                     bit_errors=h_errs)
+                     bit_errors=h_errs, symbol_errors=h_sers)
 
     step_host()
     e2e_ms = []
-    for _ in range(max(1, min(args.steps, 3))):
+    for _ in range(max(1, min(args.steps, args.e2e_steps))):
         flush.zero_()
         torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
         a = torch.cuda.Event(enable_timing=True)
         b = torch.cuda.Event(enable_timing=True)
         a.record(stream)
@@ -502,52 +628,15 @@ def main():
         b.synchronize()
         e2e_ms.append(a.elapsed_time(b))
     e2e_value = sym_per_step / (shard.max_over_ranks(statistics.mean(e2e_ms), dev) * 1e-3)
-    all_errs = shard.gather_to_rank0(h_errs.astype(np.int64))  # per-slot BER counters
+    all_errs = shard.gather_to_rank0(np.asarray(h_errs, dtype=np.int64))  # per-slot BER counters
+    all_sers = shard.gather_to_rank0(np.asarray(h_sers, dtype=np.int64))
     bit_err_total = int(all_errs.sum()) if all_errs is not None else None
+    ser_total = int(all_sers.sum()) if all_sers is not None else None
+    del h_px, h_py, h_dx, h_truth
 
-    # ---- single-slot latency (C-config, S=1) -------------------------------
-    lat = []
-    for i in range(5):
-        a = torch.cuda.Event(enable_timing=True)
-        b = torch.cuda.Event(enable_timing=True)
-        a.record(stream)
-        ctx.pipeline(dims, tcfg, 1, K, M, NT, ND, px[:1], py[:1], dx[:1], truth[:1], init_d[:1],
-                     shuf_d[:1], status[:1], codes=codes[:1], bit_errors=errs[:1])
-        b.record(stream)
-        b.synchronize()
-        if i >= 2:
-            lat.append(a.elapsed_time(b) * 1e3)
-
-    # ---- single-slot latency at C1 (the north star's sub-ms target config) --
-    lat_c1 = None
-    if args.config != "c1":
-        c1 = CONFIGS["c1"]
-        M1, K1 = c1["M"], c1["K"]
-        dims1 = [2 * M1] + c1["hidden"]
-        s1 = torch.from_numpy(seeds[:1].astype(np.int64)).to(dev)
-        px1 = torch.empty((1, NT, M1, 2), dtype=torch.float64, device=dev)
-        py1 = torch.empty((1, NT, K1, 2), dtype=torch.float64, device=dev)
-        dx1 = torch.empty((1, ND, M1, 2), dtype=torch.float32, device=dev)
-        tr1 = torch.empty((1, ND, K1), dtype=torch.uint8, device=dev)
-        ctx.synthesize(N.Scenario(K1, M1, NT, ND, c1["step"], SNR, GAIN), s1, px1, py1, dx1, tr1)
-        i1, h1 = slot_user_seeds(seeds[:1], K1)
-        i1 = torch.from_numpy(i1.astype(np.int64)).to(dev)
-        h1 = torch.from_numpy(h1.astype(np.int64)).to(dev)
-        st1 = torch.empty((1, K1), dtype=torch.int32, device=dev)
-        er1 = torch.empty((1, K1), dtype=torch.int32, device=dev)
-        co1 = torch.empty((1, K1, ND), dtype=torch.uint8, device=dev)
-        l1 = []
-        for i in range(5):
-            a = torch.cuda.Event(enable_timing=True)
-            b = torch.cuda.Event(enable_timing=True)
-            a.record(stream)
-            ctx.pipeline(dims1, tcfg, 1, K1, M1, NT, ND, px1, py1, dx1, tr1, i1, h1, st1,
-                         codes=co1, bit_errors=er1)
-            b.record(stream)
-            b.synchronize()
-            if i >= 2:
-                l1.append(a.elapsed_time(b) * 1e3)
-        lat_c1 = statistics.median(l1)
+    # ---- single-slot latency (BASELINE C1 / C2, the sub-ms target) --------
+    lat_c1, mode_c1 = slot_latency_us(ctx, N, "c1", int(seeds[0]), dev, stream)
+    lat_c2, mode_c2 = slot_latency_us(ctx, N, "c2", int(seeds[0]), dev, stream)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -556,7 +645,8 @@ def main():
         dt = run_cpu_sample(cfg, n, threads, 9000)
         cpu = {"value": n * K * ND / dt, "unit": "symbols/s", "cores": threads, "kind": "port",
                "sample": f"{n} slots x {K} users ({n * K} full 50-epoch trainings + detections), "
-                         f"{dt:.1f} s, FP64 oracle port (reference unbuildable: Eigen absent)"}
+                         f"{dt:.1f} s, FP64 oracle port (reference unbuildable: Eigen absent)",
+               "cpu_model": cpu_model()}
 
     if rank == 0:
         clocks = clk.summary()
@@ -564,34 +654,46 @@ def main():
             "metric": "detected symbols/sec (per-slot train+detect)",
             "value": value, "unit": "symbols/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "higher_is_better": True, "scaling": cfg["scaling"], "vs_baseline": None, "dtype": "f32",
             "data": "synthetic (device port of the reference channel simulator; seeds 1000+slot)",
             "config": {"workload": f"{args.config}: M={M} K={K} QPSK dims={dims} N_T={NT} N_D={ND} "
                                    f"{EPOCHS} epochs batch {BATCH} Adam lr {LR}, IQ symmetry on, "
                                    f"SNR {SNR} dB, step {cfg['step']} dB, gamma {GAIN}; "
-                                   f"{S} slots per GPU per step",
-                       "slots_per_gpu": S, "parallelism": f"slot-sharded x{world}, no collective",
-                       "l2": "flushed (256 MiB write) between timed steps"},
-            "latency_us_per_slot": statistics.mean(lat),
-            "latency_note": "one slot (all K user nets) LLS+init+shuffles+50-epoch training+detection, "
-                            "device time; training in the neuron-split cluster kernel (16 CTAs per net)",
+                                   f"{total} slots in total, {S} on rank 0",
+                       "slots_total": total, "slots_per_gpu": S,
+                       "parallelism": f"slot-sharded x{world} ({cfg['scaling']} scaling), no collective",
+                       "l2": "flushed (256 MiB write) between timed steps; inputs "
+                             f"{(px.numel() * 8 + py.numel() * 8 + dx.numel() * 4) / 2**30:.1f} GiB per rank"},
             "latency_c1_us_per_slot": lat_c1,
+            "latency_c2_us_per_slot": lat_c2,
+            "latency_note": "one slot (all K user nets) LLS+init+shuffles+50-epoch training+detection, "
+                            f"device time, median of 5; training kernel modes {mode_c1} (C1) / {mode_c2} (C2): "
+                            "neuron-split cluster per net",
             "phase_ms": {k: statistics.mean(p[k] for p in phases) for k in phases[0]},
-            "roofline": {"bound": "fp32", "kernel": "train_kernel", "achieved": achieved,
-                         "peak": peak_fp32, "unit": "TFLOP/s", "frac": achieved / peak_fp32,
+            "train_kernel_mode": train_mode,
+            "roofline": {"bound": "fp32", "kernel": "train_w4_kernel" if train_mode == 3 else "train_kernel",
+                         "achieved": achieved, "peak": peak_fp32, "unit": "TFLOP/s",
+                         "frac": achieved / peak_fp32,
                          "peak_source": "measured in this run: constant-operand FFMA probe (issue-rate peak)",
                          "register_tile_ceiling": peak_tile,
                          "frac_of_register_tile_ceiling": achieved / peak_tile,
-                         "register_tile_ceiling_source": "measured in this run: 8x4 register outer-product FFMA probe (3-register FFMA is RF-read limited on B200)",
+                         "register_tile_ceiling_source": "measured in this run: 8x4 outer product in FFMA2 "
+                                                         "(the training tiles' instruction form)",
                          "traffic": traffic,
-                         "algorithmic_flop_per_launch": nets * tr_flops},
+                         "algorithmic_flop_per_step": nets * tr_flops,
+                         "launches_per_step": nchunks,
+                         "algorithmic_flop_per_net": tr_flops,
+                         "timing": "train phase = CUDA events around the training launches of every chunk "
+                                   "(Adam table + widened rows + train kernel), summed per step"},
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_value, "unit": "symbols/s", "h2d_bytes_per_step": h2d,
-                    "d2h_bytes_per_step": d2h, "ms_per_step": statistics.mean(e2e_ms)},
+                    "d2h_bytes_per_step": d2h, "ms_per_step": statistics.mean(e2e_ms),
+                    "steps": len(e2e_ms), "host_buffers": "page-locked (noma_host_alloc)"},
             "gpu_launches": launches,
             "clocks": clocks,
             "wall_s_timed_region": t_wall,
             "bit_errors_last_e2e_step": bit_err_total,
+            "symbol_errors_last_e2e_step": ser_total,
         }
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -125,6 +125,8 @@ NOMA_API int noma_ctx_train_mode(noma_ctx_t ctx);
  * kernel (k_detect_tc.cu; widened input 32/64, hidden layers of 64),
  * 0 = none yet.  NOMA_DETECT_TC=0 in the environment forces the FFMA kernel. */
 NOMA_API int noma_ctx_detect_mode(noma_ctx_t ctx);
+/* Slot chunks the last noma_pipeline call ran in (instrumentation). */
+NOMA_API int noma_ctx_pipeline_chunks(noma_ctx_t ctx);
 /* Instrumentation: when on, noma_pipeline records CUDA events around its
  * phases (init and shuffles run on a side stream, overlapping the LLS);
  * noma_ctx_phase_ms waits for the last call and returns ms for
@@ -134,13 +136,21 @@ NOMA_API int noma_ctx_phase_ms(noma_ctx_t ctx, double *ms6);
 /* FP32 FFMA throughput of this device (TFLOP/s) over every SM, the roofline
  * denominators of the FP32-bound training and detection kernels.
  * form 0: FFMA with constant operands (the issue-rate peak);
- * form 1: an 8x4 register outer product, all operands in registers (the
- *         ceiling of any register-tiled FP32 GEMM inner loop on this part --
- *         3-register FFMA is register-file-read limited, profiles/
- *         r01_microbench_ffma_forms.txt). */
+ * form 1: an 8x4 register outer product in scalar FFMA, all operands in
+ *         registers (3-register FFMA is register-file-read limited,
+ *         profiles/r01_microbench_ffma_forms.txt);
+ * form 2: the same outer product in packed FFMA2 with one broadcast operand
+ *         -- the instruction form the training tiles use, so the ceiling of
+ *         their inner loops (profiles/r01_microbench_ffma2.txt). */
 NOMA_API int noma_measure_fp32_tflops(noma_ctx_t ctx, int form, double *tflops);
 
 /* Floats in the FusedPlan buffer for `desc` (fused_inference.cpp:19-42). */
+/* Page-locked host buffers for NOMA_MEM_HOST calls: with them the per-chunk
+ * uploads / downloads of noma_pipeline and noma_detect run asynchronously on
+ * the copy streams (pageable memory serialises every transfer). */
+NOMA_API int noma_host_alloc(size_t bytes, void **out);
+NOMA_API int noma_host_free(void *p);
+
 NOMA_API int noma_plan_size(const noma_net_desc *desc);
 /* Trainable parameters (HybridNetParams::trainable_count, hybrid_nn.cpp:11-16). */
 NOMA_API int noma_param_count(const noma_net_desc *desc);
@@ -203,25 +213,32 @@ NOMA_API int noma_train_f64(noma_ctx_t ctx, const noma_dataset *ds, const noma_n
  *   WIDEN_COMPLEX: data [n_designs][rows][width/2] complex f32 (rows = N_D
  *     symbols); soft [net][rows] complex f32; codes [net][rows] u8 with
  *     bit0 = Re<0, bit1 = Im<0; truth [n_designs][rows][nets_per_design] u8
- *     codes; bit_errors [net] u32.
+ *     codes; bit_errors [net] u32 (mismatched bits, the numerator of
+ *     bit_error_rate); symbol_errors [net] u32 (symbols whose decision
+ *     differs from the truth in either bit: SER numerator).
  *   REAL: data [n_designs][rows][width] f32; soft [net][rows] f32 (no codes).
- * All outputs nullable. */
+ * All outputs nullable.  An ill-conditioned net's counters read 0xFFFFFFFF. */
 NOMA_API int noma_detect(noma_ctx_t ctx, const noma_net_desc *desc, int layout, int n_designs,
                          int nets_per_design, int rows, const float *data, const float *plans,
                          const uint8_t *truth, float *soft, uint8_t *codes, uint32_t *bit_errors,
-                         int mem);
+                         uint32_t *symbol_errors, int mem);
 
 /* One slot batch end to end (noma_cli.cpp:86-160 per user, eval.cpp:228-241):
  * LLS -> init (Rng(init_seeds[net])) -> train (shuffle_seeds[net]) -> detect.
  * pilots/targets as the WIDEN_COMPLEX dataset; data_rx [S][ND][M] complex f32;
- * truth [S][ND][K] codes (nullable).  Outputs nullable except status. */
+ * truth [S][ND][K] codes (nullable).  Outputs nullable except status;
+ * bit_errors / symbol_errors [S][K] as noma_detect.  Slots run in chunks of
+ * bounded scratch (NOMA_CHUNK_MB, default 4096); with NOMA_MEM_HOST each
+ * chunk's inputs are uploaded ahead on a copy stream and its results
+ * downloaded while the next chunk computes.  Networks wider than 128 or
+ * minibatches above 128 rows return NOMA_ERR_UNSUPPORTED before any work. */
 NOMA_API int noma_pipeline(noma_ctx_t ctx, const noma_net_desc *desc, const noma_train_cfg *cfg,
                            int S, int K, int M, int NT, int ND, const double *pilot_rx,
                            const double *pilot_sym, const float *data_rx, const uint8_t *truth,
                            const uint64_t *init_seeds, const uint64_t *shuffle_seeds,
                            double *w0, double *gram_condition, float *plans, double *loss_trace,
-                           float *soft, uint8_t *codes, uint32_t *bit_errors, int *status,
-                           int mem);
+                           float *soft, uint8_t *codes, uint32_t *bit_errors,
+                           uint32_t *symbol_errors, int *status, int mem);
 
 /* Replaces synthesize(cfg, SeedBundle::from_master(seed)) (channel_sim.cpp:76-117)
  * on device for S slots with master seeds [S].  Outputs (nullable):

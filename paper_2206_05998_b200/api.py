@@ -271,6 +271,7 @@ class SlotBatch:
     soft: np.ndarray
     codes: np.ndarray
     bit_errors: np.ndarray
+    symbol_errors: np.ndarray = None
 
 
 def pipeline(dims, pilot_rx, pilot_sym, data_rx, truth_codes, init_seeds, shuffle_seeds,
@@ -287,7 +288,7 @@ def pipeline(dims, pilot_rx, pilot_sym, data_rx, truth_codes, init_seeds, shuffl
     out = SlotBatch(np.zeros((S, K, 2 * M)), np.zeros((S, K)), np.zeros((S, K), np.int32),
                     np.zeros((S, K, ps), np.float32), np.zeros((S, K, max(epochs, 1))),
                     np.zeros((S, K, ND), np.complex64), np.zeros((S, K, ND), np.uint8),
-                    np.zeros((S, K), np.uint32))
+                    np.zeros((S, K), np.uint32), np.zeros((S, K), np.uint32))
     cfg = N.TrainCfg.of(epochs, batch_size, lr)
     context().pipeline(dims, cfg, S, K, M, NT, ND, px.view(np.float64), py.view(np.float64),
                        dx.view(np.float32),
@@ -296,7 +297,8 @@ def pipeline(dims, pilot_rx, pilot_sym, data_rx, truth_codes, init_seeds, shuffl
                        np.ascontiguousarray(shuffle_seeds, np.uint64).reshape(nets),
                        out.status, w0=out.w0, cond=out.gram_condition, plans=out.plans,
                        trace=out.trace if epochs > 0 else None, soft=out.soft.view(np.float32),
-                       codes=out.codes, bit_errors=out.bit_errors if truth_codes is not None else None)
+                       codes=out.codes, bit_errors=out.bit_errors if truth_codes is not None else None,
+                       symbol_errors=out.symbol_errors if truth_codes is not None else None)
     out.trace = out.trace[..., :epochs]
     return out
 

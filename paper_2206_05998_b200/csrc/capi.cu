@@ -2,11 +2,14 @@
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
+#include <array>
 #include <cstring>
 #include <string>
+#include <type_traits>
 #include <vector>
 
 #include "kernels.cuh"
+#include "tiles.cuh"
 
 namespace noma_dev {
 
@@ -89,6 +92,32 @@ __global__ void ffma_outer_kernel(float *out, int iters) {
     if (s == 12345.678f) out[0] = s;
 }
 
+// FFMA2 register-tile probe: the 8 x 4 outer product the training tiles are
+// built from, in packed FP32x2 FMAs (one operand broadcast), no memory traffic.
+__global__ void ffma2_outer_kernel(float *out, int iters) {
+    unsigned long long acc[8][2], wp[8], xp[2];
+    for (int i = 0; i < 8; ++i) {
+        const float w = 1e-3f * (threadIdx.x + i);
+        wp[i] = f2_pack(w, w);
+        acc[i][0] = acc[i][1] = 0ull;
+    }
+    xp[0] = f2_pack(0.5f, 0.25f);
+    xp[1] = f2_pack(0.125f + threadIdx.x * 1e-6f, 0.75f);
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                f2_fma(acc[i][0], wp[i], xp[0]);
+                f2_fma(acc[i][1], wp[i], xp[1]);
+            }
+        wp[it & 7] ^= 1ull;
+    }
+    unsigned long long sacc = 0;
+    for (int i = 0; i < 8; ++i) sacc ^= acc[i][0] ^ acc[i][1];
+    if (sacc == 12345ull) out[0] = 1.f;
+}
+
 // FFMA peak probe: 8 independent FMA chains per thread, no memory traffic.
 __global__ void ffma_peak_kernel(float *out, int iters, float a, float b) {
     float x[8];
@@ -116,21 +145,32 @@ struct noma_ctx_s {
     int train_mode = 0;
     int detect_mode = 0;
     bool profiling = false;
-    // [0] start, [1] after LLS, [2] side start, [3] after init, [4] after
-    // shuffles (side stream), [5] joined, [6] after train, [7] after detect
-    cudaEvent_t ev[8] = {};
+    // per chunk of the last pipeline call: [0] start, [1] after LLS, [2] side
+    // start, [3] after init, [4] after shuffles (side stream), [5] joined,
+    // [6] after train, [7] after detect, [8] shuffle start
+    std::vector<std::array<cudaEvent_t, 9>> pev;
+    int pev_used = 0;
+    int chunks_last = 0;  // slot chunks of the last pipeline call
     cudaStream_t side = nullptr;          // init overlaps the LLS
     cudaStream_t side2 = nullptr;         // shuffles overlap the LLS and the init
     cudaEvent_t fork = nullptr, join = nullptr, join2 = nullptr;
     cudaEvent_t ev_perm0 = nullptr;       // profiling: shuffle start on side2
     cudaEvent_t join3 = nullptr;          // LLS condition numbers (side2, joined at the end)
     cudaStream_t copy = nullptr;          // late host->device input copies (data phase)
+    cudaStream_t copy2 = nullptr;         // per-chunk device->host result copies
     cudaEvent_t ev_alloc = nullptr, copied = nullptr;
 };
 
 namespace {
-inline void mark(noma_ctx_s *c, int i, cudaStream_t s = nullptr) {
-    if (c->profiling) cudaEventRecord(c->ev[i], s ? s : c->stream);
+// profiling event i of pipeline chunk `ch` (events created on first use)
+inline void mark(noma_ctx_s *c, int ch, int i, cudaStream_t s = nullptr) {
+    if (!c->profiling) return;
+    while ((int)c->pev.size() <= ch) {
+        std::array<cudaEvent_t, 9> a{};
+        for (auto &e : a) cudaEventCreate(&e);
+        c->pev.push_back(a);
+    }
+    cudaEventRecord(c->pev[ch][i], s ? s : c->stream);
 }
 }  // namespace
 
@@ -155,10 +195,12 @@ struct Stage {
     struct Back { void *host; const void *dev; size_t bytes; };
     std::vector<Back> backs;
     bool ok = true;
-    bool late = false;  // host->device copies pending on c->copy
+    bool late = false;    // host->device copies pending on c->copy
+    bool forked = false;  // work pending on c->side / c->side2
     Stage(noma_ctx_t c_, int mem_) : c(c_), mem(mem_) {}
     ~Stage() {
         late_join();  // no buffer is freed under an in-flight copy
+        side_join();  // ... nor under a side-stream kernel (early error returns)
         for (void *p : allocs) cudaFreeAsync(p, c->stream);
     }
     // an input needed only late in the call (the data phase): allocated on the
@@ -174,6 +216,15 @@ struct Stage {
         if (cudaMemcpyAsync(d, p, n * sizeof(T), cudaMemcpyHostToDevice, c->copy) != cudaSuccess) ok = false;
         late = true;
         return d;
+    }
+    // order the context stream after everything issued on the side streams
+    void side_join() {
+        if (!forked) return;
+        cudaEventRecord(c->join, c->side);
+        cudaStreamWaitEvent(c->stream, c->join, 0);
+        cudaEventRecord(c->join2, c->side2);
+        cudaStreamWaitEvent(c->stream, c->join2, 0);
+        forked = false;
     }
     void late_join() {
         if (!late) return;
@@ -342,6 +393,7 @@ NOMA_API int noma_ctx_create(int device, noma_ctx_t *out) {
         cudaEventCreateWithFlags(&c->join2, cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&c->join3, cudaEventDisableTiming) != cudaSuccess ||
         cudaStreamCreateWithFlags(&c->copy, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaStreamCreateWithFlags(&c->copy2, cudaStreamNonBlocking) != cudaSuccess ||
         cudaEventCreateWithFlags(&c->ev_alloc, cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&c->copied, cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreate(&c->ev_perm0) != cudaSuccess) {
@@ -368,13 +420,14 @@ NOMA_API int noma_ctx_destroy(noma_ctx_t c) {
     if (c->join2) cudaEventDestroy(c->join2);
     if (c->join3) cudaEventDestroy(c->join3);
     if (c->copy) cudaStreamSynchronize(c->copy), cudaStreamDestroy(c->copy);
+    if (c->copy2) cudaStreamSynchronize(c->copy2), cudaStreamDestroy(c->copy2);
+    for (auto &a : c->pev)
+        for (auto &e : a) cudaEventDestroy(e);
     if (c->ev_alloc) cudaEventDestroy(c->ev_alloc);
     if (c->copied) cudaEventDestroy(c->copied);
     if (c->ev_perm0) cudaEventDestroy(c->ev_perm0);
     if (c->fork) cudaEventDestroy(c->fork);
     if (c->join) cudaEventDestroy(c->join);
-    for (auto &e : c->ev)
-        if (e) cudaEventDestroy(e);
     if (c->own) cudaStreamDestroy(c->own);
     delete c;
     return NOMA_OK;
@@ -399,38 +452,43 @@ NOMA_API int noma_ctx_train_mode(noma_ctx_t c) { return c ? c->train_mode : 0; }
 
 NOMA_API int noma_ctx_detect_mode(noma_ctx_t c) { return c ? c->detect_mode : 0; }
 
+NOMA_API int noma_ctx_pipeline_chunks(noma_ctx_t c) { return c ? c->chunks_last : 0; }
+
 NOMA_API int noma_ctx_set_profiling(noma_ctx_t c, int on) {
     if (!c) return NOMA_ERR_ARGUMENT;
-    if (on && !c->ev[0])
-        for (auto &e : c->ev)
-            if (cudaEventCreate(&e) != cudaSuccess) return cuda_fail(c, "event");
     c->profiling = on != 0;
     return NOMA_OK;
 }
 
+// Phase times of the last profiled pipeline call, summed over its slot chunks:
+// lls, init (side stream), shuffle (side stream), train, detect, whole call.
 NOMA_API int noma_ctx_phase_ms(noma_ctx_t c, double *ms6) {
-    if (!c || !ms6 || !c->ev[0]) return NOMA_ERR_ARGUMENT;
-    if (cudaEventSynchronize(c->ev[7]) != cudaSuccess) return cuda_fail(c, "event sync");
-    auto el = [&](int a, int b) {
+    if (!c || !ms6 || c->pev_used < 1 || (int)c->pev.size() < c->pev_used) return NOMA_ERR_ARGUMENT;
+    const int n = c->pev_used;
+    if (cudaEventSynchronize(c->pev[n - 1][7]) != cudaSuccess) return cuda_fail(c, "event sync");
+    auto el = [&](int ch, int a, int b) {
         float ms = 0.f;
-        cudaEventElapsedTime(&ms, c->ev[a], c->ev[b]);
+        cudaEventElapsedTime(&ms, c->pev[ch][a], c->pev[ch][b]);
         return (double)ms;
     };
-    ms6[0] = el(0, 1);  // lls
-    ms6[1] = el(2, 3);  // init   (side stream, overlaps lls)
-    {  // shuffle (second side stream, concurrent with init and lls)
-        float ms = 0.f;
-        cudaEventElapsedTime(&ms, c->ev_perm0, c->ev[4]);
-        ms6[2] = ms;
+    for (int i = 0; i < 6; ++i) ms6[i] = 0.0;
+    for (int ch = 0; ch < n; ++ch) {
+        ms6[0] += el(ch, 0, 1);  // lls
+        ms6[1] += el(ch, 2, 3);  // init   (side stream, overlaps lls)
+        ms6[2] += el(ch, 8, 4);  // shuffle (second side stream)
+        ms6[3] += el(ch, 5, 6);  // train
+        ms6[4] += el(ch, 6, 7);  // detect
     }
-    ms6[3] = el(5, 6);  // train
-    ms6[4] = el(6, 7);  // detect
-    ms6[5] = el(0, 7);  // whole pipeline
+    {
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, c->pev[0][0], c->pev[n - 1][7]);
+        ms6[5] = ms;  // whole call
+    }
     return NOMA_OK;
 }
 
 NOMA_API int noma_measure_fp32_tflops(noma_ctx_t c, int form, double *tflops) {
-    if (!c || !tflops || form < 0 || form > 1) return NOMA_ERR_ARGUMENT;
+    if (!c || !tflops || form < 0 || form > 2) return NOMA_ERR_ARGUMENT;
     int sms = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device);
     float *out = nullptr;
@@ -444,12 +502,15 @@ NOMA_API int noma_measure_fp32_tflops(noma_ctx_t c, int form, double *tflops) {
         cudaEventRecord(a, c->stream);
         if (form == 0)
             ffma_peak_kernel<<<blocks, threads, 0, c->stream>>>(out, iters, 0.9999f, 1e-4f);
-        else
+        else if (form == 1)
             ffma_outer_kernel<<<blocks, threads, 0, c->stream>>>(out, iters);
+        else
+            ffma2_outer_kernel<<<blocks, threads, 0, c->stream>>>(out, iters);
         cudaEventRecord(b, c->stream);
         cudaEventSynchronize(b);
         float ms = 0.f;
         cudaEventElapsedTime(&ms, a, b);
+        // form 2: 4 x 8 x 2 FFMA2 = 128 FMAs per iteration, like form 1
         const double fma_per_thread = form == 0 ? 16.0 * 8 * iters : 4.0 * 32 * iters;
         const double flops = 2.0 * fma_per_thread * blocks * threads;
         if (rep > 0) best = std::max(best, flops / (ms * 1e-3) / 1e12);
@@ -460,6 +521,16 @@ NOMA_API int noma_measure_fp32_tflops(noma_ctx_t c, int form, double *tflops) {
     if (cudaStreamSynchronize(c->stream) != cudaSuccess) return cuda_fail(c, "ffma probe");
     *tflops = best;
     return NOMA_OK;
+}
+
+NOMA_API int noma_host_alloc(size_t bytes, void **out) {
+    if (!out) return NOMA_ERR_ARGUMENT;
+    *out = nullptr;
+    return cudaHostAlloc(out, bytes ? bytes : 16, cudaHostAllocPortable) == cudaSuccess ? NOMA_OK : NOMA_ERR_CUDA;
+}
+
+NOMA_API int noma_host_free(void *p) {
+    return !p || cudaFreeHost(p) == cudaSuccess ? NOMA_OK : NOMA_ERR_CUDA;
 }
 
 NOMA_API int noma_plan_size(const noma_net_desc *desc) {
@@ -683,7 +754,7 @@ NOMA_API int noma_train_f64(noma_ctx_t c, const noma_dataset *ds, const noma_net
 NOMA_API int noma_detect(noma_ctx_t c, const noma_net_desc *desc, int layout, int n_designs,
                          int nets_per_design, int rows, const float *data, const float *plans,
                          const uint8_t *truth, float *soft, uint8_t *codes, uint32_t *bit_errors,
-                         int mem) {
+                         uint32_t *symbol_errors, int mem) {
     if (!c) return NOMA_ERR_ARGUMENT;
     NetGeom g;
     if (!make_geom(desc, &g)) return fail(c, NOMA_ERR_DIMENSION, "detect: bad dims");
@@ -709,8 +780,10 @@ NOMA_API int noma_detect(noma_ctx_t c, const noma_net_desc *desc, int layout, in
     float *dso = s.out(soft, nets * rows * (layout == NOMA_LAYOUT_WIDEN_COMPLEX ? 2 : 1));
     uint8_t *dco = layout == NOMA_LAYOUT_WIDEN_COMPLEX ? s.out(codes, nets * rows) : nullptr;
     uint32_t *der = s.out(bit_errors, nets);
+    uint32_t *dse = s.out(symbol_errors, nets);
     if (!s.ok) return s.finish();
     if (der) cudaMemsetAsync(der, 0, nets * sizeof(uint32_t), c->stream);
+    if (dse) cudaMemsetAsync(dse, 0, nets * sizeof(uint32_t), c->stream);
     DetectParams dpp;
     dpp.g = g;
     dpp.layout = layout;
@@ -724,6 +797,7 @@ NOMA_API int noma_detect(noma_ctx_t c, const noma_net_desc *desc, int layout, in
     dpp.soft = dso;
     dpp.codes = dco;
     dpp.errors = der;
+    dpp.sym_errors = dse;
     dpp.status = nullptr;
     dpp.mode = 0;
     dpp.stride = rows;
@@ -738,14 +812,25 @@ NOMA_API int noma_detect(noma_ctx_t c, const noma_net_desc *desc, int layout, in
     // every design through offset pointers and the full row stride
     const size_t row_f = g.dims[0], soft_f = layout == NOMA_LAYOUT_WIDEN_COMPLEX ? 2 : 1;
     const int per = ((rows + chunks - 1) / chunks + 63) / 64 * 64;
+    int max_pitch_i = 0;
+    cudaDeviceGetAttribute(&max_pitch_i, cudaDevAttrMaxPitch, c->device);
+    const size_t max_pitch = (size_t)(unsigned)max_pitch_i;
     cudaEventRecord(c->ev_alloc, c->stream);  // the buffer is allocated on the context stream
     cudaStreamWaitEvent(c->copy, c->ev_alloc, 0);
     for (int r0 = 0; r0 < rows; r0 += per) {
         const int n = rows - r0 < per ? rows - r0 : per;
-        if (cudaMemcpy2DAsync(dd_chunked + r0 * row_f, rows * row_f * sizeof(float), data + r0 * row_f,
-                              rows * row_f * sizeof(float), n * row_f * sizeof(float), n_designs,
-                              cudaMemcpyHostToDevice, c->copy) != cudaSuccess)
-            return cuda_fail(c, "detect: chunk upload");
+        const size_t pitch = (size_t)rows * row_f * sizeof(float), wbytes = n * row_f * sizeof(float);
+        bool up_ok = true;
+        if (n_designs > 1 && pitch <= max_pitch) {  // one strided copy across designs
+            up_ok = cudaMemcpy2DAsync(dd_chunked + r0 * row_f, pitch, data + r0 * row_f, pitch, wbytes,
+                                      n_designs, cudaMemcpyHostToDevice, c->copy) == cudaSuccess;
+        } else {  // pitch beyond cudaDevAttrMaxPitch (or one design): a copy per design
+            for (int d = 0; d < n_designs && up_ok; ++d)
+                up_ok = cudaMemcpyAsync(dd_chunked + d * (size_t)rows * row_f + r0 * row_f,
+                                        data + d * (size_t)rows * row_f + r0 * row_f, wbytes,
+                                        cudaMemcpyHostToDevice, c->copy) == cudaSuccess;
+        }
+        if (!up_ok) return cuda_fail(c, "detect: chunk upload");
         cudaEventRecord(c->copied, c->copy);
         cudaStreamWaitEvent(c->stream, c->copied, 0);
         DetectParams dc = dpp;
@@ -767,7 +852,8 @@ NOMA_API int noma_pipeline(noma_ctx_t c, const noma_net_desc *desc, const noma_t
                            const double *pilot_sym, const float *data_rx, const uint8_t *truth,
                            const uint64_t *init_seeds, const uint64_t *shuffle_seeds, double *w0,
                            double *gram_condition, float *plans, double *loss_trace, float *soft,
-                           uint8_t *codes, uint32_t *bit_errors, int *status, int mem) {
+                           uint8_t *codes, uint32_t *bit_errors, uint32_t *symbol_errors, int *status,
+                           int mem) {
     if (!c) return NOMA_ERR_ARGUMENT;
     int st;
     if ((st = check_cfg(c, cfg))) return st;
@@ -779,145 +865,250 @@ NOMA_API int noma_pipeline(noma_ctx_t c, const noma_net_desc *desc, const noma_t
     if (S < 0 || K < 1 || M < 1 || NT < 1 || ND < 0) return fail(c, NOMA_ERR_DIMENSION, "bad sizes");
     if (2 * NT < 2 * M) return fail(c, NOMA_ERR_DIMENSION, "lls::fit: system must be over-determined");
     if (2 * NT > 65535) return fail(c, NOMA_ERR_UNSUPPORTED, "too many pilot rows");
+    if (cfg->epochs > 0 && (cfg->batch_size > NOMA_MAX_BATCH || g.maxfp > NOMA_MAX_WIDTH))
+        return fail(c, NOMA_ERR_UNSUPPORTED, "train: batch > 128 or a layer wider than 128");
     if (S == 0) return NOMA_OK;
     const size_t nets = (size_t)S * K;
     const int n = 2 * NT;
-    Stage s(c, mem);
-    const double *px = s.in(pilot_rx, (size_t)S * NT * M * 2);
-    const double *py = s.in(pilot_sym, (size_t)S * NT * K * 2);
-    const uint64_t *iseed = s.in(init_seeds, nets);
-    const uint64_t *sseed = s.in(shuffle_seeds, nets);
-    double *dw = w0 ? s.out(w0, nets * 2 * M) : s.scratch<double>(nets * 2 * M);
-    double *dc = s.out(gram_condition, nets);
-    float *dp = plans ? s.out(plans, nets * g.plan_total) : s.scratch<float>(nets * g.plan_total);
-    double *dt = s.out(loss_trace, nets * (size_t)cfg->epochs);
-    float *dso = s.out(soft, nets * ND * 2);
-    uint8_t *dco = s.out(codes, nets * ND);
-    uint32_t *der = s.out(bit_errors, nets);
-    int *dst = s.out(status, nets);
-    float *d32 = s.scratch<float>((size_t)S * NT * 2 * M);
-    float *r0 = s.scratch<float>(nets * n);
-    uint16_t *perm = s.scratch<uint16_t>(nets * (size_t)cfg->epochs * n);
-    // data-phase inputs (~2/3 of the host->device bytes) travel while the LLS
-    // and training run; the detection launch waits for them
-    const float *dx = s.in_late(data_rx, (size_t)S * ND * M * 2);
-    const uint8_t *dtr = s.in_late(truth, (size_t)S * ND * K);
+    // Slots run in chunks whose scratch (FP32 design, r0, shuffles, widened
+    // rows, plans) stays under NOMA_CHUNK_MB (default 4096): C5's 32768 slots
+    // would need 72 GB of shuffles at once.  Results are identical to one
+    // call per chunk (every slot is independent).
+    const size_t per_slot = (size_t)NT * 2 * M * 4 * 3 + (size_t)K * n * 4 +
+                            (size_t)K * cfg->epochs * n * 2 + (size_t)K * (g.plan_total * 4 + 2 * M * 8);
+    size_t budget = (size_t)4096 << 20;
+    if (const char *e = std::getenv("NOMA_CHUNK_MB")) budget = (size_t)std::atoll(e) << 20;
+    const int chunk = (int)std::max<size_t>(1, std::min<size_t>((size_t)S, budget / std::max<size_t>(per_slot, 1)));
+    const int nchunk = (S + chunk - 1) / chunk;
+    const bool host = mem == NOMA_MEM_HOST;
+    Stage s(c, NOMA_MEM_DEVICE);  // host buffers are staged per chunk below
+    auto dev = [&](auto *p, size_t cnt) {  // device view of a caller buffer
+        using T = std::remove_cv_t<std::remove_pointer_t<decltype(p)>>;
+        if (!p) return (T *)nullptr;
+        return host ? s.scratch<T>(cnt) : const_cast<T *>(p);
+    };
+    const size_t px_n = (size_t)NT * M * 2, py_n = (size_t)NT * K * 2, dx_n = (size_t)ND * M * 2;
+    const double *px = dev(pilot_rx, S * px_n);
+    const double *py = dev(pilot_sym, S * py_n);
+    const float *dx = dev(data_rx, S * dx_n);
+    const uint8_t *dtr = dev(truth, (size_t)S * ND * K);
+    const uint64_t *iseed = dev(init_seeds, nets);
+    const uint64_t *sseed = dev(shuffle_seeds, nets);
+    double *dw = w0 ? dev(w0, nets * 2 * M) : s.scratch<double>((size_t)chunk * K * 2 * M);
+    double *dc = dev(gram_condition, nets);
+    float *dp = plans ? dev(plans, nets * g.plan_total) : s.scratch<float>((size_t)chunk * K * g.plan_total);
+    double *dt = dev(loss_trace, nets * (size_t)cfg->epochs);
+    float *dso = dev(soft, nets * ND * 2);
+    uint8_t *dco = dev(codes, nets * ND);
+    uint32_t *der = dev(bit_errors, nets);
+    uint32_t *dse = dev(symbol_errors, nets);
+    int *dst = dev(status, nets);
+    float *d32 = s.scratch<float>((size_t)chunk * NT * 2 * M);
+    float *r0 = s.scratch<float>((size_t)chunk * K * n);
+    uint16_t *perm = s.scratch<uint16_t>((size_t)chunk * K * cfg->epochs * n);
     if (!s.ok) return s.finish();
 
-    noma_dataset ds{NOMA_LAYOUT_WIDEN_COMPLEX, S, K, n, 2 * M, px, py};
-    // fork: He-normal init and the per-epoch shuffles depend only on seeds,
-    // so they run on the side stream while the LLS kernel runs; join before
-    // w0 is copied into the plans and training starts.
-    mark(c, 0);
-    cudaEventRecord(c->fork, c->stream);
-    cudaStreamWaitEvent(c->side, c->fork, 0);
-    cudaStreamWaitEvent(c->side2, c->fork, 0);
-    mark(c, 2, c->side);
-    if (init_launch(g, (int)nets, iseed, nullptr, dp, c->side)) return cuda_fail(c, "init");
-    mark(c, 3, c->side);
-    cudaEventRecord(c->join, c->side);
-    if (c->profiling) cudaEventRecord(c->ev_perm0, c->side2);
-    if (perm_launch((int)nets, cfg->epochs, n, sseed, perm, c->side2)) return cuda_fail(c, "perm");
-    mark(c, 4, c->side2);
-    cudaEventRecord(c->join2, c->side2);
-    // critical path: Gram + Cholesky solve (Jacobi only for slots whose
-    // Cholesky pivots fall near the rank threshold); the condition numbers
-    // of the other slots come from a Jacobi launch on side2 that overlaps
-    // training and joins before the outputs
-    LlsParams lp = lls_params(&ds, px, py, dw, dc, dst, d32, r0);
-    lp.mode = 1;
-    const bool lclk = std::getenv("NOMA_PHASE_CLOCKS") != nullptr;
-    if (lclk) {
-        lp.clocks = s.scratch<long long>(8);
-        if (lp.clocks) cudaMemsetAsync(lp.clocks, 0, 8 * sizeof(long long), c->stream);
+    // host buffers: every chunk's inputs are queued on the copy stream up
+    // front (pilots first, data-phase inputs second), each chunk's results go
+    // back on copy2 as soon as the chunk is done -- transfers overlap compute
+    std::vector<cudaEvent_t> evs;
+    auto new_event = [&]() {
+        cudaEvent_t e = nullptr;
+        cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+        evs.push_back(e);
+        return e;
+    };
+    struct EvGuard {
+        std::vector<cudaEvent_t> &v;
+        ~EvGuard() {
+            for (auto e : v) cudaEventDestroy(e);
+        }
+    } ev_guard{evs};
+    std::vector<cudaEvent_t> ev_pil(nchunk, nullptr), ev_dat(nchunk, nullptr);
+    bool copy_ok = true;
+    auto h2d = [&](const void *hp, const void *dp_, size_t bytes) {
+        if (hp && bytes && cudaMemcpyAsync(const_cast<void *>(dp_), hp, bytes, cudaMemcpyHostToDevice, c->copy) != cudaSuccess)
+            copy_ok = false;
+    };
+    if (host) {
+        cudaEventRecord(c->ev_alloc, c->stream);
+        cudaStreamWaitEvent(c->copy, c->ev_alloc, 0);
+        for (int ch = 0; ch < nchunk; ++ch) {
+            const size_t a = (size_t)ch * chunk, sc = std::min<size_t>(chunk, S - a);
+            h2d(pilot_rx + a * px_n, px + a * px_n, sc * px_n * 8);
+            h2d(pilot_sym + a * py_n, py + a * py_n, sc * py_n * 8);
+            h2d(init_seeds + a * K, iseed + a * K, sc * K * 8);
+            h2d(shuffle_seeds + a * K, sseed + a * K, sc * K * 8);
+            ev_pil[ch] = new_event();
+            cudaEventRecord(ev_pil[ch], c->copy);
+        }
+        for (int ch = 0; ch < nchunk; ++ch) {
+            const size_t a = (size_t)ch * chunk, sc = std::min<size_t>(chunk, S - a);
+            h2d(data_rx + a * dx_n, dx + a * dx_n, sc * dx_n * 4);
+            if (truth) h2d(truth + a * ND * K, dtr + a * ND * K, sc * ND * K);
+            ev_dat[ch] = new_event();
+            cudaEventRecord(ev_dat[ch], c->copy);
+        }
+        if (!copy_ok) return cuda_fail(c, "pipeline: host upload");
     }
-    st = lls_launch(lp, c->stream);
-    if (lclk && lp.clocks && !st) {
-        long long h[8];
-        cudaMemcpyAsync(h, lp.clocks, sizeof(h), cudaMemcpyDeviceToHost, c->stream);
-        cudaStreamSynchronize(c->stream);
-        std::fprintf(stderr, "NOMA_LLS_CLOCKS gram %lld frob %lld jacobi %lld solve %lld residual %lld sweeps %lld\n",
-                     h[0], h[1], h[2], h[3], h[4], h[5]);
-    }
-    if (st) return st == NOMA_ERR_CUDA ? cuda_fail(c, "lls") : fail(c, st, "lls: unsupported shape");
-    const bool cond_side = dc != nullptr;
-    if (cond_side) {
-        LlsParams lc = lls_params(&ds, px, py, nullptr, dc, nullptr, nullptr, nullptr);
-        lc.mode = 2;
-        if (lls_launch(lc, c->side2)) return cuda_fail(c, "lls condition");
-        cudaEventRecord(c->join3, c->side2);
-    }
-    mark(c, 1);
-    cudaStreamWaitEvent(c->stream, c->join, 0);
-    cudaStreamWaitEvent(c->stream, c->join2, 0);
-    if (set_w0_launch((int)nets, 2 * M, g.plan_total, dw, dp, c->stream)) return cuda_fail(c, "w0");
-    mark(c, 5);
-    c->launches += 4;
-    if (cfg->epochs > 0) {
-        TrainParams tp;
-        fill_train(tp, g, cfg);
-        tp.layout = NOMA_LAYOUT_WIDEN_COMPLEX;
-        tp.n_nets = (int)nets;
-        tp.K = K;
-        tp.rows = n;
-        tp.width = 2 * M;
-        tp.design32 = d32;
-        tp.r0 = r0;
-        tp.perm = perm;
-        tp.plans = dp;
-        tp.trace = dt;
-        tp.status = dst;
-        const bool clocks = std::getenv("NOMA_PHASE_CLOCKS") != nullptr;
-        // [0..8) phase totals, [8..) per-warp timeline of 4 steps (latency kernel)
-        constexpr int kClk = 8 + 4 * 16 * 16;
-        if (clocks) tp.clocks = s.scratch<long long>(kClk);
-        if (clocks && tp.clocks) cudaMemsetAsync(tp.clocks, 0, kClk * sizeof(long long), c->stream);
-        prep_scratch(s, tp);
-        st = train_launch(tp, c->stream);
-        c->train_mode = tp.mode;
-        if (st) return st == NOMA_ERR_CUDA ? cuda_fail(c, "train") : fail(c, st, "train: unsupported network shape");
-        c->launches += 1;
-        if (clocks) {  // instrumentation only: per-phase cycles of net 0
-            std::vector<long long> h(kClk, 0);
-            cudaMemcpyAsync(h.data(), tp.clocks, kClk * sizeof(long long), cudaMemcpyDeviceToHost, c->stream);
+    auto d2h = [&](void *hp, const void *dp_, size_t bytes) {
+        if (hp && bytes && cudaMemcpyAsync(hp, dp_, bytes, cudaMemcpyDeviceToHost, c->copy2) != cudaSuccess)
+            copy_ok = false;
+    };
+
+    c->pev_used = c->profiling ? nchunk : 0;
+    c->chunks_last = nchunk;
+    for (int ch = 0; ch < nchunk; ++ch) {
+        const size_t a = (size_t)ch * chunk;
+        const int Sc = (int)std::min<size_t>(chunk, S - a);
+        const size_t an = a * K, cn = (size_t)Sc * K;  // first net, nets of the chunk
+        const double *cpx = px + a * px_n, *cpy = py + a * py_n;
+        double *cdw = w0 ? dw + an * 2 * M : dw;
+        double *cdc = dc ? dc + an : nullptr;
+        float *cdp = plans ? dp + an * g.plan_total : dp;
+        int *cdst = dst + an;
+        if (host) cudaStreamWaitEvent(c->stream, ev_pil[ch], 0);
+        noma_dataset ds{NOMA_LAYOUT_WIDEN_COMPLEX, Sc, K, n, 2 * M, cpx, cpy};
+        // fork: He-normal init and the per-epoch shuffles depend only on seeds,
+        // so they run on the side streams while the LLS kernel runs; join
+        // before w0 is copied into the plans and training starts.
+        mark(c, ch, 0);
+        cudaEventRecord(c->fork, c->stream);
+        cudaStreamWaitEvent(c->side, c->fork, 0);
+        cudaStreamWaitEvent(c->side2, c->fork, 0);
+        s.forked = true;
+        mark(c, ch, 2, c->side);
+        if (init_launch(g, (int)cn, iseed + an, nullptr, cdp, c->side)) return cuda_fail(c, "init");
+        mark(c, ch, 3, c->side);
+        cudaEventRecord(c->join, c->side);
+        mark(c, ch, 8, c->side2);
+        if (perm_launch((int)cn, cfg->epochs, n, sseed + an, perm, c->side2)) return cuda_fail(c, "perm");
+        mark(c, ch, 4, c->side2);
+        cudaEventRecord(c->join2, c->side2);
+        // critical path: Gram + Cholesky solve (Jacobi only for slots whose
+        // Cholesky pivots fall near the rank threshold); the condition numbers
+        // of the other slots come from a Jacobi launch on side2 that overlaps
+        // training and joins before the outputs
+        LlsParams lp = lls_params(&ds, cpx, cpy, cdw, cdc, cdst, d32, r0);
+        lp.mode = 1;
+        const bool lclk = std::getenv("NOMA_PHASE_CLOCKS") != nullptr;
+        if (lclk) {
+            lp.clocks = s.scratch<long long>(8);
+            if (lp.clocks) cudaMemsetAsync(lp.clocks, 0, 8 * sizeof(long long), c->stream);
+        }
+        st = lls_launch(lp, c->stream);
+        if (lclk && lp.clocks && !st) {
+            long long h[8];
+            cudaMemcpyAsync(h, lp.clocks, sizeof(h), cudaMemcpyDeviceToHost, c->stream);
             cudaStreamSynchronize(c->stream);
-            std::fprintf(stderr, "NOMA_PHASE_CLOCKS mode %d: %lld %lld %lld %lld %lld %lld %lld %lld\n",
-                         tp.mode, h[0], h[1], h[2], h[3], h[4], h[5], h[6], h[7]);
-            if (const char *path = std::getenv("NOMA_PHASE_TRACE")) {
-                if (FILE *f = std::fopen(path, "w")) {
-                    for (int i = 8; i < kClk; ++i) std::fprintf(f, "%lld\n", h[i]);
-                    std::fclose(f);
+            std::fprintf(stderr, "NOMA_LLS_CLOCKS gram %lld frob %lld jacobi %lld solve %lld residual %lld sweeps %lld\n",
+                         h[0], h[1], h[2], h[3], h[4], h[5]);
+        }
+        if (st) return st == NOMA_ERR_CUDA ? cuda_fail(c, "lls") : fail(c, st, "lls: unsupported shape");
+        const bool cond_side = cdc != nullptr;
+        if (cond_side) {
+            LlsParams lc = lls_params(&ds, cpx, cpy, nullptr, cdc, nullptr, nullptr, nullptr);
+            lc.mode = 2;
+            if (lls_launch(lc, c->side2)) return cuda_fail(c, "lls condition");
+            cudaEventRecord(c->join3, c->side2);
+        }
+        mark(c, ch, 1);
+        cudaStreamWaitEvent(c->stream, c->join, 0);
+        cudaStreamWaitEvent(c->stream, c->join2, 0);
+        if (set_w0_launch((int)cn, 2 * M, g.plan_total, cdw, cdp, c->stream)) return cuda_fail(c, "w0");
+        mark(c, ch, 5);
+        c->launches += 4;
+        if (cfg->epochs > 0) {
+            TrainParams tp;
+            fill_train(tp, g, cfg);
+            tp.layout = NOMA_LAYOUT_WIDEN_COMPLEX;
+            tp.n_nets = (int)cn;
+            tp.K = K;
+            tp.rows = n;
+            tp.width = 2 * M;
+            tp.design32 = d32;
+            tp.r0 = r0;
+            tp.perm = perm;
+            tp.plans = cdp;
+            tp.trace = dt ? dt + an * cfg->epochs : nullptr;
+            tp.status = cdst;
+            const bool clocks = std::getenv("NOMA_PHASE_CLOCKS") != nullptr && ch == 0;
+            // [0..8) phase totals, [8..) per-warp timeline of 4 steps (latency kernel)
+            constexpr int kClk = 8 + 4 * 16 * 16;
+            if (clocks) tp.clocks = s.scratch<long long>(kClk);
+            if (clocks && tp.clocks) cudaMemsetAsync(tp.clocks, 0, kClk * sizeof(long long), c->stream);
+            prep_scratch(s, tp);
+            st = train_launch(tp, c->stream);
+            c->train_mode = tp.mode;
+            if (st) return st == NOMA_ERR_CUDA ? cuda_fail(c, "train") : fail(c, st, "train: unsupported network shape");
+            c->launches += 1;
+            if (clocks) {  // instrumentation only: per-phase cycles of net 0
+                std::vector<long long> h(kClk, 0);
+                cudaMemcpyAsync(h.data(), tp.clocks, kClk * sizeof(long long), cudaMemcpyDeviceToHost, c->stream);
+                cudaStreamSynchronize(c->stream);
+                std::fprintf(stderr, "NOMA_PHASE_CLOCKS mode %d: %lld %lld %lld %lld %lld %lld %lld %lld\n",
+                             tp.mode, h[0], h[1], h[2], h[3], h[4], h[5], h[6], h[7]);
+                if (const char *path = std::getenv("NOMA_PHASE_TRACE")) {
+                    if (FILE *f = std::fopen(path, "w")) {
+                        for (int i = 8; i < kClk; ++i) std::fprintf(f, "%lld\n", h[i]);
+                        std::fclose(f);
+                    }
                 }
             }
         }
+        mark(c, ch, 6);
+        if (host) cudaStreamWaitEvent(c->stream, ev_dat[ch], 0);
+        if (ND > 0) {
+            uint32_t *cder = der ? der + an : nullptr, *cdse = dse ? dse + an : nullptr;
+            if (cder) cudaMemsetAsync(cder, 0, cn * sizeof(uint32_t), c->stream);
+            if (cdse) cudaMemsetAsync(cdse, 0, cn * sizeof(uint32_t), c->stream);
+            DetectParams dpp;
+            dpp.g = g;
+            dpp.layout = NOMA_LAYOUT_WIDEN_COMPLEX;
+            dpp.n_nets = (int)cn;
+            dpp.K = K;
+            dpp.rows = ND;
+            dpp.width = 2 * M;
+            dpp.data = dx + a * dx_n;
+            dpp.plans = cdp;
+            dpp.truth = dtr ? dtr + a * ND * K : nullptr;
+            dpp.soft = dso ? dso + an * ND * 2 : nullptr;
+            dpp.codes = dco ? dco + an * ND : nullptr;
+            dpp.errors = cder;
+            dpp.sym_errors = cdse;
+            dpp.status = cdst;
+            dpp.mode = 0;
+            st = detect_launch(dpp, c->stream);
+            c->detect_mode = dpp.mode;
+            if (st) return st == NOMA_ERR_CUDA ? cuda_fail(c, "detect") : fail(c, st, "detect: unsupported network shape");
+            c->launches += 1;
+        }
+        if (cond_side) cudaStreamWaitEvent(c->stream, c->join3, 0);
+        mark(c, ch, 7);
+        if (host) {  // this chunk's results back while the next chunk runs
+            cudaEvent_t done = new_event();
+            cudaEventRecord(done, c->stream);
+            cudaStreamWaitEvent(c->copy2, done, 0);
+            if (w0) d2h(w0 + an * 2 * M, cdw, cn * 2 * M * 8);
+            if (gram_condition) d2h(gram_condition + an, cdc, cn * 8);
+            if (plans) d2h(plans + an * g.plan_total, cdp, cn * g.plan_total * 4);
+            if (loss_trace && dt) d2h(loss_trace + an * cfg->epochs, dt + an * cfg->epochs, cn * cfg->epochs * 8);
+            if (soft) d2h(soft + an * ND * 2, dso + an * ND * 2, cn * ND * 2 * 4);
+            if (codes) d2h(codes + an * ND, dco + an * ND, cn * ND);
+            if (bit_errors) d2h(bit_errors + an, der + an, cn * 4);
+            if (symbol_errors) d2h(symbol_errors + an, dse + an, cn * 4);
+            d2h(status + an, cdst, cn * 4);
+            if (!copy_ok) return cuda_fail(c, "pipeline: result download");
+        }
     }
-    mark(c, 6);
-    s.late_join();
-    if (ND > 0) {
-        if (der) cudaMemsetAsync(der, 0, nets * sizeof(uint32_t), c->stream);
-        DetectParams dpp;
-        dpp.g = g;
-        dpp.layout = NOMA_LAYOUT_WIDEN_COMPLEX;
-        dpp.n_nets = (int)nets;
-        dpp.K = K;
-        dpp.rows = ND;
-        dpp.width = 2 * M;
-        dpp.data = dx;
-        dpp.plans = dp;
-        dpp.truth = dtr;
-        dpp.soft = dso;
-        dpp.codes = dco;
-        dpp.errors = der;
-        dpp.status = dst;
-        dpp.mode = 0;
-        st = detect_launch(dpp, c->stream);
-        c->detect_mode = dpp.mode;
-        if (st) return st == NOMA_ERR_CUDA ? cuda_fail(c, "detect") : fail(c, st, "detect: unsupported network shape");
-        c->launches += 1;
+    if (host) {  // the call returns after the last download
+        cudaEvent_t done = new_event();
+        cudaEventRecord(done, c->copy2);
+        cudaStreamWaitEvent(c->stream, done, 0);
     }
-    if (cond_side) cudaStreamWaitEvent(c->stream, c->join3, 0);
-    mark(c, 7);
-    return s.finish();
+    st = s.finish();
+    if (st == NOMA_OK && host) st = cudaStreamSynchronize(c->stream) == cudaSuccess ? NOMA_OK : cuda_fail(c, "synchronize");
+    return st;
 }
 
 }  // extern "C"

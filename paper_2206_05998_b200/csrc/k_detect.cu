@@ -21,6 +21,7 @@ __global__ void __launch_bounds__(kThreads) detect_kernel(DetectParams p) {
     const int net = blockIdx.y, tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     if (p.status && p.status[net] != NOMA_OK) {
         if (blockIdx.x == 0 && tid == 0 && p.errors) p.errors[net] = 0xFFFFFFFFu;
+        if (blockIdx.x == 0 && tid == 0 && p.sym_errors) p.sym_errors[net] = 0xFFFFFFFFu;
         return;
     }
     const NetGeom &g = p.g;
@@ -47,7 +48,7 @@ __global__ void __launch_bounds__(kThreads) detect_kernel(DetectParams p) {
     const bool widen = p.layout == NOMA_LAYOUT_WIDEN_COMPLEX;
     const int M = p.width / 2;
     const int rows_per_tile = widen ? kBatchRows / 2 : kBatchRows;  // symbols or rows
-    uint32_t my_err = 0;
+    uint32_t my_err = 0, my_ser = 0;
     for (int tile = blockIdx.x; tile < p.tiles; tile += gridDim.x) {
         const int t0 = tile * rows_per_tile;
         const int tn = min(rows_per_tile, p.rows - t0);
@@ -109,16 +110,21 @@ __global__ void __launch_bounds__(kThreads) detect_kernel(DetectParams p) {
                     if (p.truth) e = __popc((code ^ p.truth[((size_t)d * p.stride + t) * p.K + k]) & 3u);
                 }
                 my_err += e;
+                my_ser += e ? 1u : 0u;
             }
         } else if (tid < tn && p.soft) {
             p.soft[(size_t)net * p.stride + t0 + tid] = Y[tid];
         }
         __syncthreads();
     }
-    if (p.errors && p.truth && warp < 2) {
+    if ((p.errors || p.sym_errors) && p.truth && warp < 2) {
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) my_err += __shfl_xor_sync(0xffffffffu, my_err, o);
-        if (lane == 0 && my_err) atomicAdd(p.errors + net, my_err);
+        for (int o = 16; o > 0; o >>= 1) {
+            my_err += __shfl_xor_sync(0xffffffffu, my_err, o);
+            my_ser += __shfl_xor_sync(0xffffffffu, my_ser, o);
+        }
+        if (lane == 0 && my_err && p.errors) atomicAdd(p.errors + net, my_err);
+        if (lane == 0 && my_ser && p.sym_errors) atomicAdd(p.sym_errors + net, my_ser);
     }
 }
 

@@ -159,6 +159,7 @@ struct DetectTcParams {
     float *soft;                 // [net][rows] complex, nullable
     uint8_t *codes;              // [net][rows], nullable
     uint32_t *errors;            // [net], nullable
+    uint32_t *sym_errors;        // [net], nullable
     const int *status;
     long long *clocks;           // NOMA_DETECT_CLK: per-role cycles of CTA (0, 0), nullable
 };
@@ -300,7 +301,7 @@ __global__ void __launch_bounds__(WsRoles<W0, NL>::kThreads, 1) detect_ws_kernel
     const long long t_lo = T * blockIdx.x / gridDim.x, t_hi = T * (blockIdx.x + 1) / gridDim.x;
     int net = 0, d = 0, k = 0, first = 0, ntile = 0, ib = 0;
     // decision + bit errors of widened row r (lane pairs = Re/Im of a symbol)
-    uint32_t my_err = 0;
+    uint32_t my_err = 0, my_ser = 0;
     auto emit = [&](int tile, int r, float y, uint8_t truth) {
         const float yo = __shfl_xor_sync(0xffffffffu, y, 1);
         const int s = tile * 64 + (r >> 1);
@@ -308,7 +309,11 @@ __global__ void __launch_bounds__(WsRoles<W0, NL>::kThreads, 1) detect_ws_kernel
             const uint8_t code = (uint8_t)((y < 0.f ? 1 : 0) | (yo < 0.f ? 2 : 0));  // eval.cpp:41-42
             if (p.codes) p.codes[(size_t)net * p.stride + s] = code;
             if (p.soft) *reinterpret_cast<float2 *>(p.soft + ((size_t)net * p.stride + s) * 2) = make_float2(y, yo);
-            if (p.truth) my_err += __popc((unsigned)(truth ^ code) & 3u);
+            if (p.truth) {
+                const uint32_t e = __popc((unsigned)(truth ^ code) & 3u);
+                my_err += e;
+                my_ser += e ? 1u : 0u;
+            }
         }
     };
     auto truth_of = [&](int tile, int r) -> uint8_t {
@@ -365,6 +370,7 @@ __global__ void __launch_bounds__(WsRoles<W0, NL>::kThreads, 1) detect_ws_kernel
     k = net % p.K;
     if (p.status && p.status[net] != NOMA_OK) {
         if (first == 0 && threadIdx.x == 0 && p.errors) p.errors[net] = 0xFFFFFFFFu;
+        if (first == 0 && threadIdx.x == 0 && p.sym_errors) p.sym_errors[net] = 0xFFFFFFFFu;
         continue;
     }
     // ---- the net's weights: hi/lo planes in the K-major core layout (FusedPlan
@@ -620,11 +626,16 @@ __global__ void __launch_bounds__(WsRoles<W0, NL>::kThreads, 1) detect_ws_kernel
             }
         }
     }
-    if ((NL == 1 ? (warp >= 4 && warp < 8) : (warp >= 8 && warp < 12)) && p.errors && p.truth) {
+    if ((NL == 1 ? (warp >= 4 && warp < 8) : (warp >= 8 && warp < 12)) && (p.errors || p.sym_errors) &&
+        p.truth) {
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) my_err += __shfl_xor_sync(0xffffffffu, my_err, o);
-        if (lane == 0 && my_err) atomicAdd(p.errors + net, my_err);
-        my_err = 0;
+        for (int o = 16; o > 0; o >>= 1) {
+            my_err += __shfl_xor_sync(0xffffffffu, my_err, o);
+            my_ser += __shfl_xor_sync(0xffffffffu, my_ser, o);
+        }
+        if (lane == 0 && my_err && p.errors) atomicAdd(p.errors + net, my_err);
+        if (lane == 0 && my_ser && p.sym_errors) atomicAdd(p.sym_errors + net, my_ser);
+        my_err = my_ser = 0;
     }
     asm volatile("tcgen05.fence::before_thread_sync;");
     __syncthreads();
@@ -662,6 +673,7 @@ int detect_tc_launch(const DetectParams &dp, cudaStream_t st) {
     p.soft = dp.soft;
     p.codes = dp.codes;
     p.errors = dp.errors;
+    p.sym_errors = dp.sym_errors;
     p.status = dp.status;
     p.clocks = nullptr;
     if (p.tiles == 0 || p.n_nets == 0) return NOMA_OK;

@@ -284,6 +284,9 @@ __global__ void __launch_bounds__(kInitThreads) init_block_kernel(
     start[g.nd] = total;
     const Xoshiro r0 = states ? Xoshiro(states[net * 4], states[net * 4 + 1], states[net * 4 + 2], states[net * 4 + 3])
                               : Xoshiro(seeds[net]);
+    // every thread holds the caller's state before the last block's lane
+    // writes the advanced state back over it
+    __syncthreads();
     constexpr int G = kJumpDraws / 2;  // gaussians per block
     const int blocks = (total + G - 1) / G;
     // chunks of 32 blocks per warp: the chunk's first state by c steps of

@@ -65,7 +65,8 @@ struct DetectParams {
     const uint8_t *truth;   // WIDEN: [S][rows][K] codes, nullable
     float *soft;            // WIDEN: [net][rows] c32; REAL: [net][rows]
     uint8_t *codes;         // WIDEN: [net][rows]
-    uint32_t *errors;       // [net]
+    uint32_t *errors;       // [net] bit errors (nullable)
+    uint32_t *sym_errors;   // [net] symbol errors: decision != truth (nullable)
     const int *status;      // [net] nullable
     int tiles;              // per net
     int stride = 0;         // row stride of data / truth / soft / codes (0: rows); a
@@ -105,6 +106,8 @@ int lls_predict_launch(int layout, int S, int K, int rows, int width, const doub
                        const double *w0, double *out, cudaStream_t st);
 int train_launch(TrainParams &p, cudaStream_t st);
 int train_lat_launch(TrainParams &p, cudaStream_t st);
+bool train_w4_fits(const TrainParams &p);
+int train_w4_launch(TrainParams &p, cudaStream_t st);
 int train_f64_launch(TrainF64Params &p, cudaStream_t st);
 int detect_launch(DetectParams &p, cudaStream_t st);
 int detect_tc_launch(const DetectParams &p, cudaStream_t st);

@@ -114,7 +114,7 @@ std::vector<float> infer_rows(const std::vector<int> &dims, const std::vector<fl
     const noma_net_desc d = desc_of(dims);
     std::vector<float> out(static_cast<std::size_t>(nrows));
     check(noma_detect(ctx(), &d, NOMA_LAYOUT_REAL, 1, 1, nrows, rows_f32.data(), plan.data(),
-                      nullptr, out.data(), nullptr, nullptr, NOMA_MEM_HOST),
+                      nullptr, out.data(), nullptr, nullptr, nullptr, NOMA_MEM_HOST),
           "forward");
     return out;
 }

@@ -25,8 +25,9 @@ EXPORTED = [
     "noma_ctx_set_stream", "noma_ctx_synchronize", "noma_ctx_kernel_launches",
     "noma_plan_size", "noma_param_count", "noma_lls_fit", "noma_init_params", "noma_train",
     "noma_detect", "noma_pipeline", "noma_synthesize", "noma_ctx_set_profiling",
-    "noma_ctx_phase_ms", "noma_measure_fp32_tflops", "noma_init_params_state",
+    "noma_ctx_phase_ms", "noma_measure_fp32_tflops", "noma_host_alloc", "noma_host_free", "noma_init_params_state",
     "noma_lls_predict", "noma_train_f64", "noma_ctx_train_mode", "noma_ctx_detect_mode", "noma_synthesize_bundles",
+    "noma_ctx_pipeline_chunks",
 ]
 PHASES = ("lls", "init", "shuffle", "train", "detect", "total")
 
@@ -115,20 +116,23 @@ def load():
     L.noma_ctx_kernel_launches.argtypes = [vp]
     L.noma_ctx_train_mode.argtypes = [vp]
     L.noma_ctx_detect_mode.argtypes = [vp]
+    L.noma_ctx_pipeline_chunks.argtypes = [vp]
     L.noma_plan_size.argtypes = [C.POINTER(NetDesc)]
     L.noma_param_count.argtypes = [C.POINTER(NetDesc)]
     L.noma_lls_fit.argtypes = [vp, C.POINTER(Dataset), vp, vp, vp, ip]
     L.noma_init_params.argtypes = [vp, C.POINTER(NetDesc), ip, vp, vp, vp, ip]
     L.noma_train.argtypes = [vp, C.POINTER(Dataset), C.POINTER(NetDesc), C.POINTER(TrainCfg),
                              vp, vp, vp, vp, vp, ip]
-    L.noma_detect.argtypes = [vp, C.POINTER(NetDesc), ip, ip, ip, ip, vp, vp, vp, vp, vp, vp, ip]
+    L.noma_detect.argtypes = [vp, C.POINTER(NetDesc), ip, ip, ip, ip, vp, vp, vp, vp, vp, vp, vp, ip]
     L.noma_pipeline.argtypes = [vp, C.POINTER(NetDesc), C.POINTER(TrainCfg), ip, ip, ip, ip, ip,
-                                vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, ip]
+                                vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, ip]
     L.noma_synthesize.argtypes = [vp, C.POINTER(Scenario), ip, vp, vp, vp, vp, vp, vp, vp, ip]
     L.noma_synthesize_bundles.argtypes = [vp, C.POINTER(Scenario), ip, vp, vp, vp, vp, vp, vp, vp, ip]
     L.noma_ctx_set_profiling.argtypes = [vp, ip]
     L.noma_ctx_phase_ms.argtypes = [vp, C.POINTER(C.c_double)]
     L.noma_measure_fp32_tflops.argtypes = [vp, ip, C.POINTER(C.c_double)]
+    L.noma_host_alloc.argtypes = [C.c_size_t, C.POINTER(vp)]
+    L.noma_host_free.argtypes = [vp]
     L.noma_init_params_state.argtypes = [vp, C.POINTER(NetDesc), ip, vp, vp, vp, vp, ip]
     L.noma_lls_predict.argtypes = [vp, ip, ip, ip, ip, ip, vp, vp, vp, ip]
     L.noma_train_f64.argtypes = [vp, C.POINTER(Dataset), C.POINTER(NetDesc), C.POINTER(TrainCfg),
@@ -157,6 +161,25 @@ def _ptr(a):
     # torch tensor
     assert a.is_contiguous()
     return a.data_ptr()
+
+
+def pinned_empty(shape, dtype) -> np.ndarray:
+    """numpy array in page-locked host memory (noma_host_alloc), freed with
+    the array: the host buffers of NOMA_MEM_HOST calls whose chunked copies
+    should overlap the device work."""
+    import weakref
+
+    dtype = np.dtype(dtype)
+    nbytes = int(np.prod(shape)) * dtype.itemsize
+    ptr = C.c_void_p()
+    st = load().noma_host_alloc(max(nbytes, 1), C.byref(ptr))
+    if st != OK:
+        raise NomaError(st, f"noma_host_alloc({nbytes}) failed")
+    raw = (C.c_uint8 * max(nbytes, 1)).from_address(ptr.value)
+    base = np.frombuffer(raw, dtype=np.uint8, count=nbytes)
+    arr = base.view(dtype).reshape(shape)
+    weakref.finalize(raw, load().noma_host_free, ptr)
+    return arr
 
 
 def _mem_of(*arrays):
@@ -205,6 +228,11 @@ class Context:
 
     def synchronize(self):
         self._check(self.L.noma_ctx_synchronize(self.h))
+
+    @property
+    def pipeline_chunks(self) -> int:
+        """Slot chunks of the last pipeline call (noma_ctx_pipeline_chunks)."""
+        return self.L.noma_ctx_pipeline_chunks(self.h)
 
     @property
     def kernel_launches(self) -> int:
@@ -294,23 +322,23 @@ class Context:
                                           _ptr(status), mem))
 
     def detect(self, dims, layout, n_designs, K, rows, data, plans, truth=None, soft=None,
-               codes=None, bit_errors=None):
+               codes=None, bit_errors=None, symbol_errors=None):
         mem = _mem_of(data, plans)
         d = NetDesc.of(dims)
         self._check(self.L.noma_detect(self.h, C.byref(d), layout, n_designs, K, rows,
                                        _ptr(data), _ptr(plans), _ptr(truth), _ptr(soft),
-                                       _ptr(codes), _ptr(bit_errors), mem))
+                                       _ptr(codes), _ptr(bit_errors), _ptr(symbol_errors), mem))
 
     def pipeline(self, dims, cfg: TrainCfg, S, K, M, NT, ND, pilot_rx, pilot_sym, data_rx, truth,
                  init_seeds, shuffle_seeds, status, w0=None, cond=None, plans=None, trace=None,
-                 soft=None, codes=None, bit_errors=None):
+                 soft=None, codes=None, bit_errors=None, symbol_errors=None):
         mem = _mem_of(pilot_rx, pilot_sym, data_rx, status)
         d = NetDesc.of(dims)
         self._check(self.L.noma_pipeline(
             self.h, C.byref(d), C.byref(cfg), S, K, M, NT, ND, _ptr(pilot_rx), _ptr(pilot_sym),
             _ptr(data_rx), _ptr(truth), _ptr(init_seeds), _ptr(shuffle_seeds), _ptr(w0),
             _ptr(cond), _ptr(plans), _ptr(trace), _ptr(soft), _ptr(codes), _ptr(bit_errors),
-            _ptr(status), mem))
+            _ptr(symbol_errors), _ptr(status), mem))
 
     def synthesize_bundles(self, sc: Scenario, bundles, pilot_rx=None, pilot_sym=None, data_rx=None,
                            data_codes=None, channel=None, noise_power=None):

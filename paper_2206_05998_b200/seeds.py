@@ -37,10 +37,29 @@ def mix_tag(a: int, b: int, c: int = 0, d: int = 0) -> int:
     return _splitmix64(s)[0]
 
 
+def _splitmix64_np(state):
+    """Vectorised splitmix64 over uint64 arrays (wrapping arithmetic)."""
+    state = state + np.uint64(0x9E3779B97F4A7C15)
+    z = state
+    z = (z ^ (z >> np.uint64(30))) * np.uint64(0xBF58476D1CE4E5B9)
+    z = (z ^ (z >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)
+    return z ^ (z >> np.uint64(31))
+
+
+def substream_seed_np(master, tag):
+    """substream_seed over broadcast uint64 arrays (rng.hpp:18-23)."""
+    with np.errstate(over="ignore"):
+        master = np.asarray(master, dtype=np.uint64)
+        tag = np.asarray(tag, dtype=np.uint64)
+        a = _splitmix64_np(master)
+        s = a ^ (tag * np.uint64(0xD1B54A32D192ED03) + np.uint64(0x8BB84B93962EACC9))
+        return _splitmix64_np(s)
+
+
 def slot_user_seeds(slot_seeds, K):
     """-> (init_seeds [S,K], shuffle_seeds [S,K]) uint64 for 1-based users."""
-    init = np.array([[substream_seed(int(s), 0x1000 + u) for u in range(1, K + 1)]
-                     for s in slot_seeds], dtype=np.uint64)
-    shuf = np.array([[substream_seed(int(s), u) for u in range(1, K + 1)] for s in slot_seeds],
-                    dtype=np.uint64)
-    return init, shuf
+    s = np.asarray(slot_seeds, dtype=np.uint64).reshape(-1, 1)
+    u = np.arange(1, K + 1, dtype=np.uint64).reshape(1, -1)
+    init = substream_seed_np(s, u + np.uint64(0x1000))
+    shuf = substream_seed_np(s, u)
+    return np.ascontiguousarray(init), np.ascontiguousarray(shuf)

@@ -122,8 +122,9 @@ def test_detect_tc_many_nets(A, dims, rows, monkeypatch):
     assert np.all(np.abs(errs.astype(np.int64) - errs_f.astype(np.int64)) <= 2 * near.sum(axis=1))
 
 
+@pytest.mark.parametrize("n_designs", [2, 1])  # 1: a plain copy per design
 @pytest.mark.parametrize("tc", ["1", "0"])
-def test_detect_host_chunked_upload(A, tc, monkeypatch):
+def test_detect_host_chunked_upload(A, tc, n_designs, monkeypatch):
     """Host buffers of >= 32 MB are uploaded in row chunks on the copy stream,
     each chunk detected as it lands (strided 2-D copies across designs, ragged
     last chunk).  Outputs must be bit-identical to the same call on device
@@ -133,7 +134,8 @@ def test_detect_host_chunked_upload(A, tc, monkeypatch):
     from paper_2206_05998_b200 import native as N
 
     monkeypatch.setenv("NOMA_DETECT_TC", tc)
-    dims, n_designs, K, rows = [32, 64, 64], 2, 3, 150001
+    dims, K = [32, 64, 64], 3
+    rows = 300001 // n_designs
     M = dims[0] // 2
     nets = [A.net_from_params(o.dims, o.w0, *o.layers())
             for o in (random_net_fused(dims, 200 + i) for i in range(n_designs * K))]
@@ -146,8 +148,15 @@ def test_detect_host_chunked_upload(A, tc, monkeypatch):
     soft = np.zeros((n_designs * K, rows), np.complex64)
     codes = np.zeros((n_designs * K, rows), np.uint8)
     errs = np.zeros(n_designs * K, np.uint32)
+    sers = np.zeros(n_designs * K, np.uint32)
     ctx.detect(dims, N.LAYOUT_WIDEN, n_designs, K, rows, x.view(np.float32), plans, truth=truth,
-               soft=soft.view(np.float32), codes=codes, bit_errors=errs)
+               soft=soft.view(np.float32), codes=codes, bit_errors=errs, symbol_errors=sers)
+    # fused counters = the decisions' mismatches (eval.cpp:56-65; SER: either bit)
+    tr = np.transpose(truth, (0, 2, 1)).reshape(n_designs * K, rows)
+    assert np.array_equal(sers.astype(np.int64), np.count_nonzero(codes != tr, axis=-1))
+    xor = codes ^ tr
+    assert np.array_equal(errs.astype(np.int64),
+                          np.count_nonzero(xor & 1, axis=-1) + np.count_nonzero(xor & 2, axis=-1))
     dev = torch.device("cuda", 0)
     xd = torch.from_numpy(x.view(np.float32)).to(dev)
     pd = torch.from_numpy(plans).to(dev)
