@@ -196,6 +196,7 @@ struct Stage {
     std::vector<Back> backs;
     bool ok = true;
     bool late = false;    // host->device copies pending on c->copy
+    bool late2 = false;   // device->host copies pending on c->copy2
     bool forked = false;  // work pending on c->side / c->side2
     Stage(noma_ctx_t c_, int mem_) : c(c_), mem(mem_) {}
     ~Stage() {
@@ -227,10 +228,16 @@ struct Stage {
         forked = false;
     }
     void late_join() {
-        if (!late) return;
-        cudaEventRecord(c->copied, c->copy);
-        cudaStreamWaitEvent(c->stream, c->copied, 0);
-        late = false;
+        if (late) {
+            cudaEventRecord(c->copied, c->copy);
+            cudaStreamWaitEvent(c->stream, c->copied, 0);
+            late = false;
+        }
+        if (late2) {
+            cudaEventRecord(c->copied, c->copy2);
+            cudaStreamWaitEvent(c->stream, c->copied, 0);
+            late2 = false;
+        }
     }
     void *alloc(size_t bytes) {
         if (bytes == 0) bytes = 16;
@@ -817,6 +824,7 @@ NOMA_API int noma_detect(noma_ctx_t c, const noma_net_desc *desc, int layout, in
     const size_t max_pitch = (size_t)(unsigned)max_pitch_i;
     cudaEventRecord(c->ev_alloc, c->stream);  // the buffer is allocated on the context stream
     cudaStreamWaitEvent(c->copy, c->ev_alloc, 0);
+    s.late = true;  // an early return joins the copy stream before freeing
     for (int r0 = 0; r0 < rows; r0 += per) {
         const int n = rows - r0 < per ? rows - r0 : per;
         const size_t pitch = (size_t)rows * row_f * sizeof(float), wbytes = n * row_f * sizeof(float);
@@ -933,6 +941,8 @@ NOMA_API int noma_pipeline(noma_ctx_t c, const noma_net_desc *desc, const noma_t
     if (host) {
         cudaEventRecord(c->ev_alloc, c->stream);
         cudaStreamWaitEvent(c->copy, c->ev_alloc, 0);
+        // any return below joins the copy streams before the scratch is freed
+        s.late = s.late2 = true;
         for (int ch = 0; ch < nchunk; ++ch) {
             const size_t a = (size_t)ch * chunk, sc = std::min<size_t>(chunk, S - a);
             h2d(pilot_rx + a * px_n, px + a * px_n, sc * px_n * 8);
