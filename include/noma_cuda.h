@@ -118,11 +118,16 @@ NOMA_API long long noma_ctx_kernel_launches(noma_ctx_t ctx);
  * 1 = one CTA per net (16 warps), 2 = two 8-warp CTAs per SM,
  * 10 + c = row-split cluster of c CTAs per net (DSMEM gradient reduce),
  * 100 + c = neuron-split latency cluster of c CTAs per net (k_train_lat.cu),
- * 0 = none yet. */
+ * 3 = 4-warp one-hidden-layer kernel (k_train_w4.cu),
+ * 200 = shape-general FP32 kernel (k_train_generic.cu: layers wider than 128,
+ *       minibatches above 128 rows), 201 = its FP64 instance (noma_train_f64),
+ * 300 = on-chip FP64 kernel (k_train_f64.cu), 0 = none yet.
+ * NOMA_TRAIN_GENERIC=1 in the environment forces the shape-general kernel. */
 NOMA_API int noma_ctx_train_mode(noma_ctx_t ctx);
 /* Which detection kernel the last noma_detect / noma_pipeline call used:
  * 1 = FP32 FFMA register tiles (k_detect.cu), 2 = tcgen05 3xTF32 tensor-core
  * kernel (k_detect_tc.cu; widened input 32/64, hidden layers of 64),
+ * 3 = shape-general single-pass tiles (k_dense.cu: layers wider than 128),
  * 0 = none yet.  NOMA_DETECT_TC=0 in the environment forces the FFMA kernel. */
 NOMA_API int noma_ctx_detect_mode(noma_ctx_t ctx);
 /* Slot chunks the last noma_pipeline call ran in (instrumentation). */
@@ -190,7 +195,9 @@ NOMA_API int noma_lls_predict(noma_ctx_t ctx, int layout, int n_designs, int net
 
 /* Replaces hybrid_nn::train (hybrid_nn.hpp:70-72, hybrid_nn.cpp:158-195)
  * for every net of `ds`: one fused kernel per net runs all epochs x
- * minibatches (forward, backward, Adam) with the weights resident on chip.
+ * minibatches (forward, backward, Adam) with the weights resident on chip;
+ * shapes outside the on-chip kernels (a layer wider than 128, batch_size
+ * above 128) run the shape-general kernel (train mode 200).
  * plans_inout [net][plan] holds the initial parameters (incl. w0) and
  * receives the trained ones; shuffle_seeds [net] are TrainConfig::shuffle_seed;
  * loss_trace [net][epochs] nullable; status [net] nullable. */
@@ -231,7 +238,8 @@ NOMA_API int noma_detect(noma_ctx_t ctx, const noma_net_desc *desc, int layout, 
  * bounded scratch (NOMA_CHUNK_MB, default 4096); with NOMA_MEM_HOST each
  * chunk's inputs are uploaded ahead on a copy stream and its results
  * downloaded while the next chunk computes.  Networks wider than 128 or
- * minibatches above 128 rows return NOMA_ERR_UNSUPPORTED before any work. */
+ * minibatches above 128 rows train and detect in the shape-general kernels
+ * (train mode 200, detect mode 3). */
 NOMA_API int noma_pipeline(noma_ctx_t ctx, const noma_net_desc *desc, const noma_train_cfg *cfg,
                            int S, int K, int M, int NT, int ND, const double *pilot_rx,
                            const double *pilot_sym, const float *data_rx, const uint8_t *truth,
@@ -239,6 +247,51 @@ NOMA_API int noma_pipeline(noma_ctx_t ctx, const noma_net_desc *desc, const noma
                            double *w0, double *gram_condition, float *plans, double *loss_trace,
                            float *soft, uint8_t *codes, uint32_t *bit_errors,
                            uint32_t *symbol_errors, int *status, int mem);
+
+/* ------------------------------------------------ one network, FP64 API */
+
+/* Evaluation paths of noma_forward_* (fused_inference.cpp:172-231 dispatch). */
+enum noma_path {
+    NOMA_PATH_AUTO = 0,     /* single-pass when every width <= 128, else per-layer */
+    NOMA_PATH_FUSED = 1,    /* single-pass row tiles, activations on chip (fused_kernel) */
+    NOMA_PATH_FALLBACK = 2, /* one launch per layer, activations in HBM (fallback_kernel) */
+    NOMA_PATH_NAIVE = 3     /* per layer: GEMM, bias, ReLU as separate launches */
+};
+
+/* Replaces fused::fused_forward / fused_forward_into (FP64) and
+ * fused_forward_f32 (FP32), and hybrid_nn::forward (fused_inference.hpp:53-60,
+ * hybrid_nn.hpp:59): out[rows] = X w0 + a_N w_{N+1} for ONE network.
+ *   plan : the FusedPlan buffer (fused_inference.cpp:19-42), f64 or f32;
+ *   x    : COLUMN-major [dims[0]][rows] (Eigen storage of the B x 2M input);
+ *   path : enum noma_path.  Any widths (the on-chip tile height adapts).
+ * The linear branch is accumulated in column order without FMA, so a zero
+ * final layer returns X w0 exactly as the reference's GEMV does.  With
+ * NOMA_MEM_HOST the call stages through a persistent device workspace and
+ * performs no host heap allocation once warm (test_fused.cpp:133-144). */
+NOMA_API int noma_forward_f64(noma_ctx_t ctx, const noma_net_desc *desc, const double *plan, int rows,
+                              const double *x, double *out, int path, int mem);
+NOMA_API int noma_forward_f32(noma_ctx_t ctx, const noma_net_desc *desc, const float *plan, int rows,
+                              const float *x, float *out, int path, int mem);
+
+/* Device timing behind fused::bench_compare (fused_inference.cpp:262-314):
+ * median over `repeats` (<= 64) launches of one evaluation path with the
+ * batch resident in HBM, CUDA events on the context stream, in ns. */
+NOMA_API int noma_bench_forward_f64(noma_ctx_t ctx, const noma_net_desc *desc, const double *plan, int rows,
+                                    const double *x, int path, int repeats, double *ns_median);
+
+/* Replaces hybrid_nn::loss_and_grad (hybrid_nn.hpp:63-64, hybrid_nn.cpp:84-114)
+ * in FP64 for one network: loss = ||X w0 + a_N w - y||^2 / B, grad [trainable]
+ * in the reference flat order W_1 (row-major L_1 x L_0), b_1, ..., W_N, b_N,
+ * final.  plan: FP64 FusedPlan buffer; x column-major [dims[0]][rows]. */
+NOMA_API int noma_loss_and_grad(noma_ctx_t ctx, const noma_net_desc *desc, const double *plan, int rows,
+                                const double *x, const double *y, double *loss, double *grad, int mem);
+
+/* Replaces hybrid_nn::adam_step (hybrid_nn.hpp:67, hybrid_nn.cpp:118-144) on a
+ * flat FP64 parameter vector: m, v updated in place; corr_i = 1 - beta_i^step
+ * computed by the caller with std::pow as the reference does (:133-135). */
+NOMA_API int noma_adam_step(noma_ctx_t ctx, int n, double *theta, const double *grad, double *m, double *v,
+                            double corr1, double corr2, double lr, double beta1, double beta2, double eps,
+                            int mem);
 
 /* Replaces synthesize(cfg, SeedBundle::from_master(seed)) (channel_sim.cpp:76-117)
  * on device for S slots with master seeds [S].  Outputs (nullable):
@@ -255,6 +308,12 @@ NOMA_API int noma_synthesize_bundles(noma_ctx_t ctx, const noma_scenario *sc, in
                                      const uint64_t *bundles, double *pilot_rx, double *pilot_sym,
                                      float *data_rx, uint8_t *data_codes, double *channel,
                                      double *noise_power, int mem);
+
+/* As noma_synthesize_bundles with the data-phase receive matrix in FP64
+ * (data_rx [S][ND][M] c64): the C++ API's TransmissionRecord is all FP64. */
+NOMA_API int noma_synthesize_f64(noma_ctx_t ctx, const noma_scenario *sc, int S, const uint64_t *bundles,
+                                 double *pilot_rx, double *pilot_sym, double *data_rx, uint8_t *data_codes,
+                                 double *channel, double *noise_power, int mem);
 
 #ifdef __cplusplus
 }

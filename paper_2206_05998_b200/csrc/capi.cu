@@ -1,4 +1,5 @@
 // C-ABI (include/noma_cuda.h): context, staging and the batched entry points.
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -159,6 +160,11 @@ struct noma_ctx_s {
     cudaStream_t copy = nullptr;          // late host->device input copies (data phase)
     cudaStream_t copy2 = nullptr;         // per-chunk device->host result copies
     cudaEvent_t ev_alloc = nullptr, copied = nullptr;
+    // persistent device workspace of the per-network entry points
+    // (noma_forward_*, noma_loss_and_grad, noma_adam_step): grown, never
+    // shrunk, so steady-state calls allocate nothing (test_fused.cpp:133-144)
+    void *ws = nullptr;
+    size_t ws_bytes = 0;
 };
 
 namespace {
@@ -333,6 +339,96 @@ LlsParams lls_params(const noma_dataset *ds, const double *x, const double *y, d
     return p;
 }
 
+// Device workspace of at least `bytes` (see noma_ctx_s::ws); growing it
+// synchronises the context stream first so no queued launch loses its buffer.
+void *ws_get(noma_ctx_t c, size_t bytes) {
+    if (bytes <= c->ws_bytes) return c->ws;
+    cudaStreamSynchronize(c->stream);
+    if (c->ws) cudaFree(c->ws);
+    c->ws = nullptr;
+    c->ws_bytes = 0;
+    size_t want = bytes < 2 * c->ws_bytes ? 2 * c->ws_bytes : bytes;
+    want = (want + 255) & ~(size_t)255;
+    if (cudaMalloc(&c->ws, want) != cudaSuccess) {
+        c->ws = nullptr;
+        return nullptr;
+    }
+    c->ws_bytes = want;
+    return c->ws;
+}
+
+// bump allocator over the workspace (256-byte aligned slices)
+struct Carve {
+    size_t off = 0;
+    template <class T> size_t take(size_t n) {
+        const size_t o = off;
+        off += (n * sizeof(T) + 255) & ~(size_t)255;
+        return o;
+    }
+};
+
+// Shape-general FP32 training (k_train_generic.cu) on the inputs the on-chip
+// kernels were given: design32, r0 and perm of `tp`.
+template <class StageT>
+int train_generic_f32(noma_ctx_t c, StageT &s, const TrainParams &tp, cudaStream_t st) {
+    TrainGenParams<float> gp;
+    gp.g = tp.g;
+    gp.layout = tp.layout;
+    gp.n_nets = tp.n_nets;
+    gp.K = tp.K;
+    gp.rows = tp.rows;
+    gp.epochs = tp.epochs;
+    gp.batch = tp.batch;
+    gp.design32 = tp.design32;
+    gp.r0 = tp.r0;
+    gp.design = gp.targets = gp.w0 = nullptr;
+    gp.perm = tp.perm;
+    gp.plan = tp.plans;
+    gp.trace = tp.trace;
+    gp.status = tp.status;
+    gp.scratch_per_net = train_generic_scratch(tp.g, tp.batch);
+    gp.scratch = s.template scratch<float>((size_t)tp.n_nets * gp.scratch_per_net);
+    gp.lr = tp.lr_d;
+    gp.b1 = tp.b1d;
+    gp.b2 = tp.b2d;
+    gp.eps = (double)tp.eps;
+    if (!gp.scratch) return NOMA_ERR_CUDA;
+    c->train_mode = 200;
+    return train_generic_launch<float>(gp, st);
+}
+
+bool force_generic_train() {
+    const char *e = std::getenv("NOMA_TRAIN_GENERIC");
+    return e && e[0] == '1';
+}
+
+// Shape-general FP32 detection (fwd_tile_kernel) with the same inputs and
+// outputs as detect_launch.
+int detect_generic(noma_ctx_t c, const DetectParams &dp, cudaStream_t st) {
+    FwdParams<float> fp;
+    fp.g = dp.g;
+    const bool cplx = dp.layout == NOMA_LAYOUT_WIDEN_COMPLEX;
+    fp.src = cplx ? kSrcComplex : kSrcRowMajor;
+    fp.n_nets = dp.n_nets;
+    fp.K = dp.K;
+    const int stride = dp.stride ? dp.stride : dp.rows;
+    fp.rows = cplx ? 2 * dp.rows : dp.rows;
+    fp.stride = stride;
+    fp.x = dp.data;
+    fp.ldx = 0;
+    fp.plan = dp.plans;
+    fp.out = dp.soft;
+    fp.out_stride = cplx ? 2 * (long long)stride : stride;
+    fp.codes = dp.codes;
+    fp.code_stride = stride;
+    fp.truth = dp.truth;
+    fp.errors = dp.errors;
+    fp.sym_errors = dp.sym_errors;
+    fp.status = dp.status;
+    c->detect_mode = 3;
+    return fwd_tile_launch<float>(fp, st);
+}
+
 int check_cfg(noma_ctx_t c, const noma_train_cfg *cfg) {
     if (!cfg) return fail(c, NOMA_ERR_ARGUMENT, "null cfg");
     if (cfg->epochs < 0 || cfg->batch_size < 1 || !(cfg->lr > 0.0))
@@ -436,6 +532,7 @@ NOMA_API int noma_ctx_destroy(noma_ctx_t c) {
     if (c->fork) cudaEventDestroy(c->fork);
     if (c->join) cudaEventDestroy(c->join);
     if (c->own) cudaStreamDestroy(c->own);
+    if (c->ws) cudaFree(c->ws);
     delete c;
     return NOMA_OK;
 }
@@ -693,9 +790,14 @@ NOMA_API int noma_train(noma_ctx_t c, const noma_dataset *ds, const noma_net_des
     tp.trace = dt;
     tp.status = dst;
     if (cfg->epochs > 0) {
-        prep_scratch(s, tp);
-        st = train_launch(tp, c->stream);
-        c->train_mode = tp.mode;
+        if (force_generic_train()) {
+            st = NOMA_ERR_UNSUPPORTED;
+        } else {
+            prep_scratch(s, tp);
+            st = train_launch(tp, c->stream);
+            c->train_mode = tp.mode;
+        }
+        if (st == NOMA_ERR_UNSUPPORTED) st = train_generic_f32(c, s, tp, c->stream);
         if (st) return st == NOMA_ERR_CUDA ? cuda_fail(c, "train") : fail(c, st, "train: unsupported network shape");
     }
     c->launches += 3;
@@ -751,7 +853,37 @@ NOMA_API int noma_train_f64(noma_ctx_t c, const noma_dataset *ds, const noma_net
     tp.b2 = cfg->beta2;
     tp.eps = cfg->eps;
     if (cfg->epochs > 0) {
-        st = train_f64_launch(tp, c->stream);
+        st = force_generic_train() ? NOMA_ERR_UNSUPPORTED : train_f64_launch(tp, c->stream);
+        c->train_mode = 300;
+        if (st == NOMA_ERR_UNSUPPORTED) {  // shape-general FP64 kernel on the FusedPlan layout
+            TrainGenParams<double> gp;
+            gp.g = g;
+            gp.layout = ds->layout;
+            gp.n_nets = (int)nets;
+            gp.K = ds->nets_per_design;
+            gp.rows = ds->rows;
+            gp.epochs = cfg->epochs;
+            gp.batch = cfg->batch_size;
+            gp.design32 = gp.r0 = nullptr;
+            gp.design = x;
+            gp.targets = y;
+            gp.w0 = dw;
+            gp.perm = perm;
+            gp.plan = s.scratch<double>(nets * g.plan_total);
+            gp.trace = dt;
+            gp.status = dst;
+            gp.scratch_per_net = train_generic_scratch(g, cfg->batch_size);
+            gp.scratch = s.scratch<double>(nets * gp.scratch_per_net);
+            gp.lr = cfg->lr;
+            gp.b1 = cfg->beta1;
+            gp.b2 = cfg->beta2;
+            gp.eps = cfg->eps;
+            if (!s.ok) return s.finish();
+            if (theta_plan_launch(g, (int)nets, dth, gp.plan, dw, 1, c->stream)) return cuda_fail(c, "theta->plan");
+            st = train_generic_launch<double>(gp, c->stream);
+            if (!st && theta_plan_launch(g, (int)nets, dth, gp.plan, dw, 0, c->stream)) return cuda_fail(c, "plan->theta");
+            c->train_mode = 201;
+        }
         if (st) return st == NOMA_ERR_CUDA ? cuda_fail(c, "train f64") : fail(c, st, "train f64: unsupported shape");
     }
     c->launches += 2;
@@ -809,8 +941,9 @@ NOMA_API int noma_detect(noma_ctx_t c, const noma_net_desc *desc, int layout, in
     dpp.mode = 0;
     dpp.stride = rows;
     if (chunks == 1) {
-        const int st = detect_launch(dpp, c->stream);
+        int st = detect_launch(dpp, c->stream);
         c->detect_mode = dpp.mode;
+        if (st == NOMA_ERR_UNSUPPORTED) st = detect_generic(c, dpp, c->stream);
         if (st) return st == NOMA_ERR_CUDA ? cuda_fail(c, "detect") : fail(c, st, "detect: unsupported network shape");
         c->launches += 1;
         return s.finish();
@@ -847,8 +980,9 @@ NOMA_API int noma_detect(noma_ctx_t c, const noma_net_desc *desc, int layout, in
         dc.truth = dtr ? dtr + (size_t)r0 * nets_per_design : nullptr;
         dc.soft = dso ? dso + r0 * soft_f : nullptr;
         dc.codes = dco ? dco + r0 : nullptr;
-        const int st = detect_launch(dc, c->stream);
+        int st = detect_launch(dc, c->stream);
         c->detect_mode = dc.mode;
+        if (st == NOMA_ERR_UNSUPPORTED) st = detect_generic(c, dc, c->stream);
         if (st) return st == NOMA_ERR_CUDA ? cuda_fail(c, "detect") : fail(c, st, "detect: unsupported network shape");
         c->launches += 1;
     }
@@ -873,8 +1007,6 @@ NOMA_API int noma_pipeline(noma_ctx_t c, const noma_net_desc *desc, const noma_t
     if (S < 0 || K < 1 || M < 1 || NT < 1 || ND < 0) return fail(c, NOMA_ERR_DIMENSION, "bad sizes");
     if (2 * NT < 2 * M) return fail(c, NOMA_ERR_DIMENSION, "lls::fit: system must be over-determined");
     if (2 * NT > 65535) return fail(c, NOMA_ERR_UNSUPPORTED, "too many pilot rows");
-    if (cfg->epochs > 0 && (cfg->batch_size > NOMA_MAX_BATCH || g.maxfp > NOMA_MAX_WIDTH))
-        return fail(c, NOMA_ERR_UNSUPPORTED, "train: batch > 128 or a layer wider than 128");
     if (S == 0) return NOMA_OK;
     const size_t nets = (size_t)S * K;
     const int n = 2 * NT;
@@ -1047,9 +1179,14 @@ NOMA_API int noma_pipeline(noma_ctx_t c, const noma_net_desc *desc, const noma_t
             constexpr int kClk = 8 + 4 * 16 * 16;
             if (clocks) tp.clocks = s.scratch<long long>(kClk);
             if (clocks && tp.clocks) cudaMemsetAsync(tp.clocks, 0, kClk * sizeof(long long), c->stream);
-            prep_scratch(s, tp);
-            st = train_launch(tp, c->stream);
-            c->train_mode = tp.mode;
+            if (force_generic_train()) {
+                st = NOMA_ERR_UNSUPPORTED;
+            } else {
+                prep_scratch(s, tp);
+                st = train_launch(tp, c->stream);
+                c->train_mode = tp.mode;
+            }
+            if (st == NOMA_ERR_UNSUPPORTED) st = train_generic_f32(c, s, tp, c->stream);
             if (st) return st == NOMA_ERR_CUDA ? cuda_fail(c, "train") : fail(c, st, "train: unsupported network shape");
             c->launches += 1;
             if (clocks) {  // instrumentation only: per-phase cycles of net 0
@@ -1090,6 +1227,7 @@ NOMA_API int noma_pipeline(noma_ctx_t c, const noma_net_desc *desc, const noma_t
             dpp.mode = 0;
             st = detect_launch(dpp, c->stream);
             c->detect_mode = dpp.mode;
+            if (st == NOMA_ERR_UNSUPPORTED) st = detect_generic(c, dpp, c->stream);
             if (st) return st == NOMA_ERR_CUDA ? cuda_fail(c, "detect") : fail(c, st, "detect: unsupported network shape");
             c->launches += 1;
         }
@@ -1123,10 +1261,227 @@ NOMA_API int noma_pipeline(noma_ctx_t c, const noma_net_desc *desc, const noma_t
 
 }  // extern "C"
 
+// ------------------------------------------------ per-network FP64 entries
+// (the reference's C++ API one network at a time: fused_forward,
+// hybrid_nn::forward / loss_and_grad / adam_step).  Host buffers are staged
+// through the context's persistent workspace: no heap allocation per call.
+namespace {
+template <class T>
+int forward_impl(noma_ctx_t c, const noma_net_desc *desc, const T *plan, int rows, const T *x, T *out, int path,
+                 int mem) {
+    if (!c) return NOMA_ERR_ARGUMENT;
+    NetGeom g;
+    if (!make_geom(desc, &g)) return fail(c, NOMA_ERR_DIMENSION, "forward: bad dims");
+    if (!plan || (!x && rows > 0) || (!out && rows > 0)) return fail(c, NOMA_ERR_ARGUMENT, "null argument");
+    if (rows < 0) return fail(c, NOMA_ERR_DIMENSION, "forward: negative row count");
+    if (rows == 0) return NOMA_OK;
+    int maxw = 0;
+    size_t hsum = 0;
+    for (int l = 0; l < g.nd; ++l) maxw = g.dims[l] > maxw ? g.dims[l] : maxw;
+    for (int l = 1; l < g.nd; ++l) hsum += g.dims[l];
+    if (path == NOMA_PATH_AUTO) path = maxw <= NOMA_MAX_WIDTH ? NOMA_PATH_FUSED : NOMA_PATH_FALLBACK;
+    const bool host = mem == NOMA_MEM_HOST;
+    const size_t xe = (size_t)rows * g.dims[0];
+    Carve cv;
+    const size_t o_plan = host ? cv.take<T>(g.plan_total) : 0, o_x = host ? cv.take<T>(xe) : 0,
+                 o_out = host ? cv.take<T>(rows) : 0;
+    const size_t o_act = path == NOMA_PATH_FUSED ? 0 : cv.take<T>(hsum * (size_t)rows + 1);
+    char *base = cv.off ? static_cast<char *>(ws_get(c, cv.off)) : nullptr;
+    if (cv.off && !base) return fail(c, NOMA_ERR_CUDA, "forward: workspace allocation");
+    const T *dplan = host ? reinterpret_cast<T *>(base + o_plan) : plan;
+    const T *dx = host ? reinterpret_cast<T *>(base + o_x) : x;
+    T *dout = host ? reinterpret_cast<T *>(base + o_out) : out;
+    if (host) {
+        if (cudaMemcpyAsync(const_cast<T *>(dplan), plan, g.plan_total * sizeof(T), cudaMemcpyHostToDevice, c->stream) ||
+            cudaMemcpyAsync(const_cast<T *>(dx), x, xe * sizeof(T), cudaMemcpyHostToDevice, c->stream))
+            return cuda_fail(c, "forward: upload");
+    }
+    int st;
+    if (path == NOMA_PATH_FUSED) {
+        FwdParams<T> fp{};
+        fp.g = g;
+        fp.src = kSrcColMajor;
+        fp.n_nets = 1;
+        fp.K = 1;
+        fp.rows = rows;
+        fp.stride = rows;
+        fp.x = dx;
+        fp.ldx = rows;
+        fp.plan = dplan;
+        fp.out = dout;
+        fp.out_stride = rows;
+        st = fwd_tile_launch<T>(fp, c->stream);
+        c->launches += 1;
+    } else {
+        T *acts = reinterpret_cast<T *>(base + o_act);
+        st = layer_forward_launch<T>(g, dplan, dx, rows, rows, acts, path == NOMA_PATH_NAIVE, nullptr, dout, nullptr,
+                                     c->stream);
+        c->launches += (g.nd - 1) * (path == NOMA_PATH_NAIVE ? 3 : 1) + 1;
+    }
+    if (st) return st == NOMA_ERR_CUDA ? cuda_fail(c, "forward") : fail(c, st, "forward: unsupported shape");
+    if (host) {
+        if (cudaMemcpyAsync(out, dout, rows * sizeof(T), cudaMemcpyDeviceToHost, c->stream))
+            return cuda_fail(c, "forward: download");
+        if (cudaStreamSynchronize(c->stream) != cudaSuccess) return cuda_fail(c, "forward: synchronize");
+    }
+    return NOMA_OK;
+}
+}  // namespace
+
+extern "C" {
+
+NOMA_API int noma_forward_f64(noma_ctx_t c, const noma_net_desc *desc, const double *plan, int rows,
+                              const double *x, double *out, int path, int mem) {
+    return forward_impl<double>(c, desc, plan, rows, x, out, path, mem);
+}
+
+NOMA_API int noma_forward_f32(noma_ctx_t c, const noma_net_desc *desc, const float *plan, int rows,
+                              const float *x, float *out, int path, int mem) {
+    return forward_impl<float>(c, desc, plan, rows, x, out, path, mem);
+}
+
+NOMA_API int noma_bench_forward_f64(noma_ctx_t c, const noma_net_desc *desc, const double *plan, int rows,
+                                    const double *x, int path, int repeats, double *ns_median) {
+    if (!c) return NOMA_ERR_ARGUMENT;
+    NetGeom g;
+    if (!make_geom(desc, &g)) return fail(c, NOMA_ERR_DIMENSION, "bench_forward: bad dims");
+    if (!plan || !x || !ns_median || rows < 1 || repeats < 1) return fail(c, NOMA_ERR_ARGUMENT, "bad argument");
+    size_t hsum = 0;
+    for (int l = 1; l < g.nd; ++l) hsum += g.dims[l];
+    const size_t xe = (size_t)rows * g.dims[0];
+    Carve cv;
+    const size_t o_plan = cv.take<double>(g.plan_total), o_x = cv.take<double>(xe), o_out = cv.take<double>(rows),
+                 o_act = cv.take<double>(hsum * (size_t)rows + 1);
+    char *base = static_cast<char *>(ws_get(c, cv.off));
+    if (!base) return fail(c, NOMA_ERR_CUDA, "bench_forward: workspace allocation");
+    double *dplan = reinterpret_cast<double *>(base + o_plan), *dx = reinterpret_cast<double *>(base + o_x),
+           *dout = reinterpret_cast<double *>(base + o_out), *acts = reinterpret_cast<double *>(base + o_act);
+    if (cudaMemcpyAsync(dplan, plan, g.plan_total * 8, cudaMemcpyHostToDevice, c->stream) ||
+        cudaMemcpyAsync(dx, x, xe * 8, cudaMemcpyHostToDevice, c->stream))
+        return cuda_fail(c, "bench_forward: upload");
+    auto run = [&]() -> int {
+        if (path == NOMA_PATH_FUSED) {
+            FwdParams<double> fp{};
+            fp.g = g;
+            fp.src = kSrcColMajor;
+            fp.n_nets = fp.K = 1;
+            fp.rows = fp.stride = rows;
+            fp.x = dx;
+            fp.ldx = rows;
+            fp.plan = dplan;
+            fp.out = dout;
+            fp.out_stride = rows;
+            return fwd_tile_launch<double>(fp, c->stream);
+        }
+        return layer_forward_launch<double>(g, dplan, dx, rows, rows, acts, path == NOMA_PATH_NAIVE, nullptr, dout,
+                                            nullptr, c->stream);
+    };
+    if (run()) return cuda_fail(c, "bench_forward");  // warm-up
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    double best[64];
+    const int n = repeats < 64 ? repeats : 64;
+    for (int i = 0; i < n; ++i) {
+        cudaEventRecord(e0, c->stream);
+        run();
+        cudaEventRecord(e1, c->stream);
+        cudaEventSynchronize(e1);
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, e0, e1);
+        best[i] = 1e6 * (double)ms;
+    }
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    std::sort(best, best + n);
+    *ns_median = best[n / 2];
+    c->launches += n + 1;
+    return cudaGetLastError() == cudaSuccess ? NOMA_OK : cuda_fail(c, "bench_forward");
+}
+
+NOMA_API int noma_loss_and_grad(noma_ctx_t c, const noma_net_desc *desc, const double *plan, int rows,
+                                const double *x, const double *y, double *loss, double *grad, int mem) {
+    if (!c) return NOMA_ERR_ARGUMENT;
+    NetGeom g;
+    if (!make_geom(desc, &g)) return fail(c, NOMA_ERR_DIMENSION, "loss_and_grad: bad dims");
+    if (rows < 1) return fail(c, NOMA_ERR_DIMENSION, "loss_and_grad: empty batch");
+    if (!plan || !x || !y || !loss || !grad) return fail(c, NOMA_ERR_ARGUMENT, "null argument");
+    const int P = trainable_count(g);
+    const bool host = mem == NOMA_MEM_HOST;
+    const size_t xe = (size_t)rows * g.dims[0];
+    Carve cv;
+    const size_t o_plan = host ? cv.take<double>(g.plan_total) : 0, o_x = host ? cv.take<double>(xe) : 0,
+                 o_y = host ? cv.take<double>(rows) : 0, o_l = host ? cv.take<double>(1) : 0,
+                 o_g = host ? cv.take<double>(P) : 0;
+    const size_t o_ws = cv.take<double>(loss_grad_scratch(g, rows));
+    char *base = static_cast<char *>(ws_get(c, cv.off));
+    if (!base) return fail(c, NOMA_ERR_CUDA, "loss_and_grad: workspace allocation");
+    auto at = [&](size_t o) { return reinterpret_cast<double *>(base + o); };
+    const double *dplan = host ? at(o_plan) : plan, *dx = host ? at(o_x) : x, *dy = host ? at(o_y) : y;
+    double *dl = host ? at(o_l) : loss, *dg = host ? at(o_g) : grad;
+    if (host) {
+        if (cudaMemcpyAsync(at(o_plan), plan, g.plan_total * 8, cudaMemcpyHostToDevice, c->stream) ||
+            cudaMemcpyAsync(at(o_x), x, xe * 8, cudaMemcpyHostToDevice, c->stream) ||
+            cudaMemcpyAsync(at(o_y), y, (size_t)rows * 8, cudaMemcpyHostToDevice, c->stream))
+            return cuda_fail(c, "loss_and_grad: upload");
+    }
+    if (loss_grad_launch(g, dplan, dx, rows, dy, at(o_ws), dl, dg, c->stream)) return cuda_fail(c, "loss_and_grad");
+    c->launches += 3 + 4 * (g.nd - 1);
+    if (host) {
+        if (cudaMemcpyAsync(loss, dl, 8, cudaMemcpyDeviceToHost, c->stream) ||
+            cudaMemcpyAsync(grad, dg, (size_t)P * 8, cudaMemcpyDeviceToHost, c->stream))
+            return cuda_fail(c, "loss_and_grad: download");
+        if (cudaStreamSynchronize(c->stream) != cudaSuccess) return cuda_fail(c, "loss_and_grad: synchronize");
+    }
+    return NOMA_OK;
+}
+
+NOMA_API int noma_adam_step(noma_ctx_t c, int n, double *theta, const double *grad, double *m, double *v,
+                            double corr1, double corr2, double lr, double beta1, double beta2, double eps,
+                            int mem) {
+    if (!c) return NOMA_ERR_ARGUMENT;
+    if (n < 0) return fail(c, NOMA_ERR_DIMENSION, "adam_step: negative size");
+    if (n == 0) return NOMA_OK;
+    if (!theta || !grad || !m || !v) return fail(c, NOMA_ERR_ARGUMENT, "null argument");
+    const bool host = mem == NOMA_MEM_HOST;
+    double *dt = theta, *dm = m, *dv = v;
+    const double *dg = grad;
+    if (host) {
+        Carve cv;
+        const size_t o_t = cv.take<double>(n), o_g = cv.take<double>(n), o_m = cv.take<double>(n),
+                     o_v = cv.take<double>(n);
+        char *base = static_cast<char *>(ws_get(c, cv.off));
+        if (!base) return fail(c, NOMA_ERR_CUDA, "adam_step: workspace allocation");
+        dt = reinterpret_cast<double *>(base + o_t);
+        dm = reinterpret_cast<double *>(base + o_m);
+        dv = reinterpret_cast<double *>(base + o_v);
+        double *g2 = reinterpret_cast<double *>(base + o_g);
+        dg = g2;
+        if (cudaMemcpyAsync(dt, theta, (size_t)n * 8, cudaMemcpyHostToDevice, c->stream) ||
+            cudaMemcpyAsync(g2, grad, (size_t)n * 8, cudaMemcpyHostToDevice, c->stream) ||
+            cudaMemcpyAsync(dm, m, (size_t)n * 8, cudaMemcpyHostToDevice, c->stream) ||
+            cudaMemcpyAsync(dv, v, (size_t)n * 8, cudaMemcpyHostToDevice, c->stream))
+            return cuda_fail(c, "adam_step: upload");
+    }
+    if (adam_launch(n, dt, dg, dm, dv, corr1, corr2, lr, beta1, beta2, eps, c->stream)) return cuda_fail(c, "adam_step");
+    c->launches += 1;
+    if (host) {
+        if (cudaMemcpyAsync(theta, dt, (size_t)n * 8, cudaMemcpyDeviceToHost, c->stream) ||
+            cudaMemcpyAsync(m, dm, (size_t)n * 8, cudaMemcpyDeviceToHost, c->stream) ||
+            cudaMemcpyAsync(v, dv, (size_t)n * 8, cudaMemcpyDeviceToHost, c->stream))
+            return cuda_fail(c, "adam_step: download");
+        if (cudaStreamSynchronize(c->stream) != cudaSuccess) return cuda_fail(c, "adam_step: synchronize");
+    }
+    return NOMA_OK;
+}
+
+}  // extern "C"
+
 namespace {
 int synthesize_impl(noma_ctx_t c, const noma_scenario *sc, int S, const uint64_t *master_seeds,
                     int bundles, double *pilot_rx, double *pilot_sym, float *data_rx,
-                    uint8_t *data_codes, double *channel, double *noise_power, int mem) {
+                    uint8_t *data_codes, double *channel, double *noise_power, int mem,
+                    double *data_rx64 = nullptr) {
     if (!c) return NOMA_ERR_ARGUMENT;
     if (!sc || !master_seeds) return fail(c, NOMA_ERR_ARGUMENT, "null argument");
     // ScenarioConfig::validate (channel_sim.cpp:9-21)
@@ -1157,6 +1512,7 @@ int synthesize_impl(noma_ctx_t c, const noma_scenario *sc, int S, const uint64_t
     p.pilot_rx = s.out(pilot_rx, (size_t)S * NT * M * 2);
     p.pilot_sym = s.out(pilot_sym, (size_t)S * NT * K * 2);
     p.data_rx = s.out(data_rx, (size_t)S * ND * M * 2);
+    p.data_rx64 = s.out(data_rx64, (size_t)S * ND * M * 2);
     p.data_codes = s.out(data_codes, (size_t)S * ND * K);
     p.channel = channel ? s.out(channel, (size_t)S * M * K * 2) : s.scratch<double>((size_t)S * M * K * 2);
     double *np = noise_power ? s.out(noise_power, (size_t)S) : s.scratch<double>((size_t)S);
@@ -1191,6 +1547,13 @@ NOMA_API int noma_synthesize_bundles(noma_ctx_t c, const noma_scenario *sc, int 
                                      double *noise_power, int mem) {
     return synthesize_impl(c, sc, S, bundles, 1, pilot_rx, pilot_sym, data_rx, data_codes,
                            channel, noise_power, mem);
+}
+
+NOMA_API int noma_synthesize_f64(noma_ctx_t c, const noma_scenario *sc, int S, const uint64_t *bundles,
+                                 double *pilot_rx, double *pilot_sym, double *data_rx, uint8_t *data_codes,
+                                 double *channel, double *noise_power, int mem) {
+    return synthesize_impl(c, sc, S, bundles, 1, pilot_rx, pilot_sym, nullptr, data_codes, channel, noise_power,
+                           mem, data_rx);
 }
 
 }  // extern "C"

@@ -470,6 +470,11 @@ __global__ void synth_mix_kernel(SynthParams p, const double *noise_power) {
             o[0] = (float)re;
             o[1] = (float)im;
         }
+        if (p.data_rx64) {
+            double *o = p.data_rx64 + (((size_t)s * p.ND + td) * p.M + m) * 2;
+            o[0] = re;
+            o[1] = im;
+        }
         if (p.data_codes && m < p.K) p.data_codes[((size_t)s * p.ND + td) * p.K + m] = codes[m];
     }
 }

@@ -86,11 +86,56 @@ struct SynthParams {
     double *pilot_rx;      // [S][NT][M] c64
     double *pilot_sym;     // [S][NT][K] c64
     float *data_rx;        // [S][ND][M] c32
+    double *data_rx64;     // [S][ND][M] c64 (nullable; the C++ API's FP64 record)
     uint8_t *data_codes;   // [S][ND][K]
     double *channel;       // [S][M][K] c64 (scratch or output)
     double *noise_power;   // [S]
     uint8_t *codes_all;    // scratch [S][NT+ND][K]
     double *noise;         // scratch [S][NT+ND][M] c64 (unit gaussians, g++ draw order)
+};
+
+// Shape-general forward (k_dense.cu): input source of fwd_tile_kernel
+constexpr int kSrcColMajor = 0;  // x[c * ldx + R] (Eigen column-major, one design)
+constexpr int kSrcRowMajor = 1;  // REAL rows [S][stride][width]
+constexpr int kSrcComplex = 2;   // complex rows [S][stride][width/2], widened at load
+
+template <class T>
+struct FwdParams {
+    NetGeom g;
+    int src, n_nets, K;
+    int rows;                 // input rows of this launch (widened rows for kSrcComplex)
+    int stride;               // row stride per design (symbols for kSrcComplex)
+    const T *x;
+    long long ldx;            // kSrcColMajor leading dimension
+    const T *plan;            // [net][plan_total]
+    T *out;                   // out[net * out_stride + R] (nullable)
+    long long out_stride;
+    uint8_t *codes;           // kSrcComplex: [net][code_stride] QPSK codes (nullable)
+    long long code_stride;
+    const uint8_t *truth;     // kSrcComplex: [S][stride][K] (nullable)
+    uint32_t *errors, *sym_errors;  // [net] (nullable)
+    const int *status;        // [net] (nullable)
+    int TR, maxh;             // set by the launcher
+};
+
+// Shape-general training (k_train_generic.cu): parameters trained in place in
+// the FusedPlan layout; scratch [net][scratch_per_net] (train_generic_scratch)
+template <class T>
+struct TrainGenParams {
+    NetGeom g;
+    int layout, n_nets, K, rows, epochs, batch;
+    const float *design32;    // T = float: as TrainParams::design32
+    const float *r0;          // T = float: [net][rows]
+    const double *design;     // T = double: as noma_dataset
+    const double *targets;
+    const double *w0;         // T = double: [net][dims[0]]
+    const uint16_t *perm;     // [net][epochs][rows]
+    T *plan;                  // [net][plan_total] in/out
+    double *trace;            // [net][epochs] nullable
+    const int *status;
+    T *scratch;
+    size_t scratch_per_net;
+    double lr, b1, b2, eps;
 };
 
 int lls_launch(const LlsParams &p, cudaStream_t st);
@@ -112,5 +157,21 @@ int train_f64_launch(TrainF64Params &p, cudaStream_t st);
 int detect_launch(DetectParams &p, cudaStream_t st);
 int detect_tc_launch(const DetectParams &p, cudaStream_t st);
 int synth_launch(SynthParams p, double *noise_power_scratch, cudaStream_t st);
+
+template <class T>
+int fwd_tile_launch(FwdParams<T> &p, cudaStream_t st);
+template <class T>
+int layer_forward_launch(const NetGeom &g, const T *plan, const T *X, long long ld, int rows, T *acts, bool naive,
+                         const T *y, T *out, T *dy, cudaStream_t st);
+size_t loss_grad_scratch(const NetGeom &g, int rows);
+int loss_grad_launch(const NetGeom &g, const double *plan, const double *X, int rows, const double *y, double *ws,
+                     double *loss, double *grad, cudaStream_t st);
+int adam_launch(int n, double *theta, const double *grad, double *m, double *v, double c1, double c2, double lr,
+                double b1, double b2, double eps, cudaStream_t st);
+size_t train_generic_scratch(const NetGeom &g, int batch);
+int theta_plan_launch(const NetGeom &g, int n_nets, double *theta, double *plan, const double *w0, int to_plan,
+                      cudaStream_t st);
+template <class T>
+int train_generic_launch(TrainGenParams<T> &p, cudaStream_t st);
 
 }  // namespace noma_dev

@@ -1,0 +1,4 @@
+// Stand-in for the reference header noma/rng.hpp when the reference tree is
+// absent: the whole API is declared in noma/detector.hpp.
+#pragma once
+#include "noma/detector.hpp"
