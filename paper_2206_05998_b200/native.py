@@ -27,7 +27,8 @@ EXPORTED = [
     "noma_detect", "noma_pipeline", "noma_synthesize", "noma_ctx_set_profiling",
     "noma_ctx_phase_ms", "noma_measure_fp32_tflops", "noma_host_alloc", "noma_host_free", "noma_init_params_state",
     "noma_lls_predict", "noma_train_f64", "noma_ctx_train_mode", "noma_ctx_detect_mode", "noma_synthesize_bundles",
-    "noma_ctx_pipeline_chunks",
+    "noma_ctx_pipeline_chunks", "noma_forward_f64", "noma_forward_f32", "noma_loss_and_grad", "noma_adam_step",
+    "noma_bench_forward_f64", "noma_synthesize_f64",
 ]
 PHASES = ("lls", "init", "shuffle", "train", "detect", "total")
 

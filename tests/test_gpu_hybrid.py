@@ -120,12 +120,16 @@ def test_repeat_bit_identical(A):
     assert np.array_equal(A.fused_forward_f32(net, x), A.fused_forward_f32(net, x))
 
 
-def test_wide_layer_is_reported_unsupported(A):
-    from paper_2206_05998_b200 import native as N
-
+def test_wide_layer_runs_the_shape_general_path(A, O):
+    """[8, 256] (test_fused.cpp:112-119): the single-pass kernel with an
+    adaptive tile height (detect mode 3) within the FP32 bar of the FP64
+    forward."""
     onet = random_net_fused([8, 256], 9)
-    with pytest.raises(N.UnsupportedError):
-        A.fused_forward_f32(_dev_net(A, onet), random_mat(10, 8, 10))
+    x = random_mat(513, 8, 10)
+    got = A.fused_forward_f32(_dev_net(A, onet), x)
+    assert A.context().detect_mode == 3
+    want = O.forward(onet, x)
+    assert np.abs(got - want).max() / max(1.0, np.abs(want).max()) < 1e-5
 
 
 # ------------------------------------------------------------- training
