@@ -481,6 +481,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--dry-run", action="store_true", help="launcher/partition check without a GPU")
+    ap.add_argument("--precision", type=int, default=32, choices=[32, 64],
+                    help="64: the reference's FP64 training (noma_pipeline_f64, bit-consistent mode)")
     args = ap.parse_args()
     cfg = dict(CONFIGS[args.config])
     if args.slots:
@@ -542,9 +544,11 @@ def main():
     tcfg = N.TrainCfg.of(EPOCHS, BATCH, LR)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
 
+    prec = args.precision
+
     def step():
         ctx.pipeline(dims, tcfg, S, K, M, NT, ND, px, py, dx, truth, init_d, shuf_d, status,
-                     w0=w0, plans=plans, codes=codes, bit_errors=errs, symbol_errors=sers)
+                     w0=w0, plans=plans, codes=codes, bit_errors=errs, symbol_errors=sers, precision=prec)
 
     peak_fp32 = ctx.measure_fp32_tflops(0)
     peak_tile = ctx.measure_fp32_tflops(2)
@@ -611,7 +615,7 @@ def main():
     def step_host():
         ctx.pipeline(dims, tcfg, S, K, M, NT, ND, h_px.view(np.float64), h_py.view(np.float64),
                      h_dx.view(np.float32), h_truth, h_init, h_shuf, h_status, codes=h_codes,
-                     bit_errors=h_errs, symbol_errors=h_sers)
+                     bit_errors=h_errs, symbol_errors=h_sers, precision=prec)
 
     step_host()
     e2e_ms = []
@@ -654,7 +658,8 @@ def main():
             "metric": "detected symbols/sec (per-slot train+detect)",
             "value": value, "unit": "symbols/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
-            "higher_is_better": True, "scaling": cfg["scaling"], "vs_baseline": None, "dtype": "f32",
+            "higher_is_better": True, "scaling": cfg["scaling"], "vs_baseline": None,
+            "dtype": "f32" if prec == 32 else "f64 (training), f32 (detection)",
             "data": "synthetic (device port of the reference channel simulator; seeds 1000+slot)",
             "config": {"workload": f"{args.config}: M={M} K={K} QPSK dims={dims} N_T={NT} N_D={ND} "
                                    f"{EPOCHS} epochs batch {BATCH} Adam lr {LR}, IQ symmetry on, "

@@ -293,6 +293,19 @@ NOMA_API int noma_adam_step(noma_ctx_t ctx, int n, double *theta, const double *
                             double corr1, double corr2, double lr, double beta1, double beta2, double eps,
                             int mem);
 
+/* noma_pipeline in the reference's FP64 arithmetic (bit-consistent mode):
+ * FP64 He-normal init from Rng(init_seeds[net]), FP64 training on the FP64
+ * pilots (train mode 300, or 201 for shapes beyond k_train_f64's on-chip
+ * layout), the trained parameters rounded to FP32 for detection.  Same
+ * arguments and outputs as noma_pipeline. */
+NOMA_API int noma_pipeline_f64(noma_ctx_t ctx, const noma_net_desc *desc, const noma_train_cfg *cfg,
+                               int S, int K, int M, int NT, int ND, const double *pilot_rx,
+                               const double *pilot_sym, const float *data_rx, const uint8_t *truth,
+                               const uint64_t *init_seeds, const uint64_t *shuffle_seeds,
+                               double *w0, double *gram_condition, float *plans, double *loss_trace,
+                               float *soft, uint8_t *codes, uint32_t *bit_errors,
+                               uint32_t *symbol_errors, int *status, int mem);
+
 /* Replaces synthesize(cfg, SeedBundle::from_master(seed)) (channel_sim.cpp:76-117)
  * on device for S slots with master seeds [S].  Outputs (nullable):
  * pilot_rx [S][NT][M] c64, pilot_sym [S][NT][K] c64, data_rx [S][ND][M] c32,

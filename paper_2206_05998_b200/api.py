@@ -275,8 +275,9 @@ class SlotBatch:
 
 
 def pipeline(dims, pilot_rx, pilot_sym, data_rx, truth_codes, init_seeds, shuffle_seeds,
-             epochs=50, batch_size=128, lr=0.005) -> SlotBatch:
-    """LLS -> init -> train -> detect for S slots x K users (one C-ABI call)."""
+             epochs=50, batch_size=128, lr=0.005, precision=32) -> SlotBatch:
+    """LLS -> init -> train -> detect for S slots x K users (one C-ABI call).
+    precision=64: the reference's FP64 training (noma_pipeline_f64)."""
     px = np.ascontiguousarray(pilot_rx, dtype=np.complex128)
     py = np.ascontiguousarray(pilot_sym, dtype=np.complex128)
     dx = np.ascontiguousarray(data_rx, dtype=np.complex64)
@@ -298,7 +299,8 @@ def pipeline(dims, pilot_rx, pilot_sym, data_rx, truth_codes, init_seeds, shuffl
                        out.status, w0=out.w0, cond=out.gram_condition, plans=out.plans,
                        trace=out.trace if epochs > 0 else None, soft=out.soft.view(np.float32),
                        codes=out.codes, bit_errors=out.bit_errors if truth_codes is not None else None,
-                       symbol_errors=out.symbol_errors if truth_codes is not None else None)
+                       symbol_errors=out.symbol_errors if truth_codes is not None else None,
+                       precision=precision)
     out.trace = out.trace[..., :epochs]
     return out
 

@@ -989,14 +989,19 @@ NOMA_API int noma_detect(noma_ctx_t c, const noma_net_desc *desc, int layout, in
     return s.finish();
 }
 
-NOMA_API int noma_pipeline(noma_ctx_t c, const noma_net_desc *desc, const noma_train_cfg *cfg,
-                           int S, int K, int M, int NT, int ND, const double *pilot_rx,
-                           const double *pilot_sym, const float *data_rx, const uint8_t *truth,
-                           const uint64_t *init_seeds, const uint64_t *shuffle_seeds, double *w0,
-                           double *gram_condition, float *plans, double *loss_trace, float *soft,
-                           uint8_t *codes, uint32_t *bit_errors, uint32_t *symbol_errors, int *status,
-                           int mem) {
+}  // extern "C"
+
+namespace {
+// precision 32: FP32 FFMA training (the product path); 64: the reference's
+// FP64 arithmetic end to end (FP64 He-normal init, k_train_f64 / generic FP64
+// training on the FP64 pilots), parameters rounded to FP32 for detection.
+int pipeline_impl(noma_ctx_t c, const noma_net_desc *desc, const noma_train_cfg *cfg, int S, int K, int M,
+                  int NT, int ND, const double *pilot_rx, const double *pilot_sym, const float *data_rx,
+                  const uint8_t *truth, const uint64_t *init_seeds, const uint64_t *shuffle_seeds, double *w0,
+                  double *gram_condition, float *plans, double *loss_trace, float *soft, uint8_t *codes,
+                  uint32_t *bit_errors, uint32_t *symbol_errors, int *status, int mem, int precision) {
     if (!c) return NOMA_ERR_ARGUMENT;
+    const bool f64 = precision == 64;
     int st;
     if ((st = check_cfg(c, cfg))) return st;
     NetGeom g;
@@ -1014,8 +1019,10 @@ NOMA_API int noma_pipeline(noma_ctx_t c, const noma_net_desc *desc, const noma_t
     // rows, plans) stays under NOMA_CHUNK_MB (default 4096): C5's 32768 slots
     // would need 72 GB of shuffles at once.  Results are identical to one
     // call per chunk (every slot is independent).
+    const int ptrain = trainable_count(g);
     const size_t per_slot = (size_t)NT * 2 * M * 4 * 3 + (size_t)K * n * 4 +
-                            (size_t)K * cfg->epochs * n * 2 + (size_t)K * (g.plan_total * 4 + 2 * M * 8);
+                            (size_t)K * cfg->epochs * n * 2 + (size_t)K * (g.plan_total * 4 + 2 * M * 8) +
+                            (f64 ? (size_t)K * 3 * ptrain * 8 : 0);
     size_t budget = (size_t)4096 << 20;
     if (const char *e = std::getenv("NOMA_CHUNK_MB")) budget = (size_t)std::atoll(e) << 20;
     const int chunk = (int)std::max<size_t>(1, std::min<size_t>((size_t)S, budget / std::max<size_t>(per_slot, 1)));
@@ -1046,6 +1053,8 @@ NOMA_API int noma_pipeline(noma_ctx_t c, const noma_net_desc *desc, const noma_t
     float *d32 = s.scratch<float>((size_t)chunk * NT * 2 * M);
     float *r0 = s.scratch<float>((size_t)chunk * K * n);
     uint16_t *perm = s.scratch<uint16_t>((size_t)chunk * K * cfg->epochs * n);
+    double *th64 = f64 ? s.scratch<double>((size_t)chunk * K * ptrain) : nullptr;
+    double *mom64 = f64 ? s.scratch<double>((size_t)chunk * K * 2 * ptrain) : nullptr;
     if (!s.ok) return s.finish();
 
     // host buffers: every chunk's inputs are queued on the copy stream up
@@ -1120,7 +1129,9 @@ NOMA_API int noma_pipeline(noma_ctx_t c, const noma_net_desc *desc, const noma_t
         cudaStreamWaitEvent(c->side2, c->fork, 0);
         s.forked = true;
         mark(c, ch, 2, c->side);
-        if (init_launch(g, (int)cn, iseed + an, nullptr, cdp, c->side)) return cuda_fail(c, "init");
+        if (f64 ? init_theta_launch(g, (int)cn, iseed + an, th64, ptrain, c->side)
+                : init_launch(g, (int)cn, iseed + an, nullptr, cdp, c->side))
+            return cuda_fail(c, "init");
         mark(c, ch, 3, c->side);
         cudaEventRecord(c->join, c->side);
         mark(c, ch, 8, c->side2);
@@ -1160,7 +1171,68 @@ NOMA_API int noma_pipeline(noma_ctx_t c, const noma_net_desc *desc, const noma_t
         if (set_w0_launch((int)cn, 2 * M, g.plan_total, cdw, cdp, c->stream)) return cuda_fail(c, "w0");
         mark(c, ch, 5);
         c->launches += 4;
-        if (cfg->epochs > 0) {
+        if (f64) {
+            // FP64 training on the FP64 pilots (WIDEN_COMPLEX layout) from the
+            // FP64 init, then the FP32 plan for detection
+            if (cfg->epochs > 0) {
+                TrainF64Params tq;
+                tq.g = g;
+                tq.layout = NOMA_LAYOUT_WIDEN_COMPLEX;
+                tq.n_nets = (int)cn;
+                tq.K = K;
+                tq.rows = n;
+                tq.width = 2 * M;
+                tq.epochs = cfg->epochs;
+                tq.batch = cfg->batch_size;
+                tq.design = cpx;
+                tq.targets = cpy;
+                tq.w0 = cdw;
+                tq.perm = perm;
+                tq.theta = th64;
+                tq.moments = mom64;
+                tq.trace = dt ? dt + an * cfg->epochs : nullptr;
+                tq.status = cdst;
+                tq.lr = cfg->lr;
+                tq.b1 = cfg->beta1;
+                tq.b2 = cfg->beta2;
+                tq.eps = cfg->eps;
+                st = force_generic_train() ? NOMA_ERR_UNSUPPORTED : train_f64_launch(tq, c->stream);
+                c->train_mode = 300;
+                if (st == NOMA_ERR_UNSUPPORTED) {
+                    TrainGenParams<double> gp;
+                    gp.g = g;
+                    gp.layout = NOMA_LAYOUT_WIDEN_COMPLEX;
+                    gp.n_nets = (int)cn;
+                    gp.K = K;
+                    gp.rows = n;
+                    gp.epochs = cfg->epochs;
+                    gp.batch = cfg->batch_size;
+                    gp.design32 = gp.r0 = nullptr;
+                    gp.design = cpx;
+                    gp.targets = cpy;
+                    gp.w0 = cdw;
+                    gp.perm = perm;
+                    gp.plan = s.scratch<double>(cn * g.plan_total);
+                    gp.trace = tq.trace;
+                    gp.status = cdst;
+                    gp.scratch_per_net = train_generic_scratch(g, cfg->batch_size);
+                    gp.scratch = s.scratch<double>(cn * gp.scratch_per_net);
+                    gp.lr = cfg->lr;
+                    gp.b1 = cfg->beta1;
+                    gp.b2 = cfg->beta2;
+                    gp.eps = cfg->eps;
+                    if (!s.ok) return s.finish();
+                    if (theta_plan_launch(g, (int)cn, th64, gp.plan, cdw, 1, c->stream)) return cuda_fail(c, "theta->plan");
+                    st = train_generic_launch<double>(gp, c->stream);
+                    if (!st && theta_plan_launch(g, (int)cn, th64, gp.plan, cdw, 0, c->stream))
+                        return cuda_fail(c, "plan->theta");
+                    c->train_mode = 201;
+                }
+                if (st) return st == NOMA_ERR_CUDA ? cuda_fail(c, "train f64") : fail(c, st, "train f64: unsupported shape");
+                c->launches += 1;
+            }
+            if (theta_plan32_launch(g, (int)cn, th64, cdp, cdw, c->stream)) return cuda_fail(c, "theta->plan32");
+        } else if (cfg->epochs > 0) {
             TrainParams tp;
             fill_train(tp, g, cfg);
             tp.layout = NOMA_LAYOUT_WIDEN_COMPLEX;
@@ -1257,6 +1329,33 @@ NOMA_API int noma_pipeline(noma_ctx_t c, const noma_net_desc *desc, const noma_t
     st = s.finish();
     if (st == NOMA_OK && host) st = cudaStreamSynchronize(c->stream) == cudaSuccess ? NOMA_OK : cuda_fail(c, "synchronize");
     return st;
+}
+}  // namespace
+
+extern "C" {
+
+NOMA_API int noma_pipeline(noma_ctx_t c, const noma_net_desc *desc, const noma_train_cfg *cfg,
+                           int S, int K, int M, int NT, int ND, const double *pilot_rx,
+                           const double *pilot_sym, const float *data_rx, const uint8_t *truth,
+                           const uint64_t *init_seeds, const uint64_t *shuffle_seeds, double *w0,
+                           double *gram_condition, float *plans, double *loss_trace, float *soft,
+                           uint8_t *codes, uint32_t *bit_errors, uint32_t *symbol_errors, int *status,
+                           int mem) {
+    return pipeline_impl(c, desc, cfg, S, K, M, NT, ND, pilot_rx, pilot_sym, data_rx, truth, init_seeds,
+                         shuffle_seeds, w0, gram_condition, plans, loss_trace, soft, codes, bit_errors,
+                         symbol_errors, status, mem, 32);
+}
+
+NOMA_API int noma_pipeline_f64(noma_ctx_t c, const noma_net_desc *desc, const noma_train_cfg *cfg,
+                               int S, int K, int M, int NT, int ND, const double *pilot_rx,
+                               const double *pilot_sym, const float *data_rx, const uint8_t *truth,
+                               const uint64_t *init_seeds, const uint64_t *shuffle_seeds, double *w0,
+                               double *gram_condition, float *plans, double *loss_trace, float *soft,
+                               uint8_t *codes, uint32_t *bit_errors, uint32_t *symbol_errors, int *status,
+                               int mem) {
+    return pipeline_impl(c, desc, cfg, S, K, M, NT, ND, pilot_rx, pilot_sym, data_rx, truth, init_seeds,
+                         shuffle_seeds, w0, gram_condition, plans, loss_trace, soft, codes, bit_errors,
+                         symbol_errors, status, mem, 64);
 }
 
 }  // extern "C"

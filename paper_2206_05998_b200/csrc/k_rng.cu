@@ -356,6 +356,18 @@ int init_launch(const NetGeom &g, int n_nets, const uint64_t *seeds, const doubl
     return cudaGetLastError() == cudaSuccess ? NOMA_OK : NOMA_ERR_CUDA;
 }
 
+int init_theta_launch(const NetGeom &g, int n_nets, const uint64_t *seeds, double *theta, int ptrain,
+                      cudaStream_t st) {
+    if (n_nets == 0) return NOMA_OK;
+    const uint64_t *jt = jump_table();
+    if (!jt) return NOMA_ERR_CUDA;
+    int total = 0;
+    for (int l = 1; l < g.nd; ++l) total += g.dims[l] * g.dims[l - 1];
+    if ((total + kJumpDraws / 2 - 1) / (kJumpDraws / 2) > kJumpLo * kJumpHi) return NOMA_ERR_UNSUPPORTED;
+    init_block_kernel<<<n_nets, kInitThreads, 0, st>>>(g, seeds, nullptr, nullptr, nullptr, theta, ptrain, jt);
+    return cudaGetLastError() == cudaSuccess ? NOMA_OK : NOMA_ERR_CUDA;
+}
+
 // Copies FP64 w0 [net][d0] into the plans' w0 slots.
 __global__ void set_w0_kernel(int n_nets, int d0, int plan_total, const double *w0,
                               float *plans) {

@@ -286,4 +286,42 @@ int theta_plan_launch(const NetGeom &g, int n_nets, double *theta, double *plan,
     return cudaGetLastError() == cudaSuccess ? NOMA_OK : NOMA_ERR_CUDA;
 }
 
+// FP64 theta (flat reference order) -> FP32 FusedPlan with w0 in its slot:
+// the detection parameters of an FP64-trained net
+__global__ void theta_plan32_kernel(NetGeom g, int n_nets, int ptrain, const double *theta, float *plan,
+                                    const double *w0) {
+    const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= (size_t)n_nets * ptrain + (size_t)n_nets * g.dims[0]) return;
+    if (i >= (size_t)n_nets * ptrain) {  // w0 slots
+        const size_t k = i - (size_t)n_nets * ptrain;
+        const int net = (int)(k / g.dims[0]), c = (int)(k - (size_t)net * g.dims[0]);
+        plan[(size_t)net * g.plan_total + c] = (float)w0[k];
+        return;
+    }
+    const int net = (int)(i / ptrain), t = (int)(i - (size_t)net * ptrain);
+    int o = 0, q = -1;
+    for (int l = 1; l < g.nd && q < 0; ++l) {
+        const int nw = g.dims[l] * g.dims[l - 1];
+        if (t < o + nw) {
+            const int j = (t - o) / g.dims[l - 1], c = (t - o) - j * g.dims[l - 1];
+            q = g.plan_w[l] + j * g.plan_pad[l - 1] + c;
+        } else if (t < o + nw + g.dims[l]) {
+            q = g.plan_b[l] + (t - o - nw);
+        }
+        o += nw + g.dims[l];
+    }
+    if (q < 0) q = g.plan_f + (t - o);
+    plan[(size_t)net * g.plan_total + q] = (float)theta[i];
+}
+
+int theta_plan32_launch(const NetGeom &g, int n_nets, const double *theta, float *plan, const double *w0,
+                        cudaStream_t st) {
+    const int ptrain = trainable_count(g);
+    const size_t n = (size_t)n_nets * (ptrain + g.dims[0]);
+    if (n == 0) return NOMA_OK;
+    cudaMemsetAsync(plan, 0, (size_t)n_nets * g.plan_total * sizeof(float), st);
+    theta_plan32_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(g, n_nets, ptrain, theta, plan, w0);
+    return cudaGetLastError() == cudaSuccess ? NOMA_OK : NOMA_ERR_CUDA;
+}
+
 }  // namespace noma_dev

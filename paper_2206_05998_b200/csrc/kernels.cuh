@@ -171,6 +171,10 @@ int adam_launch(int n, double *theta, const double *grad, double *m, double *v, 
 size_t train_generic_scratch(const NetGeom &g, int batch);
 int theta_plan_launch(const NetGeom &g, int n_nets, double *theta, double *plan, const double *w0, int to_plan,
                       cudaStream_t st);
+int theta_plan32_launch(const NetGeom &g, int n_nets, const double *theta, float *plan, const double *w0,
+                        cudaStream_t st);
+int init_theta_launch(const NetGeom &g, int n_nets, const uint64_t *seeds, double *theta, int ptrain,
+                      cudaStream_t st);
 template <class T>
 int train_generic_launch(TrainGenParams<T> &p, cudaStream_t st);
 

@@ -28,7 +28,7 @@ EXPORTED = [
     "noma_ctx_phase_ms", "noma_measure_fp32_tflops", "noma_host_alloc", "noma_host_free", "noma_init_params_state",
     "noma_lls_predict", "noma_train_f64", "noma_ctx_train_mode", "noma_ctx_detect_mode", "noma_synthesize_bundles",
     "noma_ctx_pipeline_chunks", "noma_forward_f64", "noma_forward_f32", "noma_loss_and_grad", "noma_adam_step",
-    "noma_bench_forward_f64", "noma_synthesize_f64",
+    "noma_bench_forward_f64", "noma_synthesize_f64", "noma_pipeline_f64",
 ]
 PHASES = ("lls", "init", "shuffle", "train", "detect", "total")
 
@@ -127,6 +127,7 @@ def load():
     L.noma_detect.argtypes = [vp, C.POINTER(NetDesc), ip, ip, ip, ip, vp, vp, vp, vp, vp, vp, vp, ip]
     L.noma_pipeline.argtypes = [vp, C.POINTER(NetDesc), C.POINTER(TrainCfg), ip, ip, ip, ip, ip,
                                 vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, ip]
+    L.noma_pipeline_f64.argtypes = L.noma_pipeline.argtypes
     L.noma_synthesize.argtypes = [vp, C.POINTER(Scenario), ip, vp, vp, vp, vp, vp, vp, vp, ip]
     L.noma_synthesize_bundles.argtypes = [vp, C.POINTER(Scenario), ip, vp, vp, vp, vp, vp, vp, vp, ip]
     L.noma_ctx_set_profiling.argtypes = [vp, ip]
@@ -332,10 +333,11 @@ class Context:
 
     def pipeline(self, dims, cfg: TrainCfg, S, K, M, NT, ND, pilot_rx, pilot_sym, data_rx, truth,
                  init_seeds, shuffle_seeds, status, w0=None, cond=None, plans=None, trace=None,
-                 soft=None, codes=None, bit_errors=None, symbol_errors=None):
+                 soft=None, codes=None, bit_errors=None, symbol_errors=None, precision=32):
         mem = _mem_of(pilot_rx, pilot_sym, data_rx, status)
         d = NetDesc.of(dims)
-        self._check(self.L.noma_pipeline(
+        fn = self.L.noma_pipeline_f64 if precision == 64 else self.L.noma_pipeline
+        self._check(fn(
             self.h, C.byref(d), C.byref(cfg), S, K, M, NT, ND, _ptr(pilot_rx), _ptr(pilot_sym),
             _ptr(data_rx), _ptr(truth), _ptr(init_seeds), _ptr(shuffle_seeds), _ptr(w0),
             _ptr(cond), _ptr(plans), _ptr(trace), _ptr(soft), _ptr(codes), _ptr(bit_errors),

@@ -130,3 +130,53 @@ def test_full_training_batch_kernel(A, O, tag):
     assert soft_dev < tol_soft, soft_dev
     assert wdev < tol_w, wdev
     assert trace_dev < tol_trace, trace_dev
+
+
+# FP64 mode (noma_pipeline_f64): the reference's arithmetic end to end on the
+# device.  The FP32-vs-FP64 drift above is a property of FP32 training (an
+# FP32 restatement on the CPU drifts as far, profiles/r02_precision_probe.txt);
+# in FP64 the device follows the oracle's trajectory, so the north star's
+# decision bar holds at every configuration, including C4 and C5.
+# config: (M, K, hidden, power step, slots)
+CONFIGS_F64 = {
+    "c1": (16, 6, [64], 3.0, 2),
+    "c2": (16, 6, [64, 64], 3.0, 2),
+    "c5": (32, 16, [64], 1.0, 2),
+    "c4": (64, 32, [64], 1.0, 1),
+}
+
+
+@pytest.mark.parametrize("tag", list(CONFIGS_F64))
+def test_full_training_fp64_mode(A, O, tag):
+    M, K, hidden, step, S = CONFIGS_F64[tag]
+    NT, ND, snr, gain, epochs = 685, 3840, 25.0, 0.05, 50
+    sc = O.Scenario(num_users=K, num_antennas=M, train_symbols=NT, data_symbols=ND,
+                    power_step_db=step, snr_db=snr, rx_nonlinearity_gain=gain)
+    seeds = [1000 + s for s in range(S)]
+    recs = [O.synthesize(sc, O.seed_bundle(s)) for s in seeds]
+    dims = [2 * M] + hidden
+    init, shuf = _seeds(O, seeds, K)
+    truth = np.stack([A.codes_of(r.data_symbols) for r in recs])
+    out = A.pipeline(dims, np.stack([r.train_rx for r in recs]), np.stack([r.train_symbols for r in recs]),
+                     np.stack([r.data_rx for r in recs]), truth, init, shuf, epochs=epochs, precision=64)
+    assert A.context().train_mode in (300, 201), A.context().train_mode
+    assert (out.status == 0).all()
+    ref = O.run_slots(sc, hidden, seeds, epochs=epochs, threads=16)
+    scale = np.maximum(1.0, np.max(np.abs(ref.soft), axis=-1, keepdims=True))
+    soft_dev = float(np.max(np.abs(out.soft - ref.soft) / scale))
+    wfro, welem = _weight_dev(dims, out.plans, ref.plans)
+    trace_dev = float(np.max(np.abs(out.trace - ref.trace) / np.abs(ref.trace)))
+    rcodes = A.codes_of(ref.soft)
+    flips_net = np.count_nonzero(out.codes != rcodes, axis=-1)
+    flips = int(flips_net.sum())
+    dber = np.abs(out.bit_errors.astype(np.int64) - ref.bit_errors)
+    record("full_training_fp64", config=tag, slots=S, soft_dev=soft_dev, weight_dev=float(np.max(wfro)),
+           weight_elem_max=float(np.max(welem)), trace_dev=trace_dev, flips=flips,
+           symbols=int(out.codes.size), dev_bit_errors=int(out.bit_errors.sum()),
+           ref_bit_errors=int(ref.bit_errors.sum()), train_mode=A.context().train_mode)
+    assert flips <= 1e-4 * out.codes.size, flips  # north star: >= 99.99 % identical
+    assert np.all(dber <= 2 * flips_net)
+    # FP64 trajectory; the plans hold it rounded to FP32, data samples are FP32
+    assert trace_dev < 1e-9, trace_dev
+    assert float(np.max(wfro)) < 1e-6
+    assert soft_dev < 1e-5, soft_dev
