@@ -1050,10 +1050,35 @@ int pipeline_impl(noma_ctx_t c, const noma_net_desc *desc, const noma_train_cfg 
     uint32_t *der = dev(bit_errors, nets);
     uint32_t *dse = dev(symbol_errors, nets);
     int *dst = dev(status, nets);
-    float *d32 = s.scratch<float>((size_t)chunk * NT * 2 * M);
-    float *r0 = s.scratch<float>((size_t)chunk * K * n);
-    uint16_t *perm = s.scratch<uint16_t>((size_t)chunk * K * cfg->epochs * n);
-    double *th64 = f64 ? s.scratch<double>((size_t)chunk * K * ptrain) : nullptr;
+    // chunk scratch, double-buffered by chunk parity when chunks overlap.
+    // NOMA_OVERLAP=1 issues the prologue of chunk ch+1 (LLS, init, shuffles)
+    // before chunk ch's training so it can run beside it.  Measured on B200
+    // (C5, 7 chunks): +0.5 % -- the LLS kernel's shared memory does not fit
+    // next to two training CTAs, so it waits for the training's tail and then
+    // slows the detection it overlaps; off by default.
+    const char *ov = std::getenv("NOMA_OVERLAP");
+    const bool overlap = nchunk > 1 && ov && ov[0] == '1';
+    const int nset = overlap ? 2 : 1;
+    float *d32s[2] = {nullptr, nullptr}, *r0s[2] = {nullptr, nullptr};
+    uint16_t *perms[2] = {nullptr, nullptr};
+    double *th64s[2] = {nullptr, nullptr}, *dws[2] = {dw, dw};
+    float *dps[2] = {dp, dp};
+    for (int b = 0; b < 2; ++b) {
+        const int src = b < nset ? b : 0;
+        if (b < nset) {
+            d32s[b] = s.scratch<float>((size_t)chunk * NT * 2 * M);
+            r0s[b] = s.scratch<float>((size_t)chunk * K * n);
+            perms[b] = s.scratch<uint16_t>((size_t)chunk * K * cfg->epochs * n);
+            th64s[b] = f64 ? s.scratch<double>((size_t)chunk * K * ptrain) : nullptr;
+            if (b > 0 && !w0) dws[b] = s.scratch<double>((size_t)chunk * K * 2 * M);
+            if (b > 0 && !plans) dps[b] = s.scratch<float>((size_t)chunk * K * g.plan_total);
+        } else {
+            d32s[b] = d32s[src];
+            r0s[b] = r0s[src];
+            perms[b] = perms[src];
+            th64s[b] = th64s[src];
+        }
+    }
     double *mom64 = f64 ? s.scratch<double>((size_t)chunk * K * 2 * ptrain) : nullptr;
     if (!s.ok) return s.finish();
 
@@ -1109,68 +1134,102 @@ int pipeline_impl(noma_ctx_t c, const noma_net_desc *desc, const noma_train_cfg 
 
     c->pev_used = c->profiling ? nchunk : 0;
     c->chunks_last = nchunk;
+    // Chunk prologue: LLS (Gram + Cholesky, Jacobi only near the rank
+    // threshold) on `side`; He-normal init, the per-epoch shuffles and the
+    // condition-number Jacobi launch on `side2`; w0 into the plans once LLS and
+    // init are done.  With NOMA_OVERLAP=1 it is issued for chunk ch+1 before
+    // chunk ch's training; the shuffle kernel is then one small CTA per SM,
+    // sized to fit next to two training CTAs.
+    std::vector<cudaEvent_t> ev_ready(nchunk), ev_perm(nchunk), ev_cond(nchunk);
     for (int ch = 0; ch < nchunk; ++ch) {
+        ev_ready[ch] = new_event();
+        ev_perm[ch] = new_event();
+        ev_cond[ch] = new_event();
+    }
+    const bool lclk = std::getenv("NOMA_PHASE_CLOCKS") != nullptr;
+    auto prologue = [&](int ch, cudaEvent_t after) -> int {
+        const int b = ch & 1;
+        const size_t a = (size_t)ch * chunk;
+        const int Sc = (int)std::min<size_t>(chunk, S - a);
+        const size_t an = a * K, cn = (size_t)Sc * K;
+        const double *cpx = px + a * px_n, *cpy = py + a * py_n;
+        double *cdw = w0 ? dw + an * 2 * M : dws[b];
+        double *cdc = dc ? dc + an : nullptr;
+        float *cdp = plans ? dp + an * g.plan_total : dps[b];
+        int *cdst = dst + an;
+        cudaStreamWaitEvent(c->side, after, 0);
+        cudaStreamWaitEvent(c->side2, after, 0);
+        if (host) {
+            cudaStreamWaitEvent(c->side, ev_pil[ch], 0);
+            cudaStreamWaitEvent(c->side2, ev_pil[ch], 0);
+        }
+        s.forked = true;
+        noma_dataset ds{NOMA_LAYOUT_WIDEN_COMPLEX, Sc, K, n, 2 * M, cpx, cpy};
+        mark(c, ch, 2, c->side2);
+        if (f64 ? init_theta_launch(g, (int)cn, iseed + an, th64s[b], ptrain, c->side2)
+                : init_launch(g, (int)cn, iseed + an, nullptr, cdp, c->side2))
+            return cuda_fail(c, "init");
+        mark(c, ch, 3, c->side2);
+        cudaEventRecord(c->join, c->side2);
+        mark(c, ch, 8, c->side2);
+        if (perm_launch((int)cn, cfg->epochs, n, sseed + an, perms[b], c->side2, overlap && ch > 0 ? 16 : 64))
+            return cuda_fail(c, "perm");
+        mark(c, ch, 4, c->side2);
+        cudaEventRecord(ev_perm[ch], c->side2);
+        mark(c, ch, 0, c->side);
+        LlsParams lp = lls_params(&ds, cpx, cpy, cdw, cdc, cdst, d32s[b], r0s[b]);
+        lp.mode = 1;
+        if (lclk) {
+            lp.clocks = s.scratch<long long>(8);
+            if (lp.clocks) cudaMemsetAsync(lp.clocks, 0, 8 * sizeof(long long), c->side);
+        }
+        int r = lls_launch(lp, c->side);
+        if (lclk && lp.clocks && !r) {
+            long long h[8];
+            cudaMemcpyAsync(h, lp.clocks, sizeof(h), cudaMemcpyDeviceToHost, c->side);
+            cudaStreamSynchronize(c->side);
+            std::fprintf(stderr, "NOMA_LLS_CLOCKS gram %lld frob %lld jacobi %lld solve %lld residual %lld sweeps %lld\n",
+                         h[0], h[1], h[2], h[3], h[4], h[5]);
+        }
+        if (r) return r == NOMA_ERR_CUDA ? cuda_fail(c, "lls") : fail(c, r, "lls: unsupported shape");
+        mark(c, ch, 1, c->side);
+        if (cdc) {  // condition numbers of the Cholesky-path slots, joined at the chunk's end
+            LlsParams lc = lls_params(&ds, cpx, cpy, nullptr, cdc, nullptr, nullptr, nullptr);
+            lc.mode = 2;
+            if (lls_launch(lc, c->side2)) return cuda_fail(c, "lls condition");
+        }
+        cudaEventRecord(ev_cond[ch], c->side2);
+        cudaStreamWaitEvent(c->side, c->join, 0);
+        if (set_w0_launch((int)cn, 2 * M, g.plan_total, cdw, cdp, c->side)) return cuda_fail(c, "w0");
+        cudaEventRecord(ev_ready[ch], c->side);
+        c->launches += 4;
+        return NOMA_OK;
+    };
+    cudaEventRecord(c->fork, c->stream);
+    if ((st = prologue(0, c->fork))) return st;
+    for (int ch = 0; ch < nchunk; ++ch) {
+        const int b = ch & 1;
         const size_t a = (size_t)ch * chunk;
         const int Sc = (int)std::min<size_t>(chunk, S - a);
         const size_t an = a * K, cn = (size_t)Sc * K;  // first net, nets of the chunk
         const double *cpx = px + a * px_n, *cpy = py + a * py_n;
-        double *cdw = w0 ? dw + an * 2 * M : dw;
+        double *cdw = w0 ? dw + an * 2 * M : dws[b];
         double *cdc = dc ? dc + an : nullptr;
-        float *cdp = plans ? dp + an * g.plan_total : dp;
+        float *cdp = plans ? dp + an * g.plan_total : dps[b];
         int *cdst = dst + an;
-        if (host) cudaStreamWaitEvent(c->stream, ev_pil[ch], 0);
-        noma_dataset ds{NOMA_LAYOUT_WIDEN_COMPLEX, Sc, K, n, 2 * M, cpx, cpy};
-        // fork: He-normal init and the per-epoch shuffles depend only on seeds,
-        // so they run on the side streams while the LLS kernel runs; join
-        // before w0 is copied into the plans and training starts.
-        mark(c, ch, 0);
-        cudaEventRecord(c->fork, c->stream);
-        cudaStreamWaitEvent(c->side, c->fork, 0);
-        cudaStreamWaitEvent(c->side2, c->fork, 0);
-        s.forked = true;
-        mark(c, ch, 2, c->side);
-        if (f64 ? init_theta_launch(g, (int)cn, iseed + an, th64, ptrain, c->side)
-                : init_launch(g, (int)cn, iseed + an, nullptr, cdp, c->side))
-            return cuda_fail(c, "init");
-        mark(c, ch, 3, c->side);
-        cudaEventRecord(c->join, c->side);
-        mark(c, ch, 8, c->side2);
-        if (perm_launch((int)cn, cfg->epochs, n, sseed + an, perm, c->side2)) return cuda_fail(c, "perm");
-        mark(c, ch, 4, c->side2);
-        cudaEventRecord(c->join2, c->side2);
-        // critical path: Gram + Cholesky solve (Jacobi only for slots whose
-        // Cholesky pivots fall near the rank threshold); the condition numbers
-        // of the other slots come from a Jacobi launch on side2 that overlaps
-        // training and joins before the outputs
-        LlsParams lp = lls_params(&ds, cpx, cpy, cdw, cdc, cdst, d32, r0);
-        lp.mode = 1;
-        const bool lclk = std::getenv("NOMA_PHASE_CLOCKS") != nullptr;
-        if (lclk) {
-            lp.clocks = s.scratch<long long>(8);
-            if (lp.clocks) cudaMemsetAsync(lp.clocks, 0, 8 * sizeof(long long), c->stream);
+        float *d32 = d32s[b], *r0 = r0s[b];
+        uint16_t *perm = perms[b];
+        double *th64 = th64s[b];
+        (void)cpx;
+        (void)cpy;
+        cudaStreamWaitEvent(c->stream, ev_ready[ch], 0);
+        cudaStreamWaitEvent(c->stream, ev_perm[ch], 0);
+        if (overlap && ch + 1 < nchunk) {  // chunk ch+1's prologue beside this training
+            cudaEvent_t go = new_event();
+            cudaEventRecord(go, c->stream);
+            if ((st = prologue(ch + 1, go))) return st;
         }
-        st = lls_launch(lp, c->stream);
-        if (lclk && lp.clocks && !st) {
-            long long h[8];
-            cudaMemcpyAsync(h, lp.clocks, sizeof(h), cudaMemcpyDeviceToHost, c->stream);
-            cudaStreamSynchronize(c->stream);
-            std::fprintf(stderr, "NOMA_LLS_CLOCKS gram %lld frob %lld jacobi %lld solve %lld residual %lld sweeps %lld\n",
-                         h[0], h[1], h[2], h[3], h[4], h[5]);
-        }
-        if (st) return st == NOMA_ERR_CUDA ? cuda_fail(c, "lls") : fail(c, st, "lls: unsupported shape");
-        const bool cond_side = cdc != nullptr;
-        if (cond_side) {
-            LlsParams lc = lls_params(&ds, cpx, cpy, nullptr, cdc, nullptr, nullptr, nullptr);
-            lc.mode = 2;
-            if (lls_launch(lc, c->side2)) return cuda_fail(c, "lls condition");
-            cudaEventRecord(c->join3, c->side2);
-        }
-        mark(c, ch, 1);
-        cudaStreamWaitEvent(c->stream, c->join, 0);
-        cudaStreamWaitEvent(c->stream, c->join2, 0);
-        if (set_w0_launch((int)cn, 2 * M, g.plan_total, cdw, cdp, c->stream)) return cuda_fail(c, "w0");
         mark(c, ch, 5);
-        c->launches += 4;
         if (f64) {
             // FP64 training on the FP64 pilots (WIDEN_COMPLEX layout) from the
             // FP64 init, then the FP32 plan for detection
@@ -1303,7 +1362,7 @@ int pipeline_impl(noma_ctx_t c, const noma_net_desc *desc, const noma_train_cfg 
             if (st) return st == NOMA_ERR_CUDA ? cuda_fail(c, "detect") : fail(c, st, "detect: unsupported network shape");
             c->launches += 1;
         }
-        if (cond_side) cudaStreamWaitEvent(c->stream, c->join3, 0);
+        cudaStreamWaitEvent(c->stream, ev_cond[ch], 0);
         mark(c, ch, 7);
         if (host) {  // this chunk's results back while the next chunk runs
             cudaEvent_t done = new_event();
@@ -1319,6 +1378,11 @@ int pipeline_impl(noma_ctx_t c, const noma_net_desc *desc, const noma_train_cfg 
             if (symbol_errors) d2h(symbol_errors + an, dse + an, cn * 4);
             d2h(status + an, cdst, cn * 4);
             if (!copy_ok) return cuda_fail(c, "pipeline: result download");
+        }
+        if (!overlap && ch + 1 < nchunk) {
+            cudaEvent_t go = new_event();
+            cudaEventRecord(go, c->stream);
+            if ((st = prologue(ch + 1, go))) return st;
         }
     }
     if (host) {  // the call returns after the last download

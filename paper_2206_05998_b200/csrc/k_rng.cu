@@ -203,24 +203,25 @@ __global__ void __launch_bounds__(32 * kPermWarps) perm_kernel(int n_nets, int e
 __global__ void perm_thread_kernel(int n_nets, int epochs, int n, const uint64_t *shuffle_seeds,
                                    uint16_t *perm) {
     extern __shared__ uint16_t sidx[];
-    const int job = blockIdx.x * blockDim.x + threadIdx.x;
-    if (job >= n_nets * epochs) return;
-    const int net = job / epochs, epoch = job % epochs;
     uint16_t *idx = sidx + (size_t)threadIdx.x * n;
-    for (int i = 0; i < n; ++i) idx[i] = (uint16_t)i;
-    Xoshiro r(substream_seed(shuffle_seeds[net], (uint64_t)epoch));
-    for (int i = n - 1; i > 0; --i) {
-        const int j = (int)r.below((uint64_t)i + 1);
-        const uint16_t t = idx[i];
-        idx[i] = idx[j];
-        idx[j] = t;
+    // grid-stride over jobs: the overlapped form runs one small CTA per SM
+    for (int job = blockIdx.x * blockDim.x + threadIdx.x; job < n_nets * epochs; job += gridDim.x * blockDim.x) {
+        const int net = job / epochs, epoch = job % epochs;
+        for (int i = 0; i < n; ++i) idx[i] = (uint16_t)i;
+        Xoshiro r(substream_seed(shuffle_seeds[net], (uint64_t)epoch));
+        for (int i = n - 1; i > 0; --i) {
+            const int j = (int)r.below((uint64_t)i + 1);
+            const uint16_t t = idx[i];
+            idx[i] = idx[j];
+            idx[j] = t;
+        }
+        uint16_t *out = perm + (size_t)job * n;
+        for (int i = 0; i < n; ++i) out[i] = idx[i];
     }
-    uint16_t *out = perm + (size_t)job * n;
-    for (int i = 0; i < n; ++i) out[i] = idx[i];
 }
 
 int perm_launch(int n_nets, int epochs, int n, const uint64_t *seeds, uint16_t *perm,
-                cudaStream_t st) {
+                cudaStream_t st, int max_tpb) {
     if (n > 65535) return NOMA_ERR_UNSUPPORTED;
     const int jobs = n_nets * epochs;
     if (jobs == 0 || n < 1) return NOMA_OK;
@@ -228,12 +229,16 @@ int perm_launch(int n_nets, int epochs, int n, const uint64_t *seeds, uint16_t *
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     if (jobs > 16 * sms) {  // many shuffles: thread per job
+        // max_tpb 16: 44 KB of index arrays at n = 1370, small enough to run
+        // beside two training CTAs per SM (pipeline prologue overlap)
         int tpb = (int)((160 * 1024) / (2 * (size_t)n));
-        tpb = tpb > 64 ? 64 : tpb;
+        tpb = tpb > max_tpb ? max_tpb : tpb;
         if (tpb < 1) return NOMA_ERR_UNSUPPORTED;
         const size_t smem = (size_t)tpb * n * sizeof(uint16_t);
         cudaFuncSetAttribute(perm_thread_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        perm_thread_kernel<<<(jobs + tpb - 1) / tpb, tpb, smem, st>>>(n_nets, epochs, n, seeds, perm);
+        // small form: one resident CTA per SM that never blocks a training CTA
+        const int grid = max_tpb < 64 ? sms : (jobs + tpb - 1) / tpb;
+        perm_thread_kernel<<<grid, tpb, smem, st>>>(n_nets, epochs, n, seeds, perm);
         return cudaGetLastError() == cudaSuccess ? NOMA_OK : NOMA_ERR_CUDA;
     }
     if ((n - 1 + kJumpDraws - 1) / kJumpDraws > kJumpLo * kJumpHi) return NOMA_ERR_UNSUPPORTED;

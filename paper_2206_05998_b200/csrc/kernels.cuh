@@ -140,7 +140,7 @@ struct TrainGenParams {
 
 int lls_launch(const LlsParams &p, cudaStream_t st);
 int perm_launch(int n_nets, int epochs, int n, const uint64_t *seeds, uint16_t *perm,
-                cudaStream_t st);
+                cudaStream_t st, int max_tpb = 64);
 int init_launch(const NetGeom &g, int n_nets, const uint64_t *seeds, const double *w0,
                 float *plans, cudaStream_t st);
 int set_w0_launch(int n_nets, int d0, int plan_total, const double *w0, float *plans,
