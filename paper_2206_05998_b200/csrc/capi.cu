@@ -585,8 +585,8 @@ NOMA_API int noma_ctx_phase_ms(noma_ctx_t c, double *ms6) {
     }
     {
         float ms = 0.f;
-        cudaEventElapsedTime(&ms, c->pev[0][0], c->pev[n - 1][7]);
-        ms6[5] = ms;  // whole call
+        cudaEventElapsedTime(&ms, c->pev[0][2], c->pev[n - 1][7]);
+        ms6[5] = ms;  // whole call: first chunk's init start (its prologue's first launch) to the end
     }
     return NOMA_OK;
 }
@@ -1134,10 +1134,10 @@ int pipeline_impl(noma_ctx_t c, const noma_net_desc *desc, const noma_train_cfg 
 
     c->pev_used = c->profiling ? nchunk : 0;
     c->chunks_last = nchunk;
-    // Chunk prologue: LLS (Gram + Cholesky, Jacobi only near the rank
-    // threshold) on `side`; He-normal init, the per-epoch shuffles and the
-    // condition-number Jacobi launch on `side2`; w0 into the plans once LLS and
-    // init are done.  With NOMA_OVERLAP=1 it is issued for chunk ch+1 before
+    // Chunk prologue: He-normal init, then LLS (Gram + Cholesky, Jacobi only
+    // near the rank threshold) and w0 into the plans on `side`; the per-epoch
+    // shuffles (the longest part) and the condition-number Jacobi launch on
+    // `side2`.  With NOMA_OVERLAP=1 it is issued for chunk ch+1 before
     // chunk ch's training; the shuffle kernel is then one small CTA per SM,
     // sized to fit next to two training CTAs.
     std::vector<cudaEvent_t> ev_ready(nchunk), ev_perm(nchunk), ev_cond(nchunk);
@@ -1165,12 +1165,11 @@ int pipeline_impl(noma_ctx_t c, const noma_net_desc *desc, const noma_train_cfg 
         }
         s.forked = true;
         noma_dataset ds{NOMA_LAYOUT_WIDEN_COMPLEX, Sc, K, n, 2 * M, cpx, cpy};
-        mark(c, ch, 2, c->side2);
-        if (f64 ? init_theta_launch(g, (int)cn, iseed + an, th64s[b], ptrain, c->side2)
-                : init_launch(g, (int)cn, iseed + an, nullptr, cdp, c->side2))
+        mark(c, ch, 2, c->side);
+        if (f64 ? init_theta_launch(g, (int)cn, iseed + an, th64s[b], ptrain, c->side)
+                : init_launch(g, (int)cn, iseed + an, nullptr, cdp, c->side))
             return cuda_fail(c, "init");
-        mark(c, ch, 3, c->side2);
-        cudaEventRecord(c->join, c->side2);
+        mark(c, ch, 3, c->side);
         mark(c, ch, 8, c->side2);
         if (perm_launch((int)cn, cfg->epochs, n, sseed + an, perms[b], c->side2, overlap && ch > 0 ? 16 : 64))
             return cuda_fail(c, "perm");
@@ -1199,7 +1198,6 @@ int pipeline_impl(noma_ctx_t c, const noma_net_desc *desc, const noma_train_cfg 
             if (lls_launch(lc, c->side2)) return cuda_fail(c, "lls condition");
         }
         cudaEventRecord(ev_cond[ch], c->side2);
-        cudaStreamWaitEvent(c->side, c->join, 0);
         if (set_w0_launch((int)cn, 2 * M, g.plan_total, cdw, cdp, c->side)) return cuda_fail(c, "w0");
         cudaEventRecord(ev_ready[ch], c->side);
         c->launches += 4;
