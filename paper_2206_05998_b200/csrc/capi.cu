@@ -1171,7 +1171,7 @@ int pipeline_impl(noma_ctx_t c, const noma_net_desc *desc, const noma_train_cfg 
             return cuda_fail(c, "init");
         mark(c, ch, 3, c->side);
         mark(c, ch, 8, c->side2);
-        if (perm_launch((int)cn, cfg->epochs, n, sseed + an, perms[b], c->side2, overlap && ch > 0 ? 16 : 64))
+        if (perm_launch((int)cn, cfg->epochs, n, sseed + an, perms[b], c->side2, overlap && ch > 0 ? 32 : 64))
             return cuda_fail(c, "perm");
         mark(c, ch, 4, c->side2);
         cudaEventRecord(ev_perm[ch], c->side2);

@@ -199,24 +199,50 @@ __global__ void __launch_bounds__(32 * kPermWarps) perm_kernel(int n_nets, int e
 
 // Throughput form: one thread per (net, epoch) with its own sequential
 // stream and index array -- the right shape when there are many more
-// shuffles than SMs x warps (the swap chains then fill the machine).
+// shuffles than SMs x warps (the swap chains then fill the machine).  The
+// finished arrays leave through the warp: for each of its 32 jobs the lanes
+// store consecutive 32-bit words, so every store instruction is one coalesced
+// line instead of 32 scattered 2-byte writes (the scattered form was L2
+// transaction bound: ~70 ms per C5 chunk).
 __global__ void perm_thread_kernel(int n_nets, int epochs, int n, const uint64_t *shuffle_seeds,
                                    uint16_t *perm) {
-    extern __shared__ uint16_t sidx[];
-    uint16_t *idx = sidx + (size_t)threadIdx.x * n;
-    // grid-stride over jobs: the overlapped form runs one small CTA per SM
-    for (int job = blockIdx.x * blockDim.x + threadIdx.x; job < n_nets * epochs; job += gridDim.x * blockDim.x) {
-        const int net = job / epochs, epoch = job % epochs;
-        for (int i = 0; i < n; ++i) idx[i] = (uint16_t)i;
-        Xoshiro r(substream_seed(shuffle_seeds[net], (uint64_t)epoch));
-        for (int i = n - 1; i > 0; --i) {
-            const int j = (int)r.below((uint64_t)i + 1);
-            const uint16_t t = idx[i];
-            idx[i] = idx[j];
-            idx[j] = t;
+    extern __shared__ __align__(16) uint16_t sidx[];
+    const int lane = threadIdx.x & 31;
+    const int np = (n + 1) & ~1;  // per-thread array stride: whole 32-bit words
+    uint16_t *idx = sidx + (size_t)threadIdx.x * np;
+    const int jobs = n_nets * epochs;
+    const int warps_total = gridDim.x * (blockDim.x >> 5);
+    for (int base = (blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * 32; base < jobs;
+         base += warps_total * 32) {
+        const int job = base + lane;
+        if (job < jobs) {
+            const int net = job / epochs, epoch = job % epochs;
+            for (int i = 0; i < n; ++i) idx[i] = (uint16_t)i;
+            Xoshiro r(substream_seed(shuffle_seeds[net], (uint64_t)epoch));
+            for (int i = n - 1; i > 0; --i) {
+                const int j = (int)r.below((uint64_t)i + 1);
+                const uint16_t t = idx[i];
+                idx[i] = idx[j];
+                idx[j] = t;
+            }
         }
-        uint16_t *out = perm + (size_t)job * n;
-        for (int i = 0; i < n; ++i) out[i] = idx[i];
+        __syncwarp();
+        const int nj = min(32, jobs - base);
+        const uint16_t *wbase = sidx + (size_t)(threadIdx.x & ~31) * np;
+        for (int t = 0; t < nj; ++t) {
+            const uint16_t *src = wbase + (size_t)t * np;
+            uint16_t *dst = perm + (size_t)(base + t) * n;
+            // dst is 4-byte aligned when (base + t) * n is even
+            if ((((size_t)(base + t) * n) & 1) == 0) {
+                const uint32_t *s32 = reinterpret_cast<const uint32_t *>(src);
+                uint32_t *d32 = reinterpret_cast<uint32_t *>(dst);
+                for (int w = lane; w < n / 2; w += 32) d32[w] = s32[w];
+                if ((n & 1) && lane == 0) dst[n - 1] = src[n - 1];
+            } else {
+                for (int i = lane; i < n; i += 32) dst[i] = src[i];
+            }
+        }
+        __syncwarp();
     }
 }
 
@@ -228,15 +254,15 @@ int perm_launch(int n_nets, int epochs, int n, const uint64_t *seeds, uint16_t *
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    if (jobs > 16 * sms) {  // many shuffles: thread per job
-        // max_tpb 16: 44 KB of index arrays at n = 1370, small enough to run
-        // beside two training CTAs per SM (pipeline prologue overlap)
-        int tpb = (int)((160 * 1024) / (2 * (size_t)n));
-        tpb = tpb > max_tpb ? max_tpb : tpb;
-        if (tpb < 1) return NOMA_ERR_UNSUPPORTED;
-        const size_t smem = (size_t)tpb * n * sizeof(uint16_t);
+    // many shuffles: thread per job, whole warps of index arrays in shared
+    // memory (max_tpb 32: one warp, 88 KB at n = 1370, one CTA per SM -- the
+    // form that can sit beside two training CTAs in the overlapped pipeline)
+    const int np = (n + 1) & ~1;
+    int tpb = (int)((200 * 1024) / (2 * (size_t)np));
+    tpb = (tpb > max_tpb ? max_tpb : tpb) & ~31;
+    if (jobs > 16 * sms && tpb >= 32) {
+        const size_t smem = (size_t)tpb * np * sizeof(uint16_t);
         cudaFuncSetAttribute(perm_thread_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        // small form: one resident CTA per SM that never blocks a training CTA
         const int grid = max_tpb < 64 ? sms : (jobs + tpb - 1) / tpb;
         perm_thread_kernel<<<grid, tpb, smem, st>>>(n_nets, epochs, n, seeds, perm);
         return cudaGetLastError() == cudaSuccess ? NOMA_OK : NOMA_ERR_CUDA;
