@@ -154,6 +154,7 @@ struct noma_ctx_s {
     int chunks_last = 0;  // slot chunks of the last pipeline call
     cudaStream_t side = nullptr;          // init overlaps the LLS
     cudaStream_t side2 = nullptr;         // shuffles overlap the LLS and the init
+    cudaStream_t side3 = nullptr;         // He-normal init beside the LLS and the shuffles
     cudaEvent_t fork = nullptr, join = nullptr, join2 = nullptr;
     cudaEvent_t ev_perm0 = nullptr;       // profiling: shuffle start on side2
     cudaEvent_t join3 = nullptr;          // LLS condition numbers (side2, joined at the end)
@@ -230,6 +231,8 @@ struct Stage {
         cudaEventRecord(c->join, c->side);
         cudaStreamWaitEvent(c->stream, c->join, 0);
         cudaEventRecord(c->join2, c->side2);
+        cudaStreamWaitEvent(c->stream, c->join2, 0);
+        cudaEventRecord(c->join2, c->side3);
         cudaStreamWaitEvent(c->stream, c->join2, 0);
         forked = false;
     }
@@ -491,6 +494,7 @@ NOMA_API int noma_ctx_create(int device, noma_ctx_t *out) {
     c->stream = c->own;
     if (cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking) != cudaSuccess ||
         cudaStreamCreateWithFlags(&c->side2, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaStreamCreateWithFlags(&c->side3, cudaStreamNonBlocking) != cudaSuccess ||
         cudaEventCreateWithFlags(&c->fork, cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&c->join, cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&c->join2, cudaEventDisableTiming) != cudaSuccess ||
@@ -520,6 +524,7 @@ NOMA_API int noma_ctx_destroy(noma_ctx_t c) {
     cudaStreamSynchronize(c->stream);
     if (c->side) cudaStreamSynchronize(c->side), cudaStreamDestroy(c->side);
     if (c->side2) cudaStreamSynchronize(c->side2), cudaStreamDestroy(c->side2);
+    if (c->side3) cudaStreamSynchronize(c->side3), cudaStreamDestroy(c->side3);
     if (c->join2) cudaEventDestroy(c->join2);
     if (c->join3) cudaEventDestroy(c->join3);
     if (c->copy) cudaStreamSynchronize(c->copy), cudaStreamDestroy(c->copy);
@@ -1134,10 +1139,10 @@ int pipeline_impl(noma_ctx_t c, const noma_net_desc *desc, const noma_train_cfg 
 
     c->pev_used = c->profiling ? nchunk : 0;
     c->chunks_last = nchunk;
-    // Chunk prologue: He-normal init, then LLS (Gram + Cholesky, Jacobi only
-    // near the rank threshold) and w0 into the plans on `side`; the per-epoch
-    // shuffles (the longest part) and the condition-number Jacobi launch on
-    // `side2`.  With NOMA_OVERLAP=1 it is issued for chunk ch+1 before
+    // Chunk prologue, three concurrent streams: LLS (Gram + Cholesky, Jacobi
+    // only near the rank threshold) on `side`, then w0 into the plans once the
+    // He-normal init (`side3`) is done; the per-epoch shuffles and the
+    // condition-number Jacobi launch on `side2`.  With NOMA_OVERLAP=1 it is issued for chunk ch+1 before
     // chunk ch's training; the shuffle kernel is then one small CTA per SM,
     // sized to fit next to two training CTAs.
     std::vector<cudaEvent_t> ev_ready(nchunk), ev_perm(nchunk), ev_cond(nchunk);
@@ -1157,19 +1162,18 @@ int pipeline_impl(noma_ctx_t c, const noma_net_desc *desc, const noma_train_cfg 
         double *cdc = dc ? dc + an : nullptr;
         float *cdp = plans ? dp + an * g.plan_total : dps[b];
         int *cdst = dst + an;
-        cudaStreamWaitEvent(c->side, after, 0);
-        cudaStreamWaitEvent(c->side2, after, 0);
-        if (host) {
-            cudaStreamWaitEvent(c->side, ev_pil[ch], 0);
-            cudaStreamWaitEvent(c->side2, ev_pil[ch], 0);
+        for (cudaStream_t q : {c->side, c->side2, c->side3}) {
+            cudaStreamWaitEvent(q, after, 0);
+            if (host) cudaStreamWaitEvent(q, ev_pil[ch], 0);
         }
         s.forked = true;
         noma_dataset ds{NOMA_LAYOUT_WIDEN_COMPLEX, Sc, K, n, 2 * M, cpx, cpy};
-        mark(c, ch, 2, c->side);
-        if (f64 ? init_theta_launch(g, (int)cn, iseed + an, th64s[b], ptrain, c->side)
-                : init_launch(g, (int)cn, iseed + an, nullptr, cdp, c->side))
+        mark(c, ch, 2, c->side3);
+        if (f64 ? init_theta_launch(g, (int)cn, iseed + an, th64s[b], ptrain, c->side3)
+                : init_launch(g, (int)cn, iseed + an, nullptr, cdp, c->side3))
             return cuda_fail(c, "init");
-        mark(c, ch, 3, c->side);
+        mark(c, ch, 3, c->side3);
+        cudaEventRecord(c->join, c->side3);
         mark(c, ch, 8, c->side2);
         if (perm_launch((int)cn, cfg->epochs, n, sseed + an, perms[b], c->side2, overlap && ch > 0 ? 32 : 64))
             return cuda_fail(c, "perm");
@@ -1198,6 +1202,7 @@ int pipeline_impl(noma_ctx_t c, const noma_net_desc *desc, const noma_train_cfg 
             if (lls_launch(lc, c->side2)) return cuda_fail(c, "lls condition");
         }
         cudaEventRecord(ev_cond[ch], c->side2);
+        cudaStreamWaitEvent(c->side, c->join, 0);  // the init is in the plans
         if (set_w0_launch((int)cn, 2 * M, g.plan_total, cdw, cdp, c->side)) return cuda_fail(c, "w0");
         cudaEventRecord(ev_ready[ch], c->side);
         c->launches += 4;

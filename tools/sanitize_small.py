@@ -50,4 +50,24 @@ if mode in ("all", "tcmulti"):  # detection CTAs spanning several nets (persiste
         api.context().detect(dims, N.LAYOUT_WIDEN, nd, K, rows, x.view(np.float32), plans, truth=truth,
                              codes=codes, bit_errors=errs)
         print("tcmulti", dims, api.context().detect_mode, errs)
+if mode in ("all", "w4"):  # the 4-warp throughput kernel (one hidden layer of 64, many nets)
+    sy8 = api.synthesize(6, 16, 100, 256, [5, 6, 7, 8, 9, 10, 11, 12], snr_db=15.0, rx_nonlinearity_gain=0.05)
+    i8, s8 = slot_user_seeds(np.arange(5, 13, dtype=np.uint64), 6)
+    os.environ["NOMA_LAT_CLUSTER"] = "1"
+    out = api.pipeline([32, 64], sy8.pilot_rx, sy8.pilot_sym, sy8.data_rx, sy8.data_codes, i8, s8, epochs=2)
+    print("w4", api.context().train_mode, api.context().detect_mode, out.bit_errors.ravel()[:6])
+    os.environ.pop("NOMA_LAT_CLUSTER")
+if mode in ("all", "generic"):  # shape-general training / detection, FP64 pipeline mode
+    out = api.pipeline([32, 160], sy.pilot_rx, sy.pilot_sym, sy.data_rx, sy.data_codes, init, shuf, epochs=2)
+    print("generic", api.context().train_mode, api.context().detect_mode, out.bit_errors.ravel())
+    out = api.pipeline([32, 64], sy.pilot_rx, sy.pilot_sym, sy.data_rx, sy.data_codes, init, shuf, epochs=2,
+                       precision=64)
+    print("f64", api.context().train_mode, api.context().detect_mode, out.bit_errors.ravel())
+if mode in ("all", "dense"):  # the C++ API's FP64 entry points (k_dense.cu)
+    import subprocess
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    for t in ("fused", "hybrid_nn"):
+        r = subprocess.run([os.path.join(root, "oracle", "_ref", "reftests", "test_" + t)], capture_output=True,
+                           text=True)
+        print("dense", t, r.returncode, r.stdout.strip().splitlines()[-1] if r.stdout else "")
 print("done")
