@@ -362,8 +362,13 @@ __global__ void __launch_bounds__(kThreads) lls_kernel(LlsParams p) {
     // V <- V U, two barriers per round.
     const int mm = m + (m & 1);
     const int npairs = mm / 2;
+    // round_rot alternates by a round counter that runs across sweeps: the
+    // last round of a sweep and the first of the next must not share a slot
+    // (an identity round skips the second barrier, so a fast thread's write
+    // for the next round could reach the slot a slow thread is still testing)
+    int gr = 0;
     for (int sweep = 0; sweep < 30; ++sweep) {
-        for (int r = 0; r < mm - 1; ++r) {
+        for (int r = 0; r < mm - 1; ++r, ++gr) {
             if (tid < npairs) {
                 const int i = tid;
                 const int pi = (i == 0) ? 0 : ((i - 1 + r) % (mm - 1)) + 1;
@@ -387,7 +392,7 @@ __global__ void __launch_bounds__(kThreads) lls_kernel(LlsParams p) {
                         c = rsqrt(fma(t, t, 1.0));
                         s = t * c;
                         any_rot[sweep & 1] = 1;
-                        round_rot[r & 1] = 1;
+                        round_rot[gr & 1] = 1;
                     }
                 }
                 pair_p[i] = pp;
@@ -400,9 +405,9 @@ __global__ void __launch_bounds__(kThreads) lls_kernel(LlsParams p) {
             __syncthreads();
             // every thread has passed the previous sweep's break test
             if (r == 0 && tid == 0) any_rot[(sweep + 1) & 1] = 0;
-            if (!round_rot[r & 1]) continue;  // no pair rotates: identity round
+            if (!round_rot[gr & 1]) continue;  // no pair rotates: identity round
             __syncthreads();
-            if (tid == 0) round_rot[r & 1] = 0;  // reset for round r + 2
+            if (tid == 0) round_rot[gr & 1] = 0;  // reset for round gr + 2
             // A block (row pair I, column pair J): rows get U^H, columns U
             for (int it = tid; it < npairs * npairs + npairs * m; it += kThreads) {
                 if (it < npairs * npairs) {
