@@ -152,12 +152,6 @@ __global__ void __launch_bounds__(kW4Threads, 2) train_w4_kernel(TrainParams p, 
         gather(v ? permn[tid] : 0, v);
         cp_async_wait_all();
     }
-    // the two CTAs of an SM start out of phase so one's non-GEMM phases
-    // (residual, Adam, gather) overlap the other's GEMMs
-    if (p.dephase > 0 && (blockIdx.x & 1)) {
-        const long long t0 = clock64();
-        while (clock64() - t0 < p.dephase) __nanosleep(256);
-    }
     __syncthreads();
 
     float lossacc = 0.f;
@@ -368,26 +362,22 @@ __global__ void __launch_bounds__(kW4Threads, 2) train_w4_kernel(TrainParams p, 
             if (nb > 0) gather(nidx, tid < nb);
 
             // ---- Adam (hybrid_nn.cpp:118-144), FP32 moments in registers -----
-            // packed FP32x2 on the neuron pair: same IEEE operations and order
-            // as the scalar form, half the issue slots
-            const f2_t b1_2 = f2_bcast(p.b1), omb1_2 = f2_bcast(p.omb1), b2_2 = f2_bcast(p.b2),
-                       omb2_2 = f2_bcast(p.omb2), lrc2 = f2_bcast(lrc), ic2_2 = f2_bcast(ic2);
 #pragma unroll
             for (int i = 0; i < 4; ++i) {
                 const int jp = 8 * warp + jq + 2 * i;
 #pragma unroll
                 for (int u = 0; u < NK; ++u) {
                     const int uu = rh * NK + u, c = 4 * l8 + 32 * (uu >> 2) + (uu & 3);
-                    f2_t *wp = reinterpret_cast<f2_t *>(W2 + jp * G::WS + 2 * c);
-                    const f2_t gg = f2_pack(gk[i][u].x, gk[i][u].y);
-                    const f2_t m = f2_fmac(b1_2, f2_pack(mw[i][u].x, mw[i][u].y), f2_mul(omb1_2, gg));
-                    const f2_t v = f2_fmac(b2_2, f2_pack(vw[i][u].x, vw[i][u].y), f2_mul(omb2_2, f2_mul(gg, gg)));
-                    const float2 mf = f2_unpack(m), vf = f2_unpack(v);
-                    mw[i][u] = mf;
-                    vw[i][u] = vf;
-                    const float2 num = f2_unpack(f2_mul(lrc2, m)), den = f2_unpack(f2_mul(v, ic2_2));
-                    const float2 th = f2_unpack(*wp);
-                    *wp = f2_pack(th.x - adam_step(num.x, den.x, p.eps), th.y - adam_step(num.y, den.y, p.eps));
+                    float2 *wp = reinterpret_cast<float2 *>(W2 + jp * G::WS + 2 * c);
+                    float2 th = *wp;
+                    const float2 gg = gk[i][u];
+                    mw[i][u].x = p.b1 * mw[i][u].x + p.omb1 * gg.x;
+                    mw[i][u].y = p.b1 * mw[i][u].y + p.omb1 * gg.y;
+                    vw[i][u].x = p.b2 * vw[i][u].x + p.omb2 * (gg.x * gg.x);
+                    vw[i][u].y = p.b2 * vw[i][u].y + p.omb2 * (gg.y * gg.y);
+                    th.x -= adam_step(lrc * mw[i][u].x, vw[i][u].x * ic2, p.eps);
+                    th.y -= adam_step(lrc * mw[i][u].y, vw[i][u].y * ic2, p.eps);
+                    *wp = th;
                 }
             }
             {  // biases (tid < 64) and final weights: fixed-order sum of the warps
@@ -451,7 +441,6 @@ bool train_w4_fits(const TrainParams &p) {
 
 int train_w4_launch(TrainParams &p, cudaStream_t st) {
     const int IN = p.g.dims[0];
-    if (const char *e = std::getenv("NOMA_W4_DEPHASE")) p.dephase = std::atoi(e);
     const float *wide = p.design32;
     float *tmp = nullptr;
     if (p.layout == NOMA_LAYOUT_WIDEN_COMPLEX) {

@@ -40,7 +40,6 @@ struct TrainParams {
     float *xprep, *r0prep;  // latency kernel: per-step minibatch tiles (scratch, nullable)
     const float *atab;      // [total steps][2] Adam constants lr / c1, 1 / c2 (nullable)
     size_t prep_floats;     // capacity of xprep (floats)
-    int dephase = 0;        // 4-warp kernel: odd CTAs start this many cycles late
 };
 
 struct TrainF64Params {

@@ -52,23 +52,6 @@ __device__ __forceinline__ void f2_fma(f2_t &d, f2_t a, f2_t b) {
     asm volatile("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(d) : "l"(a), "l"(b));
 }
 
-// packed elementwise forms the scheduler may reorder (Adam, epilogues)
-__device__ __forceinline__ f2_t f2_mul(f2_t a, f2_t b) {
-    f2_t r;
-    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
-    return r;
-}
-__device__ __forceinline__ f2_t f2_add(f2_t a, f2_t b) {
-    f2_t r;
-    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
-    return r;
-}
-__device__ __forceinline__ f2_t f2_fmac(f2_t a, f2_t b, f2_t c) {  // a * b + c
-    f2_t r;
-    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
-    return r;
-}
-
 template <int KK>
 __device__ __forceinline__ float f4c(const float4 &v) {
     return KK == 0 ? v.x : KK == 1 ? v.y : KK == 2 ? v.z : v.w;
