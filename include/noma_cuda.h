@@ -118,7 +118,8 @@ NOMA_API long long noma_ctx_kernel_launches(noma_ctx_t ctx);
  * 1 = one CTA per net (16 warps), 2 = two 8-warp CTAs per SM,
  * 10 + c = row-split cluster of c CTAs per net (DSMEM gradient reduce),
  * 100 + c = neuron-split latency cluster of c CTAs per net (k_train_lat.cu),
- * 3 = 4-warp one-hidden-layer kernel (k_train_w4.cu),
+ * 3 = 4-warp one-hidden-layer kernel (k_train_w4.cu: inputs 32 / 64),
+ * 4 = 8-warp one-hidden-layer kernel (k_train_w8.cu: 128-wide inputs, C4),
  * 200 = shape-general FP32 kernel (k_train_generic.cu: layers wider than 128,
  *       minibatches above 128 rows), 201 = its FP64 instance (noma_train_f64),
  * 300 = on-chip FP64 kernel (k_train_f64.cu), 0 = none yet.

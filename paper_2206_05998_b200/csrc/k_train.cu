@@ -611,6 +611,8 @@ int train_launch(TrainParams &p, cudaStream_t st) {
 int train_thr_launch(TrainParams &p, cudaStream_t st, size_t smem, int mom_smem, int need) {
     // one hidden layer of 64 (C1, C5): 4-warp CTAs, several nets per SM
     if (train_w4_fits(p)) return train_w4_launch(p, st);
+    // one hidden layer of 64 on a 128-wide input (C4): 8-warp CTAs
+    if (train_w8_fits(p)) return train_w8_launch(p, st);
     // row-split cluster: fewer nets than SMs -> a cluster of CS CTAs per net
     int sms = 148;
     {

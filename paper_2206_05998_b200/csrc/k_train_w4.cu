@@ -431,6 +431,13 @@ __global__ void widen_rows_kernel(const float *__restrict__ d32, float *__restri
     wide[(2 * t + 1) * width + c] = c < M ? row[M + c] : -row[c - M];
 }
 
+int widen_rows_launch(const float *d32, float *wide, size_t nrow_c, int width, cudaStream_t st) {
+    const size_t tot = nrow_c * width;
+    if (tot == 0) return NOMA_OK;
+    widen_rows_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(d32, wide, nrow_c, width);
+    return cudaGetLastError() == cudaSuccess ? NOMA_OK : NOMA_ERR_CUDA;
+}
+
 // 1 hidden layer of 64, input 32 or 64, minibatch <= 128: the 4-warp kernel.
 bool train_w4_fits(const TrainParams &p) {
     const NetGeom &g = p.g;

@@ -47,7 +47,8 @@ CONFIGS = {
     "c1": (16, 6, [64], 3.0, 16, 4, 3, 1e-4, (0.1, 0.3, 0.1)),
     # the bench default (C5) runs the 4-warp kernel
     "c5": (32, 16, [64], 1.0, 6, 3, 3, 2.5e-3, (0.16, 0.25, 0.35)),
-    "c4": (64, 32, [64], 1.0, 3, 2, 1, 2.7e-2, (0.37, 0.4, 1.0)),
+    # C4 (128-wide input) runs the 8-warp kernel
+    "c4": (64, 32, [64], 1.0, 3, 2, 4, 2.7e-2, (0.37, 0.4, 1.0)),
 }
 
 

@@ -168,6 +168,30 @@ def test_throughput_kernel_c2_shape(A, O, NT):
     assert soft_dev < 1e-4 and trace_dev < 1e-4
 
 
+@pytest.mark.parametrize("NT", [128, 150])
+def test_throughput_kernel_c4_shape(A, O, NT):
+    """The 8-warp kernel (k_train_w8.cu) at the C4 network shape ([128, 64],
+    3 slots x 32 users): K split across the warp halves, gradient tiles over
+    all 128 columns; NT = 150 (300 widened rows) ends every epoch on a ragged
+    44-row minibatch.  Short trainings against the FP64 oracle."""
+    sc = O.Scenario(num_users=32, num_antennas=64, train_symbols=NT, data_symbols=128,
+                    power_step_db=1.0, snr_db=20.0, rx_nonlinearity_gain=0.05)
+    S = 3
+    seeds = [4000 + s for s in range(S)]
+    recs = [O.synthesize(sc, O.seed_bundle(s)) for s in seeds]
+    ref = O.run_slots(sc, [64], seeds, epochs=3, threads=8)
+    init, shuf = _seeds(O, seeds, 32)
+    out = A.pipeline([128, 64], np.stack([r.train_rx for r in recs]),
+                     np.stack([r.train_symbols for r in recs]), np.stack([r.data_rx for r in recs]),
+                     np.stack([A.codes_of(r.data_symbols) for r in recs]), init, shuf, epochs=3)
+    assert A.context().train_mode == 4
+    assert (out.status == 0).all()
+    soft_dev = np.max(np.abs(out.soft - ref.soft)) / max(1.0, np.max(np.abs(ref.soft)))
+    trace_dev = float(np.max(np.abs(out.trace - ref.trace) / np.abs(ref.trace)))
+    record("throughput_c4_shape", config=f"NT={sc.train_symbols}", soft_dev=soft_dev, trace_dev=trace_dev)
+    assert soft_dev < 1e-4 and trace_dev < 1e-4
+
+
 @pytest.mark.parametrize("mode", ["1", "2", "4"])
 def test_train_modes_agree(A, O, mode, monkeypatch):
     """The one-CTA-per-net kernel (throughput mode) and the cluster kernels
