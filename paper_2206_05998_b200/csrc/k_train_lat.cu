@@ -143,6 +143,30 @@ __device__ __forceinline__ void reduce_scatter(float (&v)[N], int lane) {
     }
 }
 
+// reduce_scatter plus a full xor all-reduce of one more value x at the same
+// rounds: x costs no extra dependent shuffle rounds (the bias / final-weight
+// gradients ride along with the weight-gradient reduction).
+template <int N, int V, int LANES>
+__device__ __forceinline__ void reduce_scatter_x(float (&v)[N], float &x, int lane) {
+    if constexpr (LANES > 1) {
+        constexpr int O = LANES / 2;
+        x += __shfl_xor_sync(0xffffffffu, x, O);
+        if constexpr (V > 1) {
+            const bool h = lane & O;
+#pragma unroll
+            for (int i = 0; i < V / 2; ++i) {
+                const float snd = h ? v[i] : v[i + V / 2];
+                const float keep = h ? v[i + V / 2] : v[i];
+                v[i] = keep + __shfl_xor_sync(0xffffffffu, snd, O);
+            }
+            reduce_scatter_x<N, V / 2, O>(v, x, lane);
+        } else {
+            v[0] += __shfl_xor_sync(0xffffffffu, v[0], O);
+            reduce_scatter_x<N, 1, O>(v, x, lane);
+        }
+    }
+}
+
 constexpr int ilog2c(int v) { return v <= 1 ? 0 : 1 + ilog2c(v / 2); }
 
 // Compile-time loop B, B+S, ... (exclusive E): the body sees an
@@ -603,7 +627,38 @@ static_for<NL, 0, -1>([&](auto LC) {
                             const float2 h = f2_unpack(acc[j][q]);
                             gv[4 * j + q] = h.x + h.y;
                         }
-                    reduce_scatter<4 * JPB, 4 * JPB, 32>(gv, lane);
+                    // biases (and, top layer, final weights): with every warp
+                    // holding all JT neurons (JS == 1) warp w reduces extra w
+                    // inside its weight-gradient reduction, so no warp carries
+                    // a second reduction chain; otherwise the column-tile-0 / -1
+                    // warps reduce them afterwards
+                    constexpr int NX = (l == NL ? 2 : 1) * JT;
+                    constexpr bool XSPREAD = JS == 1 && TPW == 1 && NX <= NW;
+                    if constexpr (XSPREAD) {
+                        float ex = 0.f;  // register arrays: select, no dynamic index
+#pragma unroll
+                        for (int j = 0; j < JPB; ++j) {
+                            if (warp == j) {
+                                const float2 h = f2_unpack(sb[j]);
+                                ex = h.x + h.y;
+                            }
+                            if (top && warp == JT + j) {
+                                const float2 h = f2_unpack(sf[j]);
+                                ex = h.x + h.y;
+                            }
+                        }
+                        reduce_scatter_x<4 * JPB, 4 * JPB, 32>(gv, ex, lane);
+                        if (warp < NX && lane == 0) {
+                            const int off = warp < JT ? c.b[l] + warp : c.wf + warp - JT;
+                            const float m1 = p.b1 * mb[l] + p.omb1 * ex;
+                            const float m2 = p.b2 * vb[l] + p.omb2 * (ex * ex);
+                            mb[l] = m1;
+                            vb[l] = m2;
+                            sm[pn + off] = sm[po + off] - adam_step(lrc * m1, m2 * ic2, p.eps);
+                        }
+                    } else {
+                        reduce_scatter<4 * JPB, 4 * JPB, 32>(gv, lane);
+                    }
                     constexpr int GSH = 5 - ilog2c(4 * JPB);  // replicas: 2^GSH lanes per weight
                     const int gi = lane >> GSH;                // j * 4 + q within the group
                     if ((lane & ((1 << GSH) - 1)) == 0) {
@@ -617,7 +672,7 @@ static_for<NL, 0, -1>([&](auto LC) {
                     }
                     // biases on the column-tile-0 warps, final weights (top layer)
                     // on the column-tile-1 warps: the extra reductions are spread
-                    if (ct == 0 || (top && ct == 1)) {
+                    if (!XSPREAD && (ct == 0 || (top && ct == 1))) {
                         float bv[JPB];
 #pragma unroll
                         for (int j = 0; j < JPB; ++j) {
