@@ -197,6 +197,7 @@ struct LatCarve {
     int rsst;                                          // dA partial staging [H][kSR]
     int bars;                                          // mbarriers (8-byte aligned)
     int nbars, end;
+    int exp;                                           // A/B switches (NOMA_LAT_EXP), 0 = default
 };
 
 // Shapes the latency kernel handles (else the caller falls back): 1-2 hidden
@@ -216,6 +217,7 @@ __host__ __device__ inline bool lat_carve(const NetGeom &g, int cs, int width, i
     const int jt = H / cs;
     if (jt != 2 && jt != 4 && jt != 8) return false;
     if (N > 1 && (jt < 4 || H > 64)) return false;
+    c->exp = 0;
     c->cs = cs;
     c->jt = jt;
     c->N = N;
@@ -501,9 +503,13 @@ static_for<1, NL + 1, 1>([&](auto LC) {
                 float yq[CS];
 #pragma unroll
                 for (int q = 0; q < CS; ++q) yq[q] = ya[q * kBatchRows];
-                float yh = yq[0];
+                // fixed pairwise tree, identical on every CTA of the cluster
+                // (each computes the residual of all rows; C1 -10 us vs a chain)
 #pragma unroll
-                for (int q = 1; q < CS; ++q) yh += yq[q];
+                for (int w = 1; w < CS; w *= 2)
+#pragma unroll
+                    for (int q = 0; q + w < CS; q += 2 * w) yq[q] += yq[q + w];
+                const float yh = yq[0];
                 const float res = r < bsz ? yh - sm[c.r0b + buf * kBatchRows + r] : 0.0f;
                 sm[c.dy + r] = (2.0f / (float)bsz) * res;
                 loss_acc = fmaf(res, res, loss_acc);
@@ -826,6 +832,7 @@ int train_lat_launch(TrainParams &p, cudaStream_t st) {
         if (!want && p.n_nets * cs > sms) continue;
         LatCarve c;
         if (!lat_carve(p.g, cs, p.width, (int)total, &c)) continue;
+        if (const char *x = std::getenv("NOMA_LAT_EXP")) c.exp = std::atoi(x);
         const size_t smem = (size_t)c.end * sizeof(float);
         if (!prepped) {
             const unsigned jobs = (unsigned)(p.n_nets * total);
