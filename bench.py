@@ -676,7 +676,8 @@ def main():
                             "neuron-split cluster per net",
             "phase_ms": {k: statistics.mean(p[k] for p in phases) for k in phases[0]},
             "train_kernel_mode": train_mode,
-            "roofline": {"bound": "fp32", "kernel": "train_w4_kernel" if train_mode == 3 else "train_kernel",
+            "roofline": {"bound": "fp32", "kernel": {3: "train_w4_kernel", 4: "train_w8_kernel",
+                                                     301: "train_w8d_kernel"}.get(train_mode, "train_kernel"),
                          "achieved": achieved, "peak": peak_fp32, "unit": "TFLOP/s",
                          "frac": achieved / peak_fp32,
                          "peak_source": "measured in this run: constant-operand FFMA probe (issue-rate peak)",
@@ -700,6 +701,15 @@ def main():
             "bit_errors_last_e2e_step": bit_err_total,
             "symbol_errors_last_e2e_step": ser_total,
         }
+        if prec == 64:  # FP64 training: the DFMA rate is the roofline denominator
+            sms = torch.cuda.get_device_properties(dev).multi_processor_count
+            ghz = (clocks.get("sm_mhz") or 1965.0) / 1e3
+            fp64_peak = 63.3 * 2 * sms * ghz / 1e3  # DFMA/clk/SM measured, profiles/r02_microbench_dfma.txt
+            line["roofline"].update({"bound": "fp64", "peak": fp64_peak, "frac": achieved / fp64_peak,
+                                     "peak_source": "63.3 DFMA/clk/SM (tools/microbench/dfma_rate.cu, "
+                                                    "profiles/r02_microbench_dfma.txt) x SMs x the run's SM clock",
+                                     "register_tile_ceiling": None, "frac_of_register_tile_ceiling": None,
+                                     "register_tile_ceiling_source": None})
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()

@@ -122,7 +122,8 @@ NOMA_API long long noma_ctx_kernel_launches(noma_ctx_t ctx);
  * 4 = 8-warp one-hidden-layer kernel (k_train_w8.cu: 128-wide inputs, C4),
  * 200 = shape-general FP32 kernel (k_train_generic.cu: layers wider than 128,
  *       minibatches above 128 rows), 201 = its FP64 instance (noma_train_f64),
- * 300 = on-chip FP64 kernel (k_train_f64.cu), 0 = none yet.
+ * 300 = on-chip FP64 kernel (k_train_f64.cu), 301 = register-tiled FP64
+ *       kernel (k_train_w8d.cu: one hidden layer of 64, inputs 32 / 64), 0 = none yet.
  * NOMA_TRAIN_GENERIC=1 in the environment forces the shape-general kernel. */
 NOMA_API int noma_ctx_train_mode(noma_ctx_t ctx);
 /* Which detection kernel the last noma_detect / noma_pipeline call used:

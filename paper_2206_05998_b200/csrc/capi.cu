@@ -859,7 +859,7 @@ NOMA_API int noma_train_f64(noma_ctx_t c, const noma_dataset *ds, const noma_net
     tp.eps = cfg->eps;
     if (cfg->epochs > 0) {
         st = force_generic_train() ? NOMA_ERR_UNSUPPORTED : train_f64_launch(tp, c->stream);
-        c->train_mode = 300;
+        c->train_mode = tp.mode ? tp.mode : 300;
         if (st == NOMA_ERR_UNSUPPORTED) {  // shape-general FP64 kernel on the FusedPlan layout
             TrainGenParams<double> gp;
             gp.g = g;
@@ -1259,7 +1259,7 @@ int pipeline_impl(noma_ctx_t c, const noma_net_desc *desc, const noma_train_cfg 
                 tq.b2 = cfg->beta2;
                 tq.eps = cfg->eps;
                 st = force_generic_train() ? NOMA_ERR_UNSUPPORTED : train_f64_launch(tq, c->stream);
-                c->train_mode = 300;
+                c->train_mode = tq.mode ? tq.mode : 300;
                 if (st == NOMA_ERR_UNSUPPORTED) {
                     TrainGenParams<double> gp;
                     gp.g = g;

@@ -185,6 +185,13 @@ __global__ void __launch_bounds__(kT64) train_f64_kernel(TrainF64Params p) {
 int train_f64_launch(TrainF64Params &p, cudaStream_t st) {
     const NetGeom &g = p.g;
     if (p.batch < 1) return NOMA_ERR_CONFIG;
+    p.ptrain = trainable_count(g);
+    // one hidden layer of 64 on a 32 / 64-wide input: register-tiled DFMA kernel
+    if (train_w8d_fits(p)) {
+        p.mode = 301;
+        return train_w8d_launch(p, st);
+    }
+    p.mode = 300;
     int maxw = 0;
     for (int l = 0; l < g.nd; ++l) maxw = g.dims[l] > maxw ? g.dims[l] : maxw;
     p.maxw = maxw;

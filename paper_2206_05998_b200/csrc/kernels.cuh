@@ -55,6 +55,7 @@ struct TrainF64Params {
     const int *status;
     double lr, b1, b2, eps;
     int ptrain, maxw, chunk, act_total;
+    int mode = 0;           // out: 300 = k_train_f64, 301 = register-tiled k_train_w8d
 };
 
 struct DetectParams {
@@ -158,6 +159,8 @@ int train_w8_launch(TrainParams &p, cudaStream_t st);
 // widened FP32 design rows (2t = [Re|Im], 2t+1 = [Im|-Re]) for the cp.async gathers
 int widen_rows_launch(const float *d32, float *wide, size_t nrow_c, int width, cudaStream_t st);
 int train_f64_launch(TrainF64Params &p, cudaStream_t st);
+bool train_w8d_fits(const TrainF64Params &p);
+int train_w8d_launch(TrainF64Params &p, cudaStream_t st);
 int detect_launch(DetectParams &p, cudaStream_t st);
 int detect_tc_launch(const DetectParams &p, cudaStream_t st);
 int synth_launch(SynthParams p, double *noise_power_scratch, cudaStream_t st);

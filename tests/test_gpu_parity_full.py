@@ -160,7 +160,9 @@ def test_full_training_fp64_mode(A, O, tag):
     truth = np.stack([A.codes_of(r.data_symbols) for r in recs])
     out = A.pipeline(dims, np.stack([r.train_rx for r in recs]), np.stack([r.train_symbols for r in recs]),
                      np.stack([r.data_rx for r in recs]), truth, init, shuf, epochs=epochs, precision=64)
-    assert A.context().train_mode in (300, 201), A.context().train_mode
+    # C1 / C5: the register-tiled FP64 kernel (301); C2 / C4: k_train_f64 (300)
+    want = (301,) if hidden == [64] and M <= 32 else (300, 201)
+    assert A.context().train_mode in want, A.context().train_mode
     assert (out.status == 0).all()
     ref = O.run_slots(sc, hidden, seeds, epochs=epochs, threads=16)
     scale = np.maximum(1.0, np.max(np.abs(ref.soft), axis=-1, keepdims=True))
