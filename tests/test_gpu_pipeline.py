@@ -263,3 +263,24 @@ def test_pipeline_chunks_bit_identical(A, O, where, monkeypatch):
     for a, b in zip(one, many):
         assert np.array_equal(a, b)
     assert int(np.asarray(one[7]).sum()) > 0  # the low-SNR slots do make symbol errors
+    # chunk ch+1's prologue issued beside chunk ch's training (double-buffered
+    # scratch, NOMA_OVERLAP=1): the same bits
+    monkeypatch.setenv("NOMA_OVERLAP", "1")
+    over = run()
+    for a, b in zip(one, over):
+        assert np.array_equal(a, b)
+    if where == "device":  # no w0 / plans requested: per-chunk scratch, double-buffered
+        dev = torch.device("cuda", 0)
+        t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)  # noqa: E731
+        soft = torch.zeros((S, K, ND, 2), dtype=torch.float32, device=dev)
+        codes = torch.zeros((S, K, ND), dtype=torch.uint8, device=dev)
+        errs = torch.zeros((S, K), dtype=torch.int32, device=dev)
+        st = torch.zeros((S, K), dtype=torch.int32, device=dev)
+        A.context().pipeline(dims, cfg, S, K, M, NT, ND, t(sy.pilot_rx.view(np.float64)),
+                             t(sy.pilot_sym.view(np.float64)), t(sy.data_rx.view(np.float32)),
+                             t(sy.data_codes), t(init.view(np.int64)), t(shuf.view(np.int64)), st,
+                             soft=soft, codes=codes, bit_errors=errs)
+        torch.cuda.synchronize()
+        assert np.array_equal(soft.cpu().numpy(), one[4])
+        assert np.array_equal(codes.cpu().numpy(), one[5])
+        assert np.array_equal(errs.cpu().numpy(), one[6])
