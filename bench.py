@@ -676,7 +676,7 @@ def main():
                             "neuron-split cluster per net",
             "phase_ms": {k: statistics.mean(p[k] for p in phases) for k in phases[0]},
             "train_kernel_mode": train_mode,
-            "roofline": {"bound": "fp32", "kernel": {3: "train_w4_kernel", 4: "train_w8_kernel",
+            "roofline": {"bound": "fp32", "kernel": {3: "train_w4_kernel", 4: "train_w8_kernel", 5: "train_l2_kernel",
                                                      301: "train_w8d_kernel"}.get(train_mode, "train_kernel"),
                          "achieved": achieved, "peak": peak_fp32, "unit": "TFLOP/s",
                          "frac": achieved / peak_fp32,

@@ -16,7 +16,7 @@ BUILD = os.path.join(PKG, "_build")
 LIB = os.path.join(PKG, "libnoma_b200.so")
 INCLUDE = os.path.join(ROOT, "include")
 
-SOURCES = ["capi.cu", "k_lls.cu", "k_rng.cu", "k_train.cu", "k_train_w4.cu", "k_train_w8.cu", "k_train_w8d.cu", "k_train_lat.cu", "k_train_f64.cu", "k_train_generic.cu", "k_dense.cu", "k_detect.cu", "k_detect_tc.cu"]
+SOURCES = ["capi.cu", "k_lls.cu", "k_rng.cu", "k_train.cu", "k_train_w4.cu", "k_train_w8.cu", "k_train_w8d.cu", "k_train_l2.cu", "k_train_lat.cu", "k_train_f64.cu", "k_train_generic.cu", "k_dense.cu", "k_detect.cu", "k_detect_tc.cu"]
 NVCC_FLAGS = [
     "-O3", "-lineinfo", "-std=c++17",
     "-gencode", "arch=compute_100a,code=sm_100a",

@@ -613,6 +613,8 @@ int train_thr_launch(TrainParams &p, cudaStream_t st, size_t smem, int mom_smem,
     if (train_w4_fits(p)) return train_w4_launch(p, st);
     // one hidden layer of 64 on a 128-wide input (C4): 8-warp CTAs
     if (train_w8_fits(p)) return train_w8_launch(p, st);
+    // two hidden layers of 64 on a 32/64-wide input (C2): 8-warp CTAs
+    if (train_l2_fits(p)) return train_l2_launch(p, st);
     // row-split cluster: fewer nets than SMs -> a cluster of CS CTAs per net
     int sms = 148;
     {

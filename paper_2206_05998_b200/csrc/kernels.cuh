@@ -156,6 +156,8 @@ bool train_w4_fits(const TrainParams &p);
 int train_w4_launch(TrainParams &p, cudaStream_t st);
 bool train_w8_fits(const TrainParams &p);
 int train_w8_launch(TrainParams &p, cudaStream_t st);
+bool train_l2_fits(const TrainParams &p);
+int train_l2_launch(TrainParams &p, cudaStream_t st);
 // widened FP32 design rows (2t = [Re|Im], 2t+1 = [Im|-Re]) for the cp.async gathers
 int widen_rows_launch(const float *d32, float *wide, size_t nrow_c, int width, cudaStream_t st);
 int train_f64_launch(TrainF64Params &p, cudaStream_t st);

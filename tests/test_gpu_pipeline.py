@@ -142,14 +142,16 @@ def test_large_detect_self_consistent(A, O):
     assert np.max(np.abs(soft[sl] - ref)) / max(1.0, np.max(np.abs(ref))) < 1e-5
 
 
-@pytest.mark.parametrize("NT", [64, 100])
-def test_throughput_kernel_c2_shape(A, O, NT):
-    """The one-CTA-per-net kernel at the C2 network shape ([32, 64, 64], 78
-    nets): exercises the paths that only this shape takes -- idle warps
-    summing the first layer's bias gradient and staging the next minibatch by
-    cp.async into a dead activation region (NT = 64: one minibatch per epoch,
-    staging across epoch boundaries; NT = 100: a partial second minibatch) --
-    against the FP64 oracle for short trainings."""
+@pytest.mark.parametrize("NT,l2", [(64, "1"), (100, "1"), (64, "0"), (100, "0")])
+def test_throughput_kernel_c2_shape(A, O, NT, l2, monkeypatch):
+    """The C2 network shape ([32, 64, 64], 78 nets) on the two-hidden-layer
+    8-warp kernel (k_train_l2.cu, mode 5) and, with NOMA_TRAIN_L2=0, on the
+    general one-CTA-per-net kernel (mode 1: idle warps summing the first
+    layer's bias gradient, next minibatch staged into a dead activation
+    region).  NT = 64: one minibatch per epoch, staging across epoch
+    boundaries; NT = 100: a partial second minibatch.  Short trainings against
+    the FP64 oracle."""
+    monkeypatch.setenv("NOMA_TRAIN_L2", l2)
     sc = O.Scenario(num_users=6, num_antennas=16, train_symbols=NT, data_symbols=128,
                     power_step_db=3.0, snr_db=20.0, rx_nonlinearity_gain=0.05)
     S = 13  # 78 nets: the throughput kernel
@@ -160,11 +162,34 @@ def test_throughput_kernel_c2_shape(A, O, NT):
     out = A.pipeline([32, 64, 64], np.stack([r.train_rx for r in recs]),
                      np.stack([r.train_symbols for r in recs]), np.stack([r.data_rx for r in recs]),
                      np.stack([A.codes_of(r.data_symbols) for r in recs]), init, shuf, epochs=3)
-    assert A.context().train_mode == 1
+    assert A.context().train_mode == (5 if l2 == "1" else 1)
     assert (out.status == 0).all()
     soft_dev = np.max(np.abs(out.soft - ref.soft)) / max(1.0, np.max(np.abs(ref.soft)))
     trace_dev = float(np.max(np.abs(out.trace - ref.trace) / np.abs(ref.trace)))
-    record("throughput_c2_shape", config=f"NT={NT}", soft_dev=soft_dev, trace_dev=trace_dev)
+    record("throughput_c2_shape", config=f"NT={NT} l2={l2}", soft_dev=soft_dev, trace_dev=trace_dev)
+    assert soft_dev < 1e-4 and trace_dev < 1e-4
+
+
+@pytest.mark.parametrize("NT", [128, 75])
+def test_throughput_kernel_l2_wide_input(A, O, NT):
+    """The two-hidden-layer kernel at a 64-wide input ([64, 64, 64]: 32
+    antennas, 8 users x 10 slots); NT = 75 (150 widened rows) leaves a
+    22-row ragged minibatch at every epoch end."""
+    sc = O.Scenario(num_users=8, num_antennas=32, train_symbols=NT, data_symbols=128,
+                    power_step_db=2.0, snr_db=20.0, rx_nonlinearity_gain=0.05)
+    S = 10
+    seeds = [3500 + s for s in range(S)]
+    recs = [O.synthesize(sc, O.seed_bundle(s)) for s in seeds]
+    ref = O.run_slots(sc, [64, 64], seeds, epochs=3, threads=8)
+    init, shuf = _seeds(O, seeds, 8)
+    out = A.pipeline([64, 64, 64], np.stack([r.train_rx for r in recs]),
+                     np.stack([r.train_symbols for r in recs]), np.stack([r.data_rx for r in recs]),
+                     np.stack([A.codes_of(r.data_symbols) for r in recs]), init, shuf, epochs=3)
+    assert A.context().train_mode == 5
+    assert (out.status == 0).all()
+    soft_dev = np.max(np.abs(out.soft - ref.soft)) / max(1.0, np.max(np.abs(ref.soft)))
+    trace_dev = float(np.max(np.abs(out.trace - ref.trace) / np.abs(ref.trace)))
+    record("throughput_l2_wide", config=f"NT={NT}", soft_dev=soft_dev, trace_dev=trace_dev)
     assert soft_dev < 1e-4 and trace_dev < 1e-4
 
 
