@@ -423,6 +423,7 @@ static_for<1, NL + 1, 1>([&](auto LC) {
                             }
                         }
                     }
+                    if constexpr (NL == 1) { NOMA_TL(12) }
                     float v[FVV];
 #pragma unroll
                     for (int j = 0; j < JPF; ++j) {
@@ -433,6 +434,7 @@ static_for<1, NL + 1, 1>([&](auto LC) {
                         v[4 * j + 3] = b.y;
                     }
                     reduce_scatter<FVV, FVV, 8>(v, lane);
+                    if constexpr (NL == 1) { NOMA_TL(13) }
                     const float bj = sm[po + c.b[l] + fj];
 #pragma unroll
                     for (int i = 0; i < FV; ++i) v[i] = fmaxf(v[i] + bj, 0.f);
@@ -625,6 +627,7 @@ static_for<NL, 0, -1>([&](auto LC) {
                             ffma2(acc[j][q], zb, x[q].y);
                         }
                     }
+                    if constexpr (NL == 1) { NOMA_TL(10) }
                     float gv[4 * JPB];
 #pragma unroll
                     for (int j = 0; j < JPB; ++j)
@@ -654,6 +657,7 @@ static_for<NL, 0, -1>([&](auto LC) {
                             }
                         }
                         reduce_scatter_x<4 * JPB, 4 * JPB, 32>(gv, ex, lane);
+                        if constexpr (NL == 1) { NOMA_TL(11) }
                         if (warp < NX && lane == 0) {
                             const int off = warp < JT ? c.b[l] + warp : c.wf + warp - JT;
                             const float m1 = p.b1 * mb[l] + p.omb1 * ex;
@@ -727,6 +731,7 @@ static_for<NL, 0, -1>([&](auto LC) {
                 }
             });
             NOMA_LPHASE(5)
+            if constexpr (NL == 1) { NOMA_TL(14) }
             NOMA_TL(8)
             __syncthreads();
             NOMA_LPHASE(6)
