@@ -50,12 +50,17 @@ def build(verbose: bool = False, ptxas_info: bool = False) -> str:
     hdrs = _headers()
     objs = []
     jobs = []
+    # NOMA_BUILD_TRACE=1: the kernels with their cycle probes compiled in
+    # (-DNOMA_PROBES: NOMA_PHASE_CLOCKS / NOMA_PHASE_TRACE / NOMA_LLS_CLOCKS /
+    # NOMA_DETECT_CLK, tools/latency_probe.py); off in the product build
+    trace = os.environ.get("NOMA_BUILD_TRACE") == "1"
     for src in SOURCES:
         s = os.path.join(CSRC, src)
-        o = os.path.join(BUILD, src.replace(".cu", ".o"))
+        tr = trace
+        o = os.path.join(BUILD, src.replace(".cu", ".trace.o" if tr else ".o"))
         objs.append(o)
         if _stale(o, [s] + hdrs) or ptxas_info:
-            cmd = [cc, *NVCC_FLAGS, "-I", INCLUDE, "-I", CSRC, "-c", s, "-o", o]
+            cmd = [cc, *NVCC_FLAGS, *(["-DNOMA_PROBES"] if tr else []), "-I", INCLUDE, "-I", CSRC, "-c", s, "-o", o]
             if ptxas_info:
                 cmd += ["-Xptxas", "-v"]
             jobs.append(cmd)
@@ -69,11 +74,15 @@ def build(verbose: bool = False, ptxas_info: bool = False) -> str:
 
     with cf.ThreadPoolExecutor(max_workers=len(jobs) or 1) as ex:
         list(ex.map(run, jobs))
-    if _stale(LIB, objs):
+    stamp = os.path.join(BUILD, "link.txt")
+    linked = open(stamp).read() if os.path.exists(stamp) else ""
+    if _stale(LIB, objs) or linked != "\n".join(objs):
         cmd = [cc, "-shared", "-o", LIB, *objs, "-lcudart"]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError("link failed:\n" + r.stdout + r.stderr)
+        with open(stamp, "w") as f:
+            f.write("\n".join(objs))
     return LIB
 
 

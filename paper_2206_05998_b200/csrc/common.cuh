@@ -10,6 +10,15 @@ namespace noma_dev {
 
 constexpr int kThreads = 256;     // CTA size of the train / detect / LLS kernels
 constexpr int kBatchRows = 128;   // minibatch tile (NOMA_MAX_BATCH)
+// Cycle probes (NOMA_PHASE_CLOCKS, NOMA_PHASE_TRACE, NOMA_LLS_CLOCKS,
+// NOMA_DETECT_CLK) exist only in a build with -DNOMA_PROBES
+// (NOMA_BUILD_TRACE=1 python -m paper_2206_05998_b200.build): predicated off
+// they still cost the latency kernel ~8 % of a C1 slot (same-box A/B).
+#ifdef NOMA_PROBES
+#define NOMA_PROBE_ON(cond) (cond)
+#else
+#define NOMA_PROBE_ON(cond) false
+#endif
 constexpr int kSR = kBatchRows + 4;  // feature-major row stride: 132 == 4 (mod 32)
 constexpr int kFeatPad = 32;      // every feature dim padded to 32 on chip
 

@@ -257,7 +257,7 @@ __global__ void __launch_bounds__(WsRoles<W0, NL>::kThreads, 1) detect_ws_kernel
     // emit] per role (roles: loaders, epilogue 1, epilogue 2, then one per
     // issuing warp)
     const int role = (threadIdx.x >> 7) < 3 ? (int)(threadIdx.x >> 7) : 3 + (int)(threadIdx.x >> 5) - 12;
-    long long *ck = p.clocks && blockIdx.x == 0 && (threadIdx.x & (threadIdx.x < 384 ? 127 : 31)) == 0
+    long long *ck = NOMA_PROBE_ON(p.clocks && blockIdx.x == 0 && (threadIdx.x & (threadIdx.x < 384 ? 127 : 31)) == 0)
                         ? p.clocks + 6 * role
                         : nullptr;
     // accumulated in shared memory: a global += per tile would distort the stage

@@ -96,7 +96,7 @@ __global__ void __launch_bounds__(kThreads) lls_kernel(LlsParams p) {
         cp_async_commit();
     };
 
-    const bool clk = p.clocks && d == 0 && tid == 0;
+    const bool clk = NOMA_PROBE_ON(p.clocks && d == 0 && tid == 0);
     long long ck = clk ? clock64() : 0;
 #define NOMA_LLS_CLK(I)                      \
     if (clk) {                               \

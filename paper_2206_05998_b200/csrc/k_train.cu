@@ -89,7 +89,7 @@ __global__ void __launch_bounds__(NT, MINB) train_kernel(TrainParams p) {
     float *misc = sm + p.off_misc;  // [0] lr/corr1, [1] 1/corr2
     float *yp = sm + p.off_yp;      // [fp_N/32][128] final-layer partials
     // optional phase-cycle instrumentation (block 0, thread 0; NOMA_PHASE_CLOCKS)
-    const bool clk_on = p.clocks && blockIdx.x == 0 && threadIdx.x == 0;
+    const bool clk_on = NOMA_PROBE_ON(p.clocks && blockIdx.x == 0 && threadIdx.x == 0);
     long long clk_acc[6] = {0, 0, 0, 0, 0, 0}, clk_prev = clk_on ? clock64() : 0;
 #define NOMA_PHASE(I)                                \
     if (clk_on) {                                    \

@@ -286,8 +286,9 @@ __global__ void __launch_bounds__(NW * 32, 1) train_lat_kernel(TrainParams p, La
     // barrier, 2 yp send + gather, 3 yp wait, 4 residual + barrier, 5 backward
     // + Adam, 6 end-of-step barrier, 7 prologue / epilogue.  After a barrier a
     // volatile shared load blocks until the barrier has actually released.
-    const bool clk_on = p.clocks && blockIdx.x == 0 && tid == 0;
+    const bool clk_on = NOMA_PROBE_ON(p.clocks && blockIdx.x == 0 && tid == 0);
     long long clk_acc[8] = {0, 0, 0, 0, 0, 0, 0, 0}, clk_prev = clk_on ? clock64() : 0;
+#ifdef NOMA_PROBES
 #define NOMA_LPHASE(I)                                            \
     if (clk_on) {                                                 \
         (void)*reinterpret_cast<volatile float *>(sm + c.dy);     \
@@ -295,10 +296,17 @@ __global__ void __launch_bounds__(NW * 32, 1) train_lat_kernel(TrainParams p, La
         clk_acc[I] += now - clk_prev;                             \
         clk_prev = now;                                           \
     }
+#else
+#define NOMA_LPHASE(I)
+#endif
     // per-warp timeline of steps 100-103 (lane 0 of every warp of block 0)
     long long *tl = p.clocks && blockIdx.x == 0 && lane == 0 ? p.clocks + 8 + warp * 16 : nullptr;
+#ifdef NOMA_PROBES
 #define NOMA_TL(PT)                                                              \
     if (tl && s >= 100 && s < 104) tl[(s - 100) * 256 + (PT)] = clock64();
+#else
+#define NOMA_TL(PT)
+#endif
 
     for (int i = tid; i < c.bars; i += kLT) sm[i] = 0.0f;
     __syncthreads();
@@ -423,7 +431,6 @@ static_for<1, NL + 1, 1>([&](auto LC) {
                             }
                         }
                     }
-                    if constexpr (NL == 1) { NOMA_TL(12) }
                     float v[FVV];
 #pragma unroll
                     for (int j = 0; j < JPF; ++j) {
@@ -434,7 +441,6 @@ static_for<1, NL + 1, 1>([&](auto LC) {
                         v[4 * j + 3] = b.y;
                     }
                     reduce_scatter<FVV, FVV, 8>(v, lane);
-                    if constexpr (NL == 1) { NOMA_TL(13) }
                     const float bj = sm[po + c.b[l] + fj];
 #pragma unroll
                     for (int i = 0; i < FV; ++i) v[i] = fmaxf(v[i] + bj, 0.f);
@@ -627,7 +633,6 @@ static_for<NL, 0, -1>([&](auto LC) {
                             ffma2(acc[j][q], zb, x[q].y);
                         }
                     }
-                    if constexpr (NL == 1) { NOMA_TL(10) }
                     float gv[4 * JPB];
 #pragma unroll
                     for (int j = 0; j < JPB; ++j)
@@ -657,7 +662,6 @@ static_for<NL, 0, -1>([&](auto LC) {
                             }
                         }
                         reduce_scatter_x<4 * JPB, 4 * JPB, 32>(gv, ex, lane);
-                        if constexpr (NL == 1) { NOMA_TL(11) }
                         if (warp < NX && lane == 0) {
                             const int off = warp < JT ? c.b[l] + warp : c.wf + warp - JT;
                             const float m1 = p.b1 * mb[l] + p.omb1 * ex;
@@ -731,7 +735,6 @@ static_for<NL, 0, -1>([&](auto LC) {
                 }
             });
             NOMA_LPHASE(5)
-            if constexpr (NL == 1) { NOMA_TL(14) }
             NOMA_TL(8)
             __syncthreads();
             NOMA_LPHASE(6)
@@ -751,8 +754,15 @@ static_for<NL, 0, -1>([&](auto LC) {
         loss_acc = 0.0f;
     }
     NOMA_LPHASE(7)
+#ifdef NOMA_PROBES
     if (clk_on)
         for (int i = 0; i < 8; ++i) p.clocks[i] = clk_acc[i];
+#else
+    (void)clk_on;
+    (void)clk_acc;
+    (void)clk_prev;
+    (void)tl;
+#endif
 #undef NOMA_LPHASE
     // ---- own slice of the trained parameters back to the FusedPlan layout ----
     const int pf = (total & 1) * c.npar;  // copy written by the last step

@@ -106,7 +106,7 @@ __global__ void __launch_bounds__(kW4Threads, 2) train_w4_kernel(TrainParams p, 
     float *RED = sm + G::off_red;
     float *R0 = sm + G::off_r0;
     float *LS = sm + G::off_loss;
-    const bool clk_on = p.clocks && blockIdx.x == 0 && threadIdx.x == 0;
+    const bool clk_on = NOMA_PROBE_ON(p.clocks && blockIdx.x == 0 && threadIdx.x == 0);
     long long clk_acc[5] = {0, 0, 0, 0, 0}, clk_prev = clk_on ? clock64() : 0;
 #define NOMA_W4_PHASE(I)                             \
     if (clk_on) {                                    \

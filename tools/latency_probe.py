@@ -1,5 +1,6 @@
 """Single-slot (S=1) latency breakdown of the pipeline: per-phase device ms
-(CUDA events recorded by the C-ABI) and, with NOMA_PHASE_CLOCKS, the train
+(CUDA events recorded by the C-ABI) and, with NOMA_PHASE_CLOCKS in a
+NOMA_BUILD_TRACE=1 build (the cycle probes are compiled out otherwise), the train
 kernel's per-phase cycles for net 0, for each training-cluster shape.
 
   python tools/latency_probe.py [--configs c1,c2] [--clusters 1,2,4]

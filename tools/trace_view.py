@@ -4,10 +4,7 @@ import sys
 import numpy as np
 
 t = np.loadtxt(sys.argv[1]).reshape(4, 16, 16)
-import os
 names = ["start", "fwd", "bar1", "ysent", "gath", "ywait", "resid", "bar2", "bwd", "bar3", "f1done", "agwait", "rsissue", "wg2done", "rswait", "-"]
-if os.environ.get("NOMA_TRACE_C1"):  # one-hidden-layer kernel: finer forward / backward points
-    names[10:15] = ["bffma", "bred", "fffma", "fred", "adam"]
 for st in range(int(sys.argv[2]) if len(sys.argv) > 2 else 1):
     print("step", 100 + st, " ".join(f"{n:>6s}" for n in names))
     rel = t[st] - t[st, :, 0].min()
