@@ -1191,8 +1191,10 @@ int pipeline_impl(noma_ctx_t c, const noma_net_desc *desc, const noma_train_cfg 
             long long h[8];
             cudaMemcpyAsync(h, lp.clocks, sizeof(h), cudaMemcpyDeviceToHost, c->side);
             cudaStreamSynchronize(c->side);
-            std::fprintf(stderr, "NOMA_LLS_CLOCKS gram %lld frob %lld jacobi %lld solve %lld residual %lld sweeps %lld\n",
-                         h[0], h[1], h[2], h[3], h[4], h[5]);
+            std::fprintf(stderr,
+                         "NOMA_LLS_CLOCKS gram %lld frob %lld jacobi %lld solve %lld residual %lld sweeps %lld "
+                         "gram_wait %lld residual_wait %lld\n",
+                         h[0], h[1], h[2], h[3], h[4], h[5], h[6], h[7]);
         }
         if (r) return r == NOMA_ERR_CUDA ? cuda_fail(c, "lls") : fail(c, r, "lls: unsupported shape");
         mark(c, ch, 1, c->side);

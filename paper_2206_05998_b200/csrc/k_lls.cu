@@ -61,7 +61,7 @@ __global__ void __launch_bounds__(kThreads) lls_kernel(LlsParams p) {
     double *V = A + 2 * m * m;              // m*m complex eigenvectors
     double *D = V + 2 * m * m;              // m*K complex RHS X^H y, later the solutions c_k
     double *bufs = D + 2 * m * K;           // 2 x (CH rows of x | CH rows of y), complex
-    const int bstride = 2 * CH * m + 2 * CH * K;
+    const int bstride = 2 * CH * (m + 1) + 2 * CH * K;  // (+1: phase D's padded rows)
     double *rot = bufs + 2 * bstride;       // per pair: c, s, e_re, e_im
     double *lam = rot + 4 * (kLlsMaxM / 2 + 1);  // m eigenvalues
     double *red = lam + m;                  // 2 * kThreads reduction scratch
@@ -135,15 +135,17 @@ __global__ void __launch_bounds__(kThreads) lls_kernel(LlsParams p) {
 #pragma unroll
         for (int q = 0; q < 4; ++q) acc[e][q][0] = acc[e][q][1] = 0.0;
     }
+    long long wait_a = 0, wait_d = 0;  // probes: cycles thread 0 waits for staged rows
     issue(0, 0);
     for (int ch = 0; ch < nch; ++ch) {
-        if (ch + 1 < nch) {
-            issue(ch + 1, (ch + 1) & 1);
+        if (ch + 1 < nch) issue(ch + 1, (ch + 1) & 1);
+        const long long tw = clk ? clock64() : 0;
+        if (ch + 1 < nch)
             cp_async_wait<1>();
-        } else {
+        else
             cp_async_wait<0>();
-        }
         __syncthreads();
+        if (clk) wait_a += clock64() - tw;
         const int t0 = ch * CH, tn = min(CH, p.nrow_c - t0);
         const double *xs = bufs + (ch & 1) * bstride, *ys = xs + 2 * CH * m;
         if (p.design32) {  // FP32 copy of the design for the training kernels
@@ -271,84 +273,121 @@ __global__ void __launch_bounds__(kThreads) lls_kernel(LlsParams p) {
     // with the pseudo-inverse one to rounding.  The condition number is left
     // to a mode-2 launch (off the critical path).
     bool fast = false;
-    if (p.mode == 1 && 2 * m * m <= 2 * bstride) {
-        double *L = bufs;  // m x m complex, lower triangle used
+    const int ms = m + 1;  // padded row stride: column reads hit distinct banks
+    if (p.mode == 1 && 4 * m * ms + m <= 2 * bstride) {
+        // Right-looking, one barrier per pivot: step k reads column k of the
+        // working matrix W (final after step k-1), updates W's trailing
+        // lower triangle with the column scaled on the fly, and stores the
+        // scaled column in the factor F -- F and W are separate, so no
+        // thread writes what another reads within a step.
+        double *W = bufs;              // m x m complex, lower triangle
+        double *F = W + 2 * m * ms;    // the factor L (lower triangle)
+        double *ilv = F + 2 * m * ms;  // 1 / L[k][k]
         for (int i = tid; i < m * m; i += kThreads) {
-            L[2 * i] = A[2 * i];
-            L[2 * i + 1] = A[2 * i + 1];
+            W[2 * (i + i / m)] = A[2 * i];
+            W[2 * (i + i / m) + 1] = A[2 * i + 1];
         }
         if (tid == 0) chol_ok = 1;
         const double floor_piv = 1e-10 * sqrt(red[0]);
+        int msh = 0;  // trailing-block grid width 2^msh >= m - 1
+        while ((1 << msh) < m - 1) ++msh;
         __syncthreads();
         for (int k = 0; k < m; ++k) {
-            const double dkk = L[2 * (k * m + k)];
+            const double dkk = W[2 * (k * ms + k)];
             if (!(dkk > floor_piv)) {  // uniform: every thread read the same pivot
                 if (tid == 0) chol_ok = 0;
                 break;
             }
-            const double lkk = sqrt(dkk), il = 1.0 / lkk;
-            __syncthreads();
-            for (int i = k + 1 + tid; i < m; i += kThreads) {
-                L[2 * (i * m + k)] *= il;
-                L[2 * (i * m + k) + 1] *= il;
-            }
-            if (tid == 0) L[2 * (k * m + k)] = lkk;
-            __syncthreads();
-            const int nt = m - k - 1;  // trailing update C[i][j] -= L[i][k] conj(L[j][k])
-            for (int t = tid; t < nt * nt; t += kThreads) {
-                const int i = k + 1 + t / nt, j = k + 1 + t % nt;
+            // 1/sqrt by rsqrt + one Newton step (~1 ulp; an IEEE sqrt and
+            // divide per pivot were the serial chain of this phase)
+            double il = rsqrt(dkk);
+            il = il * fma(-0.5 * dkk, il * il, 1.5);
+            const double lkk = dkk * il;
+            const int nt = m - k - 1;  // W[i][j] -= L[i][k] conj(L[j][k]), k < j <= i
+            for (int t = tid; t < (nt << msh); t += kThreads) {
+                const int i = k + 1 + (t >> msh), j = k + 1 + (t & ((1 << msh) - 1));
                 if (j <= i) {
-                    const double ar = L[2 * (i * m + k)], ai = L[2 * (i * m + k) + 1];
-                    const double br = L[2 * (j * m + k)], bi = L[2 * (j * m + k) + 1];
-                    L[2 * (i * m + j)] -= ar * br + ai * bi;
-                    L[2 * (i * m + j) + 1] -= ai * br - ar * bi;
+                    const double ar = W[2 * (i * ms + k)] * il, ai = W[2 * (i * ms + k) + 1] * il;
+                    const double br = W[2 * (j * ms + k)] * il, bi = W[2 * (j * ms + k) + 1] * il;
+                    W[2 * (i * ms + j)] -= ar * br + ai * bi;
+                    W[2 * (i * ms + j) + 1] -= ai * br - ar * bi;
                 }
+            }
+            for (int i = k + 1 + tid; i < m; i += kThreads) {
+                F[2 * (i * ms + k)] = W[2 * (i * ms + k)] * il;
+                F[2 * (i * ms + k) + 1] = W[2 * (i * ms + k) + 1] * il;
+            }
+            if (tid == 0) {
+                F[2 * (k * ms + k)] = lkk;
+                ilv[k] = il;
             }
             __syncthreads();
         }
         __syncthreads();
         fast = chol_ok != 0;
         if (fast) {
-            for (int j = 0; j < m; ++j) {  // forward: L y = d
-                const double ij = 1.0 / L[2 * (j * m + j)];
-                for (int k = tid; k < K; k += kThreads) {
-                    D[2 * (j * K + k)] *= ij;
-                    D[2 * (j * K + k) + 1] *= ij;
+            // L y = d, then L^H c = y: one warp per user, lane a holds rows
+            // a and a + 32 of the right-hand side in registers; each step
+            // broadcasts the finished entry by shuffle (no block barriers)
+            for (int k = warp; k < K; k += kThreads / 32) {
+                double yr[2], yi[2];
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const int a = lane + 32 * h;
+                    yr[h] = a < m ? D[2 * (a * K + k)] : 0.0;
+                    yi[h] = a < m ? D[2 * (a * K + k) + 1] : 0.0;
                 }
-                __syncthreads();
-                for (int t = tid; t < (m - j - 1) * K; t += kThreads) {
-                    const int i = j + 1 + t / K, k = t % K;
-                    const double lr = L[2 * (i * m + j)], li = L[2 * (i * m + j) + 1];
-                    const double yr = D[2 * (j * K + k)], yi = D[2 * (j * K + k) + 1];
-                    D[2 * (i * K + k)] -= lr * yr - li * yi;
-                    D[2 * (i * K + k) + 1] -= lr * yi + li * yr;
+                for (int j = 0; j < m; ++j) {  // forward
+                    const int hj = j >> 5;
+                    double cr = __shfl_sync(0xffffffffu, hj ? yr[1] : yr[0], j & 31);
+                    double ci = __shfl_sync(0xffffffffu, hj ? yi[1] : yi[0], j & 31);
+                    cr *= ilv[j];
+                    ci *= ilv[j];
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        const int i = lane + 32 * h;
+                        if (i == j) {
+                            yr[h] = cr;
+                            yi[h] = ci;
+                        } else if (i > j && i < m) {
+                            const double lr = F[2 * (i * ms + j)], li = F[2 * (i * ms + j) + 1];
+                            yr[h] -= lr * cr - li * ci;
+                            yi[h] -= lr * ci + li * cr;
+                        }
+                    }
                 }
-                __syncthreads();
-            }
-            for (int j = m - 1; j >= 0; --j) {  // backward: L^H c = y
-                const double ij = 1.0 / L[2 * (j * m + j)];
-                for (int k = tid; k < K; k += kThreads) {
-                    D[2 * (j * K + k)] *= ij;
-                    D[2 * (j * K + k) + 1] *= ij;
+                for (int j = m - 1; j >= 0; --j) {  // backward: c_i -= conj(L[j][i]) c_j
+                    const int hj = j >> 5;
+                    double cr = __shfl_sync(0xffffffffu, hj ? yr[1] : yr[0], j & 31);
+                    double ci = __shfl_sync(0xffffffffu, hj ? yi[1] : yi[0], j & 31);
+                    cr *= ilv[j];
+                    ci *= ilv[j];
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        const int i = lane + 32 * h;
+                        if (i == j) {
+                            yr[h] = cr;
+                            yi[h] = ci;
+                        } else if (i < j) {
+                            const double lr = F[2 * (j * ms + i)], li = -F[2 * (j * ms + i) + 1];
+                            yr[h] -= lr * cr - li * ci;
+                            yi[h] -= lr * ci + li * cr;
+                        }
+                    }
                 }
-                __syncthreads();
-                for (int t = tid; t < j * K; t += kThreads) {
-                    const int i = t / K, k = t % K;  // c_i -= conj(L[j][i]) c_j
-                    const double lr = L[2 * (j * m + i)], li = -L[2 * (j * m + i) + 1];
-                    const double cr = D[2 * (j * K + k)], ci = D[2 * (j * K + k) + 1];
-                    D[2 * (i * K + k)] -= lr * cr - li * ci;
-                    D[2 * (i * K + k) + 1] -= lr * ci + li * cr;
-                }
-                __syncthreads();
-            }
-            for (int it = tid; it < m * K; it += kThreads) {  // w0, as phase C
-                const int a = it / K, k = it % K;
-                double *w = p.w0 + ((size_t)d * K + k) * p.width;
-                if (cplx_layout) {
-                    w[a] = D[2 * it];
-                    w[m + a] = -D[2 * it + 1];
-                } else {
-                    w[a] = D[2 * it];
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {  // w0, as phase C
+                    const int a = lane + 32 * h;
+                    if (a >= m) continue;
+                    D[2 * (a * K + k)] = yr[h];
+                    D[2 * (a * K + k) + 1] = yi[h];
+                    double *w = p.w0 + ((size_t)d * K + k) * p.width;
+                    if (cplx_layout) {
+                        w[a] = yr[h];
+                        w[m + a] = -yi[h];
+                    } else {
+                        w[a] = yr[h];
+                    }
                 }
             }
             __syncthreads();
@@ -546,108 +585,180 @@ __global__ void __launch_bounds__(kThreads) lls_kernel(LlsParams p) {
     }  // !fast
     NOMA_LLS_CLK(3)
 
-    // ---- phase D: residuals r0 = y - X w0 (FP64) and norms: thread per row
-    // (rows read once from global / L2), users in groups of 8; per-user sums
-    // in fixed order (warp tree, then warps in order).
-    double *sums = red;  // [8 warps][8 users][2]
-    for (int k0 = 0; k0 < K; k0 += 8) {
-        const int kn = min(8, K - k0);
-        double rr[8], yy[8];
-#pragma unroll
-        for (int k = 0; k < 8; ++k) rr[k] = yy[k] = 0.0;
-        for (int t = tid; t < p.nrow_c; t += kThreads) {
-            double pe[8], po[8];
-#pragma unroll
-            for (int k = 0; k < 8; ++k) pe[k] = po[k] = 0.0;
-            // the row's samples are loaded four at a time, all in flight
-            // before the FMAs (one dependent L2 load per column made this
-            // phase latency-bound); the sums keep the column order
-            for (int a0 = 0; a0 < m; a0 += 4) {
-                double2 xv[4];
-#pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    const int a = a0 + u;
-                    xv[u] = a >= m ? make_double2(0.0, 0.0)
-                            : cplx_layout
-                                ? *reinterpret_cast<const double2 *>(p.design + (((size_t)d * p.nrow_c + t) * m + a) * 2)
-                                : make_double2(p.design[((size_t)d * p.nrow_c + t) * m + a], 0.0);
+    // ---- phase D: residuals r0 = y - X w0 (FP64) and their norms (status of
+    // rank-deficient designs, lls.cpp:43-49)
+    auto decide = [&](int k, double sr, double sy) {
+        const double res = sqrt(sr), ynorm = sqrt(sy);
+        const size_t net = (size_t)d * K + k;
+        int st = NOMA_OK;
+        double cond;
+        if (rank == m) {
+            cond = lmax / lmin;
+        } else if (rank > 0 && res <= 1e-8 * sqrt(lmax) * fmax(1.0, ynorm)) {
+            cond = lmax / lkeep;
+        } else {
+            st = NOMA_ERR_ILL_CONDITIONED;
+            cond = lmin > 0.0 ? lmax / lmin : INFINITY;
+        }
+        if (p.cond && !fast) p.cond[net] = cond;
+        if (p.status) p.status[net] = st;
+    };
+    if (cplx_layout) {
+        // Rows staged by cp.async in chunks again (row stride m + 1 complex,
+        // so a warp reading one column of 32 rows hits distinct banks);
+        // TPU threads per user, each a row of the chunk at a time; per-user
+        // sums over the threads in fixed order.
+        const int TPU = kThreads / K, uk = tid / TPU, slot = tid - uk * TPU;
+        const bool act = uk < K;
+        const int ms1 = m + 1;
+        auto issue_pad = [&](int ch, int b) {
+            const int t0 = ch * CH, tn = min(CH, p.nrow_c - t0);
+            double *xb = bufs + b * bstride, *yb = xb + 2 * CH * ms1;
+            const double *xs = p.design + ((size_t)d * p.nrow_c + t0) * m * 2;
+            const double *ys = p.targets + ((size_t)d * p.nrow_c + t0) * K * 2;
+            for (int i = tid; i < tn * m; i += kThreads) cp_async16(xb + 2 * (i + i / m), xs + 2 * i);
+            for (int i = tid; i < tn * K; i += kThreads) cp_async16(yb + 2 * i, ys + 2 * i);
+            cp_async_commit();
+        };
+        __syncthreads();  // the factor / eigenvectors in bufs are dead
+        double rr = 0.0, yy = 0.0;
+        issue_pad(0, 0);
+        for (int ch = 0; ch < nch; ++ch) {
+            if (ch + 1 < nch) issue_pad(ch + 1, (ch + 1) & 1);
+            const long long tw = clk ? clock64() : 0;
+            if (ch + 1 < nch)
+                cp_async_wait<1>();
+            else
+                cp_async_wait<0>();
+            __syncthreads();
+            if (clk) wait_d += clock64() - tw;
+            const int t0 = ch * CH, tn = min(CH, p.nrow_c - t0);
+            const double *xs = bufs + (ch & 1) * bstride, *ys = xs + 2 * CH * ms1;
+            if (act) {
+                const size_t net = (size_t)d * K + uk;
+                for (int t = slot; t < tn; t += TPU) {
+                    double pe = 0.0, po = 0.0;  // column order, as the reference GEMV
+                    for (int a = 0; a < m; ++a) {
+                        const double2 x = *reinterpret_cast<const double2 *>(xs + 2 * (t * ms1 + a));
+                        const double w0a = D[2 * (a * K + uk)], w1a = -D[2 * (a * K + uk) + 1];
+                        pe += x.x * w0a + x.y * w1a;  // row 2t = [Re x; Im x]
+                        po += x.y * w0a - x.x * w1a;  // row 2t+1 = [Im x; -Re x]
+                    }
+                    const double2 y = *reinterpret_cast<const double2 *>(ys + 2 * (t * K + uk));
+                    const double r_e = y.x - pe, r_o = y.y - po;
+                    rr += r_e * r_e + r_o * r_o;
+                    yy += y.x * y.x + y.y * y.y;
+                    if (p.r0) {
+                        p.r0[net * p.rows + 2 * (t0 + t)] = (float)r_e;
+                        p.r0[net * p.rows + 2 * (t0 + t) + 1] = (float)r_o;
+                    }
                 }
+            }
+            __syncthreads();  // buffer (ch & 1) is refilled by the next issue
+        }
+        red[2 * tid] = rr;
+        red[2 * tid + 1] = yy;
+        __syncthreads();
+        if (tid < K) {
+            double sr = 0.0, sy = 0.0;
+            for (int q = 0; q < TPU; ++q) {
+                sr += red[2 * (tid * TPU + q)];
+                sy += red[2 * (tid * TPU + q) + 1];
+            }
+            decide(tid, sr, sy);
+        }
+    } else {
+        double *sums = red;  // [8 warps][8 users][2]
+        for (int k0 = 0; k0 < K; k0 += 8) {
+            const int kn = min(8, K - k0);
+            double rr[8], yy[8];
 #pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    const int a = a0 + u;
-                    if (a >= m) break;
-                    const double xr = xv[u].x, xi = xv[u].y;
+            for (int k = 0; k < 8; ++k) rr[k] = yy[k] = 0.0;
+            for (int t = tid; t < p.nrow_c; t += kThreads) {
+                double pe[8], po[8];
 #pragma unroll
-                    for (int k = 0; k < 8; ++k) {
-                        if (k < kn) {
-                            const double w0a = D[2 * (a * K + k0 + k)], w1a = -D[2 * (a * K + k0 + k) + 1];
-                            pe[k] += xr * w0a + xi * w1a;  // row 2t = [Re x; Im x]
-                            po[k] += xi * w0a - xr * w1a;  // row 2t+1 = [Im x; -Re x]
+                for (int k = 0; k < 8; ++k) pe[k] = po[k] = 0.0;
+                // the row's samples are loaded four at a time, all in flight
+                // before the FMAs (one dependent L2 load per column made this
+                // phase latency-bound); the sums keep the column order
+                for (int a0 = 0; a0 < m; a0 += 4) {
+                    double2 xv[4];
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        const int a = a0 + u;
+                        xv[u] = a >= m ? make_double2(0.0, 0.0)
+                                : cplx_layout
+                                    ? *reinterpret_cast<const double2 *>(p.design + (((size_t)d * p.nrow_c + t) * m + a) * 2)
+                                    : make_double2(p.design[((size_t)d * p.nrow_c + t) * m + a], 0.0);
+                    }
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        const int a = a0 + u;
+                        if (a >= m) break;
+                        const double xr = xv[u].x, xi = xv[u].y;
+#pragma unroll
+                        for (int k = 0; k < 8; ++k) {
+                            if (k < kn) {
+                                const double w0a = D[2 * (a * K + k0 + k)], w1a = -D[2 * (a * K + k0 + k) + 1];
+                                pe[k] += xr * w0a + xi * w1a;  // row 2t = [Re x; Im x]
+                                po[k] += xi * w0a - xr * w1a;  // row 2t+1 = [Im x; -Re x]
+                            }
                         }
                     }
                 }
-            }
 #pragma unroll
-            for (int k = 0; k < 8; ++k) {
-                if (k >= kn) continue;
-                const size_t net = (size_t)d * K + k0 + k;
-                if (cplx_layout) {
-                    const double2 y = *reinterpret_cast<const double2 *>(p.targets + (((size_t)d * p.nrow_c + t) * K + k0 + k) * 2);
-                    const double r_e = y.x - pe[k], r_o = y.y - po[k];
-                    rr[k] += r_e * r_e + r_o * r_o;
-                    yy[k] += y.x * y.x + y.y * y.y;
-                    if (p.r0) {
-                        p.r0[net * p.rows + 2 * t] = (float)r_e;
-                        p.r0[net * p.rows + 2 * t + 1] = (float)r_o;
+                for (int k = 0; k < 8; ++k) {
+                    if (k >= kn) continue;
+                    const size_t net = (size_t)d * K + k0 + k;
+                    if (cplx_layout) {
+                        const double2 y = *reinterpret_cast<const double2 *>(p.targets + (((size_t)d * p.nrow_c + t) * K + k0 + k) * 2);
+                        const double r_e = y.x - pe[k], r_o = y.y - po[k];
+                        rr[k] += r_e * r_e + r_o * r_o;
+                        yy[k] += y.x * y.x + y.y * y.y;
+                        if (p.r0) {
+                            p.r0[net * p.rows + 2 * t] = (float)r_e;
+                            p.r0[net * p.rows + 2 * t + 1] = (float)r_o;
+                        }
+                    } else {
+                        const double y = p.targets[((size_t)d * K + k0 + k) * p.rows + t];
+                        const double r_e = y - pe[k];
+                        rr[k] += r_e * r_e;
+                        yy[k] += y * y;
+                        if (p.r0) p.r0[net * p.rows + t] = (float)r_e;
                     }
-                } else {
-                    const double y = p.targets[((size_t)d * K + k0 + k) * p.rows + t];
-                    const double r_e = y - pe[k];
-                    rr[k] += r_e * r_e;
-                    yy[k] += y * y;
-                    if (p.r0) p.r0[net * p.rows + t] = (float)r_e;
                 }
             }
+#pragma unroll
+            for (int k = 0; k < 8; ++k)
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) {
+                    rr[k] += __shfl_xor_sync(0xffffffffu, rr[k], o);
+                    yy[k] += __shfl_xor_sync(0xffffffffu, yy[k], o);
+                }
+            if (lane == 0)
+#pragma unroll
+                for (int k = 0; k < 8; ++k) {
+                    sums[(warp * 8 + k) * 2] = rr[k];
+                    sums[(warp * 8 + k) * 2 + 1] = yy[k];
+                }
+            __syncthreads();
+            if (tid < kn) {
+                double sr = 0.0, sy = 0.0;
+                for (int w = 0; w < kThreads / 32; ++w) {
+                    sr += sums[(w * 8 + tid) * 2];
+                    sy += sums[(w * 8 + tid) * 2 + 1];
+                }
+                decide(k0 + tid, sr, sy);
+            }
+            __syncthreads();
         }
-#pragma unroll
-        for (int k = 0; k < 8; ++k)
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) {
-                rr[k] += __shfl_xor_sync(0xffffffffu, rr[k], o);
-                yy[k] += __shfl_xor_sync(0xffffffffu, yy[k], o);
-            }
-        if (lane == 0)
-#pragma unroll
-            for (int k = 0; k < 8; ++k) {
-                sums[(warp * 8 + k) * 2] = rr[k];
-                sums[(warp * 8 + k) * 2 + 1] = yy[k];
-            }
-        __syncthreads();
-        if (tid < kn) {
-            double sr = 0.0, sy = 0.0;
-            for (int w = 0; w < kThreads / 32; ++w) {
-                sr += sums[(w * 8 + tid) * 2];
-                sy += sums[(w * 8 + tid) * 2 + 1];
-            }
-            const double res = sqrt(sr), ynorm = sqrt(sy);
-            const size_t net = (size_t)d * K + k0 + tid;
-            int st = NOMA_OK;
-            double cond;
-            if (rank == m) {
-                cond = lmax / lmin;
-            } else if (rank > 0 && res <= 1e-8 * sqrt(lmax) * fmax(1.0, ynorm)) {
-                cond = lmax / lkeep;
-            } else {
-                st = NOMA_ERR_ILL_CONDITIONED;
-                cond = lmin > 0.0 ? lmax / lmin : INFINITY;
-            }
-            if (p.cond && !fast) p.cond[net] = cond;
-            if (p.status) p.status[net] = st;
-        }
-        __syncthreads();
     }
     NOMA_LLS_CLK(4)
 #undef NOMA_LLS_CLK
+    if (clk) {
+        p.clocks[6] = wait_a;
+        p.clocks[7] = wait_d;
+    }
 }
 
 // lls::predict (lls.cpp:62-66): yhat = narrow(X_widened w0), FP64, one thread
@@ -690,7 +801,7 @@ int lls_predict_launch(int layout, int S, int K, int rows, int width, const doub
 }
 
 size_t lls_smem_bytes(int m, int K) {
-    const size_t bstride = 2 * (size_t)lls_chunk(m) * m + 2 * (size_t)lls_chunk(m) * K;
+    const size_t bstride = 2 * (size_t)lls_chunk(m) * (m + 1) + 2 * (size_t)lls_chunk(m) * K;
     size_t n = 2 * (size_t)m * m * 2 + 2 * (size_t)m * K + 2 * bstride + 4 * (kLlsMaxM / 2 + 1) + m +
                2 * kThreads;
     return n * sizeof(double);
@@ -700,7 +811,7 @@ int lls_launch(const LlsParams &p, cudaStream_t st) {
     if (p.m < 1 || p.m > kLlsMaxM) return NOMA_ERR_UNSUPPORTED;
     const int nent = p.m * (p.m + 1) / 2 + p.m * p.K;
     if (nent > kLlsMaxE * kThreads || p.K > kThreads) return NOMA_ERR_UNSUPPORTED;
-    if (2 * p.m * p.K > 2 * (2 * lls_chunk(p.m) * p.m + 2 * lls_chunk(p.m) * p.K)) return NOMA_ERR_UNSUPPORTED;
+    if (2 * p.m * p.K > 2 * (2 * lls_chunk(p.m) * (p.m + 1) + 2 * lls_chunk(p.m) * p.K)) return NOMA_ERR_UNSUPPORTED;
     const size_t smem = lls_smem_bytes(p.m, p.K);
     if (smem > 227 * 1024) return NOMA_ERR_UNSUPPORTED;
     const int nb = (p.m + 1) / 2, nk = (p.K + 1) / 2;
@@ -710,7 +821,7 @@ int lls_launch(const LlsParams &p, cudaStream_t st) {
     if (mb > 8) return NOMA_ERR_UNSUPPORTED;
     // task partials [task][4][2] reuse the staging buffers when RG > 1
     if (lls_row_groups(p.m) > 1 &&
-        (size_t)ntask * 8 > (size_t)2 * (2 * lls_chunk(p.m) * p.m + 2 * lls_chunk(p.m) * p.K))
+        (size_t)ntask * 8 > (size_t)2 * (2 * lls_chunk(p.m) * (p.m + 1) + 2 * lls_chunk(p.m) * p.K))
         return NOMA_ERR_UNSUPPORTED;
     auto go = [&](auto kern) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

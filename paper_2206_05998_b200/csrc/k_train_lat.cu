@@ -183,6 +183,7 @@ __device__ __forceinline__ void static_for(F &&f) {
 
 constexpr int kLatMaxLayers = 2;    // hidden layers handled by the latency kernel
 constexpr int kLatMaxSteps = 4096;  // Adam bias-correction table in shared memory
+constexpr int kLatMaxHistEpochs = 128;  // epoch-loss history in shared memory (64 KB)
 
 // Shared-memory carve-up (floats), identical on host and device.  Own
 // parameters are double-buffered by step parity: step s reads copy s&1 and
@@ -197,14 +198,14 @@ struct LatCarve {
     int rsst;                                          // dA partial staging [H][kSR]
     int bars;                                          // mbarriers (8-byte aligned)
     int nbars, end;
-    int exp;                                           // A/B switches (NOMA_LAT_EXP), 0 = default
+    int ehist;                                         // epoch-loss history [epochs][128], or -1
 };
 
 // Shapes the latency kernel handles (else the caller falls back): 1-2 hidden
 // layers of one width H = cs * jt with jt in {2, 4, 8} (jt >= 4 with two
 // layers), input width 2M in {32, 64} (k split over 8 lanes, column tiles
 // over at most 16 warps), at most kLatMaxSteps Adam steps.
-__host__ __device__ inline bool lat_carve(const NetGeom &g, int cs, int width, int total_steps,
+__host__ __device__ inline bool lat_carve(const NetGeom &g, int cs, int width, int total_steps, int epochs,
                                           LatCarve *c) {
     const int N = g.nd - 1;
     if (N < 1 || N > kLatMaxLayers || cs < 2 || cs > 16) return false;
@@ -217,7 +218,6 @@ __host__ __device__ inline bool lat_carve(const NetGeom &g, int cs, int width, i
     const int jt = H / cs;
     if (jt != 2 && jt != 4 && jt != 8) return false;
     if (N > 1 && (jt < 4 || H > 64)) return false;
-    c->exp = 0;
     c->cs = cs;
     c->jt = jt;
     c->N = N;
@@ -236,6 +236,14 @@ __host__ __device__ inline bool lat_carve(const NetGeom &g, int cs, int width, i
     off += kBatchRows;
     c->atab = off;
     off += pad_to(2 * total_steps, 4);
+    // per-epoch loss partials of the 128 residual threads, reduced once after
+    // training (a serial per-epoch sum on rank 0 held the whole cluster up at
+    // every epoch end); long runs keep the per-epoch reduction
+    c->ehist = -1;
+    if (epochs > 0 && epochs <= kLatMaxHistEpochs) {
+        c->ehist = off;
+        off += epochs * kBatchRows;
+    }
     int np = 0;
     for (int l = 1; l <= N; ++l) {
         c->sw[l] = g.dims[l - 1] + 4;
@@ -741,7 +749,9 @@ static_for<NL, 0, -1>([&](auto LC) {
             NOMA_TL(9)
         }
         // ---- epoch loss (hybrid_nn.cpp:190-192): trace[e] = sum r^2 / n -------
-        if (rank == 0 && p.trace) {
+        if (c.ehist >= 0) {
+            if (rank == 0 && p.trace && tid < kBatchRows) sm[c.ehist + e * kBatchRows + tid] = loss_acc;
+        } else if (rank == 0 && p.trace) {
             if (tid < kBatchRows) sm[c.red + tid] = loss_acc;
             __syncthreads();
             if (tid == 0) {
@@ -752,6 +762,14 @@ static_for<NL, 0, -1>([&](auto LC) {
             __syncthreads();
         }
         loss_acc = 0.0f;
+    }
+    if (c.ehist >= 0 && rank == 0 && p.trace) {  // same order as the per-epoch sum
+        __syncthreads();
+        for (int e = tid; e < p.epochs; e += kLT) {
+            double t = 0.0;
+            for (int i = 0; i < kBatchRows; ++i) t += sm[c.ehist + e * kBatchRows + i];
+            p.trace[(size_t)net * p.epochs + e] = t / (double)n;
+        }
     }
     NOMA_LPHASE(7)
 #ifdef NOMA_PROBES
@@ -846,8 +864,7 @@ int train_lat_launch(TrainParams &p, cudaStream_t st) {
         if (want && cs != want) continue;
         if (!want && p.n_nets * cs > sms) continue;
         LatCarve c;
-        if (!lat_carve(p.g, cs, p.width, (int)total, &c)) continue;
-        if (const char *x = std::getenv("NOMA_LAT_EXP")) c.exp = std::atoi(x);
+        if (!lat_carve(p.g, cs, p.width, (int)total, p.epochs, &c)) continue;
         const size_t smem = (size_t)c.end * sizeof(float);
         if (!prepped) {
             const unsigned jobs = (unsigned)(p.n_nets * total);
