@@ -387,19 +387,47 @@ __global__ void __launch_bounds__(NW * 32, 1) train_lat_kernel(TrainParams p, La
 #pragma unroll
     for (int l = 0; l <= NL; ++l) mw[l][0] = vw[l][0] = mw[l][1] = vw[l][1] = mb[l] = vb[l] = 0.f;
 
-    // forward thread map: 8 k-split lanes x 32 row quads x 2 neuron halves;
-    // after the k reduce-scatter a lane holds FV values (neuron fj, rows
-    // 4 frq + fr ..), or -- with one neuron per half -- one value on 2 lanes
-    constexpr int JPF = NW == 16 ? JT / 2 : JT;  // neurons per forward thread
+    // forward thread map: KSF k-split lanes x 32 row quads x NW / KSF neuron
+    // groups; after the k reduce-scatter a lane holds FV values (neuron fj,
+    // rows 4 frq + fr ..), or -- with fewer values than lanes -- one value on
+    // KSF / FVV lanes.  One hidden layer on 8 warps splits k over 4 lanes and
+    // the neurons over two groups: one shuffle round less than 8 lanes, at
+    // twice the input loads, which the end-of-step preload hides.
+    constexpr int KSF = (NL == 1 && NW == 8 && JT % 2 == 0) ? 4 : 8;
+    constexpr int JPF = JT / (NW / KSF);         // neurons per forward thread
     constexpr int FVV = 4 * JPF;                 // values before the reduce
-    constexpr int FV = FVV >= 8 ? FVV / 8 : 1;   // values per lane after it
-    const int fkq = tid & 7, frq = (tid >> 3) & 31, fjh = NW == 16 ? tid >> 8 : 0;
-    const int fbase = FVV >= 8 ? fkq * FV : fkq >> (3 - ilog2c(FVV));
-    const bool fown = FVV >= 8 || (fkq & ((8 / FVV) - 1)) == 0;
+    constexpr int FV = FVV >= KSF ? FVV / KSF : 1;  // values per lane after it
+    const int fkq = tid & (KSF - 1), frq = (tid / KSF) & 31, fjh = tid / (KSF * 32);
+    const int fbase = FVV >= KSF ? fkq * FV : fkq >> (ilog2c(KSF) - ilog2c(FVV));
+    const bool fown = FVV >= KSF || (fkq & ((KSF / FVV) - 1)) == 0;
     const int fj = fjh * JPF + (fbase >> 2), fr = fbase & 3;
 
     float loss_acc = 0.0f;
     int s = 0;
+    // The forward's input operands of the next step are loaded at the end of
+    // the current one (after its tile's barrier), so their shared-memory
+    // latency hides behind the end-of-step barrier instead of heading the
+    // forward's chain.
+    constexpr int NCI = W0 / 4 / KSF;  // input k-quads per forward lane
+    ulonglong2 fx[NCI][4];
+    auto load_fx = [&](int step) {
+        mbar_wait(s2u(bars + gbar0 + (step & 1)), (uint32_t)((step >> 1) & 1));  // the step's tile
+        const float *xt = sm + c.xt + (step & 1) * width * kSR;
+#pragma unroll
+        for (int ci = 0; ci < NCI; ++ci)
+#pragma unroll
+            for (int kk = 0; kk < 4; ++kk)
+                fx[ci][kk] = *reinterpret_cast<const ulonglong2 *>(xt + 4 * (fkq + KSF * ci) * kSR + 4 * frq + kk * kSR);
+    };
+    if (total > 0) load_fx(0);
+    // weight-gradient operands of one hidden layer (C1): the input columns and
+    // activations are final after the forward's barrier; every warp loads its
+    // tile while the final-layer partials cross the cluster
+    constexpr int PNCL = W0 / 4;
+    constexpr bool kPre = NL == 1 && PNCL <= NW;
+    constexpr int PJPB = JT / (PNCL >= NW ? 1 : NW / PNCL);
+    ulonglong2 bx[4];
+    float4 bz[PJPB];
     NOMA_LPHASE(7)
     for (int e = 0; e < p.epochs; ++e) {
         for (int st = 0; st < spe; ++st, ++s) {
@@ -407,7 +435,6 @@ __global__ void __launch_bounds__(NW * 32, 1) train_lat_kernel(TrainParams p, La
             const int start = st * p.batch, bsz = min(p.batch, n - start);
             const float *XT = sm + c.xt + buf * width * kSR;
             const int po = buf * c.npar, pn = (buf ^ 1) * c.npar;  // param copy: read, write
-            mbar_wait(s2u(bars + gbar0 + buf), (uint32_t)((s >> 1) & 1));  // this step's tile
             NOMA_TL(0)
             // ---- forward (hybrid_nn.cpp:60-72): all JT own neurons x 4 rows per
             // thread, k split over 8 lanes, lane reduce-scatter --------------
@@ -422,11 +449,16 @@ static_for<1, NL + 1, 1>([&](auto LC) {
 #pragma unroll
                     for (int j = 0; j < JPF; ++j) acc[j][0] = acc[j][1] = 0ull;
 #pragma unroll
-                    for (int kc = fkq; kc < NC; kc += 8) {
+                    for (int kc = fkq; kc < NC; kc += KSF) {
                         const float *ip = in + 4 * kc * kSR + 4 * frq;
                         ulonglong2 x[4];
+                        if constexpr (l == 1) {
 #pragma unroll
-                        for (int kk = 0; kk < 4; ++kk) x[kk] = *reinterpret_cast<const ulonglong2 *>(ip + kk * kSR);
+                            for (int kk = 0; kk < 4; ++kk) x[kk] = fx[kc / KSF][kk];
+                        } else {
+#pragma unroll
+                            for (int kk = 0; kk < 4; ++kk) x[kk] = *reinterpret_cast<const ulonglong2 *>(ip + kk * kSR);
+                        }
 #pragma unroll
                         for (int j = 0; j < JPF; ++j) {
                             const float4 w4 = *reinterpret_cast<const float4 *>(W + j * sw + 4 * kc);
@@ -448,7 +480,7 @@ static_for<1, NL + 1, 1>([&](auto LC) {
                         v[4 * j + 2] = b.x;
                         v[4 * j + 3] = b.y;
                     }
-                    reduce_scatter<FVV, FVV, 8>(v, lane);
+                    reduce_scatter<FVV, FVV, KSF>(v, lane);
                     const float bj = sm[po + c.b[l] + fj];
 #pragma unroll
                     for (int i = 0; i < FV; ++i) v[i] = fmaxf(v[i] + bj, 0.f);
@@ -506,6 +538,13 @@ static_for<1, NL + 1, 1>([&](auto LC) {
             // ---- next step's minibatch tile (bulk copy, one thread off the
             // critical warps; XT[buf^1] was last read in step s-1) ------------
             if (tid == kLT - 32 && s + 1 < total) fetch(s + 1);
+            if constexpr (kPre) {
+                const int ct = warp % PNCL, jg = warp / PNCL, r = 4 * lane;
+#pragma unroll
+                for (int q = 0; q < 4; ++q) bx[q] = *reinterpret_cast<const ulonglong2 *>(XT + (4 * ct + q) * kSR + r);
+#pragma unroll
+                for (int j = 0; j < PJPB; ++j) bz[j] = *reinterpret_cast<const float4 *>(sm + c.aN + (jg * PJPB + j) * kSR + r);
+            }
             NOMA_LPHASE(2)
             NOMA_TL(4)
             // ---- residual a_N w - r0, dy = 2 r / B (hybrid_nn.cpp:94-98): warps
@@ -617,14 +656,23 @@ static_for<NL, 0, -1>([&](auto LC) {
                         for (int q = 0; q < 4; ++q) acc[j][q] = 0ull;
                     }
                     ulonglong2 x[4];
+                    if constexpr (kPre && l == 1) {
 #pragma unroll
-                    for (int q = 0; q < 4; ++q) x[q] = *reinterpret_cast<const ulonglong2 *>(in + (4 * ct + q) * kSR + r);
+                        for (int q = 0; q < 4; ++q) x[q] = bx[q];
+                    } else {
+#pragma unroll
+                        for (int q = 0; q < 4; ++q) x[q] = *reinterpret_cast<const ulonglong2 *>(in + (4 * ct + q) * kSR + r);
+                    }
                     float4 y4 = make_float4(0.f, 0.f, 0.f, 0.f);
                     if (top) y4 = *reinterpret_cast<const float4 *>(dyp + r);
                     const f2_t one = f2_bcast(1.0f);
 #pragma unroll
                     for (int j = 0; j < JPB; ++j) {
-                        float4 z = *reinterpret_cast<const float4 *>(zsrc + (j0 + j) * kSR + r);
+                        float4 z;
+                        if constexpr (kPre && l == 1)
+                            z = bz[j];
+                        else
+                            z = *reinterpret_cast<const float4 *>(zsrc + (j0 + j) * kSR + r);
                         if (top) {  // dZ_N = (a_N > 0) dy w_j on the fly (:102-107)
                             ffma2(sf[j], f2_pack(z.x, z.y), f2_pack(y4.x, y4.y));
                             ffma2(sf[j], f2_pack(z.z, z.w), f2_pack(y4.z, y4.w));
@@ -744,6 +792,7 @@ static_for<NL, 0, -1>([&](auto LC) {
             });
             NOMA_LPHASE(5)
             NOMA_TL(8)
+            if (s + 1 < total) load_fx(s + 1);
             __syncthreads();
             NOMA_LPHASE(6)
             NOMA_TL(9)
