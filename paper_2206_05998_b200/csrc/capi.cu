@@ -1168,17 +1168,8 @@ int pipeline_impl(noma_ctx_t c, const noma_net_desc *desc, const noma_train_cfg 
         }
         s.forked = true;
         noma_dataset ds{NOMA_LAYOUT_WIDEN_COMPLEX, Sc, K, n, 2 * M, cpx, cpy};
-        mark(c, ch, 2, c->side3);
-        if (f64 ? init_theta_launch(g, (int)cn, iseed + an, th64s[b], ptrain, c->side3)
-                : init_launch(g, (int)cn, iseed + an, nullptr, cdp, c->side3))
-            return cuda_fail(c, "init");
-        mark(c, ch, 3, c->side3);
-        cudaEventRecord(c->join, c->side3);
-        mark(c, ch, 8, c->side2);
-        if (perm_launch((int)cn, cfg->epochs, n, sseed + an, perms[b], c->side2, overlap && ch > 0 ? 32 : 64))
-            return cuda_fail(c, "perm");
-        mark(c, ch, 4, c->side2);
-        cudaEventRecord(ev_perm[ch], c->side2);
+        // the LLS is the longest of the three and heads the critical path:
+        // it is enqueued first (a one-slot call spends ~60 us on the host)
         mark(c, ch, 0, c->side);
         LlsParams lp = lls_params(&ds, cpx, cpy, cdw, cdc, cdst, d32s[b], r0s[b]);
         lp.mode = 1;
@@ -1198,7 +1189,18 @@ int pipeline_impl(noma_ctx_t c, const noma_net_desc *desc, const noma_train_cfg 
         }
         if (r) return r == NOMA_ERR_CUDA ? cuda_fail(c, "lls") : fail(c, r, "lls: unsupported shape");
         mark(c, ch, 1, c->side);
-        if (cdc) {  // condition numbers of the Cholesky-path slots, joined at the chunk's end
+        mark(c, ch, 8, c->side2);
+        if (perm_launch((int)cn, cfg->epochs, n, sseed + an, perms[b], c->side2, overlap && ch > 0 ? 32 : 64))
+            return cuda_fail(c, "perm");
+        mark(c, ch, 4, c->side2);
+        cudaEventRecord(ev_perm[ch], c->side2);
+        mark(c, ch, 2, c->side3);
+        if (f64 ? init_theta_launch(g, (int)cn, iseed + an, th64s[b], ptrain, c->side3)
+                : init_launch(g, (int)cn, iseed + an, nullptr, cdp, c->side3))
+            return cuda_fail(c, "init");
+        mark(c, ch, 3, c->side3);
+        cudaEventRecord(c->join, c->side3);
+        if (cdc) {  // condition numbers of the Cholesky-path slots (after the shuffles), joined at the chunk's end
             LlsParams lc = lls_params(&ds, cpx, cpy, nullptr, cdc, nullptr, nullptr, nullptr);
             lc.mode = 2;
             if (lls_launch(lc, c->side2)) return cuda_fail(c, "lls condition");

@@ -636,21 +636,34 @@ __global__ void __launch_bounds__(kThreads) lls_kernel(LlsParams p) {
             const double *xs = bufs + (ch & 1) * bstride, *ys = xs + 2 * CH * ms1;
             if (act) {
                 const size_t net = (size_t)d * K + uk;
-                for (int t = slot; t < tn; t += TPU) {
-                    double pe = 0.0, po = 0.0;  // column order, as the reference GEMV
+                // two rows at a time (independent chains), columns unrolled so
+                // the operand loads run ahead; each sum keeps the column order
+                for (int t = slot; t < tn; t += 2 * TPU) {
+                    const int t2 = t + TPU < tn ? t + TPU : t;
+                    double pe0 = 0.0, po0 = 0.0, pe1 = 0.0, po1 = 0.0;
+#pragma unroll 8
                     for (int a = 0; a < m; ++a) {
-                        const double2 x = *reinterpret_cast<const double2 *>(xs + 2 * (t * ms1 + a));
+                        const double2 x0 = *reinterpret_cast<const double2 *>(xs + 2 * (t * ms1 + a));
+                        const double2 x1 = *reinterpret_cast<const double2 *>(xs + 2 * (t2 * ms1 + a));
                         const double w0a = D[2 * (a * K + uk)], w1a = -D[2 * (a * K + uk) + 1];
-                        pe += x.x * w0a + x.y * w1a;  // row 2t = [Re x; Im x]
-                        po += x.y * w0a - x.x * w1a;  // row 2t+1 = [Im x; -Re x]
+                        pe0 += x0.x * w0a + x0.y * w1a;  // row 2t = [Re x; Im x]
+                        po0 += x0.y * w0a - x0.x * w1a;  // row 2t+1 = [Im x; -Re x]
+                        pe1 += x1.x * w0a + x1.y * w1a;
+                        po1 += x1.y * w0a - x1.x * w1a;
                     }
-                    const double2 y = *reinterpret_cast<const double2 *>(ys + 2 * (t * K + uk));
-                    const double r_e = y.x - pe, r_o = y.y - po;
-                    rr += r_e * r_e + r_o * r_o;
-                    yy += y.x * y.x + y.y * y.y;
-                    if (p.r0) {
-                        p.r0[net * p.rows + 2 * (t0 + t)] = (float)r_e;
-                        p.r0[net * p.rows + 2 * (t0 + t) + 1] = (float)r_o;
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        if (h == 1 && t2 == t) break;
+                        const int tt = h ? t2 : t;
+                        const double pe = h ? pe1 : pe0, po = h ? po1 : po0;
+                        const double2 y = *reinterpret_cast<const double2 *>(ys + 2 * (tt * K + uk));
+                        const double r_e = y.x - pe, r_o = y.y - po;
+                        rr += r_e * r_e + r_o * r_o;
+                        yy += y.x * y.x + y.y * y.y;
+                        if (p.r0) {
+                            p.r0[net * p.rows + 2 * (t0 + tt)] = (float)r_e;
+                            p.r0[net * p.rows + 2 * (t0 + tt) + 1] = (float)r_o;
+                        }
                     }
                 }
             }
