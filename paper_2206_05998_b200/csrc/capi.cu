@@ -1,5 +1,6 @@
 // C-ABI (include/noma_cuda.h): context, staging and the batched entry points.
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -1006,6 +1007,14 @@ int pipeline_impl(noma_ctx_t c, const noma_net_desc *desc, const noma_train_cfg 
                   double *gram_condition, float *plans, double *loss_trace, float *soft, uint8_t *codes,
                   uint32_t *bit_errors, uint32_t *symbol_errors, int *status, int mem, int precision) {
     if (!c) return NOMA_ERR_ARGUMENT;
+    // NOMA_HOST_TIMING=1: host-side microseconds at the enqueue milestones
+    static const bool htime = std::getenv("NOMA_HOST_TIMING") != nullptr;
+    const auto ht0 = std::chrono::steady_clock::now();
+    auto ht = [&](const char *what) {
+        if (htime)
+            std::fprintf(stderr, "NOMA_HOST_TIMING %s %.1f\n", what,
+                         std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - ht0).count());
+    };
     const bool f64 = precision == 64;
     int st;
     if ((st = check_cfg(c, cfg))) return st;
@@ -1177,7 +1186,9 @@ int pipeline_impl(noma_ctx_t c, const noma_net_desc *desc, const noma_train_cfg 
             lp.clocks = s.scratch<long long>(8);
             if (lp.clocks) cudaMemsetAsync(lp.clocks, 0, 8 * sizeof(long long), c->side);
         }
+        ht("before_lls");
         int r = lls_launch(lp, c->side);
+        ht("after_lls");
         if (lclk && lp.clocks && !r) {
             long long h[8];
             cudaMemcpyAsync(h, lp.clocks, sizeof(h), cudaMemcpyDeviceToHost, c->side);
@@ -1194,6 +1205,10 @@ int pipeline_impl(noma_ctx_t c, const noma_net_desc *desc, const noma_train_cfg 
             return cuda_fail(c, "perm");
         mark(c, ch, 4, c->side2);
         cudaEventRecord(ev_perm[ch], c->side2);
+        if (ND > 0) {  // error counters of the chunk (detection adds into them), off the critical path
+            if (der) cudaMemsetAsync(der + an, 0, cn * sizeof(uint32_t), c->side3);
+            if (dse) cudaMemsetAsync(dse + an, 0, cn * sizeof(uint32_t), c->side3);
+        }
         mark(c, ch, 2, c->side3);
         if (f64 ? init_theta_launch(g, (int)cn, iseed + an, th64s[b], ptrain, c->side3)
                 : init_launch(g, (int)cn, iseed + an, nullptr, cdp, c->side3))
@@ -1210,6 +1225,7 @@ int pipeline_impl(noma_ctx_t c, const noma_net_desc *desc, const noma_train_cfg 
         if (set_w0_launch((int)cn, 2 * M, g.plan_total, cdw, cdp, c->side)) return cuda_fail(c, "w0");
         cudaEventRecord(ev_ready[ch], c->side);
         c->launches += 4;
+        ht("prologue_done");
         return NOMA_OK;
     };
     cudaEventRecord(c->fork, c->stream);
@@ -1321,7 +1337,9 @@ int pipeline_impl(noma_ctx_t c, const noma_net_desc *desc, const noma_train_cfg 
                 st = NOMA_ERR_UNSUPPORTED;
             } else {
                 prep_scratch(s, tp);
+                ht("before_train");
                 st = train_launch(tp, c->stream);
+                ht("after_train");
                 c->train_mode = tp.mode;
             }
             if (st == NOMA_ERR_UNSUPPORTED) st = train_generic_f32(c, s, tp, c->stream);
@@ -1344,9 +1362,7 @@ int pipeline_impl(noma_ctx_t c, const noma_net_desc *desc, const noma_train_cfg 
         mark(c, ch, 6);
         if (host) cudaStreamWaitEvent(c->stream, ev_dat[ch], 0);
         if (ND > 0) {
-            uint32_t *cder = der ? der + an : nullptr, *cdse = dse ? dse + an : nullptr;
-            if (cder) cudaMemsetAsync(cder, 0, cn * sizeof(uint32_t), c->stream);
-            if (cdse) cudaMemsetAsync(cdse, 0, cn * sizeof(uint32_t), c->stream);
+            uint32_t *cder = der ? der + an : nullptr, *cdse = dse ? dse + an : nullptr;  // zeroed in the prologue
             DetectParams dpp;
             dpp.g = g;
             dpp.layout = NOMA_LAYOUT_WIDEN_COMPLEX;
@@ -1397,7 +1413,9 @@ int pipeline_impl(noma_ctx_t c, const noma_net_desc *desc, const noma_train_cfg 
         cudaEventRecord(done, c->copy2);
         cudaStreamWaitEvent(c->stream, done, 0);
     }
+    ht("enqueued");
     st = s.finish();
+    ht("finished");
     if (st == NOMA_OK && host) st = cudaStreamSynchronize(c->stream) == cudaSuccess ? NOMA_OK : cuda_fail(c, "synchronize");
     return st;
 }

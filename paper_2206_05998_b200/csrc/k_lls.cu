@@ -836,14 +836,23 @@ int lls_launch(const LlsParams &p, cudaStream_t st) {
     if (lls_row_groups(p.m) > 1 &&
         (size_t)ntask * 8 > (size_t)2 * (2 * lls_chunk(p.m) * (p.m + 1) + 2 * lls_chunk(p.m) * p.K))
         return NOMA_ERR_UNSUPPORTED;
-    auto go = [&](auto kern) {
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    // the shared-memory opt-in is raised once per device and kernel (a host
+    // call per launch delayed the single-slot pipeline's critical path)
+    static int smem_set[64][4] = {};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    auto go = [&](auto kern, int ki) {
+        int *have = dev >= 0 && dev < 64 ? &smem_set[dev][ki] : nullptr;
+        if (!have || *have < (int)smem) {
+            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            if (have) *have = (int)smem;
+        }
         kern<<<p.n_designs, kThreads, smem, st>>>(p);
     };
-    if (mb == 1) go(lls_kernel<1>);
-    else if (mb == 2) go(lls_kernel<2>);
-    else if (mb <= 4) go(lls_kernel<4>);
-    else go(lls_kernel<8>);
+    if (mb == 1) go(lls_kernel<1>, 0);
+    else if (mb == 2) go(lls_kernel<2>, 1);
+    else if (mb <= 4) go(lls_kernel<4>, 2);
+    else go(lls_kernel<8>, 3);
     return cudaGetLastError() == cudaSuccess ? NOMA_OK : NOMA_ERR_CUDA;
 }
 

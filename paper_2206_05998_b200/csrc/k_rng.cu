@@ -90,6 +90,43 @@ const uint64_t *jump_table() {
     return d;
 }
 
+// Init blocks: kInitDraws draws (kInitDraws / 2 Box-Muller gaussians) per
+// lane.  Table [2][256][4]: J = T^kInitDraws and J^32 (a warp's 32 blocks).
+constexpr int kInitDraws = 32;
+namespace {
+std::mutex g_init_mu;
+const uint64_t *g_init_jump[64] = {};
+}  // namespace
+const uint64_t *init_jump_table() {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lk(g_init_mu);
+    if (dev < 0 || dev >= 64) return nullptr;
+    if (g_init_jump[dev]) return g_init_jump[dev];
+    std::vector<Gf2> tab(2);
+    Gf2 t, tmp;
+    gf2_step_matrix(t);
+    tab[0] = t;  // T^32 by squaring (32 = 2^5)
+    for (int k = 0; k < 5; ++k) {
+        gf2_mul(tab[0], tab[0], tmp);
+        tab[0] = tmp;
+    }
+    tab[1] = tab[0];  // (T^32)^32
+    for (int k = 0; k < 5; ++k) {
+        gf2_mul(tab[1], tab[1], tmp);
+        tab[1] = tmp;
+    }
+    uint64_t *d = nullptr;
+    const size_t bytes = tab.size() * sizeof(Gf2);
+    if (cudaMalloc(&d, bytes) != cudaSuccess) return nullptr;
+    if (cudaMemcpy(d, tab.data(), bytes, cudaMemcpyHostToDevice) != cudaSuccess) {
+        cudaFree(d);
+        return nullptr;
+    }
+    g_init_jump[dev] = d;
+    return d;
+}
+
 // s <- M s over GF(2) (M in row form, 256 x 4 u64)
 __device__ __forceinline__ void gf2_apply(const uint64_t *__restrict__ m, Xoshiro &x) {
     uint64_t o[4] = {0, 0, 0, 0};
@@ -318,19 +355,20 @@ __global__ void __launch_bounds__(kInitThreads) init_block_kernel(
     // every thread holds the caller's state before the last block's lane
     // writes the advanced state back over it
     __syncthreads();
-    constexpr int G = kJumpDraws / 2;  // gaussians per block
+    constexpr int G = kInitDraws / 2;  // gaussians per block (lane)
     const int blocks = (total + G - 1) / G;
     // chunks of 32 blocks per warp: the chunk's first state by c steps of
-    // J^32 (lo[32]), then the warp steps through J (lo[1]) and lane t keeps
-    // block 32 c + t (gf2_warp_apply)
+    // J^32 (jtab[1]), then the warp steps through J (jtab[0]) and lane t keeps
+    // block 32 c + t (gf2_warp_apply).  16 gaussians per lane: a C1 net's
+    // 2048 draws take four warps instead of one (Box-Muller is the long part)
     const int warp = tid >> 5, lane = tid & 31;
     for (int c = warp; 32 * c < blocks; c += kInitThreads / 32) {
         Xoshiro x = r0;
-        for (int i = 0; i < c; ++i) x = gf2_warp_apply(jtab + 32 * 1024, x, lane);
+        for (int i = 0; i < c; ++i) x = gf2_warp_apply(jtab + 1024, x, lane);
         Xoshiro r = x;
         for (int t = 0; t < 32 && 32 * c + t < blocks; ++t) {
             if (lane == t) r = x;
-            x = gf2_warp_apply(jtab + 1024, x, lane);
+            x = gf2_warp_apply(jtab, x, lane);
         }
         const int b = 32 * c + lane;
         if (b >= blocks) continue;
@@ -366,11 +404,8 @@ __global__ void __launch_bounds__(kInitThreads) init_block_kernel(
 int init_state_launch(const NetGeom &g, int n_nets, uint64_t *states, const double *w0,
                       float *plans, double *theta, int ptrain, cudaStream_t st) {
     if (n_nets == 0) return NOMA_OK;
-    const uint64_t *jt = jump_table();
+    const uint64_t *jt = init_jump_table();
     if (!jt) return NOMA_ERR_CUDA;
-    int total = 0;
-    for (int l = 1; l < g.nd; ++l) total += g.dims[l] * g.dims[l - 1];
-    if ((total + kJumpDraws / 2 - 1) / (kJumpDraws / 2) > kJumpLo * kJumpHi) return NOMA_ERR_UNSUPPORTED;
     init_block_kernel<<<n_nets, kInitThreads, 0, st>>>(g, nullptr, states, w0, plans, theta, ptrain, jt);
     return cudaGetLastError() == cudaSuccess ? NOMA_OK : NOMA_ERR_CUDA;
 }
@@ -378,11 +413,8 @@ int init_state_launch(const NetGeom &g, int n_nets, uint64_t *states, const doub
 int init_launch(const NetGeom &g, int n_nets, const uint64_t *seeds, const double *w0,
                 float *plans, cudaStream_t st) {
     if (n_nets == 0) return NOMA_OK;
-    const uint64_t *jt = jump_table();
+    const uint64_t *jt = init_jump_table();
     if (!jt) return NOMA_ERR_CUDA;
-    int total = 0;
-    for (int l = 1; l < g.nd; ++l) total += g.dims[l] * g.dims[l - 1];
-    if ((total + kJumpDraws / 2 - 1) / (kJumpDraws / 2) > kJumpLo * kJumpHi) return NOMA_ERR_UNSUPPORTED;
     init_block_kernel<<<n_nets, kInitThreads, 0, st>>>(g, seeds, nullptr, w0, plans, nullptr, 0, jt);
     return cudaGetLastError() == cudaSuccess ? NOMA_OK : NOMA_ERR_CUDA;
 }
@@ -390,11 +422,8 @@ int init_launch(const NetGeom &g, int n_nets, const uint64_t *seeds, const doubl
 int init_theta_launch(const NetGeom &g, int n_nets, const uint64_t *seeds, double *theta, int ptrain,
                       cudaStream_t st) {
     if (n_nets == 0) return NOMA_OK;
-    const uint64_t *jt = jump_table();
+    const uint64_t *jt = init_jump_table();
     if (!jt) return NOMA_ERR_CUDA;
-    int total = 0;
-    for (int l = 1; l < g.nd; ++l) total += g.dims[l] * g.dims[l - 1];
-    if ((total + kJumpDraws / 2 - 1) / (kJumpDraws / 2) > kJumpLo * kJumpHi) return NOMA_ERR_UNSUPPORTED;
     init_block_kernel<<<n_nets, kInitThreads, 0, st>>>(g, seeds, nullptr, nullptr, nullptr, theta, ptrain, jt);
     return cudaGetLastError() == cudaSuccess ? NOMA_OK : NOMA_ERR_CUDA;
 }
