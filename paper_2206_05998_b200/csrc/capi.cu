@@ -339,6 +339,8 @@ LlsParams lls_params(const noma_dataset *ds, const double *x, const double *y, d
     p.design32 = d32;
     p.r0 = r0;
     p.clocks = nullptr;
+    p.plans = nullptr;
+    p.plan_total = 0;
     p.mode = 0;
     return p;
 }
@@ -699,7 +701,7 @@ NOMA_API int noma_init_params(noma_ctx_t c, const noma_net_desc *desc, int n_net
     const double *dw = s.in(w0, (size_t)n_nets * g.dims[0]);
     float *dp = s.out(plans, (size_t)n_nets * g.plan_total);
     if (!s.ok) return s.finish();
-    if (init_launch(g, n_nets, sd, dw, dp, c->stream)) return cuda_fail(c, "init");
+    if (init_launch(g, n_nets, sd, dw, false, dp, c->stream)) return cuda_fail(c, "init");
     c->launches += 1;
     return s.finish();
 }
@@ -1094,6 +1096,9 @@ int pipeline_impl(noma_ctx_t c, const noma_net_desc *desc, const noma_train_cfg 
         }
     }
     double *mom64 = f64 ? s.scratch<double>((size_t)chunk * K * 2 * ptrain) : nullptr;
+    // per-step Adam constants (lr / c1, 1 / c2), computed in the prologue
+    const int total_steps = cfg->epochs * ((n + cfg->batch_size - 1) / cfg->batch_size);
+    float *atab = !f64 && total_steps > 0 ? s.scratch<float>(2 * (size_t)total_steps) : nullptr;
     if (!s.ok) return s.finish();
 
     // host buffers: every chunk's inputs are queued on the copy stream up
@@ -1182,6 +1187,10 @@ int pipeline_impl(noma_ctx_t c, const noma_net_desc *desc, const noma_train_cfg 
         mark(c, ch, 0, c->side);
         LlsParams lp = lls_params(&ds, cpx, cpy, cdw, cdc, cdst, d32s[b], r0s[b]);
         lp.mode = 1;
+        if (!f64) {  // the LLS writes the plans' w0 slots (the init leaves them alone)
+            lp.plans = cdp;
+            lp.plan_total = g.plan_total;
+        }
         if (lclk) {
             lp.clocks = s.scratch<long long>(8);
             if (lp.clocks) cudaMemsetAsync(lp.clocks, 0, 8 * sizeof(long long), c->side);
@@ -1209,9 +1218,11 @@ int pipeline_impl(noma_ctx_t c, const noma_net_desc *desc, const noma_train_cfg 
             if (der) cudaMemsetAsync(der + an, 0, cn * sizeof(uint32_t), c->side3);
             if (dse) cudaMemsetAsync(dse + an, 0, cn * sizeof(uint32_t), c->side3);
         }
+        if (ch == 0 && atab && adam_table_launch(cfg->lr, cfg->beta1, cfg->beta2, total_steps, atab, c->side3))
+            return cuda_fail(c, "adam table");
         mark(c, ch, 2, c->side3);
         if (f64 ? init_theta_launch(g, (int)cn, iseed + an, th64s[b], ptrain, c->side3)
-                : init_launch(g, (int)cn, iseed + an, nullptr, cdp, c->side3))
+                : init_launch(g, (int)cn, iseed + an, nullptr, true, cdp, c->side3))
             return cuda_fail(c, "init");
         mark(c, ch, 3, c->side3);
         cudaEventRecord(c->join, c->side3);
@@ -1222,9 +1233,9 @@ int pipeline_impl(noma_ctx_t c, const noma_net_desc *desc, const noma_train_cfg 
         }
         cudaEventRecord(ev_cond[ch], c->side2);
         cudaStreamWaitEvent(c->side, c->join, 0);  // the init is in the plans
-        if (set_w0_launch((int)cn, 2 * M, g.plan_total, cdw, cdp, c->side)) return cuda_fail(c, "w0");
+        if (f64 && set_w0_launch((int)cn, 2 * M, g.plan_total, cdw, cdp, c->side)) return cuda_fail(c, "w0");
         cudaEventRecord(ev_ready[ch], c->side);
-        c->launches += 4;
+        c->launches += f64 ? 4 : 3;
         ht("prologue_done");
         return NOMA_OK;
     };
@@ -1328,6 +1339,7 @@ int pipeline_impl(noma_ctx_t c, const noma_net_desc *desc, const noma_train_cfg 
             tp.plans = cdp;
             tp.trace = dt ? dt + an * cfg->epochs : nullptr;
             tp.status = cdst;
+            tp.atab = atab;
             const bool clocks = std::getenv("NOMA_PHASE_CLOCKS") != nullptr && ch == 0;
             // [0..8) phase totals, [8..) per-warp timeline of 4 steps (latency kernel)
             constexpr int kClk = 8 + 4 * 16 * 16;

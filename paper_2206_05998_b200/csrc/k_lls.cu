@@ -382,11 +382,17 @@ __global__ void __launch_bounds__(kThreads) lls_kernel(LlsParams p) {
                     D[2 * (a * K + k)] = yr[h];
                     D[2 * (a * K + k) + 1] = yi[h];
                     double *w = p.w0 + ((size_t)d * K + k) * p.width;
+                    float *pw = p.plans ? p.plans + ((size_t)d * K + k) * p.plan_total : nullptr;
                     if (cplx_layout) {
                         w[a] = yr[h];
                         w[m + a] = -yi[h];
+                        if (pw) {
+                            pw[a] = (float)yr[h];
+                            pw[m + a] = (float)(-yi[h]);
+                        }
                     } else {
                         w[a] = yr[h];
+                        if (pw) pw[a] = (float)yr[h];
                     }
                 }
             }
@@ -574,11 +580,17 @@ __global__ void __launch_bounds__(kThreads) lls_kernel(LlsParams p) {
         D[2 * it] = sr;
         D[2 * it + 1] = si;
         double *w = p.w0 + ((size_t)d * K + k) * p.width;
+        float *pw = p.plans ? p.plans + ((size_t)d * K + k) * p.plan_total : nullptr;
         if (cplx_layout) {
             w[a] = sr;
             w[m + a] = -si;
+            if (pw) {
+                pw[a] = (float)sr;
+                pw[m + a] = (float)(-si);
+            }
         } else {
             w[a] = sr;
+            if (pw) pw[a] = (float)sr;
         }
     }
     __syncthreads();

@@ -327,14 +327,15 @@ int perm_launch(int n_nets, int epochs, int n, const uint64_t *seeds, uint16_t *
 constexpr int kInitThreads = 128;
 
 __global__ void __launch_bounds__(kInitThreads) init_block_kernel(
-    NetGeom g, const uint64_t *seeds, uint64_t *states, const double *w0, float *plans,
+    NetGeom g, const uint64_t *seeds, uint64_t *states, const double *w0, bool keep_w0, float *plans,
     double *theta, int ptrain, const uint64_t *jtab) {
     const int net = blockIdx.x, tid = threadIdx.x;
     float *pl = plans ? plans + (size_t)net * g.plan_total : nullptr;
     double *th = theta ? theta + (size_t)net * ptrain : nullptr;
-    // zero outputs, w0 slot, biases / final (theta)
+    // zero outputs, w0 slot (unless a concurrent LLS writes it: keep_w0),
+    // biases / final (theta)
     if (pl) {
-        for (int i = tid; i < g.plan_total; i += kInitThreads) pl[i] = 0.0f;
+        for (int i = tid + (keep_w0 ? g.dims[0] : 0); i < g.plan_total; i += kInitThreads) pl[i] = 0.0f;
     }
     if (th) {
         for (int i = tid; i < ptrain; i += kInitThreads) th[i] = 0.0;
@@ -406,16 +407,16 @@ int init_state_launch(const NetGeom &g, int n_nets, uint64_t *states, const doub
     if (n_nets == 0) return NOMA_OK;
     const uint64_t *jt = init_jump_table();
     if (!jt) return NOMA_ERR_CUDA;
-    init_block_kernel<<<n_nets, kInitThreads, 0, st>>>(g, nullptr, states, w0, plans, theta, ptrain, jt);
+    init_block_kernel<<<n_nets, kInitThreads, 0, st>>>(g, nullptr, states, w0, false, plans, theta, ptrain, jt);
     return cudaGetLastError() == cudaSuccess ? NOMA_OK : NOMA_ERR_CUDA;
 }
 
-int init_launch(const NetGeom &g, int n_nets, const uint64_t *seeds, const double *w0,
+int init_launch(const NetGeom &g, int n_nets, const uint64_t *seeds, const double *w0, bool keep_w0,
                 float *plans, cudaStream_t st) {
     if (n_nets == 0) return NOMA_OK;
     const uint64_t *jt = init_jump_table();
     if (!jt) return NOMA_ERR_CUDA;
-    init_block_kernel<<<n_nets, kInitThreads, 0, st>>>(g, seeds, nullptr, w0, plans, nullptr, 0, jt);
+    init_block_kernel<<<n_nets, kInitThreads, 0, st>>>(g, seeds, nullptr, w0, keep_w0, plans, nullptr, 0, jt);
     return cudaGetLastError() == cudaSuccess ? NOMA_OK : NOMA_ERR_CUDA;
 }
 
@@ -424,7 +425,7 @@ int init_theta_launch(const NetGeom &g, int n_nets, const uint64_t *seeds, doubl
     if (n_nets == 0) return NOMA_OK;
     const uint64_t *jt = init_jump_table();
     if (!jt) return NOMA_ERR_CUDA;
-    init_block_kernel<<<n_nets, kInitThreads, 0, st>>>(g, seeds, nullptr, nullptr, nullptr, theta, ptrain, jt);
+    init_block_kernel<<<n_nets, kInitThreads, 0, st>>>(g, seeds, nullptr, nullptr, false, nullptr, theta, ptrain, jt);
     return cudaGetLastError() == cudaSuccess ? NOMA_OK : NOMA_ERR_CUDA;
 }
 

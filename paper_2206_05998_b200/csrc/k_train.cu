@@ -516,6 +516,8 @@ int train_thr_launch(TrainParams &p, cudaStream_t st, size_t smem, int mom_smem,
 // Adam bias-correction constants of every step, FP64 pow as hybrid_nn.cpp:133-135:
 // one FP64 pow pair per step in the training kernel sat on the minibatch
 // gather's barrier (a long dependent FP64 chain on one thread)
+int adam_table_launch(double lr, double b1, double b2, int total, float *t, cudaStream_t st);
+
 __global__ void adam_table_kernel(double lr, double b1, double b2, int total, float *t) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i < total) {
@@ -524,6 +526,12 @@ __global__ void adam_table_kernel(double lr, double b1, double b2, int total, fl
         t[2 * i] = (float)(lr / c1);
         t[2 * i + 1] = (float)(1.0 / c2);
     }
+}
+
+int adam_table_launch(double lr, double b1, double b2, int total, float *t, cudaStream_t st) {
+    if (total <= 0) return NOMA_OK;
+    adam_table_kernel<<<(total + 255) / 256, 256, 0, st>>>(lr, b1, b2, total, t);
+    return cudaGetLastError() == cudaSuccess ? NOMA_OK : NOMA_ERR_CUDA;
 }
 
 int train_launch(TrainParams &p, cudaStream_t st) {
@@ -592,9 +600,12 @@ int train_launch(TrainParams &p, cudaStream_t st) {
         }
     }
     // throughput kernels: per-step Adam constants precomputed once per launch
+    // (unless the caller already did, off the critical path)
+    const float *given = p.atab;
     float *tab = nullptr;
     const int total = p.epochs * ((p.rows + p.batch - 1) / p.batch);
-    if (total > 0 && cudaMallocAsync(&tab, 2 * (size_t)total * sizeof(float), st) == cudaSuccess) {
+    if (given) {
+    } else if (total > 0 && cudaMallocAsync(&tab, 2 * (size_t)total * sizeof(float), st) == cudaSuccess) {
         adam_table_kernel<<<(total + 255) / 256, 256, 0, st>>>(p.lr_d, p.b1d, p.b2d, total, tab);
         if (cudaGetLastError() == cudaSuccess) p.atab = tab;
     } else {
@@ -603,7 +614,7 @@ int train_launch(TrainParams &p, cudaStream_t st) {
     }
     const int r = train_thr_launch(p, st, smem, mom_smem, need);
     if (tab) cudaFreeAsync(tab, st);
-    p.atab = nullptr;
+    p.atab = given;
     return r;
 }
 

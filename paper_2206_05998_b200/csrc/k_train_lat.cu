@@ -332,10 +332,15 @@ __global__ void __launch_bounds__(NW * 32, 1) train_lat_kernel(TrainParams p, La
     if (tid < JT) sm[c.wf + tid] = pl[g.plan_f + rank * JT + tid];
     // Adam bias corrections per step, FP64 pow like hybrid_nn.cpp:133-135
     for (int i = tid; i < c.total; i += kLT) {
-        const double c1 = 1.0 - pow(p.b1d, (double)(i + 1));
-        const double c2 = 1.0 - pow(p.b2d, (double)(i + 1));
-        sm[c.atab + 2 * i] = (float)(p.lr_d / c1);
-        sm[c.atab + 2 * i + 1] = (float)(1.0 / c2);
+        if (p.atab) {  // precomputed beside the LLS (adam_table_kernel, same arithmetic)
+            sm[c.atab + 2 * i] = p.atab[2 * i];
+            sm[c.atab + 2 * i + 1] = p.atab[2 * i + 1];
+        } else {
+            const double c1 = 1.0 - pow(p.b1d, (double)(i + 1));
+            const double c2 = 1.0 - pow(p.b2d, (double)(i + 1));
+            sm[c.atab + 2 * i] = (float)(p.lr_d / c1);
+            sm[c.atab + 2 * i + 1] = (float)(1.0 / c2);
+        }
     }
     constexpr uint32_t ybytes = CS * kBatchRows * 4;
     // all-gather / reduce-scatter move whole [JT][kSR] tiles by bulk copy

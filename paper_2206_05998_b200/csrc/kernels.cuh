@@ -17,6 +17,8 @@ struct LlsParams {
     float *design32;      // nullable: FP32 copy for training, [S][nrow_c][width]
     float *r0;            // nullable: [net][rows]
     long long *clocks;    // nullable: phase cycles of block 0 (NOMA_PHASE_CLOCKS)
+    float *plans;         // nullable: FusedPlan buffers whose w0 slot gets (float) w0
+    int plan_total;
     int mode;             // 0: Jacobi path; 1: Cholesky fast path (Jacobi fallback), no
                           // cond for fast-path nets; 2: condition numbers only
 };
@@ -142,7 +144,7 @@ struct TrainGenParams {
 int lls_launch(const LlsParams &p, cudaStream_t st);
 int perm_launch(int n_nets, int epochs, int n, const uint64_t *seeds, uint16_t *perm,
                 cudaStream_t st, int max_tpb = 64);
-int init_launch(const NetGeom &g, int n_nets, const uint64_t *seeds, const double *w0,
+int init_launch(const NetGeom &g, int n_nets, const uint64_t *seeds, const double *w0, bool keep_w0,
                 float *plans, cudaStream_t st);
 int set_w0_launch(int n_nets, int d0, int plan_total, const double *w0, float *plans,
                   cudaStream_t st);
@@ -156,6 +158,7 @@ bool train_w4_fits(const TrainParams &p);
 int train_w4_launch(TrainParams &p, cudaStream_t st);
 bool train_w8_fits(const TrainParams &p);
 int train_w8_launch(TrainParams &p, cudaStream_t st);
+int adam_table_launch(double lr, double b1, double b2, int total, float *t, cudaStream_t st);
 bool train_l2_fits(const TrainParams &p);
 int train_l2_launch(TrainParams &p, cudaStream_t st);
 // widened FP32 design rows (2t = [Re|Im], 2t+1 = [Im|-Re]) for the cp.async gathers
