@@ -341,6 +341,7 @@ LlsParams lls_params(const noma_dataset *ds, const double *x, const double *y, d
     p.clocks = nullptr;
     p.plans = nullptr;
     p.plan_total = 0;
+    p.fast = nullptr;
     p.mode = 0;
     return p;
 }
@@ -1099,6 +1100,7 @@ int pipeline_impl(noma_ctx_t c, const noma_net_desc *desc, const noma_train_cfg 
     // per-step Adam constants (lr / c1, 1 / c2), computed in the prologue
     const int total_steps = cfg->epochs * ((n + cfg->batch_size - 1) / cfg->batch_size);
     float *atab = !f64 && total_steps > 0 ? s.scratch<float>(2 * (size_t)total_steps) : nullptr;
+    unsigned char *fastf = s.scratch<unsigned char>((size_t)chunk);  // per slot: Cholesky path taken
     if (!s.ok) return s.finish();
 
     // host buffers: every chunk's inputs are queued on the copy stream up
@@ -1191,6 +1193,7 @@ int pipeline_impl(noma_ctx_t c, const noma_net_desc *desc, const noma_train_cfg 
             lp.plans = cdp;
             lp.plan_total = g.plan_total;
         }
+        lp.fast = fastf;  // residuals of the Cholesky-path slots by lls_r0_launch
         if (lclk) {
             lp.clocks = s.scratch<long long>(8);
             if (lp.clocks) cudaMemsetAsync(lp.clocks, 0, 8 * sizeof(long long), c->side);
@@ -1207,6 +1210,7 @@ int pipeline_impl(noma_ctx_t c, const noma_net_desc *desc, const noma_train_cfg 
                          "gram_wait %lld residual_wait %lld\n",
                          h[0], h[1], h[2], h[3], h[4], h[5], h[6], h[7]);
         }
+        if (!r) r = lls_r0_launch(lp, c->side);
         if (r) return r == NOMA_ERR_CUDA ? cuda_fail(c, "lls") : fail(c, r, "lls: unsupported shape");
         mark(c, ch, 1, c->side);
         mark(c, ch, 8, c->side2);

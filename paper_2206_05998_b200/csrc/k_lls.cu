@@ -46,6 +46,15 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
+// One column's term of the widened prediction x_t . w0 (phase D and
+// lls_r0_kernel: same rounding, so either pass gives the same r0 bits)
+__device__ __forceinline__ double r0_even(double2 x, double w0a, double w1a) {
+    return __fma_rn(x.x, w0a, __dmul_rn(x.y, w1a));
+}
+__device__ __forceinline__ double r0_odd(double2 x, double w0a, double w1a) {
+    return __fma_rn(x.y, w0a, -__dmul_rn(x.x, w1a));
+}
+
 // Phase A register blocking: a thread accumulates 2 x 2 complex blocks
 // (columns a, a+1 against columns b, b+1 of the design, or targets k, k+1) --
 // four complex operands per row feed four MACs -- over the rows of its row
@@ -597,6 +606,16 @@ __global__ void __launch_bounds__(kThreads) lls_kernel(LlsParams p) {
     }  // !fast
     NOMA_LLS_CLK(3)
 
+    // a Cholesky-path design is full rank: status OK, and with p.fast its
+    // residuals come from lls_r0_kernel (spread over many CTAs)
+    if (p.fast && cplx_layout) {
+        if (tid == 0) p.fast[d] = fast ? 1 : 0;
+        if (fast) {
+            for (int k = tid; k < K; k += kThreads)
+                if (p.status) p.status[(size_t)d * K + k] = NOMA_OK;
+            return;
+        }
+    }
     // ---- phase D: residuals r0 = y - X w0 (FP64) and their norms (status of
     // rank-deficient designs, lls.cpp:43-49)
     auto decide = [&](int k, double sr, double sy) {
@@ -658,10 +677,10 @@ __global__ void __launch_bounds__(kThreads) lls_kernel(LlsParams p) {
                         const double2 x0 = *reinterpret_cast<const double2 *>(xs + 2 * (t * ms1 + a));
                         const double2 x1 = *reinterpret_cast<const double2 *>(xs + 2 * (t2 * ms1 + a));
                         const double w0a = D[2 * (a * K + uk)], w1a = -D[2 * (a * K + uk) + 1];
-                        pe0 += x0.x * w0a + x0.y * w1a;  // row 2t = [Re x; Im x]
-                        po0 += x0.y * w0a - x0.x * w1a;  // row 2t+1 = [Im x; -Re x]
-                        pe1 += x1.x * w0a + x1.y * w1a;
-                        po1 += x1.y * w0a - x1.x * w1a;
+                        pe0 = __dadd_rn(pe0, r0_even(x0, w0a, w1a));  // row 2t = [Re x; Im x]
+                        po0 = __dadd_rn(po0, r0_odd(x0, w0a, w1a));   // row 2t+1 = [Im x; -Re x]
+                        pe1 = __dadd_rn(pe1, r0_even(x1, w0a, w1a));
+                        po1 = __dadd_rn(po1, r0_odd(x1, w0a, w1a));
                     }
 #pragma unroll
                     for (int h = 0; h < 2; ++h) {
@@ -822,6 +841,37 @@ int lls_predict_launch(int layout, int S, int K, int rows, int width, const doub
     if (n == 0) return NOMA_OK;
     lls_predict_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(layout, S, K, rows, width,
                                                                      data, w0, out);
+    return cudaGetLastError() == cudaSuccess ? NOMA_OK : NOMA_ERR_CUDA;
+}
+
+// r0 = y - X w0 of the Cholesky-path designs (WIDEN layout), one thread per
+// (design, user, complex row); phase D's arithmetic, column order.
+__global__ void lls_r0_kernel(LlsParams p) {
+    const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int m = p.m, K = p.K, nr = p.nrow_c;
+    if (i >= (size_t)p.n_designs * K * nr) return;
+    const int t = (int)(i % nr);
+    const size_t net = i / nr;
+    const int d = (int)(net / K);
+    if (!p.fast[d]) return;
+    const double *w = p.w0 + net * p.width;
+    const double2 *x = reinterpret_cast<const double2 *>(p.design + ((size_t)d * nr + t) * m * 2);
+    double pe = 0.0, po = 0.0;
+    for (int a = 0; a < m; ++a) {
+        const double2 xv = x[a];
+        const double w0a = w[a], w1a = w[m + a];
+        pe = __dadd_rn(pe, r0_even(xv, w0a, w1a));
+        po = __dadd_rn(po, r0_odd(xv, w0a, w1a));
+    }
+    const double2 y = *reinterpret_cast<const double2 *>(p.targets + (((size_t)d * nr + t) * K + (net - (size_t)d * K)) * 2);
+    p.r0[net * p.rows + 2 * t] = (float)(y.x - pe);
+    p.r0[net * p.rows + 2 * t + 1] = (float)(y.y - po);
+}
+
+int lls_r0_launch(const LlsParams &p, cudaStream_t st) {
+    const size_t n = (size_t)p.n_designs * p.K * p.nrow_c;
+    if (!p.fast || !p.r0 || n == 0) return NOMA_OK;
+    lls_r0_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(p);
     return cudaGetLastError() == cudaSuccess ? NOMA_OK : NOMA_ERR_CUDA;
 }
 

@@ -19,6 +19,8 @@ struct LlsParams {
     long long *clocks;    // nullable: phase cycles of block 0 (NOMA_PHASE_CLOCKS)
     float *plans;         // nullable: FusedPlan buffers whose w0 slot gets (float) w0
     int plan_total;
+    unsigned char *fast;  // nullable (WIDEN, mode 1): per design, 1 = Cholesky path taken and r0
+                          // left to lls_r0_launch (many CTAs) instead of the one-CTA pass
     int mode;             // 0: Jacobi path; 1: Cholesky fast path (Jacobi fallback), no
                           // cond for fast-path nets; 2: condition numbers only
 };
@@ -159,6 +161,7 @@ int train_w4_launch(TrainParams &p, cudaStream_t st);
 bool train_w8_fits(const TrainParams &p);
 int train_w8_launch(TrainParams &p, cudaStream_t st);
 int adam_table_launch(double lr, double b1, double b2, int total, float *t, cudaStream_t st);
+int lls_r0_launch(const LlsParams &p, cudaStream_t st);
 bool train_l2_fits(const TrainParams &p);
 int train_l2_launch(TrainParams &p, cudaStream_t st);
 // widened FP32 design rows (2t = [Re|Im], 2t+1 = [Im|-Re]) for the cp.async gathers
