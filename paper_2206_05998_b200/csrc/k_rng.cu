@@ -324,7 +324,7 @@ int perm_launch(int n_nets, int epochs, int n, const uint64_t *seeds, uint16_t *
 // and/or the flat FP64 parameter vector.  Seeds come from `seeds`
 // (Rng(seed)) or, when `states` is non-null, from caller xoshiro states that
 // are advanced in place past all draws (init_params(..., Rng&)).
-constexpr int kInitThreads = 128;
+constexpr int kInitThreads = 512;  // 16 warps: a [32, 64, 64] net's 12 chunks of 32 blocks run at once
 
 __global__ void __launch_bounds__(kInitThreads) init_block_kernel(
     NetGeom g, const uint64_t *seeds, uint64_t *states, const double *w0, bool keep_w0, float *plans,
