@@ -57,6 +57,20 @@ if mode in ("all", "w4"):  # the 4-warp throughput kernel (one hidden layer of 6
     out = api.pipeline([32, 64], sy8.pilot_rx, sy8.pilot_sym, sy8.data_rx, sy8.data_codes, i8, s8, epochs=2)
     print("w4", api.context().train_mode, api.context().detect_mode, out.bit_errors.ravel()[:6])
     os.environ.pop("NOMA_LAT_CLUSTER")
+if mode in ("all", "l2"):  # the two-hidden-layer 8-warp kernel (train mode 5), 8 slots x 6 users
+    sy8 = api.synthesize(6, 16, 100, 256, [5, 6, 7, 8, 9, 10, 11, 12], snr_db=15.0, rx_nonlinearity_gain=0.05)
+    i8, s8 = slot_user_seeds(np.arange(5, 13, dtype=np.uint64), 6)
+    os.environ["NOMA_LAT_CLUSTER"] = "1"
+    out = api.pipeline([32, 64, 64], sy8.pilot_rx, sy8.pilot_sym, sy8.data_rx, sy8.data_codes, i8, s8, epochs=2)
+    print("l2", api.context().train_mode, api.context().detect_mode, out.bit_errors.ravel()[:6])
+    os.environ.pop("NOMA_LAT_CLUSTER")
+if mode in ("all", "w8"):  # the 8-warp kernel on a 128-wide input (train mode 4), 2 slots x 8 users
+    sy2 = api.synthesize(8, 64, 130, 256, [5, 6], snr_db=15.0, rx_nonlinearity_gain=0.05)
+    i2, s2 = slot_user_seeds(np.arange(5, 7, dtype=np.uint64), 8)
+    os.environ["NOMA_LAT_CLUSTER"] = "1"
+    out = api.pipeline([128, 64], sy2.pilot_rx, sy2.pilot_sym, sy2.data_rx, sy2.data_codes, i2, s2, epochs=2)
+    print("w8", api.context().train_mode, api.context().detect_mode, out.bit_errors.ravel()[:6])
+    os.environ.pop("NOMA_LAT_CLUSTER")
 if mode in ("all", "generic"):  # shape-general training / detection, FP64 pipeline mode
     out = api.pipeline([32, 160], sy.pilot_rx, sy.pilot_sym, sy.data_rx, sy.data_codes, init, shuf, epochs=2)
     print("generic", api.context().train_mode, api.context().detect_mode, out.bit_errors.ravel())
