@@ -45,9 +45,10 @@ struct L2Geom {
     static constexpr int off_b2 = off_b1 + 64;
     static constexpr int off_f = off_b2 + 64;
     static constexpr int off_dz = off_f + 64;
-    static constexpr int off_ks = off_dz + 32 * DS;    // [4][32 acc][32 lanes] f2
+    static constexpr int off_ks = off_dz + 32 * DS;    // [4 wr][2 halves][16 acc][32 lanes] f2
     static constexpr int off_red = off_ks + 4 * 32 * 32 * 2;  // [4 warps][gf | gb2 | gb1][64]
-    static constexpr int off_r0 = off_red + 4 * 3 * 64;
+    static constexpr int off_yx = off_red + 4 * 3 * 64;    // [2 halves][128 rows] final-layer partials
+    static constexpr int off_r0 = off_yx + 2 * kBatchRows;
     static constexpr int off_loss = off_r0 + kBatchRows;
     static constexpr int off_end = off_loss + kL2Threads;
     static constexpr size_t bytes = (size_t)off_end * sizeof(float);
@@ -68,12 +69,15 @@ __device__ __forceinline__ void cp_wait_l() {
 }
 
 // out[pair jp = l8 + 8m][row 32 wr + q + 4i] = bias + sum_k Wp[jp][2k + e] in[row][k]
-// over the warp half's K range (kh), the upper half's partials added by the
-// lower half through shared memory (fixed order).  Every thread calls it (it
-// holds a block barrier); afterwards the lower half (kh = 0) has the sums.
+// over the warp half's K range (kh); the halves then swap partials through
+// shared memory so that each ends with the full sums of its own two pair
+// groups m = 2 kh, 2 kh + 1 (own[mm] = group 2 kh + mm), always added as
+// lower-K + upper-K (fixed order, bias in the lower half).  Every thread
+// calls it (it holds a block barrier).
 template <int K>
-__device__ __forceinline__ void fwd_ksplit(f2_t (&acc)[4][8], const float *Wp, int ws, const float *in, int is,
+__device__ __forceinline__ void fwd_ksplit(f2_t (&own)[2][8], const float *Wp, int ws, const float *in, int is,
                                            const float *bias, f2_t *KS, int kh, int wr, int q, int l8, int lane) {
+    f2_t acc[4][8];
 #pragma unroll
     for (int m = 0; m < 4; ++m) {
         const f2_t bb = (kh || !bias) ? 0ull : *reinterpret_cast<const f2_t *>(bias + 2 * (l8 + 8 * m));
@@ -104,23 +108,27 @@ __device__ __forceinline__ void fwd_ksplit(f2_t (&acc)[4][8], const float *Wp, i
         NOMA_L2_FWD(3, w[m][1].y)
 #undef NOMA_L2_FWD
     }
-    f2_t *ks = KS + (size_t)wr * 32 * 32 + lane;
-    if (kh) {
+    // [wr][source half][16 values][32 lanes]: the groups the partner owns
+    f2_t *ks = KS + (size_t)(wr * 2 + kh) * 16 * 32 + lane;
 #pragma unroll
-        for (int m = 0; m < 4; ++m)
+    for (int mm = 0; mm < 2; ++mm)
 #pragma unroll
-            for (int i = 0; i < 8; ++i) ks[(m * 8 + i) * 32] = acc[m][i];
-    }
+        for (int i = 0; i < 8; ++i) ks[(mm * 8 + i) * 32] = kh ? acc[mm][i] : acc[2 + mm][i];
     __syncthreads();
-    if (!kh) {
+    const f2_t *kr = KS + (size_t)(wr * 2 + (kh ^ 1)) * 16 * 32 + lane;
 #pragma unroll
-        for (int m = 0; m < 4; ++m)
+    for (int mm = 0; mm < 2; ++mm)
 #pragma unroll
-            for (int i = 0; i < 8; ++i) {
-                const float2 lo = f2_unpack(acc[m][i]), hi = f2_unpack(ks[(m * 8 + i) * 32]);
-                acc[m][i] = f2_pack(lo.x + hi.x, lo.y + hi.y);
-            }
-    }
+        for (int i = 0; i < 8; ++i) {
+            const float2 mine = f2_unpack(kh ? acc[2 + mm][i] : acc[mm][i]);
+            const float2 other = f2_unpack(kr[(mm * 8 + i) * 32]);
+            own[mm][i] = kh ? f2_pack(other.x + mine.x, other.y + mine.y) : f2_pack(mine.x + other.x, mine.y + other.y);
+        }
+}
+
+// named barrier of the two warps (w, w + 4) that cover the same 32 rows
+__device__ __forceinline__ void pair_sync(int wr) {
+    asm volatile("bar.sync %0, 64;" ::"r"(1 + wr) : "memory");
 }
 
 // gW[pair jp = 4 warp + jq + 2i][column c = 4 l8 + 32 g + t] = sum over all 128
@@ -215,6 +223,7 @@ __global__ void __launch_bounds__(kL2Threads, 1) train_l2_kernel(TrainParams p, 
     float *W1 = sm + G::off_w1, *W2 = sm + G::off_w2, *W2T = sm + G::off_w2t;
     float *B1 = sm + G::off_b1, *B2 = sm + G::off_b2, *F = sm + G::off_f;
     float *DZ = sm + G::off_dz, *RED = sm + G::off_red, *R0 = sm + G::off_r0, *LS = sm + G::off_loss;
+    float *YX = sm + G::off_yx;
     f2_t *KS = reinterpret_cast<f2_t *>(sm + G::off_ks);
 
     // ---- parameters in (FusedPlan layout, fused_inference.cpp:19-42) ------
@@ -287,43 +296,42 @@ __global__ void __launch_bounds__(kL2Threads, 1) train_l2_kernel(TrainParams p, 
                 lrc = (float)(p.lr_d / c1);
                 ic2 = (float)(1.0 / c2);
             }
-            f2_t acc[4][8];
+            // each warp half finishes pair groups m = 2 kh, 2 kh + 1 (own[mm])
+            f2_t own[2][8];
 
             // ---- F1: a1 = relu(W1 x + b1) (hybrid_nn.cpp:60-67) ----------------
-            fwd_ksplit<IN>(acc, W1, G::WS1, X, G::XS, B1, KS, kh, wr, q, l8, lane);
-            if (!kh) {
+            fwd_ksplit<IN>(own, W1, G::WS1, X, G::XS, B1, KS, kh, wr, q, l8, lane);
 #pragma unroll
-                for (int m = 0; m < 4; ++m)
+            for (int mm = 0; mm < 2; ++mm)
 #pragma unroll
-                    for (int i = 0; i < 8; ++i) {
-                        float2 a = f2_unpack(acc[m][i]);
-                        a.x = fmaxf(a.x, 0.f);
-                        a.y = fmaxf(a.y, 0.f);
-                        *reinterpret_cast<float2 *>(A1 + (32 * wr + q + 4 * i) * G::AS + 2 * (l8 + 8 * m)) = a;
-                    }
-            }
+                for (int i = 0; i < 8; ++i) {
+                    float2 a = f2_unpack(own[mm][i]);
+                    a.x = fmaxf(a.x, 0.f);
+                    a.y = fmaxf(a.y, 0.f);
+                    *reinterpret_cast<float2 *>(A1 + (32 * wr + q + 4 * i) * G::AS + 2 * (l8 + 8 * (2 * kh + mm))) = a;
+                }
             __syncthreads();
 
             // ---- F2: a2 = relu(W2 a1 + b2), residual, dZ2 (:60-107) ------------
-            fwd_ksplit<64>(acc, W2, G::WS2, A1, G::AS, B2, KS, kh, wr, q, l8, lane);
-            if (!kh) {
+            fwd_ksplit<64>(own, W2, G::WS2, A1, G::AS, B2, KS, kh, wr, q, l8, lane);
+            {
                 float yp[8];
 #pragma unroll
                 for (int i = 0; i < 8; ++i) yp[i] = 0.f;
 #pragma unroll
-                for (int m = 0; m < 4; ++m) {
-                    const float2 fw = *reinterpret_cast<const float2 *>(F + 2 * (l8 + 8 * m));
+                for (int mm = 0; mm < 2; ++mm) {
+                    const float2 fw = *reinterpret_cast<const float2 *>(F + 2 * (l8 + 8 * (2 * kh + mm)));
 #pragma unroll
                     for (int i = 0; i < 8; ++i) {
-                        float2 a = f2_unpack(acc[m][i]);
+                        float2 a = f2_unpack(own[mm][i]);
                         a.x = fmaxf(a.x, 0.f);
                         a.y = fmaxf(a.y, 0.f);
-                        acc[m][i] = f2_pack(a.x, a.y);
+                        own[mm][i] = f2_pack(a.x, a.y);
                         yp[i] = fmaf(fw.x, a.x, yp[i]);
                         yp[i] = fmaf(fw.y, a.y, yp[i]);
                     }
                 }
-                float yhat;  // reduce-scatter over the quarter's 8 lanes
+                float yhalf;  // reduce-scatter over the quarter's 8 lanes: row rr_own
                 {
                     const bool b4 = l8 & 4, b2 = l8 & 2, b1 = l8 & 1;
                     float y4[4];
@@ -342,50 +350,56 @@ __global__ void __launch_bounds__(kL2Threads, 1) train_l2_kernel(TrainParams p, 
                     }
                     const float send = b1 ? y2[0] : y2[1];
                     const float keep = b1 ? y2[1] : y2[0];
-                    yhat = keep + __shfl_xor_sync(kFullL2, send, 1);
+                    yhalf = keep + __shfl_xor_sync(kFullL2, send, 1);
                 }
+                // the two halves' neuron partials of each row meet in shared
+                // memory (the warp pair covering these rows syncs alone)
+                YX[kh * kBatchRows + rr_own] = yhalf;
+                pair_sync(wr);
+                const float yhat = YX[rr_own] + YX[kBatchRows + rr_own];
                 const float res = rr_own < bsz ? yhat - R0[rr_own] : 0.f;  // (:94)
                 const float dy_own = (2.0f / (float)bsz) * res;              // (:98)
-                lossacc = fmaf(res, res, lossacc);
+                if (!kh) lossacc = fmaf(res, res, lossacc);
                 float dy[8];
 #pragma unroll
                 for (int i = 0; i < 8; ++i) dy[i] = __shfl_sync(kFullL2, dy_own, (lane & 24) | i);
-                float2 gf[4], gb[4];
+                float2 gf[2], gb[2];
 #pragma unroll
-                for (int m = 0; m < 4; ++m) {
-                    const int jp = l8 + 8 * m;
+                for (int mm = 0; mm < 2; ++mm) {
+                    const int jp = l8 + 8 * (2 * kh + mm);
                     const float2 fw = *reinterpret_cast<const float2 *>(F + 2 * jp);
-                    gf[m] = gb[m] = make_float2(0.f, 0.f);
+                    gf[mm] = gb[mm] = make_float2(0.f, 0.f);
 #pragma unroll
                     for (int i = 0; i < 8; ++i) {
                         const int r = 32 * wr + q + 4 * i;
-                        const float2 a = f2_unpack(acc[m][i]);
+                        const float2 a = f2_unpack(own[mm][i]);
                         const float2 z =
                             make_float2(a.x > 0.f ? dy[i] * fw.x : 0.f, a.y > 0.f ? dy[i] * fw.y : 0.f);
-                        gf[m].x = fmaf(a.x, dy[i], gf[m].x);
-                        gf[m].y = fmaf(a.y, dy[i], gf[m].y);
-                        gb[m].x += z.x;
-                        gb[m].y += z.y;
+                        gf[mm].x = fmaf(a.x, dy[i], gf[mm].x);
+                        gf[mm].y = fmaf(a.y, dy[i], gf[mm].y);
+                        gb[mm].x += z.x;
+                        gb[mm].y += z.y;
                         *reinterpret_cast<float2 *>(DZ + jp * G::DS + 2 * r) = z;
                         *reinterpret_cast<float2 *>(D2 + r * G::AS + 2 * jp) = z;
                     }
                 }
 #pragma unroll
-                for (int m = 0; m < 4; ++m) {
-                    gf[m].x += __shfl_xor_sync(kFullL2, gf[m].x, 8);
-                    gf[m].y += __shfl_xor_sync(kFullL2, gf[m].y, 8);
-                    gb[m].x += __shfl_xor_sync(kFullL2, gb[m].x, 8);
-                    gb[m].y += __shfl_xor_sync(kFullL2, gb[m].y, 8);
-                    gf[m].x += __shfl_xor_sync(kFullL2, gf[m].x, 16);
-                    gf[m].y += __shfl_xor_sync(kFullL2, gf[m].y, 16);
-                    gb[m].x += __shfl_xor_sync(kFullL2, gb[m].x, 16);
-                    gb[m].y += __shfl_xor_sync(kFullL2, gb[m].y, 16);
+                for (int mm = 0; mm < 2; ++mm) {
+                    gf[mm].x += __shfl_xor_sync(kFullL2, gf[mm].x, 8);
+                    gf[mm].y += __shfl_xor_sync(kFullL2, gf[mm].y, 8);
+                    gb[mm].x += __shfl_xor_sync(kFullL2, gb[mm].x, 8);
+                    gb[mm].y += __shfl_xor_sync(kFullL2, gb[mm].y, 8);
+                    gf[mm].x += __shfl_xor_sync(kFullL2, gf[mm].x, 16);
+                    gf[mm].y += __shfl_xor_sync(kFullL2, gf[mm].y, 16);
+                    gb[mm].x += __shfl_xor_sync(kFullL2, gb[mm].x, 16);
+                    gb[mm].y += __shfl_xor_sync(kFullL2, gb[mm].y, 16);
                 }
                 if (q == 0) {
 #pragma unroll
-                    for (int m = 0; m < 4; ++m) {
-                        *reinterpret_cast<float2 *>(RED + wr * 192 + 2 * (l8 + 8 * m)) = gf[m];
-                        *reinterpret_cast<float2 *>(RED + wr * 192 + 64 + 2 * (l8 + 8 * m)) = gb[m];
+                    for (int mm = 0; mm < 2; ++mm) {
+                        const int jp = l8 + 8 * (2 * kh + mm);
+                        *reinterpret_cast<float2 *>(RED + wr * 192 + 2 * jp) = gf[mm];
+                        *reinterpret_cast<float2 *>(RED + wr * 192 + 64 + 2 * jp) = gb[mm];
                     }
                 }
             }
@@ -396,35 +410,35 @@ __global__ void __launch_bounds__(kL2Threads, 1) train_l2_kernel(TrainParams p, 
             grad_rows<64>(gk2, DZ, G::DS, A1, G::AS, warp, q, l8);
 
             // ---- B1: dA1 = dZ2 W2 (:111, W2 before its update), dZ1 (:107) ----
-            fwd_ksplit<64>(acc, W2T, G::WS2, D2, G::AS, nullptr, KS, kh, wr, q, l8, lane);
-            if (!kh) {
-                float2 gb1[4];
+            fwd_ksplit<64>(own, W2T, G::WS2, D2, G::AS, nullptr, KS, kh, wr, q, l8, lane);
+            {
+                float2 gb1[2];
 #pragma unroll
-                for (int m = 0; m < 4; ++m) {
-                    const int cp = l8 + 8 * m;
-                    gb1[m] = make_float2(0.f, 0.f);
+                for (int mm = 0; mm < 2; ++mm) {
+                    const int cp = l8 + 8 * (2 * kh + mm);
+                    gb1[mm] = make_float2(0.f, 0.f);
 #pragma unroll
                     for (int i = 0; i < 8; ++i) {
                         const int r = 32 * wr + q + 4 * i;
                         const float2 a1 = *reinterpret_cast<const float2 *>(A1 + r * G::AS + 2 * cp);
-                        const float2 da = f2_unpack(acc[m][i]);
+                        const float2 da = f2_unpack(own[mm][i]);
                         const float2 z = make_float2(a1.x > 0.f ? da.x : 0.f, a1.y > 0.f ? da.y : 0.f);
-                        gb1[m].x += z.x;
-                        gb1[m].y += z.y;
+                        gb1[mm].x += z.x;
+                        gb1[mm].y += z.y;
                         *reinterpret_cast<float2 *>(DZ + cp * G::DS + 2 * r) = z;
                     }
                 }
 #pragma unroll
-                for (int m = 0; m < 4; ++m) {
-                    gb1[m].x += __shfl_xor_sync(kFullL2, gb1[m].x, 8);
-                    gb1[m].y += __shfl_xor_sync(kFullL2, gb1[m].y, 8);
-                    gb1[m].x += __shfl_xor_sync(kFullL2, gb1[m].x, 16);
-                    gb1[m].y += __shfl_xor_sync(kFullL2, gb1[m].y, 16);
+                for (int mm = 0; mm < 2; ++mm) {
+                    gb1[mm].x += __shfl_xor_sync(kFullL2, gb1[mm].x, 8);
+                    gb1[mm].y += __shfl_xor_sync(kFullL2, gb1[mm].y, 8);
+                    gb1[mm].x += __shfl_xor_sync(kFullL2, gb1[mm].x, 16);
+                    gb1[mm].y += __shfl_xor_sync(kFullL2, gb1[mm].y, 16);
                 }
                 if (q == 0) {
 #pragma unroll
-                    for (int m = 0; m < 4; ++m)
-                        *reinterpret_cast<float2 *>(RED + wr * 192 + 128 + 2 * (l8 + 8 * m)) = gb1[m];
+                    for (int mm = 0; mm < 2; ++mm)
+                        *reinterpret_cast<float2 *>(RED + wr * 192 + 128 + 2 * (l8 + 8 * (2 * kh + mm))) = gb1[mm];
                 }
             }
             __syncthreads();
