@@ -120,6 +120,7 @@ NOMA_API long long noma_ctx_kernel_launches(noma_ctx_t ctx);
  * 100 + c = neuron-split latency cluster of c CTAs per net (k_train_lat.cu),
  * 3 = 4-warp one-hidden-layer kernel (k_train_w4.cu: inputs 32 / 64),
  * 4 = 8-warp one-hidden-layer kernel (k_train_w8.cu: 128-wide inputs, C4),
+ * 5 = 8-warp two-hidden-layer kernel (k_train_l2.cu: [32 | 64, 64, 64], C2),
  * 200 = shape-general FP32 kernel (k_train_generic.cu: layers wider than 128,
  *       minibatches above 128 rows), 201 = its FP64 instance (noma_train_f64),
  * 300 = on-chip FP64 kernel (k_train_f64.cu), 301 = register-tiled FP64
