@@ -295,6 +295,9 @@ __global__ void __launch_bounds__(WsRoles<W0, NL>::kThreads, 1) detect_ws_kernel
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;");
     const uint32_t tmem = *tmem_slot;
+    // launched as a programmatic dependent of the training kernel: the plans
+    // it writes are read below (a no-op for an ordinary launch)
+    asm volatile("griddepcontrol.wait;" ::: "memory");
     // this CTA's share of the global (net, tile) range; one pipeline segment
     // per net it touches, the mbarrier phases running on across segments (ib)
     const long long T = (long long)p.n_nets * p.tiles;
@@ -699,8 +702,17 @@ int detect_tc_launch(const DetectParams &dp, cudaStream_t st) {
         // one CTA per SM: each allocates all 512 TMEM columns
         smem = smem < 116 * 1024 ? 116 * 1024 : smem;
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        kern<<<ctas, threads, smem, st>>>(p);
-        const bool launched = cudaGetLastError() == cudaSuccess;
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(ctas);
+        cfg.blockDim = dim3(threads);
+        cfg.dynamicSmemBytes = smem;
+        cfg.stream = st;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[0].val.programmaticStreamSerializationAllowed = 1;  // prologue beside the producer's tail
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        const bool launched = cudaLaunchKernelEx(&cfg, kern, p) == cudaSuccess && cudaGetLastError() == cudaSuccess;
         if (clk) {  // roles: loaders, epilogue 1, epilogue 2, L1 issuers (even, odd), L2 issuers (even, odd)
             long long h[48];
             cudaMemcpyAsync(h, clk_buf, sizeof h, cudaMemcpyDeviceToHost, st);

@@ -283,6 +283,9 @@ __global__ void __launch_bounds__(NW * 32, 1) train_lat_kernel(TrainParams p, La
     constexpr int H = CS * JT;
     const int net = blockIdx.x / CS;
     if (p.status && p.status[net] != NOMA_OK) return;  // uniform over the cluster
+    // detection (programmatic dependent launch) may take the idle SMs for its
+    // prologue; it waits for this grid before reading the trained plans
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     const uint32_t rank = cl_rank();
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const NetGeom &g = p.g;
