@@ -1210,14 +1210,16 @@ int pipeline_impl(noma_ctx_t c, const noma_net_desc *desc, const noma_train_cfg 
                          "gram_wait %lld residual_wait %lld\n",
                          h[0], h[1], h[2], h[3], h[4], h[5], h[6], h[7]);
         }
-        if (!r) r = lls_r0_launch(lp, c->side);
         if (r) return r == NOMA_ERR_CUDA ? cuda_fail(c, "lls") : fail(c, r, "lls: unsupported shape");
-        mark(c, ch, 1, c->side);
         mark(c, ch, 8, c->side2);
         if (perm_launch((int)cn, cfg->epochs, n, sseed + an, perms[b], c->side2, overlap && ch > 0 ? 32 : 64))
             return cuda_fail(c, "perm");
         mark(c, ch, 4, c->side2);
         cudaEventRecord(ev_perm[ch], c->side2);
+        // the residual kernel follows the LLS on its stream; enqueued after the
+        // shuffles so that their launch is not held up by it
+        if (lls_r0_launch(lp, c->side)) return cuda_fail(c, "lls r0");
+        mark(c, ch, 1, c->side);
         if (ND > 0) {  // error counters of the chunk (detection adds into them), off the critical path
             if (der) cudaMemsetAsync(der + an, 0, cn * sizeof(uint32_t), c->side3);
             if (dse) cudaMemsetAsync(dse + an, 0, cn * sizeof(uint32_t), c->side3);
