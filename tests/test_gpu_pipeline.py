@@ -86,6 +86,42 @@ def test_pipeline_lls_paths_match_lls_fit(A, O):
     assert werr.max() <= 1e-10, werr
 
 
+def test_jacobi_path_slot_trains_like_the_oracle(A, O):
+    # A consistent rank-deficient slot takes the LLS's Jacobi path (min-norm
+    # w0, status OK) next to a full-rank Cholesky-path slot: its residuals
+    # come from the in-kernel pass, the other's from the r0 kernel, and both
+    # w0 go straight into the plans.  Three epochs of training and detection
+    # against the FP64 oracle's lls_fit -> init_params -> train -> detect:
+    # the full-rank slot to 1e-4; the consistent slot's residual targets are
+    # rounding noise (~1e-15), which Adam turns into full-size steps, so its
+    # network part is chaotic in FP32 and only the LLS-dominated output is
+    # compared (w0 to 1e-10, soft to 2e-2).
+    rng = np.random.default_rng(21)
+    S, NT, M, K, ND, dims = 2, 96, 4, 2, 64, [8, 16]
+    x = rng.normal(size=(S, NT, M)) + 1j * rng.normal(size=(S, NT, M))
+    x[1, :, 3] = x[1, :, 0]                            # rank 3 of 4: Jacobi path
+    c = rng.normal(size=(S, M, K)) + 1j * rng.normal(size=(S, M, K))
+    y = np.einsum("stm,smk->stk", x, c)                # slot 1 consistent: min-norm, OK
+    y[0] += 0.05 * (rng.normal(size=(NT, K)) + 1j * rng.normal(size=(NT, K)))
+    xd = (rng.normal(size=(S, ND, M)) + 1j * rng.normal(size=(S, ND, M))).astype(np.complex64)
+    init, shuf = _seeds(O, [41, 42], K)
+    out = A.pipeline(dims, x, y, xd, np.zeros((S, ND, K), np.uint8), init, shuf, epochs=3)
+    assert (out.status == 0).all()
+    for s in range(S):
+        wx = O.widen_design(x[s])
+        for k in range(K):
+            wy = O.widen_targets(y[s][:, k])
+            lls = O.lls_fit(wx, wy)
+            net = O.init_params(dims, lls.w, O.Rng(int(init[s, k])))
+            O.train(net, wx, wy, epochs=3, batch_size=128, lr=0.005, shuffle_seed=int(shuf[s, k]))
+            ref = O.detect(net, O.widen_design(xd[s].astype(np.complex128)))
+            wdev = np.max(np.abs(out.w0[s, k] - lls.w)) / np.max(np.abs(lls.w))
+            dev = np.max(np.abs(out.soft[s, k] - ref)) / max(1.0, np.max(np.abs(ref)))
+            record("jacobi_path_training", config=f"slot={s} user={k}", soft_dev=dev, w0_dev=wdev)
+            assert wdev < 1e-10, (s, k, wdev)
+            assert dev < (1e-4 if s == 0 else 2e-2), (s, k, dev)
+
+
 def test_ill_conditioned_slot_is_flagged(A, O):
     # duplicate antennas -> rank-deficient complex design; random targets are
     # inconsistent -> status ILL for every user, no training for them.
