@@ -398,10 +398,11 @@ __global__ void __launch_bounds__(NW * 32, 1) train_lat_kernel(TrainParams p, La
     // forward thread map: KSF k-split lanes x 32 row quads x NW / KSF neuron
     // groups; after the k reduce-scatter a lane holds FV values (neuron fj,
     // rows 4 frq + fr ..), or -- with fewer values than lanes -- one value on
-    // KSF / FVV lanes.  One hidden layer on 8 warps splits k over 4 lanes and
-    // the neurons over two groups: one shuffle round less than 8 lanes, at
-    // twice the input loads, which the end-of-step preload hides.
-    constexpr int KSF = (NL == 1 && NW == 8 && JT % 2 == 0) ? 4 : 8;
+    // KSF / FVV lanes.  On 8 warps k splits over 4 lanes and the neurons over
+    // two groups: one shuffle round less than 8 lanes, at twice the input
+    // loads (C1 -1.3 %, C2 -0.9 %; for the first layer the end-of-step
+    // preload hides them).
+    constexpr int KSF = (NW == 8 && JT % 2 == 0) ? 4 : 8;
     constexpr int JPF = JT / (NW / KSF);         // neurons per forward thread
     constexpr int FVV = 4 * JPF;                 // values before the reduce
     constexpr int FV = FVV >= KSF ? FVV / KSF : 1;  // values per lane after it
