@@ -53,9 +53,9 @@ __global__ void __launch_bounds__(kT64) train_f64_kernel(TrainF64Params p) {
             boff[l] = o;
             o += g.dims[l];
         }
-        for (int l = 0; l <= N; ++l) {
+        for (int l = 0; l <= N; ++l) {  // activation rows padded by one double (banks)
             aoff[l] = a;
-            a += CH * g.dims[l];
+            a += CH * (g.dims[l] + 1);
         }
     }
     const int foff = p.ptrain - g.dims[N];
@@ -84,7 +84,7 @@ __global__ void __launch_bounds__(kT64) train_f64_kernel(TrainF64Params p) {
                     } else {
                         v = p.design[((size_t)d * n + idx) * width + c];
                     }
-                    ACT[aoff[0] + r * width + c] = v;
+                    ACT[aoff[0] + r * (width + 1) + c] = v;
                 }
                 for (int r = tid; r < cn; r += kT64) {
                     const int idx = IDX[r];
@@ -98,12 +98,14 @@ __global__ void __launch_bounds__(kT64) train_f64_kernel(TrainF64Params p) {
                     const int in = g.dims[l - 1], out = g.dims[l];
                     const double *A = ACT + aoff[l - 1], *W = TH + woff[l], *B = TH + boff[l];
                     double *Z = ACT + aoff[l];
+                    // consecutive threads take consecutive rows of one neuron: W
+                    // broadcasts, the padded activation rows hit distinct banks
                     for (int i = tid; i < cn * out; i += kT64) {
-                        const int r = i / out, j = i % out;
+                        const int j = i / cn, r = i - j * cn;
                         double s = 0.0;
-                        for (int k = 0; k < in; ++k) s += A[r * in + k] * W[j * in + k];
+                        for (int k = 0; k < in; ++k) s += A[r * (in + 1) + k] * W[j * in + k];
                         s += B[j];
-                        Z[r * out + j] = s > 0.0 ? s : 0.0;
+                        Z[r * (out + 1) + j] = s > 0.0 ? s : 0.0;
                     }
                     __syncthreads();
                 }
@@ -112,8 +114,8 @@ __global__ void __launch_bounds__(kT64) train_f64_kernel(TrainF64Params p) {
                 const double *AN = ACT + aoff[N];
                 for (int r = tid; r < cn; r += kT64) {
                     double lin = 0.0, br = 0.0;
-                    for (int c = 0; c < width; ++c) lin += ACT[aoff[0] + r * width + c] * w0[c];
-                    for (int c = 0; c < LN; ++c) br += AN[r * LN + c] * TH[foff + c];
+                    for (int c = 0; c < width; ++c) lin += ACT[aoff[0] + r * (width + 1) + c] * w0[c];
+                    for (int c = 0; c < LN; ++c) br += AN[r * (LN + 1) + c] * TH[foff + c];
                     const double res = lin + br - YB[r];
                     sq += res * res;
                     YB[r] = (2.0 / (double)bsz) * res;  // dy
@@ -122,7 +124,7 @@ __global__ void __launch_bounds__(kT64) train_f64_kernel(TrainF64Params p) {
                 // ---- final layer gradient, da = dy wf^T (hybrid_nn.cpp:99-102)
                 for (int j = tid; j < LN; j += kT64) {
                     double s = 0.0;
-                    for (int r = 0; r < cn; ++r) s += AN[r * LN + j] * YB[r];
+                    for (int r = 0; r < cn; ++r) s += AN[r * (LN + 1) + j] * YB[r];
                     GR[foff + j] += s;
                 }
                 for (int i = tid; i < cn * LN; i += kT64) DA[i] = YB[i / LN] * TH[foff + i % LN];
@@ -131,12 +133,12 @@ __global__ void __launch_bounds__(kT64) train_f64_kernel(TrainF64Params p) {
                 for (int l = N; l >= 1; --l) {
                     const int out = g.dims[l], in = g.dims[l - 1];
                     const double *A = ACT + aoff[l], *Ab = ACT + aoff[l - 1];
-                    for (int i = tid; i < cn * out; i += kT64) DZ[i] = A[i] > 0.0 ? DA[i] : 0.0;
+                    for (int i = tid; i < cn * out; i += kT64) DZ[i] = A[(i / out) * (out + 1) + i % out] > 0.0 ? DA[i] : 0.0;
                     __syncthreads();
                     for (int i = tid; i < out * in; i += kT64) {  // gW = dz^T below
                         const int j = i / in, c = i % in;
                         double s = 0.0;
-                        for (int r = 0; r < cn; ++r) s += DZ[r * out + j] * Ab[r * in + c];
+                        for (int r = 0; r < cn; ++r) s += DZ[r * out + j] * Ab[r * (in + 1) + c];
                         GR[woff[l] + i] += s;
                     }
                     for (int j = tid; j < out; j += kT64) {  // gb = colsum dz
@@ -198,7 +200,7 @@ int train_f64_launch(TrainF64Params &p, cudaStream_t st) {
     p.ptrain = trainable_count(g);
     for (int ch = 128; ch >= 8; ch /= 2) {
         int act = 0;
-        for (int l = 0; l < g.nd; ++l) act += ch * g.dims[l];
+        for (int l = 0; l < g.nd; ++l) act += ch * (g.dims[l] + 1);
         const size_t smem = (size_t)(2 * p.ptrain + act + 2 * ch * maxw + ch + kT64) * sizeof(double) +
                             ch * sizeof(int);
         if (smem <= 227 * 1024) {
