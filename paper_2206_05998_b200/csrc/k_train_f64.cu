@@ -100,12 +100,26 @@ __global__ void __launch_bounds__(kT64) train_f64_kernel(TrainF64Params p) {
                     double *Z = ACT + aoff[l];
                     // consecutive threads take consecutive rows of one neuron: W
                     // broadcasts, the padded activation rows hit distinct banks
-                    for (int i = tid; i < cn * out; i += kT64) {
-                        const int j = i / cn, r = i - j * cn;
-                        double s = 0.0;
-                        for (int k = 0; k < in; ++k) s += A[r * (in + 1) + k] * W[j * in + k];
-                        s += B[j];
-                        Z[r * (out + 1) + j] = s > 0.0 ? s : 0.0;
+                    // four outputs per thread at a time: independent FP64 chains
+                    for (int i0 = tid; i0 < cn * out; i0 += 4 * kT64) {
+                        int jj[4], rr[4];
+                        double s[4];
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) {
+                            const int i = min(i0 + u * kT64, cn * out - 1);
+                            jj[u] = i / cn;
+                            rr[u] = i - jj[u] * cn;
+                            s[u] = 0.0;
+                        }
+                        for (int k = 0; k < in; ++k)
+#pragma unroll
+                            for (int u = 0; u < 4; ++u) s[u] += A[rr[u] * (in + 1) + k] * W[jj[u] * in + k];
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) {
+                            if (i0 + u * kT64 >= cn * out) break;
+                            const double z = s[u] + B[jj[u]];
+                            Z[rr[u] * (out + 1) + jj[u]] = z > 0.0 ? z : 0.0;
+                        }
                     }
                     __syncthreads();
                 }
@@ -135,11 +149,22 @@ __global__ void __launch_bounds__(kT64) train_f64_kernel(TrainF64Params p) {
                     const double *A = ACT + aoff[l], *Ab = ACT + aoff[l - 1];
                     for (int i = tid; i < cn * out; i += kT64) DZ[i] = A[(i / out) * (out + 1) + i % out] > 0.0 ? DA[i] : 0.0;
                     __syncthreads();
-                    for (int i = tid; i < out * in; i += kT64) {  // gW = dz^T below
-                        const int j = i / in, c = i % in;
-                        double s = 0.0;
-                        for (int r = 0; r < cn; ++r) s += DZ[r * out + j] * Ab[r * (in + 1) + c];
-                        GR[woff[l] + i] += s;
+                    for (int i0 = tid; i0 < out * in; i0 += 4 * kT64) {  // gW = dz^T below
+                        int jj[4], cc[4];
+                        double s[4];
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) {
+                            const int i = min(i0 + u * kT64, out * in - 1);
+                            jj[u] = i / in;
+                            cc[u] = i - jj[u] * in;
+                            s[u] = 0.0;
+                        }
+                        for (int r = 0; r < cn; ++r)
+#pragma unroll
+                            for (int u = 0; u < 4; ++u) s[u] += DZ[r * out + jj[u]] * Ab[r * (in + 1) + cc[u]];
+#pragma unroll
+                        for (int u = 0; u < 4; ++u)
+                            if (i0 + u * kT64 < out * in) GR[woff[l] + i0 + u * kT64] += s[u];
                     }
                     for (int j = tid; j < out; j += kT64) {  // gb = colsum dz
                         double s = 0.0;
@@ -147,11 +172,22 @@ __global__ void __launch_bounds__(kT64) train_f64_kernel(TrainF64Params p) {
                         GR[boff[l] + j] += s;
                     }
                     if (l > 1) {  // da = dz W_l
-                        for (int i = tid; i < cn * in; i += kT64) {
-                            const int r = i / in, c = i % in;
-                            double s = 0.0;
-                            for (int j = 0; j < out; ++j) s += DZ[r * out + j] * TH[woff[l] + j * in + c];
-                            DA[i] = s;
+                        for (int i0 = tid; i0 < cn * in; i0 += 4 * kT64) {
+                            int rr[4], cc[4];
+                            double s[4];
+#pragma unroll
+                            for (int u = 0; u < 4; ++u) {
+                                const int i = min(i0 + u * kT64, cn * in - 1);
+                                rr[u] = i / in;
+                                cc[u] = i - rr[u] * in;
+                                s[u] = 0.0;
+                            }
+                            for (int j = 0; j < out; ++j)
+#pragma unroll
+                                for (int u = 0; u < 4; ++u) s[u] += DZ[rr[u] * out + j] * TH[woff[l] + j * in + cc[u]];
+#pragma unroll
+                            for (int u = 0; u < 4; ++u)
+                                if (i0 + u * kT64 < cn * in) DA[i0 + u * kT64] = s[u];
                         }
                     }
                     __syncthreads();
