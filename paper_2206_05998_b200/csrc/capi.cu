@@ -1348,7 +1348,7 @@ int pipeline_impl(noma_ctx_t c, const noma_net_desc *desc, const noma_train_cfg 
             tp.atab = atab;
             const bool clocks = std::getenv("NOMA_PHASE_CLOCKS") != nullptr && ch == 0;
             // [0..8) phase totals, [8..) per-warp timeline of 4 steps (latency kernel)
-            constexpr int kClk = 8 + 4 * 16 * 16;
+            constexpr int kClk = 8 + 4 * 16 * 16 + 16 * 16;
             if (clocks) tp.clocks = s.scratch<long long>(kClk);
             if (clocks && tp.clocks) cudaMemsetAsync(tp.clocks, 0, kClk * sizeof(long long), c->stream);
             if (force_generic_train()) {

@@ -315,8 +315,17 @@ __global__ void __launch_bounds__(NW * 32, 1) train_lat_kernel(TrainParams p, La
 #ifdef NOMA_PROBES
 #define NOMA_TL(PT)                                                              \
     if (tl && s >= 100 && s < 104) tl[(s - 100) * 256 + (PT)] = clock64();
+    // cross-CTA timeline (globaltimer, ns): thread 0 of the first cluster's
+    // CTAs at step 101, slots [8 + 1024 + 16 * block + PT]
+#define NOMA_GT(PT)                                                                       \
+    if (p.clocks && tid == 0 && blockIdx.x < 16 && s == 101) {                            \
+        unsigned long long gt_;                                                           \
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt_));                           \
+        p.clocks[8 + 1024 + 16 * blockIdx.x + (PT)] = (long long)gt_;                     \
+    }
 #else
 #define NOMA_TL(PT)
+#define NOMA_GT(PT)
 #endif
 
     for (int i = tid; i < c.bars; i += kLT) sm[i] = 0.0f;
@@ -445,6 +454,7 @@ __global__ void __launch_bounds__(NW * 32, 1) train_lat_kernel(TrainParams p, La
             const float *XT = sm + c.xt + buf * width * kSR;
             const int po = buf * c.npar, pn = (buf ^ 1) * c.npar;  // param copy: read, write
             NOMA_TL(0)
+            NOMA_GT(0)
             // ---- forward (hybrid_nn.cpp:60-72): all JT own neurons x 4 rows per
             // thread, k split over 8 lanes, lane reduce-scatter --------------
 static_for<1, NL + 1, 1>([&](auto LC) {
@@ -505,14 +515,18 @@ static_for<1, NL + 1, 1>([&](auto LC) {
                     // before this CTA's last read of af (the weight gradient).
                     const uint32_t lb = s2u(bars + 2 + 2 * (l - 1));
                     NOMA_TL(10)
+                    NOMA_GT(1)
                     __syncthreads();
-                    if (tid < CS) {
+                    if (tid < CS) {  // destination order rotated by rank: each CTA's copies
+                                     // do not all queue for the same peer first
+                        const uint32_t dst = (rank + tid) % CS;
                         fence_proxy_async();
-                        bulk_s2s(mapa(s2u(sm + c.af[l] + (buf * H + rank * JT) * kSR), tid), s2u(sm + c.aloc[l]),
-                                 JT * kSR * 4, mapa(lb, tid));
+                        bulk_s2s(mapa(s2u(sm + c.af[l] + (buf * H + rank * JT) * kSR), dst), s2u(sm + c.aloc[l]),
+                                 JT * kSR * 4, mapa(lb, dst));
                     }
                     mbar_wait(lb, (uint32_t)(s & 1));
                     NOMA_TL(11)
+                    NOMA_GT(2)
                     // re-arm for step s+1 (its bytes cannot land before every
                     // CTA has finished step s)
                     if (tid == 0) mbar_arm(lb, agbytes);
@@ -520,6 +534,7 @@ static_for<1, NL + 1, 1>([&](auto LC) {
             });
             NOMA_LPHASE(0)
             NOMA_TL(1)
+            NOMA_GT(3)
             __syncthreads();
             NOMA_LPHASE(1)
             NOMA_TL(2)
@@ -541,9 +556,15 @@ static_for<1, NL + 1, 1>([&](auto LC) {
                 }
                 const uint32_t la = s2u(sm + c.yall + (buf * CS + rank) * kBatchRows + r0);
 #pragma unroll
-                for (int q = warp; q < CS; q += 4) st_async4(mapa(la, q), y, mapa(ybar, q));
+                for (int q = warp; q < CS; q += 4) {
+                    // two layers: destinations rotated by rank (as the bulk
+                    // exchanges); one layer: in order (rotated measured +2 %)
+                    const uint32_t dst = NL > 1 ? (rank + q) % CS : q;
+                    st_async4(mapa(la, dst), y, mapa(ybar, dst));
+                }
             }
             NOMA_TL(3)
+            NOMA_GT(4)
             // ---- next step's minibatch tile (bulk copy, one thread off the
             // critical warps; XT[buf^1] was last read in step s-1) ------------
             if (tid == kLT - 32 && s + 1 < total) fetch(s + 1);
@@ -562,6 +583,7 @@ static_for<1, NL + 1, 1>([&](auto LC) {
                 mbar_wait(ybar, (uint32_t)((s >> 1) & 1));
                 NOMA_LPHASE(3)
                 NOMA_TL(5)
+                NOMA_GT(5)
                 const int r = tid;  // 0..127
                 const float *ya = sm + c.yall + buf * CS * kBatchRows + r;
                 float yq[CS];
@@ -636,9 +658,10 @@ static_for<NL, 0, -1>([&](auto LC) {
                     const uint32_t rb = s2u(bars + 3 + 2 * (l - 2));
                     __syncthreads();
                     if (tid < CS) {
+                        const uint32_t dst = (rank + tid) % CS;
                         fence_proxy_async();
-                        bulk_s2s(mapa(s2u(sm + c.rsb[l - 1] + rank * JT * kSR), tid),
-                                 s2u(sm + c.rsst + tid * JT * kSR), JT * kSR * 4, mapa(rb, tid));
+                        bulk_s2s(mapa(s2u(sm + c.rsb[l - 1] + rank * JT * kSR), dst),
+                                 s2u(sm + c.rsst + dst * JT * kSR), JT * kSR * 4, mapa(rb, dst));
                     }
                     NOMA_TL(12)
                 }
@@ -801,6 +824,7 @@ static_for<NL, 0, -1>([&](auto LC) {
             });
             NOMA_LPHASE(5)
             NOMA_TL(8)
+            NOMA_GT(6)
             if (s + 1 < total) load_fx(s + 1);
             __syncthreads();
             NOMA_LPHASE(6)
