@@ -448,6 +448,7 @@ void fill_train(TrainParams &tp, const NetGeom &g, const noma_train_cfg *cfg) {
     tp.clocks = nullptr;
     tp.mode = 0;
     tp.xprep = tp.r0prep = nullptr;
+    tp.agbuf = nullptr;
     tp.atab = nullptr;
     tp.prep_floats = 0;
     tp.epochs = cfg->epochs;
@@ -476,6 +477,8 @@ void prep_scratch(StageT &s, TrainParams &tp) {
     if (steps == 0 || xf > ((size_t)256 << 20)) return;
     tp.xprep = s.template scratch<float>(xf);
     tp.r0prep = s.template scratch<float>((size_t)tp.n_nets * steps * noma_dev::kBatchRows);
+    if (tp.g.nd > 2)  // the multicast all-gather of the hidden activations
+        tp.agbuf = s.template scratch<float>((size_t)tp.n_nets * 2 * tp.g.dims[1] * noma_dev::kSR);
     tp.prep_floats = tp.xprep && tp.r0prep ? xf : 0;
 }
 

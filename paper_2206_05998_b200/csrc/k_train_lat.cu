@@ -94,6 +94,18 @@ __device__ __forceinline__ void bulk_s2s(uint32_t rdst, uint32_t src, uint32_t b
         "r"(src), "r"(bytes), "r"(rbar)
         : "memory");
 }
+// Bulk async copy global -> the same shared-memory offset of every CTA in
+// `mask`, completing on each one's mbarrier at `mbar`'s offset (multicast).
+__device__ __forceinline__ void bulk_g2s_mc(uint32_t dst, const void *src, uint32_t bytes, uint32_t mbar,
+                                            uint16_t mask) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster [%0], [%1], %2, [%3], %4;" ::"r"(dst),
+        "l"(src), "r"(bytes), "r"(mbar), "h"(mask)
+        : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async_global() {
+    asm volatile("fence.proxy.async.global;" ::: "memory");
+}
 // Bulk async copy global -> this CTA's shared memory, completing on `mbar`.
 __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void *src, uint32_t bytes, uint32_t mbar) {
     asm volatile(
@@ -505,6 +517,13 @@ static_for<1, NL + 1, 1>([&](auto LC) {
                     for (int i = 0; i < FV; ++i) v[i] = fmaxf(v[i] + bj, 0.f);
                     const int r = 4 * frq + fr;
                     if (fown) sts_n<FV>((l == NL ? sm + c.aN : sm + c.aloc[l]) + fj * kSR + r, v);
+                    if (l < NL && p.agbuf) {  // staged in global for the multicast all-gather
+                        float *gt = p.agbuf + ((size_t)net * 2 + buf) * H * kSR + rank * JT * kSR;
+                        if (fown) sts_n<FV>(gt + fj * kSR + r, v);
+                        if (tid < JT * (kSR - kBatchRows))  // pad columns stay zero
+                            gt[(tid / (kSR - kBatchRows)) * kSR + kBatchRows + tid % (kSR - kBatchRows)] = 0.0f;
+                        fence_proxy_async_global();
+                    }
                 }
                 if (l < NL) {
                     // all-gather a_l: the own [JT][kSR] tile to every CTA (incl.
@@ -517,8 +536,16 @@ static_for<1, NL + 1, 1>([&](auto LC) {
                     NOMA_TL(10)
                     NOMA_GT(1)
                     __syncthreads();
-                    if (tid < CS) {  // destination order rotated by rank: each CTA's copies
-                                     // do not all queue for the same peer first
+                    if (p.agbuf) {
+                        // one multicast copy from the global staging tile into
+                        // every CTA's af slot (the SM's outbound smem -> peer
+                        // copies ran at ~16 B/clk: 34 KB per step)
+                        if (tid == 0)
+                            bulk_g2s_mc(s2u(sm + c.af[l] + (buf * H + rank * JT) * kSR),
+                                        p.agbuf + ((size_t)net * 2 + buf) * H * kSR + rank * JT * kSR,
+                                        JT * kSR * 4, lb, (uint16_t)((1u << CS) - 1));
+                    } else if (tid < CS) {  // destination order rotated by rank: each CTA's
+                                            // copies do not all queue for the same peer first
                         const uint32_t dst = (rank + tid) % CS;
                         fence_proxy_async();
                         bulk_s2s(mapa(s2u(sm + c.af[l] + (buf * H + rank * JT) * kSR), dst), s2u(sm + c.aloc[l]),

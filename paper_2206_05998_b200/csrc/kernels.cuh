@@ -42,6 +42,7 @@ struct TrainParams {
     long long *clocks;      // nullable: phase cycles of block 0 (NOMA_PHASE_CLOCKS)
     int mode;               // out: kernel shape launched (noma_ctx_train_mode codes)
     float *xprep, *r0prep;  // latency kernel: per-step minibatch tiles (scratch, nullable)
+    float *agbuf;           // latency kernel, 2+ layers: [net][2][H][kSR] all-gather staging (nullable)
     const float *atab;      // [total steps][2] Adam constants lr / c1, 1 / c2 (nullable)
     size_t prep_floats;     // capacity of xprep (floats)
 };
