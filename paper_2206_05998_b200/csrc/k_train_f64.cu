@@ -98,27 +98,38 @@ __global__ void __launch_bounds__(kT64) train_f64_kernel(TrainF64Params p) {
                     const int in = g.dims[l - 1], out = g.dims[l];
                     const double *A = ACT + aoff[l - 1], *W = TH + woff[l], *B = TH + boff[l];
                     double *Z = ACT + aoff[l];
-                    // consecutive threads take consecutive rows of one neuron: W
-                    // broadcasts, the padded activation rows hit distinct banks
-                    // four outputs per thread at a time: independent FP64 chains
-                    for (int i0 = tid; i0 < cn * out; i0 += 4 * kT64) {
-                        int jj[4], rr[4];
-                        double s[4];
+                    // register tiles of 2 rows (r, r + cn2) x 4 neurons per
+                    // thread, rows across the lanes: the padded activation rows
+                    // hit distinct banks, the weights broadcast; six loads per
+                    // eight DFMA (each output still sums k in order)
+                    const int cn2 = (cn + 1) >> 1, nq = (out + 3) >> 2;
+                    for (int t = tid; t < cn2 * nq; t += kT64) {
+                        const int rq = t % cn2, j0 = 4 * (t / cn2);
+                        const int r1 = min(rq + cn2, cn - 1);
+                        const double *a0 = A + rq * (in + 1), *a1 = A + r1 * (in + 1);
+                        const double *w[4];
 #pragma unroll
-                        for (int u = 0; u < 4; ++u) {
-                            const int i = min(i0 + u * kT64, cn * out - 1);
-                            jj[u] = i / cn;
-                            rr[u] = i - jj[u] * cn;
-                            s[u] = 0.0;
+                        for (int u = 0; u < 4; ++u) w[u] = W + min(j0 + u, out - 1) * in;
+                        double s0[4] = {0.0, 0.0, 0.0, 0.0}, s1[4] = {0.0, 0.0, 0.0, 0.0};
+                        for (int k = 0; k < in; ++k) {
+                            const double x0 = a0[k], x1 = a1[k];
+#pragma unroll
+                            for (int u = 0; u < 4; ++u) {
+                                const double wk = w[u][k];
+                                s0[u] += x0 * wk;
+                                s1[u] += x1 * wk;
+                            }
                         }
-                        for (int k = 0; k < in; ++k)
-#pragma unroll
-                            for (int u = 0; u < 4; ++u) s[u] += A[rr[u] * (in + 1) + k] * W[jj[u] * in + k];
 #pragma unroll
                         for (int u = 0; u < 4; ++u) {
-                            if (i0 + u * kT64 >= cn * out) break;
-                            const double z = s[u] + B[jj[u]];
-                            Z[rr[u] * (out + 1) + jj[u]] = z > 0.0 ? z : 0.0;
+                            const int j = j0 + u;
+                            if (j >= out) break;
+                            const double z0 = s0[u] + B[j];
+                            Z[rq * (out + 1) + j] = z0 > 0.0 ? z0 : 0.0;
+                            if (rq + cn2 < cn) {
+                                const double z1 = s1[u] + B[j];
+                                Z[(rq + cn2) * (out + 1) + j] = z1 > 0.0 ? z1 : 0.0;
+                            }
                         }
                     }
                     __syncthreads();
@@ -149,22 +160,31 @@ __global__ void __launch_bounds__(kT64) train_f64_kernel(TrainF64Params p) {
                     const double *A = ACT + aoff[l], *Ab = ACT + aoff[l - 1];
                     for (int i = tid; i < cn * out; i += kT64) DZ[i] = A[(i / out) * (out + 1) + i % out] > 0.0 ? DA[i] : 0.0;
                     __syncthreads();
-                    for (int i0 = tid; i0 < out * in; i0 += 4 * kT64) {  // gW = dz^T below
-                        int jj[4], cc[4];
-                        double s[4];
+                    {  // gW = dz^T below: tiles of 4 neurons x 2 columns (c, c + in2)
+                        const int in2 = (in + 1) >> 1, nq = (out + 3) >> 2;
+                        for (int t = tid; t < in2 * nq; t += kT64) {
+                            const int cq = t % in2, j0 = 4 * (t / in2);
+                            const int c1 = min(cq + in2, in - 1);
+                            int jj[4];
 #pragma unroll
-                        for (int u = 0; u < 4; ++u) {
-                            const int i = min(i0 + u * kT64, out * in - 1);
-                            jj[u] = i / in;
-                            cc[u] = i - jj[u] * in;
-                            s[u] = 0.0;
+                            for (int u = 0; u < 4; ++u) jj[u] = min(j0 + u, out - 1);
+                            double s0[4] = {0.0, 0.0, 0.0, 0.0}, s1[4] = {0.0, 0.0, 0.0, 0.0};
+                            for (int r = 0; r < cn; ++r) {
+                                const double b0 = Ab[r * (in + 1) + cq], b1 = Ab[r * (in + 1) + c1];
+#pragma unroll
+                                for (int u = 0; u < 4; ++u) {
+                                    const double zq = DZ[r * out + jj[u]];
+                                    s0[u] += zq * b0;
+                                    s1[u] += zq * b1;
+                                }
+                            }
+#pragma unroll
+                            for (int u = 0; u < 4; ++u) {
+                                if (j0 + u >= out) break;
+                                GR[woff[l] + (j0 + u) * in + cq] += s0[u];
+                                if (cq + in2 < in) GR[woff[l] + (j0 + u) * in + cq + in2] += s1[u];
+                            }
                         }
-                        for (int r = 0; r < cn; ++r)
-#pragma unroll
-                            for (int u = 0; u < 4; ++u) s[u] += DZ[r * out + jj[u]] * Ab[r * (in + 1) + cc[u]];
-#pragma unroll
-                        for (int u = 0; u < 4; ++u)
-                            if (i0 + u * kT64 < out * in) GR[woff[l] + i0 + u * kT64] += s[u];
                     }
                     for (int j = tid; j < out; j += kT64) {  // gb = colsum dz
                         double s = 0.0;
@@ -172,22 +192,31 @@ __global__ void __launch_bounds__(kT64) train_f64_kernel(TrainF64Params p) {
                         GR[boff[l] + j] += s;
                     }
                     if (l > 1) {  // da = dz W_l
-                        for (int i0 = tid; i0 < cn * in; i0 += 4 * kT64) {
-                            int rr[4], cc[4];
-                            double s[4];
+                        // tiles of 4 rows x 2 columns (c, c + in2), columns across
+                        // the lanes (contiguous weight reads), dz broadcast
+                        const int in2 = (in + 1) >> 1, rq4 = (cn + 3) >> 2;
+                        for (int t = tid; t < in2 * rq4; t += kT64) {
+                            const int cq = t % in2, r0 = 4 * (t / in2);
+                            const int c1 = min(cq + in2, in - 1);
+                            int rr[4];
+#pragma unroll
+                            for (int u = 0; u < 4; ++u) rr[u] = min(r0 + u, cn - 1);
+                            double s0[4] = {0.0, 0.0, 0.0, 0.0}, s1[4] = {0.0, 0.0, 0.0, 0.0};
+                            for (int j = 0; j < out; ++j) {
+                                const double t0 = TH[woff[l] + j * in + cq], t1 = TH[woff[l] + j * in + c1];
+#pragma unroll
+                                for (int u = 0; u < 4; ++u) {
+                                    const double zq = DZ[rr[u] * out + j];
+                                    s0[u] += zq * t0;
+                                    s1[u] += zq * t1;
+                                }
+                            }
 #pragma unroll
                             for (int u = 0; u < 4; ++u) {
-                                const int i = min(i0 + u * kT64, cn * in - 1);
-                                rr[u] = i / in;
-                                cc[u] = i - rr[u] * in;
-                                s[u] = 0.0;
+                                if (r0 + u >= cn) break;
+                                DA[(r0 + u) * in + cq] = s0[u];
+                                if (cq + in2 < in) DA[(r0 + u) * in + cq + in2] = s1[u];
                             }
-                            for (int j = 0; j < out; ++j)
-#pragma unroll
-                                for (int u = 0; u < 4; ++u) s[u] += DZ[rr[u] * out + j] * TH[woff[l] + j * in + cc[u]];
-#pragma unroll
-                            for (int u = 0; u < 4; ++u)
-                                if (i0 + u * kT64 < cn * in) DA[i0 + u * kT64] = s[u];
                         }
                     }
                     __syncthreads();
