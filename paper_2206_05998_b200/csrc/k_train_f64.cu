@@ -234,13 +234,27 @@ __global__ void __launch_bounds__(kT64) train_f64_kernel(TrainF64Params p) {
             ++step;
             const double corr1 = 1.0 - pow(p.b1, (double)step);
             const double corr2 = 1.0 - pow(p.b2, (double)step);
-            for (int i = tid; i < p.ptrain; i += kT64) {
-                const double gi = GR[i];
-                const double a = p.b1 * m1[i] + (1.0 - p.b1) * gi;
-                const double b = p.b2 * m2[i] + (1.0 - p.b2) * (gi * gi);
-                m1[i] = a;
-                m2[i] = b;
-                TH[i] -= p.lr * (a / corr1) / (sqrt(b / corr2) + p.eps);
+            // moments live in global memory (L2): four parameters per thread
+            // at a time so that their eight loads are in flight together
+            for (int i0 = tid; i0 < p.ptrain; i0 += 4 * kT64) {
+                double pm1[4], pm2[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int i = min(i0 + u * kT64, p.ptrain - 1);
+                    pm1[u] = m1[i];
+                    pm2[u] = m2[i];
+                }
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int i = i0 + u * kT64;
+                    if (i >= p.ptrain) break;
+                    const double gi = GR[i];
+                    const double a = p.b1 * pm1[u] + (1.0 - p.b1) * gi;
+                    const double b = p.b2 * pm2[u] + (1.0 - p.b2) * (gi * gi);
+                    m1[i] = a;
+                    m2[i] = b;
+                    TH[i] -= p.lr * (a / corr1) / (sqrt(b / corr2) + p.eps);
+                }
             }
             __syncthreads();
         }
