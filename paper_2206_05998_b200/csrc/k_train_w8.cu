@@ -48,7 +48,8 @@ struct W8Geom {
     static constexpr int off_red = off_ks + 4 * 32 * 32 * 2;
     static constexpr int off_r0 = off_red + 4 * 2 * 64;
     static constexpr int off_loss = off_r0 + kBatchRows;
-    static constexpr int off_end = off_loss + kW8Threads;
+    static constexpr int off_gbar = off_loss + kW8Threads;  // 8-byte mbarrier (minibatch rows)
+    static constexpr int off_end = off_gbar + 2;
     static constexpr size_t bytes = (size_t)off_end * sizeof(float);
 };
 
@@ -64,6 +65,27 @@ __device__ __forceinline__ void cp4z(float *dst, const float *src, bool valid) {
 }
 __device__ __forceinline__ void cp_wait_all() {
     asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
+}
+// the minibatch rows arrive by one bulk copy each (TMA engine), counted on an
+// mbarrier: 128 copies per step instead of 4096 cp.async, which held the
+// load/store queue (lg_throttle) while Adam ran
+__device__ __forceinline__ uint32_t w8_s2u(const void *p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void w8_row_copy(float *dst, const float *src, uint32_t bytes, uint32_t bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     w8_s2u(dst)),
+                 "l"(src), "r"(bytes), "r"(bar)
+                 : "memory");
+}
+__device__ __forceinline__ void w8_bar_wait(uint32_t bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "W8_MBW_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra W8_MBW_%=;\n}" ::"r"(bar),
+        "r"(parity)
+        : "memory");
 }
 
 }  // namespace
@@ -116,20 +138,35 @@ __global__ void __launch_bounds__(kW8Threads, 1) train_w8_kernel(TrainParams p, 
     const uint16_t *permn = p.perm + (size_t)net * p.epochs * n;
     const float *wrow = wide + (size_t)d * n * IN;
     const float *r0n = p.r0 + (size_t)net * n;
-    // minibatch copy: two threads per widened row (64 columns each), zeros past
-    // the batch end (hybrid_nn.cpp:180-187); the even thread also copies r0
-    const int grow = tid >> 1, ghalf = tid & 1;
-    auto gather = [&](int idx, bool valid) {
-        const float *src = wrow + (size_t)idx * IN + 64 * ghalf;
-        float *dst = X + grow * G::XS + 64 * ghalf;
-#pragma unroll
-        for (int c = 0; c < 64; c += 4) cp16z(dst + c, src + c, valid);
-        if (!ghalf) cp4z(R0 + grow, r0n + idx, valid);
+    // minibatch copy (hybrid_nn.cpp:180-187): thread r < 128 copies widened row
+    // r (one bulk copy) and its r0 (cp.async, zero past the batch end); rows
+    // past the batch end keep the previous, finite values -- their dZ is zero
+    // -- and start as zeros
+    const uint32_t gbar = w8_s2u(sm + G::off_gbar);
+    const int grow = tid;
+    for (int i = tid; i < kBatchRows * G::XS; i += kW8Threads) X[i] = 0.0f;
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // before the bulk copies overwrite
+    if (tid == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(gbar) : "memory");
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    auto gather = [&](int idx, int nrows) {  // every thread; nrows valid rows
+        if (tid == 0)
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(gbar),
+                         "r"((uint32_t)nrows * IN * 4)
+                         : "memory");
+        if (grow < nrows) w8_row_copy(X + grow * G::XS, wrow + (size_t)idx * IN, IN * 4, gbar);
+        if (grow < kBatchRows) cp4z(R0 + grow, r0n + idx, grow < nrows);
     };
+    uint32_t gphase = 0;
     {
-        const int b0 = min(p.batch, n);
-        const bool v = grow < b0 && p.epochs > 0;
-        gather(v ? permn[grow] : 0, v);
+        const int b0 = p.epochs > 0 ? min(p.batch, n) : 0;
+        if (b0 > 0) {
+            gather(grow < b0 ? permn[grow] : 0, b0);
+            w8_bar_wait(gbar, gphase);
+            gphase ^= 1;
+        }
         cp_wait_all();
     }
     __syncthreads();
@@ -348,7 +385,7 @@ __global__ void __launch_bounds__(kW8Threads, 1) train_w8_kernel(TrainParams p, 
             __syncthreads();  // X and DZ are dead
 
             // ---- next minibatch in flight while Adam runs ---------------------
-            if (nb > 0) gather(nidx, grow < nb);
+            if (nb > 0) gather(nidx, nb);
 
             // ---- Adam (hybrid_nn.cpp:118-144), FP32 moments in registers -----
 #pragma unroll
@@ -379,6 +416,10 @@ __global__ void __launch_bounds__(kW8Threads, 1) train_w8_kernel(TrainParams p, 
                 *tp -= adam_step(lrc * mb, vb * ic2, p.eps);
             }
             cp_wait_all();
+            if (nb > 0) {
+                w8_bar_wait(gbar, gphase);
+                gphase ^= 1;
+            }
             ++step;
             __syncthreads();
         }
