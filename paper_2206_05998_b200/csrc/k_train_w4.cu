@@ -55,15 +55,11 @@ struct W4Geom {
     static constexpr int off_red = off_dz + 32 * DS;   // [warp][gf | gb][64]
     static constexpr int off_r0 = off_red + 4 * 2 * 64;
     static constexpr int off_loss = off_r0 + kBatchRows;
-    static constexpr int off_end = off_loss + kBatchRows;
+    static constexpr int off_gbar = off_loss + kBatchRows;  // 8-byte mbarrier (minibatch rows)
+    static constexpr int off_end = off_gbar + 2;
     static constexpr size_t bytes = (size_t)off_end * sizeof(float);
 };
 
-__device__ __forceinline__ void cp16_zfill(float *dst, const float *src, bool valid) {
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"((unsigned)__cvta_generic_to_shared(dst)),
-                 "l"(src), "r"(valid ? 16 : 0)
-                 : "memory");
-}
 __device__ __forceinline__ void cp4_zfill(float *dst, const float *src, bool valid) {
     asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"((unsigned)__cvta_generic_to_shared(dst)),
                  "l"(src), "r"(valid ? 4 : 0)
@@ -71,6 +67,26 @@ __device__ __forceinline__ void cp4_zfill(float *dst, const float *src, bool val
 }
 __device__ __forceinline__ void cp_async_wait_all() {
     asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
+}
+// minibatch rows by one bulk copy each (TMA engine) counted on an mbarrier:
+// 128 copies per step instead of IN / 4 cp.async per thread
+__device__ __forceinline__ uint32_t w4_s2u(const void *p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void w4_row_copy(float *dst, const float *src, uint32_t bytes, uint32_t bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     w4_s2u(dst)),
+                 "l"(src), "r"(bytes), "r"(bar)
+                 : "memory");
+}
+__device__ __forceinline__ void w4_bar_wait(uint32_t bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "W4_MBW_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra W4_MBW_%=;\n}" ::"r"(bar),
+        "r"(parity)
+        : "memory");
 }
 
 __device__ __forceinline__ float2 lo_hi(unsigned long long v) { return f2_unpack(v); }
@@ -137,19 +153,34 @@ __global__ void __launch_bounds__(kW4Threads, 2) train_w4_kernel(TrainParams p, 
     const uint16_t *permn = p.perm + (size_t)net * p.epochs * n;
     const float *wrow = wide + (size_t)d * n * IN;
     const float *r0n = p.r0 + (size_t)net * n;
-    // minibatch copy: thread t copies widened row perm[t] of the step (zeros
-    // past the batch end, hybrid_nn.cpp:180-187) and its r0
-    auto gather = [&](int idx, bool valid) {
-        const float *src = wrow + (size_t)idx * IN;
-        float *dst = X + tid * G::XS;
-#pragma unroll
-        for (int c = 0; c < IN; c += 4) cp16_zfill(dst + c, src + c, valid);
-        cp4_zfill(R0 + tid, r0n + idx, valid);
+    // minibatch copy (hybrid_nn.cpp:180-187): thread t copies widened row
+    // perm[t] of the step (one bulk copy) and its r0 (cp.async, zero past the
+    // batch end); rows past the batch end keep the previous, finite values --
+    // their dZ is zero -- and start as zeros
+    const uint32_t gbar = w4_s2u(sm + G::off_gbar);
+    for (int i = tid; i < kBatchRows * G::XS; i += kW4Threads) X[i] = 0.0f;
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // before the bulk copies overwrite
+    if (tid == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(gbar) : "memory");
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    auto gather = [&](int idx, int nrows) {  // every thread; nrows valid rows
+        if (tid == 0)
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(gbar),
+                         "r"((uint32_t)nrows * IN * 4)
+                         : "memory");
+        if (tid < nrows) w4_row_copy(X + tid * G::XS, wrow + (size_t)idx * IN, IN * 4, gbar);
+        cp4_zfill(R0 + tid, r0n + idx, tid < nrows);
     };
+    uint32_t gphase = 0;
     {
-        const int b0 = min(p.batch, n);
-        const bool v = tid < b0 && p.epochs > 0;
-        gather(v ? permn[tid] : 0, v);
+        const int b0 = p.epochs > 0 ? min(p.batch, n) : 0;
+        if (b0 > 0) {
+            gather(tid < b0 ? permn[tid] : 0, b0);
+            w4_bar_wait(gbar, gphase);
+            gphase ^= 1;
+        }
         cp_async_wait_all();
     }
     __syncthreads();
@@ -359,7 +390,7 @@ __global__ void __launch_bounds__(kW4Threads, 2) train_w4_kernel(TrainParams p, 
             NOMA_W4_PHASE(3)
 
             // ---- next minibatch in flight while Adam runs ---------------------
-            if (nb > 0) gather(nidx, tid < nb);
+            if (nb > 0) gather(nidx, nb);
 
             // ---- Adam (hybrid_nn.cpp:118-144), FP32 moments in registers -----
 #pragma unroll
@@ -389,6 +420,10 @@ __global__ void __launch_bounds__(kW4Threads, 2) train_w4_kernel(TrainParams p, 
                 *tp -= adam_step(lrc * mb, vb * ic2, p.eps);
             }
             cp_async_wait_all();
+            if (nb > 0) {
+                w4_bar_wait(gbar, gphase);
+                gphase ^= 1;
+            }
             ++step;
             __syncthreads();
             NOMA_W4_PHASE(4)

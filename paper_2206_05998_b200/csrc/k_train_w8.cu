@@ -53,11 +53,6 @@ struct W8Geom {
     static constexpr size_t bytes = (size_t)off_end * sizeof(float);
 };
 
-__device__ __forceinline__ void cp16z(float *dst, const float *src, bool valid) {
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"((unsigned)__cvta_generic_to_shared(dst)),
-                 "l"(src), "r"(valid ? 16 : 0)
-                 : "memory");
-}
 __device__ __forceinline__ void cp4z(float *dst, const float *src, bool valid) {
     asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"((unsigned)__cvta_generic_to_shared(dst)),
                  "l"(src), "r"(valid ? 4 : 0)
