@@ -45,15 +45,11 @@ struct W8dGeom {
     static constexpr int off_dz = off_w0 + IN;
     static constexpr int off_red = off_dz + 64 * DS;  // [8 warps][gf | gb][64]
     static constexpr int off_ls = off_red + 8 * 2 * 64;
-    static constexpr int off_end = off_ls + kW8dThreads;
+    static constexpr int off_gbar = off_ls + kW8dThreads;  // mbarrier (minibatch rows), one double
+    static constexpr int off_end = off_gbar + 1;
     static constexpr size_t bytes = (size_t)off_end * sizeof(double);
 };
 
-__device__ __forceinline__ void cp16d(double *dst, const double *src, bool valid) {
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"((unsigned)__cvta_generic_to_shared(dst)),
-                 "l"(src), "r"(valid ? 16 : 0)
-                 : "memory");
-}
 __device__ __forceinline__ void cp8d(double *dst, const double *src, bool valid) {
     asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"((unsigned)__cvta_generic_to_shared(dst)),
                  "l"(src), "r"(valid ? 8 : 0)
@@ -61,6 +57,25 @@ __device__ __forceinline__ void cp8d(double *dst, const double *src, bool valid)
 }
 __device__ __forceinline__ void cp_wait_d() {
     asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
+}
+// minibatch rows by one bulk copy each (TMA engine) counted on an mbarrier
+__device__ __forceinline__ uint32_t w8d_s2u(const void *p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void w8d_row_copy(double *dst, const double *src, uint32_t bytes, uint32_t bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     w8d_s2u(dst)),
+                 "l"(src), "r"(bytes), "r"(bar)
+                 : "memory");
+}
+__device__ __forceinline__ void w8d_bar_wait(uint32_t bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "W8D_MBW_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra W8D_MBW_%=;\n}" ::"r"(bar),
+        "r"(parity)
+        : "memory");
 }
 __device__ __forceinline__ double shfl_xor_d(double v, int o) { return __shfl_xor_sync(kFullD, v, o); }
 __device__ __forceinline__ double shfl_d(double v, int src) { return __shfl_sync(kFullD, v, src); }
@@ -116,23 +131,38 @@ __global__ void __launch_bounds__(kW8dThreads, 1)
     // row's target (hybrid_nn.cpp:180-187); zeros past the batch end
     const uint16_t *permn = p.perm + (size_t)net * p.epochs * n;
     const double *wrow = wide + (size_t)d * n * IN;
-    const int grow = tid >> 1, ghalf = tid & 1;
+    const int grow = tid;  // thread r < 128: row r (one bulk copy) and its target
     auto target = [&](int row) -> const double * {
         return p.layout == NOMA_LAYOUT_WIDEN_COMPLEX
                    ? p.targets + (((size_t)d * (n / 2) + (row >> 1)) * p.K + k_user) * 2 + (row & 1)
                    : p.targets + ((size_t)d * p.K + k_user) * n + row;
     };
-    auto gather = [&](int idx, bool valid) {
-        const double *src = wrow + (size_t)idx * IN + (IN / 2) * ghalf;
-        double *dst = X + grow * G::XS + (IN / 2) * ghalf;
-#pragma unroll
-        for (int c = 0; c < IN / 2; c += 2) cp16d(dst + c, src + c, valid);
-        if (!ghalf) cp8d(Y + grow, target(valid ? idx : 0), valid);
+    // rows past the batch end keep the previous, finite values (their dZ is
+    // zero) and start as zeros
+    const uint32_t gbar = w8d_s2u(smd + G::off_gbar);
+    for (int i = tid; i < kBatchRows * G::XS; i += kW8dThreads) X[i] = 0.0;
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // before the bulk copies overwrite
+    if (tid == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(gbar) : "memory");
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    auto gather = [&](int idx, int nrows) {  // every thread; nrows valid rows
+        if (tid == 0)
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(gbar),
+                         "r"((uint32_t)nrows * IN * 8)
+                         : "memory");
+        if (grow < nrows) w8d_row_copy(X + grow * G::XS, wrow + (size_t)idx * IN, IN * 8, gbar);
+        if (grow < kBatchRows) cp8d(Y + grow, target(grow < nrows ? idx : 0), grow < nrows);
     };
+    uint32_t gphase = 0;
     {
-        const int b0 = min(p.batch, n);
-        const bool v = grow < b0 && p.epochs > 0;
-        gather(v ? permn[grow] : 0, v);
+        const int b0 = p.epochs > 0 ? min(p.batch, n) : 0;
+        if (b0 > 0) {
+            gather(grow < b0 ? permn[grow] : 0, b0);
+            w8d_bar_wait(gbar, gphase);
+            gphase ^= 1;
+        }
         cp_wait_d();
     }
     __syncthreads();
@@ -297,7 +327,7 @@ __global__ void __launch_bounds__(kW8dThreads, 1)
             __syncthreads();  // X and DZ are dead
 
             // ---- next minibatch in flight while Adam runs ---------------------
-            if (nb > 0) gather(nidx, grow < nb);
+            if (nb > 0) gather(nidx, nb);
 
             // ---- Adam (hybrid_nn.cpp:118-124): theta -= lr (m / c1) / (sqrt(v / c2) + eps)
 #pragma unroll
@@ -325,6 +355,10 @@ __global__ void __launch_bounds__(kW8dThreads, 1)
                 th -= p.lr * (mb / c1) / (sqrt(vb / c2) + p.eps);
             }
             cp_wait_d();
+            if (nb > 0) {
+                w8d_bar_wait(gbar, gphase);
+                gphase ^= 1;
+            }
             ++step;
             __syncthreads();
         }
