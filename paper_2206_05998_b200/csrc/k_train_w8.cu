@@ -9,10 +9,13 @@
 // doubles the threads:
 //   * forward: the two warp halves split K (input columns 0-63 / 64-127) over
 //     the same 32-row block with w4's 8x8 FFMA2 tiles (4 neuron pairs x 8 rows
-//     per thread); the upper half hands its partial sums over through shared
-//     memory in a fixed order (lower + upper), so results are bit-reproducible;
-//   * residual, dZ, final-layer and bias gradients: the lower 4 warps, as in
-//     w4 (activations in registers, one barrier);
+//     per thread); the halves swap partial sums through shared memory so that
+//     each finishes half of the neuron pairs, always added lower + upper, so
+//     results are bit-reproducible;
+//   * residual, dZ, final-layer and bias gradients: every warp for its own
+//     neuron pairs (activations in registers); the halves' final-layer
+//     partials of a row meet in shared memory under a named barrier of the
+//     warp pair;
 //   * weight gradient gW = dZ^T X: each warp owns 4 neuron pairs x all 128
 //     columns, rows in two halves exchanged by one lane-xor-16 shuffle; the
 //     thread that finishes an element owns that parameter and its Adam moments
@@ -46,7 +49,8 @@ struct W8Geom {
     static constexpr int off_dz = off_f + 64;
     static constexpr int off_ks = off_dz + 32 * DS;   // K-split partials [4][32 acc][32 lanes] f2
     static constexpr int off_red = off_ks + 4 * 32 * 32 * 2;
-    static constexpr int off_r0 = off_red + 4 * 2 * 64;
+    static constexpr int off_yx = off_red + 4 * 2 * 64;  // [2 halves][128 rows] final-layer partials
+    static constexpr int off_r0 = off_yx + 2 * kBatchRows;
     static constexpr int off_loss = off_r0 + kBatchRows;
     static constexpr int off_gbar = off_loss + kW8Threads;  // 8-byte mbarrier (minibatch rows)
     static constexpr int off_end = off_gbar + 2;
@@ -109,6 +113,7 @@ __global__ void __launch_bounds__(kW8Threads, 1) train_w8_kernel(TrainParams p, 
     float *DZ = sm + G::off_dz;
     f2_t *KS = reinterpret_cast<f2_t *>(sm + G::off_ks);
     float *RED = sm + G::off_red;
+    float *YX = sm + G::off_yx;
     float *R0 = sm + G::off_r0;
     float *LS = sm + G::off_loss;
 
@@ -223,42 +228,45 @@ __global__ void __launch_bounds__(kW8Threads, 1) train_w8_kernel(TrainParams p, 
 #undef NOMA_W8_FWD
                 }
             }
-            // upper half -> shared memory; the lower half adds (lower + upper)
-            f2_t *ks = KS + (size_t)wr * 32 * 32 + lane;
-            if (kh) {
+            // the halves swap partials: each finishes pair groups m = 2 kh,
+            // 2 kh + 1 (always lower-K + upper-K) and runs their epilogue
+            f2_t own[2][8];
+            {
+                f2_t *ks = KS + (size_t)(wr * 2 + kh) * 16 * 32 + lane;
 #pragma unroll
-                for (int m = 0; m < 4; ++m)
+                for (int mm = 0; mm < 2; ++mm)
 #pragma unroll
-                    for (int i = 0; i < 8; ++i) ks[(m * 8 + i) * 32] = acc[m][i];
-            }
-            __syncthreads();
-            if (!kh) {
+                    for (int i = 0; i < 8; ++i) ks[(mm * 8 + i) * 32] = kh ? acc[mm][i] : acc[2 + mm][i];
+                __syncthreads();
+                const f2_t *kr = KS + (size_t)(wr * 2 + (kh ^ 1)) * 16 * 32 + lane;
 #pragma unroll
-                for (int m = 0; m < 4; ++m)
+                for (int mm = 0; mm < 2; ++mm)
 #pragma unroll
                     for (int i = 0; i < 8; ++i) {
-                        const float2 lo = f2_unpack(acc[m][i]), hi = f2_unpack(ks[(m * 8 + i) * 32]);
-                        acc[m][i] = f2_pack(lo.x + hi.x, lo.y + hi.y);
+                        const float2 mine = f2_unpack(kh ? acc[2 + mm][i] : acc[mm][i]);
+                        const float2 other = f2_unpack(kr[(mm * 8 + i) * 32]);
+                        own[mm][i] = kh ? f2_pack(other.x + mine.x, other.y + mine.y)
+                                        : f2_pack(mine.x + other.x, mine.y + other.y);
                     }
-                // ReLU; the final dot a . w_final (hybrid_nn.cpp:81) per row
+            }
+            {
                 float yp[8];
 #pragma unroll
                 for (int i = 0; i < 8; ++i) yp[i] = 0.f;
 #pragma unroll
-                for (int m = 0; m < 4; ++m) {
-                    const float2 fw = *reinterpret_cast<const float2 *>(F + 2 * (l8 + 8 * m));
+                for (int mm = 0; mm < 2; ++mm) {
+                    const float2 fw = *reinterpret_cast<const float2 *>(F + 2 * (l8 + 8 * (2 * kh + mm)));
 #pragma unroll
                     for (int i = 0; i < 8; ++i) {
-                        float2 a = f2_unpack(acc[m][i]);
+                        float2 a = f2_unpack(own[mm][i]);
                         a.x = fmaxf(a.x, 0.f);
                         a.y = fmaxf(a.y, 0.f);
-                        acc[m][i] = f2_pack(a.x, a.y);
+                        own[mm][i] = f2_pack(a.x, a.y);
                         yp[i] = fmaf(fw.x, a.x, yp[i]);
                         yp[i] = fmaf(fw.y, a.y, yp[i]);
                     }
                 }
-                // reduce-scatter of the 8 row partials over the quarter's 8 lanes
-                float yhat;
+                float yhalf;
                 {
                     const bool b4 = l8 & 4, b2 = l8 & 2, b1 = l8 & 1;
                     float y4[4];
@@ -277,51 +285,54 @@ __global__ void __launch_bounds__(kW8Threads, 1) train_w8_kernel(TrainParams p, 
                     }
                     const float send = b1 ? y2[0] : y2[1];
                     const float keep = b1 ? y2[1] : y2[0];
-                    yhat = keep + __shfl_xor_sync(kFull8, send, 1);
+                    yhalf = keep + __shfl_xor_sync(kFull8, send, 1);
                 }
-                // residual a.w_f - r0 (hybrid_nn.cpp:94), dy = 2r/B (:98)
+                YX[kh * kBatchRows + rr_own] = yhalf;
+                asm volatile("bar.sync %0, 64;" ::"r"(1 + wr) : "memory");
+                const float yhat = YX[rr_own] + YX[kBatchRows + rr_own];
                 const bool own_valid = rr_own < bsz;
                 const float res = own_valid ? yhat - R0[rr_own] : 0.f;
                 const float dy_own = (2.0f / (float)bsz) * res;
-                lossacc = fmaf(res, res, lossacc);
+                if (!kh) lossacc = fmaf(res, res, lossacc);
                 float dy[8];
 #pragma unroll
                 for (int i = 0; i < 8; ++i) dy[i] = __shfl_sync(kFull8, dy_own, (lane & 24) | i);
-                // dZ (:102, :107), g_final (:99), g_b (:110) partials over 8 rows
-                float2 gf[4], gb[4];
+                float2 gf[2], gb[2];
 #pragma unroll
-                for (int m = 0; m < 4; ++m) {
-                    const float2 fw = *reinterpret_cast<const float2 *>(F + 2 * (l8 + 8 * m));
-                    gf[m] = gb[m] = make_float2(0.f, 0.f);
-                    float *dzrow = DZ + (l8 + 8 * m) * G::DS + 2 * (32 * wr + q);
+                for (int mm = 0; mm < 2; ++mm) {
+                    const int jp = l8 + 8 * (2 * kh + mm);
+                    const float2 fw = *reinterpret_cast<const float2 *>(F + 2 * jp);
+                    gf[mm] = gb[mm] = make_float2(0.f, 0.f);
+                    float *dzrow = DZ + jp * G::DS + 2 * (32 * wr + q);
 #pragma unroll
                     for (int i = 0; i < 8; ++i) {
-                        const float2 a = f2_unpack(acc[m][i]);
+                        const float2 a = f2_unpack(own[mm][i]);
                         const float2 z =
                             make_float2(a.x > 0.f ? dy[i] * fw.x : 0.f, a.y > 0.f ? dy[i] * fw.y : 0.f);
-                        gf[m].x = fmaf(a.x, dy[i], gf[m].x);
-                        gf[m].y = fmaf(a.y, dy[i], gf[m].y);
-                        gb[m].x += z.x;
-                        gb[m].y += z.y;
+                        gf[mm].x = fmaf(a.x, dy[i], gf[mm].x);
+                        gf[mm].y = fmaf(a.y, dy[i], gf[mm].y);
+                        gb[mm].x += z.x;
+                        gb[mm].y += z.y;
                         *reinterpret_cast<float2 *>(dzrow + 8 * i) = z;
                     }
                 }
 #pragma unroll
-                for (int m = 0; m < 4; ++m) {
-                    gf[m].x += __shfl_xor_sync(kFull8, gf[m].x, 8);
-                    gf[m].y += __shfl_xor_sync(kFull8, gf[m].y, 8);
-                    gb[m].x += __shfl_xor_sync(kFull8, gb[m].x, 8);
-                    gb[m].y += __shfl_xor_sync(kFull8, gb[m].y, 8);
-                    gf[m].x += __shfl_xor_sync(kFull8, gf[m].x, 16);
-                    gf[m].y += __shfl_xor_sync(kFull8, gf[m].y, 16);
-                    gb[m].x += __shfl_xor_sync(kFull8, gb[m].x, 16);
-                    gb[m].y += __shfl_xor_sync(kFull8, gb[m].y, 16);
+                for (int mm = 0; mm < 2; ++mm) {
+                    gf[mm].x += __shfl_xor_sync(kFull8, gf[mm].x, 8);
+                    gf[mm].y += __shfl_xor_sync(kFull8, gf[mm].y, 8);
+                    gb[mm].x += __shfl_xor_sync(kFull8, gb[mm].x, 8);
+                    gb[mm].y += __shfl_xor_sync(kFull8, gb[mm].y, 8);
+                    gf[mm].x += __shfl_xor_sync(kFull8, gf[mm].x, 16);
+                    gf[mm].y += __shfl_xor_sync(kFull8, gf[mm].y, 16);
+                    gb[mm].x += __shfl_xor_sync(kFull8, gb[mm].x, 16);
+                    gb[mm].y += __shfl_xor_sync(kFull8, gb[mm].y, 16);
                 }
                 if (q == 0) {
 #pragma unroll
-                    for (int m = 0; m < 4; ++m) {
-                        *reinterpret_cast<float2 *>(RED + wr * 128 + 2 * (l8 + 8 * m)) = gf[m];
-                        *reinterpret_cast<float2 *>(RED + wr * 128 + 64 + 2 * (l8 + 8 * m)) = gb[m];
+                    for (int mm = 0; mm < 2; ++mm) {
+                        const int jp = l8 + 8 * (2 * kh + mm);
+                        *reinterpret_cast<float2 *>(RED + wr * 128 + 2 * jp) = gf[mm];
+                        *reinterpret_cast<float2 *>(RED + wr * 128 + 64 + 2 * jp) = gb[mm];
                     }
                 }
             }
