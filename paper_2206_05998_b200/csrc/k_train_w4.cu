@@ -15,7 +15,8 @@
 //   * Adam moments live in registers for the whole training: the thread that
 //     finishes a weight-gradient element owns that parameter, so no gradient
 //     buffer and no moment traffic;
-//   * the minibatch is copied with cp.async from a pre-widened FP32 design
+//   * the minibatch is copied by one bulk copy per row (TMA engine, counted on
+//     an mbarrier) from a pre-widened FP32 design
 //     (rows 2t = [Re x_t; Im x_t], 2t+1 = [Im x_t; -Re x_t], iq_transform.cpp:
 //     17-20) straight into a row-major tile while the previous step's Adam
 //     runs -- no transposition, no registers;
@@ -453,7 +454,7 @@ __global__ void __launch_bounds__(kW4Threads, 2) train_w4_kernel(TrainParams p, 
     }
 }
 
-// Widened FP32 design rows for the cp.async gather: row 2t = [Re x_t | Im x_t]
+// Widened FP32 design rows for the minibatch gather: row 2t = [Re x_t | Im x_t]
 // (the LLS kernel's FP32 copy), row 2t+1 = [Im x_t | -Re x_t].
 __global__ void widen_rows_kernel(const float *__restrict__ d32, float *__restrict__ wide, size_t nrow_c,
                                   int width) {

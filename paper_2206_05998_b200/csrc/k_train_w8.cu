@@ -20,8 +20,8 @@
 //     columns, rows in two halves exchanged by one lane-xor-16 shuffle; the
 //     thread that finishes an element owns that parameter and its Adam moments
 //     (registers) for the whole training;
-//   * the next minibatch arrives by cp.async (two threads per row) while Adam
-//     runs.
+//   * the next minibatch arrives by one bulk copy per row (mbarrier) while
+//     Adam runs.
 // One CTA (8 warps, ~170 KB) per SM.  FP32 FMA throughout; the frozen branch
 // enters through r0 = y - X w0 (FP64, LLS kernel).
 #include <cstdlib>

@@ -15,8 +15,8 @@
 //     parameters and their FP64 Adam moments in registers for the whole
 //     training; biases / final weights on threads 0-127 from fixed-order warp
 //     partials;
-//   * the next minibatch's pre-widened FP64 rows arrive by cp.async while
-//     Adam runs.
+//   * the next minibatch's pre-widened FP64 rows arrive by one bulk copy
+//     each (mbarrier) while Adam runs.
 // Summation orders are fixed (bit-reproducible runs); they differ from
 // Eigen's, which FP64 absorbs (reordered-sum FP64 training stays within
 // 1e-14 of the reference, profiles/r02_precision_probe.txt).
