@@ -647,7 +647,10 @@ static_for<NL, 0, -1>([&](auto LC) {
                     // every c (4 c x 4 r per thread), sent to the owner of c.
                     const float *W = sm + po + c.w[l];
                     const uint32_t rb = s2u(bars + 3 + 2 * (l - 2));
-                    const int cq = tt >> 5, r = 4 * lane, cc = 4 * cq;
+                    // JT == 4: column quad = one peer's tile; quads rotated by rank
+                    // so the CTAs' early copies go to different peers
+                    const int cq = JT == 4 ? ((tt >> 5) + (int)rank) % (H / 4) : tt >> 5;
+                    const int r = 4 * lane, cc = 4 * cq;
                     f2_t acc[4][2];
 #pragma unroll
                     for (int q = 0; q < 4; ++q) acc[q][0] = acc[q][1] = 0ull;
@@ -677,19 +680,33 @@ static_for<NL, 0, -1>([&](auto LC) {
                         const float2 u = f2_unpack(acc[q][0]), v = f2_unpack(acc[q][1]);
                         *reinterpret_cast<float4 *>(sm + c.rsst + (cc + q) * kSR + r) = make_float4(u.x, u.y, v.x, v.y);
                     }
+                    if constexpr (JT == 4) {
+                        // reduce-scatter as soon as this warp's tile is done:
+                        // rows [cq*JT, (cq+1)*JT) of the partial to CTA cq's
+                        // slot `rank` (single-buffered: rewritten at step s+1
+                        // only after every peer has consumed step s)
+                        fence_proxy_async();
+                        __syncwarp();
+                        if (lane == 0)
+                            bulk_s2s(mapa(s2u(sm + c.rsb[l - 1] + rank * JT * kSR), cq),
+                                     s2u(sm + c.rsst + cq * JT * kSR), JT * kSR * 4, mapa(rb, cq));
+                    }
                 }
                 if (l > 1) {
                     // reduce-scatter: rows [q*JT, (q+1)*JT) of the partial to CTA
                     // q's slot `rank` (single-buffered: rewritten at step s+1 only
                     // after every peer has consumed step s, see the Y exchange)
                     const uint32_t rb = s2u(bars + 3 + 2 * (l - 2));
-                    __syncthreads();
-                    if (tid < CS) {
-                        const uint32_t dst = (rank + tid) % CS;
-                        fence_proxy_async();
-                        bulk_s2s(mapa(s2u(sm + c.rsb[l - 1] + rank * JT * kSR), dst),
-                                 s2u(sm + c.rsst + dst * JT * kSR), JT * kSR * 4, mapa(rb, dst));
+                    if constexpr (JT != 4) {
+                        __syncthreads();
+                        if (tid < CS) {
+                            const uint32_t dst = (rank + tid) % CS;
+                            fence_proxy_async();
+                            bulk_s2s(mapa(s2u(sm + c.rsb[l - 1] + rank * JT * kSR), dst),
+                                     s2u(sm + c.rsst + dst * JT * kSR), JT * kSR * 4, mapa(rb, dst));
+                        }
                     }
+                    (void)rb;
                     NOMA_TL(12)
                 }
                 // weight gradient dZ^T A (:109), bias colsum (:110), final a_N^T dy
