@@ -25,13 +25,17 @@
 //     residual, dZ and the final-layer / bias gradients need no barrier.
 //
 // Layouts (floats, shared memory):
-//   X   [128][IN+4]       minibatch rows, row-major (stride == 4 mod 32)
+//   X   [128][IN+8]       minibatch rows, row-major (stride == 8 mod 32)
 //   W2  [32][2*IN+4]      W2[jp][2c+e] = W[2jp+e][c]  (neuron pairs, FFMA2 lanes)
 //   DZ  [32][2*128+8]     DZ[jp][2r+e] = dZ[2jp+e][r]
 // Arithmetic is FP32 FMA (fma.rn.f32x2 = two IEEE FP32 FMAs); the frozen
 // linear branch enters through r0 = y - X w0, precomputed in FP64 by the LLS
 // kernel (as in k_train.cu).  Summation orders are fixed: bit-reproducible.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
 #include <cstdlib>
+#include <cstring>
 
 #include "kernels.cuh"
 #include "tiles.cuh"
@@ -45,7 +49,7 @@ constexpr unsigned kFull = 0xffffffffu;
 
 template <int IN>
 struct W4Geom {
-    static constexpr int XS = IN + 4;                  // X row stride
+    static constexpr int XS = IN + 8;                  // X row stride: == 8 mod 32, 4 rows = k x 128 B (TMA)
     static constexpr int WS = 2 * IN + 4;              // W2 row (neuron pair) stride
     static constexpr int DS = 2 * kBatchRows + 8;      // DZ row stride, == 8 mod 32
     static constexpr int off_x = 0;
@@ -80,6 +84,17 @@ __device__ __forceinline__ void w4_row_copy(float *dst, const float *src, uint32
                  "l"(src), "r"(bytes), "r"(bar)
                  : "memory");
 }
+// four widened rows by one TMA gather (tile::gather4): box [XS floats x 1 row]
+// per row over a [rows][IN] tensor map, so the XS - IN pad columns come back
+// as out-of-bounds zeros and the tile keeps its padded row stride
+__device__ __forceinline__ void w4_gather4(float *dst, const CUtensorMap *tm, int r0, int r1, int r2, int r3,
+                                           uint32_t bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(w4_s2u(dst)),
+        "l"(reinterpret_cast<uint64_t>(tm)), "r"(0), "r"(r0), "r"(r1), "r"(r2), "r"(r3), "r"(bar)
+        : "memory");
+}
 __device__ __forceinline__ void w4_bar_wait(uint32_t bar, uint32_t parity) {
     asm volatile(
         "{\n\t.reg .pred p;\n"
@@ -103,8 +118,9 @@ __device__ __forceinline__ float2 lo_hi(unsigned long long v) { return f2_unpack
 //            the two halves add through one lane-xor-16 exchange and each keeps
 //            half of the columns: those parameters (and their Adam moments)
 //            belong to the thread for the whole training.
-template <int IN>
-__global__ void __launch_bounds__(kW4Threads, 2) train_w4_kernel(TrainParams p, const float *__restrict__ wide) {
+template <int IN, bool G4>
+__global__ void __launch_bounds__(kW4Threads, 2)
+    train_w4_kernel(TrainParams p, const float *__restrict__ wide, const __grid_constant__ CUtensorMap tmap) {
     using G = W4Geom<IN>;
     constexpr int NG = IN / 32;  // 32-column groups per gradient thread
     constexpr int NU = 4 * NG;   // gradient columns per thread before the exchange
@@ -167,11 +183,33 @@ __global__ void __launch_bounds__(kW4Threads, 2) train_w4_kernel(TrainParams p, 
     }
     __syncthreads();
     auto gather = [&](int idx, int nrows) {  // every thread; nrows valid rows
-        if (tid == 0)
-            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(gbar),
-                         "r"((uint32_t)nrows * IN * 4)
-                         : "memory");
-        if (tid < nrows) w4_row_copy(X + tid * G::XS, wrow + (size_t)idx * IN, IN * 4, gbar);
+        if constexpr (G4) {
+            // groups of four rows; a short last group repeats its last valid
+            // row (finite values with dZ = 0).  Lane 0 of each warp issues
+            // its warp's groups.
+            const int ng = (nrows + 3) >> 2;
+            if (tid == 0)
+                asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(gbar),
+                             "r"((uint32_t)ng * 4 * G::XS * 4)
+                             : "memory");
+            const int grow = d * n + idx;
+#pragma unroll
+            for (int gq = 0; gq < 8; ++gq) {
+                const int base = 32 * warp + 4 * gq;
+                const int last = nrows - 1 - 32 * warp;
+                const int r0 = __shfl_sync(kFull, grow, min(4 * gq, last));
+                const int r1 = __shfl_sync(kFull, grow, min(4 * gq + 1, last));
+                const int r2 = __shfl_sync(kFull, grow, min(4 * gq + 2, last));
+                const int r3 = __shfl_sync(kFull, grow, min(4 * gq + 3, last));
+                if (lane == 0 && base < nrows) w4_gather4(X + base * G::XS, &tmap, r0, r1, r2, r3, gbar);
+            }
+        } else {
+            if (tid == 0)
+                asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(gbar),
+                             "r"((uint32_t)nrows * IN * 4)
+                             : "memory");
+            if (tid < nrows) w4_row_copy(X + tid * G::XS, wrow + (size_t)idx * IN, IN * 4, gbar);
+        }
         cp4_zfill(R0 + tid, r0n + idx, tid < nrows);
     };
     uint32_t gphase = 0;
@@ -474,6 +512,25 @@ int widen_rows_launch(const float *d32, float *wide, size_t nrow_c, int width, c
     return cudaGetLastError() == cudaSuccess ? NOMA_OK : NOMA_ERR_CUDA;
 }
 
+bool tensor_map_encode_tiled(CUtensorMap *tm, CUtensorMapDataType dt, int rank, void *base, const cuuint64_t *gdim,
+                             const cuuint64_t *gstride, const cuuint32_t *box, const cuuint32_t *estride) {
+    using Fn = CUresult (*)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
+                            const cuuint64_t *, const cuuint32_t *, const cuuint32_t *, CUtensorMapInterleave,
+                            CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+    static Fn fn = [] {
+        void *f = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            f = nullptr;
+        return reinterpret_cast<Fn>(f);
+    }();
+    if (!fn) return false;
+    return fn(tm, dt, (cuuint32_t)rank, base, gdim, gstride, box, estride, CU_TENSOR_MAP_INTERLEAVE_NONE,
+              CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 // 1 hidden layer of 64, input 32 or 64, minibatch <= 128: the 4-warp kernel.
 bool train_w4_fits(const TrainParams &p) {
     const NetGeom &g = p.g;
@@ -494,15 +551,32 @@ int train_w4_launch(TrainParams &p, cudaStream_t st) {
         wide = tmp;
     }
     int rc = NOMA_OK;
+    // tensor map over the widened rows [designs * rows][IN] for the gather4
+    // path (NOMA_W4_GATHER4=0: one bulk copy per row)
+    CUtensorMap tmap;
+    std::memset(&tmap, 0, sizeof(tmap));
+    const char *ge = std::getenv("NOMA_W4_GATHER4");
+    bool g4 = !(ge && std::atoi(ge) == 0);
+    const size_t total_rows = (size_t)((p.n_nets + p.K - 1) / p.K) * p.rows;
+    if (g4 && total_rows > 0x7fffffffu) g4 = false;
+    if (g4) {
+        const int XS = IN == 32 ? W4Geom<32>::XS : W4Geom<64>::XS;
+        const cuuint64_t gdim[2] = {(cuuint64_t)IN, (cuuint64_t)total_rows};
+        const cuuint64_t gstride[1] = {(cuuint64_t)IN * sizeof(float)};
+        const cuuint32_t box[2] = {(cuuint32_t)XS, 1};
+        const cuuint32_t estr[2] = {1, 1};
+        g4 = tensor_map_encode_tiled(&tmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float *>(wide), gdim,
+                                     gstride, box, estr);
+    }
     auto go = [&](auto kern, size_t smem) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        kern<<<p.n_nets, kW4Threads, smem, st>>>(p, wide);
+        kern<<<p.n_nets, kW4Threads, smem, st>>>(p, wide, tmap);
         rc = cudaGetLastError() == cudaSuccess ? NOMA_OK : NOMA_ERR_CUDA;
     };
     if (IN == 32)
-        go(train_w4_kernel<32>, W4Geom<32>::bytes);
+        g4 ? go(train_w4_kernel<32, true>, W4Geom<32>::bytes) : go(train_w4_kernel<32, false>, W4Geom<32>::bytes);
     else
-        go(train_w4_kernel<64>, W4Geom<64>::bytes);
+        g4 ? go(train_w4_kernel<64, true>, W4Geom<64>::bytes) : go(train_w4_kernel<64, false>, W4Geom<64>::bytes);
     if (tmp) cudaFreeAsync(tmp, st);
     p.mode = 3;
     return rc;

@@ -2,6 +2,8 @@
 // the kernel translation units and the C-ABI in capi.cu).
 #pragma once
 
+#include <cuda.h>
+
 #include "common.cuh"
 
 namespace noma_dev {
@@ -159,6 +161,10 @@ int train_launch(TrainParams &p, cudaStream_t st);
 int train_lat_launch(TrainParams &p, cudaStream_t st);
 bool train_w4_fits(const TrainParams &p);
 int train_w4_launch(TrainParams &p, cudaStream_t st);
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no libcuda
+// link); no swizzle / interleave, zero fill out of bounds.  false on failure.
+bool tensor_map_encode_tiled(CUtensorMap *tm, CUtensorMapDataType dt, int rank, void *base, const cuuint64_t *gdim,
+                             const cuuint64_t *gstride, const cuuint32_t *box, const cuuint32_t *estride);
 bool train_w8_fits(const TrainParams &p);
 int train_w8_launch(TrainParams &p, cudaStream_t st);
 int adam_table_launch(double lr, double b1, double b2, int total, float *t, cudaStream_t st);
