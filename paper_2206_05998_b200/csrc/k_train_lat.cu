@@ -129,28 +129,28 @@ __device__ __forceinline__ void sts_n(float *p, const float *v) {
 }
 
 // In-register reduce-scatter of V values (v[0..V)) over a group of LANES
-// lanes (aligned, xor offsets LANES/2 .. 1).  Halving rounds split the value
-// range on the lane bits from the top; once one value is left the remaining
-// rounds are xor sums.  Afterwards v[0 .. max(1, V/LANES)) hold the lane's
-// values: block (lane & (LANES-1)) of V/LANES values if V >= LANES, else the
-// full sum of value index (lane & (LANES-1)) >> log2(LANES/V), replicated on
-// LANES/V lanes.  Fixed summation tree: deterministic.
-template <int N, int V, int LANES>
+// lanes spaced STR apart (xor offsets (LANES/2) STR .. STR).  Halving rounds
+// split the value range on the group-index bits from the top; once one value
+// is left the remaining rounds are xor sums.  Afterwards v[0 .. max(1,
+// V/LANES)) hold the lane's values: block g of V/LANES values if V >= LANES,
+// else the full sum of value index g >> log2(LANES/V), replicated on LANES/V
+// lanes (g = (lane / STR) & (LANES-1)).  Fixed summation tree: deterministic.
+template <int N, int V, int LANES, int STR = 1>
 __device__ __forceinline__ void reduce_scatter(float (&v)[N], int lane) {
     if constexpr (LANES > 1) {
         constexpr int O = LANES / 2;
         if constexpr (V > 1) {
-            const bool h = lane & O;
+            const bool h = lane & (O * STR);
 #pragma unroll
             for (int i = 0; i < V / 2; ++i) {
                 const float snd = h ? v[i] : v[i + V / 2];
                 const float keep = h ? v[i + V / 2] : v[i];
-                v[i] = keep + __shfl_xor_sync(0xffffffffu, snd, O);
+                v[i] = keep + __shfl_xor_sync(0xffffffffu, snd, O * STR);
             }
-            reduce_scatter<N, V / 2, O>(v, lane);
+            reduce_scatter<N, V / 2, O, STR>(v, lane);
         } else {
-            v[0] += __shfl_xor_sync(0xffffffffu, v[0], O);
-            reduce_scatter<N, 1, O>(v, lane);
+            v[0] += __shfl_xor_sync(0xffffffffu, v[0], O * STR);
+            reduce_scatter<N, 1, O, STR>(v, lane);
         }
     }
 }
@@ -427,7 +427,13 @@ __global__ void __launch_bounds__(NW * 32, 1) train_lat_kernel(TrainParams p, La
     constexpr int JPF = JT / (NW / KSF);         // neurons per forward thread
     constexpr int FVV = 4 * JPF;                 // values before the reduce
     constexpr int FV = FVV >= KSF ? FVV / KSF : 1;  // values per lane after it
-    const int fkq = tid & (KSF - 1), frq = (tid / KSF) & 31, fjh = tid / (KSF * 32);
+    // The KSF k lanes of a row quad sit STR = 32 / KSF lanes apart, so the 8
+    // lanes of a 16-byte load phase read 8 consecutive row quads of one
+    // k-quad: bank groups (4 kc + kk + frq) mod 8 all differ.  (Adjacent k
+    // lanes put k-quads kc and kc + 2 in one phase -- bank groups 4 kc mod 8
+    // coincide -- a 2-way conflict on every activation load of the forward.)
+    constexpr int FSTR = 32 / KSF;
+    const int fkq = lane / FSTR, frq = (lane & (FSTR - 1)) | ((warp % KSF) * FSTR), fjh = warp / KSF;
     const int fbase = FVV >= KSF ? fkq * FV : fkq >> (ilog2c(KSF) - ilog2c(FVV));
     const bool fown = FVV >= KSF || (fkq & ((KSF / FVV) - 1)) == 0;
     const int fj = fjh * JPF + (fbase >> 2), fr = fbase & 3;
@@ -511,7 +517,7 @@ static_for<1, NL + 1, 1>([&](auto LC) {
                         v[4 * j + 2] = b.x;
                         v[4 * j + 3] = b.y;
                     }
-                    reduce_scatter<FVV, FVV, KSF>(v, lane);
+                    reduce_scatter<FVV, FVV, KSF, FSTR>(v, lane);
                     const float bj = sm[po + c.b[l] + fj];
 #pragma unroll
                     for (int i = 0; i < FV; ++i) v[i] = fmaxf(v[i] + bj, 0.f);
@@ -715,8 +721,95 @@ static_for<NL, 0, -1>([&](auto LC) {
                 constexpr int NCL = (l == 1 ? W0 : H) / 4;
                 constexpr int TPW = NCL > NW ? NCL / NW : 1;  // column tiles per warp
                 static_assert(TPW <= 2 && (NCL <= NW || NCL % NW == 0), "tile map");
+                // Two column tiles per warp (C2's second layer on 8 warps): both
+                // tiles' 2 x 4 JT sums go through ONE 32-value reduce-scatter (5
+                // dependent shuffle rounds instead of 2 x 5, and every lane then
+                // owns one weight), the dZ operands are loaded once for both, and
+                // the bias / final-weight sums ride along as in XSPREAD.
+                constexpr int NXP = (l == NL ? 2 : 1) * JT;
+                constexpr bool PAIR = TPW == 2 && 8 * JT == 32 && NXP <= NW;
+                if constexpr (PAIR) {
+                    const int r = 4 * lane;
+                    f2_t acc[2][JT][4], sb[JT], sf[JT];
 #pragma unroll
-                for (int tw = 0; tw < TPW; ++tw) {
+                    for (int j = 0; j < JT; ++j) {
+                        sb[j] = sf[j] = 0ull;
+#pragma unroll
+                        for (int q = 0; q < 4; ++q) acc[0][j][q] = acc[1][j][q] = 0ull;
+                    }
+                    ulonglong2 x[2][4];
+#pragma unroll
+                    for (int tw = 0; tw < 2; ++tw)
+#pragma unroll
+                        for (int q = 0; q < 4; ++q)
+                            x[tw][q] = *reinterpret_cast<const ulonglong2 *>(in + (4 * (warp + NW * tw) + q) * kSR + r);
+                    float4 y4 = make_float4(0.f, 0.f, 0.f, 0.f);
+                    if (top) y4 = *reinterpret_cast<const float4 *>(dyp + r);
+                    const f2_t one = f2_bcast(1.0f);
+#pragma unroll
+                    for (int j = 0; j < JT; ++j) {
+                        float4 z = *reinterpret_cast<const float4 *>(zsrc + j * kSR + r);
+                        if (top) {  // dZ_N = (a_N > 0) dy w_j on the fly (:102-107)
+                            ffma2(sf[j], f2_pack(z.x, z.y), f2_pack(y4.x, y4.y));
+                            ffma2(sf[j], f2_pack(z.z, z.w), f2_pack(y4.z, y4.w));
+                            const float f = wfp[j];
+                            z = make_float4(z.x > 0.f ? y4.x * f : 0.f, z.y > 0.f ? y4.y * f : 0.f,
+                                            z.z > 0.f ? y4.z * f : 0.f, z.w > 0.f ? y4.w * f : 0.f);
+                        }
+                        const f2_t za = f2_pack(z.x, z.y), zb = f2_pack(z.z, z.w);
+                        ffma2(sb[j], za, one);
+                        ffma2(sb[j], zb, one);
+#pragma unroll
+                        for (int tw = 0; tw < 2; ++tw)
+#pragma unroll
+                            for (int q = 0; q < 4; ++q) {
+                                ffma2(acc[tw][j][q], za, x[tw][q].x);
+                                ffma2(acc[tw][j][q], zb, x[tw][q].y);
+                            }
+                    }
+                    float gv[32];
+#pragma unroll
+                    for (int tw = 0; tw < 2; ++tw)
+#pragma unroll
+                        for (int j = 0; j < JT; ++j)
+#pragma unroll
+                            for (int q = 0; q < 4; ++q) {
+                                const float2 h = f2_unpack(acc[tw][j][q]);
+                                gv[16 * tw + 4 * j + q] = h.x + h.y;
+                            }
+                    float ex = 0.f;  // warp w < JT: bias w; JT <= w < 2 JT: final weight w - JT
+#pragma unroll
+                    for (int j = 0; j < JT; ++j) {
+                        if (warp == j) {
+                            const float2 h = f2_unpack(sb[j]);
+                            ex = h.x + h.y;
+                        }
+                        if (top && warp == JT + j) {
+                            const float2 h = f2_unpack(sf[j]);
+                            ex = h.x + h.y;
+                        }
+                    }
+                    reduce_scatter_x<32, 32, 32>(gv, ex, lane);
+                    if (warp < NXP && lane == 0) {
+                        const int off = warp < JT ? c.b[l] + warp : c.wf + warp - JT;
+                        const float m1 = p.b1 * mb[l] + p.omb1 * ex;
+                        const float m2 = p.b2 * vb[l] + p.omb2 * (ex * ex);
+                        mb[l] = m1;
+                        vb[l] = m2;
+                        sm[pn + off] = sm[po + off] - adam_step(lrc * m1, m2 * ic2, p.eps);
+                    }
+                    // lane = 16 tile + 4 j + q: weight (j, column 4 ct + q) of tile ct
+                    const int gi = lane & 15, ct = warp + NW * (lane >> 4);
+                    const int off = (gi >> 2) * sw + 4 * ct + (gi & 3);
+                    const float gsum = gv[0];
+                    const float m1 = p.b1 * mw[l][0] + p.omb1 * gsum;
+                    const float m2 = p.b2 * vw[l][0] + p.omb2 * (gsum * gsum);
+                    mw[l][0] = m1;
+                    vw[l][0] = m2;
+                    sm[pn + c.w[l] + off] = sm[po + c.w[l] + off] - adam_step(lrc * m1, m2 * ic2, p.eps);
+                }
+#pragma unroll
+                for (int tw = 0; tw < (PAIR ? 0 : TPW); ++tw) {
                     // warp -> column tile ct (4 columns) x neuron group jg
                     // (JPB neurons): JS = NW / NC groups cover all warps
                     constexpr int JS = NCL >= NW ? 1 : NW / NCL;
