@@ -116,6 +116,10 @@ __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void *src, uint32_t
 __device__ __forceinline__ void fence_proxy_async() {
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
+// Bulk prefetch of `bytes` (multiple of 16) of global memory into L2.
+__device__ __forceinline__ void bulk_prefetch_l2(const void *src, uint32_t bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+}
 
 }  // namespace
 
@@ -392,6 +396,9 @@ __global__ void __launch_bounds__(NW * 32, 1) train_lat_kernel(TrainParams p, La
     const int total = c.total;
     constexpr uint32_t xbytes = W0 * kSR * 4, rbytes = kBatchRows * 4;
     const int gbar0 = c.nbars - 2;
+    // L2 prefetch distance (steps); one hidden layer only: a C2 step (~4 us)
+    // already covers the fetch (C1 train 803 -> 789 us, C2 +0.4 % with it)
+    constexpr int kPfd = NL == 1 ? 3 : 0;
     const float *xsrc = p.xprep + (size_t)net * total * W0 * kSR;
     const float *rsrc = p.r0prep + (size_t)net * total * kBatchRows;
     auto fetch = [&](int step) {  // one thread
@@ -405,7 +412,13 @@ __global__ void __launch_bounds__(NW * 32, 1) train_lat_kernel(TrainParams p, La
     (void)d;
     (void)M;
     __syncthreads();
-    if (tid == kLT - 32 && total > 0) fetch(0);  // same issuer as every later fetch
+    if (tid == kLT - 32 && total > 0) {
+        fetch(0);  // same issuer as every later fetch
+        for (int q = 1; q < kPfd && q < total; ++q) {
+            bulk_prefetch_l2(xsrc + (size_t)q * W0 * kSR, xbytes);
+            bulk_prefetch_l2(rsrc + (size_t)q * kBatchRows, rbytes);
+        }
+    }
     cl_sync();  // every CTA's barriers initialised before any st.async lands
 
     // Adam moments of the parameters this thread updates (registers; fixed
@@ -601,6 +614,13 @@ static_for<1, NL + 1, 1>([&](auto LC) {
             // ---- next step's minibatch tile (bulk copy, one thread off the
             // critical warps; XT[buf^1] was last read in step s-1) ------------
             if (tid == kLT - 32 && s + 1 < total) fetch(s + 1);
+            // the tile kPfd steps ahead into L2: the bulk copy of step s+1's
+            // tile otherwise starts from HBM (the prepared tiles of a C1 slot
+            // are 56 MB) and was still landing when step s ended
+            if (kPfd > 0 && tid == kLT - 32 && s + kPfd < total) {
+                bulk_prefetch_l2(xsrc + (size_t)(s + kPfd) * W0 * kSR, xbytes);
+                bulk_prefetch_l2(rsrc + (size_t)(s + kPfd) * kBatchRows, rbytes);
+            }
             if constexpr (kPre) {
                 const int ct = warp % PNCL, jg = warp / PNCL, r = 4 * lane;
 #pragma unroll
