@@ -584,9 +584,13 @@ static_for<1, NL + 1, 1>([&](auto LC) {
             __syncthreads();
             NOMA_LPHASE(1)
             NOMA_TL(2)
-            // ---- final-layer partials yp (hybrid_nn.cpp:81): warps 0-3 send --
+            // ---- final-layer partials yp (hybrid_nn.cpp:81): kYW warps send ---
             const uint32_t ybar = s2u(bars + buf);
-            if (warp < 4) {
+            // two layers: every warp computes the (cheap) partial and sends to
+            // CS / NW peers (C2 -16 us); one layer: warps 0-3 (all 8: C1 +39 us,
+            // warps 4-7 preload the weight-gradient operands meanwhile)
+            constexpr int kYW = NL > 1 ? (NW < CS ? NW : CS) : 4;
+            if (warp < kYW) {
                 const int r0 = 4 * lane;
                 const float *aN = sm + c.aN;
                 const float *wf = sm + po + c.wf;
@@ -602,7 +606,7 @@ static_for<1, NL + 1, 1>([&](auto LC) {
                 }
                 const uint32_t la = s2u(sm + c.yall + (buf * CS + rank) * kBatchRows + r0);
 #pragma unroll
-                for (int q = warp; q < CS; q += 4) {
+                for (int q = warp; q < CS; q += kYW) {
                     // two layers: destinations rotated by rank (as the bulk
                     // exchanges); one layer: in order (rotated measured +2 %)
                     const uint32_t dst = NL > 1 ? (rank + q) % CS : q;
