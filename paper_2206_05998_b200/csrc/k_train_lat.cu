@@ -475,6 +475,9 @@ __global__ void __launch_bounds__(NW * 32, 1) train_lat_kernel(TrainParams p, La
     constexpr int PNCL = W0 / 4;
     constexpr bool kPre = NL == 1 && PNCL <= NW;
     constexpr int PJPB = JT / (PNCL >= NW ? 1 : NW / PNCL);
+    // two layers with one input column tile per warp: the first layer's
+    // weight-gradient inputs are loaded before the dA reduce-scatter wait
+    constexpr bool kPre1 = NL > 1 && W0 / 4 == NW;
     ulonglong2 bx[4];
     float4 bz[PJPB];
     NOMA_LPHASE(7)
@@ -849,7 +852,7 @@ static_for<NL, 0, -1>([&](auto LC) {
                         for (int q = 0; q < 4; ++q) acc[j][q] = 0ull;
                     }
                     ulonglong2 x[4];
-                    if constexpr (kPre && l == 1) {
+                    if constexpr ((kPre || kPre1) && l == 1) {
 #pragma unroll
                         for (int q = 0; q < 4; ++q) x[q] = bx[q];
                     } else {
@@ -960,6 +963,11 @@ static_for<NL, 0, -1>([&](auto LC) {
                     // receive: dZ_{l-1} own = (a_{l-1} > 0) * sum_q partial_q (:107)
                     const uint32_t rb = s2u(bars + 3 + 2 * (l - 2));
                     NOMA_TL(13)
+                    if constexpr (kPre1 && l == 2) {  // layer 1's weight-gradient inputs, ahead of the wait
+#pragma unroll
+                        for (int q = 0; q < 4; ++q)
+                            bx[q] = *reinterpret_cast<const ulonglong2 *>(XT + (4 * warp + q) * kSR + 4 * lane);
+                    }
                     mbar_wait(rb, (uint32_t)(s & 1));
                     NOMA_TL(14)
                     if (tid < JT * 32) {
