@@ -435,7 +435,9 @@ __global__ void __launch_bounds__(NW * 32, 1) train_lat_kernel(TrainParams p, La
     // KSF / FVV lanes.  On 8 warps k splits over 4 lanes and the neurons over
     // two groups: one shuffle round less than 8 lanes, at twice the input
     // loads (C1 -1.3 %, C2 -0.9 %; for the first layer the end-of-step
-    // preload hides them).
+    // preload hides them).  Two layers with 8 lanes and one group (each
+    // gathered a1 element read once) measured the same once the dZ1 sum ran
+    // on all warps.
     constexpr int KSF = (NW == 8 && JT % 2 == 0) ? 4 : 8;
     constexpr int JPF = JT / (NW / KSF);         // neurons per forward thread
     constexpr int FVV = 4 * JPF;                 // values before the reduce
@@ -970,7 +972,20 @@ static_for<NL, 0, -1>([&](auto LC) {
                     }
                     mbar_wait(rb, (uint32_t)(s & 1));
                     NOMA_TL(14)
-                    if (tid < JT * 32) {
+                    if constexpr (JT * 64 == kLT) {  // all threads, two rows each (C2 -39 us vs 4 warps x 4 rows)
+                        const int j = tid >> 6, r = 2 * (tid & 63);
+                        const float *rs_ = sm + c.rsb[l - 1] + j * kSR + r;
+                        float2 sum = *reinterpret_cast<const float2 *>(rs_);
+#pragma unroll
+                        for (int q = 1; q < CS; ++q) {
+                            const float2 v = *reinterpret_cast<const float2 *>(rs_ + q * JT * kSR);
+                            sum.x += v.x;
+                            sum.y += v.y;
+                        }
+                        float2 *ap = reinterpret_cast<float2 *>(sm + c.aloc[l - 1] + j * kSR + r);
+                        const float2 a = *ap;
+                        *ap = make_float2(a.x > 0.f ? sum.x : 0.f, a.y > 0.f ? sum.y : 0.f);
+                    } else if (tid < JT * 32) {
                         const int j = tid >> 5, r = 4 * lane;
                         const float *rs_ = sm + c.rsb[l - 1] + j * kSR + r;
                         float4 sum = *reinterpret_cast<const float4 *>(rs_);
