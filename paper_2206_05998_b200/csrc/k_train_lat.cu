@@ -212,6 +212,7 @@ struct LatCarve {
     int aN;                                            // own a_N [JT][kSR]
     int aloc[NOMA_MAX_DIMS], af[NOMA_MAX_DIMS], rsb[NOMA_MAX_DIMS];  // l < N
     int rsst;                                          // dA partial staging [H][kSR]
+    int mk, wt, wfa, wtbar;                            // local-dA mode (two layers of 64 on 16 CTAs), else -1
     int bars;                                          // mbarriers (8-byte aligned)
     int nbars, end;
     int ehist;                                         // epoch-loss history [epochs][128], or -1
@@ -284,9 +285,22 @@ __host__ __device__ inline bool lat_carve(const NetGeom &g, int cs, int width, i
     }
     c->rsst = off;
     if (N > 1) off += H * kSR;
+    // local-dA mode: ReLU masks of every CTA's a2 [2][cs][jt][4] words, the
+    // own layer-1 neurons' columns of W2 [2][H][4] and all final weights [2][H]
+    c->mk = c->wt = c->wfa = c->wtbar = -1;
+    const bool lda = N == 2 && jt == 4 && cs == 16 && width == 32;  // the 8-warp instance (train_lat_kernel LDA)
+    if (lda) {
+        c->mk = off;
+        off += 2 * cs * 16;
+        c->wt = off;
+        off += 2 * H * 4;
+        c->wfa = off;
+        off += 2 * H;
+    }
     off = pad_to(off, 2);
     c->bars = off;
-    c->nbars = 2 + 2 * (N - 1) + 2;  // Y[2], AG_l, RS_l, G[2] (minibatch tiles)
+    c->nbars = 2 + 2 * (N - 1) + (lda ? 2 : 0) + 2;  // Y[2], AG_l, RS_l, [WT[2]], G[2] (minibatch tiles)
+    if (lda) c->wtbar = 2 + 2 * (N - 1);
     off += 2 * c->nbars;
     c->end = off;
     return (size_t)off * sizeof(float) <= 227 * 1024;
@@ -370,7 +384,15 @@ __global__ void __launch_bounds__(NW * 32, 1) train_lat_kernel(TrainParams p, La
             sm[c.atab + 2 * i + 1] = (float)(1.0 / c2);
         }
     }
-    constexpr uint32_t ybytes = CS * kBatchRows * 4;
+    // Local-dA mode (C2: two layers of 64 on 16 CTAs of 8 warps): instead of
+    // reduce-scattering dA1 partials (16 x 2 KB per CTA per step), every CTA
+    // receives the ReLU masks of all a2 rows with the final-layer partials (64
+    // bytes per peer) and keeps W2's columns of its own layer-1 neurons and all
+    // final weights current (each owner sends its updated rows after Adam, a
+    // whole step ahead of use), and forms dA1 of its own neurons locally.
+    constexpr bool LDA = NL == 2 && JT == 4 && NW == 8 && CS == 16;
+    constexpr uint32_t ybytes = CS * kBatchRows * 4 + (LDA ? CS * 64 : 0);
+    constexpr uint32_t wtbytes = CS * (JT * 16 + 16);
     // all-gather / reduce-scatter move whole [JT][kSR] tiles by bulk copy
     constexpr uint32_t agbytes = H * kSR * 4;
     constexpr uint32_t rsbytes = CS * JT * kSR * 4;
@@ -384,6 +406,16 @@ __global__ void __launch_bounds__(NW * 32, 1) train_lat_kernel(TrainParams p, La
             mbar_arm(s2u(bars + 2 + 2 * (l - 1)), agbytes);
             mbar_arm(s2u(bars + 3 + 2 * (l - 1)), rsbytes);
         }
+        if constexpr (LDA) {
+            mbar_arm(s2u(bars + c.wtbar), 0);             // phase 0: step 0 (initial weights)
+            mbar_arm(s2u(bars + c.wtbar), wtbytes);       // phase 1: step 2
+            mbar_arm(s2u(bars + c.wtbar + 1), wtbytes);   // phase 0: step 1
+        }
+    }
+    if constexpr (LDA) {  // step 0's W2 columns and final weights from the plans
+        for (int t = tid; t < H * JT; t += kLT)
+            sm[c.wt + t] = pl[g.plan_w[2] + (t / JT) * g.plan_pad[1] + rank * JT + t % JT];
+        for (int t = tid; t < H; t += kLT) sm[c.wfa + t] = pl[g.plan_f + t];
     }
 
     // ---- step schedule: minibatch tiles by bulk copy --------------------------
@@ -479,7 +511,7 @@ __global__ void __launch_bounds__(NW * 32, 1) train_lat_kernel(TrainParams p, La
     constexpr int PJPB = JT / (PNCL >= NW ? 1 : NW / PNCL);
     // two layers with one input column tile per warp: the first layer's
     // weight-gradient inputs are loaded before the dA reduce-scatter wait
-    constexpr bool kPre1 = NL > 1 && W0 / 4 == NW;
+    constexpr bool kPre1 = NL > 1 && W0 / 4 == NW && !LDA;
     ulonglong2 bx[4];
     float4 bz[PJPB];
     NOMA_LPHASE(7)
@@ -617,6 +649,32 @@ static_for<1, NL + 1, 1>([&](auto LC) {
                     const uint32_t dst = NL > 1 ? (rank + q) % CS : q;
                     st_async4(mapa(la, dst), y, mapa(ybar, dst));
                 }
+                if constexpr (LDA) {
+                    // ReLU mask of the own a2: word 4 j + k = rows 32 k .. 32 k + 31 of
+                    // neuron j; lanes 0-3 send 16 bytes each to this warp's peers
+                    uint32_t mw = 0;
+#pragma unroll
+                    for (int j = 0; j < JT; ++j)
+#pragma unroll
+                        for (int k = 0; k < 4; ++k) {
+                            const uint32_t bt = __ballot_sync(0xffffffffu, aN[j * kSR + 32 * k + lane] > 0.f);
+                            if (lane == 4 * j + k) mw = bt;
+                        }
+                    const uint32_t m0 = __shfl_sync(0xffffffffu, mw, (4 * lane) & 31),
+                                   m1 = __shfl_sync(0xffffffffu, mw, (4 * lane + 1) & 31),
+                                   m2 = __shfl_sync(0xffffffffu, mw, (4 * lane + 2) & 31),
+                                   m3 = __shfl_sync(0xffffffffu, mw, (4 * lane + 3) & 31);
+                    if (lane < 4) {
+                        const uint32_t ma = s2u(sm + c.mk + (buf * CS + rank) * 16 + 4 * lane);
+                        const float4 mv = make_float4(__uint_as_float(m0), __uint_as_float(m1), __uint_as_float(m2),
+                                                      __uint_as_float(m3));
+#pragma unroll
+                        for (int q = warp; q < CS; q += kYW) {
+                            const uint32_t dst = (rank + q) % CS;
+                            st_async4(mapa(ma, dst), mv, mapa(ybar, dst));
+                        }
+                    }
+                }
             }
             NOMA_TL(3)
             NOMA_GT(4)
@@ -676,7 +734,52 @@ static_for<NL, 0, -1>([&](auto LC) {
                 const float *dyp = sm + c.dy, *wfp = sm + po + c.wf;
                 const float *in = l == 1 ? XT : sm + c.af[l - 1] + buf * H * kSR;
                 const int sw = c.sw[l];
-                if (l > 1)
+                if constexpr (LDA && l == 2) {
+                    // dA1[j][r] = sum_i W2[i][own j] dZ2[i][r] (:111) for the own
+                    // layer-1 neurons, dZ2[i][r] = mask_i[r] dy[r] wf[i] (:102-107):
+                    // lane = 8 i-splits x 4 row quads, warps over row quads; the
+                    // 8-lane reduce-scatter leaves two rows of one neuron per lane
+                    const int b = s & 1;
+                    if (s > 0) mbar_wait(s2u(bars + c.wtbar + b), (uint32_t)((s >> 1) & 1));
+                    const int ks = lane & 7, rq = (lane >> 3) + 4 * warp, r = 4 * rq;
+                    const float4 dy4 = *reinterpret_cast<const float4 *>(dyp + r);
+                    const uint32_t *mk = reinterpret_cast<const uint32_t *>(sm + c.mk) + buf * CS * 16 + (rq >> 3);
+                    const int sh = 4 * (rq & 7);
+                    f2_t acc[JT][2];
+#pragma unroll
+                    for (int j = 0; j < JT; ++j) acc[j][0] = acc[j][1] = 0ull;
+#pragma unroll
+                    for (int ii = 0; ii < H / 8; ++ii) {
+                        const int i = 8 * ii + ks;
+                        const float4 w = *reinterpret_cast<const float4 *>(sm + c.wt + (b * H + i) * 4);
+                        const float f = sm[c.wfa + b * H + i];
+                        const uint32_t bits = mk[(i >> 2) * 16 + (i & 3) * 4] >> sh;
+                        const f2_t za = f2_pack(bits & 1u ? dy4.x * f : 0.f, bits & 2u ? dy4.y * f : 0.f);
+                        const f2_t zb = f2_pack(bits & 4u ? dy4.z * f : 0.f, bits & 8u ? dy4.w * f : 0.f);
+                        const float wc[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+                        for (int j = 0; j < JT; ++j) {
+                            const f2_t wj = f2_bcast(wc[j]);
+                            ffma2(acc[j][0], wj, za);
+                            ffma2(acc[j][1], wj, zb);
+                        }
+                    }
+                    float v[4 * JT];
+#pragma unroll
+                    for (int j = 0; j < JT; ++j) {
+                        const float2 u = f2_unpack(acc[j][0]), t2 = f2_unpack(acc[j][1]);
+                        v[4 * j] = u.x;
+                        v[4 * j + 1] = u.y;
+                        v[4 * j + 2] = t2.x;
+                        v[4 * j + 3] = t2.y;
+                    }
+                    reduce_scatter<4 * JT, 4 * JT, 8>(v, lane);
+                    // dZ1 own = (a1 > 0) dA1, in place
+                    float2 *ap = reinterpret_cast<float2 *>(sm + c.aloc[1] + (ks >> 1) * kSR + r + 2 * (ks & 1));
+                    const float2 a = *ap;
+                    *ap = make_float2(a.x > 0.f ? v[0] : 0.f, a.y > 0.f ? v[1] : 0.f);
+                }
+                if (l > 1 && !LDA)
                 for (int tt = tid; tt < (H / 4) * 32; tt += kLT) {
                     // dA_{l-1} partial = sum_{j own} W_l[j][c] dZ_l[j][r] (:111) for
                     // every c (4 c x 4 r per thread), sent to the owner of c.
@@ -961,7 +1064,20 @@ static_for<NL, 0, -1>([&](auto LC) {
                         }
                     }
                 }
-                if (l > 1) {
+                if constexpr (LDA && l == 2) {
+                    // dZ1 complete, the own W2 rows / final weights of step s+1 written
+                    __syncthreads();
+                    if (s >= 1 && tid == 0) mbar_arm(s2u(bars + c.wtbar + (s & 1)), wtbytes);  // step s+2
+                    if (s + 1 < c.total && tid < CS * (JT + 1)) {
+                        // to peer p: W2[own i][p's 4 columns] (k < JT), own final weights (k == JT)
+                        const int pp = tid / (JT + 1), k = tid % (JT + 1), nb = (s + 1) & 1;
+                        const float *src = k < JT ? sm + pn + c.w[2] + k * c.sw[2] + JT * pp : sm + pn + c.wf;
+                        const uint32_t dst = k < JT ? s2u(sm + c.wt + (nb * H + rank * JT + k) * 4)
+                                                    : s2u(sm + c.wfa + nb * H + rank * JT);
+                        st_async4(mapa(dst, pp), *reinterpret_cast<const float4 *>(src), mapa(s2u(bars + c.wtbar + nb), pp));
+                    }
+                }
+                if (l > 1 && !LDA) {
                     // receive: dZ_{l-1} own = (a_{l-1} > 0) * sum_q partial_q (:107)
                     const uint32_t rb = s2u(bars + 3 + 2 * (l - 2));
                     NOMA_TL(13)
