@@ -11,7 +11,11 @@
 //     (128 floats per CTA, all-to-all) -- the only exchange for one hidden
 //     layer (C1);
 //   * with N >= 2 hidden layers, the all-gather of a_l (l < N) in the forward
-//     pass and the reduce-scatter of dA_l = W_{l+1}^T dZ_{l+1} in the backward.
+//     pass and the reduce-scatter of dA_l = W_{l+1}^T dZ_{l+1} in the backward
+//     -- except in local-dA mode (C2: two layers of 64, 16 CTAs of 8 warps),
+//     where the ReLU masks of a_2 travel with the final-layer partials and
+//     every owner sends its updated W_2 rows / final weights a step ahead, so
+//     each CTA forms dA_1 of its own neurons without a reduce-scatter.
 // Exchanges use st.async into the peers' shared memory with mbarrier
 // complete_tx byte counting (no cluster-wide barrier per step).  Each CTA sums
 // the CS partials in rank order, so every CTA sees the same yhat bit for bit
