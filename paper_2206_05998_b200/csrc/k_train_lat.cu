@@ -628,9 +628,10 @@ static_for<1, NL + 1, 1>([&](auto LC) {
             // ---- final-layer partials yp (hybrid_nn.cpp:81): kYW warps send ---
             const uint32_t ybar = s2u(bars + buf);
             // two layers: every warp computes the (cheap) partial and sends to
-            // CS / NW peers (C2 -16 us); one layer: warps 0-3 (all 8: C1 +39 us,
-            // warps 4-7 preload the weight-gradient operands meanwhile)
-            constexpr int kYW = NL > 1 ? (NW < CS ? NW : CS) : 4;
+            // CS / NW peers (C2 -16 us); one layer: warps 0-1, 8 peers each
+            // (4 warps: +3 us, all 8: +42 us; the other warps preload the
+            // weight-gradient operands meanwhile)
+            constexpr int kYW = NL > 1 ? (NW < CS ? NW : CS) : 2;
             if (warp < kYW) {
                 const int r0 = 4 * lane;
                 const float *aN = sm + c.aN;
