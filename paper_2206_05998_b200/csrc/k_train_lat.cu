@@ -398,7 +398,10 @@ __global__ void __launch_bounds__(NW * 32, 1) train_lat_kernel(TrainParams p, La
     constexpr uint32_t ybytes = CS * kBatchRows * 4 + (LDA ? CS * 64 : 0);
     constexpr uint32_t wtbytes = CS * (JT * 16 + 16);
     // all-gather / reduce-scatter move whole [JT][kSR] tiles by bulk copy
-    constexpr uint32_t agbytes = H * kSR * 4;
+    // local-dA mode: the a1 all-gather leaves per warp (kBatchRows columns
+    // only, the pad columns of af stay zero from the start)
+    const bool WMC = LDA && p.agbuf;  // uniform over the cluster
+    const uint32_t agbytes = H * (WMC ? kBatchRows : kSR) * 4;
     constexpr uint32_t rsbytes = CS * JT * kSR * 4;
     if (tid == 0) {
         for (int b = 0; b < c.nbars; ++b) mbar_init(s2u(bars + b), 1);
@@ -580,9 +583,20 @@ static_for<1, NL + 1, 1>([&](auto LC) {
                     if (l < NL && p.agbuf) {  // staged in global for the multicast all-gather
                         float *gt = p.agbuf + ((size_t)net * 2 + buf) * H * kSR + rank * JT * kSR;
                         if (fown) sts_n<FV>(gt + fj * kSR + r, v);
-                        if (tid < JT * (kSR - kBatchRows))  // pad columns stay zero
+                        if (!WMC && tid < JT * (kSR - kBatchRows))  // pad columns stay zero
                             gt[(tid / (kSR - kBatchRows)) * kSR + kBatchRows + tid % (kSR - kBatchRows)] = 0.0f;
                         fence_proxy_async_global();
+                        if (WMC) {
+                            // this warp's 32 rows of its two neurons leave as soon
+                            // as they are written: one multicast per neuron row
+                            __syncwarp();
+                            if (lane < JPF) {
+                                const int nj = fjh * JPF + lane, c0 = 32 * (warp % KSF);
+                                bulk_g2s_mc(s2u(sm + c.af[l] + (buf * H + rank * JT + nj) * kSR + c0),
+                                            gt + nj * kSR + c0, 128, s2u(bars + 2 + 2 * (l - 1)),
+                                            (uint16_t)((1u << CS) - 1));
+                            }
+                        }
                     }
                 }
                 if (l < NL) {
@@ -595,8 +609,9 @@ static_for<1, NL + 1, 1>([&](auto LC) {
                     const uint32_t lb = s2u(bars + 2 + 2 * (l - 1));
                     NOMA_TL(10)
                     NOMA_GT(1)
-                    __syncthreads();
-                    if (p.agbuf) {
+                    if (!WMC) __syncthreads();
+                    if (WMC) {
+                    } else if (p.agbuf) {
                         // one multicast copy from the global staging tile into
                         // every CTA's af slot (the SM's outbound smem -> peer
                         // copies ran at ~16 B/clk: 34 KB per step)
